@@ -1,0 +1,207 @@
+/*
+ * infllm_b200.h — C-ABI drop-in boundary for the InfLLM block-memory attention
+ * layer (arXiv 2402.04617), B200-native (sm_100a).
+ *
+ * The reference exposes its hot path as a header-only C++ template API in
+ * namespace `blockmem` (see /root/reference/proj/include/blockmem/). This
+ * header is the flat C boundary a C++/cgo/ctypes host binds instead. Every
+ * entry point below names the reference interface it replaces (file:line,
+ * paths relative to proj/include/blockmem/).
+ *
+ * Conventions
+ *  - Return value: INFLLM_OK (0) or an error code; infllm_last_error() gives a
+ *    thread-local one-line message. INFLLM_ERR_CONFIG mirrors blockmem::
+ *    ConfigError (types.hpp:20-22), INFLLM_ERR_STREAM mirrors
+ *    blockmem::StreamError (types.hpp:24-26).
+ *  - Tensor arguments are DEVICE pointers (unless the name says host_), dense
+ *    row-major, element type = the engine dtype (fp32 or bf16):
+ *        q   [l_x][n_heads][head_dim]
+ *        k   [l_x][n_kv_heads][head_dim]
+ *        v   [l_x][n_kv_heads][value_dim]
+ *        out [l_x][n_heads][value_dim]
+ *    n_heads must be a multiple of n_kv_heads (GQA); with n_kv_heads ==
+ *    n_heads this is the reference's MHA layout transposed from per-head
+ *    matrices (types.hpp:158-169) to token-major.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). All compute
+ *    entry points are asynchronous on it; nothing data-dependent is read back
+ *    to the host inside a step (lookup ids, representative indices and LRU
+ *    state live on the device).
+ *  - One host thread per engine at a time (reference: SPEC.md "Concurrency
+ *    Model"; no internal locking, like blockmem::StreamEngine).
+ */
+#ifndef INFLLM_B200_H
+#define INFLLM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define INFLLM_OK 0
+#define INFLLM_ERR_CONFIG 1 /* blockmem::ConfigError   (types.hpp:20-22) */
+#define INFLLM_ERR_STREAM 2 /* blockmem::StreamError   (types.hpp:24-26) */
+#define INFLLM_ERR_CUDA 3
+#define INFLLM_ERR_NCCL 4
+#define INFLLM_ERR_ARG 5
+
+/* blockmem::LookupMode (types.hpp:51) */
+#define INFLLM_LOOKUP_ENCODE_AND_DECODE 0
+#define INFLLM_LOOKUP_DECODE_ONLY 1
+#define INFLLM_LOOKUP_NONE 2
+
+/* blockmem::PositionMode (types.hpp:52) */
+#define INFLLM_POSITION_CLAMPED 0
+#define INFLLM_POSITION_ABSOLUTE 1
+
+/* engine element type; the reference's Real is float (real.hpp:7-11) */
+#define INFLLM_DTYPE_F32 0
+#define INFLLM_DTYPE_BF16 1
+
+/* blockmem::EngineConfig (types.hpp:84-110); same field names and defaults */
+typedef struct infllm_engine_config {
+    int64_t chunk_size;   /* l_C  (default 512)  */
+    int64_t unit_size;    /* l_bs (default 128)  */
+    int64_t n_repr;       /* r_k  (default 4)    */
+    int64_t local_size;   /* l_L  (default 4096) */
+    int64_t init_size;    /* l_I  (default 128)  */
+    int64_t n_lookup;     /* k_m  (default 32)   */
+    int64_t hot_capacity; /* default 32          */
+    double decay;         /* d    (default 0.1)  */
+    int32_t lookup_mode;   /* INFLLM_LOOKUP_*    */
+    int32_t position_mode; /* INFLLM_POSITION_*  */
+} infllm_engine_config;
+
+/* blockmem::ModelShape (types.hpp:29-49) + the GQA KV-head count the
+ * reference lacks. */
+typedef struct infllm_model_shape {
+    int32_t n_layers;
+    int32_t n_heads;    /* query heads */
+    int32_t n_kv_heads; /* key/value heads; n_heads % n_kv_heads == 0 */
+    int32_t head_dim;
+    int32_t value_dim;  /* <= 0: same as head_dim */
+} infllm_model_shape;
+
+/* blockmem::CacheCounters (memory.hpp:151-157) + EngineLayerMetrics
+ * (engine.hpp:35-41) */
+typedef struct infllm_layer_metrics {
+    int64_t units;
+    int64_t hot_units;
+    int64_t peak_hot_units;
+    int64_t peak_hot_bytes;
+    uint64_t hits;
+    uint64_t misses;
+    uint64_t loads;
+    uint64_t evictions;
+    uint64_t requested;
+} infllm_layer_metrics;
+
+typedef struct infllm_engine* infllm_engine_t;
+
+/* Thread-local message of the last failed call on this thread. */
+const char* infllm_last_error(void);
+/* Library build string (arch, dtype support). */
+const char* infllm_version(void);
+
+/* EngineConfig{} defaults (types.hpp:84-94). */
+int infllm_config_default(infllm_engine_config* cfg);
+/* EngineConfig::validate (types.hpp:96-109) + ModelShape::validate
+ * (types.hpp:45-48); shape may be NULL. */
+int infllm_config_validate(const infllm_engine_config* cfg, const infllm_model_shape* shape);
+
+/* StreamEngine<Scalar>(EngineConfig, ModelShape, seed) (engine.hpp:66-73),
+ * minus the synthetic adapter: q/k/v are supplied per call. `device` is the
+ * CUDA ordinal. kv_group_begin/kv_group_count select the KV heads this engine
+ * owns (multi-GPU KV-group sharding; pass 0 / n_kv_heads for the whole
+ * layer); its q/k/v/out pointers then hold only the owned heads. */
+int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_shape* shape,
+                         int32_t dtype, int32_t device, int32_t kv_group_begin,
+                         int32_t kv_group_count, infllm_engine_t* out);
+int infllm_engine_destroy(infllm_engine_t eng);
+
+/* Cross-shard reduction hook for KV-group sharding. The
+ * engine calls it with its per-KV-group fp64 partials laid out
+ * [count][kv_group_count]; the callee must return, in `full`, the
+ * [count][n_kv_heads] all-gather (device pointers, on `stream`). NULL (the
+ * default) = single shard. */
+typedef int (*infllm_allgather_fn)(void* user, const double* local, double* full, int64_t count,
+                                   void* stream);
+int infllm_engine_set_allgather(infllm_engine_t eng, infllm_allgather_fn fn, void* user);
+
+/* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if
+ * lookup_mode == encode_and_decode), attention over [initial | retrieved
+ * units | local | causal chunk], frequency update + capacity, representative
+ * scoring, window roll and unit packing (engine.hpp:242-359). Requires
+ * 1 <= l_x <= chunk_size. Layers advance independently; a step of the
+ * reference engine is one call per layer in order 0..n_layers-1. */
+int infllm_encode_chunk(infllm_engine_t eng, int32_t layer, const void* q, const void* k,
+                        const void* v, int64_t l_x, void* out, void* stream);
+
+/* StreamEngine::decode_step (engine.hpp:100-103): l_x = 1, lookup unless
+ * lookup_mode == none. */
+int infllm_decode_step(infllm_engine_t eng, int32_t layer, const void* q, const void* k,
+                       const void* v, void* out, void* stream);
+
+/* StreamEngine::finish (engine.hpp:115-119): flushes each layer's held-back
+ * partial unit. Synchronous. */
+int infllm_finish(infllm_engine_t eng, void* stream);
+
+/* ---- diagnostics (synchronous: they wait for the engine's queued work) ---- */
+
+/* LayerStepOutput::retrieved_ids of the most recent step of `layer`
+ * (engine.hpp:26-30), ascending unit ids. */
+int infllm_retrieved_ids(infllm_engine_t eng, int32_t layer, int64_t* host_ids, int64_t cap,
+                         int64_t* n_out);
+/* StreamEngine::metrics() per layer (engine.hpp:121-138). */
+int infllm_get_layer_metrics(infllm_engine_t eng, int32_t layer, infllm_layer_metrics* out);
+/* TieredStore::unit(id) (memory.hpp:178-180): span and representative
+ * positions (MemoryUnit::repr_abs, memory.hpp:25). host_repr_abs holds
+ * n_repr entries. */
+int infllm_unit_info(infllm_engine_t eng, int32_t layer, int64_t unit_id, int64_t* start_abs,
+                     int64_t* size, int64_t* host_repr_abs, int64_t* n_repr_out);
+/* Stream bookkeeping: tokens fed, steps done, initial_len, local_len,
+ * pending_partial (engine.hpp:77-78,140-148). */
+int infllm_stream_state(infllm_engine_t eng, int32_t layer, int64_t* tokens_fed,
+                        int64_t* steps_done, int64_t* initial_len, int64_t* local_len,
+                        int64_t* pending_partial);
+/* Per-unit decayed-frequency scores s_b (MemoryUnit::freq_score,
+ * memory.hpp:27) and tiers (1 = hot) for units [0, n). */
+int infllm_unit_freq(infllm_engine_t eng, int32_t layer, double* host_freq, int32_t* host_hot,
+                     int64_t n);
+/* Engine trace (TieredStore::trace, memory.hpp:159-163,182): up to cap
+ * records (step, unit_id, hit). */
+int infllm_trace(infllm_engine_t eng, int32_t layer, int64_t* host_step, int64_t* host_unit,
+                 int32_t* host_hit, int64_t cap, int64_t* n_out);
+/* Number of kernels this engine launched so far (all layers). */
+int infllm_kernel_launches(infllm_engine_t eng, int64_t* n_out);
+/* Fill host_out with the dominant attention kernel's average device time of
+ * the last timed window (ms) and the number of launches in it;
+ * infllm_profile_begin starts the window (events on the engine stream). */
+int infllm_profile_begin(infllm_engine_t eng, int32_t enable);
+int infllm_profile_read(infllm_engine_t eng, double* attn_ms_total, int64_t* attn_launches,
+                        double* lookup_ms_total, int64_t* lookup_launches);
+
+/* ---- standalone operators (device pointers, async on stream) ---- */
+
+/* select_representatives (repr_score.hpp:94-112) for `n_units` units at
+ * once: scores [n_units][unit_len] fp32 (row u has lens[u] valid entries,
+ * lens may be NULL = all unit_len); writes min(r_k, len) ascending indices
+ * per unit into idx [n_units][r_k] (unused slots = -1). */
+int infllm_select_representatives(const float* scores, const int64_t* lens, int64_t n_units,
+                                  int64_t unit_len, int64_t r_k, int64_t* idx, void* stream);
+
+/* TieredStore::relevance_all + lookup's top-k (memory.hpp:217-253) over an
+ * explicit representative index: qsum [n_kv_heads][head_dim] fp64 (sum of
+ * the chunk's queries over the heads of each KV group), repr
+ * [n_units][r_k][n_kv_heads][head_dim] (dtype), -> rel [n_units] fp64 and
+ * ids [min(k_m, n_units)] ascending. */
+int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n_units,
+                  int64_t r_k, int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel,
+                  int64_t* ids, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INFLLM_B200_H */
