@@ -120,14 +120,26 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
                          int32_t kv_group_count, infllm_engine_t* out);
 int infllm_engine_destroy(infllm_engine_t eng);
 
-/* Cross-shard reduction hook for KV-group sharding. The
- * engine calls it with its per-KV-group fp64 partials laid out
- * [count][kv_group_count]; the callee must return, in `full`, the
- * [count][n_kv_heads] all-gather (device pointers, on `stream`). NULL (the
- * default) = single shard. */
-typedef int (*infllm_allgather_fn)(void* user, const double* local, double* full, int64_t count,
-                                   void* stream);
+/* Cross-shard exchange hook for KV-group sharding.
+ * Relevance, representative scores and attention masses are sums over ALL
+ * heads (memory.hpp:221-228, repr_score.hpp:55-57, engine.hpp:278-281), so
+ * each shard computes fp64 partials per KV group into a [rows][g_total]
+ * device buffer (its own columns [g0, g0 + g_count)); the hook must fill the
+ * other columns in place (an all-gather, on `stream`) before the engine sums
+ * the groups in fixed order 0..g_total-1, which keeps ids bit-identical for
+ * any number of shards. NULL (the default) = single shard. Return 0 on
+ * success. */
+typedef int (*infllm_allgather_fn)(void* user, double* buf, int64_t rows, int32_t g0,
+                                   int32_t g_count, int32_t g_total, void* stream);
 int infllm_engine_set_allgather(infllm_engine_t eng, infllm_allgather_fn fn, void* user);
+
+/* Pre-size the unit pool and trace for a stream of max_tokens tokens (the
+ * reference grows its std::vectors on demand; the engine grows its device
+ * pools too, this only moves the growth out of the timed region). */
+int infllm_engine_reserve(infllm_engine_t eng, int64_t max_tokens);
+/* Engine options: "tc_attention" (1 = tcgen05 attention when the shape
+ * allows, 0 = CUDA-core attention). */
+int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if
  * lookup_mode == encode_and_decode), attention over [initial | retrieved

@@ -206,7 +206,10 @@ class OracleEngine:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib().oracle_engine_destroy(self.h)
+            try:
+                lib().oracle_engine_destroy(self.h)
+            except Exception:
+                pass
             self.h = None
 
     def set_always_emit_weights(self, v=True):

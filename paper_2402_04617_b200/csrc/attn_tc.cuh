@@ -1,0 +1,13 @@
+// attn_tc.cuh — tcgen05/TMEM/TMA attention kernel interface (bf16, d = 128).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace infllm {
+
+// true when the tensor-core kernel covers this shape/mode
+bool attn_tc_supported(int d, int dv, int unit_size, bool absolute);
+// launches the tensor-core attention for one step; returns #kernels launched
+int launch_attn_tc(const AttnParams& p, cudaStream_t st);
+
+}  // namespace infllm

@@ -1,0 +1,69 @@
+// common.cuh — shared device helpers for the InfLLM B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace infllm {
+
+using bf16 = __nv_bfloat16;
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<bf16>(bf16 x) { return __bfloat162float(x); }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// Rotary factors (rotary.hpp:19-34): angle = pos * freq in double (freq table
+// computed on the host with std::pow exactly like the reference), cos/sin in
+// double, narrowed to float.
+struct RopeFreqs {
+    double f[128];  // up to head_dim 256
+};
+
+// rotate one pair exactly like rotate_row (rotary.hpp:40-51): no FMA
+// contraction, so the float result matches the reference's separate
+// multiply/subtract rounding.
+__device__ __forceinline__ void rope_pair(float x0, float x1, float c, float s, float& y0, float& y1) {
+    y0 = __fsub_rn(__fmul_rn(x0, c), __fmul_rn(x1, s));
+    y1 = __fadd_rn(__fmul_rn(x0, s), __fmul_rn(x1, c));
+}
+
+__device__ __forceinline__ void rope_cs(const RopeFreqs& fr, int a, int64_t pos, float& c, float& s) {
+    const double ang = static_cast<double>(pos) * fr.f[a];
+    double sd, cd;
+    sincos(ang, &sd, &cd);
+    c = static_cast<float>(cd);
+    s = static_cast<float>(sd);
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Device LRU/bookkeeping state of one layer's TieredStore (memory.hpp:170-323).
+struct LruState {
+    int64_t hot_count;
+    uint64_t hits, misses, loads, evictions, requested;
+    int64_t peak_hot_units;
+    int64_t peak_hot_bytes;
+    int64_t trace_count;
+};
+
+}  // namespace infllm

@@ -1,0 +1,872 @@
+// engine.cu — host side of the B200 InfLLM layer: the C-ABI declared in
+// include/infllm_b200.h and the per-step orchestration that mirrors
+// blockmem::StreamEngine::step (engine.hpp:242-359). All data-dependent state
+// (lookup ids, representative indices, LRU tiers/frequencies/counters, trace)
+// lives on the device; the host only advances the stream arithmetic that the
+// reference derives from token counts (local window bounds, initial-token
+// pinning, unit packing boundaries), so a step is a fixed kernel sequence on
+// the caller's stream with no host synchronisation.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <type_traits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/infllm_b200.h"
+#include "attn_tc.cuh"
+#include "kernels.cuh"
+
+using namespace infllm;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ConfigError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct StreamError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return INFLLM_OK;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return INFLLM_ERR_CONFIG;
+    } catch (const StreamError& e) {
+        g_err = e.what();
+        return INFLLM_ERR_STREAM;
+    } catch (const CudaError& e) {
+        g_err = e.what();
+        return INFLLM_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return INFLLM_ERR_ARG;
+    }
+}
+
+void validate_cfg(const infllm_engine_config& c) {  // types.hpp:96-109
+    if (c.chunk_size < 1) throw ConfigError("chunk_size must be >= 1");
+    if (c.unit_size < 1) throw ConfigError("unit_size must be >= 1");
+    if (c.n_repr < 1) throw ConfigError("n_repr must be >= 1");
+    if (c.local_size < 1) throw ConfigError("local_size must be >= 1");
+    if (c.init_size < 0) throw ConfigError("init_size must be >= 0");
+    if (c.n_lookup < 0) throw ConfigError("n_lookup must be >= 0");
+    if (c.n_repr > c.unit_size) throw ConfigError("n_repr must not exceed unit_size");
+    if (c.hot_capacity < c.n_lookup) throw ConfigError("hot_capacity must be >= n_lookup");
+    if (c.decay < 0.0 || c.decay > 1.0) throw ConfigError("decay must lie in [0, 1]");
+    if (c.lookup_mode < 0 || c.lookup_mode > 2) throw ConfigError("lookup_mode: unknown value");
+    if (c.position_mode < 0 || c.position_mode > 1) throw ConfigError("position_mode: unknown value");
+}
+
+void validate_shape(const infllm_model_shape& s) {  // types.hpp:45-48
+    if (s.n_layers < 1 || s.n_heads < 1 || s.head_dim < 1)
+        throw ConfigError("ModelShape: all fields must be >= 1");
+    const int hkv = s.n_kv_heads > 0 ? s.n_kv_heads : s.n_heads;
+    if (s.n_heads % hkv != 0) throw ConfigError("ModelShape: n_heads must be a multiple of n_kv_heads");
+}
+
+// device allocation (stream-ordered so pools can grow mid-stream)
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b, cudaStream_t st, bool zero = true) {
+        release(st);
+        if (b == 0) return;
+        ck(cudaMallocAsync(&p, b, st), "cudaMallocAsync");
+        bytes = b;
+        if (zero) ck(cudaMemsetAsync(p, 0, b, st), "cudaMemsetAsync");
+    }
+    void grow(size_t b, cudaStream_t st) {  // keep contents
+        if (b <= bytes) return;
+        void* n = nullptr;
+        ck(cudaMallocAsync(&n, b, st), "cudaMallocAsync");
+        ck(cudaMemsetAsync(n, 0, b, st), "cudaMemsetAsync");
+        if (p) {
+            ck(cudaMemcpyAsync(n, p, bytes, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+            ck(cudaFreeAsync(p, st), "cudaFreeAsync");
+        }
+        p = n;
+        bytes = b;
+    }
+    void release(cudaStream_t st) {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+__global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = v;
+}
+
+}  // namespace
+
+struct infllm_engine {
+    infllm_engine_config cfg{};
+    int H = 1, Gt = 1, rep = 1, d = 0, dv = 0, n_layers = 1;
+    int g0 = 0, Gs = 1, Hs = 1;  // shard
+    int dtype = INFLLM_DTYPE_F32;
+    int device = 0;
+    size_t esz = 4;
+    int64_t R = 0;  // ring capacity
+    int64_t lxp = 0;
+    RopeFreqs freqs{};
+    infllm_allgather_fn allgather = nullptr;
+    void* allgather_user = nullptr;
+    int64_t launches = 0;
+    bool use_tc = false;
+    bool tc_disabled = false;
+
+    // scratch shared by layers (layers run sequentially on one stream)
+    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l;
+
+    struct Layer {
+        int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
+        int64_t n_units = 0, pend_start = 0, pend_count = 0;
+        int64_t trace_count = 0, last_n_sel = 0;
+        int64_t unit_cap = 0, trace_cap = 0;
+        std::vector<int64_t> unit_start;
+        std::vector<int32_t> unit_len;
+        DBuf ring_k, ring_krot, ring_v, P;
+        DBuf init_k, init_krot, init_v;
+        DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
+        DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
+    };
+    std::vector<Layer> layers;
+
+    // profiling (dominant kernel + lookup timing with events on the caller stream)
+    bool prof = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_attn, ev_lookup;
+    std::vector<cudaEvent_t> ev_pool;
+
+    cudaEvent_t take_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        return e;
+    }
+
+    size_t unit_elems_k() const { return static_cast<size_t>(Gs) * cfg.unit_size * d; }
+    size_t unit_elems_v() const { return static_cast<size_t>(Gs) * cfg.unit_size * dv; }
+
+    void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
+        if (need <= L.unit_cap) return;
+        const int64_t cap = std::max<int64_t>({need, 2 * L.unit_cap, 16});
+        L.unit_k.grow(cap * unit_elems_k() * esz, st);
+        if (cfg.position_mode == INFLLM_POSITION_ABSOLUTE) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
+        L.unit_v.grow(cap * unit_elems_v() * esz, st);
+        L.unit_scores.grow(cap * cfg.unit_size * sizeof(float), st);
+        L.repr.grow(cap * static_cast<size_t>(Gs) * cfg.n_repr * d * esz, st);
+        L.repr_idx.grow(cap * cfg.n_repr * sizeof(int32_t), st);
+        const int64_t old = L.unit_cap;
+        L.ulen.grow(cap * sizeof(int32_t), st);
+        k_fill_i32<<<static_cast<unsigned>((cap - old + 255) / 256), 256, 0, st>>>(L.ulen.as<int32_t>() + old, cap - old,
+                                                                                 static_cast<int32_t>(cfg.unit_size));
+        ++launches;
+        L.freq.grow(cap * sizeof(double), st);
+        L.hot.grow(cap * sizeof(int8_t), st);
+        L.rel.grow(cap * sizeof(double), st);
+        L.relw.grow(cap * sizeof(double), st);
+        L.lookup_part.grow(cap * Gt * sizeof(double), st);
+        L.unit_cap = cap;
+    }
+
+    void ensure_trace(Layer& L, int64_t need, cudaStream_t st) {
+        if (need <= L.trace_cap) return;
+        const int64_t cap = std::max<int64_t>({need, 2 * L.trace_cap, 1024});
+        L.trace.grow(cap * 3 * sizeof(int64_t), st);
+        L.trace_cap = cap;
+    }
+
+    void gather(double* buf, int64_t rows, cudaStream_t st) {
+        if (!allgather || Gs == Gt) return;
+        if (allgather(allgather_user, buf, rows, g0, Gs, Gt, st) != 0)
+            throw std::runtime_error("allgather hook failed");
+    }
+
+    bool tc_eligible(int64_t lx) const {
+        (void)lx;
+        return use_tc && !tc_disabled;
+    }
+
+    template <typename T>
+    void step(int li, const void* q, const void* k, const void* v, int64_t lx, bool decode, void* out,
+              cudaStream_t st) {
+        if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
+        if (lx < 1) throw StreamError("step: empty batch");
+        if (!decode && lx > cfg.chunk_size) throw StreamError("encode_chunk: batch exceeds chunk_size");
+        Layer& L = layers[static_cast<size_t>(li)];
+        const bool lookup_enabled = decode ? cfg.lookup_mode != INFLLM_LOOKUP_NONE
+                                           : cfg.lookup_mode == INFLLM_LOOKUP_ENCODE_AND_DECODE;
+        const int64_t s = L.n_fed;
+        const bool do_lookup = lookup_enabled && cfg.n_lookup > 0 && L.n_units > 0;  // engine.hpp:254-255
+        const int64_t n_sel = do_lookup ? std::min<int64_t>(cfg.n_lookup, L.n_units) : 0;
+        const int64_t local_len = s - L.local_start;
+        const int64_t overflow = std::max<int64_t>(0, local_len + lx - cfg.local_size);  // engine.hpp:306
+        const int64_t to_init = std::clamp<int64_t>(cfg.init_size - L.local_start, 0, overflow);  // 311-312
+        const int64_t to_evict = overflow - to_init;
+        const int64_t new_pending = L.pend_count + to_evict;
+        const int64_t completed = new_pending / cfg.unit_size;
+        ensure_units(L, L.n_units + completed + 1, st);
+        ensure_trace(L, L.trace_count + n_sel, st);
+
+        // K7: ring append, RoPE, prefix sums
+        PrepParams pp{};
+        pp.q = q;
+        pp.k = k;
+        pp.v = v;
+        pp.qa = qa.p;
+        pp.qc = qc.p;
+        pp.ring_k = L.ring_k.p;
+        pp.ring_krot = L.ring_krot.p;
+        pp.ring_v = L.ring_v.p;
+        pp.P = L.P.as<double>();
+        pp.chunk_qsum = chunk_qsum.as<double>();
+        pp.s = s;
+        pp.lx = lx;
+        pp.lxp = lxp;
+        pp.R = R;
+        pp.L = cfg.local_size;
+        pp.H = Hs;
+        pp.G = Gs;
+        pp.rep = rep;
+        pp.d = d;
+        pp.dv = dv;
+        pp.freqs = freqs;
+        launch_prep<T>(pp, st);
+        launches += 2;
+
+        // K1 + K2: lookup (memory.hpp:239-269)
+        if (do_lookup) {
+            std::pair<cudaEvent_t, cudaEvent_t> evp{};
+            if (prof) {
+                evp = {take_event(), take_event()};
+                cudaEventRecord(evp.first, st);
+            }
+            LookupParams lp{};
+            lp.qsum = chunk_qsum.as<double>();
+            lp.repr = L.repr.p;
+            lp.part = L.lookup_part.as<double>();
+            lp.U = L.n_units;
+            lp.G = Gs;
+            lp.Gtot = Gt;
+            lp.g0 = g0;
+            lp.r_k = static_cast<int>(cfg.n_repr);
+            lp.d = d;
+            launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            gather(L.lookup_part.as<double>(), L.n_units, st);
+            TopkParams tp{};
+            tp.part = L.lookup_part.as<double>();
+            tp.rel = L.rel.as<double>();
+            tp.relw = L.relw.as<double>();
+            tp.sel = L.sel.as<int64_t>();
+            tp.hot = L.hot.as<int8_t>();
+            tp.hot_list = L.hot_list.as<int64_t>();
+            tp.lru = L.lru.as<LruState>();
+            tp.trace = L.trace.as<int64_t>();
+            tp.U = L.n_units;
+            tp.n_sel = n_sel;
+            tp.step = L.step;
+            tp.Gtot = Gt;
+            launch_topk(tp, st);
+            launches += 2;
+            if (prof) {
+                cudaEventRecord(evp.second, st);
+                ev_lookup.push_back(evp);
+            }
+        }
+
+        // K3: attention over [initial | retrieved | local | chunk] (attention.hpp:116-230)
+        const bool want_mass = do_lookup && n_sel > 0;
+        AttnParams ap{};
+        ap.qa = qa.p;
+        ap.qc = qc.p;
+        ap.out = out;
+        ap.init_k = L.init_k.p;
+        ap.init_krot = L.init_krot.p;
+        ap.init_v = L.init_v.p;
+        ap.unit_k = L.unit_k.p;
+        ap.unit_krot = L.unit_krot.p;
+        ap.unit_v = L.unit_v.p;
+        ap.unit_len = L.ulen.as<int32_t>();
+        ap.sel = L.sel.as<int64_t>();
+        ap.ring_k = L.ring_k.p;
+        ap.ring_krot = L.ring_krot.p;
+        ap.ring_v = L.ring_v.p;
+        ap.mass_e = mass_e.as<float>();
+        ap.mass_m = mass_m.as<float>();
+        ap.row_m = row_m.as<float>();
+        ap.row_l = row_l.as<float>();
+        ap.R = R;
+        ap.s = s;
+        ap.lx = lx;
+        ap.lxp = lxp;
+        ap.init_len = L.init_len;
+        ap.local_start = L.local_start;
+        ap.L = cfg.local_size;
+        ap.l_I = cfg.init_size;
+        ap.n_sel = static_cast<int>(n_sel);
+        ap.H = Hs;
+        ap.G = Gs;
+        ap.rep = rep;
+        ap.d = d;
+        ap.dv = dv;
+        ap.l_bs = static_cast<int>(cfg.unit_size);
+        ap.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+        ap.want_mass = want_mass;
+        ap.scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.hpp:140
+        std::pair<cudaEvent_t, cudaEvent_t> eva{};
+        if (prof) {
+            eva = {take_event(), take_event()};
+            cudaEventRecord(eva.first, st);
+        }
+        if constexpr (std::is_same_v<T, bf16>) {
+            if (tc_eligible(lx)) {
+                launches += launch_attn_tc(ap, st);
+            } else {
+                launch_attn_simt<T>(ap, st);
+                ++launches;
+            }
+        } else {
+            launch_attn_simt<T>(ap, st);
+            ++launches;
+        }
+        if (prof) {
+            cudaEventRecord(eva.second, st);
+            ev_attn.push_back(eva);
+        }
+
+        // attention masses -> frequency update + capacity (engine.hpp:271-285)
+        if (want_mass) {
+            MassParams mp{};
+            mp.mass_e = mass_e.as<float>();
+            mp.mass_m = mass_m.as<float>();
+            mp.row_m = row_m.as<float>();
+            mp.row_l = row_l.as<float>();
+            mp.part = L.mass_part.as<double>();
+            mp.lx = lx;
+            mp.n_sel = static_cast<int>(n_sel);
+            mp.H = Hs;
+            mp.G = Gs;
+            mp.Gtot = Gt;
+            mp.g0 = g0;
+            mp.rep = rep;
+            launch_mass(mp, st);
+            ++launches;
+            gather(L.mass_part.as<double>(), n_sel, st);
+        }
+        LruParams lp{};
+        lp.mass_part = L.mass_part.as<double>();
+        lp.sel = L.sel.as<int64_t>();
+        lp.freq = L.freq.as<double>();
+        lp.hot = L.hot.as<int8_t>();
+        lp.hot_list = L.hot_list.as<int64_t>();
+        lp.unit_len = L.ulen.as<int32_t>();
+        lp.lru = L.lru.as<LruState>();
+        lp.n_sel = want_mass ? n_sel : 0;
+        lp.cap = cfg.hot_capacity;
+        lp.Gtot = Gt;
+        lp.H_total = H;
+        lp.decay = cfg.decay;
+        lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
+        launch_lru(lp, st);
+        ++launches;
+
+        // window roll: init pinning, eviction, representative scoring, packing
+        if (overflow > 0) {
+            // UnitPacker::add: an empty packer starts its pending run at the
+            // first evicted token (memory.hpp:65-66)
+            if (L.pend_count == 0 && to_evict > 0) L.pend_start = L.local_start + to_init;
+            EvictParams ep{};
+            ep.ring_k = L.ring_k.p;
+            ep.ring_krot = L.ring_krot.p;
+            ep.ring_v = L.ring_v.p;
+            ep.P = L.P.as<double>();
+            ep.init_k = L.init_k.p;
+            ep.init_krot = L.init_krot.p;
+            ep.init_v = L.init_v.p;
+            ep.unit_k = L.unit_k.p;
+            ep.unit_krot = L.unit_krot.p;
+            ep.unit_v = L.unit_v.p;
+            ep.ev_part = L.ev_part.as<double>();
+            ep.pop0 = L.local_start;
+            ep.n_init = to_init;
+            ep.n_evict = to_evict;
+            ep.R = R;
+            ep.L = cfg.local_size;
+            ep.l_I = cfg.init_size;
+            ep.pend_start = L.pend_start;
+            ep.unit0 = L.n_units;
+            ep.G = Gs;
+            ep.Gtot = Gt;
+            ep.g0 = g0;
+            ep.d = d;
+            ep.dv = dv;
+            ep.l_bs = static_cast<int>(cfg.unit_size);
+            ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+            launch_evict<T>(ep, st);
+            ++launches;
+            if (to_evict > 0) {
+                gather(L.ev_part.as<double>(), to_evict, st);
+                FinalizeParams fp{};
+                fp.ev_part = L.ev_part.as<double>();
+                fp.unit_scores = L.unit_scores.as<float>();
+                fp.e0 = L.local_start + to_init;
+                fp.n_evict = to_evict;
+                fp.pend_start = L.pend_start;
+                fp.unit0 = L.n_units;
+                fp.L = cfg.local_size;
+                fp.Gtot = Gt;
+                fp.l_bs = static_cast<int>(cfg.unit_size);
+                launch_finalize(fp, st);
+                ++launches;
+            }
+            if (completed > 0) {
+                SelectParams sp{};
+                sp.unit_scores = L.unit_scores.as<float>();
+                sp.unit_len = L.ulen.as<int32_t>();
+                sp.unit_k = L.unit_k.p;
+                sp.repr = L.repr.p;
+                sp.repr_idx = L.repr_idx.as<int32_t>();
+                sp.u0 = L.n_units;
+                sp.n_units = completed;
+                sp.G = Gs;
+                sp.r_k = static_cast<int>(cfg.n_repr);
+                sp.d = d;
+                sp.l_bs = static_cast<int>(cfg.unit_size);
+                launch_select<T>(sp, st);
+                ++launches;
+                for (int64_t c = 0; c < completed; ++c) {
+                    L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
+                    L.unit_len.push_back(static_cast<int32_t>(cfg.unit_size));
+                }
+                L.n_units += completed;
+                L.pend_start += completed * cfg.unit_size;
+            }
+            L.pend_count = new_pending - completed * cfg.unit_size;
+            L.local_start += overflow;
+            L.init_len += to_init;
+        }
+        L.trace_count += n_sel;
+        L.last_n_sel = n_sel;
+        L.n_fed += lx;
+        L.step += 1;
+        ck(cudaGetLastError(), "kernel launch");
+    }
+
+    template <typename T>
+    void finish(cudaStream_t st) {  // engine.hpp:115-119, UnitPacker::flush memory.hpp:81-84
+        for (auto& L : layers) {
+            if (L.pend_count == 0) continue;
+            ensure_units(L, L.n_units + 1, st);
+            const int32_t len = static_cast<int32_t>(L.pend_count);
+            k_fill_i32<<<1, 1, 0, st>>>(L.ulen.as<int32_t>() + L.n_units, 1, len);
+            ++launches;
+            SelectParams sp{};
+            sp.unit_scores = L.unit_scores.as<float>();
+            sp.unit_len = L.ulen.as<int32_t>();
+            sp.unit_k = L.unit_k.p;
+            sp.repr = L.repr.p;
+            sp.repr_idx = L.repr_idx.as<int32_t>();
+            sp.u0 = L.n_units;
+            sp.n_units = 1;
+            sp.G = Gs;
+            sp.r_k = static_cast<int>(cfg.n_repr);
+            sp.d = d;
+            sp.l_bs = static_cast<int>(cfg.unit_size);
+            launch_select<T>(sp, st);
+            ++launches;
+            L.unit_start.push_back(L.pend_start);
+            L.unit_len.push_back(len);
+            L.n_units += 1;
+            L.pend_start += L.pend_count;
+            L.pend_count = 0;
+        }
+        ck(cudaStreamSynchronize(st), "finish");
+    }
+};
+
+extern "C" {
+
+const char* infllm_last_error(void) { return g_err.c_str(); }
+
+const char* infllm_version(void) {
+    return "infllm_b200 0.1 (sm_100a; fp32 CUDA-core + bf16 tcgen05 attention)";
+}
+
+int infllm_config_default(infllm_engine_config* c) {
+    if (!c) return INFLLM_ERR_ARG;
+    c->chunk_size = 512;
+    c->unit_size = 128;
+    c->n_repr = 4;
+    c->local_size = 4096;
+    c->init_size = 128;
+    c->n_lookup = 32;
+    c->hot_capacity = 32;
+    c->decay = 0.1;
+    c->lookup_mode = INFLLM_LOOKUP_ENCODE_AND_DECODE;
+    c->position_mode = INFLLM_POSITION_CLAMPED;
+    return INFLLM_OK;
+}
+
+int infllm_config_validate(const infllm_engine_config* cfg, const infllm_model_shape* shape) {
+    return guard([&] {
+        if (!cfg) throw ConfigError("null config");
+        validate_cfg(*cfg);
+        if (shape) validate_shape(*shape);
+    });
+}
+
+int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_shape* shape, int32_t dtype,
+                         int32_t device, int32_t kv_group_begin, int32_t kv_group_count, infllm_engine_t* out) {
+    return guard([&] {
+        if (!cfg || !shape || !out) throw ConfigError("null argument");
+        validate_cfg(*cfg);
+        validate_shape(*shape);
+        if (dtype != INFLLM_DTYPE_F32 && dtype != INFLLM_DTYPE_BF16) throw ConfigError("dtype must be f32 or bf16");
+        auto e = std::make_unique<infllm_engine>();
+        e->cfg = *cfg;
+        e->H = shape->n_heads;
+        e->Gt = shape->n_kv_heads > 0 ? shape->n_kv_heads : shape->n_heads;
+        e->rep = e->H / e->Gt;
+        e->d = shape->head_dim;
+        e->dv = shape->value_dim > 0 ? shape->value_dim : shape->head_dim;
+        e->n_layers = shape->n_layers;
+        if (e->d > 256 || e->dv > 128) throw ConfigError("head_dim <= 256 and value_dim <= 128 supported");
+        if (cfg->n_repr > 32) throw ConfigError("n_repr <= 32 supported");
+        if (kv_group_count <= 0) {
+            kv_group_begin = 0;
+            kv_group_count = e->Gt;
+        }
+        if (kv_group_begin < 0 || kv_group_begin + kv_group_count > e->Gt)
+            throw ConfigError("kv group shard out of range");
+        e->g0 = kv_group_begin;
+        e->Gs = kv_group_count;
+        e->Hs = e->Gs * e->rep;
+        e->dtype = dtype;
+        e->device = device;
+        e->esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
+        const int64_t need = cfg->local_size + cfg->chunk_size + 1;
+        e->R = (need + 127) / 128 * 128;
+        e->lxp = (cfg->chunk_size + 127) / 128 * 128;
+        for (int a = 0; a < e->d / 2; ++a) e->freqs.f[a] = std::pow(10000.0, -2.0 * a / e->d);  // rotary.hpp:25
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaStream_t st = nullptr;
+        const size_t es = e->esz;
+        e->qa.alloc(static_cast<size_t>(e->Hs) * e->lxp * e->d * es, st);
+        e->qc.alloc(static_cast<size_t>(e->Hs) * e->lxp * e->d * es, st);
+        e->chunk_qsum.alloc(static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
+        const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
+        e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
+        e->mass_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
+        e->row_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
+        e->row_l.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
+        e->layers.resize(static_cast<size_t>(e->n_layers));
+        for (auto& L : e->layers) {
+            L.ring_k.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
+            L.ring_krot.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
+            L.ring_v.alloc(static_cast<size_t>(e->Gs) * e->R * e->dv * es, st);
+            L.P.alloc(static_cast<size_t>(e->R) * e->Gs * e->d * sizeof(double), st);
+            const size_t ni = static_cast<size_t>(std::max<int64_t>(cfg->init_size, 1));
+            L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
+            if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
+                L.init_krot.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
+            L.init_v.alloc(static_cast<size_t>(e->Gs) * ni * e->dv * es, st);
+            L.hot_list.alloc(static_cast<size_t>(cfg->hot_capacity + km + 1) * sizeof(int64_t), st);
+            L.lru.alloc(sizeof(LruState), st);
+            L.sel.alloc(km * sizeof(int64_t), st);
+            L.mass_part.alloc(km * e->Gt * sizeof(double), st);
+            L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
+        }
+        e->use_tc = dtype == INFLLM_DTYPE_BF16 && attn_tc_supported(e->d, e->dv, static_cast<int>(cfg->unit_size),
+                                                                     cfg->position_mode == INFLLM_POSITION_ABSOLUTE);
+        ck(cudaStreamSynchronize(st), "engine_create");
+        *out = e.release();
+    });
+}
+
+int infllm_engine_destroy(infllm_engine_t e) {
+    return guard([&] {
+        if (!e) return;
+        cudaDeviceSynchronize();
+        cudaStream_t st = nullptr;
+        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l}) b->release(st);
+        for (auto& L : e->layers)
+            for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
+                            &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
+                            &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
+                            &L.ev_part})
+                b->release(st);
+        for (auto& p : e->ev_attn) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        for (auto& p : e->ev_lookup) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        for (auto ev : e->ev_pool) cudaEventDestroy(ev);
+        cudaDeviceSynchronize();
+        delete e;
+    });
+}
+
+int infllm_engine_set_allgather(infllm_engine_t e, infllm_allgather_fn fn, void* user) {
+    if (!e) return INFLLM_ERR_ARG;
+    e->allgather = fn;
+    e->allgather_user = user;
+    return INFLLM_OK;
+}
+
+int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
+    return guard([&] {
+        cudaStream_t st = nullptr;
+        const int64_t units = std::max<int64_t>(0, max_tokens - e->cfg.init_size) / e->cfg.unit_size + 2;
+        for (auto& L : e->layers) {
+            e->ensure_units(L, units, st);
+            const int64_t steps = (max_tokens + e->cfg.chunk_size - 1) / e->cfg.chunk_size + 1;
+            e->ensure_trace(L, steps * std::max<int64_t>(e->cfg.n_lookup, 1), st);
+        }
+        ck(cudaStreamSynchronize(st), "reserve");
+    });
+}
+
+int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) {
+    return guard([&] {
+        const std::string k = key ? key : "";
+        if (k == "tc_attention")
+            e->tc_disabled = value == 0;
+        else
+            throw ConfigError("unknown option '" + k + "'");
+    });
+}
+
+int infllm_encode_chunk(infllm_engine_t e, int32_t layer, const void* q, const void* k, const void* v, int64_t l_x,
+                        void* out, void* stream) {
+    return guard([&] {
+        if (!e) throw ConfigError("null engine");
+        auto st = static_cast<cudaStream_t>(stream);
+        if (e->dtype == INFLLM_DTYPE_BF16)
+            e->step<bf16>(layer, q, k, v, l_x, false, out, st);
+        else
+            e->step<float>(layer, q, k, v, l_x, false, out, st);
+    });
+}
+
+int infllm_decode_step(infllm_engine_t e, int32_t layer, const void* q, const void* k, const void* v, void* out,
+                       void* stream) {
+    return guard([&] {
+        if (!e) throw ConfigError("null engine");
+        auto st = static_cast<cudaStream_t>(stream);
+        if (e->dtype == INFLLM_DTYPE_BF16)
+            e->step<bf16>(layer, q, k, v, 1, true, out, st);
+        else
+            e->step<float>(layer, q, k, v, 1, true, out, st);
+    });
+}
+
+int infllm_finish(infllm_engine_t e, void* stream) {
+    return guard([&] {
+        auto st = static_cast<cudaStream_t>(stream);
+        if (e->dtype == INFLLM_DTYPE_BF16)
+            e->finish<bf16>(st);
+        else
+            e->finish<float>(st);
+    });
+}
+
+int infllm_retrieved_ids(infllm_engine_t e, int32_t layer, int64_t* host_ids, int64_t cap, int64_t* n_out) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        ck(cudaDeviceSynchronize(), "sync");
+        *n_out = L.last_n_sel;
+        const int64_t n = std::min(cap, L.last_n_sel);
+        if (n > 0) ck(cudaMemcpy(host_ids, L.sel.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int infllm_get_layer_metrics(infllm_engine_t e, int32_t layer, infllm_layer_metrics* m) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        ck(cudaDeviceSynchronize(), "sync");
+        LruState s{};
+        ck(cudaMemcpy(&s, L.lru.p, sizeof(s), cudaMemcpyDeviceToHost), "D2H");
+        m->units = L.n_units;
+        m->hot_units = s.hot_count;
+        m->peak_hot_units = s.peak_hot_units;
+        m->peak_hot_bytes = s.peak_hot_bytes;
+        m->hits = s.hits;
+        m->misses = s.misses;
+        m->loads = s.loads;
+        m->evictions = s.evictions;
+        m->requested = s.requested;
+    });
+}
+
+int infllm_unit_info(infllm_engine_t e, int32_t layer, int64_t id, int64_t* start_abs, int64_t* size,
+                     int64_t* host_repr_abs, int64_t* n_repr_out) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        if (id < 0 || id >= L.n_units) throw StreamError("unit id out of range");
+        ck(cudaDeviceSynchronize(), "sync");
+        std::vector<int32_t> idx(static_cast<size_t>(e->cfg.n_repr));
+        ck(cudaMemcpy(idx.data(), L.repr_idx.as<int32_t>() + id * e->cfg.n_repr, idx.size() * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost),
+           "D2H");
+        *start_abs = L.unit_start[static_cast<size_t>(id)];
+        *size = L.unit_len[static_cast<size_t>(id)];
+        int64_t n = 0;
+        for (auto x : idx)
+            if (x >= 0) host_repr_abs[n++] = *start_abs + x;
+        *n_repr_out = n;
+    });
+}
+
+int infllm_stream_state(infllm_engine_t e, int32_t layer, int64_t* fed, int64_t* steps, int64_t* init_len,
+                        int64_t* local_len, int64_t* pending) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        *fed = L.n_fed;
+        *steps = L.step;
+        *init_len = L.init_len;
+        *local_len = L.n_fed - L.local_start;
+        *pending = L.pend_count;
+    });
+}
+
+int infllm_unit_freq(infllm_engine_t e, int32_t layer, double* host_freq, int32_t* host_hot, int64_t n) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        n = std::min(n, L.n_units);
+        ck(cudaDeviceSynchronize(), "sync");
+        if (n <= 0) return;
+        ck(cudaMemcpy(host_freq, L.freq.p, n * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+        std::vector<int8_t> h(static_cast<size_t>(n));
+        ck(cudaMemcpy(h.data(), L.hot.p, n, cudaMemcpyDeviceToHost), "D2H");
+        for (int64_t i = 0; i < n; ++i) host_hot[i] = h[static_cast<size_t>(i)];
+    });
+}
+
+int infllm_trace(infllm_engine_t e, int32_t layer, int64_t* host_step, int64_t* host_unit, int32_t* host_hit,
+                 int64_t cap, int64_t* n_out) {
+    return guard([&] {
+        auto& L = e->layers.at(static_cast<size_t>(layer));
+        ck(cudaDeviceSynchronize(), "sync");
+        *n_out = L.trace_count;
+        const int64_t n = std::min(cap, L.trace_count);
+        if (n <= 0) return;
+        std::vector<int64_t> t(static_cast<size_t>(3 * n));
+        ck(cudaMemcpy(t.data(), L.trace.p, t.size() * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+        for (int64_t i = 0; i < n; ++i) {
+            host_step[i] = t[static_cast<size_t>(3 * i)];
+            host_unit[i] = t[static_cast<size_t>(3 * i + 1)];
+            host_hit[i] = static_cast<int32_t>(t[static_cast<size_t>(3 * i + 2)]);
+        }
+    });
+}
+
+int infllm_kernel_launches(infllm_engine_t e, int64_t* n_out) {
+    *n_out = e->launches;
+    return INFLLM_OK;
+}
+
+int infllm_profile_begin(infllm_engine_t e, int32_t enable) {
+    return guard([&] {
+        for (auto& p : e->ev_attn) {
+            e->ev_pool.push_back(p.first);
+            e->ev_pool.push_back(p.second);
+        }
+        for (auto& p : e->ev_lookup) {
+            e->ev_pool.push_back(p.first);
+            e->ev_pool.push_back(p.second);
+        }
+        e->ev_attn.clear();
+        e->ev_lookup.clear();
+        e->prof = enable != 0;
+    });
+}
+
+int infllm_profile_read(infllm_engine_t e, double* attn_ms, int64_t* attn_n, double* lookup_ms, int64_t* lookup_n) {
+    return guard([&] {
+        ck(cudaDeviceSynchronize(), "sync");
+        double a = 0, b = 0;
+        for (auto& p : e->ev_attn) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
+            a += ms;
+        }
+        for (auto& p : e->ev_lookup) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
+            b += ms;
+        }
+        *attn_ms = a;
+        *attn_n = static_cast<int64_t>(e->ev_attn.size());
+        *lookup_ms = b;
+        *lookup_n = static_cast<int64_t>(e->ev_lookup.size());
+    });
+}
+
+int infllm_select_representatives(const float* scores, const int64_t* lens, int64_t n_units, int64_t unit_len,
+                                  int64_t r_k, int64_t* idx, void* stream) {
+    return guard([&] {
+        if (r_k < 1 || r_k > 32) throw ConfigError("r_k must be in [1, 32]");
+        launch_select_standalone(scores, lens, n_units, unit_len, r_k, idx, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "select");
+    });
+}
+
+int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n_units, int64_t r_k,
+                  int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel, int64_t* ids, void* stream) {
+    return guard([&] {
+        auto st = static_cast<cudaStream_t>(stream);
+        if (n_units <= 0) return;
+        DBuf part, relw;
+        part.alloc(static_cast<size_t>(n_units) * n_kv_heads * sizeof(double), st, false);
+        relw.alloc(static_cast<size_t>(n_units) * sizeof(double), st, false);
+        LookupParams lp{};
+        lp.qsum = qsum;
+        lp.repr = repr;
+        lp.part = part.as<double>();
+        lp.U = n_units;
+        lp.G = n_kv_heads;
+        lp.Gtot = n_kv_heads;
+        lp.g0 = 0;
+        lp.r_k = static_cast<int>(r_k);
+        lp.d = head_dim;
+        launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+        launch_rel_topk_standalone(part.as<double>(), n_units, n_kv_heads, std::min(k_m, n_units), rel,
+                                   relw.as<double>(), ids, st);
+        part.release(st);
+        relw.release(st);
+        ck(cudaGetLastError(), "lookup");
+    });
+}
+
+}  // extern "C"

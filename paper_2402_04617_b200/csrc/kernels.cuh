@@ -1,0 +1,160 @@
+// kernels.cuh — device-side layer state layout and kernel launch interfaces.
+//
+// HBM layout of one layer (G = KV groups owned by this engine, R = ring
+// capacity, a multiple of 128 >= local_size + chunk_size + 1):
+//   ring_k / ring_krot / ring_v  [G][R][d]       raw keys, RoPE'd keys
+//                                                 (rotated once at append by
+//                                                 their absolute position), values
+//   P                            [R][G][d] f64   prefix sums of qs_t = sum of
+//                                                 the group's query heads
+//   init_k / init_krot / init_v  [G][l_I][d]     pinned initial tokens
+//   unit_k / unit_krot / unit_v  [U][G][l_bs][d] unit pages (krot only in
+//                                                 absolute position mode)
+//   repr                         [U][G][r_k][d]  representative keys (lookup index)
+//   unit_scores                  [U][l_bs] f32   finalized r_m per token
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace infllm {
+
+struct PrepParams {
+    const void* q;  // [lx][H][d]
+    const void* k;  // [lx][G][d]
+    const void* v;  // [lx][G][dv]
+    void* qa;       // [H][lxp][d]  rope(q, pos)
+    void* qc;       // [H][lxp][d]  rope(q, L)
+    void* ring_k;
+    void* ring_krot;
+    void* ring_v;
+    double* P;           // [R][G][d]
+    double* chunk_qsum;  // [G][d]
+    int64_t s, lx, lxp, R, L;
+    int H, G, rep, d, dv;
+    RopeFreqs freqs;
+};
+
+struct LookupParams {
+    const double* qsum;  // [G][d]
+    const void* repr;    // [U][G][r_k][d]
+    double* part;        // [U][Gtot] (writes columns g0..g0+G)
+    int64_t U;
+    int G, Gtot, g0, r_k, d;
+};
+
+struct TopkParams {
+    const double* part;  // [U][Gtot]
+    double* rel;         // [U]
+    double* relw;        // [U] scratch
+    int64_t* sel;        // [n_sel] ascending
+    int8_t* hot;         // [U]
+    int64_t* hot_list;   // [cap + k_m + 1]
+    LruState* lru;
+    int64_t* trace;      // [trace_cap][3]: step, unit, hit
+    int64_t U, n_sel, step;
+    int Gtot;
+};
+
+struct AttnParams {
+    const void* qa;
+    const void* qc;
+    void* out;  // [lx][H][dv]
+    const void* init_k;
+    const void* init_krot;
+    const void* init_v;
+    const void* unit_k;
+    const void* unit_krot;
+    const void* unit_v;
+    const int32_t* unit_len;
+    const int64_t* sel;
+    const void* ring_k;
+    const void* ring_krot;
+    const void* ring_v;
+    float* mass_e;  // [H][lx][n_sel]
+    float* mass_m;
+    float* row_m;   // [H][lx]
+    float* row_l;
+    int64_t R, s, lx, lxp, init_len, local_start, L, l_I;
+    int n_sel, H, G, rep, d, dv, l_bs;
+    int absolute, want_mass;
+    float scale;
+};
+
+struct MassParams {
+    const float* mass_e;
+    const float* mass_m;
+    const float* row_m;
+    const float* row_l;
+    double* part;  // [n_sel][Gtot]
+    int64_t lx;
+    int n_sel, H, G, Gtot, g0, rep;
+};
+
+struct LruParams {
+    const double* mass_part;  // [n_sel][Gtot]
+    const int64_t* sel;
+    double* freq;       // [U]
+    int8_t* hot;        // [U]
+    int64_t* hot_list;
+    const int32_t* unit_len;
+    LruState* lru;
+    int64_t n_sel, cap;
+    int Gtot, H_total;
+    double decay;
+    int64_t bytes_per_token;
+};
+
+struct EvictParams {
+    const void* ring_k;
+    const void* ring_krot;
+    const void* ring_v;
+    const double* P;
+    void* init_k;
+    void* init_krot;
+    void* init_v;
+    void* unit_k;
+    void* unit_krot;
+    void* unit_v;
+    double* ev_part;  // [n_evict][Gtot]
+    int64_t pop0, n_init, n_evict, R, L, l_I;
+    int64_t pend_start, unit0;  // token pend_start belongs to unit id unit0 at offset 0
+    int G, Gtot, g0, d, dv, l_bs, absolute;
+};
+
+struct FinalizeParams {
+    const double* ev_part;
+    float* unit_scores;  // [U][l_bs]
+    int64_t e0, n_evict, pend_start, unit0, L;
+    int Gtot, l_bs;
+};
+
+struct SelectParams {
+    const float* unit_scores;
+    const int32_t* unit_len;
+    const void* unit_k;
+    void* repr;        // [U][G][r_k][d]
+    int32_t* repr_idx; // [U][r_k]
+    int64_t u0, n_units;
+    int G, r_k, d, l_bs;
+};
+
+template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
+void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
+void launch_topk(const TopkParams& p, cudaStream_t st);
+template <typename T> void launch_attn_simt(const AttnParams& p, cudaStream_t st);
+void launch_mass(const MassParams& p, cudaStream_t st);
+void launch_lru(const LruParams& p, cudaStream_t st);
+template <typename T> void launch_evict(const EvictParams& p, cudaStream_t st);
+void launch_finalize(const FinalizeParams& p, cudaStream_t st);
+template <typename T> void launch_select(const SelectParams& p, cudaStream_t st);
+
+// standalone select (C ABI infllm_select_representatives)
+void launch_select_standalone(const float* scores, const int64_t* lens, int64_t n_units, int64_t unit_len,
+                              int64_t r_k, int64_t* idx, cudaStream_t st);
+// standalone relevance reduce + top-k (C ABI infllm_lookup)
+void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
+                                int64_t* ids, cudaStream_t st);
+
+}  // namespace infllm
