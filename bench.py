@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""bench.py — InfLLM layer prefill tokens/s @128K context, Llama-3-8B heads.
+
+Workload (BASELINE.json configs[2], the metric's config): one InfLLM layer,
+32 query / 8 KV heads, d = 128, bf16, chunked prefill of a 131072-token
+stream (chunk 512, unit 128, r_k 4, k_m 16, init 128, local window 4096,
+hot capacity 32, decay 0.1). One bench "step" = the whole 128K-token stream
+(256 chunk steps: lookup, attention, LRU, scoring, packing) through a freshly
+reset engine. Inputs: synthetic N(0,1) q/k/v (seeded), resident in HBM
+(1.5 GB > L2, so no flush is needed between steps).
+
+--gpus N (torchrun): N independent streams, one per GPU (weak scaling, no
+collective on the data path; KV-group sharding with the cross-shard score
+exchange is a latency mode).
+--impl reference: the reference algorithm on the host CPU (the oracle port,
+pinned bit-exact to the reference engine), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=4096, init_size=128, n_lookup=16, hot_capacity=32,
+           decay=0.1, lookup_mode=0, position_mode=0)
+SHAPE = dict(n_heads=32, n_kv_heads=8, head_dim=128)
+N_TOKENS = 131072
+METRIC = "InfLLM layer prefill tokens/s @128K ctx (Llama-3-8B heads), 1/2/4/8 B200"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm=j.get("hbm_gbs", 6650.0), bf16=j.get("bf16_tflops", 1590.0),
+                    bf16_sust=j.get("bf16_tflops_sustained", 1400.0), src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback")
+
+
+def stream_schedule(n, cfg):
+    """Host replay of the stream arithmetic (engine.hpp:242-346): per chunk
+    step (l_x, n_ctx keys before the chunk, units U at lookup, n_sel)."""
+    steps = []
+    fed = local_start = init_len = units = pend = 0
+    C, L, I, bs, km = cfg["chunk_size"], cfg["local_size"], cfg["init_size"], cfg["unit_size"], cfg["n_lookup"]
+    while fed < n:
+        lx = min(C, n - fed)
+        n_sel = min(km, units) if (km > 0 and units > 0) else 0
+        local_len = fed - local_start
+        steps.append(dict(lx=lx, n_ctx=init_len + n_sel * bs + local_len, units=units, n_sel=n_sel))
+        overflow = max(0, local_len + lx - L)
+        to_init = min(max(I - local_start, 0), overflow)
+        pend += overflow - to_init
+        units += pend // bs
+        pend %= bs
+        local_start += overflow
+        init_len += to_init
+        fed += lx
+    return steps
+
+
+def attention_flops(steps, H, d):
+    """QK^T + PV over attended pairs only: 4 d H [l_x W + l_x(l_x+1)/2]."""
+    return sum(4.0 * d * H * (s["lx"] * s["n_ctx"] + s["lx"] * (s["lx"] + 1) / 2) for s in steps)
+
+
+def lookup_bytes(steps, cfg, Hkv, d, H, elem=2):
+    """repr-index scan + chunk queries read."""
+    return sum(s["units"] * cfg["n_repr"] * Hkv * d * elem + s["lx"] * H * d * elem for s in steps if s["n_sel"] > 0)
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        busy = [r for r in self.rows if (num(r[6]) or 0) > 0] or self.rows
+        sm = [num(r[0]) for r in busy if num(r[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- reference arm
+def cpu_sample(threads, steps=2, warm=8192, seed=0):
+    """The reference algorithm (oracle port, bit-exact to the reference engine
+    compiled here) on host cores: warm-start 8192 tokens of C2 through the
+    window/packing bookkeeping, then time `steps` full steady-state chunk
+    steps (lookup + attend + score + evict, PhaseTimings phases)."""
+    from oracle import oracle as O
+
+    O.build()
+    H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
+    C = CFG["chunk_size"]
+    rng = np.random.default_rng(seed)
+    n = warm + steps * C
+
+    def bf(x):
+        import torch
+        return torch.from_numpy(x).bfloat16().float().numpy()
+
+    q = bf(rng.standard_normal((n, H, d), dtype=np.float32))
+    k = bf(rng.standard_normal((n, Hkv, d), dtype=np.float32))
+    v = bf(rng.standard_normal((n, Hkv, d), dtype=np.float32))
+    eng = O.OracleEngine(O.EngineConfig.make(**CFG), O.ModelShape.make(n_heads=H, n_kv_heads=Hkv, head_dim=d),
+                         n_threads=threads)
+    eng.warm_start(q[:warm], k[:warm], v[:warm])
+    t0 = time.perf_counter()
+    for s in range(steps):
+        a = warm + s * C
+        eng.step(q[a:a + C], k[a:a + C], v[a:a + C])
+    dt = time.perf_counter() - t0
+    return dict(value=steps * C / dt, unit="tokens/s", cores=threads, kind="port",
+                sample=f"{steps} steady-state C2 chunk steps ({steps * C} tokens, window {CFG['init_size']}+"
+                       f"{CFG['n_lookup']}x{CFG['unit_size']}+{CFG['local_size']}) after an {warm}-token warm start; "
+                       f"oracle port of the reference engine (bit-exact pinned), {threads} threads over heads",
+                seconds=dt)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(threads, steps=1, seed=i)
+        if i >= args.warmup:
+            vals.append(r)
+    v = statistics.mean(x["value"] for x in vals)
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 * CFG["chunk_size"] / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C2: Llama-3-8B heads (32q/8kv, d128), 128K ctx chunked prefill, k_m 16, "
+                                   "l_L 4096, l_I 128, chunk 512; CPU sample of steady-state chunk steps"},
+            "cpu_baseline": {k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
+    n, C = args.tokens, CFG["chunk_size"]
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    Q = torch.randn((n, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    K = torch.randn((n, Hkv, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    V = torch.randn((n, Hkv, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    OUT = torch.empty((n, H, d), device=dev, dtype=torch.bfloat16)
+    eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16, device=local_rank)
+    if args.no_tc:
+        eng.set_option("tc_attention", 0)
+    eng.reserve(n)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_stream():
+        eng.reset()
+        for off in range(0, n, C):
+            e = min(n, off + C)
+            eng.encode_chunk(Q[off:e], K[off:e], V[off:e], out=OUT[off:e])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        one_stream()
+    barrier()
+    launches0 = eng.kernel_launches()
+    eng.profile_begin(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_stream()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    prof = eng.profile_read()
+    eng.profile_begin(False)
+    launches = eng.kernel_launches() - launches0
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = world * n * args.steps / (ms / 1000.0)
+
+    # end-to-end through the C-ABI with HOST buffers: per chunk H2D of q/k/v
+    # from pinned memory and D2H of the attention output, pipelined on copy
+    # streams (inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(eng, Q, K, V, n, C, dev, args, world)
+
+    steps = stream_schedule(n, CFG)
+    flops = attention_flops(steps, H, d)
+    peaks = load_peaks()
+    attn_ms = prof["attn_ms"] / max(1, args.steps)
+    achieved = flops / (attn_ms / 1000.0) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    lk_bytes = lookup_bytes(steps, CFG, Hkv, d, H)
+    lk_ms = prof["lookup_ms"] / max(1, args.steps)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            try:
+                cpu = cpu_sample(os.cpu_count() or 1, steps=1)
+                cpu.pop("seconds", None)
+            except Exception as ex:  # reported, not fatal
+                cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "C2: Llama-3-8B heads (32q/8kv, d128), 131072-token chunked prefill of one "
+                                   "InfLLM layer per GPU (chunk 512, unit 128, r_k 4, k_m 16, init 128, local 4096, "
+                                   "hot 32); step = whole stream",
+                       "tokens_per_step_per_gpu": n, "l2": "inputs 1.5 GB > L2 (no flush needed)",
+                       "parallelism": f"{world} independent streams" if world > 1 else "1 stream"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
+                         "frac": achieved / peaks["bf16"], "traffic": traffic,
+                         "kernel": "attention (K3)", "flops_per_stream": flops,
+                         "avg_launch_ms": attn_ms / len(steps), "launches_per_stream": len(steps),
+                         "peak_src": peaks["src"] + " burst bf16 (sustained %.1f)" % peaks["bf16_sust"],
+                         "lookup": {"achieved_gbs": lk_bytes / (lk_ms / 1000.0) / 1e9 if lk_ms > 0 else None,
+                                    "peak_gbs": peaks["hbm"], "bytes_per_stream": lk_bytes,
+                                    "ms_per_stream": lk_ms}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(eng, Q, K, V, n, C, dev, args, world):
+    import torch
+
+    Hq = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+    Hk = torch.empty(K.shape, dtype=K.dtype, pin_memory=True)
+    Hv = torch.empty(V.shape, dtype=V.dtype, pin_memory=True)
+    Hq.copy_(Q)
+    Hk.copy_(K)
+    Hv.copy_(V)
+    Hout = torch.empty(Q.shape, dtype=Q.dtype, pin_memory=True)
+    nb = 3
+    dq = [torch.empty((C,) + tuple(Q.shape[1:]), dtype=Q.dtype, device=dev) for _ in range(nb)]
+    dk = [torch.empty((C,) + tuple(K.shape[1:]), dtype=K.dtype, device=dev) for _ in range(nb)]
+    dvv = [torch.empty((C,) + tuple(V.shape[1:]), dtype=V.dtype, device=dev) for _ in range(nb)]
+    do = [torch.empty((C,) + tuple(Q.shape[1:]), dtype=Q.dtype, device=dev) for _ in range(nb)]
+    comp = torch.cuda.current_stream(dev)
+    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    torch.cuda.synchronize(dev)
+
+    def stream_once():
+        eng.reset(comp)
+        chunks = list(range(0, n, C))
+        loaded, computed, freed = {}, {}, {}
+        def load(i):
+            off = chunks[i]
+            e = min(n, off + C)
+            b = i % nb
+            with torch.cuda.stream(h2d):
+                if i >= nb:
+                    h2d.wait_event(freed[i - nb])
+                dq[b][: e - off].copy_(Hq[off:e], non_blocking=True)
+                dk[b][: e - off].copy_(Hk[off:e], non_blocking=True)
+                dvv[b][: e - off].copy_(Hv[off:e], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d)
+                loaded[i] = ev
+        for i in range(min(nb - 1, len(chunks))):
+            load(i)
+        for i, off in enumerate(chunks):
+            if i + nb - 1 < len(chunks):
+                load(i + nb - 1)
+            e = min(n, off + C)
+            b = i % nb
+            comp.wait_event(loaded[i])
+            eng.encode_chunk(dq[b][: e - off], dk[b][: e - off], dvv[b][: e - off], out=do[b][: e - off], stream=comp)
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev)
+                Hout[off:e].copy_(do[b][: e - off], non_blocking=True)
+                fe = torch.cuda.Event()
+                fe.record(d2h)
+                freed[i] = fe
+        comp.wait_stream(d2h)
+
+    stream_once()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        stream_once()
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    # device-side check: the e2e output must equal the resident-input run's output
+    h2d_b = (Q.numel() + K.numel() + V.numel()) * Q.element_size()
+    d2h_b = Q.numel() * Q.element_size()
+    return {"value": world * n * args.steps / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b,
+            "note": "C-ABI encode_chunk with pinned-host q/k/v/out, H2D/D2H on copy streams overlapped with compute"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--tokens", type=int, default=N_TOKENS)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tc", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_b200(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

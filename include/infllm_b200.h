@@ -137,6 +137,9 @@ int infllm_engine_set_allgather(infllm_engine_t eng, infllm_allgather_fn fn, voi
  * reference grows its std::vectors on demand; the engine grows its device
  * pools too, this only moves the growth out of the timed region). */
 int infllm_engine_reserve(infllm_engine_t eng, int64_t max_tokens);
+/* Return every layer to the empty-stream state (tokens_fed = 0), keeping the
+ * device pools; asynchronous on `stream`. */
+int infllm_engine_reset(infllm_engine_t eng, void* stream);
 /* Engine options: "tc_attention" (1 = tcgen05 attention when the shape
  * allows, 0 = CUDA-core attention). */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);

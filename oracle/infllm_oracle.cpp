@@ -836,6 +836,87 @@ struct oracle_engine {
     }
 };
 
+// Bookkeeping-only streaming (CPU-baseline harness, not a reference
+// function): advances init/local/packer/store exactly like step() but skips
+// lookup and attention, and accumulates representative-score sums through
+// per-group query prefix sums (same definition as repr_score.hpp:53-67).
+void oracle_engine_warm(oracle_engine* e, int li, const float* q, const float* k, const float* v, Index n) {
+    auto& layer = e->layers.at(static_cast<size_t>(li));
+    const int H = e->H, Hkv = e->Hkv, d = e->d, dv = e->dv, rep = e->rep;
+    const auto& cfg = e->cfg;
+    for (Index off = 0; off < n; off += cfg.chunk_size) {
+        const Index lx = std::min<Index>(cfg.chunk_size, n - off);
+        const Index s = layer.n_fed;
+        auto& acc = layer.acc;
+        acc.hi = s + lx;
+        acc.sums.resize(acc.sums.size() + static_cast<size_t>(lx), 0.0);
+        const Index n_pending = acc.hi - acc.lo;
+        // prefix over the chunk of qs[g][c]
+        std::vector<double> pre(static_cast<size_t>((lx + 1) * Hkv * d), 0.0);
+        for (Index i = 0; i < lx; ++i)
+            for (int g = 0; g < Hkv; ++g)
+                for (int c = 0; c < d; ++c) {
+                    double a = 0.0;
+                    for (int hh = 0; hh < rep; ++hh) a += q[((off + i) * H + g * rep + hh) * d + c];
+                    pre[static_cast<size_t>(((i + 1) * Hkv + g) * d + c)] = pre[static_cast<size_t>((i * Hkv + g) * d + c)] + a;
+                }
+        for (Index j = 0; j < n_pending; ++j) {
+            const Index m = acc.lo + j;
+            const Index first = std::max<Index>(0, m + 1 - s);
+            const Index last = std::min<Index>(lx - 1, m + cfg.local_size - s);
+            if (first > last) continue;
+            const float* km = m < s ? nullptr : k + (off + (m - s)) * Hkv * d;
+            double tot = 0.0;
+            for (int g = 0; g < Hkv; ++g) {
+                const float* kr = km ? km + g * d : layer.local_keys[static_cast<size_t>(g)].row(m - layer.local_start);
+                for (int c = 0; c < d; ++c)
+                    tot += static_cast<double>(kr[c]) * (pre[static_cast<size_t>(((last + 1) * Hkv + g) * d + c)] -
+                                                         pre[static_cast<size_t>((first * Hkv + g) * d + c)]);
+            }
+            acc.sums[static_cast<size_t>(j)] += tot;
+        }
+        acc.next_query_abs = acc.hi;
+        std::vector<Mat<Scalar>> bk, bv;
+        for (int g = 0; g < Hkv; ++g) {
+            Mat<Scalar> mk(lx, d), mv(lx, dv);
+            for (Index i = 0; i < lx; ++i) {
+                std::memcpy(mk.row(i), k + ((off + i) * Hkv + g) * d, sizeof(float) * static_cast<size_t>(d));
+                std::memcpy(mv.row(i), v + ((off + i) * Hkv + g) * dv, sizeof(float) * static_cast<size_t>(dv));
+            }
+            layer.local_keys[static_cast<size_t>(g)].append_rows(mk.a.data(), lx);
+            layer.local_values[static_cast<size_t>(g)].append_rows(mv.a.data(), lx);
+        }
+        const Index overflow = std::max<Index>(0, layer.local_len() - cfg.local_size);
+        if (overflow > 0) {
+            const auto scores = acc.finalize_front(overflow);
+            const Index pop_start = layer.local_start;
+            const Index to_init = std::clamp<Index>(cfg.init_size - pop_start, 0, overflow);
+            for (int g = 0; g < Hkv; ++g)
+                if (to_init > 0) {
+                    layer.init_keys[static_cast<size_t>(g)].append_rows(layer.local_keys[static_cast<size_t>(g)].row(0), to_init);
+                    layer.init_values[static_cast<size_t>(g)].append_rows(layer.local_values[static_cast<size_t>(g)].row(0), to_init);
+                }
+            const Index to_evict = overflow - to_init;
+            if (to_evict > 0) {
+                std::vector<Mat<Scalar>> ek, ev;
+                for (int g = 0; g < Hkv; ++g) {
+                    ek.push_back(layer.local_keys[static_cast<size_t>(g)].slice_rows(to_init, to_evict));
+                    ev.push_back(layer.local_values[static_cast<size_t>(g)].slice_rows(to_init, to_evict));
+                }
+                auto units = layer.packer.add(pop_start + to_init, ek, ev, scores.data() + to_init, to_evict);
+                for (auto& u : units) layer.store.add_unit(std::move(u));
+            }
+            for (int g = 0; g < Hkv; ++g) {
+                layer.local_keys[static_cast<size_t>(g)].drop_front(overflow);
+                layer.local_values[static_cast<size_t>(g)].drop_front(overflow);
+            }
+            layer.local_start += overflow;
+        }
+        layer.n_fed += lx;
+        layer.step += 1;
+    }
+}
+
 extern "C" {
 
 const char* oracle_last_error(void) { return g_err.c_str(); }
@@ -882,6 +963,10 @@ oracle_engine* oracle_engine_create(const infllm_engine_config* cfg, const infll
 }
 
 void oracle_engine_destroy(oracle_engine* e) { delete e; }
+
+int32_t oracle_warm_start(oracle_engine* e, int32_t layer, const float* q, const float* k, const float* v, int64_t n) {
+    return guard([&] { oracle_engine_warm(e, layer, q, k, v, n); });
+}
 void oracle_set_always_emit_weights(oracle_engine* e, int32_t v) { e->always_emit = v != 0; }
 
 int32_t oracle_step(oracle_engine* e, int32_t layer, const float* q, const float* k, const float* v,

@@ -48,6 +48,10 @@ int32_t oracle_step(oracle_engine* e, int32_t layer, const float* q, const float
                     const float* v, int64_t l_x, int32_t is_decode, float* out,
                     int64_t* ids_out, int64_t ids_cap, int64_t* n_ids, double* masses_out);
 int32_t oracle_finish(oracle_engine* e);
+/* CPU-baseline harness: stream n tokens through the window/packing/score
+ * bookkeeping only (no lookup, no attention) to reach a steady state. */
+int32_t oracle_warm_start(oracle_engine* e, int32_t layer, const float* q, const float* k, const float* v,
+                          int64_t n);
 
 int32_t oracle_layer_metrics(oracle_engine* e, int32_t layer, infllm_layer_metrics* m);
 int32_t oracle_stream_state(oracle_engine* e, int32_t layer, int64_t* tokens_fed,

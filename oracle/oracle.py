@@ -117,6 +117,7 @@ def lib():
         L.oracle_step.argtypes = [P, C.c_int32, f32p, f32p, f32p, C.c_int64, C.c_int32, f32p, i64p,
                                   C.c_int64, i64p, f64p]
         L.oracle_finish.argtypes = [P]
+        L.oracle_warm_start.argtypes = [P, C.c_int32, f32p, f32p, f32p, C.c_int64]
         L.oracle_layer_metrics.argtypes = [P, C.c_int32, C.POINTER(LayerMetrics)]
         L.oracle_stream_state.argtypes = [P, C.c_int32] + [i64p] * 5
         L.oracle_unit_info.argtypes = [P, C.c_int32, C.c_int64, i64p, i64p, i64p, i64p]
@@ -231,6 +232,11 @@ class OracleEngine:
 
     def finish(self):
         _check(lib().oracle_finish(self.h))
+
+    def warm_start(self, q, k, v, layer=0):
+        q, k, v = f32(q), f32(k), f32(v)
+        _check(lib().oracle_warm_start(self.h, layer, _p(q, C.c_float), _p(k, C.c_float), _p(v, C.c_float),
+                                       q.shape[0]))
 
     def metrics(self, layer=0):
         m = LayerMetrics()

@@ -101,6 +101,7 @@ SIGNATURES = {
     "infllm_engine_destroy": (C.c_int, [P]),
     "infllm_engine_set_allgather": (C.c_int, [P, ALLGATHER_FN, P]),
     "infllm_engine_reserve": (C.c_int, [P, i64]),
+    "infllm_engine_reset": (C.c_int, [P, P]),
     "infllm_engine_set_option": (C.c_int, [P, C.c_char_p, i64]),
     "infllm_encode_chunk": (C.c_int, [P, i32, P, P, P, i64, P, P]),
     "infllm_decode_step": (C.c_int, [P, i32, P, P, P, P, P]),

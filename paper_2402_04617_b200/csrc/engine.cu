@@ -657,6 +657,29 @@ int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
     });
 }
 
+int infllm_engine_reset(infllm_engine_t e, void* stream) {
+    return guard([&] {
+        auto st = static_cast<cudaStream_t>(stream);
+        for (auto& L : e->layers) {
+            L.n_fed = L.step = L.local_start = L.init_len = 0;
+            L.n_units = L.pend_start = L.pend_count = 0;
+            L.trace_count = L.last_n_sel = 0;
+            L.unit_start.clear();
+            L.unit_len.clear();
+            ck(cudaMemsetAsync(L.P.p, 0, L.P.bytes, st), "memset");
+            ck(cudaMemsetAsync(L.lru.p, 0, L.lru.bytes, st), "memset");
+            if (L.hot.p) ck(cudaMemsetAsync(L.hot.p, 0, L.hot.bytes, st), "memset");
+            if (L.freq.p) ck(cudaMemsetAsync(L.freq.p, 0, L.freq.bytes, st), "memset");
+            if (L.ulen.p) {
+                k_fill_i32<<<static_cast<unsigned>((L.unit_cap + 255) / 256), 256, 0, st>>>(
+                    L.ulen.as<int32_t>(), L.unit_cap, static_cast<int32_t>(e->cfg.unit_size));
+                ++e->launches;
+            }
+        }
+        ck(cudaGetLastError(), "reset");
+    });
+}
+
 int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) {
     return guard([&] {
         const std::string k = key ? key : "";

@@ -62,6 +62,10 @@ class StreamEngine:
     def reserve(self, max_tokens: int):
         check(lib().infllm_engine_reserve(self.h, int(max_tokens)))
 
+    def reset(self, stream=None):
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        check(lib().infllm_engine_reset(self.h, st))
+
     def set_option(self, key: str, value: int):
         check(lib().infllm_engine_set_option(self.h, key.encode(), int(value)))
 
