@@ -215,6 +215,12 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
                   int64_t r_k, int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel,
                   int64_t* ids, void* stream);
 
+/* Diagnostic: tcgen05 building-block self-test on one 128x128x128 bf16 tile
+ * (q, k, vt row-major [128][128] device bf16): s_out = q k^T, o_out =
+ * bf16(s_out) vt^T, both fp32 [128][128]. */
+int infllm_debug_tc_selftest(const void* q, const void* k, const void* vt, float* s_out, float* o_out,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

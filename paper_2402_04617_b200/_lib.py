@@ -117,6 +117,7 @@ SIGNATURES = {
     "infllm_profile_read": (C.c_int, [P, f64p, i64p, f64p, i64p]),
     "infllm_select_representatives": (C.c_int, [P, P, i64, i64, i64, P, P]),
     "infllm_lookup": (C.c_int, [P, P, i32, i64, i64, i32, i32, i64, P, P, P]),
+    "infllm_debug_tc_selftest": (C.c_int, [P, P, P, P, P, P]),
 }
 
 

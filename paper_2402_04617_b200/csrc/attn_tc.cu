@@ -1,10 +1,513 @@
-// attn_tc.cu — placeholder until the tcgen05 kernel lands.
+// attn_tc.cu — tcgen05 / TMEM / TMA attention for the InfLLM window
+// (bf16, head_dim = value_dim = 128, 128-token memory units).
+#include <cuda.h>
+
 #include "attn_tc.cuh"
+#include "tc_prims.cuh"
+#include "tmap.cuh"
 
 namespace infllm {
-bool attn_tc_supported(int, int, int, bool) { return false; }
-int launch_attn_tc(const AttnParams& p, cudaStream_t st) {
-    launch_attn_simt<bf16>(p, st);
+
+using namespace tc;
+
+// ---------------------------------------------------------------------------
+// Self-test of the building blocks on one 128x128x128 tile:
+//   S = Q K^T      (SS MMA, both operands TMA-loaded K-major SW128)
+//   P = bf16(S)    (stored back into TMEM, packed pairs)
+//   O = P V        (TS MMA: A = P from TMEM, B = V^T tile K-major)
+__global__ void __launch_bounds__(192, 1)
+    k_tc_selftest(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                  const __grid_constant__ CUtensorMap tv, float* s_out, float* o_out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = smem + 32768;
+    uint8_t* sV = smem + 65536;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 98304);
+    uint64_t* tma_bar = bars;
+    uint64_t* mma_bar = bars + 1;
+    uint64_t* p_bar = bars + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        mbar_init(tma_bar, 1);
+        mbar_init(mma_bar, 1);
+        mbar_init(p_bar, 128);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+    if (warp == 0 && lane == 0) {
+        mbar_expect_tx(tma_bar, 6 * 16384);
+        tma_load_2d(&tq, tma_bar, sQ, 0, 0);
+        tma_load_2d(&tq, tma_bar, sQ + 16384, 64, 0);
+        tma_load_2d(&tk, tma_bar, sK, 0, 0);
+        tma_load_2d(&tk, tma_bar, sK + 16384, 64, 0);
+        tma_load_2d(&tv, tma_bar, sV, 0, 0);
+        tma_load_2d(&tv, tma_bar, sV + 16384, 64, 0);
+    }
+    const uint32_t idesc = idesc_bf16(128, 128);
+    if (warp == 1 && lane == 0) {
+        mbar_wait(tma_bar, 0);
+        tc_fence_after();
+        for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ss(tbase, sdesc_sw128(smem_u32(sQ) + off), sdesc_sw128(smem_u32(sK) + off), idesc, kk > 0);
+        }
+        mma_commit(mma_bar);
+    }
+    if (warp >= 2) {
+        const int q = warp & 3;
+        const int row = 32 * q + lane;
+        mbar_wait(mma_bar, 0);
+        tc_fence_after();
+        uint32_t pk[64];
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tbase + ((32u * q) << 16) + 32 * c, r);
+            tmem_wait_ld();
+            for (int j = 0; j < 32; ++j) s_out[row * 128 + 32 * c + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) pk[16 * c + j] = pack_bf16(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+        }
+        uint32_t a[32], b[32];
+        for (int j = 0; j < 32; ++j) {
+            a[j] = pk[j];
+            b[j] = pk[32 + j];
+        }
+        tmem_st32(tbase + ((32u * q) << 16) + 128, a);
+        tmem_st32(tbase + ((32u * q) << 16) + 160, b);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_bar);
+    }
+    if (warp == 1 && lane == 0) {
+        mbar_wait(p_bar, 0);
+        tc_fence_after();
+        for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            mma_ts(tbase + 256, tbase + 128 + 8 * kk, sdesc_sw128(smem_u32(sV) + off), idesc, kk > 0);
+        }
+        mma_commit(mma_bar);
+    }
+    if (warp >= 2) {
+        const int q = warp & 3;
+        const int row = 32 * q + lane;
+        mbar_wait(mma_bar, 1);
+        tc_fence_after();
+        for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            tmem_ld32(tbase + ((32u * q) << 16) + 256 + 32 * c, r);
+            tmem_wait_ld();
+            for (int j = 0; j < 32; ++j) o_out[row * 128 + 32 * c + j] = __uint_as_float(r[j]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+void tc_selftest(const void* q, const void* k, const void* vt, float* s_out, float* o_out, cudaStream_t st) {
+    const CUtensorMap tq = make_tmap_bf16_sw128(q, 128, 128, 128);
+    const CUtensorMap tk = make_tmap_bf16_sw128(k, 128, 128, 128);
+    const CUtensorMap tv = make_tmap_bf16_sw128(vt, 128, 128, 128);
+    const int smem = 98304 + 64 + 1024;
+    cudaFuncSetAttribute(k_tc_selftest, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_tc_selftest<<<1, 192, smem, st>>>(tq, tk, tv, s_out, o_out);
+}
+
+// ---------------------------------------------------------------------------
+// InfLLM window attention on tcgen05 (attention.hpp:116-230 semantics).
+//
+// CTA = (128 query tokens) x (one query head h of KV group g). KV tiles of
+// 128 keys in window order: initial tokens, the k_m retrieved units (unit id
+// from the device-side lookup result), then the local window + causal chunk
+// (ring pages). Per tile: S = Q K^T into TMEM (SS MMA, K-major SW128 operands
+// staged by TMA), the softmax warps read S rows from TMEM (one thread per
+// query row), apply the clamped-position / causal masks, online softmax in
+// the exp2 domain with lazy (thresholded) rescaling of the TMEM O
+// accumulator, write P (bf16) back into TMEM over S, and O += P V^T runs as a
+// TS MMA (A = P from TMEM, B = V^T page from smem).
+// Position modes per tile (SURVEY Appendix A rules 1-3):
+//   CLAMP: far tiles (initial / retrieved) and local keys beyond l_L:
+//          S = rope(q, l_L) . k_raw
+//   ABS  : near keys: S = rope(q, pos_q) . rope(k, pos_k)
+//   MIXED: tiles straddling the l_L staircase: both products, selected per
+//          element by pos_q - pos_k > l_L (attention.hpp:96-108,179-187).
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer (+TMEM owner),
+// warps 2-5 softmax/epilogue (TMEM lane quarter = warp % 4).
+
+constexpr int kNS = 4;                 // smem stages (32 KB each: one K or V^T tile)
+constexpr int kTcThreads = 192;
+constexpr uint32_t kStageBytes = 32768;
+constexpr uint32_t kSmemBytes = 65536 + kNS * kStageBytes + 256 + 1024;
+constexpr uint32_t kColS0 = 0, kColS1 = 128, kColSX = 256, kColO = 384;
+
+enum { SRC_INIT = 0, SRC_UNIT = 1, SRC_RING = 2 };
+enum { MODE_CLAMP = 0, MODE_ABS = 1, MODE_MIXED = 2 };
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+struct TcParams {
+    CUtensorMap tm_qa, tm_qc, tm_rk, tm_rkr, tm_rv, tm_ik, tm_iv, tm_uk, tm_uv;
+    AttnParams a;
+};
+
+struct Tile {
+    int src, mode, lo, hi, slot;
+    int64_t key0, id;
+};
+
+struct TileSched {
+    int n_init, n_units, n_near, T;
+    int64_t near0, near_end, qp_lo, qp_hi;
+    __device__ void init(const AttnParams& a, int m) {
+        n_init = static_cast<int>((a.init_len + 127) / 128);
+        n_units = a.n_sel;
+        const int64_t rows = imin64(a.lx, 128 * m + 128);
+        near0 = (a.local_start / 128) * 128;
+        near_end = a.s + rows;
+        n_near = static_cast<int>((near_end - near0 + 127) / 128);
+        T = n_init + n_units + n_near;
+        qp_lo = a.s + 128 * m;
+        qp_hi = a.s + rows - 1;
+    }
+    __device__ Tile get(const AttnParams& a, int j) const {
+        Tile t;
+        t.slot = -1;
+        if (j < n_init) {
+            t.src = SRC_INIT;
+            t.mode = MODE_CLAMP;
+            t.key0 = 128 * j;
+            t.id = j;
+            t.lo = 0;
+            t.hi = static_cast<int>(imin64(128, a.init_len - 128 * j));
+        } else if (j < n_init + n_units) {
+            const int u = j - n_init;
+            t.src = SRC_UNIT;
+            t.mode = MODE_CLAMP;
+            t.id = a.sel[u];
+            t.key0 = 0;
+            t.lo = 0;
+            t.hi = a.unit_len[t.id];
+            t.slot = u;
+        } else {
+            const int64_t P = near0 + 128 * static_cast<int64_t>(j - n_init - n_units);
+            t.src = SRC_RING;
+            t.key0 = P;
+            t.id = 0;
+            t.lo = static_cast<int>(imax64(0, a.local_start - P));
+            t.hi = static_cast<int>(imin64(128, near_end - P));
+            const int64_t max_dist = qp_hi - (P + t.lo);
+            const int64_t min_dist = qp_lo - (P + t.hi - 1);
+            t.mode = max_dist <= a.L ? MODE_ABS : (min_dist > a.L ? MODE_CLAMP : MODE_MIXED);
+        }
+        return t;
+    }
+};
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant__ TcParams P) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQa = smem;
+    uint8_t* sQc = smem + 32768;
+    uint8_t* sStage = smem + 65536;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 65536 + kNS * kStageBytes);
+    uint64_t* q_full = bars;
+    uint64_t* st_full = bars + 1;
+    uint64_t* st_empty = bars + 1 + kNS;
+    uint64_t* s_full = bars + 1 + 2 * kNS;
+    uint64_t* p_full = bars + 3 + 2 * kNS;
+    uint64_t* o_done = bars + 5 + 2 * kNS;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * kNS);
+
+    const AttnParams& a = P.a;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int m = blockIdx.x, h = blockIdx.y, g = h / a.rep;
+    TileSched ts;
+    ts.init(a, m);
+
+    if (warp == 0 && lane == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < kNS; ++i) {
+            mbar_init(st_full + i, 1);
+            mbar_init(st_empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(p_full + i, 128);
+        }
+        mbar_init(o_done, 1);
+        fence_barrier_init();
+        prefetch_tmap(&P.tm_qa);
+        prefetch_tmap(&P.tm_qc);
+        prefetch_tmap(&P.tm_rk);
+        prefetch_tmap(&P.tm_rkr);
+        prefetch_tmap(&P.tm_rv);
+        prefetch_tmap(&P.tm_uk);
+        prefetch_tmap(&P.tm_uv);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+    const uint32_t idesc = idesc_bf16(128, 128);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            const int qrow = static_cast<int>(h * a.lxp + 128 * m);
+            mbar_expect_tx(q_full, 65536);
+            tma_load_2d(&P.tm_qa, q_full, sQa, 0, qrow);
+            tma_load_2d(&P.tm_qa, q_full, sQa + 16384, 64, qrow);
+            tma_load_2d(&P.tm_qc, q_full, sQc, 0, qrow);
+            tma_load_2d(&P.tm_qc, q_full, sQc + 16384, 64, qrow);
+            int it = 0;
+            auto load = [&](const CUtensorMap* map, int row) {
+                const int s = it % kNS;
+                if (it >= kNS) mbar_wait(st_empty + s, ((it / kNS) - 1) & 1);
+                uint8_t* dst = sStage + s * kStageBytes;
+                mbar_expect_tx(st_full + s, kStageBytes);
+                tma_load_2d(map, st_full + s, dst, 0, row);
+                tma_load_2d(map, st_full + s, dst + 16384, 64, row);
+                ++it;
+            };
+            const int R128 = static_cast<int>(a.R / 128);
+            for (int j = 0; j < ts.T; ++j) {
+                const Tile t = ts.get(a, j);
+                if (t.src == SRC_INIT) {
+                    load(&P.tm_ik, static_cast<int>(g * a.l_I + t.key0));
+                    load(&P.tm_iv, static_cast<int>((g * a.vl.nI + t.id) * a.dv));
+                } else if (t.src == SRC_UNIT) {
+                    load(&P.tm_uk, static_cast<int>((t.id * a.G + g) * 128));
+                    load(&P.tm_uv, static_cast<int>((t.id * a.G + g) * a.dv));
+                } else {
+                    const int slot = static_cast<int>(t.key0 % a.R);
+                    load(t.mode == MODE_CLAMP ? &P.tm_rk : &P.tm_rkr, g * static_cast<int>(a.R) + slot);
+                    if (t.mode == MODE_MIXED) load(&P.tm_rk, g * static_cast<int>(a.R) + slot);
+                    load(&P.tm_rv, (g * R128 + slot / 128) * a.dv);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer
+            mbar_wait(q_full, 0);
+            tc_fence_after();
+            const uint32_t aQa = smem_u32(sQa), aQc = smem_u32(sQc), aSt = smem_u32(sStage);
+            int it = 0, v_prev = -1;
+            auto pv = [&](int jj, int vi) {
+                const int b = jj & 1;
+                mbar_wait(p_full + b, (jj >> 1) & 1);
+                const int s = vi % kNS;
+                mbar_wait(st_full + s, (vi / kNS) & 1);
+                tc_fence_after();
+                const uint32_t vb = aSt + s * kStageBytes;
+                const uint32_t pcol = tbase + (b ? kColS1 : kColS0);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_ts(tbase + kColO, pcol + 8 * kk, sdesc_sw128(vb + (kk >> 2) * 16384 + (kk & 3) * 32), idesc,
+                           (jj > 0 || kk > 0) ? 1u : 0u);
+                mma_commit(st_empty + s);
+                mma_commit(o_done);
+            };
+            for (int j = 0; j < ts.T; ++j) {
+                const Tile t = ts.get(a, j);
+                const int b = j & 1;
+                {
+                    const int s = it % kNS;
+                    mbar_wait(st_full + s, (it / kNS) & 1);
+                    tc_fence_after();
+                    const uint32_t qb = t.mode == MODE_CLAMP ? aQc : aQa;
+                    const uint32_t kb = aSt + s * kStageBytes;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                        mma_ss(tbase + (b ? kColS1 : kColS0), sdesc_sw128(qb + off), sdesc_sw128(kb + off), idesc,
+                               kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit(st_empty + s);
+                    ++it;
+                }
+                if (t.mode == MODE_MIXED) {
+                    if (j > 0) mbar_wait(p_full + ((j - 1) & 1), ((j - 1) >> 1) & 1);  // SX consumed
+                    const int s = it % kNS;
+                    mbar_wait(st_full + s, (it / kNS) & 1);
+                    tc_fence_after();
+                    const uint32_t kb = aSt + s * kStageBytes;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+                        mma_ss(tbase + kColSX, sdesc_sw128(aQc + off), sdesc_sw128(kb + off), idesc, kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit(st_empty + s);
+                    ++it;
+                }
+                mma_commit(s_full + b);
+                const int v_item = it++;
+                if (j > 0) pv(j - 1, v_prev);
+                v_prev = v_item;
+            }
+            if (ts.T > 0) pv(ts.T - 1, v_prev);
+        }
+    } else {
+        // ---------------- softmax / epilogue warps (one query row per thread)
+        const int q4 = warp & 3;
+        const int row = 32 * q4 + lane;
+        const int64_t i = 128 * static_cast<int64_t>(m) + row;
+        const bool row_ok = i < a.lx;
+        const int64_t qp = row_ok ? a.s + i : ts.qp_hi;
+        const uint32_t tl = tbase + ((32u * q4) << 16);
+        const float sl2 = a.scale * 1.4426950408889634f;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int j = 0; j < ts.T; ++j) {
+            const Tile t = ts.get(a, j);
+            const int b = j & 1;
+            const uint32_t tS = tl + (b ? kColS1 : kColS0);
+            mbar_wait(s_full + b, (j >> 1) & 1);
+            tc_fence_after();
+            float x[128];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                uint32_t r[32];
+                tmem_ld32(tS + 32 * c4, r);
+                tmem_wait_ld();
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) x[32 * c4 + jj] = __uint_as_float(r[jj]);
+            }
+            // valid key columns [lo, kmax); staircase columns [lo, cmax) use the clamped product
+            int kmax = t.hi;
+            if (t.src == SRC_RING) kmax = static_cast<int>(imax64(t.lo, imin64(t.hi, qp - t.key0 + 1)));
+            if (t.mode == MODE_MIXED) {
+                const int cmax = static_cast<int>(imax64(0, imin64(128, qp - a.L - t.key0)));
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    uint32_t r[32];
+                    tmem_ld32(tl + kColSX + 32 * c4, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj)
+                        if (32 * c4 + jj < cmax) x[32 * c4 + jj] = __uint_as_float(r[jj]);
+                }
+            }
+            float mt = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                x[c] = (c >= t.lo && c < kmax) ? x[c] * sl2 : -INFINITY;
+                mt = fmaxf(mt, x[c]);
+            }
+            const float m_new = fmaxf(m_run, mt);
+            const bool need = m_new > m_run + 8.0f;
+            if (__any_sync(0xffffffffu, need)) {
+                const float corr = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
+                l_run *= corr;
+                if (j > 0) {
+                    mbar_wait(o_done, (j - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4) {
+                        uint32_t r[32];
+                        tmem_ld32(tl + kColO + 32 * c4, r);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) * corr);
+                        tmem_st32(tl + kColO + 32 * c4, r);
+                    }
+                    tmem_wait_st();
+                }
+                m_run = m_new;
+            }
+            float rs = 0.f;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+                x[c] = (x[c] == -INFINITY) ? 0.f : ex2(x[c] - m_run);
+                rs += x[c];
+            }
+            l_run += rs;
+            if (t.slot >= 0 && a.want_mass && row_ok) {
+                const int64_t o = (static_cast<int64_t>(h) * a.lx + i) * a.n_sel + t.slot;
+                a.mass_e[o] = rs;
+                a.mass_m[o] = m_run * 0.6931471805599453f;
+            }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) pk[jj] = pack_bf16(x[64 * half + 2 * jj], x[64 * half + 2 * jj + 1]);
+                tmem_st32(tS + 32 * half, pk);
+            }
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(p_full + b);
+        }
+        // epilogue: O / l -> bf16 token-major output
+        if (ts.T > 0) {
+            mbar_wait(o_done, (ts.T - 1) & 1);
+            tc_fence_after();
+        }
+        const float inv = 1.f / l_run;
+        bf16* out = static_cast<bf16*>(a.out) + (i * a.H + h) * a.dv;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+            uint32_t r[32];
+            tmem_ld32(tl + kColO + 32 * c4, r);
+            tmem_wait_ld();
+            if (row_ok) {
+                uint32_t w[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                    w[jj] = pack_bf16(__uint_as_float(r[2 * jj]) * inv, __uint_as_float(r[2 * jj + 1]) * inv);
+                uint4* dst = reinterpret_cast<uint4*>(out + 32 * c4);
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) dst[v4] = make_uint4(w[4 * v4], w[4 * v4 + 1], w[4 * v4 + 2], w[4 * v4 + 3]);
+            }
+        }
+        if (row_ok && a.want_mass) {
+            a.row_m[static_cast<int64_t>(h) * a.lx + i] = m_run * 0.6931471805599453f;
+            a.row_l[static_cast<int64_t>(h) * a.lx + i] = l_run;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+bool attn_tc_supported(int d, int dv, int unit_size, bool absolute) {
+    return d == 128 && dv == 128 && unit_size == 128 && !absolute;
+}
+
+int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
+    TcParams P;
+    P.a = a;
+    const uint64_t R = static_cast<uint64_t>(a.R);
+    P.tm_qa = make_tmap_bf16_sw128(a.qa, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
+    P.tm_qc = make_tmap_bf16_sw128(a.qc, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
+    P.tm_rk = make_tmap_bf16_sw128(a.ring_k, a.G * R, 128, 128);
+    P.tm_rkr = make_tmap_bf16_sw128(a.ring_krot, a.G * R, 128, 128);
+    P.tm_rv = make_tmap_bf16_sw128(a.ring_v, a.G * (R / 128) * 128, 128, 128);
+    P.tm_ik = make_tmap_bf16_sw128(a.init_k, static_cast<uint64_t>(a.G) * a.l_I, 128, 128);
+    P.tm_iv = make_tmap_bf16_sw128(a.init_v, static_cast<uint64_t>(a.G) * a.vl.nI * 128, 128, 128);
+    const uint64_t ucap = static_cast<uint64_t>(a.unit_cap > 0 ? a.unit_cap : 1);
+    P.tm_uk = make_tmap_bf16_sw128(a.unit_k ? a.unit_k : a.ring_k, a.unit_k ? ucap * a.G * 128 : 128, 128, 128);
+    P.tm_uv = make_tmap_bf16_sw128(a.unit_v ? a.unit_v : a.ring_v, a.unit_v ? ucap * a.G * 128 : 128, 128, 128);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        attr = true;
+    }
+    dim3 grid(static_cast<unsigned>((a.lx + 127) / 128), a.H);
+    k_attn_tc<<<grid, kTcThreads, kSmemBytes, st>>>(P);
     return 1;
 }
+
 }  // namespace infllm

@@ -9,5 +9,7 @@ namespace infllm {
 bool attn_tc_supported(int d, int dv, int unit_size, bool absolute);
 // launches the tensor-core attention for one step; returns #kernels launched
 int launch_attn_tc(const AttnParams& p, cudaStream_t st);
+// building-block self-test (one 128x128x128 tile), see attn_tc.cu
+void tc_selftest(const void* q, const void* k, const void* vt, float* s_out, float* o_out, cudaStream_t st);
 
 }  // namespace infllm

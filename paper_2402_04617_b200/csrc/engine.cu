@@ -138,6 +138,7 @@ struct infllm_engine {
     int64_t launches = 0;
     bool use_tc = false;
     bool tc_disabled = false;
+    VLayout vl{};
 
     // scratch shared by layers (layers run sequentially on one stream)
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l;
@@ -259,6 +260,7 @@ struct infllm_engine {
         pp.d = d;
         pp.dv = dv;
         pp.freqs = freqs;
+        pp.vl = vl;
         launch_prep<T>(pp, st);
         launches += 2;
 
@@ -341,6 +343,8 @@ struct infllm_engine {
         ap.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
         ap.want_mass = want_mass;
         ap.scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.hpp:140
+        ap.vl = vl;
+        ap.unit_cap = L.unit_cap;
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
             eva = {take_event(), take_event()};
@@ -430,6 +434,7 @@ struct infllm_engine {
             ep.dv = dv;
             ep.l_bs = static_cast<int>(cfg.unit_size);
             ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+            ep.vl = vl;
             launch_evict<T>(ep, st);
             ++launches;
             if (to_evict > 0) {
@@ -576,6 +581,15 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->R = (need + 127) / 128 * 128;
         e->lxp = (cfg->chunk_size + 127) / 128 * 128;
         for (int a = 0; a < e->d / 2; ++a) e->freqs.f[a] = std::pow(10000.0, -2.0 * a / e->d);  // rotary.hpp:25
+        e->use_tc = dtype == INFLLM_DTYPE_BF16 && attn_tc_supported(e->d, e->dv, static_cast<int>(cfg->unit_size),
+                                                                     cfg->position_mode == INFLLM_POSITION_ABSOLUTE);
+        e->vl.vt = e->use_tc ? 1 : 0;
+        e->vl.R = e->R;
+        e->vl.nI = static_cast<int>((std::max<int64_t>(cfg->init_size, 1) + 127) / 128);
+        e->vl.l_I = cfg->init_size;
+        e->vl.l_bs = static_cast<int>(cfg->unit_size);
+        e->vl.dv = e->dv;
+        e->vl.G = e->Gs;
         ck(cudaSetDevice(device), "cudaSetDevice");
         cudaStream_t st = nullptr;
         const size_t es = e->esz;
@@ -597,15 +611,13 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
             if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
                 L.init_krot.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
-            L.init_v.alloc(static_cast<size_t>(e->Gs) * ni * e->dv * es, st);
+            L.init_v.alloc(static_cast<size_t>(e->Gs) * (e->vl.vt ? e->vl.nI * 128 : ni) * e->dv * es, st);
             L.hot_list.alloc(static_cast<size_t>(cfg->hot_capacity + km + 1) * sizeof(int64_t), st);
             L.lru.alloc(sizeof(LruState), st);
             L.sel.alloc(km * sizeof(int64_t), st);
             L.mass_part.alloc(km * e->Gt * sizeof(double), st);
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
-        e->use_tc = dtype == INFLLM_DTYPE_BF16 && attn_tc_supported(e->d, e->dv, static_cast<int>(cfg->unit_size),
-                                                                     cfg->position_mode == INFLLM_POSITION_ABSOLUTE);
         ck(cudaStreamSynchronize(st), "engine_create");
         *out = e.release();
     });
@@ -889,6 +901,14 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         part.release(st);
         relw.release(st);
         ck(cudaGetLastError(), "lookup");
+    });
+}
+
+int infllm_debug_tc_selftest(const void* q, const void* k, const void* vt, float* s_out, float* o_out,
+                             void* stream) {
+    return guard([&] {
+        tc_selftest(q, k, vt, s_out, o_out, static_cast<cudaStream_t>(stream));
+        ck(cudaGetLastError(), "tc_selftest");
     });
 }
 

@@ -77,7 +77,7 @@ __global__ void k_prep(PrepParams p) {
     }
     for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
         const int g = t / p.dv, c = t % p.dv;
-        rv[(static_cast<int64_t>(g) * p.R + slot) * p.dv + c] = v[(i * p.G + g) * p.dv + c];
+        rv[p.vl.ring(g, pos, c)] = v[(i * p.G + g) * p.dv + c];
     }
 }
 
@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(kThreads) k_attn_simt(AttnParams p) {
             for (int t = tid; t < nk * dv; t += kThreads) {
                 const int rr = t / dv, c = t % dv;
                 const int64_t off = seg_start + t0 + rr;
-                sv[rr * dvp + c] = to_f(row_ptr<T>(p, kind, g, id, off, p.init_v, p.unit_v, p.ring_v, dv)[c]);
+                const int64_t vi = kind == 0 ? p.vl.init(g, off, c) : (kind == 1 ? p.vl.unit(id, g, off, c) : p.vl.ring(g, off, c));
+                const T* vb = static_cast<const T*>(kind == 0 ? p.init_v : (kind == 1 ? p.unit_v : p.ring_v));
+                sv[rr * dvp + c] = to_f(vb[vi]);
             }
             __syncthreads();
             // scores
@@ -601,7 +603,7 @@ __global__ void k_evict(EvictParams p) {
         }
         for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
             const int g = t / p.dv, c = t % p.dv;
-            iv[(static_cast<int64_t>(g) * p.l_I + pos) * p.dv + c] = rv[(static_cast<int64_t>(g) * p.R + slot) * p.dv + c];
+            iv[p.vl.init(g, pos, c)] = rv[p.vl.ring(g, pos, c)];
         }
         return;
     }
@@ -619,7 +621,7 @@ __global__ void k_evict(EvictParams p) {
     }
     for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
         const int g = t / p.dv, c = t % p.dv;
-        uv[((u * p.G + g) * p.l_bs + off) * p.dv + c] = rv[(static_cast<int64_t>(g) * p.R + slot) * p.dv + c];
+        uv[p.vl.unit(u, g, off, c)] = rv[p.vl.ring(g, pos, c)];
     }
     // score partials: warp w handles groups w, w + nwarps, ...
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;

@@ -20,6 +20,27 @@
 
 namespace infllm {
 
+// Value pages are stored either row-major ([token][dv]) or, when the tcgen05
+// attention is used (unit_size == 128), as transposed 128-token pages
+// ([dv][128 tokens]) so V^T tiles are K-major UMMA B operands.
+struct VLayout {
+    int vt;      // 1: transposed pages
+    int64_t R;   // ring capacity (multiple of 128)
+    int nI;      // init pages (ceil(l_I / 128))
+    int64_t l_I;
+    int l_bs, dv, G;
+    __device__ __forceinline__ int64_t ring(int g, int64_t pos, int c) const {
+        const int64_t sl = pos % R;
+        return vt ? ((g * (R / 128) + sl / 128) * dv + c) * 128 + sl % 128 : (g * R + sl) * dv + c;
+    }
+    __device__ __forceinline__ int64_t init(int g, int64_t pos, int c) const {
+        return vt ? ((static_cast<int64_t>(g) * nI + pos / 128) * dv + c) * 128 + pos % 128 : (g * l_I + pos) * dv + c;
+    }
+    __device__ __forceinline__ int64_t unit(int64_t u, int g, int64_t off, int c) const {
+        return vt ? ((u * G + g) * dv + c) * l_bs + off : ((u * G + g) * l_bs + off) * dv + c;
+    }
+};
+
 struct PrepParams {
     const void* q;  // [lx][H][d]
     const void* k;  // [lx][G][d]
@@ -33,6 +54,7 @@ struct PrepParams {
     double* chunk_qsum;  // [G][d]
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
+    VLayout vl;
     RopeFreqs freqs;
 };
 
@@ -76,10 +98,11 @@ struct AttnParams {
     float* mass_m;
     float* row_m;   // [H][lx]
     float* row_l;
-    int64_t R, s, lx, lxp, init_len, local_start, L, l_I;
+    int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;
     float scale;
+    VLayout vl;
 };
 
 struct MassParams {
@@ -121,6 +144,7 @@ struct EvictParams {
     int64_t pop0, n_init, n_evict, R, L, l_I;
     int64_t pend_start, unit0;  // token pend_start belongs to unit id unit0 at offset 0
     int G, Gtot, g0, d, dv, l_bs, absolute;
+    VLayout vl;
 };
 
 struct FinalizeParams {

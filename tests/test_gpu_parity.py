@@ -127,3 +127,30 @@ def test_select_and_lookup_standalone():
     assert np.allclose(rel.cpu().numpy(), want, rtol=1e-12, atol=1e-9)
     top = sorted(O.argsort_topk(want, 10))
     assert ids.cpu().tolist() == top
+
+
+def test_tc_vs_simt_c2_shape():
+    """tcgen05 attention vs the CUDA-core kernel on the C2 head shape (32q/8kv,
+    d128), several steady-state steps with staircase tiles and retrieved units."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=1024, init_size=128, n_lookup=8, hot_capacity=16)
+    n = 4096
+    q, k, v = gaussian_inputs(21, n, 32, 8, 128, scale=0.3, bf16=True)
+    outs = []
+    for tc in (1, 0):
+        eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128),
+                           dtype=torch.bfloat16)
+        eng.set_option("tc_attention", tc)
+        qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+        outs.append((eng.feed(qt, kt, vt).float().cpu().numpy(), eng.metrics(), eng.kernel_launches()))
+    assert rel_err(outs[0][0], outs[1][0]) < 2e-2
+    assert outs[0][1] == outs[1][1]
+    # and against the oracle on the last chunks
+    ocfg = O.EngineConfig.make(**cfg)
+    oeng = O.OracleEngine(ocfg, O.ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128), n_threads=8)
+    got = []
+    for off in range(0, n, 512):
+        got.append(oeng.step(q[off:off + 512], k[off:off + 512], v[off:off + 512]).out)
+    want = np.concatenate(got, 0)
+    assert rel_err(outs[0][0], want) < 2e-2
