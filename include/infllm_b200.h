@@ -141,7 +141,8 @@ int infllm_engine_reserve(infllm_engine_t eng, int64_t max_tokens);
  * device pools; asynchronous on `stream`. */
 int infllm_engine_reset(infllm_engine_t eng, void* stream);
 /* Engine options: "tc_attention" (1 = tcgen05 attention when the shape
- * allows, 0 = CUDA-core attention). */
+ * allows, 0 = CUDA-core attention), "cuda_graphs" (1 = graph-replayed
+ * encode_stream, default). */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if
@@ -152,6 +153,20 @@ int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value
  * reference engine is one call per layer in order 0..n_layers-1. */
 int infllm_encode_chunk(infllm_engine_t eng, int32_t layer, const void* q, const void* k,
                         const void* v, int64_t l_x, void* out, void* stream);
+
+/* StreamEngine::feed (engine.hpp:106-112) for one layer: n_tokens of
+ * device q/k/v [n_tokens][heads][dim] as consecutive encode_chunk steps of
+ * chunk_size tokens, outputs into out [n_tokens][n_heads][value_dim]. The
+ * whole chunk schedule is captured once into a CUDA graph (keyed by
+ * pointers, length and the starting stream state) and replayed; option
+ * "cuda_graphs" = 0 launches the steps directly. */
+int infllm_encode_stream(infllm_engine_t eng, int32_t layer, const void* q, const void* k, const void* v,
+                         int64_t n_tokens, void* out, void* stream);
+/* Same with HOST (preferably pinned) q/k/v/out: per-chunk H2D into device
+ * staging buffers and D2H of each output chunk, on copy streams overlapped
+ * with the neighbouring chunks' compute. */
+int infllm_encode_stream_host(infllm_engine_t eng, int32_t layer, const void* host_q, const void* host_k,
+                              const void* host_v, int64_t n_tokens, void* host_out, void* stream);
 
 /* StreamEngine::decode_step (engine.hpp:100-103): l_x = 1, lookup unless
  * lookup_mode == none. */

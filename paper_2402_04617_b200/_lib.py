@@ -105,6 +105,8 @@ SIGNATURES = {
     "infllm_engine_set_option": (C.c_int, [P, C.c_char_p, i64]),
     "infllm_encode_chunk": (C.c_int, [P, i32, P, P, P, i64, P, P]),
     "infllm_decode_step": (C.c_int, [P, i32, P, P, P, P, P]),
+    "infllm_encode_stream": (C.c_int, [P, i32, P, P, P, i64, P, P]),
+    "infllm_encode_stream_host": (C.c_int, [P, i32, P, P, P, i64, P, P]),
     "infllm_finish": (C.c_int, [P, P]),
     "infllm_retrieved_ids": (C.c_int, [P, i32, i64p, i64, i64p]),
     "infllm_get_layer_metrics": (C.c_int, [P, i32, C.POINTER(LayerMetrics)]),

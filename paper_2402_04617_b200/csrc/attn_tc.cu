@@ -2,6 +2,8 @@
 // (bf16, head_dim = value_dim = 128, 128-token memory units).
 #include <cuda.h>
 
+#include <vector>
+
 #include "attn_tc.cuh"
 #include "tc_prims.cuh"
 #include "tmap.cuh"
@@ -143,6 +145,7 @@ constexpr int kNS = 4;                 // smem stages (32 KB each: one K or V^T 
 constexpr int kTcThreads = 192;
 constexpr uint32_t kStageBytes = 32768;
 constexpr uint32_t kSmemBytes = 65536 + kNS * kStageBytes + 256 + 1024;
+constexpr int kMassSlots = 24;  // retrieved units whose masses are reduced in-kernel
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColSX = 256, kColO = 384;
 
 enum { SRC_INIT = 0, SRC_UNIT = 1, SRC_RING = 2 };
@@ -229,8 +232,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     uint64_t* p_full = bars + 3 + 2 * kNS;
     uint64_t* o_done = bars + 5 + 2 * kNS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * kNS);
+    float2* sMass = reinterpret_cast<float2*>(smem + 65536 + kNS * kStageBytes + 256);  // [slot][128 rows]
+    double* sRed = reinterpret_cast<double*>(sMass + kMassSlots * 128);                  // [slot][4]
 
     const AttnParams& a = P.a;
+    const bool mass_in_kernel = a.want_mass && a.n_sel <= kMassSlots;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m = blockIdx.x, h = blockIdx.y, g = h / a.rep;
     TileSched ts;
@@ -434,10 +440,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 rs += x[c];
             }
             l_run += rs;
-            if (t.slot >= 0 && a.want_mass && row_ok) {
-                const int64_t o = (static_cast<int64_t>(h) * a.lx + i) * a.n_sel + t.slot;
-                a.mass_e[o] = rs;
-                a.mass_m[o] = m_run * 0.6931471805599453f;
+            if (t.slot >= 0 && a.want_mass) {
+                if (mass_in_kernel) {
+                    sMass[t.slot * 128 + row] = make_float2(row_ok ? rs : 0.f, m_run);
+                } else if (row_ok) {
+                    const int64_t o = (static_cast<int64_t>(h) * a.lx + i) * a.n_sel + t.slot;
+                    a.mass_e[o] = rs;
+                    a.mass_m[o] = m_run * 0.6931471805599453f;
+                }
             }
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -472,7 +482,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 for (int v4 = 0; v4 < 4; ++v4) dst[v4] = make_uint4(w[4 * v4], w[4 * v4 + 1], w[4 * v4 + 2], w[4 * v4 + 3]);
             }
         }
-        if (row_ok && a.want_mass) {
+        if (mass_in_kernel) {
+            // per-unit attention mass of this CTA's rows: sum_rows e_u 2^(m_u - m) / l
+            // (engine.hpp:271-283), fp64, fixed order: lanes (xor tree), then quarters 0..3
+            for (int u = 0; u < a.n_sel; ++u) {
+                const float2 em = sMass[u * 128 + row];
+                double w = (row_ok && em.x > 0.f) ? static_cast<double>(em.x * ex2(em.y - m_run) * inv) : 0.0;
+                w = warp_sum_d(w);
+                if (lane == 0) sRed[u * 4 + q4] = w;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int tid = threadIdx.x - 64;
+            if (tid < a.n_sel) {
+                const double* r4 = sRed + tid * 4;
+                a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
+            }
+        } else if (row_ok && a.want_mass) {
             a.row_m[static_cast<int64_t>(h) * a.lx + i] = m_run * 0.6931471805599453f;
             a.row_l[static_cast<int64_t>(h) * a.lx + i] = l_run;
         }
@@ -482,31 +507,74 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
+bool attn_tc_masses_in_kernel(int n_sel) { return n_sel <= kMassSlots; }
+
 bool attn_tc_supported(int d, int dv, int unit_size, bool absolute) {
     return d == 128 && dv == 128 && unit_size == 128 && !absolute;
 }
+
+// Tensor maps depend only on buffer pointers/extents: cache them so a step
+// costs no host-side re-encoding (a handful of layers x engines in flight).
+struct TmapKey {
+    const void* p[9];
+    uint64_t n[4];
+    bool operator==(const TmapKey& o) const {
+        for (int i = 0; i < 9; ++i)
+            if (p[i] != o.p[i]) return false;
+        for (int i = 0; i < 4; ++i)
+            if (n[i] != o.n[i]) return false;
+        return true;
+    }
+};
+struct TmapEntry {
+    TmapKey key;
+    CUtensorMap m[9];
+};
 
 int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     TcParams P;
     P.a = a;
     const uint64_t R = static_cast<uint64_t>(a.R);
-    P.tm_qa = make_tmap_bf16_sw128(a.qa, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
-    P.tm_qc = make_tmap_bf16_sw128(a.qc, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
-    P.tm_rk = make_tmap_bf16_sw128(a.ring_k, a.G * R, 128, 128);
-    P.tm_rkr = make_tmap_bf16_sw128(a.ring_krot, a.G * R, 128, 128);
-    P.tm_rv = make_tmap_bf16_sw128(a.ring_v, a.G * (R / 128) * 128, 128, 128);
-    P.tm_ik = make_tmap_bf16_sw128(a.init_k, static_cast<uint64_t>(a.G) * a.l_I, 128, 128);
-    P.tm_iv = make_tmap_bf16_sw128(a.init_v, static_cast<uint64_t>(a.G) * a.vl.nI * 128, 128, 128);
     const uint64_t ucap = static_cast<uint64_t>(a.unit_cap > 0 ? a.unit_cap : 1);
-    P.tm_uk = make_tmap_bf16_sw128(a.unit_k ? a.unit_k : a.ring_k, a.unit_k ? ucap * a.G * 128 : 128, 128, 128);
-    P.tm_uv = make_tmap_bf16_sw128(a.unit_v ? a.unit_v : a.ring_v, a.unit_v ? ucap * a.G * 128 : 128, 128, 128);
+    TmapKey key{{a.qa, a.qc, a.ring_k, a.ring_krot, a.ring_v, a.init_k, a.init_v, a.unit_k, a.unit_v},
+                {static_cast<uint64_t>(a.H) * a.lxp, a.G * R, ucap, static_cast<uint64_t>(a.G) * a.l_I}};
+    static thread_local std::vector<TmapEntry> cache;
+    TmapEntry* hit = nullptr;
+    for (auto& e : cache)
+        if (e.key == key) hit = &e;
+    if (!hit) {
+        if (cache.size() >= 32) cache.erase(cache.begin());
+        TmapEntry e;
+        e.key = key;
+        e.m[0] = make_tmap_bf16_sw128(a.qa, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
+        e.m[1] = make_tmap_bf16_sw128(a.qc, static_cast<uint64_t>(a.H) * a.lxp, 128, 128);
+        e.m[2] = make_tmap_bf16_sw128(a.ring_k, a.G * R, 128, 128);
+        e.m[3] = make_tmap_bf16_sw128(a.ring_krot, a.G * R, 128, 128);
+        e.m[4] = make_tmap_bf16_sw128(a.ring_v, a.G * (R / 128) * 128, 128, 128);
+        e.m[5] = make_tmap_bf16_sw128(a.init_k, static_cast<uint64_t>(a.G) * a.l_I, 128, 128);
+        e.m[6] = make_tmap_bf16_sw128(a.init_v, static_cast<uint64_t>(a.G) * a.vl.nI * 128, 128, 128);
+        e.m[7] = make_tmap_bf16_sw128(a.unit_k ? a.unit_k : a.ring_k, a.unit_k ? ucap * a.G * 128 : 128, 128, 128);
+        e.m[8] = make_tmap_bf16_sw128(a.unit_v ? a.unit_v : a.ring_v, a.unit_v ? ucap * a.G * 128 : 128, 128, 128);
+        cache.push_back(e);
+        hit = &cache.back();
+    }
+    P.tm_qa = hit->m[0];
+    P.tm_qc = hit->m[1];
+    P.tm_rk = hit->m[2];
+    P.tm_rkr = hit->m[3];
+    P.tm_rv = hit->m[4];
+    P.tm_ik = hit->m[5];
+    P.tm_iv = hit->m[6];
+    P.tm_uk = hit->m[7];
+    P.tm_uv = hit->m[8];
+    const uint32_t smem = kSmemBytes + kMassSlots * 128 * sizeof(float2) + kMassSlots * 4 * sizeof(double);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+        cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     dim3 grid(static_cast<unsigned>((a.lx + 127) / 128), a.H);
-    k_attn_tc<<<grid, kTcThreads, kSmemBytes, st>>>(P);
+    k_attn_tc<<<grid, kTcThreads, smem, st>>>(P);
     return 1;
 }
 

@@ -7,6 +7,8 @@ namespace infllm {
 
 // true when the tensor-core kernel covers this shape/mode
 bool attn_tc_supported(int d, int dv, int unit_size, bool absolute);
+// true when the tc kernel reduces the per-unit masses itself (AttnParams::mass_cta)
+bool attn_tc_masses_in_kernel(int n_sel);
 // launches the tensor-core attention for one step; returns #kernels launched
 int launch_attn_tc(const AttnParams& p, cudaStream_t st);
 // building-block self-test (one 128x128x128 tile), see attn_tc.cu

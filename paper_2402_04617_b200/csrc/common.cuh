@@ -27,7 +27,9 @@ __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_
 // computed on the host with std::pow exactly like the reference), cos/sin in
 // double, narrowed to float.
 struct RopeFreqs {
-    double f[128];  // up to head_dim 256
+    double f[128];   // up to head_dim 256
+    float cL[128];   // float(cos(l_L * f)), float(sin(l_L * f)): the constant
+    float sL[128];   // rotation of rotate_by_constant (rotary.hpp:66-72)
 };
 
 // rotate one pair exactly like rotate_row (rotary.hpp:40-51): no FMA

@@ -141,7 +141,7 @@ struct infllm_engine {
     VLayout vl{};
 
     // scratch shared by layers (layers run sequentially on one stream)
-    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l;
+    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb;
 
     struct Layer {
         int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
@@ -156,6 +156,68 @@ struct infllm_engine {
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
     };
     std::vector<Layer> layers;
+
+    // host stream arithmetic of a layer (everything a step derives on the host)
+    struct HostState {
+        int64_t n_fed, step, local_start, init_len, n_units, pend_start, pend_count, trace_count, last_n_sel;
+        std::vector<int64_t> unit_start;
+        std::vector<int32_t> unit_len;
+        bool operator==(const HostState& o) const {
+            return n_fed == o.n_fed && step == o.step && local_start == o.local_start && init_len == o.init_len &&
+                   n_units == o.n_units && pend_start == o.pend_start && pend_count == o.pend_count &&
+                   trace_count == o.trace_count && last_n_sel == o.last_n_sel && unit_start == o.unit_start &&
+                   unit_len == o.unit_len;
+        }
+    };
+    static HostState save(const Layer& L) {
+        return HostState{L.n_fed,      L.step,        L.local_start, L.init_len,   L.n_units,   L.pend_start,
+                         L.pend_count, L.trace_count, L.last_n_sel,  L.unit_start, L.unit_len};
+    }
+    static void restore(Layer& L, const HostState& h) {
+        L.n_fed = h.n_fed;
+        L.step = h.step;
+        L.local_start = h.local_start;
+        L.init_len = h.init_len;
+        L.n_units = h.n_units;
+        L.pend_start = h.pend_start;
+        L.pend_count = h.pend_count;
+        L.trace_count = h.trace_count;
+        L.last_n_sel = h.last_n_sel;
+        L.unit_start = h.unit_start;
+        L.unit_len = h.unit_len;
+    }
+
+    // CUDA graphs of whole multi-chunk streams: the launch sequence and every
+    // kernel parameter follow from the host arithmetic alone (data-dependent
+    // values stay on the device), so a stream from a given host state replays
+    // as one graph launch.
+    struct GraphEntry {
+        int layer;
+        const void *q, *k, *v;
+        void* out;
+        int64_t n;
+        bool host, prof;
+        HostState before, after;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, lookup_ev;
+        int64_t replays_in_window = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    cudaStream_t cap_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
+    bool use_graphs = true;
+    bool capturing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_attn_ev = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_lookup_ev = nullptr;
+    static constexpr int kNB = 3;  // host-pointer staging buffers
+    DBuf stage_q[kNB], stage_k[kNB], stage_v[kNB], stage_o[kNB];
+
+    void record(cudaEvent_t e, cudaStream_t st) {
+        if (capturing)
+            ck(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal), "event record (capture)");
+        else
+            ck(cudaEventRecord(e, st), "event record");
+    }
 
     // profiling (dominant kernel + lookup timing with events on the caller stream)
     bool prof = false;
@@ -261,15 +323,17 @@ struct infllm_engine {
         pp.dv = dv;
         pp.freqs = freqs;
         pp.vl = vl;
+        pp.rtab = rtab.as<float2>();
+        pp.qs = qsb.as<double>();
         launch_prep<T>(pp, st);
-        launches += 2;
+        launches += (d % 8 == 0 && dv % 8 == 0) ? 3 : 2;
 
         // K1 + K2: lookup (memory.hpp:239-269)
         if (do_lookup) {
             std::pair<cudaEvent_t, cudaEvent_t> evp{};
             if (prof) {
                 evp = {take_event(), take_event()};
-                cudaEventRecord(evp.first, st);
+                record(evp.first, st);
             }
             LookupParams lp{};
             lp.qsum = chunk_qsum.as<double>();
@@ -286,21 +350,15 @@ struct infllm_engine {
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
             tp.rel = L.rel.as<double>();
-            tp.relw = L.relw.as<double>();
             tp.sel = L.sel.as<int64_t>();
-            tp.hot = L.hot.as<int8_t>();
-            tp.hot_list = L.hot_list.as<int64_t>();
-            tp.lru = L.lru.as<LruState>();
-            tp.trace = L.trace.as<int64_t>();
             tp.U = L.n_units;
             tp.n_sel = n_sel;
-            tp.step = L.step;
             tp.Gtot = Gt;
             launch_topk(tp, st);
             launches += 2;
             if (prof) {
-                cudaEventRecord(evp.second, st);
-                ev_lookup.push_back(evp);
+                record(evp.second, st);
+                (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
             }
         }
 
@@ -325,6 +383,7 @@ struct infllm_engine {
         ap.mass_m = mass_m.as<float>();
         ap.row_m = row_m.as<float>();
         ap.row_l = row_l.as<float>();
+        ap.mass_cta = mass_cta.as<double>();
         ap.R = R;
         ap.s = s;
         ap.lx = lx;
@@ -348,7 +407,7 @@ struct infllm_engine {
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
             eva = {take_event(), take_event()};
-            cudaEventRecord(eva.first, st);
+            record(eva.first, st);
         }
         if constexpr (std::is_same_v<T, bf16>) {
             if (tc_eligible(lx)) {
@@ -362,41 +421,63 @@ struct infllm_engine {
             ++launches;
         }
         if (prof) {
-            cudaEventRecord(eva.second, st);
-            ev_attn.push_back(eva);
+            record(eva.second, st);
+            (capturing ? *cap_attn_ev : ev_attn).push_back(eva);
         }
 
-        // attention masses -> frequency update + capacity (engine.hpp:271-285)
+        // attention masses -> lookup bookkeeping, frequency update, capacity
+        // (engine.hpp:257,271-285; memory.hpp:254-300)
+        const bool tc_ran = std::is_same_v<T, bf16> && tc_eligible(lx);
+        int mass_src = 0;
         if (want_mass) {
-            MassParams mp{};
-            mp.mass_e = mass_e.as<float>();
-            mp.mass_m = mass_m.as<float>();
-            mp.row_m = row_m.as<float>();
-            mp.row_l = row_l.as<float>();
-            mp.part = L.mass_part.as<double>();
-            mp.lx = lx;
-            mp.n_sel = static_cast<int>(n_sel);
-            mp.H = Hs;
-            mp.G = Gs;
-            mp.Gtot = Gt;
-            mp.g0 = g0;
-            mp.rep = rep;
-            launch_mass(mp, st);
-            ++launches;
-            gather(L.mass_part.as<double>(), n_sel, st);
+            if (tc_ran && attn_tc_masses_in_kernel(static_cast<int>(n_sel))) {
+                if (Gs == Gt) {
+                    mass_src = 1;
+                } else {
+                    launch_mass_cta_reduce(mass_cta.as<double>(), L.mass_part.as<double>(), static_cast<int>(n_sel), Gs,
+                                           Gt, g0, rep, static_cast<int>((lx + 127) / 128), st);
+                    ++launches;
+                    gather(L.mass_part.as<double>(), n_sel, st);
+                }
+            } else {
+                MassParams mp{};
+                mp.mass_e = mass_e.as<float>();
+                mp.mass_m = mass_m.as<float>();
+                mp.row_m = row_m.as<float>();
+                mp.row_l = row_l.as<float>();
+                mp.part = L.mass_part.as<double>();
+                mp.lx = lx;
+                mp.n_sel = static_cast<int>(n_sel);
+                mp.H = Hs;
+                mp.G = Gs;
+                mp.Gtot = Gt;
+                mp.g0 = g0;
+                mp.rep = rep;
+                launch_mass(mp, st);
+                ++launches;
+                gather(L.mass_part.as<double>(), n_sel, st);
+            }
         }
         LruParams lp{};
         lp.mass_part = L.mass_part.as<double>();
+        lp.mass_cta = mass_cta.as<double>();
         lp.sel = L.sel.as<int64_t>();
         lp.freq = L.freq.as<double>();
         lp.hot = L.hot.as<int8_t>();
         lp.hot_list = L.hot_list.as<int64_t>();
         lp.unit_len = L.ulen.as<int32_t>();
         lp.lru = L.lru.as<LruState>();
-        lp.n_sel = want_mass ? n_sel : 0;
+        lp.trace = L.trace.as<int64_t>();
+        lp.n_sel = n_sel;
+        lp.n_mass = want_mass ? n_sel : 0;
         lp.cap = cfg.hot_capacity;
+        lp.step = L.step;
         lp.Gtot = Gt;
+        lp.G = Gs;
+        lp.rep = rep;
+        lp.n_mt = static_cast<int>((lx + 127) / 128);
         lp.H_total = H;
+        lp.mass_src = mass_src;
         lp.decay = cfg.decay;
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
         launch_lru(lp, st);
@@ -485,6 +566,162 @@ struct infllm_engine {
         ck(cudaGetLastError(), "kernel launch");
     }
 
+    // pointer to chunk `off` of a token-major tensor with `row` elements per token
+    const void* at(const void* p, int64_t off, int64_t row) const {
+        return static_cast<const uint8_t*>(p) + off * row * static_cast<int64_t>(esz);
+    }
+
+    template <typename T>
+    void run_chunks(int li, const void* q, const void* k, const void* v, int64_t n, void* out, cudaStream_t st) {
+        for (int64_t off = 0; off < n; off += cfg.chunk_size) {
+            const int64_t lx = std::min<int64_t>(cfg.chunk_size, n - off);
+            step<T>(li, at(q, off, Hs * d), at(k, off, Gs * d), at(v, off, Gs * dv), lx, false,
+                    const_cast<void*>(at(out, off, Hs * dv)), st);
+        }
+    }
+
+    // host-pointer stream: per chunk H2D of q/k/v into staging buffers, the
+    // step, D2H of the output; copies run on their own streams and overlap the
+    // neighbouring chunks' compute
+    template <typename T>
+    void run_chunks_host(int li, const void* hq, const void* hk, const void* hv, int64_t n, void* hout,
+                         cudaStream_t st) {
+        const int64_t C = cfg.chunk_size;
+        const int64_t nch = (n + C - 1) / C;
+        std::vector<cudaEvent_t> ev_in(nch), ev_comp(nch), ev_out(nch);
+        for (int64_t t = 0; t < nch; ++t) {
+            ev_in[t] = take_event();
+            ev_comp[t] = take_event();
+            ev_out[t] = take_event();
+        }
+        cudaEvent_t fork = take_event();
+        ck(cudaEventRecord(fork, st), "fork");
+        ck(cudaStreamWaitEvent(h2d_stream, fork, 0), "fork");
+        ck(cudaStreamWaitEvent(d2h_stream, fork, 0), "fork");
+        auto h2d = [&](int64_t t) {
+            const int64_t off = t * C, lx = std::min<int64_t>(C, n - off);
+            const int b = static_cast<int>(t % kNB);
+            if (t >= kNB) {
+                ck(cudaStreamWaitEvent(h2d_stream, ev_comp[t - kNB], 0), "wait");
+            }
+            ck(cudaMemcpyAsync(stage_q[b].p, at(hq, off, Hs * d), lx * Hs * d * esz, cudaMemcpyHostToDevice, h2d_stream),
+               "H2D");
+            ck(cudaMemcpyAsync(stage_k[b].p, at(hk, off, Gs * d), lx * Gs * d * esz, cudaMemcpyHostToDevice, h2d_stream),
+               "H2D");
+            ck(cudaMemcpyAsync(stage_v[b].p, at(hv, off, Gs * dv), lx * Gs * dv * esz, cudaMemcpyHostToDevice,
+                               h2d_stream),
+               "H2D");
+            ck(cudaEventRecord(ev_in[t], h2d_stream), "record");
+        };
+        for (int64_t t = 0; t < std::min<int64_t>(kNB - 1, nch); ++t) h2d(t);
+        for (int64_t t = 0; t < nch; ++t) {
+            if (t + kNB - 1 < nch) h2d(t + kNB - 1);
+            const int64_t off = t * C, lx = std::min<int64_t>(C, n - off);
+            const int b = static_cast<int>(t % kNB);
+            ck(cudaStreamWaitEvent(st, ev_in[t], 0), "wait");
+            if (t >= kNB) ck(cudaStreamWaitEvent(st, ev_out[t - kNB], 0), "wait");  // stage_o[b] drained
+            step<T>(li, stage_q[b].p, stage_k[b].p, stage_v[b].p, lx, false, stage_o[b].p, st);
+            ck(cudaEventRecord(ev_comp[t], st), "record");
+            ck(cudaStreamWaitEvent(d2h_stream, ev_comp[t], 0), "wait");
+            ck(cudaMemcpyAsync(const_cast<void*>(at(hout, off, Hs * dv)), stage_o[b].p, lx * Hs * dv * esz,
+                               cudaMemcpyDeviceToHost, d2h_stream),
+               "D2H");
+            ck(cudaEventRecord(ev_out[t], d2h_stream), "record");
+        }
+        ck(cudaStreamWaitEvent(st, ev_out[nch - 1], 0), "join");
+        ck(cudaStreamWaitEvent(st, ev_in[nch - 1], 0), "join");
+        for (int64_t t = 0; t < nch; ++t) {
+            ev_pool.push_back(ev_in[t]);
+            ev_pool.push_back(ev_comp[t]);
+            ev_pool.push_back(ev_out[t]);
+        }
+        ev_pool.push_back(fork);
+    }
+
+    template <typename T>
+    void encode_stream(int li, const void* q, const void* k, const void* v, int64_t n, void* out, cudaStream_t st,
+                       bool host) {
+        if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
+        if (n < 1) throw StreamError("encode_stream: empty stream");
+        Layer& L = layers[static_cast<size_t>(li)];
+        if (!cap_stream) {
+            ck(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking), "stream");
+        }
+        // capacity for the whole stream up front (no pool growth inside a graph)
+        const int64_t steps = (n + cfg.chunk_size - 1) / cfg.chunk_size;
+        ensure_units(L, L.n_units + (L.pend_count + n) / cfg.unit_size + 2, st);
+        ensure_trace(L, L.trace_count + steps * std::max<int64_t>(cfg.n_lookup, 1), st);
+        if (host && !stage_q[0].p) {
+            const int64_t C = cfg.chunk_size;
+            for (int b = 0; b < kNB; ++b) {
+                stage_q[b].alloc(C * Hs * d * esz, st, false);
+                stage_k[b].alloc(C * Gs * d * esz, st, false);
+                stage_v[b].alloc(C * Gs * dv * esz, st, false);
+                stage_o[b].alloc(C * Hs * dv * esz, st, false);
+            }
+        }
+        if (!use_graphs) {
+            if (host)
+                run_chunks_host<T>(li, q, k, v, n, out, st);
+            else
+                run_chunks<T>(li, q, k, v, n, out, st);
+            return;
+        }
+        const HostState cur = save(L);
+        GraphEntry* ge = nullptr;
+        for (auto& g : graphs)
+            if (g.layer == li && g.q == q && g.k == k && g.v == v && g.out == out && g.n == n && g.host == host &&
+                g.prof == prof && g.before == cur)
+                ge = &g;
+        if (!ge) {
+            ck(cudaStreamSynchronize(st), "pre-capture sync");
+            GraphEntry g;
+            g.layer = li;
+            g.q = q;
+            g.k = k;
+            g.v = v;
+            g.out = out;
+            g.n = n;
+            g.host = host;
+            g.prof = prof;
+            g.before = cur;
+            const int64_t l0 = launches;
+            cudaGraph_t graph = nullptr;
+            capturing = true;
+            cap_attn_ev = &g.attn_ev;
+            cap_lookup_ev = &g.lookup_ev;
+            ck(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+            try {
+                if (host)
+                    run_chunks_host<T>(li, q, k, v, n, out, cap_stream);
+                else
+                    run_chunks<T>(li, q, k, v, n, out, cap_stream);
+            } catch (...) {
+                capturing = false;
+                cudaStreamEndCapture(cap_stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                restore(L, cur);
+                throw;
+            }
+            capturing = false;
+            ck(cudaStreamEndCapture(cap_stream, &graph), "end capture");
+            ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+            cudaGraphDestroy(graph);
+            g.after = save(L);
+            g.launches = launches - l0;
+            launches = l0;
+            restore(L, cur);
+            graphs.push_back(std::move(g));
+            ge = &graphs.back();
+        }
+        ck(cudaGraphLaunch(ge->exec, st), "graph launch");
+        restore(L, ge->after);
+        launches += ge->launches;
+        if (prof) ge->replays_in_window++;
+    }
+
     template <typename T>
     void finish(cudaStream_t st) {  // engine.hpp:115-119, UnitPacker::flush memory.hpp:81-84
         for (auto& L : layers) {
@@ -565,6 +802,8 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->n_layers = shape->n_layers;
         if (e->d > 256 || e->dv > 128) throw ConfigError("head_dim <= 256 and value_dim <= 128 supported");
         if (cfg->n_repr > 32) throw ConfigError("n_repr <= 32 supported");
+        if (cfg->n_lookup > 128) throw ConfigError("n_lookup <= 128 supported");
+        if (cfg->hot_capacity + cfg->n_lookup > 510) throw ConfigError("hot_capacity + n_lookup <= 510 supported");
         if (kv_group_count <= 0) {
             kv_group_begin = 0;
             kv_group_count = e->Gt;
@@ -580,7 +819,12 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         const int64_t need = cfg->local_size + cfg->chunk_size + 1;
         e->R = (need + 127) / 128 * 128;
         e->lxp = (cfg->chunk_size + 127) / 128 * 128;
-        for (int a = 0; a < e->d / 2; ++a) e->freqs.f[a] = std::pow(10000.0, -2.0 * a / e->d);  // rotary.hpp:25
+        for (int a = 0; a < e->d / 2; ++a) {  // rotary.hpp:25-30 (RotaryTable::make)
+            e->freqs.f[a] = std::pow(10000.0, -2.0 * a / e->d);
+            const double ang = static_cast<double>(cfg->local_size) * e->freqs.f[a];
+            e->freqs.cL[a] = static_cast<float>(std::cos(ang));
+            e->freqs.sL[a] = static_cast<float>(std::sin(ang));
+        }
         e->use_tc = dtype == INFLLM_DTYPE_BF16 && attn_tc_supported(e->d, e->dv, static_cast<int>(cfg->unit_size),
                                                                      cfg->position_mode == INFLLM_POSITION_ABSOLUTE);
         e->vl.vt = e->use_tc ? 1 : 0;
@@ -601,6 +845,9 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->mass_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
         e->row_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
         e->row_l.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
+        e->rtab.alloc(static_cast<size_t>(cfg->chunk_size) * std::max(1, e->d / 2) * sizeof(float2), st);
+        e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
+        e->mass_cta.alloc(static_cast<size_t>(e->Hs) * (e->lxp / 128) * km * sizeof(double), st);
         e->layers.resize(static_cast<size_t>(e->n_layers));
         for (auto& L : e->layers) {
             L.ring_k.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
@@ -628,7 +875,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         if (!e) return;
         cudaDeviceSynchronize();
         cudaStream_t st = nullptr;
-        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l}) b->release(st);
+        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb}) b->release(st);
         for (auto& L : e->layers)
             for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
@@ -644,6 +891,21 @@ int infllm_engine_destroy(infllm_engine_t e) {
             cudaEventDestroy(p.second);
         }
         for (auto ev : e->ev_pool) cudaEventDestroy(ev);
+        for (auto& g : e->graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            for (auto& p : g.attn_ev) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+            for (auto& p : g.lookup_ev) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+        }
+        for (int b = 0; b < infllm_engine::kNB; ++b)
+            for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
+        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream})
+            if (s2) cudaStreamDestroy(s2);
         cudaDeviceSynchronize();
         delete e;
     });
@@ -697,6 +959,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         const std::string k = key ? key : "";
         if (k == "tc_attention")
             e->tc_disabled = value == 0;
+        else if (k == "cuda_graphs")
+            e->use_graphs = value != 0;
         else
             throw ConfigError("unknown option '" + k + "'");
     });
@@ -723,6 +987,30 @@ int infllm_decode_step(infllm_engine_t e, int32_t layer, const void* q, const vo
             e->step<bf16>(layer, q, k, v, 1, true, out, st);
         else
             e->step<float>(layer, q, k, v, 1, true, out, st);
+    });
+}
+
+int infllm_encode_stream(infllm_engine_t e, int32_t layer, const void* q, const void* k, const void* v,
+                         int64_t n_tokens, void* out, void* stream) {
+    return guard([&] {
+        if (!e) throw ConfigError("null engine");
+        auto st = static_cast<cudaStream_t>(stream);
+        if (e->dtype == INFLLM_DTYPE_BF16)
+            e->encode_stream<bf16>(layer, q, k, v, n_tokens, out, st, false);
+        else
+            e->encode_stream<float>(layer, q, k, v, n_tokens, out, st, false);
+    });
+}
+
+int infllm_encode_stream_host(infllm_engine_t e, int32_t layer, const void* host_q, const void* host_k,
+                              const void* host_v, int64_t n_tokens, void* host_out, void* stream) {
+    return guard([&] {
+        if (!e) throw ConfigError("null engine");
+        auto st = static_cast<cudaStream_t>(stream);
+        if (e->dtype == INFLLM_DTYPE_BF16)
+            e->encode_stream<bf16>(layer, host_q, host_k, host_v, n_tokens, host_out, st, true);
+        else
+            e->encode_stream<float>(layer, host_q, host_k, host_v, n_tokens, host_out, st, true);
     });
 }
 
@@ -843,6 +1131,7 @@ int infllm_profile_begin(infllm_engine_t e, int32_t enable) {
         }
         e->ev_attn.clear();
         e->ev_lookup.clear();
+        for (auto& g : e->graphs) g.replays_in_window = 0;
         e->prof = enable != 0;
     });
 }
@@ -861,10 +1150,30 @@ int infllm_profile_read(infllm_engine_t e, double* attn_ms, int64_t* attn_n, dou
             ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
             b += ms;
         }
+        int64_t na = static_cast<int64_t>(e->ev_attn.size()), nb = static_cast<int64_t>(e->ev_lookup.size());
+        // graph replays: event nodes hold the timings of the latest replay
+        for (auto& g : e->graphs) {
+            if (g.replays_in_window == 0) continue;
+            double ga = 0, gb = 0;
+            for (auto& p : g.attn_ev) {
+                float ms = 0;
+                ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
+                ga += ms;
+            }
+            for (auto& p : g.lookup_ev) {
+                float ms = 0;
+                ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
+                gb += ms;
+            }
+            a += ga * g.replays_in_window;
+            b += gb * g.replays_in_window;
+            na += static_cast<int64_t>(g.attn_ev.size()) * g.replays_in_window;
+            nb += static_cast<int64_t>(g.lookup_ev.size()) * g.replays_in_window;
+        }
         *attn_ms = a;
-        *attn_n = static_cast<int64_t>(e->ev_attn.size());
+        *attn_n = na;
         *lookup_ms = b;
-        *lookup_n = static_cast<int64_t>(e->ev_lookup.size());
+        *lookup_n = nb;
     });
 }
 

@@ -15,13 +15,23 @@ namespace infllm {
 
 // --------------------------------------------------------------------------
 // K7 prep: append k/v to the ring, K_rot = rope(k, pos), q_abs = rope(q, pos),
-// q_clamp = rope(q, L)  (rotary.hpp:55-72; attention.hpp:166-167)
+// q_clamp = rope(q, L)  (rotary.hpp:55-72; attention.hpp:166-167).
+// Block = 4 tokens; the (cos, sin) factors of each (token, pair) are computed
+// once (fp64 angle, rotary.hpp:25-30) and shared by all heads.
+constexpr int kPrepTok = 4;
 template <typename T>
-__global__ void k_prep(PrepParams p) {
-    const int64_t i = blockIdx.x;
-    const int64_t pos = p.s + i;
+__global__ void __launch_bounds__(256) k_prep(PrepParams p) {
+    __shared__ float2 cs[kPrepTok][128];
     const int pairs = p.d / 2;
-    const int64_t slot = pos % p.R;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kPrepTok;
+    const int nt = static_cast<int>(min(static_cast<int64_t>(kPrepTok), p.lx - i0));
+    for (int t = threadIdx.x; t < nt * pairs; t += blockDim.x) {
+        const int tok = t / pairs, a = t % pairs;
+        float c, sn;
+        rope_cs(p.freqs, a, p.s + i0 + tok, c, sn);
+        cs[tok][a] = make_float2(c, sn);
+    }
+    __syncthreads();
     const T* q = static_cast<const T*>(p.q);
     const T* k = static_cast<const T*>(p.k);
     const T* v = static_cast<const T*>(p.v);
@@ -30,63 +40,65 @@ __global__ void k_prep(PrepParams p) {
     T* rk = static_cast<T*>(p.ring_k);
     T* rkr = static_cast<T*>(p.ring_krot);
     T* rv = static_cast<T*>(p.ring_v);
-    // queries: H heads x pairs
-    for (int t = threadIdx.x; t < p.H * pairs; t += blockDim.x) {
-        const int h = t / pairs, a = t % pairs;
+    const int dh = (p.d + 1) / 2;  // pairs + odd tail slot
+    for (int t = threadIdx.x; t < nt * p.H * dh; t += blockDim.x) {
+        const int tok = t / (p.H * dh), rem = t % (p.H * dh), h = rem / dh, a = rem % dh;
+        const int64_t i = i0 + tok;
         const T* src = q + (i * p.H + h) * p.d;
-        const float x0 = to_f(src[2 * a]), x1 = to_f(src[2 * a + 1]);
-        float c, s, y0, y1;
-        rope_cs(p.freqs, a, pos, c, s);
-        rope_pair(x0, x1, c, s, y0, y1);
         T* da = qa + (static_cast<int64_t>(h) * p.lxp + i) * p.d;
+        T* dc = qc + (static_cast<int64_t>(h) * p.lxp + i) * p.d;
+        if (a == pairs) {  // odd trailing component is left as is (rotary.hpp:36-37)
+            da[p.d - 1] = src[p.d - 1];
+            dc[p.d - 1] = src[p.d - 1];
+            continue;
+        }
+        const float x0 = to_f(src[2 * a]), x1 = to_f(src[2 * a + 1]);
+        float y0, y1;
+        const float2 f = cs[tok][a];
+        rope_pair(x0, x1, f.x, f.y, y0, y1);
         da[2 * a] = from_f<T>(y0);
         da[2 * a + 1] = from_f<T>(y1);
-        rope_cs(p.freqs, a, p.L, c, s);
-        rope_pair(x0, x1, c, s, y0, y1);
-        T* dc = qc + (static_cast<int64_t>(h) * p.lxp + i) * p.d;
+        rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
         dc[2 * a] = from_f<T>(y0);
         dc[2 * a + 1] = from_f<T>(y1);
     }
-    if (p.d & 1) {  // odd trailing component is left as is (rotary.hpp:36-37)
-        for (int h = threadIdx.x; h < p.H; h += blockDim.x) {
-            const T x = q[(i * p.H + h) * p.d + p.d - 1];
-            qa[(static_cast<int64_t>(h) * p.lxp + i) * p.d + p.d - 1] = x;
-            qc[(static_cast<int64_t>(h) * p.lxp + i) * p.d + p.d - 1] = x;
-        }
-    }
-    // keys: raw copy + rotated copy
-    for (int t = threadIdx.x; t < p.G * pairs; t += blockDim.x) {
-        const int g = t / pairs, a = t % pairs;
+    for (int t = threadIdx.x; t < nt * p.G * dh; t += blockDim.x) {
+        const int tok = t / (p.G * dh), rem = t % (p.G * dh), g = rem / dh, a = rem % dh;
+        const int64_t i = i0 + tok, pos = p.s + i;
         const T* src = k + (i * p.G + g) * p.d;
+        const int64_t o = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d;
+        if (a == pairs) {
+            rk[o + p.d - 1] = src[p.d - 1];
+            rkr[o + p.d - 1] = src[p.d - 1];
+            continue;
+        }
         const T x0r = src[2 * a], x1r = src[2 * a + 1];
-        float c, s, y0, y1;
-        rope_cs(p.freqs, a, pos, c, s);
-        rope_pair(to_f(x0r), to_f(x1r), c, s, y0, y1);
-        const int64_t o = (static_cast<int64_t>(g) * p.R + slot) * p.d;
+        float y0, y1;
+        const float2 f = cs[tok][a];
+        rope_pair(to_f(x0r), to_f(x1r), f.x, f.y, y0, y1);
         rk[o + 2 * a] = x0r;
         rk[o + 2 * a + 1] = x1r;
         rkr[o + 2 * a] = from_f<T>(y0);
         rkr[o + 2 * a + 1] = from_f<T>(y1);
     }
-    if (p.d & 1) {
-        for (int g = threadIdx.x; g < p.G; g += blockDim.x) {
-            const int64_t o = (static_cast<int64_t>(g) * p.R + slot) * p.d + p.d - 1;
-            rk[o] = k[(i * p.G + g) * p.d + p.d - 1];
-            rkr[o] = rk[o];
-        }
-    }
-    for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
-        const int g = t / p.dv, c = t % p.dv;
-        rv[p.vl.ring(g, pos, c)] = v[(i * p.G + g) * p.dv + c];
+    // values: consecutive threads take consecutive tokens so transposed pages
+    // get adjacent 2-byte stores
+    for (int t = threadIdx.x; t < nt * p.G * p.dv; t += blockDim.x) {
+        const int tok = t % nt, rem = t / nt, g = rem / p.dv, c = rem % p.dv;
+        const int64_t i = i0 + tok;
+        rv[p.vl.ring(g, p.s + i, c)] = v[(i * p.G + g) * p.dv + c];
     }
 }
 
 // prefix of qs_t[g][c] = sum_{h in g} q[t][h][c] (fp64) into the P ring, and
-// the chunk total (the lookup's query sum, memory.hpp:224-225).
-constexpr int kScanSegs = 16;
+// the chunk total (the lookup's query sum, memory.hpp:224-225). Block = one
+// group x 32 columns; 32 token segments scanned in parallel, then combined.
+// (bf16 inputs make every fp64 partial exact, so the association does not
+// change the values.)
+constexpr int kScanSegs = 32;
 template <typename T>
-__global__ void k_prefix(PrepParams p) {
-    __shared__ double tot[kScanSegs][32];
+__global__ void __launch_bounds__(1024) k_prefix(PrepParams p) {
+    __shared__ double tot[kScanSegs][33];
     const int g = blockIdx.x;
     const int c = blockIdx.y * 32 + threadIdx.x;
     const int seg = threadIdx.y;
@@ -118,9 +130,180 @@ __global__ void k_prefix(PrepParams p) {
     }
 }
 
+// ---- vectorised prep path (head_dim, value_dim multiples of 8) ----------------
+// (1) per-step rotation-factor table: one fp64 sincos per (token, pair)
+__global__ void k_rope_table(PrepParams p) {
+    const int pairs = p.d / 2;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= p.lx * pairs) return;
+    const int64_t i = t / pairs;
+    const int a = static_cast<int>(t % pairs);
+    float c, s;
+    rope_cs(p.freqs, a, p.s + i, c, s);
+    p.rtab[t] = make_float2(c, s);
+}
+
+template <typename T>
+struct V8 {
+    T v[8];
+};
+template <typename T>
+__device__ __forceinline__ V8<T> ld8(const T* p) {
+    V8<T> r;
+    if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(&r) = *reinterpret_cast<const uint4*>(p);
+    } else {
+        reinterpret_cast<uint4*>(&r)[0] = reinterpret_cast<const uint4*>(p)[0];
+        reinterpret_cast<uint4*>(&r)[1] = reinterpret_cast<const uint4*>(p)[1];
+    }
+    return r;
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const V8<T>& r) {
+    if constexpr (sizeof(T) == 2) {
+        *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(&r);
+    } else {
+        reinterpret_cast<uint4*>(p)[0] = reinterpret_cast<const uint4*>(&r)[0];
+        reinterpret_cast<uint4*>(p)[1] = reinterpret_cast<const uint4*>(&r)[1];
+    }
+}
+
+// (2) one thread per (token, KV group, 8 dims): k raw -> ring, k_rot -> ring,
+// every query head of the group -> q_abs / q_clamp, and the fp64 group sum
+// qs[token][g][8 dims]; plus one thread per (8-token run, g, value dim) for
+// the (transposed) value pages.
+template <typename T>
+__global__ void __launch_bounds__(256) k_prep_vec(PrepParams p) {
+    const int pairs = p.d / 2, n8 = p.d / 8;
+    const int64_t n_qk = p.lx * p.G * n8;
+    int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n_qk) {
+        const int c8 = static_cast<int>(t % n8);
+        const int g = static_cast<int>((t / n8) % p.G);
+        const int64_t i = t / (static_cast<int64_t>(n8) * p.G);
+        const int64_t pos = p.s + i;
+        const float2* rt = p.rtab + i * pairs + 4 * c8;
+        float2 f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[j] = rt[j];
+        const T* kq = static_cast<const T*>(p.k) + (i * p.G + g) * p.d + 8 * c8;
+        const V8<T> kv = ld8(kq);
+        V8<T> kr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float y0, y1;
+            rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
+            kr.v[2 * j] = from_f<T>(y0);
+            kr.v[2 * j + 1] = from_f<T>(y1);
+        }
+        const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
+        st8(static_cast<T*>(p.ring_k) + ro, kv);
+        st8(static_cast<T*>(p.ring_krot) + ro, kr);
+        double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int hh = 0; hh < p.rep; ++hh) {
+            const int h = g * p.rep + hh;
+            const V8<T> qv = ld8(static_cast<const T*>(p.q) + (i * p.H + h) * p.d + 8 * c8);
+            V8<T> qa, qc;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float x0 = to_f(qv.v[2 * j]), x1 = to_f(qv.v[2 * j + 1]);
+                float y0, y1;
+                rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
+                qa.v[2 * j] = from_f<T>(y0);
+                qa.v[2 * j + 1] = from_f<T>(y1);
+                const int a = 4 * c8 + j;
+                rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
+                qc.v[2 * j] = from_f<T>(y0);
+                qc.v[2 * j + 1] = from_f<T>(y1);
+                qs[2 * j] += static_cast<double>(x0);
+                qs[2 * j + 1] += static_cast<double>(x1);
+            }
+            const int64_t qo = (static_cast<int64_t>(h) * p.lxp + i) * p.d + 8 * c8;
+            st8(static_cast<T*>(p.qa) + qo, qa);
+            st8(static_cast<T*>(p.qc) + qo, qc);
+        }
+        double* qd = p.qs + (i * p.G + g) * p.d + 8 * c8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) qd[e] = qs[e];
+        return;
+    }
+    t -= n_qk;
+    const T* v = static_cast<const T*>(p.v);
+    T* rv = static_cast<T*>(p.ring_v);
+    if (!p.vl.vt) {
+        const int nv8 = p.dv / 8;
+        if (t >= p.lx * p.G * nv8) return;
+        const int c8 = static_cast<int>(t % nv8);
+        const int g = static_cast<int>((t / nv8) % p.G);
+        const int64_t i = t / (static_cast<int64_t>(nv8) * p.G);
+        st8(rv + p.vl.ring(g, p.s + i, 8 * c8), ld8(v + (i * p.G + g) * p.dv + 8 * c8));
+        return;
+    }
+    // transposed pages: 8 consecutive positions of one value dim -> one 16 B store
+    const int64_t r0 = p.s / 8, r1 = (p.s + p.lx + 7) / 8;
+    if (t >= (r1 - r0) * p.G * p.dv) return;
+    const int c = static_cast<int>(t % p.dv);
+    const int g = static_cast<int>((t / p.dv) % p.G);
+    const int64_t run = r0 + t / (static_cast<int64_t>(p.dv) * p.G);
+    const int64_t pa = 8 * run;
+    if (pa >= p.s && pa + 8 <= p.s + p.lx && sizeof(T) == 2) {
+        V8<T> w;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w.v[j] = v[((pa - p.s + j) * p.G + g) * p.dv + c];
+        st8(rv + p.vl.ring(g, pa, c), w);
+    } else {
+        for (int j = 0; j < 8; ++j) {
+            const int64_t pos = pa + j;
+            if (pos >= p.s && pos < p.s + p.lx) rv[p.vl.ring(g, pos, c)] = v[((pos - p.s) * p.G + g) * p.dv + c];
+        }
+    }
+}
+
+// (3) fp64 prefix of qs over the chunk into the P ring + the chunk total.
+// Block = (group, 32 dims); 16 token segments scanned in parallel.
+constexpr int kPfxSegs = 16;
+__global__ void __launch_bounds__(512) k_qs_prefix(PrepParams p) {
+    __shared__ double tot[kPfxSegs][33];
+    const int g = blockIdx.x, c = blockIdx.y * 32 + threadIdx.x, seg = threadIdx.y;
+    const bool live = c < p.d;
+    const int64_t len = (p.lx + kPfxSegs - 1) / kPfxSegs;
+    const int64_t i0 = seg * len, i1 = min(p.lx, i0 + len);
+    const double* qs = p.qs + static_cast<int64_t>(g) * p.d + c;
+    const int64_t stride = static_cast<int64_t>(p.G) * p.d;
+    double t = 0.0;
+    if (live) {
+#pragma unroll 8
+        for (int64_t i = i0; i < i1; ++i) t += qs[i * stride];
+    }
+    tot[seg][threadIdx.x] = t;
+    __syncthreads();
+    if (!live) return;
+    double run = p.P[((p.s % p.R) * p.G + g) * p.d + c];
+    for (int j = 0; j < seg; ++j) run += tot[j][threadIdx.x];
+#pragma unroll 8
+    for (int64_t i = i0; i < i1; ++i) {
+        run += qs[i * stride];
+        p.P[(((p.s + i + 1) % p.R) * p.G + g) * p.d + c] = run;
+    }
+    if (seg == 0) {
+        double all = 0.0;
+        for (int j = 0; j < kPfxSegs; ++j) all += tot[j][threadIdx.x];
+        p.chunk_qsum[g * p.d + c] = all;
+    }
+}
+
 template <typename T>
 void launch_prep(const PrepParams& p, cudaStream_t st) {
-    k_prep<T><<<static_cast<unsigned>(p.lx), 256, 0, st>>>(p);
+    if (p.d % 8 == 0 && p.dv % 8 == 0 && p.rtab && p.qs) {
+        const int64_t nt = p.lx * (p.d / 2);
+        k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
+        const int64_t n_qk = p.lx * p.G * (p.d / 8);
+        const int64_t n_v = p.vl.vt ? ((p.s + p.lx + 7) / 8 - p.s / 8) * p.G * p.dv : p.lx * p.G * (p.dv / 8);
+        k_prep_vec<T><<<static_cast<unsigned>((n_qk + n_v + 255) / 256), 256, 0, st>>>(p);
+        k_qs_prefix<<<dim3(p.G, (p.d + 31) / 32), dim3(32, kPfxSegs), 0, st>>>(p);
+        return;
+    }
+    k_prep<T><<<static_cast<unsigned>((p.lx + kPrepTok - 1) / kPrepTok), 256, 0, st>>>(p);
     dim3 grid(p.G, (p.d + 31) / 32);
     k_prefix<T><<<grid, dim3(32, kScanSegs), 0, st>>>(p);
 }
@@ -208,106 +391,124 @@ void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
 }
 
 // --------------------------------------------------------------------------
-// K2 top-k: rel[u] = sum_g part[u][g] (group order), then top n_sel by
-// (rel desc, id asc), ids ascending (memory.hpp:240-253), then the lookup's
-// tier bookkeeping (memory.hpp:254-267).
-__device__ __forceinline__ bool better(double va, int64_t ia, double vb, int64_t ib) {
-    return va > vb || (va == vb && ia < ib);
+// K2 top-k: rel[u] = sum_g part[u][g] (group order 0..Gtot-1), then the top
+// n_sel by (rel desc, id asc), returned ascending (memory.hpp:240-253).
+// Two-level warp selection over shared memory: each warp extracts the top
+// n_sel of its slice, warp 0 merges the candidates; ids are placed by rank.
+__device__ __forceinline__ bool better(double va, int ia, double vb, int ib) {
+    return ia >= 0 && (ib < 0 || va > vb || (va == vb && ia < ib));
+}
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (better(ov, oi, v, i)) {
+            v = ov;
+            i = oi;
+        }
+    }
 }
 
-__device__ void block_topk(const double* rel_in, double* relw, int64_t U, int64_t n_sel, int64_t* out_sorted) {
-    __shared__ double wv[32];
-    __shared__ int64_t wi[32];
-    int64_t* picked = out_sorted;  // written by thread 0 only, sorted in place at the end
-    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32, nw = blockDim.x / 32;
-    for (int64_t u = tid; u < U; u += blockDim.x) relw[u] = rel_in[u];
+constexpr int kTopkMax = 128;  // max k_m
+constexpr int kTopkWarps = 16;
+constexpr int kTopkSmemU = 12288;  // units kept in shared memory (else global)
+// rel: [U] values (read only); work: scratch [U] (global, used when U > kTopkSmemU)
+__device__ void block_topk(const double* rel, double* work, int64_t U, int64_t n_sel, int64_t* out) {
+    extern __shared__ double sh_rel[];
+    __shared__ double cv[kTopkWarps][kTopkMax];
+    __shared__ int ci[kTopkWarps][kTopkMax];
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    double* w = U <= kTopkSmemU ? sh_rel : work;
+    for (int64_t u = threadIdx.x; u < U; u += blockDim.x) w[u] = rel[u];
     __syncthreads();
+    const int64_t S = (U + nw - 1) / nw;
+    const int b0 = static_cast<int>(warp * S), b1 = static_cast<int>(min(U, warp * S + S));
     for (int64_t r = 0; r < n_sel; ++r) {
         double bv = -INFINITY;
-        int64_t bi = INT64_MAX;
-        for (int64_t u = tid; u < U; u += blockDim.x) {
-            const double x = relw[u];
-            if (x != -INFINITY && (bi == INT64_MAX || better(x, u, bv, bi))) {
+        int bi = -1;
+        for (int u = b0 + lane; u < b1; u += 32) {
+            const double x = w[u];
+            if (x != -INFINITY && better(x, u, bv, bi)) {
                 bv = x;
                 bi = u;
             }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi != INT64_MAX && (bi == INT64_MAX || better(ov, oi, bv, bi))) {
-                bv = ov;
-                bi = oi;
-            }
-        }
+        warp_argmax(bv, bi);
         if (lane == 0) {
-            wv[warp] = bv;
-            wi[warp] = bi;
+            cv[warp][r] = bv;
+            ci[warp][r] = bi;
         }
-        __syncthreads();
-        if (tid == 0) {
-            double v = wv[0];
-            int64_t id = wi[0];
-            for (int w = 1; w < nw; ++w)
-                if (wi[w] != INT64_MAX && (id == INT64_MAX || better(wv[w], wi[w], v, id))) {
-                    v = wv[w];
-                    id = wi[w];
-                }
-            picked[r] = id;
-            relw[id] = -INFINITY;
-        }
-        __syncthreads();
+        if (bi >= 0 && (bi - b0) % 32 == lane) w[bi] = -INFINITY;
+        __syncwarp();
     }
-    if (tid == 0) {
-        for (int64_t a = 1; a < n_sel; ++a) {  // ascending ids
-            const int64_t x = picked[a];
-            int64_t b = a - 1;
-            while (b >= 0 && picked[b] > x) {
-                picked[b + 1] = picked[b];
-                --b;
+    __syncthreads();
+    if (warp == 0) {
+        int mine[kTopkMax / 32];
+#pragma unroll
+        for (int k = 0; k < kTopkMax / 32; ++k) mine[k] = -1;
+        const int ns = static_cast<int>(n_sel);
+        for (int r = 0; r < ns; ++r) {
+            double bv = -INFINITY;
+            int bi = -1, bt = -1;
+            for (int t = lane; t < nw * ns; t += 32) {
+                const int ww = t / ns, rr = t % ns;
+                if (better(cv[ww][rr], ci[ww][rr], bv, bi)) {
+                    bv = cv[ww][rr];
+                    bi = ci[ww][rr];
+                    bt = t;
+                }
             }
-            picked[b + 1] = x;
+            const int mybi = bi;
+            warp_argmax(bv, bi);
+            if (mybi == bi && bi >= 0) ci[bt / ns][bt % ns] = -1;  // unique id -> unique owner
+            __syncwarp();
+#pragma unroll
+            for (int kk = 0; kk < kTopkMax / 32; ++kk)
+                if (kk == r / 32 && r % 32 == lane) mine[kk] = bi;
+        }
+        // place by rank (ids are distinct); every lane joins every shuffle
+#pragma unroll
+        for (int k = 0; k < kTopkMax / 32; ++k) {
+            if (32 * k >= ns) break;
+            const int id = mine[k];
+            int rank = 0;
+            for (int r = 0; r < ns; ++r) {
+                int o = 0x7fffffff;
+#pragma unroll
+                for (int kk = 0; kk < kTopkMax / 32; ++kk)
+                    if (kk == r / 32) o = __shfl_sync(0xffffffffu, mine[kk], r % 32);
+                rank += o < id;
+            }
+            if (id >= 0) out[rank] = id;
         }
     }
     __syncthreads();
 }
 
-__global__ void k_topk(TopkParams p) {
+__global__ void __launch_bounds__(512) k_topk(TopkParams p) {
     for (int64_t u = threadIdx.x; u < p.U; u += blockDim.x) {
         double a = 0.0;
         for (int g = 0; g < p.Gtot; ++g) a += p.part[u * p.Gtot + g];
         p.rel[u] = a;
     }
     __syncthreads();
-    block_topk(p.rel, p.relw, p.U, p.n_sel, p.sel);
-    if (threadIdx.x == 0) {
-        LruState& s = *p.lru;
-        for (int64_t a = 0; a < p.n_sel; ++a) {
-            const int64_t id = p.sel[a];
-            s.requested++;
-            int64_t* tr = p.trace + 3 * s.trace_count;
-            tr[0] = p.step;
-            tr[1] = id;
-            if (p.hot[id]) {
-                s.hits++;
-                tr[2] = 1;
-            } else {
-                s.misses++;
-                s.loads++;
-                p.hot[id] = 1;
-                p.hot_list[s.hot_count++] = id;
-                tr[2] = 0;
-            }
-            s.trace_count++;
-        }
-    }
+    block_topk(p.rel, p.rel, p.U, p.n_sel, p.sel);
 }
 
-void launch_topk(const TopkParams& p, cudaStream_t st) { k_topk<<<1, 1024, 0, st>>>(p); }
+static size_t topk_smem(int64_t U) { return U <= kTopkSmemU ? static_cast<size_t>(U) * sizeof(double) : 0; }
 
-__global__ void k_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
-                                      int64_t* ids) {
+void launch_topk(const TopkParams& p, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkSmemU * sizeof(double));
+        attr = true;
+    }
+    k_topk<<<1, 32 * kTopkWarps, topk_smem(p.U), st>>>(p);
+}
+
+__global__ void __launch_bounds__(512) k_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k,
+                                                              double* rel, double* relw, int64_t* ids) {
     for (int64_t u = threadIdx.x; u < U; u += blockDim.x) {
         double a = 0.0;
         for (int g = 0; g < Gtot; ++g) a += part[u * Gtot + g];
@@ -319,7 +520,13 @@ __global__ void k_rel_topk_standalone(const double* part, int64_t U, int Gtot, i
 
 void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
                                 int64_t* ids, cudaStream_t st) {
-    k_rel_topk_standalone<<<1, 1024, 0, st>>>(part, U, Gtot, k, rel, relw, ids);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_rel_topk_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kTopkSmemU * sizeof(double));
+        attr = true;
+    }
+    k_rel_topk_standalone<<<1, 32 * kTopkWarps, topk_smem(U), st>>>(part, U, Gtot, k, rel, relw, ids);
 }
 
 // --------------------------------------------------------------------------
@@ -545,38 +752,155 @@ __global__ void k_mass(MassParams p) {
     }
 }
 
+// mass_part[j][g0+g] = sum_{hh, m-tile} mass_cta (sharded runs exchange per-group partials)
+__global__ void k_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep,
+                                  int n_mt) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_sel) return;
+    for (int g = 0; g < G; ++g) {
+        double mg = 0.0;
+        for (int hh = 0; hh < rep; ++hh)
+            for (int mt = 0; mt < n_mt; ++mt) mg += mass_cta[((static_cast<int64_t>(g) * rep + hh) * n_mt + mt) * n_sel + j];
+        part[static_cast<int64_t>(j) * Gtot + g0 + g] = mg;
+    }
+}
+
+void launch_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep, int n_mt,
+                            cudaStream_t st) {
+    if (n_sel > 0) k_mass_cta_reduce<<<(n_sel + 63) / 64, 64, 0, st>>>(mass_cta, part, n_sel, G, Gtot, g0, rep, n_mt);
+}
+
 void launch_mass(const MassParams& p, cudaStream_t st) {
     if (p.n_sel > 0) k_mass<<<p.n_sel, 256, 0, st>>>(p);
 }
 
-// frequency decay + masses + capacity (memory.hpp:273-300) + step-boundary
-// peaks (memory.hpp:303-308). Single thread: |hot| <= cap + k_m.
-__global__ void k_lru(LruParams p) {
-    LruState& s = *p.lru;
-    for (int64_t a = 0; a < s.hot_count; ++a) p.freq[p.hot_list[a]] *= p.decay;
-    for (int64_t j = 0; j < p.n_sel; ++j) {
+// TieredStore bookkeeping for one step: lookup tier transfers + counters +
+// trace (memory.hpp:254-267), decay of every hot unit then + attention mass
+// (273-281), capacity eviction of the min-(s_b, id) unit (285-300),
+// residency peaks (303-308). All global reads are issued up front by 8
+// warps; the sequential logic then runs in warp 0 over shared memory.
+constexpr int kLruMax = 512;  // hot_capacity + k_m bound
+__global__ void __launch_bounds__(256) k_lru(LruParams p) {
+    __shared__ int64_t ids[kLruMax];
+    __shared__ double fr[kLruMax];
+    __shared__ int64_t sel[kTopkMax];
+    __shared__ int8_t sel_hot[kTopkMax];
+    __shared__ double sel_f[kTopkMax];
+    __shared__ double mass[kTopkMax];
+    __shared__ LruState st;
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+    if (threadIdx.x == 0) st = *p.lru;
+    __syncthreads();
+    const int64_t n0 = st.hot_count;
+    for (int64_t a = threadIdx.x; a < n0; a += blockDim.x) {
+        const int64_t id = p.hot_list[a];
+        ids[a] = id;
+        fr[a] = p.freq[id];
+    }
+    for (int64_t j = threadIdx.x; j < p.n_sel; j += blockDim.x) {
+        const int64_t id = p.sel[j];
+        sel[j] = id;
+        sel_hot[j] = p.hot[id];
+        sel_f[j] = p.freq[id];
+    }
+    // attention masses of the retrieved units (engine.hpp:271-283)
+    for (int64_t j = warp; j < p.n_mass; j += blockDim.x / 32) {
         double m = 0.0;
-        for (int g = 0; g < p.Gtot; ++g) m += p.mass_part[j * p.Gtot + g];
-        p.freq[p.sel[j]] += m / static_cast<double>(p.H_total);
-    }
-    while (s.hot_count > p.cap) {
-        int64_t worst = 0;
-        for (int64_t a = 1; a < s.hot_count; ++a) {
-            const int64_t ia = p.hot_list[a], iw = p.hot_list[worst];
-            if (p.freq[ia] < p.freq[iw] || (p.freq[ia] == p.freq[iw] && ia < iw)) worst = a;
+        if (p.mass_src == 0) {
+            if (lane == 0)
+                for (int g = 0; g < p.Gtot; ++g) m += p.mass_part[j * p.Gtot + g];
+        } else {
+            const int nt = p.G * p.rep * p.n_mt;  // flattened (g, hh, m-tile) in order
+            for (int t = lane; t < nt; t += 32) m += p.mass_cta[static_cast<int64_t>(t) * p.n_sel + j];
+            m = warp_sum_d(m);
         }
-        p.hot[p.hot_list[worst]] = 0;
-        p.hot_list[worst] = p.hot_list[s.hot_count - 1];
-        s.hot_count--;
-        s.evictions++;
+        if (lane == 0) mass[j] = m / static_cast<double>(p.H_total);
     }
-    if (s.hot_count > s.peak_hot_units) s.peak_hot_units = s.hot_count;
+    __syncthreads();
+    if (warp != 0) return;
+    // 1. lookup bookkeeping, ids ascending as returned by lookup
+    int64_t n = n0;
+    if (lane == 0) {
+        for (int64_t j = 0; j < p.n_sel; ++j) {
+            const int64_t id = sel[j];
+            st.requested++;
+            int64_t* tr = p.trace + 3 * st.trace_count;
+            tr[0] = p.step;
+            tr[1] = id;
+            tr[2] = sel_hot[j] ? 1 : 0;
+            st.trace_count++;
+            if (sel_hot[j]) {
+                st.hits++;
+            } else {
+                st.misses++;
+                st.loads++;
+                p.hot[id] = 1;
+                ids[n] = id;
+                fr[n] = sel_f[j];
+                ++n;
+            }
+        }
+    }
+    n = __shfl_sync(0xffffffffu, n, 0);
+    __syncwarp();
+    // 2. decay every hot unit, 3. add this step's masses
+    for (int64_t a = lane; a < n; a += 32) {
+        double f = fr[a] * p.decay;
+        for (int64_t j = 0; j < p.n_mass; ++j)
+            if (sel[j] == ids[a]) f += mass[j];
+        fr[a] = f;
+    }
+    __syncwarp();
+    // 4. capacity
+    int64_t cnt = n;
+    while (cnt > p.cap) {
+        double bv = INFINITY;
+        int64_t bi = INT64_MAX, ba = -1;
+        for (int64_t a = lane; a < cnt; a += 32)
+            if (fr[a] < bv || (fr[a] == bv && ids[a] < bi)) {
+                bv = fr[a];
+                bi = ids[a];
+                ba = a;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int64_t oa = __shfl_xor_sync(0xffffffffu, ba, o);
+            if (ov < bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+                ba = oa;
+            }
+        }
+        if (lane == 0) {
+            p.hot[bi] = 0;
+            p.freq[bi] = bv;  // s_b persists in the cold tier
+            ids[ba] = ids[cnt - 1];
+            fr[ba] = fr[cnt - 1];
+            st.evictions++;
+        }
+        --cnt;
+        __syncwarp();
+    }
+    // 5. write back + peaks
     int64_t bytes = 0;
-    for (int64_t a = 0; a < s.hot_count; ++a) bytes += p.bytes_per_token * p.unit_len[p.hot_list[a]];
-    if (bytes > s.peak_hot_bytes) s.peak_hot_bytes = bytes;
+    for (int64_t a = lane; a < cnt; a += 32) {
+        p.hot_list[a] = ids[a];
+        p.freq[ids[a]] = fr[a];
+        bytes += p.bytes_per_token * p.unit_len[ids[a]];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    if (lane == 0) {
+        st.hot_count = cnt;
+        if (cnt > st.peak_hot_units) st.peak_hot_units = cnt;
+        if (bytes > st.peak_hot_bytes) st.peak_hot_bytes = bytes;
+        *p.lru = st;
+    }
 }
 
-void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 1, 0, st>>>(p); }
+void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 256, 0, st>>>(p); }
 
 // --------------------------------------------------------------------------
 // K8 evict + K5 representative-score partials. Popped positions
@@ -584,63 +908,94 @@ void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 1, 0, st>>>(p)
 // the rest are evicted into unit pages (engine.hpp:323-340, UnitPacker::add
 // memory.hpp:59-78). r_m partial per group: k_m . (P[m+L+1] - P[m+1]), i.e.
 // sum over the L following queries of the group's q . k_m (repr_score.hpp:53-67).
+// Grid (token groups of 8, KV group); warp w handles one token.
 template <typename T>
-__global__ void k_evict(EvictParams p) {
-    const int64_t idx = blockIdx.x;
+__global__ void __launch_bounds__(256) k_evict(EvictParams p) {
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const int g = blockIdx.y;
+    // transposed value pages: when this block's 8 tokens are one 8-aligned run
+    // that stays inside one source and one destination page (always the case
+    // for page-aligned units), each value dim moves as one 16 B vector
+    const int64_t idx0 = static_cast<int64_t>(blockIdx.x) * 8;
+    const int64_t pos0 = p.pop0 + idx0;
+    bool fast_v = false;
+    if (p.vl.vt && sizeof(T) == 2 && pos0 % 8 == 0 && idx0 + 8 <= p.n_init + p.n_evict) {
+        const bool all_init = idx0 + 8 <= p.n_init, all_unit = idx0 >= p.n_init;
+        if (all_init) fast_v = true;
+        if (all_unit && (pos0 - p.pend_start) % 8 == 0 && (pos0 - p.pend_start) % p.l_bs <= p.l_bs - 8) fast_v = true;
+    }
+    if (fast_v) {
+        const T* rv = static_cast<const T*>(p.ring_v);
+        for (int c = threadIdx.x; c < p.dv; c += blockDim.x) {
+            const uint4 x = *reinterpret_cast<const uint4*>(rv + p.vl.ring(g, pos0, c));
+            T* dst;
+            if (idx0 < p.n_init) {
+                dst = static_cast<T*>(p.init_v) + p.vl.init(g, pos0, c);
+            } else {
+                const int64_t rel = pos0 - p.pend_start;
+                dst = static_cast<T*>(p.unit_v) + p.vl.unit(p.unit0 + rel / p.l_bs, g, rel % p.l_bs, c);
+            }
+            *reinterpret_cast<uint4*>(dst) = x;
+        }
+    }
+    if (idx >= p.n_init + p.n_evict) return;
     const int64_t pos = p.pop0 + idx;
     const int64_t slot = pos % p.R;
-    const T* rk = static_cast<const T*>(p.ring_k);
-    const T* rkr = static_cast<const T*>(p.ring_krot);
+    const T* rk = static_cast<const T*>(p.ring_k) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
+    const T* rkr = static_cast<const T*>(p.ring_krot) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
     const T* rv = static_cast<const T*>(p.ring_v);
-    if (idx < p.n_init) {
-        T* ik = static_cast<T*>(p.init_k);
-        T* ikr = static_cast<T*>(p.init_krot);
-        T* iv = static_cast<T*>(p.init_v);
-        for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) {
-            const int g = t / p.d, c = t % p.d;
-            ik[(static_cast<int64_t>(g) * p.l_I + pos) * p.d + c] = rk[(static_cast<int64_t>(g) * p.R + slot) * p.d + c];
-            if (p.absolute) ikr[(static_cast<int64_t>(g) * p.l_I + pos) * p.d + c] = rkr[(static_cast<int64_t>(g) * p.R + slot) * p.d + c];
+    T *dk, *dkr;
+    T* dvb;
+    int64_t u = 0, off = 0;
+    const bool to_init = idx < p.n_init;
+    if (to_init) {
+        dk = static_cast<T*>(p.init_k) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d;
+        dkr = p.absolute ? static_cast<T*>(p.init_krot) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d : nullptr;
+        dvb = static_cast<T*>(p.init_v);
+    } else {
+        const int64_t rel = pos - p.pend_start;
+        u = p.unit0 + rel / p.l_bs;
+        off = rel % p.l_bs;
+        dk = static_cast<T*>(p.unit_k) + ((u * p.G + g) * p.l_bs + off) * p.d;
+        dkr = p.absolute ? static_cast<T*>(p.unit_krot) + ((u * p.G + g) * p.l_bs + off) * p.d : nullptr;
+        dvb = static_cast<T*>(p.unit_v);
+    }
+    if ((p.d * sizeof(T)) % 16 == 0) {
+        const int nv = p.d * static_cast<int>(sizeof(T)) / 16;
+        for (int t = lane; t < nv; t += 32) {
+            reinterpret_cast<uint4*>(dk)[t] = reinterpret_cast<const uint4*>(rk)[t];
+            if (dkr) reinterpret_cast<uint4*>(dkr)[t] = reinterpret_cast<const uint4*>(rkr)[t];
         }
-        for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
-            const int g = t / p.dv, c = t % p.dv;
-            iv[p.vl.init(g, pos, c)] = rv[p.vl.ring(g, pos, c)];
-        }
-        return;
-    }
-    const int64_t e = idx - p.n_init;
-    const int64_t rel = pos - p.pend_start;
-    const int64_t u = p.unit0 + rel / p.l_bs, off = rel % p.l_bs;
-    T* uk = static_cast<T*>(p.unit_k);
-    T* ukr = static_cast<T*>(p.unit_krot);
-    T* uv = static_cast<T*>(p.unit_v);
-    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) {
-        const int g = t / p.d, c = t % p.d;
-        const int64_t o = ((u * p.G + g) * p.l_bs + off) * p.d + c;
-        uk[o] = rk[(static_cast<int64_t>(g) * p.R + slot) * p.d + c];
-        if (p.absolute) ukr[o] = rkr[(static_cast<int64_t>(g) * p.R + slot) * p.d + c];
-    }
-    for (int t = threadIdx.x; t < p.G * p.dv; t += blockDim.x) {
-        const int g = t / p.dv, c = t % p.dv;
-        uv[p.vl.unit(u, g, off, c)] = rv[p.vl.ring(g, pos, c)];
-    }
-    // score partials: warp w handles groups w, w + nwarps, ...
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    const int64_t hi = ((pos + p.L + 1) % p.R) * p.G, lo = ((pos + 1) % p.R) * p.G;
-    for (int g = warp; g < p.G; g += nw) {
-        double a = 0.0;
+    } else {
         for (int c = lane; c < p.d; c += 32) {
-            const double w = p.P[(hi + g) * p.d + c] - p.P[(lo + g) * p.d + c];
-            a += static_cast<double>(to_f(rk[(static_cast<int64_t>(g) * p.R + slot) * p.d + c])) * w;
+            dk[c] = rk[c];
+            if (dkr) dkr[c] = rkr[c];
         }
-        a = warp_sum_d(a);
-        if (lane == 0) p.ev_part[e * p.Gtot + p.g0 + g] = a;
     }
+    if (!(p.vl.vt && fast_v)) {
+        for (int c = lane; c < p.dv; c += 32) {
+            const T x = rv[p.vl.ring(g, pos, c)];
+            if (to_init)
+                dvb[p.vl.init(g, pos, c)] = x;
+            else
+                dvb[p.vl.unit(u, g, off, c)] = x;
+        }
+    }
+    if (to_init) return;
+    const int64_t e = idx - p.n_init;
+    const double* Phi = p.P + (((pos + p.L + 1) % p.R) * p.G + g) * p.d;
+    const double* Plo = p.P + (((pos + 1) % p.R) * p.G + g) * p.d;
+    double a = 0.0;
+    for (int c = lane; c < p.d; c += 32) a += static_cast<double>(to_f(rk[c])) * (Phi[c] - Plo[c]);
+    a = warp_sum_d(a);
+    if (lane == 0) p.ev_part[e * p.Gtot + p.g0 + g] = a;
 }
 
 template <typename T>
 void launch_evict(const EvictParams& p, cudaStream_t st) {
     const int64_t n = p.n_init + p.n_evict;
-    if (n > 0) k_evict<T><<<static_cast<unsigned>(n), 256, 0, st>>>(p);
+    if (n > 0) k_evict<T><<<dim3(static_cast<unsigned>((n + 7) / 8), p.G), 256, 0, st>>>(p);
 }
 template void launch_evict<float>(const EvictParams&, cudaStream_t);
 template void launch_evict<bf16>(const EvictParams&, cudaStream_t);
@@ -706,31 +1061,46 @@ __device__ void warp_select(const float* sc, int len, int r_k, int* out) {
 }
 
 template <typename T>
-__global__ void k_select(SelectParams p) {
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t u = p.u0 + static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
-    if (u >= p.u0 + p.n_units) return;
+__global__ void __launch_bounds__(128) k_select(SelectParams p) {
+    __shared__ int idx[32];
+    const int64_t u = p.u0 + blockIdx.x;
     const int len = p.unit_len[u];
-    int idx[32];
-    warp_select(p.unit_scores + u * p.l_bs, len, p.r_k, idx);
     const int take = min(p.r_k, len);
-    if (lane < p.r_k) p.repr_idx[u * p.r_k + lane] = lane < take ? idx[lane] : -1;
+    if (threadIdx.x < 32) {
+        int r[32];
+        warp_select(p.unit_scores + u * p.l_bs, len, p.r_k, r);
+        if (threadIdx.x == 0)
+            for (int k = 0; k < take; ++k) idx[k] = r[k];
+        if (threadIdx.x < p.r_k) p.repr_idx[u * p.r_k + threadIdx.x] = threadIdx.x < take ? r[threadIdx.x] : -1;
+    }
+    __syncthreads();
     const T* uk = static_cast<const T*>(p.unit_k);
     T* rp = static_cast<T*>(p.repr);
-    for (int g = 0; g < p.G; ++g)
-        for (int r = 0; r < p.r_k; ++r)
-            for (int c = lane; c < p.d; c += 32) {
-                // units shorter than r_k (final flush) repeat their last representative row with zero keys
-                const T x = r < take ? uk[((u * p.G + g) * p.l_bs + idx[r]) * p.d + c] : from_f<T>(0.f);
-                rp[((u * p.G + g) * p.r_k + r) * p.d + c] = x;
-            }
+    // repr[u][g][r][:] = key row idx[r] of the unit (memory.hpp:111-123);
+    // units shorter than r_k (final flush) get zero rows, which add 0 to relevance
+    if ((p.d * sizeof(T)) % 16 == 0) {
+        const int nv = p.d * static_cast<int>(sizeof(T)) / 16;
+        const int n = p.G * p.r_k * nv;
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+            const int g = t / (p.r_k * nv), rem = t % (p.r_k * nv), r = rem / nv, c = rem % nv;
+            uint4 x = make_uint4(0, 0, 0, 0);
+            if (r < take) x = reinterpret_cast<const uint4*>(uk + ((u * p.G + g) * p.l_bs + idx[r]) * p.d)[c];
+            reinterpret_cast<uint4*>(rp + ((u * p.G + g) * p.r_k + r) * p.d)[c] = x;
+        }
+        return;
+    }
+    const int n = p.G * p.r_k * p.d;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const int g = t / (p.r_k * p.d), rem = t % (p.r_k * p.d), r = rem / p.d, c = rem % p.d;
+        rp[((u * p.G + g) * p.r_k + r) * p.d + c] =
+            r < take ? uk[((u * p.G + g) * p.l_bs + idx[r]) * p.d + c] : from_f<T>(0.f);
+    }
 }
 
 template <typename T>
 void launch_select(const SelectParams& p, cudaStream_t st) {
     if (p.n_units <= 0) return;
-    const int warps = 4;
-    k_select<T><<<static_cast<unsigned>((p.n_units + warps - 1) / warps), warps * 32, 0, st>>>(p);
+    k_select<T><<<static_cast<unsigned>(p.n_units), 128, 0, st>>>(p);
 }
 template void launch_select<float>(const SelectParams&, cudaStream_t);
 template void launch_select<bf16>(const SelectParams&, cudaStream_t);

@@ -52,6 +52,8 @@ struct PrepParams {
     void* ring_v;
     double* P;           // [R][G][d]
     double* chunk_qsum;  // [G][d]
+    float2* rtab;        // [lx][d/2] rotation factors of the chunk positions (scratch)
+    double* qs;          // [lx][G][d] per-token group query sums (scratch)
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
     VLayout vl;
@@ -69,13 +71,8 @@ struct LookupParams {
 struct TopkParams {
     const double* part;  // [U][Gtot]
     double* rel;         // [U]
-    double* relw;        // [U] scratch
     int64_t* sel;        // [n_sel] ascending
-    int8_t* hot;         // [U]
-    int64_t* hot_list;   // [cap + k_m + 1]
-    LruState* lru;
-    int64_t* trace;      // [trace_cap][3]: step, unit, hit
-    int64_t U, n_sel, step;
+    int64_t U, n_sel;
     int Gtot;
 };
 
@@ -98,6 +95,7 @@ struct AttnParams {
     float* mass_m;
     float* row_m;   // [H][lx]
     float* row_l;
+    double* mass_cta;  // [H][n_mt][n_sel] (tcgen05 path)
     int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;
@@ -115,16 +113,21 @@ struct MassParams {
     int n_sel, H, G, Gtot, g0, rep;
 };
 
+// One step of TieredStore bookkeeping after the attention: the lookup's
+// tier transfers/counters/trace (memory.hpp:254-267), update_frequency
+// (273-281), enforce_capacity (285-300) and note_step_boundary (303-308).
 struct LruParams {
-    const double* mass_part;  // [n_sel][Gtot]
+    const double* mass_part;  // [n_sel][Gtot]            (mass_src 0)
+    const double* mass_cta;   // [H][n_mt][n_sel] per CTA (mass_src 1)
     const int64_t* sel;
     double* freq;       // [U]
     int8_t* hot;        // [U]
     int64_t* hot_list;
     const int32_t* unit_len;
     LruState* lru;
-    int64_t n_sel, cap;
-    int Gtot, H_total;
+    int64_t* trace;     // [trace_cap][3]
+    int64_t n_sel, n_mass, cap, step;
+    int Gtot, G, rep, n_mt, H_total, mass_src;
     double decay;
     int64_t bytes_per_token;
 };
@@ -169,6 +172,8 @@ void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
 template <typename T> void launch_attn_simt(const AttnParams& p, cudaStream_t st);
 void launch_mass(const MassParams& p, cudaStream_t st);
+void launch_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep, int n_mt,
+                            cudaStream_t st);
 void launch_lru(const LruParams& p, cudaStream_t st);
 template <typename T> void launch_evict(const EvictParams& p, cudaStream_t st);
 void launch_finalize(const FinalizeParams& p, cudaStream_t st);

@@ -116,6 +116,28 @@ class StreamEngine:
             outs.append(self.encode_chunk(q[off:off + c], k[off:off + c], v[off:off + c], layer))
         return torch.cat(outs, 0)
 
+    def encode_stream(self, q, k, v, out=None, layer=0, stream=None) -> torch.Tensor:
+        """Whole-sequence feed through the C-ABI in one call (graph-replayed
+        chunk schedule); q/k/v/out device tensors."""
+        self._check_inputs(q, k, v)
+        n = q.shape[0]
+        if out is None:
+            out = torch.empty((n, self.n_heads_local, self.shape.value_dim), dtype=self.dtype, device=self.device)
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        check(lib().infllm_encode_stream(self.h, layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), n, out.data_ptr(),
+                                         st))
+        return out
+
+    def encode_stream_host(self, q, k, v, out, layer=0, stream=None):
+        """Host-buffer feed (pinned CPU tensors q/k/v/out) through the C-ABI."""
+        for t in (q, k, v, out):
+            if t.device.type != "cpu" or t.dtype != self.dtype or not t.is_contiguous():
+                raise ValueError("host tensors must be contiguous CPU tensors of the engine dtype")
+        st = (stream or torch.cuda.current_stream(self.device)).cuda_stream
+        check(lib().infllm_encode_stream_host(self.h, layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), q.shape[0],
+                                              out.data_ptr(), st))
+        return out
+
     def finish(self):
         """StreamEngine::finish (engine.hpp:115-119)."""
         check(lib().infllm_finish(self.h, torch.cuda.current_stream(self.device).cuda_stream))

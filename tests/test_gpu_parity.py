@@ -154,3 +154,30 @@ def test_tc_vs_simt_c2_shape():
         got.append(oeng.step(q[off:off + 512], k[off:off + 512], v[off:off + 512]).out)
     want = np.concatenate(got, 0)
     assert rel_err(outs[0][0], want) < 2e-2
+
+
+def test_encode_stream_graph_matches_chunks():
+    """infllm_encode_stream (graph-captured chunk schedule, replayed) and the
+    host-buffer variant reproduce the per-chunk encode_chunk results exactly."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    cfg = dict(chunk_size=256, unit_size=128, n_repr=4, local_size=1024, init_size=128, n_lookup=8, hot_capacity=12)
+    n = 5000
+    q, k, v = gaussian_inputs(31, n, 8, 2, 128, scale=0.3, bf16=True)
+    qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+    shape = ModelShape.make(n_heads=8, n_kv_heads=2, head_dim=128)
+    ref_eng = StreamEngine(EngineConfig.make(**cfg), shape, dtype=torch.bfloat16)
+    ref = ref_eng.feed(qt, kt, vt)
+    eng = StreamEngine(EngineConfig.make(**cfg), shape, dtype=torch.bfloat16)
+    for rep in range(3):  # capture, then replays from a reset state
+        eng.reset()
+        got = eng.encode_stream(qt, kt, vt)
+        assert torch.equal(got, ref), f"replay {rep}"
+        assert eng.metrics() == ref_eng.metrics()
+        assert eng.trace() == ref_eng.trace()
+    hq, hk, hv = [x.cpu().pin_memory() for x in (qt, kt, vt)]
+    hout = torch.empty((n, 8, 128), dtype=torch.bfloat16).pin_memory()
+    eng.reset()
+    eng.encode_stream_host(hq, hk, hv, hout)
+    torch.cuda.synchronize()
+    assert torch.equal(hout, ref.cpu())
