@@ -383,35 +383,61 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             mbar_wait(s_full + b, (j >> 1) & 1);
             tc_fence_after();
             float x[128];
+            {
+                uint32_t r0[32], r1[32], r2[32], r3[32];
+                tmem_ld32(tS, r0);
+                tmem_ld32(tS + 32, r1);
+                tmem_ld32(tS + 64, r2);
+                tmem_ld32(tS + 96, r3);
+                tmem_wait_ld_r(r0);
+                tmem_wait_ld_r(r1);
+                tmem_wait_ld_r(r2);
+                tmem_wait_ld_r(r3);
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-                uint32_t r[32];
-                tmem_ld32(tS + 32 * c4, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) x[32 * c4 + jj] = __uint_as_float(r[jj]);
+                for (int jj = 0; jj < 32; ++jj) {
+                    x[jj] = __uint_as_float(r0[jj]);
+                    x[32 + jj] = __uint_as_float(r1[jj]);
+                    x[64 + jj] = __uint_as_float(r2[jj]);
+                    x[96 + jj] = __uint_as_float(r3[jj]);
+                }
             }
             // valid key columns [lo, kmax); staircase columns [lo, cmax) use the clamped product
             int kmax = t.hi;
             if (t.src == SRC_RING) kmax = static_cast<int>(imax64(t.lo, imin64(t.hi, qp - t.key0 + 1)));
             if (t.mode == MODE_MIXED) {
                 const int cmax = static_cast<int>(imax64(0, imin64(128, qp - a.L - t.key0)));
+                uint32_t r0[32], r1[32], r2[32], r3[32];
+                tmem_ld32(tl + kColSX, r0);
+                tmem_ld32(tl + kColSX + 32, r1);
+                tmem_ld32(tl + kColSX + 64, r2);
+                tmem_ld32(tl + kColSX + 96, r3);
+                tmem_wait_ld_r(r0);
+                tmem_wait_ld_r(r1);
+                tmem_wait_ld_r(r2);
+                tmem_wait_ld_r(r3);
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    uint32_t r[32];
-                    tmem_ld32(tl + kColSX + 32 * c4, r);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int jj = 0; jj < 32; ++jj)
-                        if (32 * c4 + jj < cmax) x[32 * c4 + jj] = __uint_as_float(r[jj]);
+                for (int jj = 0; jj < 32; ++jj) {
+                    if (jj < cmax) x[jj] = __uint_as_float(r0[jj]);
+                    if (32 + jj < cmax) x[32 + jj] = __uint_as_float(r1[jj]);
+                    if (64 + jj < cmax) x[64 + jj] = __uint_as_float(r2[jj]);
+                    if (96 + jj < cmax) x[96 + jj] = __uint_as_float(r3[jj]);
                 }
             }
-            float mt = -INFINITY;
+            // masks only on edge tiles (partial pages, causal diagonal)
+            if (__any_sync(0xffffffffu, t.lo > 0 || kmax < 128)) {
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                x[c] = (c >= t.lo && c < kmax) ? x[c] * sl2 : -INFINITY;
-                mt = fmaxf(mt, x[c]);
+                for (int c = 0; c < 128; ++c)
+                    if (c < t.lo || c >= kmax) x[c] = -INFINITY;
             }
+            float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 128; c += 4) {
+                mx0 = fmaxf(mx0, x[c]);
+                mx1 = fmaxf(mx1, x[c + 1]);
+                mx2 = fmaxf(mx2, x[c + 2]);
+                mx3 = fmaxf(mx3, x[c + 3]);
+            }
+            const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;  // scale > 0 commutes with max
             const float m_new = fmaxf(m_run, mt);
             const bool need = m_new > m_run + 8.0f;
             if (__any_sync(0xffffffffu, need)) {
@@ -424,7 +450,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                     for (int c4 = 0; c4 < 4; ++c4) {
                         uint32_t r[32];
                         tmem_ld32(tl + kColO + 32 * c4, r);
-                        tmem_wait_ld();
+                        tmem_wait_ld_r(r);
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) * corr);
                         tmem_st32(tl + kColO + 32 * c4, r);
@@ -433,12 +459,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 }
                 m_run = m_new;
             }
-            float rs = 0.f;
+            // p = 2^(s * scale * log2e - m): one FFMA + one MUFU.EX2 per score
+            const float neg = (m_run == -INFINITY) ? 0.f : -m_run;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-                x[c] = (x[c] == -INFINITY) ? 0.f : ex2(x[c] - m_run);
-                rs += x[c];
+            for (int c = 0; c < 128; c += 4) {
+                x[c] = ex2(fmaf(x[c], sl2, neg));
+                x[c + 1] = ex2(fmaf(x[c + 1], sl2, neg));
+                x[c + 2] = ex2(fmaf(x[c + 2], sl2, neg));
+                x[c + 3] = ex2(fmaf(x[c + 3], sl2, neg));
+                s0 += x[c];
+                s1 += x[c + 1];
+                s2 += x[c + 2];
+                s3 += x[c + 3];
             }
+            const float rs = (s0 + s1) + (s2 + s3);
             l_run += rs;
             if (t.slot >= 0 && a.want_mass) {
                 if (mass_in_kernel) {
@@ -471,7 +506,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         for (int c4 = 0; c4 < 4; ++c4) {
             uint32_t r[32];
             tmem_ld32(tl + kColO + 32 * c4, r);
-            tmem_wait_ld();
+            tmem_wait_ld_r(r);
             if (row_ok) {
                 uint32_t w[16];
 #pragma unroll
