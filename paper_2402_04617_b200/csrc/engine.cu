@@ -139,6 +139,18 @@ struct infllm_engine {
     bool use_tc = false;
     bool tc_disabled = false;
     VLayout vl{};
+    // two-stream step pipeline: the side stream runs prep/lookup/top-k and
+    // evict/finalize/select, the caller's (main) stream attention + LRU; step
+    // k's front half overlaps step k-1's attention. Scratch written by the
+    // side stream and read by the main stream is double-buffered by k % 2.
+    cudaStream_t side_stream = nullptr;
+    cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
+    int64_t seq = 0;                 // engine-wide step counter
+    int64_t lru_seq[2] = {-1, -1};   // step that last recorded e_lru[b]
+    int64_t capture_seq0 = -1;       // first step of the graph being captured (-1: not capturing)
+    size_t qa_half = 0;              // bytes of one qa/qc buffer
+    int64_t debug_skip = 0;          // timing experiments only: bit0 attention, bit1 lookup+top-k,
+                                     // bit2 evict/finalize/select, bit3 prep, bit4 LRU (results invalid)
 
     // scratch shared by layers (layers run sequentially on one stream)
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb;
@@ -146,7 +158,7 @@ struct infllm_engine {
     struct Layer {
         int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
         int64_t n_units = 0, pend_start = 0, pend_count = 0;
-        int64_t trace_count = 0, last_n_sel = 0;
+        int64_t trace_count = 0, last_n_sel = 0, last_b = 0;
         int64_t unit_cap = 0, trace_cap = 0;
         std::vector<int64_t> unit_start;
         std::vector<int32_t> unit_len;
@@ -159,19 +171,20 @@ struct infllm_engine {
 
     // host stream arithmetic of a layer (everything a step derives on the host)
     struct HostState {
-        int64_t n_fed, step, local_start, init_len, n_units, pend_start, pend_count, trace_count, last_n_sel;
+        int64_t n_fed, step, local_start, init_len, n_units, pend_start, pend_count, trace_count, last_n_sel, last_b;
         std::vector<int64_t> unit_start;
         std::vector<int32_t> unit_len;
         bool operator==(const HostState& o) const {
             return n_fed == o.n_fed && step == o.step && local_start == o.local_start && init_len == o.init_len &&
                    n_units == o.n_units && pend_start == o.pend_start && pend_count == o.pend_count &&
-                   trace_count == o.trace_count && last_n_sel == o.last_n_sel && unit_start == o.unit_start &&
+                   trace_count == o.trace_count && last_n_sel == o.last_n_sel && last_b == o.last_b &&
+                   unit_start == o.unit_start &&
                    unit_len == o.unit_len;
         }
     };
     static HostState save(const Layer& L) {
-        return HostState{L.n_fed,      L.step,        L.local_start, L.init_len,   L.n_units,   L.pend_start,
-                         L.pend_count, L.trace_count, L.last_n_sel,  L.unit_start, L.unit_len};
+        return HostState{L.n_fed,      L.step,        L.local_start, L.init_len, L.n_units,    L.pend_start,
+                         L.pend_count, L.trace_count, L.last_n_sel,  L.last_b,   L.unit_start, L.unit_len};
     }
     static void restore(Layer& L, const HostState& h) {
         L.n_fed = h.n_fed;
@@ -183,6 +196,7 @@ struct infllm_engine {
         L.pend_count = h.pend_count;
         L.trace_count = h.trace_count;
         L.last_n_sel = h.last_n_sel;
+        L.last_b = h.last_b;
         L.unit_start = h.unit_start;
         L.unit_len = h.unit_len;
     }
@@ -202,6 +216,7 @@ struct infllm_engine {
         int64_t launches = 0;
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, lookup_ev;
         int64_t replays_in_window = 0;
+        int64_t steps = 0;
     };
     std::vector<GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
@@ -240,6 +255,7 @@ struct infllm_engine {
 
     void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.unit_cap) return;
+        if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.unit_cap, 16});
         L.unit_k.grow(cap * unit_elems_k() * esz, st);
         if (cfg.position_mode == INFLLM_POSITION_ABSOLUTE) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
@@ -262,9 +278,17 @@ struct infllm_engine {
 
     void ensure_trace(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.trace_cap) return;
+        if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.trace_cap, 1024});
         L.trace.grow(cap * 3 * sizeof(int64_t), st);
         L.trace_cap = cap;
+    }
+
+    // make `st` wait for everything queued on the side stream
+    void join_side(cudaStream_t st) {
+        ck(cudaEventRecord(e_side, side_stream), "record");
+        ck(cudaStreamWaitEvent(st, e_side, 0), "wait");
+        lru_seq[0] = lru_seq[1] = -1;
     }
 
     void gather(double* buf, int64_t rows, cudaStream_t st) {
@@ -278,9 +302,12 @@ struct infllm_engine {
         return use_tc && !tc_disabled;
     }
 
+    // fork: the side stream starts from the caller's current point on `st`
+    // (inputs written there); inputs_ready: additionally wait for this event
+    // (host-buffer path). Within one encode_stream only the first step forks.
     template <typename T>
     void step(int li, const void* q, const void* k, const void* v, int64_t lx, bool decode, void* out,
-              cudaStream_t st) {
+              cudaStream_t st, bool fork = true, cudaEvent_t inputs_ready = nullptr) {
         if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
         if (lx < 1) throw StreamError("step: empty batch");
         if (!decode && lx > cfg.chunk_size) throw StreamError("encode_chunk: batch exceeds chunk_size");
@@ -299,13 +326,30 @@ struct infllm_engine {
         ensure_units(L, L.n_units + completed + 1, st);
         ensure_trace(L, L.trace_count + n_sel, st);
 
+        // stream fork: side waits for the caller's point (inputs) and for the
+        // main-stream step k-2 that last read this parity's buffers
+        const int64_t kseq = seq++;
+        const int b = static_cast<int>(kseq & 1);
+        cudaStream_t main = st, side = side_stream;
+        if (fork) {
+            ck(cudaEventRecord(e_call, main), "record");
+            ck(cudaStreamWaitEvent(side, e_call, 0), "wait");
+        }
+        if (inputs_ready) ck(cudaStreamWaitEvent(side, inputs_ready, 0), "wait");
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+            ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");
+        void* qa_b = static_cast<uint8_t*>(qa.p) + b * qa_half;
+        void* qc_b = static_cast<uint8_t*>(qc.p) + b * qa_half;
+        int64_t* sel_b = L.sel.as<int64_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
+        st = side;
+
         // K7: ring append, RoPE, prefix sums
         PrepParams pp{};
         pp.q = q;
         pp.k = k;
         pp.v = v;
-        pp.qa = qa.p;
-        pp.qc = qc.p;
+        pp.qa = qa_b;
+        pp.qc = qc_b;
         pp.ring_k = L.ring_k.p;
         pp.ring_krot = L.ring_krot.p;
         pp.ring_v = L.ring_v.p;
@@ -325,7 +369,7 @@ struct infllm_engine {
         pp.vl = vl;
         pp.rtab = rtab.as<float2>();
         pp.qs = qsb.as<double>();
-        launch_prep<T>(pp, st);
+        if (!(debug_skip & 8)) launch_prep<T>(pp, st);
         launches += (d % 8 == 0 && dv % 8 == 0) ? 3 : 2;
 
         // K1 + K2: lookup (memory.hpp:239-269)
@@ -345,16 +389,16 @@ struct infllm_engine {
             lp.g0 = g0;
             lp.r_k = static_cast<int>(cfg.n_repr);
             lp.d = d;
-            launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            if (!(debug_skip & 2)) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             gather(L.lookup_part.as<double>(), L.n_units, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
             tp.rel = L.rel.as<double>();
-            tp.sel = L.sel.as<int64_t>();
+            tp.sel = sel_b;
             tp.U = L.n_units;
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
-            launch_topk(tp, st);
+            if (!(debug_skip & 2)) launch_topk(tp, st);
             launches += 2;
             if (prof) {
                 record(evp.second, st);
@@ -362,11 +406,15 @@ struct infllm_engine {
             }
         }
 
+        ck(cudaEventRecord(e_topk, side), "record");
+        ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");
+        st = main;
+
         // K3: attention over [initial | retrieved | local | chunk] (attention.hpp:116-230)
         const bool want_mass = do_lookup && n_sel > 0;
         AttnParams ap{};
-        ap.qa = qa.p;
-        ap.qc = qc.p;
+        ap.qa = qa_b;
+        ap.qc = qc_b;
         ap.out = out;
         ap.init_k = L.init_k.p;
         ap.init_krot = L.init_krot.p;
@@ -375,7 +423,7 @@ struct infllm_engine {
         ap.unit_krot = L.unit_krot.p;
         ap.unit_v = L.unit_v.p;
         ap.unit_len = L.ulen.as<int32_t>();
-        ap.sel = L.sel.as<int64_t>();
+        ap.sel = sel_b;
         ap.ring_k = L.ring_k.p;
         ap.ring_krot = L.ring_krot.p;
         ap.ring_v = L.ring_v.p;
@@ -410,7 +458,8 @@ struct infllm_engine {
             record(eva.first, st);
         }
         if constexpr (std::is_same_v<T, bf16>) {
-            if (tc_eligible(lx)) {
+            if (debug_skip & 1) {
+            } else if (tc_eligible(lx)) {
                 launches += launch_attn_tc(ap, st);
             } else {
                 launch_attn_simt<T>(ap, st);
@@ -461,7 +510,7 @@ struct infllm_engine {
         LruParams lp{};
         lp.mass_part = L.mass_part.as<double>();
         lp.mass_cta = mass_cta.as<double>();
-        lp.sel = L.sel.as<int64_t>();
+        lp.sel = sel_b;
         lp.freq = L.freq.as<double>();
         lp.hot = L.hot.as<int8_t>();
         lp.hot_list = L.hot_list.as<int64_t>();
@@ -480,8 +529,11 @@ struct infllm_engine {
         lp.mass_src = mass_src;
         lp.decay = cfg.decay;
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
-        launch_lru(lp, st);
+        if (!(debug_skip & 16)) launch_lru(lp, st);
         ++launches;
+        ck(cudaEventRecord(e_lru[b], main), "record");
+        lru_seq[b] = kseq;
+        st = side;
 
         // window roll: init pinning, eviction, representative scoring, packing
         if (overflow > 0) {
@@ -516,7 +568,7 @@ struct infllm_engine {
             ep.l_bs = static_cast<int>(cfg.unit_size);
             ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
             ep.vl = vl;
-            launch_evict<T>(ep, st);
+            if (!(debug_skip & 4)) launch_evict<T>(ep, st);
             ++launches;
             if (to_evict > 0) {
                 gather(L.ev_part.as<double>(), to_evict, st);
@@ -530,7 +582,7 @@ struct infllm_engine {
                 fp.L = cfg.local_size;
                 fp.Gtot = Gt;
                 fp.l_bs = static_cast<int>(cfg.unit_size);
-                launch_finalize(fp, st);
+                if (!(debug_skip & 4)) launch_finalize(fp, st);
                 ++launches;
             }
             if (completed > 0) {
@@ -546,7 +598,7 @@ struct infllm_engine {
                 sp.r_k = static_cast<int>(cfg.n_repr);
                 sp.d = d;
                 sp.l_bs = static_cast<int>(cfg.unit_size);
-                launch_select<T>(sp, st);
+                if (!(debug_skip & 4)) launch_select<T>(sp, st);
                 ++launches;
                 for (int64_t c = 0; c < completed; ++c) {
                     L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
@@ -561,6 +613,7 @@ struct infllm_engine {
         }
         L.trace_count += n_sel;
         L.last_n_sel = n_sel;
+        L.last_b = b;
         L.n_fed += lx;
         L.step += 1;
         ck(cudaGetLastError(), "kernel launch");
@@ -576,7 +629,7 @@ struct infllm_engine {
         for (int64_t off = 0; off < n; off += cfg.chunk_size) {
             const int64_t lx = std::min<int64_t>(cfg.chunk_size, n - off);
             step<T>(li, at(q, off, Hs * d), at(k, off, Gs * d), at(v, off, Gs * dv), lx, false,
-                    const_cast<void*>(at(out, off, Hs * dv)), st);
+                    const_cast<void*>(at(out, off, Hs * dv)), st, off == 0);
         }
     }
 
@@ -618,9 +671,8 @@ struct infllm_engine {
             if (t + kNB - 1 < nch) h2d(t + kNB - 1);
             const int64_t off = t * C, lx = std::min<int64_t>(C, n - off);
             const int b = static_cast<int>(t % kNB);
-            ck(cudaStreamWaitEvent(st, ev_in[t], 0), "wait");
             if (t >= kNB) ck(cudaStreamWaitEvent(st, ev_out[t - kNB], 0), "wait");  // stage_o[b] drained
-            step<T>(li, stage_q[b].p, stage_k[b].p, stage_v[b].p, lx, false, stage_o[b].p, st);
+            step<T>(li, stage_q[b].p, stage_k[b].p, stage_v[b].p, lx, false, stage_o[b].p, st, t == 0, ev_in[t]);
             ck(cudaEventRecord(ev_comp[t], st), "record");
             ck(cudaStreamWaitEvent(d2h_stream, ev_comp[t], 0), "wait");
             ck(cudaMemcpyAsync(const_cast<void*>(at(hout, off, Hs * dv)), stage_o[b].p, lx * Hs * dv * esz,
@@ -692,20 +744,28 @@ struct infllm_engine {
             capturing = true;
             cap_attn_ev = &g.attn_ev;
             cap_lookup_ev = &g.lookup_ev;
+            const int64_t seq0 = seq;
             ck(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+            capture_seq0 = seq;
             try {
                 if (host)
                     run_chunks_host<T>(li, q, k, v, n, out, cap_stream);
                 else
                     run_chunks<T>(li, q, k, v, n, out, cap_stream);
+                join_side(cap_stream);
             } catch (...) {
                 capturing = false;
+                capture_seq0 = -1;
                 cudaStreamEndCapture(cap_stream, &graph);
                 if (graph) cudaGraphDestroy(graph);
                 restore(L, cur);
+                seq = seq0;
                 throw;
             }
             capturing = false;
+            capture_seq0 = -1;
+            g.steps = seq - seq0;
+            seq = seq0;
             ck(cudaStreamEndCapture(cap_stream, &graph), "end capture");
             ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
             cudaGraphDestroy(graph);
@@ -716,7 +776,9 @@ struct infllm_engine {
             graphs.push_back(std::move(g));
             ge = &graphs.back();
         }
+        join_side(st);  // the graph starts from a quiet side stream and joins it at its end
         ck(cudaGraphLaunch(ge->exec, st), "graph launch");
+        seq += ge->steps;
         restore(L, ge->after);
         launches += ge->launches;
         if (prof) ge->replays_in_window++;
@@ -724,6 +786,7 @@ struct infllm_engine {
 
     template <typename T>
     void finish(cudaStream_t st) {  // engine.hpp:115-119, UnitPacker::flush memory.hpp:81-84
+        join_side(st);
         for (auto& L : layers) {
             if (L.pend_count == 0) continue;
             ensure_units(L, L.n_units + 1, st);
@@ -816,7 +879,9 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->dtype = dtype;
         e->device = device;
         e->esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
-        const int64_t need = cfg->local_size + cfg->chunk_size + 1;
+        // ring: the local window, the chunk being attended and the next chunk being
+        // prepared concurrently (two-stream pipeline) never share a slot
+        const int64_t need = cfg->local_size + 2 * cfg->chunk_size + 1;
         e->R = (need + 127) / 128 * 128;
         e->lxp = (cfg->chunk_size + 127) / 128 * 128;
         for (int a = 0; a < e->d / 2; ++a) {  // rotary.hpp:25-30 (RotaryTable::make)
@@ -837,8 +902,12 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         ck(cudaSetDevice(device), "cudaSetDevice");
         cudaStream_t st = nullptr;
         const size_t es = e->esz;
-        e->qa.alloc(static_cast<size_t>(e->Hs) * e->lxp * e->d * es, st);
-        e->qc.alloc(static_cast<size_t>(e->Hs) * e->lxp * e->d * es, st);
+        e->qa_half = static_cast<size_t>(e->Hs) * e->lxp * e->d * es;
+        e->qa.alloc(2 * e->qa_half, st);
+        e->qc.alloc(2 * e->qa_half, st);
+        ck(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking), "side stream");
+        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1]})
+            ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
         e->chunk_qsum.alloc(static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
         e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
@@ -861,7 +930,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.init_v.alloc(static_cast<size_t>(e->Gs) * (e->vl.vt ? e->vl.nI * 128 : ni) * e->dv * es, st);
             L.hot_list.alloc(static_cast<size_t>(cfg->hot_capacity + km + 1) * sizeof(int64_t), st);
             L.lru.alloc(sizeof(LruState), st);
-            L.sel.alloc(km * sizeof(int64_t), st);
+            L.sel.alloc(2 * km * sizeof(int64_t), st);
             L.mass_part.alloc(km * e->Gt * sizeof(double), st);
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
@@ -904,8 +973,10 @@ int infllm_engine_destroy(infllm_engine_t e) {
         }
         for (int b = 0; b < infllm_engine::kNB; ++b)
             for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
-        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream})
+        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream})
             if (s2) cudaStreamDestroy(s2);
+        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1]})
+            if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;
     });
@@ -934,10 +1005,11 @@ int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
 int infllm_engine_reset(infllm_engine_t e, void* stream) {
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
+        e->join_side(st);
         for (auto& L : e->layers) {
             L.n_fed = L.step = L.local_start = L.init_len = 0;
             L.n_units = L.pend_start = L.pend_count = 0;
-            L.trace_count = L.last_n_sel = 0;
+            L.trace_count = L.last_n_sel = L.last_b = 0;
             L.unit_start.clear();
             L.unit_len.clear();
             ck(cudaMemsetAsync(L.P.p, 0, L.P.bytes, st), "memset");
@@ -961,6 +1033,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->tc_disabled = value == 0;
         else if (k == "cuda_graphs")
             e->use_graphs = value != 0;
+        else if (k == "debug_skip")
+            e->debug_skip = value;
         else
             throw ConfigError("unknown option '" + k + "'");
     });
@@ -1030,7 +1104,8 @@ int infllm_retrieved_ids(infllm_engine_t e, int32_t layer, int64_t* host_ids, in
         ck(cudaDeviceSynchronize(), "sync");
         *n_out = L.last_n_sel;
         const int64_t n = std::min(cap, L.last_n_sel);
-        if (n > 0) ck(cudaMemcpy(host_ids, L.sel.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
+        const int64_t* src = L.sel.as<int64_t>() + L.last_b * std::max<int64_t>(e->cfg.n_lookup, 1);
+        if (n > 0) ck(cudaMemcpy(host_ids, src, n * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H");
     });
 }
 
