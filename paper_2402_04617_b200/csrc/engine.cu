@@ -153,7 +153,7 @@ struct infllm_engine {
                                      // bit2 evict/finalize/select, bit3 prep, bit4 LRU (results invalid)
 
     // scratch shared by layers (layers run sequentially on one stream)
-    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb;
+    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, topk_done;
 
     struct Layer {
         int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
@@ -389,8 +389,14 @@ struct infllm_engine {
             lp.g0 = g0;
             lp.r_k = static_cast<int>(cfg.n_repr);
             lp.d = d;
+            // single shard: relevance + exact top-k fused into one launch
+            lp.fused = (Gs == Gt && L.n_units <= 256 * 8) ? 1 : 0;  // last lookup block (256 thr x 8 ids)
+            lp.rel = L.rel.as<double>();
+            lp.sel = sel_b;
+            lp.done = topk_done.as<unsigned int>();
+            lp.n_sel = n_sel;
             if (!(debug_skip & 2)) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
-            gather(L.lookup_part.as<double>(), L.n_units, st);
+            if (!lp.fused) gather(L.lookup_part.as<double>(), L.n_units, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
             tp.rel = L.rel.as<double>();
@@ -398,8 +404,8 @@ struct infllm_engine {
             tp.U = L.n_units;
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
-            if (!(debug_skip & 2)) launch_topk(tp, st);
-            launches += 2;
+            if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
+            launches += lp.fused ? 1 : 2;
             if (prof) {
                 record(evp.second, st);
                 (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
@@ -914,6 +920,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->mass_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
         e->row_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
         e->row_l.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
+        e->topk_done.alloc(sizeof(unsigned int), st);
         e->rtab.alloc(static_cast<size_t>(cfg->chunk_size) * std::max(1, e->d / 2) * sizeof(float2), st);
         e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
         e->mass_cta.alloc(static_cast<size_t>(e->Hs) * (e->lxp / 128) * km * sizeof(double), st);
@@ -944,7 +951,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         if (!e) return;
         cudaDeviceSynchronize();
         cudaStream_t st = nullptr;
-        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb}) b->release(st);
+        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->topk_done}) b->release(st);
         for (auto& L : e->layers)
             for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,

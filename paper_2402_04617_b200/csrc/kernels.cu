@@ -311,80 +311,102 @@ template void launch_prep<float>(const PrepParams&, cudaStream_t);
 template void launch_prep<bf16>(const PrepParams&, cudaStream_t);
 
 // --------------------------------------------------------------------------
-// K1 lookup score: part[u][g] = sum_{r,c} qsum[g][c] * repr[u][g][r][c] in
-// fp64 (TieredStore::relevance_all, memory.hpp:217-234). One warp per unit;
-// per group, lane L owns a fixed contiguous run of the group's r_k*d
-// elements, then an xor-tree: the association is independent of how groups
-// are sharded across GPUs.
+// K1 lookup score: per (unit, group) the fp64 dot of the chunk's group query
+// sum with the unit's r_k representative keys (TieredStore::relevance_all,
+// memory.hpp:217-234). One warp per unit; per group, lane L owns the fixed
+// contiguous run [L*per, (L+1)*per) of the group's r_k*d elements, then an
+// xor-tree: the association does not depend on how groups are sharded. In the
+// single-shard (fused) mode the warp sums the groups in order 0..G-1 into
+// rel[u] and the last block to finish runs the exact top-k (K2) over all units.
+__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out);
+
+template <typename T, int kPer>
+__device__ __forceinline__ double group_dot(const T* src, const double* qg, int lane, int d) {
+    // elements e = lane*kPer + j of the [r_k][d] run; dim = e % d
+    double a = 0.0;
+    const int e0 = lane * kPer;
+    int c = e0 % d;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        a += qg[c] * static_cast<double>(to_f(src[e0 + j]));
+        if (++c == d) c = 0;
+    }
+    return warp_sum_d(a);
+}
+
 template <typename T>
-__global__ void k_lookup(LookupParams p) {
+__global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
     extern __shared__ double sq[];  // [G][d]
     for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[t] = p.qsum[t];
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t u = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
-    if (u >= p.U) return;
-    const int E = p.r_k * p.d;
-    const int per = (E + 31) / 32;
-    const T* base = static_cast<const T*>(p.repr) + u * p.G * E;
-    for (int g = 0; g < p.G; ++g) {
-        const T* src = base + g * E;
-        const double* qg = sq + g * p.d;
-        double a = 0.0;
-        for (int j = 0; j < per; ++j) {
-            const int e = lane * per + j;
-            if (e < E) a += qg[e % p.d] * static_cast<double>(to_f(src[e]));
+    if (u < p.U) {
+        const int E = p.r_k * p.d;
+        const T* base = static_cast<const T*>(p.repr) + u * p.G * E;
+        double rel = 0.0;
+        if (E == 512 && sizeof(T) == 2) {
+            // 16 bf16 per lane, all groups' loads in flight before the math
+            uint4 buf[16];
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+                if (g < p.G) {
+                    buf[2 * g] = __ldcs(reinterpret_cast<const uint4*>(base + g * 512) + lane * 2);
+                    buf[2 * g + 1] = __ldcs(reinterpret_cast<const uint4*>(base + g * 512) + lane * 2 + 1);
+                }
+            const int c0 = (lane * 16) % p.d;  // 16 | d: the run stays inside one key row
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                if (g >= p.G) break;
+                const double* qg = sq + g * p.d + c0;
+                const bf16* e = reinterpret_cast<const bf16*>(&buf[2 * g]);
+                double a = 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) a += qg[j] * static_cast<double>(__bfloat162float(e[j]));
+                a = warp_sum_d(a);
+                if (p.fused) rel += a;
+                else if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+            }
+            for (int g = 8; g < p.G; ++g) {
+                const double a = group_dot<T, 16>(base + g * E, sq + g * p.d, lane, p.d);
+                if (p.fused) rel += a;
+                else if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+            }
+        } else {
+            const int per = (E + 31) / 32;
+            for (int g = 0; g < p.G; ++g) {
+                const T* src = base + g * E;
+                const double* qg = sq + g * p.d;
+                double a = 0.0;
+                for (int j = 0; j < per; ++j) {
+                    const int e = lane * per + j;
+                    if (e < E) a += qg[e % p.d] * static_cast<double>(to_f(src[e]));
+                }
+                a = warp_sum_d(a);
+                if (p.fused) rel += a;
+                else if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+            }
         }
-        a = warp_sum_d(a);
-        if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+        if (p.fused && lane == 0) p.rel[u] = rel;
     }
-}
-
-// specialised: r_k*d == 512 bf16 (16 elements = 2 x 16B per lane)
-__global__ void k_lookup_bf16_512(LookupParams p) {
-    extern __shared__ double sq[];
-    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[t] = p.qsum[t];
+    if (!p.fused) return;
+    // last block to finish selects the top-k over all units
+    __shared__ bool last;
+    __threadfence();
     __syncthreads();
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t u = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
-    if (u >= p.U) return;
-    const uint4* base = reinterpret_cast<const uint4*>(static_cast<const bf16*>(p.repr) + u * p.G * 512);
-    uint4 buf[16];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        if (g < p.G) {
-            buf[2 * g] = __ldcs(base + g * 64 + lane * 2);
-            buf[2 * g + 1] = __ldcs(base + g * 64 + lane * 2 + 1);
-        }
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-        if (g >= p.G) break;
-        const double* qg = sq + g * p.d;
-        const bf16* e = reinterpret_cast<const bf16*>(&buf[2 * g]);
-        double a = 0.0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) a += qg[(lane * 16 + j) % p.d] * static_cast<double>(__bfloat162float(e[j]));
-        a = warp_sum_d(a);
-        if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
-    }
-    for (int g = 8; g < p.G; ++g) {  // G > 8: generic tail
-        const bf16* src = static_cast<const bf16*>(p.repr) + (u * p.G + g) * 512;
-        const double* qg = sq + g * p.d;
-        double a = 0.0;
-        for (int j = 0; j < 16; ++j) a += qg[(lane * 16 + j) % p.d] * static_cast<double>(__bfloat162float(src[lane * 16 + j]));
-        a = warp_sum_d(a);
-        if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
-    }
+    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+    if (threadIdx.x == 0) *p.done = 0;
 }
 
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
     const int warps = 8;
     const unsigned blocks = static_cast<unsigned>((p.U + warps - 1) / warps);
     const size_t smem = sizeof(double) * p.G * p.d;
-    if (dtype_bf16 && p.r_k * p.d == 512)
-        k_lookup_bf16_512<<<blocks, warps * 32, smem, st>>>(p);
-    else if (dtype_bf16)
+    if (dtype_bf16)
         k_lookup<bf16><<<blocks, warps * 32, smem, st>>>(p);
     else
         k_lookup<float><<<blocks, warps * 32, smem, st>>>(p);
@@ -486,14 +508,143 @@ __device__ void block_topk(const double* rel, double* work, int64_t U, int64_t n
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(512) k_topk(TopkParams p) {
+// Exact top-K by (value desc, id asc) with an MSB-first 8-bit radix select
+// on order-preserving 64-bit keys: 8 histogram passes find the K-th key T;
+// ids with key > T are taken, and the lowest ids among key == T fill the
+// rest. Output ids ascending. Thread t owns the contiguous id range
+// [t*E, t*E+E) so block scans give id order. Works for any blockDim
+// (multiple of 32) with U <= blockDim * kRadixE.
+constexpr int kRadixE = 8;
+__device__ __forceinline__ uint64_t order_key(double v) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nw) wsum[lane] = w;  // inclusive
+    }
+    __syncthreads();
+    const int before = (warp > 0 ? wsum[warp - 1] : 0) + x - v;
+    if (total) *total = wsum[nw - 1];
+    __syncthreads();
+    return before;
+}
+
+__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out) {
+    __shared__ int hist[256];
+    __shared__ int wsum[32];
+    __shared__ uint64_t s_prefix;
+    __shared__ int s_remaining;
+    const int T = blockDim.x;
+    const int E = static_cast<int>((U + T - 1) / T);
+    const int64_t u0 = static_cast<int64_t>(threadIdx.x) * E;
+    uint64_t key[kRadixE];
+#pragma unroll
+    for (int e = 0; e < kRadixE; ++e) key[e] = (e < E && u0 + e < U) ? order_key(rel[u0 + e]) : 0ull;
+    if (threadIdx.x == 0) {
+        s_prefix = 0;
+        s_remaining = static_cast<int>(K);
+    }
+    uint64_t mask = 0;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+#pragma unroll
+        for (int e = 0; e < kRadixE; ++e)
+            if (e < E && u0 + e < U && (key[e] & mask) == prefix) atomicAdd(&hist[(key[e] >> shift) & 255], 1);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            // bins high -> low: lane l owns bins 255-8l .. 248-8l
+            const int lane = threadIdx.x;
+            int c[8], sum = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = hist[255 - 8 * lane - j];
+                sum += c[j];
+            }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int rem = s_remaining;
+            int run = incl - sum;  // count in higher bins
+            int found = -1, above = 0;
+            if (run < rem && incl >= rem) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (found < 0 && run + c[j] >= rem) {
+                        found = 255 - 8 * lane - j;
+                        above = run;
+                    }
+                    run += c[j];
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, found >= 0);
+            const int src = __ffs(m) - 1;
+            found = __shfl_sync(0xffffffffu, found, src);
+            above = __shfl_sync(0xffffffffu, above, src);
+            if (lane == 0) {
+                s_prefix = prefix | (static_cast<uint64_t>(found) << shift);
+                s_remaining = rem - above;
+            }
+        }
+        mask |= 0xFFull << shift;
+        __syncthreads();
+    }
+    const uint64_t Tk = s_prefix;
+    const int need_eq = s_remaining;  // how many of the key == T ids to take (lowest first)
+    int n_eq = 0;
+#pragma unroll
+    for (int e = 0; e < kRadixE; ++e) n_eq += (e < E && u0 + e < U && key[e] == Tk) ? 1 : 0;
+    int eq_before = block_excl_scan(n_eq, wsum, nullptr);
+    int n_sel = 0;
+#pragma unroll
+    for (int e = 0; e < kRadixE; ++e) {
+        if (!(e < E && u0 + e < U)) continue;
+        if (key[e] > Tk) ++n_sel;
+        else if (key[e] == Tk && eq_before++ < need_eq) ++n_sel;
+    }
+    int pos = block_excl_scan(n_sel, wsum, nullptr);
+    eq_before = eq_before - n_eq;  // restore for the write pass
+#pragma unroll
+    for (int e = 0; e < kRadixE; ++e) {
+        if (!(e < E && u0 + e < U)) continue;
+        bool take = key[e] > Tk;
+        if (key[e] == Tk) take = eq_before++ < need_eq;
+        if (take) out[pos++] = u0 + e;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_topk(TopkParams p) {
     for (int64_t u = threadIdx.x; u < p.U; u += blockDim.x) {
         double a = 0.0;
         for (int g = 0; g < p.Gtot; ++g) a += p.part[u * p.Gtot + g];
         p.rel[u] = a;
     }
     __syncthreads();
-    block_topk(p.rel, p.rel, p.U, p.n_sel, p.sel);
+    if (p.U <= static_cast<int64_t>(blockDim.x) * kRadixE)
+        block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+    else
+        block_topk(p.rel, p.rel, p.U, p.n_sel, p.sel);
 }
 
 static size_t topk_smem(int64_t U) { return U <= kTopkSmemU ? static_cast<size_t>(U) * sizeof(double) : 0; }
@@ -504,10 +655,12 @@ void launch_topk(const TopkParams& p, cudaStream_t st) {
         cudaFuncSetAttribute(k_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopkSmemU * sizeof(double));
         attr = true;
     }
-    k_topk<<<1, 32 * kTopkWarps, topk_smem(p.U), st>>>(p);
+    // radix select with 1024 threads x kRadixE ids, else the two-level warp selection
+    const bool radix = p.U <= 1024 * kRadixE;
+    k_topk<<<1, radix ? 1024 : 32 * kTopkWarps, radix ? 0 : topk_smem(p.U), st>>>(p);
 }
 
-__global__ void __launch_bounds__(512) k_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k,
+__global__ void __launch_bounds__(1024) k_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k,
                                                               double* rel, double* relw, int64_t* ids) {
     for (int64_t u = threadIdx.x; u < U; u += blockDim.x) {
         double a = 0.0;
@@ -515,7 +668,10 @@ __global__ void __launch_bounds__(512) k_rel_topk_standalone(const double* part,
         rel[u] = a;
     }
     __syncthreads();
-    block_topk(rel, relw, U, k, ids);
+    if (U <= static_cast<int64_t>(blockDim.x) * kRadixE)
+        block_topk_radix(rel, U, k, ids);
+    else
+        block_topk(rel, relw, U, k, ids);
 }
 
 void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
@@ -526,7 +682,9 @@ void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t
                              kTopkSmemU * sizeof(double));
         attr = true;
     }
-    k_rel_topk_standalone<<<1, 32 * kTopkWarps, topk_smem(U), st>>>(part, U, Gtot, k, rel, relw, ids);
+    const bool radix = U <= 1024 * kRadixE;
+    k_rel_topk_standalone<<<1, radix ? 1024 : 32 * kTopkWarps, radix ? 0 : topk_smem(U), st>>>(part, U, Gtot, k, rel,
+                                                                                              relw, ids);
 }
 
 // --------------------------------------------------------------------------

@@ -63,9 +63,13 @@ struct PrepParams {
 struct LookupParams {
     const double* qsum;  // [G][d]
     const void* repr;    // [U][G][r_k][d]
-    double* part;        // [U][Gtot] (writes columns g0..g0+G)
-    int64_t U;
+    double* part;        // [U][Gtot] (writes columns g0..g0+G)    (sharded mode)
+    double* rel;         // [U] relevance (fused single-shard mode)
+    int64_t* sel;        // [n_sel] ascending ids           (fused single-shard mode)
+    unsigned int* done;  // block counter for the fused top-k (zeroed, re-zeroed by the last block)
+    int64_t U, n_sel;
     int G, Gtot, g0, r_k, d;
+    int fused;           // 1: single shard: rel + top-k in this launch
 };
 
 struct TopkParams {

@@ -181,3 +181,20 @@ def test_encode_stream_graph_matches_chunks():
     eng.encode_stream_host(hq, hk, hv, hout)
     torch.cuda.synchronize()
     assert torch.equal(hout, ref.cpu())
+
+
+@pytest.mark.parametrize("U,k", [(1, 1), (37, 16), (991, 16), (2048, 64), (5000, 32), (9000, 16)])
+def test_topk_ties_and_sizes(U, k):
+    """Exact top-k (rel desc, id asc) incl. heavy ties, via the standalone lookup
+    (radix select path up to 8192 units, warp-selection path beyond)."""
+    from paper_2402_04617_b200 import lookup
+
+    rng = np.random.default_rng(U)
+    G, rk, d, H = 2, 2, 32, 4
+    reprk = rng.integers(-2, 3, size=(U, G, rk, d)).astype(np.float32)  # small ints: many exact ties
+    qb = rng.integers(-1, 2, size=(3, H, d)).astype(np.float32)
+    qsum = qb.astype(np.float64).reshape(3, G, H // G, d).sum(axis=(0, 2))
+    rel, ids = lookup(torch.from_numpy(qsum).cuda(), torch.from_numpy(reprk).cuda(), k)
+    want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
+    assert np.array_equal(rel.cpu().numpy(), want)
+    assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))
