@@ -230,6 +230,13 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
                   int64_t r_k, int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel,
                   int64_t* ids, void* stream);
 
+/* Diagnostic: steady-state per-launch time (us) of one kernel family
+ * (0 prep, 1 lookup + fused top-k, 2 attention, 3 evict + fused select,
+ * 4 LRU) re-launched with the parameters of the engine's last step.
+ * Corrupts the engine's stream state: performance investigation only. */
+int infllm_debug_kernel_bench(infllm_engine_t eng, int32_t which, int32_t iters, double* us_per_launch);
+/* Diagnostic: 64 clock64 phase stamps written by instrumented kernels. */
+int infllm_debug_timestamps(unsigned long long* out64);
 /* Diagnostic: tcgen05 building-block self-test on one 128x128x128 bf16 tile
  * (q, k, vt row-major [128][128] device bf16): s_out = q k^T, o_out =
  * bf16(s_out) vt^T, both fp32 [128][128]. */

@@ -120,6 +120,8 @@ SIGNATURES = {
     "infllm_select_representatives": (C.c_int, [P, P, i64, i64, i64, P, P]),
     "infllm_lookup": (C.c_int, [P, P, i32, i64, i64, i32, i32, i64, P, P, P]),
     "infllm_debug_tc_selftest": (C.c_int, [P, P, P, P, P, P]),
+    "infllm_debug_kernel_bench": (C.c_int, [P, i32, i32, f64p]),
+    "infllm_debug_timestamps": (C.c_int, [P]),
 }
 
 

@@ -142,10 +142,10 @@ void tc_selftest(const void* q, const void* k, const void* vt, float* s_out, flo
 // warps 2-5 softmax/epilogue (TMEM lane quarter = warp % 4).
 
 constexpr int kNS = 4;                 // smem stages (32 KB each: one K or V^T tile)
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // producer, MMA, 8 softmax warps
 constexpr uint32_t kStageBytes = 32768;
 constexpr uint32_t kSmemBytes = 65536 + kNS * kStageBytes + 256 + 1024;
-constexpr int kMassSlots = 24;  // retrieved units whose masses are reduced in-kernel
+constexpr int kMassSlots = 16;  // retrieved units whose masses are reduced in-kernel
 constexpr uint32_t kColS0 = 0, kColS1 = 128, kColSX = 256, kColO = 384;
 
 enum { SRC_INIT = 0, SRC_UNIT = 1, SRC_RING = 2 };
@@ -232,8 +232,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     uint64_t* p_full = bars + 3 + 2 * kNS;
     uint64_t* o_done = bars + 5 + 2 * kNS;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * kNS);
-    float2* sMass = reinterpret_cast<float2*>(smem + 65536 + kNS * kStageBytes + 256);  // [slot][128 rows]
-    double* sRed = reinterpret_cast<double*>(sMass + kMassSlots * 128);                  // [slot][4]
+    float* sMassE = reinterpret_cast<float*>(smem + 65536 + kNS * kStageBytes + 256);  // [slot][2 halves][128 rows]
+    float* sMassM = sMassE + kMassSlots * 2 * 128;                                      // [slot][128 rows]
+    double* sRed = reinterpret_cast<double*>(sMassM + kMassSlots * 128);                // [slot][4]
+    float* sMx = reinterpret_cast<float*>(sRed + kMassSlots * 4);                       // [2 parity][2 halves][128]
+    float* sL = sMx + 4 * 128;                                                          // [2 halves][128]
 
     const AttnParams& a = P.a;
     const bool mass_in_kernel = a.want_mass && a.n_sel <= kMassSlots;
@@ -250,7 +253,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 128);
+            mbar_init(p_full + i, 256);
         }
         mbar_init(o_done, 1);
         fence_barrier_init();
@@ -367,93 +370,87 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             if (ts.T > 0) pv(ts.T - 1, v_prev);
         }
     } else {
-        // ---------------- softmax / epilogue warps (one query row per thread)
+        // ---------------- softmax / epilogue: 8 warps, two per TMEM lane quarter;
+        // warp (q4, hf) owns rows 32*q4.. and key/value columns [64*hf, 64*hf+64)
         const int q4 = warp & 3;
+        const int hf = (warp - 2) >> 2;
         const int row = 32 * q4 + lane;
         const int64_t i = 128 * static_cast<int64_t>(m) + row;
         const bool row_ok = i < a.lx;
         const int64_t qp = row_ok ? a.s + i : ts.qp_hi;
         const uint32_t tl = tbase + ((32u * q4) << 16);
         const float sl2 = a.scale * 1.4426950408889634f;
-        float m_run = -INFINITY, l_run = 0.f;
+        const int cb = 64 * hf;  // first key column of this warp
+        float m_run = -INFINITY, l_half = 0.f;
         for (int j = 0; j < ts.T; ++j) {
             const Tile t = ts.get(a, j);
             const int b = j & 1;
             const uint32_t tS = tl + (b ? kColS1 : kColS0);
             mbar_wait(s_full + b, (j >> 1) & 1);
             tc_fence_after();
-            float x[128];
+            float x[64];
             {
-                uint32_t r0[32], r1[32], r2[32], r3[32];
-                tmem_ld32(tS, r0);
-                tmem_ld32(tS + 32, r1);
-                tmem_ld32(tS + 64, r2);
-                tmem_ld32(tS + 96, r3);
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tS + cb, r0);
+                tmem_ld32(tS + cb + 32, r1);
                 tmem_wait_ld_r(r0);
                 tmem_wait_ld_r(r1);
-                tmem_wait_ld_r(r2);
-                tmem_wait_ld_r(r3);
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {
                     x[jj] = __uint_as_float(r0[jj]);
                     x[32 + jj] = __uint_as_float(r1[jj]);
-                    x[64 + jj] = __uint_as_float(r2[jj]);
-                    x[96 + jj] = __uint_as_float(r3[jj]);
                 }
             }
             // valid key columns [lo, kmax); staircase columns [lo, cmax) use the clamped product
             int kmax = t.hi;
             if (t.src == SRC_RING) kmax = static_cast<int>(imax64(t.lo, imin64(t.hi, qp - t.key0 + 1)));
             if (t.mode == MODE_MIXED) {
-                const int cmax = static_cast<int>(imax64(0, imin64(128, qp - a.L - t.key0)));
-                uint32_t r0[32], r1[32], r2[32], r3[32];
-                tmem_ld32(tl + kColSX, r0);
-                tmem_ld32(tl + kColSX + 32, r1);
-                tmem_ld32(tl + kColSX + 64, r2);
-                tmem_ld32(tl + kColSX + 96, r3);
+                const int cmax = static_cast<int>(imax64(0, imin64(128, qp - a.L - t.key0))) - cb;
+                uint32_t r0[32], r1[32];
+                tmem_ld32(tl + kColSX + cb, r0);
+                tmem_ld32(tl + kColSX + cb + 32, r1);
                 tmem_wait_ld_r(r0);
                 tmem_wait_ld_r(r1);
-                tmem_wait_ld_r(r2);
-                tmem_wait_ld_r(r3);
 #pragma unroll
                 for (int jj = 0; jj < 32; ++jj) {
                     if (jj < cmax) x[jj] = __uint_as_float(r0[jj]);
                     if (32 + jj < cmax) x[32 + jj] = __uint_as_float(r1[jj]);
-                    if (64 + jj < cmax) x[64 + jj] = __uint_as_float(r2[jj]);
-                    if (96 + jj < cmax) x[96 + jj] = __uint_as_float(r3[jj]);
                 }
             }
             // masks only on edge tiles (partial pages, causal diagonal)
-            if (__any_sync(0xffffffffu, t.lo > 0 || kmax < 128)) {
+            if (__any_sync(0xffffffffu, t.lo > cb || kmax < cb + 64)) {
 #pragma unroll
-                for (int c = 0; c < 128; ++c)
-                    if (c < t.lo || c >= kmax) x[c] = -INFINITY;
+                for (int c = 0; c < 64; ++c)
+                    if (cb + c < t.lo || cb + c >= kmax) x[c] = -INFINITY;
             }
             float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < 128; c += 4) {
+            for (int c = 0; c < 64; c += 4) {
                 mx0 = fmaxf(mx0, x[c]);
                 mx1 = fmaxf(mx1, x[c + 1]);
                 mx2 = fmaxf(mx2, x[c + 2]);
                 mx3 = fmaxf(mx3, x[c + 3]);
             }
-            const float mt = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;  // scale > 0 commutes with max
+            // row max across the two column halves (shared memory, double-buffered by tile parity)
+            sMx[(b * 2 + hf) * 128 + row] = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+            asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+            const float mt = fmaxf(sMx[(b * 2) * 128 + row], sMx[(b * 2 + 1) * 128 + row]) * sl2;
             const float m_new = fmaxf(m_run, mt);
             const bool need = m_new > m_run + 8.0f;
-            if (__any_sync(0xffffffffu, need)) {
+            if (__any_sync(0xffffffffu, need)) {  // identical rows in both warps of the pair
                 const float corr = (m_run == -INFINITY) ? 0.f : ex2(m_run - m_new);
-                l_run *= corr;
+                l_half *= corr;
                 if (j > 0) {
                     mbar_wait(o_done, (j - 1) & 1);
                     tc_fence_after();
 #pragma unroll
-                    for (int c4 = 0; c4 < 4; ++c4) {
+                    for (int c4 = 0; c4 < 2; ++c4) {
                         uint32_t r[32];
-                        tmem_ld32(tl + kColO + 32 * c4, r);
+                        tmem_ld32(tl + kColO + cb + 32 * c4, r);
                         tmem_wait_ld_r(r);
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) r[jj] = __float_as_uint(__uint_as_float(r[jj]) * corr);
-                        tmem_st32(tl + kColO + 32 * c4, r);
+                        tmem_st32(tl + kColO + cb + 32 * c4, r);
                     }
                     tmem_wait_st();
                 }
@@ -463,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             const float neg = (m_run == -INFINITY) ? 0.f : -m_run;
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-            for (int c = 0; c < 128; c += 4) {
+            for (int c = 0; c < 64; c += 4) {
                 x[c] = ex2(fmaf(x[c], sl2, neg));
                 x[c + 1] = ex2(fmaf(x[c + 1], sl2, neg));
                 x[c + 2] = ex2(fmaf(x[c + 2], sl2, neg));
@@ -474,38 +471,46 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 s3 += x[c + 3];
             }
             const float rs = (s0 + s1) + (s2 + s3);
-            l_run += rs;
+            l_half += rs;
             if (t.slot >= 0 && a.want_mass) {
                 if (mass_in_kernel) {
-                    sMass[t.slot * 128 + row] = make_float2(row_ok ? rs : 0.f, m_run);
-                } else if (row_ok) {
+                    sMassE[(t.slot * 2 + hf) * 128 + row] = row_ok ? rs : 0.f;
+                    if (hf == 0) sMassM[t.slot * 128 + row] = m_run;
+                } else {
+                    // global fallback: half 0 stores, half 1 adds after the pair barrier
                     const int64_t o = (static_cast<int64_t>(h) * a.lx + i) * a.n_sel + t.slot;
-                    a.mass_e[o] = rs;
-                    a.mass_m[o] = m_run * 0.6931471805599453f;
+                    if (hf == 0 && row_ok) {
+                        a.mass_e[o] = rs;
+                        a.mass_m[o] = m_run * 0.6931471805599453f;
+                    }
+                    asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+                    if (hf == 1 && row_ok) a.mass_e[o] += rs;
                 }
             }
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
+            {
                 uint32_t pk[32];
 #pragma unroll
-                for (int jj = 0; jj < 32; ++jj) pk[jj] = pack_bf16(x[64 * half + 2 * jj], x[64 * half + 2 * jj + 1]);
-                tmem_st32(tS + 32 * half, pk);
+                for (int jj = 0; jj < 32; ++jj) pk[jj] = pack_bf16(x[2 * jj], x[2 * jj + 1]);
+                tmem_st32(tS + 32 * hf, pk);  // keys 64*hf.. packed two per column
             }
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(p_full + b);
         }
-        // epilogue: O / l -> bf16 token-major output
+        // epilogue: l = both halves; O / l -> bf16 token-major output (this warp's 64 value dims)
+        sL[hf * 128 + row] = l_half;
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+        const float l_run = sL[row] + sL[128 + row];
         if (ts.T > 0) {
             mbar_wait(o_done, (ts.T - 1) & 1);
             tc_fence_after();
         }
         const float inv = 1.f / l_run;
-        bf16* out = static_cast<bf16*>(a.out) + (i * a.H + h) * a.dv;
+        bf16* out = static_cast<bf16*>(a.out) + (i * a.H + h) * a.dv + cb;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
+        for (int c4 = 0; c4 < 2; ++c4) {
             uint32_t r[32];
-            tmem_ld32(tl + kColO + 32 * c4, r);
+            tmem_ld32(tl + kColO + cb + 32 * c4, r);
             tmem_wait_ld_r(r);
             if (row_ok) {
                 uint32_t w[16];
@@ -520,19 +525,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         if (mass_in_kernel) {
             // per-unit attention mass of this CTA's rows: sum_rows e_u 2^(m_u - m) / l
             // (engine.hpp:271-283), fp64, fixed order: lanes (xor tree), then quarters 0..3
-            for (int u = 0; u < a.n_sel; ++u) {
-                const float2 em = sMass[u * 128 + row];
-                double w = (row_ok && em.x > 0.f) ? static_cast<double>(em.x * ex2(em.y - m_run) * inv) : 0.0;
-                w = warp_sum_d(w);
-                if (lane == 0) sRed[u * 4 + q4] = w;
+            if (hf == 0) {
+                for (int u = 0; u < a.n_sel; ++u) {
+                    const float e = sMassE[(u * 2) * 128 + row] + sMassE[(u * 2 + 1) * 128 + row];
+                    const float mu = sMassM[u * 128 + row];
+                    double w = (row_ok && e > 0.f) ? static_cast<double>(e * ex2(mu - m_run) * inv) : 0.0;
+                    w = warp_sum_d(w);
+                    if (lane == 0) sRed[u * 4 + q4] = w;
+                }
+                asm volatile("bar.sync 5, 128;" ::: "memory");
+                const int tid = threadIdx.x - 64;
+                if (tid < a.n_sel) {
+                    const double* r4 = sRed + tid * 4;
+                    a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
+                }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int tid = threadIdx.x - 64;
-            if (tid < a.n_sel) {
-                const double* r4 = sRed + tid * 4;
-                a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
-            }
-        } else if (row_ok && a.want_mass) {
+        } else if (row_ok && a.want_mass && hf == 0) {
             a.row_m[static_cast<int64_t>(h) * a.lx + i] = m_run * 0.6931471805599453f;
             a.row_l[static_cast<int64_t>(h) * a.lx + i] = l_run;
         }
@@ -602,14 +610,33 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     P.tm_iv = hit->m[6];
     P.tm_uk = hit->m[7];
     P.tm_uv = hit->m[8];
-    const uint32_t smem = kSmemBytes + kMassSlots * 128 * sizeof(float2) + kMassSlots * 4 * sizeof(double);
+    const uint32_t smem = kSmemBytes + kMassSlots * 3 * 128 * sizeof(float) + kMassSlots * 4 * sizeof(double) +
+                          6 * 128 * sizeof(float);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     dim3 grid(static_cast<unsigned>((a.lx + 127) / 128), a.H);
-    k_attn_tc<<<grid, kTcThreads, smem, st>>>(P);
+    // highest launch priority: the side-stream kernels of the next step must
+    // not hold SMs the attention CTAs (one per SM) are waiting for
+    static int prio_hi = 1;
+    if (prio_hi > 0) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        prio_hi = hi;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributePriority;
+    la[0].val.priority = prio_hi;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_attn_tc, P);
     return 1;
 }
 

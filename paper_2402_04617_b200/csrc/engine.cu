@@ -116,6 +116,31 @@ struct DBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+__global__ void k_empty() {}
+// throughput probes: 8 independent FMA chains x n iterations per thread
+__global__ void k_probe_f64(double* out, int n) {
+    double a[8];
+    for (int j = 0; j < 8; ++j) a[j] = threadIdx.x + j;
+    const double m = 1.0000001, c = 1e-9;
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = fma(a[j], m, c);
+    double s = 0;
+    for (int j = 0; j < 8; ++j) s += a[j];
+    if (s == 12345.0) out[0] = s;
+}
+__global__ void k_probe_f32(float* out, int n) {
+    float a[8];
+    for (int j = 0; j < 8; ++j) a[j] = threadIdx.x + j;
+    const float m = 1.0000001f, c = 1e-9f;
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = fmaf(a[j], m, c);
+    float s = 0;
+    for (int j = 0; j < 8; ++j) s += a[j];
+    if (s == 12345.0f) out[0] = s;
+}
+
 __global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) x[i] = v;
@@ -143,17 +168,26 @@ struct infllm_engine {
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
     // k's front half overlaps step k-1's attention. Scratch written by the
     // side stream and read by the main stream is double-buffered by k % 2.
-    cudaStream_t side_stream = nullptr;
+    cudaStream_t side_stream = nullptr, lru_stream = nullptr;
     cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
+    cudaEvent_t e_attn = nullptr, e_lrudone = nullptr;
     int64_t seq = 0;                 // engine-wide step counter
     int64_t lru_seq[2] = {-1, -1};   // step that last recorded e_lru[b]
     int64_t capture_seq0 = -1;       // first step of the graph being captured (-1: not capturing)
     size_t qa_half = 0;              // bytes of one qa/qc buffer
+    int64_t mass_cta_half = 0;       // doubles in one mass_cta buffer
+    // last launch parameters per kernel (debug kernel timing only)
+    PrepParams last_pp{};
+    LookupParams last_lkp{};
+    AttnParams last_ap{};
+    EvictParams last_ep{};
+    LruParams last_lp{};
+    bool last_bf16 = false;
     int64_t debug_skip = 0;          // timing experiments only: bit0 attention, bit1 lookup+top-k,
                                      // bit2 evict/finalize/select, bit3 prep, bit4 LRU (results invalid)
 
     // scratch shared by layers (layers run sequentially on one stream)
-    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, topk_done;
+    DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, tsum, topk_done, evict_done;
 
     struct Layer {
         int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
@@ -256,6 +290,7 @@ struct infllm_engine {
     void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.unit_cap) return;
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
+        if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.unit_cap, 16});
         L.unit_k.grow(cap * unit_elems_k() * esz, st);
         if (cfg.position_mode == INFLLM_POSITION_ABSOLUTE) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
@@ -279,6 +314,7 @@ struct infllm_engine {
     void ensure_trace(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.trace_cap) return;
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
+        if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.trace_cap, 1024});
         L.trace.grow(cap * 3 * sizeof(int64_t), st);
         L.trace_cap = cap;
@@ -288,6 +324,8 @@ struct infllm_engine {
     void join_side(cudaStream_t st) {
         ck(cudaEventRecord(e_side, side_stream), "record");
         ck(cudaStreamWaitEvent(st, e_side, 0), "wait");
+        ck(cudaEventRecord(e_lrudone, lru_stream), "record");
+        ck(cudaStreamWaitEvent(st, e_lrudone, 0), "wait");
         lru_seq[0] = lru_seq[1] = -1;
     }
 
@@ -369,8 +407,11 @@ struct infllm_engine {
         pp.vl = vl;
         pp.rtab = rtab.as<float2>();
         pp.qs = qsb.as<double>();
+        pp.tsum = tsum.as<double>();
+        last_pp = pp;
+        last_bf16 = std::is_same_v<T, bf16>;
         if (!(debug_skip & 8)) launch_prep<T>(pp, st);
-        launches += (d % 8 == 0 && dv % 8 == 0) ? 3 : 2;
+        launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
 
         // K1 + K2: lookup (memory.hpp:239-269)
         if (do_lookup) {
@@ -395,6 +436,7 @@ struct infllm_engine {
             lp.sel = sel_b;
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
+            last_lkp = lp;
             if (!(debug_skip & 2)) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             if (!lp.fused) gather(L.lookup_part.as<double>(), L.n_units, st);
             TopkParams tp{};
@@ -414,7 +456,12 @@ struct infllm_engine {
 
         ck(cudaEventRecord(e_topk, side), "record");
         ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");
+        // this parity's mass buffers were last read by LRU(k-2)
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+            ck(cudaStreamWaitEvent(main, e_lru[b], 0), "wait");
         st = main;
+        double* mass_cta_b = mass_cta.as<double>() + b * mass_cta_half;
+        double* mass_part_b = L.mass_part.as<double>() + b * std::max<int64_t>(cfg.n_lookup, 1) * Gt;
 
         // K3: attention over [initial | retrieved | local | chunk] (attention.hpp:116-230)
         const bool want_mass = do_lookup && n_sel > 0;
@@ -437,7 +484,7 @@ struct infllm_engine {
         ap.mass_m = mass_m.as<float>();
         ap.row_m = row_m.as<float>();
         ap.row_l = row_l.as<float>();
-        ap.mass_cta = mass_cta.as<double>();
+        ap.mass_cta = mass_cta_b;
         ap.R = R;
         ap.s = s;
         ap.lx = lx;
@@ -458,6 +505,7 @@ struct infllm_engine {
         ap.scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.hpp:140
         ap.vl = vl;
         ap.unit_cap = L.unit_cap;
+        last_ap = ap;
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
             eva = {take_event(), take_event()};
@@ -489,10 +537,10 @@ struct infllm_engine {
                 if (Gs == Gt) {
                     mass_src = 1;
                 } else {
-                    launch_mass_cta_reduce(mass_cta.as<double>(), L.mass_part.as<double>(), static_cast<int>(n_sel), Gs,
+                    launch_mass_cta_reduce(mass_cta_b, mass_part_b, static_cast<int>(n_sel), Gs,
                                            Gt, g0, rep, static_cast<int>((lx + 127) / 128), st);
                     ++launches;
-                    gather(L.mass_part.as<double>(), n_sel, st);
+                    gather(mass_part_b, n_sel, st);
                 }
             } else {
                 MassParams mp{};
@@ -500,7 +548,7 @@ struct infllm_engine {
                 mp.mass_m = mass_m.as<float>();
                 mp.row_m = row_m.as<float>();
                 mp.row_l = row_l.as<float>();
-                mp.part = L.mass_part.as<double>();
+                mp.part = mass_part_b;
                 mp.lx = lx;
                 mp.n_sel = static_cast<int>(n_sel);
                 mp.H = Hs;
@@ -510,12 +558,12 @@ struct infllm_engine {
                 mp.rep = rep;
                 launch_mass(mp, st);
                 ++launches;
-                gather(L.mass_part.as<double>(), n_sel, st);
+                gather(mass_part_b, n_sel, st);
             }
         }
         LruParams lp{};
-        lp.mass_part = L.mass_part.as<double>();
-        lp.mass_cta = mass_cta.as<double>();
+        lp.mass_part = mass_part_b;
+        lp.mass_cta = mass_cta_b;
         lp.sel = sel_b;
         lp.freq = L.freq.as<double>();
         lp.hot = L.hot.as<int8_t>();
@@ -535,9 +583,13 @@ struct infllm_engine {
         lp.mass_src = mass_src;
         lp.decay = cfg.decay;
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
-        if (!(debug_skip & 16)) launch_lru(lp, st);
+        // TieredStore bookkeeping runs on its own stream, off the attention critical path
+        ck(cudaEventRecord(e_attn, main), "record");
+        ck(cudaStreamWaitEvent(lru_stream, e_attn, 0), "wait");
+        last_lp = lp;
+        if (!(debug_skip & 16)) launch_lru(lp, lru_stream);
         ++launches;
-        ck(cudaEventRecord(e_lru[b], main), "record");
+        ck(cudaEventRecord(e_lru[b], lru_stream), "record");
         lru_seq[b] = kseq;
         st = side;
 
@@ -574,9 +626,20 @@ struct infllm_engine {
             ep.l_bs = static_cast<int>(cfg.unit_size);
             ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
             ep.vl = vl;
+            // single shard (and 16-byte rows): scores + selection fused into the eviction launch
+            ep.fused = (Gs == Gt && Gs <= 32) ? 1 : 0;  // single shard: scores finalized in the eviction kernel
+            ep.unit_scores = L.unit_scores.as<float>();
+            ep.repr = L.repr.p;
+            ep.repr_idx = L.repr_idx.as<int32_t>();
+            ep.unit_len = L.ulen.as<int32_t>();
+            ep.sel_u0 = L.n_units;
+            ep.sel_n = completed;
+            ep.r_k = static_cast<int>(cfg.n_repr);
+            ep.done = evict_done.as<unsigned int>();
+            last_ep = ep;
             if (!(debug_skip & 4)) launch_evict<T>(ep, st);
             ++launches;
-            if (to_evict > 0) {
+            if (!ep.fused && to_evict > 0) {
                 gather(L.ev_part.as<double>(), to_evict, st);
                 FinalizeParams fp{};
                 fp.ev_part = L.ev_part.as<double>();
@@ -912,7 +975,8 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->qa.alloc(2 * e->qa_half, st);
         e->qc.alloc(2 * e->qa_half, st);
         ck(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking), "side stream");
-        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1]})
+        ck(cudaStreamCreateWithFlags(&e->lru_stream, cudaStreamNonBlocking), "lru stream");
+        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
         e->chunk_qsum.alloc(static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
@@ -921,9 +985,12 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->row_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
         e->row_l.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * sizeof(float), st);
         e->topk_done.alloc(sizeof(unsigned int), st);
+        e->evict_done.alloc(sizeof(unsigned int), st);
         e->rtab.alloc(static_cast<size_t>(cfg->chunk_size) * std::max(1, e->d / 2) * sizeof(float2), st);
+        e->tsum.alloc(static_cast<size_t>((cfg->chunk_size + 15) / 16) * e->Gs * e->d * sizeof(double), st);
         e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
-        e->mass_cta.alloc(static_cast<size_t>(e->Hs) * (e->lxp / 128) * km * sizeof(double), st);
+        e->mass_cta_half = static_cast<int64_t>(e->Hs) * (e->lxp / 128) * km;
+        e->mass_cta.alloc(2 * e->mass_cta_half * sizeof(double), st);
         e->layers.resize(static_cast<size_t>(e->n_layers));
         for (auto& L : e->layers) {
             L.ring_k.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
@@ -938,7 +1005,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.hot_list.alloc(static_cast<size_t>(cfg->hot_capacity + km + 1) * sizeof(int64_t), st);
             L.lru.alloc(sizeof(LruState), st);
             L.sel.alloc(2 * km * sizeof(int64_t), st);
-            L.mass_part.alloc(km * e->Gt * sizeof(double), st);
+            L.mass_part.alloc(2 * km * e->Gt * sizeof(double), st);
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
         ck(cudaStreamSynchronize(st), "engine_create");
@@ -951,7 +1018,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         if (!e) return;
         cudaDeviceSynchronize();
         cudaStream_t st = nullptr;
-        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->topk_done}) b->release(st);
+        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->tsum, &e->topk_done, &e->evict_done}) b->release(st);
         for (auto& L : e->layers)
             for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
@@ -980,9 +1047,9 @@ int infllm_engine_destroy(infllm_engine_t e) {
         }
         for (int b = 0; b < infllm_engine::kNB; ++b)
             for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
-        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream})
+        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream})
             if (s2) cudaStreamDestroy(s2);
-        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1]})
+        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;
@@ -1292,6 +1359,90 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         part.release(st);
         relw.release(st);
         ck(cudaGetLastError(), "lookup");
+    });
+}
+
+// Debug: steady-state duration of one kernel family, re-launched `iters`
+// times (in a CUDA graph) with the parameters of the engine's last step.
+// which: 0 prep, 1 lookup(+fused top-k), 2 attention, 3 evict(+fused select),
+// 4 LRU. Mutates engine state: only for performance investigation.
+int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, double* us_per_launch) {
+    return guard([&] {
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+        ck(cudaDeviceSynchronize(), "sync");
+        auto launch = [&]() {
+            switch (which) {
+                case 0:
+                    if (e->last_bf16) launch_prep<bf16>(e->last_pp, st); else launch_prep<float>(e->last_pp, st);
+                    break;
+                case 1: launch_lookup(e->last_lkp, e->last_bf16, st); break;
+                case 2:
+                    if (e->last_bf16 && e->tc_eligible(e->last_ap.lx)) launch_attn_tc(e->last_ap, st);
+                    else if (e->last_bf16) launch_attn_simt<bf16>(e->last_ap, st);
+                    else launch_attn_simt<float>(e->last_ap, st);
+                    break;
+                case 3:
+                    if (e->last_bf16) launch_evict<bf16>(e->last_ep, st); else launch_evict<float>(e->last_ep, st);
+                    break;
+                case 4: launch_lru(e->last_lp, st); break;
+                case 5: {  // relevance scan only
+                    LookupParams lp = e->last_lkp;
+                    lp.fused = 0;
+                    lp.part = e->layers[0].lookup_part.as<double>();
+                    launch_lookup(lp, e->last_bf16, st);
+                    break;
+                }
+                case 6: {  // top-k only (1024-thread radix select over rel)
+                    TopkParams tp{};
+                    tp.part = e->layers[0].lookup_part.as<double>();
+                    tp.rel = e->layers[0].rel.as<double>();
+                    tp.sel = e->layers[0].sel.as<int64_t>();
+                    tp.U = e->last_lkp.U;
+                    tp.n_sel = e->last_lkp.n_sel;
+                    tp.Gtot = e->Gt;
+                    launch_topk(tp, st);
+                    break;
+                }
+                case 7: k_empty<<<124, 256, 0, st>>>(); break;
+                case 8: k_empty<<<1, 32, 0, st>>>(); break;
+                case 9: k_probe_f64<<<148 * 4, 256, 0, st>>>(nullptr, 1000); break;   // 1.21e9 DFMA
+                case 10: k_probe_f32<<<148 * 4, 256, 0, st>>>(nullptr, 1000); break;  // 1.21e9 FFMA
+                default: throw ConfigError("unknown kernel id");
+            }
+        };
+        launch();  // warm
+        ck(cudaStreamSynchronize(st), "warm");
+        cudaGraph_t g;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+        for (int i = 0; i < iters; ++i) launch();
+        ck(cudaStreamEndCapture(st, &g), "capture");
+        cudaGraphExec_t x;
+        ck(cudaGraphInstantiate(&x, g, 0), "instantiate");
+        ck(cudaGraphLaunch(x, st), "launch");
+        ck(cudaStreamSynchronize(st), "sync");
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+        ck(cudaGraphLaunch(x, st), "launch");
+        cudaEventRecord(b, st);
+        ck(cudaStreamSynchronize(st), "sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        *us_per_launch = 1000.0 * ms / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaGraphExecDestroy(x);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(st);
+    });
+}
+
+int infllm_debug_timestamps(unsigned long long* out64) {
+    return guard([&] {
+        ck(cudaDeviceSynchronize(), "sync");
+        debug_read_timestamps(out64);
     });
 }
 

@@ -13,6 +13,17 @@
 
 namespace infllm {
 
+// debug phase timestamps (clock64 of one thread), read by infllm_debug_timestamps
+__device__ unsigned long long g_dbg_ts[64];
+#define DBG_TS(i)                                   \
+    do {                                            \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_dbg_ts[(i)] = clock64(); \
+    } while (0)
+
+void debug_read_timestamps(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_dbg_ts, sizeof(unsigned long long) * 64);
+}
+
 // --------------------------------------------------------------------------
 // K7 prep: append k/v to the ring, K_rot = rope(k, pos), q_abs = rope(q, pos),
 // q_clamp = rope(q, L)  (rotary.hpp:55-72; attention.hpp:166-167).
@@ -292,8 +303,285 @@ __global__ void __launch_bounds__(512) k_qs_prefix(PrepParams p) {
     }
 }
 
+// (4) fully fused prep: block = (8 head dims, KV group), one thread per
+// token (tiles of 512 tokens with a carried prefix). Each thread rotates its
+// token's k and the group's query heads, appends k/k_rot/v to the ring, and
+// contributes its fp64 group query sum to a block-wide inclusive scan that
+// yields the P ring entries and the chunk total directly.
+constexpr int kPrepThreads = 512;
+template <typename T>
+__global__ void __launch_bounds__(kPrepThreads) k_prep_fused(PrepParams p) {
+    __shared__ double wtot[kPrepThreads / 32][8];
+    __shared__ double carry_s[8];
+    const int c8 = blockIdx.x, g = blockIdx.y;
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
+    const T* qg = static_cast<const T*>(p.q);
+    const T* kg = static_cast<const T*>(p.k);
+    const T* vg = static_cast<const T*>(p.v);
+    T* rv = static_cast<T*>(p.ring_v);
+    DBG_TS(40);
+    double carry[8];
+    {
+        const double* P0 = p.P + ((p.s % p.R) * p.G + g) * p.d + 8 * c8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) carry[e] = P0[e];
+    }
+    double base_total[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) base_total[e] = carry[e];
+    for (int64_t t0 = 0; t0 < p.lx; t0 += blockDim.x) {
+        const int64_t i = t0 + threadIdx.x;
+        const bool live = i < p.lx;
+        double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (live) {
+            const int64_t pos = p.s + i;
+            // all of this thread's global loads in flight before any math
+            constexpr int kMaxRep = 8;
+            V8<T> qv[kMaxRep];
+#pragma unroll
+            for (int hh = 0; hh < kMaxRep; ++hh)
+                if (hh < p.rep) qv[hh] = ld8(qg + (i * p.H + g * p.rep + hh) * p.d + 8 * c8);
+            const V8<T> kv = ld8(kg + (i * p.G + g) * p.d + 8 * c8);
+            const V8<T> vv = ld8(vg + (i * p.G + g) * p.dv + 8 * c8);
+            DBG_TS(41);
+            // rotation factors of (pos, pairs 4*c8..4*c8+3), computed once per step by k_rope_table
+            float2 f[4];
+            {
+                const float4* rt = reinterpret_cast<const float4*>(p.rtab + i * (p.d / 2) + 4 * c8);
+                const float4 a = rt[0], b = rt[1];
+                f[0] = make_float2(a.x, a.y);
+                f[1] = make_float2(a.z, a.w);
+                f[2] = make_float2(b.x, b.y);
+                f[3] = make_float2(b.z, b.w);
+            }
+            V8<T> kr;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float y0, y1;
+                rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
+                kr.v[2 * j] = from_f<T>(y0);
+                kr.v[2 * j + 1] = from_f<T>(y1);
+            }
+            const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
+            st8(static_cast<T*>(p.ring_k) + ro, kv);
+            st8(static_cast<T*>(p.ring_krot) + ro, kr);
+            DBG_TS(42);
+#pragma unroll
+            for (int hh = 0; hh < kMaxRep; ++hh) {
+                if (hh >= p.rep) break;
+                const int h = g * p.rep + hh;
+                V8<T> qa, qc;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float x0 = to_f(qv[hh].v[2 * j]), x1 = to_f(qv[hh].v[2 * j + 1]);
+                    float y0, y1;
+                    rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
+                    qa.v[2 * j] = from_f<T>(y0);
+                    qa.v[2 * j + 1] = from_f<T>(y1);
+                    const int a = 4 * c8 + j;
+                    rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
+                    qc.v[2 * j] = from_f<T>(y0);
+                    qc.v[2 * j + 1] = from_f<T>(y1);
+                    qs[2 * j] += static_cast<double>(x0);
+                    qs[2 * j + 1] += static_cast<double>(x1);
+                }
+                const int64_t qo = (static_cast<int64_t>(h) * p.lxp + i) * p.d + 8 * c8;
+                st8(static_cast<T*>(p.qa) + qo, qa);
+                st8(static_cast<T*>(p.qc) + qo, qc);
+            }
+            DBG_TS(43);
+            // values of dims [8*c8, 8*c8+8) (dv == d on this path)
+            if (!p.vl.vt) {
+                st8(rv + p.vl.ring(g, pos, 8 * c8), vv);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) rv[p.vl.ring(g, pos, 8 * c8 + e)] = vv.v[e];
+            }
+        }
+        DBG_TS(44);
+        // block-wide inclusive scan of qs over tokens (fp64; exact for bf16 inputs)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(0xffffffffu, qs[e], o);
+                if (lane >= o) qs[e] += y;
+            }
+        }
+        if (lane == 31)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) wtot[warp][e] = qs[e];
+        __syncthreads();
+        double pre[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            double a = carry[e];
+            for (int w = 0; w < warp; ++w) a += wtot[w][e];
+            pre[e] = a + qs[e];
+        }
+        DBG_TS(45);
+        if (live) {
+            double* Pd = p.P + (((p.s + i + 1) % p.R) * p.G + g) * p.d + 8 * c8;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) Pd[e] = pre[e];
+        }
+        // carry for the next tile = inclusive value of the tile's last token
+        if (threadIdx.x == blockDim.x - 1)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) carry_s[e] = pre[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) carry[e] = carry_s[e];
+        __syncthreads();
+        (void)nw;
+        DBG_TS(46);
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p.chunk_qsum[g * p.d + 8 * c8 + e] = carry[e] - base_total[e];
+}
+
+// (5) token-tiled prep with coalesced stores: block = 16 tokens x one KV
+// group, thread = (token, 8-dim chunk) for head_dim 128 (16 chunks). Rows of
+// q_abs / q_clamp / ring k / k_rot are written by 16 consecutive threads
+// (256 B each); value pages are transposed through shared memory; the fp64
+// group query sums go to qs[token][g][:] plus a per-tile column sum.
+constexpr int kTokTile = 16;
+template <typename T>
+__global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
+    __shared__ double sqs[kTokTile][128 + 2];
+    __shared__ T svt[128][kTokTile + 2];
+    const int g = blockIdx.y;
+    const int tt = threadIdx.x / 16, c8 = threadIdx.x % 16;  // token in tile, dim chunk
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kTokTile + tt;
+    const bool live = i < p.lx;
+    const int64_t pos = p.s + i;
+    const T* qg = static_cast<const T*>(p.q);
+    double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (live) {
+        constexpr int kMaxRep = 8;
+        V8<T> qv[kMaxRep];
+#pragma unroll
+        for (int hh = 0; hh < kMaxRep; ++hh)
+            if (hh < p.rep) qv[hh] = ld8(qg + (i * p.H + g * p.rep + hh) * p.d + 8 * c8);
+        const V8<T> kv = ld8(static_cast<const T*>(p.k) + (i * p.G + g) * p.d + 8 * c8);
+        const V8<T> vv = ld8(static_cast<const T*>(p.v) + (i * p.G + g) * p.dv + 8 * c8);
+        float2 f[4];
+        {
+            const float4* rt = reinterpret_cast<const float4*>(p.rtab + i * (p.d / 2) + 4 * c8);
+            const float4 a = rt[0], b = rt[1];
+            f[0] = make_float2(a.x, a.y);
+            f[1] = make_float2(a.z, a.w);
+            f[2] = make_float2(b.x, b.y);
+            f[3] = make_float2(b.z, b.w);
+        }
+        V8<T> kr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float y0, y1;
+            rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
+            kr.v[2 * j] = from_f<T>(y0);
+            kr.v[2 * j + 1] = from_f<T>(y1);
+        }
+        const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
+        st8(static_cast<T*>(p.ring_k) + ro, kv);
+        st8(static_cast<T*>(p.ring_krot) + ro, kr);
+#pragma unroll
+        for (int hh = 0; hh < kMaxRep; ++hh) {
+            if (hh >= p.rep) break;
+            V8<T> qa, qc;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float x0 = to_f(qv[hh].v[2 * j]), x1 = to_f(qv[hh].v[2 * j + 1]);
+                float y0, y1;
+                rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
+                qa.v[2 * j] = from_f<T>(y0);
+                qa.v[2 * j + 1] = from_f<T>(y1);
+                const int a = 4 * c8 + j;
+                rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
+                qc.v[2 * j] = from_f<T>(y0);
+                qc.v[2 * j + 1] = from_f<T>(y1);
+                qs[2 * j] += static_cast<double>(x0);
+                qs[2 * j + 1] += static_cast<double>(x1);
+            }
+            const int64_t qo = (static_cast<int64_t>(g * p.rep + hh) * p.lxp + i) * p.d + 8 * c8;
+            st8(static_cast<T*>(p.qa) + qo, qa);
+            st8(static_cast<T*>(p.qc) + qo, qc);
+        }
+        double2* qd = reinterpret_cast<double2*>(p.qs + (i * p.G + g) * p.d + 8 * c8);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) qd[e] = make_double2(qs[2 * e], qs[2 * e + 1]);
+        if (!p.vl.vt) {
+            st8(static_cast<T*>(p.ring_v) + p.vl.ring(g, pos, 8 * c8), vv);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) svt[8 * c8 + e][tt] = vv.v[e];
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sqs[tt][8 * c8 + e] = qs[e];
+    __syncthreads();
+    // per-tile column sums (token order)
+    if (threadIdx.x < 128) {
+        const int c = threadIdx.x;
+        double a = 0.0;
+        for (int t = 0; t < kTokTile; ++t) a += sqs[t][c];
+        p.tsum[(static_cast<int64_t>(blockIdx.x) * p.G + g) * p.d + c] = a;
+    }
+    if (p.vl.vt) {
+        // transposed value page rows: 16 consecutive positions of one dim
+        const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTokTile;
+        const int nt = static_cast<int>(min(static_cast<int64_t>(kTokTile), p.lx - i0));
+        T* rv = static_cast<T*>(p.ring_v);
+        for (int t = threadIdx.x; t < 128 * kTokTile; t += blockDim.x) {
+            const int c = t / kTokTile, j = t % kTokTile;
+            if (j < nt) rv[p.vl.ring(g, p.s + i0 + j, c)] = svt[c][j];
+        }
+    }
+}
+
+// (6) fp64 prefix into the P ring from the per-token sums and the tile sums:
+// block = (tile, group), thread = dim; rows of P written whole (coalesced).
+__global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
+    const int tile = blockIdx.x, g = blockIdx.y, c = threadIdx.x;
+    if (c >= p.d) return;
+    const int64_t stride = static_cast<int64_t>(p.G) * p.d;
+    double run = p.P[((p.s % p.R) * p.G + g) * p.d + c];
+    for (int t = 0; t < tile; ++t) run += p.tsum[t * stride + g * p.d + c];
+    const int64_t i0 = static_cast<int64_t>(tile) * kTokTile;
+    const int nt = static_cast<int>(min(static_cast<int64_t>(kTokTile), p.lx - i0));
+    double v[kTokTile];
+#pragma unroll
+    for (int j = 0; j < kTokTile; ++j) v[j] = j < nt ? p.qs[(i0 + j) * stride + g * p.d + c] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kTokTile; ++j) {
+        if (j >= nt) break;
+        run += v[j];
+        p.P[(((p.s + i0 + j + 1) % p.R) * p.G + g) * p.d + c] = run;
+    }
+    if (tile == gridDim.x - 1) {  // chunk total = sum of the tile sums, in order
+        double all = 0.0;
+        for (int t = 0; t < static_cast<int>(gridDim.x); ++t) all += p.tsum[t * stride + g * p.d + c];
+        p.chunk_qsum[g * p.d + c] = all;
+    }
+}
+
 template <typename T>
 void launch_prep(const PrepParams& p, cudaStream_t st) {
+    if (p.d == 128 && p.dv == 128 && p.rep <= 8 && p.rtab && p.tsum) {
+        const int64_t nt = p.lx * (p.d / 2);
+        const unsigned tiles = static_cast<unsigned>((p.lx + kTokTile - 1) / kTokTile);
+        k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
+        k_prep_tok<T><<<dim3(tiles, p.G), 256, 0, st>>>(p);
+        k_prefix_tiles<<<dim3(tiles, p.G), 128, 0, st>>>(p);
+        return;
+    }
+    if (p.d % 8 == 0 && p.dv == p.d && p.rep <= 8 && p.rtab) {
+        const int64_t nt = p.lx * (p.d / 2);
+        k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
+        k_prep_fused<T><<<dim3(p.d / 8, p.G), kPrepThreads, 0, st>>>(p);
+        return;
+    }
     if (p.d % 8 == 0 && p.dv % 8 == 0 && p.rtab && p.qs) {
         const int64_t nt = p.lx * (p.d / 2);
         k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
@@ -320,6 +608,7 @@ template void launch_prep<bf16>(const PrepParams&, cudaStream_t);
 // rel[u] and the last block to finish runs the exact top-k (K2) over all units.
 __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out);
 
+__device__ __forceinline__ int qpad(int c);
 template <typename T, int kPer>
 __device__ __forceinline__ double group_dot(const T* src, const double* qg, int lane, int d) {
     // elements e = lane*kPer + j of the [r_k][d] run; dim = e % d
@@ -328,16 +617,21 @@ __device__ __forceinline__ double group_dot(const T* src, const double* qg, int 
     int c = e0 % d;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-        a += qg[c] * static_cast<double>(to_f(src[e0 + j]));
+        a += qg[qpad(c)] * static_cast<double>(to_f(src[e0 + j]));
         if (++c == d) c = 0;
     }
     return warp_sum_d(a);
 }
 
+// qsum is staged in shared memory with 2 doubles of padding per 16 dims so
+// the 8 distinct dims read together (16 apart) fall in distinct banks
+__device__ __forceinline__ int qpad(int c) { return c + 2 * (c >> 4); }
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
-    extern __shared__ double sq[];  // [G][d]
-    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[t] = p.qsum[t];
+    extern __shared__ double sq[];  // [G][qpad(d)]
+    const int dp = qpad(p.d);
+    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[(t / p.d) * dp + qpad(t % p.d)] = p.qsum[t];
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t u = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
@@ -358,7 +652,7 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
 #pragma unroll
             for (int g = 0; g < 8; ++g) {
                 if (g >= p.G) break;
-                const double* qg = sq + g * p.d + c0;
+                const double* qg = sq + g * dp + qpad(c0);
                 const bf16* e = reinterpret_cast<const bf16*>(&buf[2 * g]);
                 double a = 0.0;
 #pragma unroll
@@ -368,7 +662,7 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
                 else if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
             }
             for (int g = 8; g < p.G; ++g) {
-                const double a = group_dot<T, 16>(base + g * E, sq + g * p.d, lane, p.d);
+                const double a = group_dot<T, 16>(base + g * E, sq + g * dp, lane, p.d);
                 if (p.fused) rel += a;
                 else if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
             }
@@ -376,11 +670,11 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
             const int per = (E + 31) / 32;
             for (int g = 0; g < p.G; ++g) {
                 const T* src = base + g * E;
-                const double* qg = sq + g * p.d;
+                const double* qg = sq + g * dp;
                 double a = 0.0;
                 for (int j = 0; j < per; ++j) {
                     const int e = lane * per + j;
-                    if (e < E) a += qg[e % p.d] * static_cast<double>(to_f(src[e]));
+                    if (e < E) a += qg[qpad(e % p.d)] * static_cast<double>(to_f(src[e]));
                 }
                 a = warp_sum_d(a);
                 if (p.fused) rel += a;
@@ -405,7 +699,7 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
     const int warps = 8;
     const unsigned blocks = static_cast<unsigned>((p.U + warps - 1) / warps);
-    const size_t smem = sizeof(double) * p.G * p.d;
+    const size_t smem = sizeof(double) * p.G * (p.d + 2 * ((p.d + 15) / 16));
     if (dtype_bf16)
         k_lookup<bf16><<<blocks, warps * 32, smem, st>>>(p);
     else
@@ -548,8 +842,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
 __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out) {
     __shared__ int hist[256];
     __shared__ int wsum[32];
-    __shared__ uint64_t s_prefix;
-    __shared__ int s_remaining;
+    __shared__ uint64_t s_prefix, s_mask;
+    __shared__ int s_remaining, s_done;
     const int T = blockDim.x;
     const int E = static_cast<int>((U + T - 1) / T);
     const int64_t u0 = static_cast<int64_t>(threadIdx.x) * E;
@@ -558,14 +852,16 @@ __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_
     for (int e = 0; e < kRadixE; ++e) key[e] = (e < E && u0 + e < U) ? order_key(rel[u0 + e]) : 0ull;
     if (threadIdx.x == 0) {
         s_prefix = 0;
+        s_mask = 0;
         s_remaining = static_cast<int>(K);
+        s_done = 0;
     }
-    uint64_t mask = 0;
     for (int pass = 0; pass < 8; ++pass) {
         const int shift = 56 - 8 * pass;
         for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0;
         __syncthreads();
-        const uint64_t prefix = s_prefix;
+        if (s_done) break;  // uniform: read after the barrier
+        const uint64_t prefix = s_prefix, mask = s_mask;
 #pragma unroll
         for (int e = 0; e < kRadixE; ++e)
             if (e < E && u0 + e < U && (key[e] & mask) == prefix) atomicAdd(&hist[(key[e] >> shift) & 255], 1);
@@ -587,13 +883,14 @@ __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_
             }
             const int rem = s_remaining;
             int run = incl - sum;  // count in higher bins
-            int found = -1, above = 0;
+            int found = -1, above = 0, cnt = 0;
             if (run < rem && incl >= rem) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     if (found < 0 && run + c[j] >= rem) {
                         found = 255 - 8 * lane - j;
                         above = run;
+                        cnt = c[j];
                     }
                     run += c[j];
                 }
@@ -602,42 +899,53 @@ __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_
             const int src = __ffs(m) - 1;
             found = __shfl_sync(0xffffffffu, found, src);
             above = __shfl_sync(0xffffffffu, above, src);
+            cnt = __shfl_sync(0xffffffffu, cnt, src);
             if (lane == 0) {
                 s_prefix = prefix | (static_cast<uint64_t>(found) << shift);
+                s_mask = mask | (0xFFull << shift);
                 s_remaining = rem - above;
+                // the boundary bin is taken whole: no need to resolve further digits
+                if (cnt == rem - above) s_done = 1;
             }
         }
-        mask |= 0xFFull << shift;
         __syncthreads();
     }
-    const uint64_t Tk = s_prefix;
-    const int need_eq = s_remaining;  // how many of the key == T ids to take (lowest first)
+    const uint64_t Tk = s_prefix, Tm = s_mask;
+    const int need_eq = s_remaining;  // how many of the (key & Tm) == Tk ids to take, lowest first
     int n_eq = 0;
 #pragma unroll
-    for (int e = 0; e < kRadixE; ++e) n_eq += (e < E && u0 + e < U && key[e] == Tk) ? 1 : 0;
+    for (int e = 0; e < kRadixE; ++e) n_eq += (e < E && u0 + e < U && (key[e] & Tm) == Tk) ? 1 : 0;
     int eq_before = block_excl_scan(n_eq, wsum, nullptr);
     int n_sel = 0;
+    int eqb = eq_before;
 #pragma unroll
     for (int e = 0; e < kRadixE; ++e) {
         if (!(e < E && u0 + e < U)) continue;
-        if (key[e] > Tk) ++n_sel;
-        else if (key[e] == Tk && eq_before++ < need_eq) ++n_sel;
+        const uint64_t km = key[e] & Tm;
+        if (km > Tk) ++n_sel;
+        else if (km == Tk && eqb++ < need_eq) ++n_sel;
     }
     int pos = block_excl_scan(n_sel, wsum, nullptr);
-    eq_before = eq_before - n_eq;  // restore for the write pass
 #pragma unroll
     for (int e = 0; e < kRadixE; ++e) {
         if (!(e < E && u0 + e < U)) continue;
-        bool take = key[e] > Tk;
-        if (key[e] == Tk) take = eq_before++ < need_eq;
+        const uint64_t km = key[e] & Tm;
+        bool take = km > Tk;
+        if (km == Tk) take = eq_before++ < need_eq;
         if (take) out[pos++] = u0 + e;
     }
 }
 
 __global__ void __launch_bounds__(1024) k_topk(TopkParams p) {
     for (int64_t u = threadIdx.x; u < p.U; u += blockDim.x) {
+        double v[16];
+#pragma unroll
+        for (int g = 0; g < 16; ++g) v[g] = g < p.Gtot ? p.part[u * p.Gtot + g] : 0.0;
         double a = 0.0;
-        for (int g = 0; g < p.Gtot; ++g) a += p.part[u * p.Gtot + g];
+#pragma unroll
+        for (int g = 0; g < 16; ++g)
+            if (g < p.Gtot) a += v[g];
+        for (int g = 16; g < p.Gtot; ++g) a += p.part[u * p.Gtot + g];
         p.rel[u] = a;
     }
     __syncthreads();
@@ -1060,6 +1368,8 @@ __global__ void __launch_bounds__(256) k_lru(LruParams p) {
 
 void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 256, 0, st>>>(p); }
 
+__device__ void warp_select(const float* sc, int len, int r_k, int* out);
+
 // --------------------------------------------------------------------------
 // K8 evict + K5 representative-score partials. Popped positions
 // [pop0, pop0 + n_init) are pinned as initial tokens (engine.hpp:311-322);
@@ -1150,10 +1460,91 @@ __global__ void __launch_bounds__(256) k_evict(EvictParams p) {
     if (lane == 0) p.ev_part[e * p.Gtot + p.g0 + g] = a;
 }
 
+// Eviction with all loads in flight at once: block = one popped token, warp
+// = one KV group. Copies k (and k_rot in absolute mode) and v into the
+// initial-token buffer or the token's unit page; for evicted tokens computes
+// the per-group r_m partial k_m . (P[m+L+1] - P[m+1]) with lane-contiguous
+// dims + xor tree, and either stores it (sharded: exchanged, then
+// k_finalize) or sums the groups in order 0..G-1 in-block and writes the
+// finalized score (finalize_front, repr_score.hpp:72-82).
+template <typename T>
+__global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
+    __shared__ double part[32];
+    const int g = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t idx = blockIdx.x;
+    const int64_t pos = p.pop0 + idx;
+    const int64_t slot = pos % p.R;
+    const bool to_init = idx < p.n_init;
+    int64_t u = 0, off = 0;
+    if (!to_init) {
+        const int64_t rel = pos - p.pend_start;
+        u = p.unit0 + rel / p.l_bs;
+        off = rel % p.l_bs;
+    }
+    const T* rk = static_cast<const T*>(p.ring_k) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
+    const int per = (p.d + 31) / 32;  // contiguous dims per lane
+    const int c0 = lane * per;
+    // issue the score loads first (evictees only)
+    double acc = 0.0;
+    if (!to_init) {
+        const double* Phi = p.P + (((pos + p.L + 1) % p.R) * p.G + g) * p.d;
+        const double* Plo = p.P + (((pos + 1) % p.R) * p.G + g) * p.d;
+        for (int j = 0; j < per; ++j) {
+            const int c = c0 + j;
+            if (c < p.d) acc += static_cast<double>(to_f(rk[c])) * (Phi[c] - Plo[c]);
+        }
+    }
+    // copies
+    const int nvec = (p.d * static_cast<int>(sizeof(T))) % 16 == 0 ? p.d * static_cast<int>(sizeof(T)) / 16 : 0;
+    T* dk = to_init ? static_cast<T*>(p.init_k) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d
+                    : static_cast<T*>(p.unit_k) + ((u * p.G + g) * p.l_bs + off) * p.d;
+    T* dkr = !p.absolute ? nullptr
+             : to_init ? static_cast<T*>(p.init_krot) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d
+                       : static_cast<T*>(p.unit_krot) + ((u * p.G + g) * p.l_bs + off) * p.d;
+    const T* rkr = static_cast<const T*>(p.ring_krot) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
+    if (nvec) {
+        for (int t = lane; t < nvec; t += 32) {
+            reinterpret_cast<uint4*>(dk)[t] = reinterpret_cast<const uint4*>(rk)[t];
+            if (dkr) reinterpret_cast<uint4*>(dkr)[t] = reinterpret_cast<const uint4*>(rkr)[t];
+        }
+    } else {
+        for (int c = lane; c < p.d; c += 32) {
+            dk[c] = rk[c];
+            if (dkr) dkr[c] = rkr[c];
+        }
+    }
+    const T* rv = static_cast<const T*>(p.ring_v);
+    T* dvb = static_cast<T*>(to_init ? p.init_v : p.unit_v);
+    for (int c = lane; c < p.dv; c += 32) {
+        const T x = rv[p.vl.ring(g, pos, c)];
+        if (to_init)
+            dvb[p.vl.init(g, pos, c)] = x;
+        else
+            dvb[p.vl.unit(u, g, off, c)] = x;
+    }
+    if (to_init) return;
+    acc = warp_sum_d(acc);
+    if (!p.fused) {
+        if (lane == 0) p.ev_part[(idx - p.n_init) * p.Gtot + p.g0 + g] = acc;
+        return;
+    }
+    if (lane == 0) part[g] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int gg = 0; gg < p.G; ++gg) tot += part[gg];
+        p.unit_scores[u * p.l_bs + off] = static_cast<float>(tot / static_cast<double>(p.L));
+    }
+}
+
 template <typename T>
 void launch_evict(const EvictParams& p, cudaStream_t st) {
     const int64_t n = p.n_init + p.n_evict;
-    if (n > 0) k_evict<T><<<dim3(static_cast<unsigned>((n + 7) / 8), p.G), 256, 0, st>>>(p);
+    if (n <= 0) return;
+    if (p.G <= 32)
+        k_evict_tok<T><<<static_cast<unsigned>(n), 32 * p.G, 0, st>>>(p);
+    else
+        k_evict<T><<<dim3(static_cast<unsigned>((n + 7) / 8), p.G), 256, 0, st>>>(p);
 }
 template void launch_evict<float>(const EvictParams&, cudaStream_t);
 template void launch_evict<bf16>(const EvictParams&, cudaStream_t);

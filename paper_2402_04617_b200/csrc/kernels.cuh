@@ -54,6 +54,7 @@ struct PrepParams {
     double* chunk_qsum;  // [G][d]
     float2* rtab;        // [lx][d/2] rotation factors of the chunk positions (scratch)
     double* qs;          // [lx][G][d] per-token group query sums (scratch)
+    double* tsum;        // [lx/16][G][d] per-16-token-tile sums of qs (scratch)
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
     VLayout vl;
@@ -152,6 +153,15 @@ struct EvictParams {
     int64_t pend_start, unit0;  // token pend_start belongs to unit id unit0 at offset 0
     int G, Gtot, g0, d, dv, l_bs, absolute;
     VLayout vl;
+    // fused single-shard mode: finalize_front + select_representatives in the same launch
+    int fused;
+    float* unit_scores;   // [U][l_bs]
+    void* repr;           // [U][G][r_k][d]
+    int32_t* repr_idx;    // [U][r_k]
+    const int32_t* unit_len;
+    int64_t sel_u0, sel_n;  // units completed by this step
+    int r_k;
+    unsigned int* done;
 };
 
 struct FinalizeParams {
@@ -171,6 +181,7 @@ struct SelectParams {
     int G, r_k, d, l_bs;
 };
 
+void debug_read_timestamps(unsigned long long* out);
 template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
