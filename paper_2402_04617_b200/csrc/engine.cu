@@ -35,6 +35,9 @@ struct ConfigError : std::invalid_argument {
 struct StreamError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct ExchangeError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
@@ -57,6 +60,9 @@ int guard(F&& f) {
     } catch (const CudaError& e) {
         g_err = e.what();
         return INFLLM_ERR_CUDA;
+    } catch (const ExchangeError& e) {
+        g_err = e.what();
+        return INFLLM_ERR_NCCL;
     } catch (const std::exception& e) {
         g_err = e.what();
         return INFLLM_ERR_ARG;
@@ -332,7 +338,7 @@ struct infllm_engine {
     void gather(double* buf, int64_t rows, cudaStream_t st) {
         if (!allgather || Gs == Gt) return;
         if (allgather(allgather_user, buf, rows, g0, Gs, Gt, st) != 0)
-            throw std::runtime_error("allgather hook failed");
+            throw ExchangeError("allgather hook failed");
     }
 
     bool tc_eligible(int64_t lx) const {
@@ -783,7 +789,7 @@ struct infllm_engine {
                 stage_o[b].alloc(C * Hs * dv * esz, st, false);
             }
         }
-        if (!use_graphs) {
+        if (!use_graphs || (allgather && Gs != Gt)) {  // host exchange hooks cannot be captured
             if (host)
                 run_chunks_host<T>(li, q, k, v, n, out, st);
             else
