@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <stdexcept>
 #include <string>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/infllm_b200.h"
@@ -206,6 +207,7 @@ struct infllm_engine {
         DBuf init_k, init_krot, init_v;
         DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
+        DBuf kmax2;  // [2 step parities][G] running max |k|^2 (attention score bound)
     };
     std::vector<Layer> layers;
 
@@ -414,6 +416,11 @@ struct infllm_engine {
         pp.rtab = rtab.as<float2>();
         pp.qs = qsb.as<double>();
         pp.tsum = tsum.as<double>();
+        // the token-tiled prep maintains the key-norm bound the tcgen05 attention uses
+        const bool kbound = d == 128 && dv == 128 && rep <= 8;
+        const int lb = static_cast<int>(L.step & 1);  // this layer's step parity
+        pp.kmax2 = kbound ? L.kmax2.as<float>() + lb * Gs : nullptr;
+        pp.kmax2_prev = kbound ? L.kmax2.as<float>() + (lb ^ 1) * Gs : nullptr;
         last_pp = pp;
         last_bf16 = std::is_same_v<T, bf16>;
         if (!(debug_skip & 8)) launch_prep<T>(pp, st);
@@ -491,6 +498,7 @@ struct infllm_engine {
         ap.row_m = row_m.as<float>();
         ap.row_l = row_l.as<float>();
         ap.mass_cta = mass_cta_b;
+        ap.kmax2 = pp.kmax2;
         ap.R = R;
         ap.s = s;
         ap.lx = lx;
@@ -1003,6 +1011,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ring_krot.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
             L.ring_v.alloc(static_cast<size_t>(e->Gs) * e->R * e->dv * es, st);
             L.P.alloc(static_cast<size_t>(e->R) * e->Gs * e->d * sizeof(double), st);
+            L.kmax2.alloc(2 * static_cast<size_t>(e->Gs) * sizeof(float), st);
             const size_t ni = static_cast<size_t>(std::max<int64_t>(cfg->init_size, 1));
             L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
             if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
@@ -1093,6 +1102,7 @@ int infllm_engine_reset(infllm_engine_t e, void* stream) {
             L.unit_start.clear();
             L.unit_len.clear();
             ck(cudaMemsetAsync(L.P.p, 0, L.P.bytes, st), "memset");
+            ck(cudaMemsetAsync(L.kmax2.p, 0, L.kmax2.bytes, st), "memset");
             ck(cudaMemsetAsync(L.lru.p, 0, L.lru.bytes, st), "memset");
             if (L.hot.p) ck(cudaMemsetAsync(L.hot.p, 0, L.hot.bytes, st), "memset");
             if (L.freq.p) ck(cudaMemsetAsync(L.freq.p, 0, L.freq.bytes, st), "memset");
@@ -1448,7 +1458,10 @@ int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, d
 int infllm_debug_timestamps(unsigned long long* out64) {
     return guard([&] {
         ck(cudaDeviceSynchronize(), "sync");
-        debug_read_timestamps(out64);
+        if (getenv("INFLLM_TS_ATTN"))
+            debug_read_attn_timestamps(out64);
+        else
+            debug_read_timestamps(out64);
     });
 }
 

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(1024) k_prefix(PrepParams p) {
 __global__ void k_rope_table(PrepParams p) {
     const int pairs = p.d / 2;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p.kmax2 && t < p.G) p.kmax2[t] = p.kmax2_prev[t];  // k_prep_tok raises it with this chunk's keys
     if (t >= p.lx * pairs) return;
     const int64_t i = t / pairs;
     const int a = static_cast<int>(t % pairs);
@@ -458,6 +459,7 @@ __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
     const int64_t pos = p.s + i;
     const T* qg = static_cast<const T*>(p.q);
     double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float kn2 = 0.f;  // this thread's part of |k|^2
     if (live) {
         constexpr int kMaxRep = 8;
         V8<T> qv[kMaxRep];
@@ -483,6 +485,10 @@ __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
             kr.v[2 * j] = from_f<T>(y0);
             kr.v[2 * j + 1] = from_f<T>(y1);
         }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
         const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
         st8(static_cast<T*>(p.ring_k) + ro, kv);
         st8(static_cast<T*>(p.ring_krot) + ro, kr);
@@ -517,6 +523,13 @@ __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) svt[8 * c8 + e][tt] = vv.v[e];
         }
+    }
+    if (p.kmax2) {
+        // |k|^2 per token (the attention kernel's score bound), max into the running value
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) kn2 += __shfl_xor_sync(0xffffffffu, kn2, o);
+        kn2 = fmaxf(kn2, __shfl_xor_sync(0xffffffffu, kn2, 16));  // the warp's two tokens
+        if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(p.kmax2) + g, __float_as_int(kn2));
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) sqs[tt][8 * c8 + e] = qs[e];

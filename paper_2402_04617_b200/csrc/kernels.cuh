@@ -55,6 +55,8 @@ struct PrepParams {
     float2* rtab;        // [lx][d/2] rotation factors of the chunk positions (scratch)
     double* qs;          // [lx][G][d] per-token group query sums (scratch)
     double* tsum;        // [lx/16][G][d] per-16-token-tile sums of qs (scratch)
+    float* kmax2;             // [G] running max of |k|^2 over every key fed so far (this step's copy)
+    const float* kmax2_prev;  // [G] the previous step's copy
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
     VLayout vl;
@@ -101,6 +103,7 @@ struct AttnParams {
     float* row_m;   // [H][lx]
     float* row_l;
     double* mass_cta;  // [H][n_mt][n_sel] (tcgen05 path)
+    const float* kmax2;  // [G] max |k|^2 over all keys (score bound), or null
     int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;

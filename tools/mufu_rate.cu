@@ -1,0 +1,54 @@
+// Microbenchmark: MUFU.EX2 and FMA-pipe throughput per SM (cycles via clock64).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/mufu_rate.cu -o tools/mufu_rate.bin
+#include <cstdio>
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <int KIND>
+__global__ void k(int iters, float* out, unsigned long long* cyc) {
+    float v[8];
+    for (int i = 0; i < 8; ++i) v[i] = -0.001f * (threadIdx.x + i);
+    __syncthreads();
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (KIND == 0)
+                v[i] = ex2(v[i]);
+            else
+                v[i] = fmaf(v[i], 0.999f, -0.0001f);
+        }
+    }
+    __syncthreads();
+    const unsigned long long t1 = clock64();
+    float s = 0;
+    for (int i = 0; i < 8; ++i) s += v[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
+int main() {
+    float* o;
+    unsigned long long* c;
+    cudaMalloc(&o, 1 << 24);
+    cudaMalloc(&c, 8);
+    for (int threads : {128, 256, 512, 1024}) {
+        for (int kind : {0, 1}) {
+            const int iters = 4096;
+            if (kind == 0)
+                k<0><<<148, threads>>>(iters, o, c);
+            else
+                k<1><<<148, threads>>>(iters, o, c);
+            cudaDeviceSynchronize();
+            unsigned long long cy;
+            cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
+            printf("%s threads=%d: %.2f ops/clk/SM\n", kind == 0 ? "ex2" : "ffma", threads,
+                   (double)threads * iters * 8 / cy);
+        }
+    }
+    return 0;
+}
