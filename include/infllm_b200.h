@@ -142,7 +142,9 @@ int infllm_engine_reserve(infllm_engine_t eng, int64_t max_tokens);
 int infllm_engine_reset(infllm_engine_t eng, void* stream);
 /* Engine options: "tc_attention" (1 = tcgen05 attention when the shape
  * allows, 0 = CUDA-core attention), "cuda_graphs" (1 = graph-replayed
- * encode_stream, default). */
+ * encode_stream, default), "attn_score_bound" (1 = the tcgen05 attention may
+ * use the per-row score bound |q| |k|_max as a fixed softmax offset, default;
+ * 0 = always the online-max path). */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if

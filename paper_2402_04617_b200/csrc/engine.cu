@@ -170,6 +170,7 @@ struct infllm_engine {
     int64_t launches = 0;
     bool use_tc = false;
     bool tc_disabled = false;
+    bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -498,7 +499,7 @@ struct infllm_engine {
         ap.row_m = row_m.as<float>();
         ap.row_l = row_l.as<float>();
         ap.mass_cta = mass_cta_b;
-        ap.kmax2 = pp.kmax2;
+        ap.kmax2 = score_bound ? pp.kmax2 : nullptr;
         ap.R = R;
         ap.s = s;
         ap.lx = lx;
@@ -1125,6 +1126,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->use_graphs = value != 0;
         else if (k == "debug_skip")
             e->debug_skip = value;
+        else if (k == "attn_score_bound")
+            e->score_bound = value != 0;
         else
             throw ConfigError("unknown option '" + k + "'");
     });

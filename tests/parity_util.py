@@ -29,7 +29,7 @@ def rel_err(a, b):
 
 
 def run_pair(cfg_kw, H, Hkv, d, q, k, v, schedule, decode_tail=0, dtype=torch.float32, oracle_threads=8,
-             tc=True, finish=False):
+             tc=True, finish=False, options=None):
     """Streams the same q/k/v through the GPU engine and the CPU oracle and
     returns per-step records for comparison."""
     from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
@@ -42,6 +42,8 @@ def run_pair(cfg_kw, H, Hkv, d, q, k, v, schedule, decode_tail=0, dtype=torch.fl
                                                                      value_dim=dv), dtype=dtype)
     if not tc:
         geng.set_option("tc_attention", 0)
+    for key, val in (options or {}).items():
+        geng.set_option(key, val)
     dev = torch.device("cuda")
     qt = torch.from_numpy(q).to(dev, dtype)
     kt = torch.from_numpy(k).to(dev, dtype)

@@ -61,12 +61,19 @@ def test_gqa_fp32_ragged():
     _assert_pair(oeng, geng, recs, 1e-5)
 
 
-def test_bf16_gqa_d128():
+@pytest.mark.parametrize("scale,bound", [(0.25, 1), (0.25, 0), (1.8, 1)])
+def test_bf16_gqa_d128(scale, bound):
+    """tcgen05 attention. scale 0.25: every row's score bound |q| |k|max is
+    small (fixed-offset fast path); bound=0 forces the online-max path on the
+    same data; scale 1.8 pushes the bound past 60 so CTAs fall back by
+    themselves (larger scores also grow the bf16 rounding of the rotated
+    operands, which is why the scale stops there)."""
     cfg = dict(chunk_size=256, unit_size=128, n_repr=4, local_size=1024, init_size=128, n_lookup=8, hot_capacity=12)
     n = 6144
-    q, k, v = gaussian_inputs(11, n, 8, 2, 128, scale=0.25, bf16=True)
+    q, k, v = gaussian_inputs(11, n, 8, 2, 128, scale=scale, bf16=True)
     sched = O.encode_schedule(n, 256, 8)
-    oeng, geng, recs = run_pair(cfg, 8, 2, 128, q, k, v, sched, decode_tail=8, dtype=torch.bfloat16)
+    oeng, geng, recs = run_pair(cfg, 8, 2, 128, q, k, v, sched, decode_tail=8, dtype=torch.bfloat16,
+                                options={"attn_score_bound": bound})
     _assert_pair(oeng, geng, recs, 2e-2)
 
 
