@@ -281,7 +281,7 @@ def run_b200(args, rank, world, local_rank):
         cpu = None
         if world == 1 and not args.no_cpu:
             try:
-                cpu = cpu_sample(os.cpu_count() or 1, steps=1)
+                cpu = cpu_sample(os.cpu_count() or 1, steps=10)
                 cpu.pop("seconds", None)
             except Exception as ex:  # reported, not fatal
                 cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
