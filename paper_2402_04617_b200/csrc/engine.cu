@@ -344,6 +344,27 @@ struct infllm_engine {
             throw ExchangeError("allgather hook failed");
     }
 
+    // Units are whole 128-token ring pages (they start at l_I + 128 u and every
+    // token of a unit is still in the ring when it completes): copied per unit
+    // with 16-byte vectors instead of per evicted token.
+    bool page_mode() const {
+        return cfg.unit_size == 128 && cfg.init_size % 128 == 0 && cfg.chunk_size >= 64 && (d * esz) % 16 == 0 &&
+               (dv * esz) % 16 == 0;
+    }
+    void set_page(SelectParams& sp, const Layer& L, int64_t pos0) const {
+        sp.page_mode = page_mode() ? 1 : 0;
+        sp.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+        sp.dv = dv;
+        sp.pos0 = pos0;
+        sp.R = R;
+        sp.ring_k = L.ring_k.p;
+        sp.ring_krot = L.ring_krot.p;
+        sp.ring_v = L.ring_v.p;
+        sp.unit_krot = L.unit_krot.p;
+        sp.unit_v = L.unit_v.p;
+        sp.vl = vl;
+    }
+
     bool tc_eligible(int64_t lx) const {
         (void)lx;
         return use_tc && !tc_disabled;
@@ -651,6 +672,7 @@ struct infllm_engine {
             ep.sel_n = completed;
             ep.r_k = static_cast<int>(cfg.n_repr);
             ep.done = evict_done.as<unsigned int>();
+            ep.page_mode = page_mode() ? 1 : 0;
             last_ep = ep;
             if (!(debug_skip & 4)) launch_evict<T>(ep, st);
             ++launches;
@@ -682,6 +704,7 @@ struct infllm_engine {
                 sp.r_k = static_cast<int>(cfg.n_repr);
                 sp.d = d;
                 sp.l_bs = static_cast<int>(cfg.unit_size);
+                set_page(sp, L, L.pend_start);
                 if (!(debug_skip & 4)) launch_select<T>(sp, st);
                 ++launches;
                 for (int64_t c = 0; c < completed; ++c) {
@@ -889,6 +912,7 @@ struct infllm_engine {
             sp.r_k = static_cast<int>(cfg.n_repr);
             sp.d = d;
             sp.l_bs = static_cast<int>(cfg.unit_size);
+            set_page(sp, L, L.pend_start);
             launch_select<T>(sp, st);
             ++launches;
             L.unit_start.push_back(L.pend_start);

@@ -1508,6 +1508,7 @@ __global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
         }
     }
     // copies
+    if (!(p.page_mode && !to_init)) {  // page mode: k_select copies whole unit pages
     const int nvec = (p.d * static_cast<int>(sizeof(T))) % 16 == 0 ? p.d * static_cast<int>(sizeof(T)) / 16 : 0;
     T* dk = to_init ? static_cast<T*>(p.init_k) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d
                     : static_cast<T*>(p.unit_k) + ((u * p.G + g) * p.l_bs + off) * p.d;
@@ -1534,6 +1535,7 @@ __global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
             dvb[p.vl.init(g, pos, c)] = x;
         else
             dvb[p.vl.unit(u, g, off, c)] = x;
+    }
     }
     if (to_init) return;
     acc = warp_sum_d(acc);
@@ -1622,8 +1624,42 @@ __device__ void warp_select(const float* sc, int len, int r_k, int* out) {
     }
 }
 
+// page mode: block = (unit, group): the unit's K (and K_rot) rows and its V
+// page are contiguous 32 KB blocks of the ring (slots pos0 + 128 i .. + 127,
+// no wrap since R is a multiple of 128): copied with 16-byte vectors
 template <typename T>
-__global__ void __launch_bounds__(128) k_select(SelectParams p) {
+__device__ void select_page(const SelectParams& p, int64_t u, int g, const int* idx, int take) {
+    const int64_t slot = (p.pos0 + 128 * (u - p.u0)) % p.R;
+    const int64_t rowb = static_cast<int64_t>(128) * p.d * static_cast<int64_t>(sizeof(T)) / 16;  // uint4 per K page
+    const uint4* sk = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d);
+    uint4* dk = reinterpret_cast<uint4*>(static_cast<T*>(const_cast<void*>(p.unit_k)) + ((u * p.G + g) * 128) * p.d);
+    for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dk[t] = sk[t];
+    if (p.absolute) {
+        const uint4* skr = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_krot) + (g * p.R + slot) * p.d);
+        uint4* dkr = reinterpret_cast<uint4*>(static_cast<T*>(p.unit_krot) + ((u * p.G + g) * 128) * p.d);
+        for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dkr[t] = skr[t];
+    }
+    const int64_t vb = static_cast<int64_t>(128) * p.dv * static_cast<int64_t>(sizeof(T)) / 16;
+    const T* rv = static_cast<const T*>(p.ring_v);
+    T* uv = static_cast<T*>(p.unit_v);
+    // both layouts keep a unit's values contiguous: V^T page [dv][128] or rows [128][dv]
+    const uint4* sv = reinterpret_cast<const uint4*>(rv + (p.vl.vt ? p.vl.ring(g, slot, 0) : (g * p.R + slot) * p.dv));
+    uint4* dv = reinterpret_cast<uint4*>(uv + p.vl.unit(u, g, 0, 0));
+    for (int64_t t = threadIdx.x; t < vb; t += blockDim.x) dv[t] = sv[t];
+    // representative rows of this group straight from the ring (memory.hpp:111-123)
+    const T* rk = static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d;
+    T* rp = static_cast<T*>(p.repr) + ((u * p.G + g) * p.r_k) * p.d;
+    const int nv = p.d * static_cast<int>(sizeof(T)) / 16;
+    for (int t = threadIdx.x; t < p.r_k * nv; t += blockDim.x) {
+        const int r = t / nv, c = t % nv;
+        uint4 x = make_uint4(0, 0, 0, 0);
+        if (r < take) x = reinterpret_cast<const uint4*>(rk + idx[r] * p.d)[c];
+        reinterpret_cast<uint4*>(rp + r * p.d)[c] = x;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_select(SelectParams p) {
     __shared__ int idx[32];
     const int64_t u = p.u0 + blockIdx.x;
     const int len = p.unit_len[u];
@@ -1633,9 +1669,14 @@ __global__ void __launch_bounds__(128) k_select(SelectParams p) {
         warp_select(p.unit_scores + u * p.l_bs, len, p.r_k, r);
         if (threadIdx.x == 0)
             for (int k = 0; k < take; ++k) idx[k] = r[k];
-        if (threadIdx.x < p.r_k) p.repr_idx[u * p.r_k + threadIdx.x] = threadIdx.x < take ? r[threadIdx.x] : -1;
+        if (threadIdx.x < p.r_k && blockIdx.y == 0)
+            p.repr_idx[u * p.r_k + threadIdx.x] = threadIdx.x < take ? r[threadIdx.x] : -1;
     }
     __syncthreads();
+    if (p.page_mode) {
+        select_page<T>(p, u, static_cast<int>(blockIdx.y), idx, take);
+        return;
+    }
     const T* uk = static_cast<const T*>(p.unit_k);
     T* rp = static_cast<T*>(p.repr);
     // repr[u][g][r][:] = key row idx[r] of the unit (memory.hpp:111-123);
@@ -1662,7 +1703,7 @@ __global__ void __launch_bounds__(128) k_select(SelectParams p) {
 template <typename T>
 void launch_select(const SelectParams& p, cudaStream_t st) {
     if (p.n_units <= 0) return;
-    k_select<T><<<static_cast<unsigned>(p.n_units), 128, 0, st>>>(p);
+    k_select<T><<<dim3(static_cast<unsigned>(p.n_units), p.page_mode ? p.G : 1), p.page_mode ? 256 : 128, 0, st>>>(p);
 }
 template void launch_select<float>(const SelectParams&, cudaStream_t);
 template void launch_select<bf16>(const SelectParams&, cudaStream_t);

@@ -165,6 +165,7 @@ struct EvictParams {
     int64_t sel_u0, sel_n;  // units completed by this step
     int r_k;
     unsigned int* done;
+    int page_mode;  // 1: units are whole ring pages, copied per unit by k_select (not per token here)
 };
 
 struct FinalizeParams {
@@ -182,6 +183,17 @@ struct SelectParams {
     int32_t* repr_idx; // [U][r_k]
     int64_t u0, n_units;
     int G, r_k, d, l_bs;
+    // page mode (unit_size 128, units aligned to 128-token ring pages): grid
+    // (unit, group); each block copies its unit page K / V (/ K_rot) from the
+    // ring and gathers the representative rows from there
+    int page_mode, absolute, dv;
+    int64_t pos0, R;  // first token of unit u0; ring capacity
+    const void* ring_k;
+    const void* ring_krot;
+    const void* ring_v;
+    void* unit_krot;
+    void* unit_v;
+    VLayout vl;
 };
 
 void debug_read_timestamps(unsigned long long* out);
