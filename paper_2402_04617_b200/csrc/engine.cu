@@ -209,6 +209,7 @@ struct infllm_engine {
         DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
         DBuf kmax2;  // [2 step parities][G] running max |k|^2 (attention score bound)
+        DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
     };
     std::vector<Layer> layers;
 
@@ -465,8 +466,9 @@ struct infllm_engine {
             lp.g0 = g0;
             lp.r_k = static_cast<int>(cfg.n_repr);
             lp.d = d;
-            // single shard: relevance + exact top-k fused into one launch
-            lp.fused = (Gs == Gt && L.n_units <= 256 * 8) ? 1 : 0;  // last lookup block (256 thr x 8 ids)
+            // single shard: relevance + exact top-k fused into one launch (last lookup
+            // block, 256 threads x 8 ids); beyond that rel + a multi-block top-k
+            lp.fused = Gs == Gt ? (L.n_units <= 256 * 8 ? 1 : 2) : 0;
             lp.rel = L.rel.as<double>();
             lp.sel = sel_b;
             lp.done = topk_done.as<unsigned int>();
@@ -482,7 +484,15 @@ struct infllm_engine {
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
-            launches += lp.fused ? 1 : 2;
+            if (lp.fused == 2) {
+                const int64_t nc = topk_multi_scratch(L.n_units, n_sel);
+                L.cand.grow(static_cast<size_t>(nc) * 16, st);
+                double* cv = L.cand.as<double>();
+                if (!(debug_skip & 2))
+                    launch_topk_multi(L.rel.as<double>(), L.n_units, n_sel, cv, reinterpret_cast<int64_t*>(cv + nc),
+                                      sel_b, st);
+            }
+            launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
             if (prof) {
                 record(evp.second, st);
                 (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
@@ -1383,24 +1393,25 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
         if (n_units <= 0) return;
-        DBuf part, relw;
-        part.alloc(static_cast<size_t>(n_units) * n_kv_heads * sizeof(double), st, false);
-        relw.alloc(static_cast<size_t>(n_units) * sizeof(double), st, false);
+        const int64_t k = std::min(k_m, n_units);
+        const int64_t nc = topk_multi_scratch(n_units, std::max<int64_t>(k, 1));
+        static thread_local DBuf cand;  // grow-only scratch (a per-call allocation would dominate small lookups)
+        cand.grow(static_cast<size_t>(nc) * 16, st);
         LookupParams lp{};
         lp.qsum = qsum;
         lp.repr = repr;
-        lp.part = part.as<double>();
+        lp.rel = rel;
         lp.U = n_units;
         lp.G = n_kv_heads;
         lp.Gtot = n_kv_heads;
         lp.g0 = 0;
         lp.r_k = static_cast<int>(r_k);
         lp.d = head_dim;
+        lp.fused = 2;  // relevance scan, then the multi-block exact top-k
         launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
-        launch_rel_topk_standalone(part.as<double>(), n_units, n_kv_heads, std::min(k_m, n_units), rel,
-                                   relw.as<double>(), ids, st);
-        part.release(st);
-        relw.release(st);
+        if (k > 0)
+            launch_topk_multi(rel, n_units, k, cand.as<double>(), reinterpret_cast<int64_t*>(cand.as<double>() + nc),
+                              ids, st);
         ck(cudaGetLastError(), "lookup");
     });
 }

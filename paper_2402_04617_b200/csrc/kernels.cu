@@ -6,6 +6,7 @@
 // the fp32 parity mode and for shapes the tcgen05 kernel does not cover.
 // Reference citations are relative to /root/reference/proj/include/blockmem/.
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -696,7 +697,7 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
         }
         if (p.fused && lane == 0) p.rel[u] = rel;
     }
-    if (!p.fused) return;
+    if (p.fused != 1) return;  // 2: rel only, the multi-block top-k follows
     // last block to finish selects the top-k over all units
     __shared__ bool last;
     __threadfence();
@@ -947,6 +948,43 @@ __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_
         if (km == Tk) take = eq_before++ < need_eq;
         if (take) out[pos++] = u0 + e;
     }
+}
+
+// Multi-block exact top-k for large unit counts: each block selects the top
+// k of a 2048-unit slice (radix select), then one block selects the top k of
+// the candidates. Candidates are laid out in slice order with ascending ids
+// inside a slice, so candidate index order is unit id order and the
+// (rel desc, id asc) tie rule carries over (memory.hpp:245-253).
+constexpr int kSliceU = 256 * kRadixE;
+constexpr int kTopkMaxSel = 128;  // n_lookup limit
+__global__ void __launch_bounds__(256) k_topk_local(const double* rel, int64_t U, int64_t k, double* cand_v,
+                                                    int64_t* cand_i) {
+    __shared__ int64_t loc[kTopkMaxSel];
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * kSliceU;
+    const int64_t len = U - s0 < kSliceU ? U - s0 : kSliceU;
+    const int64_t kk = k < len ? k : len;
+    block_topk_radix(rel + s0, len, kk, loc);
+    __syncthreads();
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+        const bool ok = r < kk;
+        cand_v[blockIdx.x * k + r] = ok ? rel[s0 + loc[r]] : -INFINITY;
+        cand_i[blockIdx.x * k + r] = ok ? s0 + loc[r] : -1;
+    }
+}
+__global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const int64_t* cand_i, int64_t n, int64_t k,
+                                                     int64_t* sel) {
+    __shared__ int64_t loc[kTopkMaxSel];
+    block_topk_radix(cand_v, n, k, loc);
+    __syncthreads();
+    for (int r = threadIdx.x; r < k; r += blockDim.x) sel[r] = cand_i[loc[r]];
+}
+int64_t topk_multi_scratch(int64_t U, int64_t k) { return ((U + kSliceU - 1) / kSliceU) * k; }
+void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
+                       cudaStream_t st) {
+    if (U <= 0 || k <= 0) return;
+    const int64_t nb = (U + kSliceU - 1) / kSliceU;
+    k_topk_local<<<static_cast<unsigned>(nb), 256, 0, st>>>(rel, U, k, cand_v, cand_i);
+    k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, nb * k, std::min<int64_t>(k, U), sel);
 }
 
 __global__ void __launch_bounds__(1024) k_topk(TopkParams p) {

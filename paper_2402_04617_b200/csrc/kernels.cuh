@@ -72,7 +72,7 @@ struct LookupParams {
     unsigned int* done;  // block counter for the fused top-k (zeroed, re-zeroed by the last block)
     int64_t U, n_sel;
     int G, Gtot, g0, r_k, d;
-    int fused;           // 1: single shard: rel + top-k in this launch
+    int fused;           // 1: single shard: rel + top-k in this launch; 2: rel only (multi-block top-k follows)
 };
 
 struct TopkParams {
@@ -200,6 +200,10 @@ void debug_read_timestamps(unsigned long long* out);
 template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
+// exact top-k (rel desc, id asc) over rel[U] for large U; scratch of topk_multi_scratch(U, k) entries each
+int64_t topk_multi_scratch(int64_t U, int64_t k);
+void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
+                       cudaStream_t st);
 template <typename T> void launch_attn_simt(const AttnParams& p, cudaStream_t st);
 void launch_mass(const MassParams& p, cudaStream_t st);
 void launch_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep, int n_mt,
