@@ -294,7 +294,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #define ATTN_TURN 1
 #endif
 #ifndef ATTN_POLY_EVERY
-#define ATTN_POLY_EVERY 4  // every 4th score's exp2 on the FMA pipe instead of MUFU (0: none)
+#define ATTN_POLY_EVERY 0  // 4: a quarter of the exp2 on the FMA pipe instead of MUFU, 2: half, 0: none
 #endif
 
 // Blackwell packed fp32 pairs (FFMA2 / FADD2) and 3-input max (FMNMX3): the
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                     ffma2(x[c + 2], x[c + 3], x[c + 2], x[c + 3], sl2, sl2, neg, neg);
                     x[c] = ex2(x[c]);
                     x[c + 1] = ex2(x[c + 1]);
-                    if (ATTN_POLY_EVERY == 4 && (c & 4)) {
+                    if ((ATTN_POLY_EVERY == 4 && (c & 4)) || ATTN_POLY_EVERY == 2) {
                         ex2_poly2(x[c + 2], x[c + 3], x[c + 2], x[c + 3]);  // every 4th pair: FMA pipe
                     } else {
                         x[c + 2] = ex2(x[c + 2]);
