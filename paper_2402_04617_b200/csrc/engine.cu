@@ -176,9 +176,15 @@ struct infllm_engine {
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
     // k's front half overlaps step k-1's attention. Scratch written by the
     // side stream and read by the main stream is double-buffered by k % 2.
-    cudaStream_t side_stream = nullptr, lru_stream = nullptr;
+    // The prep of step k runs on its own stream, concurrently with step k-1's
+    // eviction/selection on the side stream (it only waits for step k-1's lookup,
+    // the last reader of the chunk query sums it rewrites).
+    cudaStream_t side_stream = nullptr, lru_stream = nullptr, prep_stream = nullptr, evict_stream = nullptr;
     cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
-    cudaEvent_t e_attn = nullptr, e_lrudone = nullptr;
+    cudaEvent_t e_attn = nullptr, e_lrudone = nullptr, e_prep = nullptr, e_lookup = nullptr, e_prepdone = nullptr;
+    cudaEvent_t e_evict = nullptr, e_evdone = nullptr;
+    int64_t lookup_seq = -1;         // step that last recorded e_lookup
+    int64_t evict_seq = -1;          // step that last recorded e_evict
     int64_t seq = 0;                 // engine-wide step counter
     int64_t lru_seq[2] = {-1, -1};   // step that last recorded e_lru[b]
     int64_t capture_seq0 = -1;       // first step of the graph being captured (-1: not capturing)
@@ -301,6 +307,7 @@ struct infllm_engine {
         if (need <= L.unit_cap) return;
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
+        if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.unit_cap, 16});
         L.unit_k.grow(cap * unit_elems_k() * esz, st);
         if (cfg.position_mode == INFLLM_POSITION_ABSOLUTE) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
@@ -325,6 +332,7 @@ struct infllm_engine {
         if (need <= L.trace_cap) return;
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
+        if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.trace_cap, 1024});
         L.trace.grow(cap * 3 * sizeof(int64_t), st);
         L.trace_cap = cap;
@@ -336,7 +344,13 @@ struct infllm_engine {
         ck(cudaStreamWaitEvent(st, e_side, 0), "wait");
         ck(cudaEventRecord(e_lrudone, lru_stream), "record");
         ck(cudaStreamWaitEvent(st, e_lrudone, 0), "wait");
+        ck(cudaEventRecord(e_prepdone, prep_stream), "record");
+        ck(cudaStreamWaitEvent(st, e_prepdone, 0), "wait");
+        ck(cudaEventRecord(e_evdone, evict_stream), "record");
+        ck(cudaStreamWaitEvent(st, e_evdone, 0), "wait");
         lru_seq[0] = lru_seq[1] = -1;
+        lookup_seq = -1;
+        evict_seq = -1;
     }
 
     void gather(double* buf, int64_t rows, cudaStream_t st) {
@@ -399,18 +413,23 @@ struct infllm_engine {
         // main-stream step k-2 that last read this parity's buffers
         const int64_t kseq = seq++;
         const int b = static_cast<int>(kseq & 1);
-        cudaStream_t main = st, side = side_stream;
+        cudaStream_t main = st, side = side_stream, pst = prep_stream, est = evict_stream;
         if (fork) {
             ck(cudaEventRecord(e_call, main), "record");
             ck(cudaStreamWaitEvent(side, e_call, 0), "wait");
+            ck(cudaStreamWaitEvent(pst, e_call, 0), "wait");
         }
-        if (inputs_ready) ck(cudaStreamWaitEvent(side, inputs_ready, 0), "wait");
-        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+        if (inputs_ready) ck(cudaStreamWaitEvent(pst, inputs_ready, 0), "wait");
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0)) {
             ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");
+            ck(cudaStreamWaitEvent(pst, e_lru[b], 0), "wait");  // qa/qc of this parity
+        }
+        // chunk query sums are double-buffered by step parity: the lookup of step
+        // k-2 (which read this parity) ran before attention k-2, covered by e_lru[b]
         void* qa_b = static_cast<uint8_t*>(qa.p) + b * qa_half;
         void* qc_b = static_cast<uint8_t*>(qc.p) + b * qa_half;
         int64_t* sel_b = L.sel.as<int64_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
-        st = side;
+        st = pst;
 
         // K7: ring append, RoPE, prefix sums
         PrepParams pp{};
@@ -423,7 +442,7 @@ struct infllm_engine {
         pp.ring_krot = L.ring_krot.p;
         pp.ring_v = L.ring_v.p;
         pp.P = L.P.as<double>();
-        pp.chunk_qsum = chunk_qsum.as<double>();
+        pp.chunk_qsum = chunk_qsum.as<double>() + b * Gs * d;  // double-buffered: the prep may run a step ahead
         pp.s = s;
         pp.lx = lx;
         pp.lxp = lxp;
@@ -448,6 +467,113 @@ struct infllm_engine {
         last_bf16 = std::is_same_v<T, bf16>;
         if (!(debug_skip & 8)) launch_prep<T>(pp, st);
         launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
+        ck(cudaEventRecord(e_prep, pst), "record");
+        ck(cudaStreamWaitEvent(side, e_prep, 0), "wait");
+        st = side;
+
+        // window roll: init pinning, eviction, representative scoring, packing.
+        // Its kernels only touch the evicted tokens and the units created in
+        // this step, which this step's lookup and attention never read (units
+        // of step t are visible from step t+1, engine.hpp:257-346), so they run
+        // on the eviction stream concurrently with the lookup and attention.
+        const int64_t n_units0 = L.n_units, init_len0 = L.init_len, local_start0 = L.local_start;
+        // this step's lookup (side stream) sees the units completed by the previous step
+        if (evict_seq >= 0 && (capture_seq0 < 0 || evict_seq >= capture_seq0))
+            ck(cudaStreamWaitEvent(side, e_evict, 0), "wait");
+        st = est;
+        ck(cudaStreamWaitEvent(est, e_prep, 0), "wait");
+        if (overflow > 0) {
+            // UnitPacker::add: an empty packer starts its pending run at the
+            // first evicted token (memory.hpp:65-66)
+            if (L.pend_count == 0 && to_evict > 0) L.pend_start = L.local_start + to_init;
+            EvictParams ep{};
+            ep.ring_k = L.ring_k.p;
+            ep.ring_krot = L.ring_krot.p;
+            ep.ring_v = L.ring_v.p;
+            ep.P = L.P.as<double>();
+            ep.init_k = L.init_k.p;
+            ep.init_krot = L.init_krot.p;
+            ep.init_v = L.init_v.p;
+            ep.unit_k = L.unit_k.p;
+            ep.unit_krot = L.unit_krot.p;
+            ep.unit_v = L.unit_v.p;
+            ep.ev_part = L.ev_part.as<double>();
+            ep.pop0 = L.local_start;
+            ep.n_init = to_init;
+            ep.n_evict = to_evict;
+            ep.R = R;
+            ep.L = cfg.local_size;
+            ep.l_I = cfg.init_size;
+            ep.pend_start = L.pend_start;
+            ep.unit0 = L.n_units;
+            ep.G = Gs;
+            ep.Gtot = Gt;
+            ep.g0 = g0;
+            ep.d = d;
+            ep.dv = dv;
+            ep.l_bs = static_cast<int>(cfg.unit_size);
+            ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+            ep.vl = vl;
+            // single shard (and 16-byte rows): scores + selection fused into the eviction launch
+            ep.fused = (Gs == Gt && Gs <= 32) ? 1 : 0;  // single shard: scores finalized in the eviction kernel
+            ep.unit_scores = L.unit_scores.as<float>();
+            ep.repr = L.repr.p;
+            ep.repr_idx = L.repr_idx.as<int32_t>();
+            ep.unit_len = L.ulen.as<int32_t>();
+            ep.sel_u0 = L.n_units;
+            ep.sel_n = completed;
+            ep.r_k = static_cast<int>(cfg.n_repr);
+            ep.done = evict_done.as<unsigned int>();
+            ep.page_mode = page_mode() ? 1 : 0;
+            last_ep = ep;
+            if (!(debug_skip & 4)) launch_evict<T>(ep, st);
+            ++launches;
+            if (!ep.fused && to_evict > 0) {
+                gather(L.ev_part.as<double>(), to_evict, st);
+                FinalizeParams fp{};
+                fp.ev_part = L.ev_part.as<double>();
+                fp.unit_scores = L.unit_scores.as<float>();
+                fp.e0 = L.local_start + to_init;
+                fp.n_evict = to_evict;
+                fp.pend_start = L.pend_start;
+                fp.unit0 = L.n_units;
+                fp.L = cfg.local_size;
+                fp.Gtot = Gt;
+                fp.l_bs = static_cast<int>(cfg.unit_size);
+                if (!(debug_skip & 4)) launch_finalize(fp, st);
+                ++launches;
+            }
+            if (completed > 0) {
+                SelectParams sp{};
+                sp.unit_scores = L.unit_scores.as<float>();
+                sp.unit_len = L.ulen.as<int32_t>();
+                sp.unit_k = L.unit_k.p;
+                sp.repr = L.repr.p;
+                sp.repr_idx = L.repr_idx.as<int32_t>();
+                sp.u0 = L.n_units;
+                sp.n_units = completed;
+                sp.G = Gs;
+                sp.r_k = static_cast<int>(cfg.n_repr);
+                sp.d = d;
+                sp.l_bs = static_cast<int>(cfg.unit_size);
+                set_page(sp, L, L.pend_start);
+                if (!(debug_skip & 4)) launch_select<T>(sp, st);
+                ++launches;
+                for (int64_t c = 0; c < completed; ++c) {
+                    L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
+                    L.unit_len.push_back(static_cast<int32_t>(cfg.unit_size));
+                }
+                L.n_units += completed;
+                L.pend_start += completed * cfg.unit_size;
+            }
+            L.pend_count = new_pending - completed * cfg.unit_size;
+            L.local_start += overflow;
+            L.init_len += to_init;
+        }
+        ck(cudaEventRecord(e_evict, est), "record");
+        evict_seq = kseq;
+        st = side;
+
 
         // K1 + K2: lookup (memory.hpp:239-269)
         if (do_lookup) {
@@ -457,10 +583,10 @@ struct infllm_engine {
                 record(evp.first, st);
             }
             LookupParams lp{};
-            lp.qsum = chunk_qsum.as<double>();
+            lp.qsum = chunk_qsum.as<double>() + b * Gs * d;
             lp.repr = L.repr.p;
             lp.part = L.lookup_part.as<double>();
-            lp.U = L.n_units;
+            lp.U = n_units0;
             lp.G = Gs;
             lp.Gtot = Gt;
             lp.g0 = g0;
@@ -468,28 +594,28 @@ struct infllm_engine {
             lp.d = d;
             // single shard: relevance + exact top-k fused into one launch (last lookup
             // block, 256 threads x 8 ids); beyond that rel + a multi-block top-k
-            lp.fused = Gs == Gt ? (L.n_units <= 256 * 8 ? 1 : 2) : 0;
+            lp.fused = Gs == Gt ? (n_units0 <= 256 * 8 ? 1 : 2) : 0;
             lp.rel = L.rel.as<double>();
             lp.sel = sel_b;
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
             last_lkp = lp;
             if (!(debug_skip & 2)) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
-            if (!lp.fused) gather(L.lookup_part.as<double>(), L.n_units, st);
+            if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
             tp.rel = L.rel.as<double>();
             tp.sel = sel_b;
-            tp.U = L.n_units;
+            tp.U = n_units0;
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
             if (lp.fused == 2) {
-                const int64_t nc = topk_multi_scratch(L.n_units, n_sel);
+                const int64_t nc = topk_multi_scratch(n_units0, n_sel);
                 L.cand.grow(static_cast<size_t>(nc) * 16, st);
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
-                    launch_topk_multi(L.rel.as<double>(), L.n_units, n_sel, cv, reinterpret_cast<int64_t*>(cv + nc),
+                    launch_topk_multi(L.rel.as<double>(), n_units0, n_sel, cv, reinterpret_cast<int64_t*>(cv + nc),
                                       sel_b, st);
             }
             launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
@@ -500,7 +626,9 @@ struct infllm_engine {
         }
 
         ck(cudaEventRecord(e_topk, side), "record");
-        ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");
+        if (!(debug_skip & 32)) ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");  // 32: timing experiment only
+        ck(cudaEventRecord(e_lookup, side), "record");
+        lookup_seq = kseq;
         // this parity's mass buffers were last read by LRU(k-2)
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
             ck(cudaStreamWaitEvent(main, e_lru[b], 0), "wait");
@@ -535,8 +663,8 @@ struct infllm_engine {
         ap.s = s;
         ap.lx = lx;
         ap.lxp = lxp;
-        ap.init_len = L.init_len;
-        ap.local_start = L.local_start;
+        ap.init_len = init_len0;
+        ap.local_start = local_start0;
         ap.L = cfg.local_size;
         ap.l_I = cfg.init_size;
         ap.n_sel = static_cast<int>(n_sel);
@@ -639,95 +767,6 @@ struct infllm_engine {
         lru_seq[b] = kseq;
         st = side;
 
-        // window roll: init pinning, eviction, representative scoring, packing
-        if (overflow > 0) {
-            // UnitPacker::add: an empty packer starts its pending run at the
-            // first evicted token (memory.hpp:65-66)
-            if (L.pend_count == 0 && to_evict > 0) L.pend_start = L.local_start + to_init;
-            EvictParams ep{};
-            ep.ring_k = L.ring_k.p;
-            ep.ring_krot = L.ring_krot.p;
-            ep.ring_v = L.ring_v.p;
-            ep.P = L.P.as<double>();
-            ep.init_k = L.init_k.p;
-            ep.init_krot = L.init_krot.p;
-            ep.init_v = L.init_v.p;
-            ep.unit_k = L.unit_k.p;
-            ep.unit_krot = L.unit_krot.p;
-            ep.unit_v = L.unit_v.p;
-            ep.ev_part = L.ev_part.as<double>();
-            ep.pop0 = L.local_start;
-            ep.n_init = to_init;
-            ep.n_evict = to_evict;
-            ep.R = R;
-            ep.L = cfg.local_size;
-            ep.l_I = cfg.init_size;
-            ep.pend_start = L.pend_start;
-            ep.unit0 = L.n_units;
-            ep.G = Gs;
-            ep.Gtot = Gt;
-            ep.g0 = g0;
-            ep.d = d;
-            ep.dv = dv;
-            ep.l_bs = static_cast<int>(cfg.unit_size);
-            ep.absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
-            ep.vl = vl;
-            // single shard (and 16-byte rows): scores + selection fused into the eviction launch
-            ep.fused = (Gs == Gt && Gs <= 32) ? 1 : 0;  // single shard: scores finalized in the eviction kernel
-            ep.unit_scores = L.unit_scores.as<float>();
-            ep.repr = L.repr.p;
-            ep.repr_idx = L.repr_idx.as<int32_t>();
-            ep.unit_len = L.ulen.as<int32_t>();
-            ep.sel_u0 = L.n_units;
-            ep.sel_n = completed;
-            ep.r_k = static_cast<int>(cfg.n_repr);
-            ep.done = evict_done.as<unsigned int>();
-            ep.page_mode = page_mode() ? 1 : 0;
-            last_ep = ep;
-            if (!(debug_skip & 4)) launch_evict<T>(ep, st);
-            ++launches;
-            if (!ep.fused && to_evict > 0) {
-                gather(L.ev_part.as<double>(), to_evict, st);
-                FinalizeParams fp{};
-                fp.ev_part = L.ev_part.as<double>();
-                fp.unit_scores = L.unit_scores.as<float>();
-                fp.e0 = L.local_start + to_init;
-                fp.n_evict = to_evict;
-                fp.pend_start = L.pend_start;
-                fp.unit0 = L.n_units;
-                fp.L = cfg.local_size;
-                fp.Gtot = Gt;
-                fp.l_bs = static_cast<int>(cfg.unit_size);
-                if (!(debug_skip & 4)) launch_finalize(fp, st);
-                ++launches;
-            }
-            if (completed > 0) {
-                SelectParams sp{};
-                sp.unit_scores = L.unit_scores.as<float>();
-                sp.unit_len = L.ulen.as<int32_t>();
-                sp.unit_k = L.unit_k.p;
-                sp.repr = L.repr.p;
-                sp.repr_idx = L.repr_idx.as<int32_t>();
-                sp.u0 = L.n_units;
-                sp.n_units = completed;
-                sp.G = Gs;
-                sp.r_k = static_cast<int>(cfg.n_repr);
-                sp.d = d;
-                sp.l_bs = static_cast<int>(cfg.unit_size);
-                set_page(sp, L, L.pend_start);
-                if (!(debug_skip & 4)) launch_select<T>(sp, st);
-                ++launches;
-                for (int64_t c = 0; c < completed; ++c) {
-                    L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
-                    L.unit_len.push_back(static_cast<int32_t>(cfg.unit_size));
-                }
-                L.n_units += completed;
-                L.pend_start += completed * cfg.unit_size;
-            }
-            L.pend_count = new_pending - completed * cfg.unit_size;
-            L.local_start += overflow;
-            L.init_len += to_init;
-        }
         L.trace_count += n_sel;
         L.last_n_sel = n_sel;
         L.last_b = b;
@@ -1025,9 +1064,12 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->qc.alloc(2 * e->qa_half, st);
         ck(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking), "side stream");
         ck(cudaStreamCreateWithFlags(&e->lru_stream, cudaStreamNonBlocking), "lru stream");
-        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone})
+        ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
+        ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
+        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone,
+                         &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
-        e->chunk_qsum.alloc(static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
+        e->chunk_qsum.alloc(2 * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
         e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
         e->mass_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
@@ -1097,9 +1139,11 @@ int infllm_engine_destroy(infllm_engine_t e) {
         }
         for (int b = 0; b < infllm_engine::kNB; ++b)
             for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
-        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream})
+        for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
+                        e->evict_stream})
             if (s2) cudaStreamDestroy(s2);
-        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone})
+        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone, e->e_prep,
+                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;
