@@ -182,7 +182,8 @@ struct infllm_engine {
     cudaStream_t side_stream = nullptr, lru_stream = nullptr, prep_stream = nullptr, evict_stream = nullptr;
     cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
     cudaEvent_t e_attn = nullptr, e_lrudone = nullptr, e_prep = nullptr, e_lookup = nullptr, e_prepdone = nullptr;
-    cudaEvent_t e_evict = nullptr, e_evdone = nullptr;
+    cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[2] = {nullptr, nullptr};
+    int64_t attn_seq[2] = {-1, -1};  // step that last recorded e_attnp[b]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
     int64_t seq = 0;                 // engine-wide step counter
@@ -349,6 +350,7 @@ struct infllm_engine {
         ck(cudaEventRecord(e_evdone, evict_stream), "record");
         ck(cudaStreamWaitEvent(st, e_evdone, 0), "wait");
         lru_seq[0] = lru_seq[1] = -1;
+        attn_seq[0] = attn_seq[1] = -1;
         lookup_seq = -1;
         evict_seq = -1;
     }
@@ -420,10 +422,11 @@ struct infllm_engine {
             ck(cudaStreamWaitEvent(pst, e_call, 0), "wait");
         }
         if (inputs_ready) ck(cudaStreamWaitEvent(pst, inputs_ready, 0), "wait");
-        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0)) {
-            ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");
-            ck(cudaStreamWaitEvent(pst, e_lru[b], 0), "wait");  // qa/qc of this parity
-        }
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+            ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // sel of this parity: attention + LRU k-2
+        // qa/qc/chunk sums of this parity were last read by attention k-2 (and its lookup)
+        if (attn_seq[b] >= 0 && (capture_seq0 < 0 || attn_seq[b] >= capture_seq0))
+            ck(cudaStreamWaitEvent(pst, e_attnp[b], 0), "wait");
         // chunk query sums are double-buffered by step parity: the lookup of step
         // k-2 (which read this parity) ran before attention k-2, covered by e_lru[b]
         void* qa_b = static_cast<uint8_t*>(qa.p) + b * qa_half;
@@ -759,6 +762,8 @@ struct infllm_engine {
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
         // TieredStore bookkeeping runs on its own stream, off the attention critical path
         ck(cudaEventRecord(e_attn, main), "record");
+        ck(cudaEventRecord(e_attnp[b], main), "record");
+        attn_seq[b] = kseq;
         ck(cudaStreamWaitEvent(lru_stream, e_attn, 0), "wait");
         last_lp = lp;
         if (!(debug_skip & 16)) launch_lru(lp, lru_stream);
@@ -1067,7 +1072,8 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
         ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
         for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone,
-                         &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone})
+                         &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone, &e->e_attnp[0],
+                         &e->e_attnp[1]})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
         e->chunk_qsum.alloc(2 * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
@@ -1143,7 +1149,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
                         e->evict_stream})
             if (s2) cudaStreamDestroy(s2);
         for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone, e->e_prep,
-                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone})
+                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone, e->e_attnp[0], e->e_attnp[1]})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;
