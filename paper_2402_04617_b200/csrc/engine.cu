@@ -182,8 +182,10 @@ struct infllm_engine {
     cudaStream_t side_stream = nullptr, lru_stream = nullptr, prep_stream = nullptr, evict_stream = nullptr;
     cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
     cudaEvent_t e_attn = nullptr, e_lrudone = nullptr, e_prep = nullptr, e_lookup = nullptr, e_prepdone = nullptr;
-    cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[2] = {nullptr, nullptr};
-    int64_t attn_seq[2] = {-1, -1};  // step that last recorded e_attnp[b]
+    static constexpr int kPrepAhead = 2;  // chunks the prep stream may run ahead of the attention
+    static constexpr int kPB = kPrepAhead + 1;  // prep-output buffers (qa, qc, chunk sums, key-norm bound)
+    cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[kPB] = {nullptr, nullptr, nullptr};
+    int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
     int64_t seq = 0;                 // engine-wide step counter
@@ -215,7 +217,7 @@ struct infllm_engine {
         DBuf init_k, init_krot, init_v;
         DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
-        DBuf kmax2;  // [2 step parities][G] running max |k|^2 (attention score bound)
+        DBuf kmax2;  // [kPB step buffers][G] running max |k|^2 (attention score bound)
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
     };
     std::vector<Layer> layers;
@@ -350,7 +352,7 @@ struct infllm_engine {
         ck(cudaEventRecord(e_evdone, evict_stream), "record");
         ck(cudaStreamWaitEvent(st, e_evdone, 0), "wait");
         lru_seq[0] = lru_seq[1] = -1;
-        attn_seq[0] = attn_seq[1] = -1;
+        for (auto& a : attn_seq) a = -1;
         lookup_seq = -1;
         evict_seq = -1;
     }
@@ -415,6 +417,7 @@ struct infllm_engine {
         // main-stream step k-2 that last read this parity's buffers
         const int64_t kseq = seq++;
         const int b = static_cast<int>(kseq & 1);
+        const int pb = static_cast<int>(kseq % kPB);  // prep-output buffer (the prep runs up to 2 steps ahead)
         cudaStream_t main = st, side = side_stream, pst = prep_stream, est = evict_stream;
         if (fork) {
             ck(cudaEventRecord(e_call, main), "record");
@@ -424,13 +427,13 @@ struct infllm_engine {
         if (inputs_ready) ck(cudaStreamWaitEvent(pst, inputs_ready, 0), "wait");
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
             ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // sel of this parity: attention + LRU k-2
-        // qa/qc/chunk sums of this parity were last read by attention k-2 (and its lookup)
-        if (attn_seq[b] >= 0 && (capture_seq0 < 0 || attn_seq[b] >= capture_seq0))
-            ck(cudaStreamWaitEvent(pst, e_attnp[b], 0), "wait");
+        // qa/qc/chunk sums of this buffer were last read by attention k-3 (and its lookup)
+        if (attn_seq[pb] >= 0 && (capture_seq0 < 0 || attn_seq[pb] >= capture_seq0))
+            ck(cudaStreamWaitEvent(pst, e_attnp[pb], 0), "wait");
         // chunk query sums are double-buffered by step parity: the lookup of step
         // k-2 (which read this parity) ran before attention k-2, covered by e_lru[b]
-        void* qa_b = static_cast<uint8_t*>(qa.p) + b * qa_half;
-        void* qc_b = static_cast<uint8_t*>(qc.p) + b * qa_half;
+        void* qa_b = static_cast<uint8_t*>(qa.p) + pb * qa_half;
+        void* qc_b = static_cast<uint8_t*>(qc.p) + pb * qa_half;
         int64_t* sel_b = L.sel.as<int64_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
         st = pst;
 
@@ -445,7 +448,7 @@ struct infllm_engine {
         pp.ring_krot = L.ring_krot.p;
         pp.ring_v = L.ring_v.p;
         pp.P = L.P.as<double>();
-        pp.chunk_qsum = chunk_qsum.as<double>() + b * Gs * d;  // double-buffered: the prep may run a step ahead
+        pp.chunk_qsum = chunk_qsum.as<double>() + pb * Gs * d;
         pp.s = s;
         pp.lx = lx;
         pp.lxp = lxp;
@@ -463,9 +466,9 @@ struct infllm_engine {
         pp.tsum = tsum.as<double>();
         // the token-tiled prep maintains the key-norm bound the tcgen05 attention uses
         const bool kbound = d == 128 && dv == 128 && rep <= 8;
-        const int lb = static_cast<int>(L.step & 1);  // this layer's step parity
+        const int lb = static_cast<int>(L.step % kPB);  // this layer's step, modulo the prep buffers
         pp.kmax2 = kbound ? L.kmax2.as<float>() + lb * Gs : nullptr;
-        pp.kmax2_prev = kbound ? L.kmax2.as<float>() + (lb ^ 1) * Gs : nullptr;
+        pp.kmax2_prev = kbound ? L.kmax2.as<float>() + ((lb + kPB - 1) % kPB) * Gs : nullptr;
         last_pp = pp;
         last_bf16 = std::is_same_v<T, bf16>;
         if (!(debug_skip & 8)) launch_prep<T>(pp, st);
@@ -586,7 +589,7 @@ struct infllm_engine {
                 record(evp.first, st);
             }
             LookupParams lp{};
-            lp.qsum = chunk_qsum.as<double>() + b * Gs * d;
+            lp.qsum = chunk_qsum.as<double>() + pb * Gs * d;
             lp.repr = L.repr.p;
             lp.part = L.lookup_part.as<double>();
             lp.U = n_units0;
@@ -762,8 +765,8 @@ struct infllm_engine {
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
         // TieredStore bookkeeping runs on its own stream, off the attention critical path
         ck(cudaEventRecord(e_attn, main), "record");
-        ck(cudaEventRecord(e_attnp[b], main), "record");
-        attn_seq[b] = kseq;
+        ck(cudaEventRecord(e_attnp[pb], main), "record");
+        attn_seq[pb] = kseq;
         ck(cudaStreamWaitEvent(lru_stream, e_attn, 0), "wait");
         last_lp = lp;
         if (!(debug_skip & 16)) launch_lru(lp, lru_stream);
@@ -1041,9 +1044,9 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->dtype = dtype;
         e->device = device;
         e->esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
-        // ring: the local window, the chunk being attended and the next chunk being
-        // prepared concurrently (two-stream pipeline) never share a slot
-        const int64_t need = cfg->local_size + 2 * cfg->chunk_size + 1;
+        // ring: the local window, the chunk being attended and the two chunks the
+        // prep stream may run ahead by never share a slot
+        const int64_t need = cfg->local_size + (1 + infllm_engine::kPrepAhead) * cfg->chunk_size + 1;
         e->R = (need + 127) / 128 * 128;
         e->lxp = (cfg->chunk_size + 127) / 128 * 128;
         for (int a = 0; a < e->d / 2; ++a) {  // rotary.hpp:25-30 (RotaryTable::make)
@@ -1065,17 +1068,17 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         cudaStream_t st = nullptr;
         const size_t es = e->esz;
         e->qa_half = static_cast<size_t>(e->Hs) * e->lxp * e->d * es;
-        e->qa.alloc(2 * e->qa_half, st);
-        e->qc.alloc(2 * e->qa_half, st);
+        e->qa.alloc(infllm_engine::kPB * e->qa_half, st);
+        e->qc.alloc(infllm_engine::kPB * e->qa_half, st);
         ck(cudaStreamCreateWithFlags(&e->side_stream, cudaStreamNonBlocking), "side stream");
         ck(cudaStreamCreateWithFlags(&e->lru_stream, cudaStreamNonBlocking), "lru stream");
         ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
         ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
         for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone,
                          &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone, &e->e_attnp[0],
-                         &e->e_attnp[1]})
+                         &e->e_attnp[1], &e->e_attnp[2]})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
-        e->chunk_qsum.alloc(2 * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
+        e->chunk_qsum.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
         e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
         e->mass_m.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
@@ -1094,7 +1097,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ring_krot.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
             L.ring_v.alloc(static_cast<size_t>(e->Gs) * e->R * e->dv * es, st);
             L.P.alloc(static_cast<size_t>(e->R) * e->Gs * e->d * sizeof(double), st);
-            L.kmax2.alloc(2 * static_cast<size_t>(e->Gs) * sizeof(float), st);
+            L.kmax2.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * sizeof(float), st);
             const size_t ni = static_cast<size_t>(std::max<int64_t>(cfg->init_size, 1));
             L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
             if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
@@ -1149,7 +1152,8 @@ int infllm_engine_destroy(infllm_engine_t e) {
                         e->evict_stream})
             if (s2) cudaStreamDestroy(s2);
         for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone, e->e_prep,
-                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone, e->e_attnp[0], e->e_attnp[1]})
+                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone, e->e_attnp[0], e->e_attnp[1],
+                        e->e_attnp[2]})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;

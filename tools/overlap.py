@@ -9,7 +9,7 @@ Q = torch.randn((n, 32, 128), generator=g, device='cuda').bfloat16()
 K = torch.randn((n, 8, 128), generator=g, device='cuda').bfloat16()
 V = torch.randn((n, 8, 128), generator=g, device='cuda').bfloat16()
 O = torch.empty_like(Q)
-for skip in [0, 32, 14, 30]:
+for skip in [0, 2, 4, 8, 16, 32]:
     eng = StreamEngine(EngineConfig.make(**bench.CFG), ModelShape.make(**bench.SHAPE), dtype=torch.bfloat16)
     eng.reserve(n)
     eng.set_option("debug_skip", skip)
