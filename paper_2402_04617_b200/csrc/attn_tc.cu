@@ -15,8 +15,22 @@ void debug_read_attn_timestamps(unsigned long long* out) {
 }
 }  // namespace infllm
 #define ATS(k, jj)                                                                          \
-    if (ATTN_TS && blockIdx.x == 0 && blockIdx.y == 0 && (jj) >= 20 && (jj) < 36)            \
-        g_attn_ts[((jj) - 20) / 2 * 8 + (k)] = clock64();
+    if (ATTN_TS && blockIdx.x == ATTN_TS_M && blockIdx.y == 0 && (jj) >= ATTN_TS_J0 && (jj) < ATTN_TS_J0 + 16) \
+        g_attn_ts[((jj) - ATTN_TS_J0) / 2 * 8 + (k)] = clock64();
+#define ATS1(idx)                                                                           \
+    if (ATTN_TS && blockIdx.x == ATTN_TS_M && blockIdx.y == 0) g_attn_ts[idx] = clock64();
+#ifndef ATTN_CTA_TS
+#define ATTN_CTA_TS 0
+#endif
+#ifndef ATTN_MAX_CLUSTER
+#define ATTN_MAX_CLUSTER 8
+#endif
+#ifndef ATTN_TS_J0
+#define ATTN_TS_J0 20
+#endif
+#ifndef ATTN_TS_M
+#define ATTN_TS_M 0
+#endif
 #ifndef ATTN_TS
 #define ATTN_TS 0
 #endif
@@ -382,6 +396,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     int32_t* sSel = reinterpret_cast<int32_t*>(sML + 4 * 128);                         // [k_m] unit ids
     int32_t* sLen = sSel + kMaxSel;                                                    // [k_m] unit lengths
 
+    if (threadIdx.x == 0) ATS1(56);
+    uint64_t cta_t0 = 0;
+    if (ATTN_CTA_TS && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(cta_t0));
+        if (blockIdx.x == 3 && blockIdx.y == 0) {
+            g_attn_ts[10] = cta_t0;
+            g_attn_ts[11] = clock64();
+        }
+        atomicMin(reinterpret_cast<unsigned long long*>(g_attn_ts) + 0, cta_t0);
+        atomicMax(reinterpret_cast<unsigned long long*>(g_attn_ts) + 1, cta_t0);
+    }
     const AttnParams& a = P.a;
     const bool mass_in_kernel = a.want_mass && a.n_sel <= kMassSlots;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -433,6 +458,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     __syncthreads();
     cluster_sync();  // every CTA's barriers are initialised before any multicast targets them
     tc_fence_after();
+    if (threadIdx.x == 0) ATS1(57);
     const uint32_t tbase = *tmem_slot;
     const uint32_t idesc = idesc_bf16(128, 128);
     const uint16_t cmask = static_cast<uint16_t>((1u << P.csize) - 1u);
@@ -492,10 +518,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             auto qk = [&](int jj) {
                 const Tile t = ts.get(a, jj);
                 const int s = jj % kKS;
-                if ((jj & 1) == 0) ATS(2, jj - 2);
                 mbar_wait(k_full + s, (jj / kKS) & 1);
                 tc_fence_after();
-                if ((jj & 1) == 0) ATS(5, jj - 2);
                 const uint32_t qb = clamped_operand(t.mode) ? aQc : aQa;
                 const uint32_t kb = aK + s * kStageBytes;
                 const uint32_t d = tbase + col_s(jj & 1);
@@ -506,13 +530,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 }
                 mma_commit_mc(k_empty + s, cmask);
                 mma_commit(s_full + (jj & 1));
-                if ((jj & 1) == 0) ATS(3, jj - 2);
             };
             auto pv = [&](int jj) {
                 const int w = jj & 1;
-                if (w == 0) ATS(6, jj);
                 mbar_wait(p_full + w, (jj >> 1) & 1);
-                if (w == 0) ATS(7, jj);
                 const int s = jj % kVS;
                 mbar_wait(v_full + s, (jj / kVS) & 1);
                 tc_fence_after();
@@ -525,7 +546,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                            (fast || jj > 1 || kk > 0) ? 1u : 0u);
                 mma_commit_mc(v_empty + s, cmask);
                 mma_commit(o_done + w);
-                if (w == 0) ATS(0, jj);
             };
             // Three issuers (MMA issue is nearly synchronous: one thread cannot keep
             // the tensor pipe busy): warp 1 every P V in tile order (O sums in a
@@ -540,11 +560,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             if (fast) {
                 if (pv_issuer) {
                     mbar_wait(o_zero, 0);
-                    for (int j = 0; j < ts.T; ++j) pv(j);
+                    for (int j = 0; j < ts.T; ++j) {
+                        pv(j);
+                        if (!(j & 1)) ATS(7, j);
+                    }
                 } else {
                     for (int j = 0; j + 2 < ts.T; ++j) {
                         mbar_wait(s_free + (j & 1), (j >> 1) & 1);
+                        if (!(j & 1)) ATS(5, j);
                         qk(j + 2);
+                        if (!(j & 1)) ATS(6, j);
                     }
                 }
             } else if (pv_issuer) {
@@ -608,6 +633,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             __syncwarp();
             if (lane == 0) mbar_arrive(o_zero);
         }
+        if (warp == 4 && lane == 0) ATS1(58);
         const uint32_t tP = fast ? tl + col_p(wg) : tS;  // where P_j goes
         float m_run = fast ? m_row : -INFINITY, l_run = 0.f;
         int n_mine = 0;
@@ -629,7 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             const bool edge = __any_sync(0xffffffffu, klo > 0 || kmax < 128);
             mbar_wait(s_full + wg, n_mine & 1);
             tc_fence_after();
-            if (wg == 0 && warp == 4 && lane == 0) ATS(1, j);
+            if (wg == 0 && warp == 4 && lane == 0) ATS(0, j);
             float x[128];
             {
                 uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -654,6 +680,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 __syncwarp();
                 if (lane == 0) mbar_arrive(s_free + wg);
             }
+            if (wg == 0 && warp == 4 && lane == 0) ATS(1, j);
             if (edge) {
 #pragma unroll
                 for (int c = 0; c < 128; ++c)
@@ -696,6 +723,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             // they share the MUFU pipes of every SMSP, so overlapping them only
             // stretches both, while alternating keeps the tensor pipe fed
             if (ATTN_TURN && j > 0) asm volatile("bar.sync %0, 256;" ::"r"(3 + wg) : "memory");
+            if (wg == 0 && warp == 4 && lane == 0) ATS(2, j);
             if (fast && n_mine > 0) {  // P_w is free once the previous P V of this warpgroup completed
                 mbar_wait(o_done + wg, (n_mine - 1) & 1);
                 tc_fence_after();
@@ -724,9 +752,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 tmem_st16(tP + 16 * ch, pk);  // keys 32*ch.. packed two per column
             }
             if (ATTN_TURN && j + 1 < ts.T) asm volatile("bar.arrive %0, 256;" ::"r"(4 - wg) : "memory");
+            if (wg == 0 && warp == 4 && lane == 0) ATS(3, j);
             const float rs = (s0 + s1) + (s2 + s3);
             l_run += rs;
-            if (wg == 0 && warp == 4 && lane == 0) ATS(4, j);
             if (t.slot >= 0 && a.want_mass) {
                 if (mass_in_kernel) {
                     sMassE[t.slot * 128 + row] = row_ok ? rs : 0.f;
@@ -741,6 +769,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(p_full + wg);
+            if (wg == 0 && warp == 4 && lane == 0) ATS(4, j);
         }
         // ---------------- epilogue: merge the two partial softmaxes, O / l -> bf16
         sML[(wg * 2) * 128 + row] = m_run;
@@ -750,6 +779,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         if (n0 > 0) mbar_wait(o_done, (n0 - 1) & 1);
         if (n1 > 0) mbar_wait(o_done + 1, (n1 - 1) & 1);
         tc_fence_after();
+        if (warp == 4 && lane == 0) ATS1(59);
         asm volatile("bar.sync 1, 256;" ::: "memory");
         const float m0 = sML[row], l0 = sML[128 + row], m1 = sML[256 + row], l1 = sML[384 + row];
         const float mf = fmaxf(m0, m1);
@@ -810,8 +840,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         }
     }
     tc_fence_before();
+    if (threadIdx.x == 128) ATS1(60);
     __syncthreads();
+    if (threadIdx.x == 128) ATS1(61);
     cluster_sync();  // no CTA leaves while cluster peers may still signal its barriers
+    if (threadIdx.x == 128) ATS1(62);
+    if (ATTN_CTA_TS && threadIdx.x == 0) {
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        atomicMin(reinterpret_cast<unsigned long long*>(g_attn_ts) + 2, t1);
+        atomicMax(reinterpret_cast<unsigned long long*>(g_attn_ts) + 3, t1);
+        atomicMax(reinterpret_cast<unsigned long long*>(g_attn_ts) + 4, t1 - cta_t0);
+        atomicMin(reinterpret_cast<unsigned long long*>(g_attn_ts) + 5, t1 - cta_t0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_attn_ts) + 6, t1 - cta_t0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_attn_ts) + 7, 1ull);
+        if (blockIdx.x == 3 && blockIdx.y == 0) {
+            g_attn_ts[12] = t1;
+            g_attn_ts[13] = clock64();
+        }
+    }
     if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
@@ -845,7 +892,7 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     const uint64_t R = static_cast<uint64_t>(a.R);
     const uint64_t ucap = static_cast<uint64_t>(a.unit_cap > 0 ? a.unit_cap : 1);
     int csize = 1;
-    while (csize * 2 <= 8 && a.rep % (csize * 2) == 0) csize *= 2;
+    while (csize * 2 <= ATTN_MAX_CLUSTER && a.rep % (csize * 2) == 0) csize *= 2;
     const int box = 128 / csize;
     TmapKey key{{a.qa, a.qc, a.ring_k, a.ring_krot, a.ring_v, a.init_k, a.init_v, a.unit_k, a.unit_v},
                 {static_cast<uint64_t>(a.H) * a.lxp, a.G * R, ucap,
@@ -910,6 +957,15 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     la[1].val.clusterDim.z = 1;
     cfg.attrs = la;
     cfg.numAttrs = 2;
+    if (getenv("INFLLM_ATTN_OCC")) {
+        static bool once = false;
+        if (!once) {
+            once = true;
+            int nc = 0;
+            cudaOccupancyMaxActiveClusters(&nc, k_attn_tc, &cfg);
+            fprintf(stderr, "k_attn_tc: grid %u x %u, cluster %d, max active clusters %d\n", grid.x, grid.y, csize, nc);
+        }
+    }
     cudaLaunchKernelEx(&cfg, k_attn_tc, P);
     return 1;
 }

@@ -17,7 +17,9 @@ ts = np.zeros(64, np.uint64)
 _lib.check(_lib.lib().infllm_debug_timestamps(ts.ctypes.data))
 t = ts.astype(np.int64)
 u = t[0:64].reshape(8, 8); base = u[0, 0]
-print("tile j (WG0): pv_issued s_seen(j) k_wait_start(j+2) qk_issued(j+2) exp_done(j) k_ready(j+2) p_wait_start p_ready")
+names = ["s_seen", "s_free", "exp_go", "exp_end", "p_arr", "qk+2_go", "qk+2_end", "pv_end"]
+print("tile(WG0) " + " ".join(f"{n:>9s}" for n in names))
 for j in range(8):
-    r = [int(x - base) for x in u[j]]
-    print(20 + 2 * j, r, [r[k] - r[k - 1] for k in range(1, 6)])
+    print(2 * j, " ".join(f"{int(x - base):9d}" for x in u[j]))
+e = t[56:63] - t[56]
+print("entry->cluster_sync", e[1], " ->flag", e[2], " tile0 s_seen", t[0] - t[56], " ->all PV done", e[3], " ->epilogue end", e[4], " ->syncthreads", e[5], " ->cluster_sync", e[6])
