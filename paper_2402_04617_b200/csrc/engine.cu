@@ -277,7 +277,7 @@ struct infllm_engine {
     bool capturing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_attn_ev = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_lookup_ev = nullptr;
-    static constexpr int kNB = 3;  // host-pointer staging buffers
+    static constexpr int kNB = 3;  // host-pointer staging buffers (groups of kGroup chunks)
     DBuf stage_q[kNB], stage_k[kNB], stage_v[kNB], stage_o[kNB];
 
     void record(cudaEvent_t e, cudaStream_t st) {
@@ -797,16 +797,18 @@ struct infllm_engine {
         }
     }
 
-    // host-pointer stream: per chunk H2D of q/k/v into staging buffers, the
-    // step, D2H of the output; copies run on their own streams and overlap the
-    // neighbouring chunks' compute
+    // host-pointer stream: H2D of q/k/v into staging buffers and D2H of the
+    // outputs in groups of kGroup chunks (PCIe moves multi-MB copies in both
+    // directions at once far better than per-chunk ones), on their own streams,
+    // overlapping the neighbouring groups' compute
+    static constexpr int kGroup = 16;
     template <typename T>
     void run_chunks_host(int li, const void* hq, const void* hk, const void* hv, int64_t n, void* hout,
                          cudaStream_t st) {
-        const int64_t C = cfg.chunk_size;
-        const int64_t nch = (n + C - 1) / C;
-        std::vector<cudaEvent_t> ev_in(nch), ev_comp(nch), ev_out(nch);
-        for (int64_t t = 0; t < nch; ++t) {
+        const int64_t C = cfg.chunk_size, GC = kGroup * C;
+        const int64_t ng = (n + GC - 1) / GC;
+        std::vector<cudaEvent_t> ev_in(ng), ev_comp(ng), ev_out(ng);
+        for (int64_t t = 0; t < ng; ++t) {
             ev_in[t] = take_event();
             ev_comp[t] = take_event();
             ev_out[t] = take_event();
@@ -815,38 +817,43 @@ struct infllm_engine {
         ck(cudaEventRecord(fork, st), "fork");
         ck(cudaStreamWaitEvent(h2d_stream, fork, 0), "fork");
         ck(cudaStreamWaitEvent(d2h_stream, fork, 0), "fork");
-        auto h2d = [&](int64_t t) {
-            const int64_t off = t * C, lx = std::min<int64_t>(C, n - off);
-            const int b = static_cast<int>(t % kNB);
-            if (t >= kNB) {
-                ck(cudaStreamWaitEvent(h2d_stream, ev_comp[t - kNB], 0), "wait");
-            }
-            ck(cudaMemcpyAsync(stage_q[b].p, at(hq, off, Hs * d), lx * Hs * d * esz, cudaMemcpyHostToDevice, h2d_stream),
-               "H2D");
-            ck(cudaMemcpyAsync(stage_k[b].p, at(hk, off, Gs * d), lx * Gs * d * esz, cudaMemcpyHostToDevice, h2d_stream),
-               "H2D");
-            ck(cudaMemcpyAsync(stage_v[b].p, at(hv, off, Gs * dv), lx * Gs * dv * esz, cudaMemcpyHostToDevice,
+        auto h2d = [&](int64_t gi) {
+            const int64_t off = gi * GC, len = std::min<int64_t>(GC, n - off);
+            const int b = static_cast<int>(gi % kNB);
+            if (gi >= kNB) ck(cudaStreamWaitEvent(h2d_stream, ev_comp[gi - kNB], 0), "wait");
+            ck(cudaMemcpyAsync(stage_q[b].p, at(hq, off, Hs * d), len * Hs * d * esz, cudaMemcpyHostToDevice,
                                h2d_stream),
                "H2D");
-            ck(cudaEventRecord(ev_in[t], h2d_stream), "record");
+            ck(cudaMemcpyAsync(stage_k[b].p, at(hk, off, Gs * d), len * Gs * d * esz, cudaMemcpyHostToDevice,
+                               h2d_stream),
+               "H2D");
+            ck(cudaMemcpyAsync(stage_v[b].p, at(hv, off, Gs * dv), len * Gs * dv * esz, cudaMemcpyHostToDevice,
+                               h2d_stream),
+               "H2D");
+            ck(cudaEventRecord(ev_in[gi], h2d_stream), "record");
         };
-        for (int64_t t = 0; t < std::min<int64_t>(kNB - 1, nch); ++t) h2d(t);
-        for (int64_t t = 0; t < nch; ++t) {
-            if (t + kNB - 1 < nch) h2d(t + kNB - 1);
-            const int64_t off = t * C, lx = std::min<int64_t>(C, n - off);
-            const int b = static_cast<int>(t % kNB);
-            if (t >= kNB) ck(cudaStreamWaitEvent(st, ev_out[t - kNB], 0), "wait");  // stage_o[b] drained
-            step<T>(li, stage_q[b].p, stage_k[b].p, stage_v[b].p, lx, false, stage_o[b].p, st, t == 0, ev_in[t]);
-            ck(cudaEventRecord(ev_comp[t], st), "record");
-            ck(cudaStreamWaitEvent(d2h_stream, ev_comp[t], 0), "wait");
-            ck(cudaMemcpyAsync(const_cast<void*>(at(hout, off, Hs * dv)), stage_o[b].p, lx * Hs * dv * esz,
+        for (int64_t gi = 0; gi < std::min<int64_t>(kNB - 1, ng); ++gi) h2d(gi);
+        for (int64_t gi = 0; gi < ng; ++gi) {
+            if (gi + kNB - 1 < ng) h2d(gi + kNB - 1);
+            const int64_t goff = gi * GC, glen = std::min<int64_t>(GC, n - goff);
+            const int b = static_cast<int>(gi % kNB);
+            if (gi >= kNB) ck(cudaStreamWaitEvent(st, ev_out[gi - kNB], 0), "wait");  // stage_o[b] drained
+            for (int64_t off = 0; off < glen; off += C) {
+                const int64_t lx = std::min<int64_t>(C, glen - off);
+                step<T>(li, at(stage_q[b].p, off, Hs * d), at(stage_k[b].p, off, Gs * d),
+                        at(stage_v[b].p, off, Gs * dv), lx, false, const_cast<void*>(at(stage_o[b].p, off, Hs * dv)), st,
+                        gi == 0 && off == 0, off == 0 ? ev_in[gi] : nullptr);
+            }
+            ck(cudaEventRecord(ev_comp[gi], st), "record");
+            ck(cudaStreamWaitEvent(d2h_stream, ev_comp[gi], 0), "wait");
+            ck(cudaMemcpyAsync(const_cast<void*>(at(hout, goff, Hs * dv)), stage_o[b].p, glen * Hs * dv * esz,
                                cudaMemcpyDeviceToHost, d2h_stream),
                "D2H");
-            ck(cudaEventRecord(ev_out[t], d2h_stream), "record");
+            ck(cudaEventRecord(ev_out[gi], d2h_stream), "record");
         }
-        ck(cudaStreamWaitEvent(st, ev_out[nch - 1], 0), "join");
-        ck(cudaStreamWaitEvent(st, ev_in[nch - 1], 0), "join");
-        for (int64_t t = 0; t < nch; ++t) {
+        ck(cudaStreamWaitEvent(st, ev_out[ng - 1], 0), "join");
+        ck(cudaStreamWaitEvent(st, ev_in[ng - 1], 0), "join");
+        for (int64_t t = 0; t < ng; ++t) {
             ev_pool.push_back(ev_in[t]);
             ev_pool.push_back(ev_comp[t]);
             ev_pool.push_back(ev_out[t]);
@@ -870,7 +877,7 @@ struct infllm_engine {
         ensure_units(L, L.n_units + (L.pend_count + n) / cfg.unit_size + 2, st);
         ensure_trace(L, L.trace_count + steps * std::max<int64_t>(cfg.n_lookup, 1), st);
         if (host && !stage_q[0].p) {
-            const int64_t C = cfg.chunk_size;
+            const int64_t C = cfg.chunk_size * kGroup;
             for (int b = 0; b < kNB; ++b) {
                 stage_q[b].alloc(C * Hs * d * esz, st, false);
                 stage_k[b].alloc(C * Gs * d * esz, st, false);
