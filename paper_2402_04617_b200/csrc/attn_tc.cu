@@ -781,6 +781,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         tc_fence_after();
         if (warp == 4 && lane == 0) ATS1(59);
         asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (warp == 4 && lane == 0) ATS1(53);
         const float m0 = sML[row], l0 = sML[128 + row], m1 = sML[256 + row], l1 = sML[384 + row];
         const float mf = fmaxf(m0, m1);
         const float a0 = l0 > 0.f ? ex2(m0 - mf) : 0.f;
@@ -816,23 +817,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                     dst[v4] = make_uint4(wv[4 * v4], wv[4 * v4 + 1], wv[4 * v4 + 2], wv[4 * v4 + 3]);
             }
         }
+        if (warp == 4 && lane == 0) ATS1(54);
         if (mass_in_kernel) {
             // per-unit attention mass of this CTA's rows: sum_rows e_u 2^(m_u - m) / l
-            // (engine.hpp:271-283), fp64, fixed order: lanes (xor tree), then quarters 0..3
-            if (wg == 0) {
-                for (int u = 0; u < a.n_sel; ++u) {
-                    const float e = sMassE[u * 128 + row];
-                    const float mu = sMassM[u * 128 + row];
-                    double w = (row_ok && e > 0.f) ? static_cast<double>(e * ex2(mu - mf) * inv) : 0.0;
-                    w = warp_sum_d(w);
-                    if (lane == 0) sRed[u * 4 + q4] = w;
+            // (engine.hpp:271-283) in fp64. Warpgroup w reduces units 8w..8w+7: each
+            // lane holds its row's 8 values, a transposing butterfly (masks 16, 8, 4,
+            // then 2, 1) leaves lane l with one unit's warp sum; quarters are added
+            // in order 0..3. Fixed order, so bitwise reproducible.
+            double v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int u = 8 * wg + k;
+                const float e = u < a.n_sel ? sMassE[u * 128 + row] : 0.f;
+                const float mu = u < a.n_sel ? sMassM[u * 128 + row] : 0.f;
+                v[k] = (row_ok && e > 0.f) ? static_cast<double>(e * ex2(mu - mf) * inv) : 0.0;
+            }
+#pragma unroll
+            for (int lvl = 0; lvl < 3; ++lvl) {
+                const int mask = 16 >> lvl, half = 4 >> lvl;
+                const bool upper = (lane & mask) != 0;
+#pragma unroll
+                for (int k = 0; k < half; ++k) {
+                    const double send = upper ? v[k] : v[k + half];
+                    const double keep = upper ? v[k + half] : v[k];
+                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
                 }
-                asm volatile("bar.sync 2, 128;" ::: "memory");
-                const int tid = threadIdx.x - 128;
-                if (tid < a.n_sel) {
-                    const double* r4 = sRed + tid * 4;
-                    a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
-                }
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+            const int slot = 8 * wg + ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+            if ((lane & 3) == 0) sRed[slot * 4 + q4] = v[0];
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            const int tid = threadIdx.x - 128;
+            if (tid < a.n_sel) {
+                const double* r4 = sRed + tid * 4;
+                a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
             }
         } else if (row_ok && a.want_mass && wg == 0) {
             a.row_m[static_cast<int64_t>(h) * a.lx + i] = mf * 0.6931471805599453f;

@@ -23,3 +23,4 @@ for j in range(8):
     print(2 * j, " ".join(f"{int(x - base):9d}" for x in u[j]))
 e = t[56:63] - t[56]
 print("entry->cluster_sync", e[1], " ->flag", e[2], " tile0 s_seen", t[0] - t[56], " ->all PV done", e[3], " ->epilogue end", e[4], " ->syncthreads", e[5], " ->cluster_sync", e[6])
+print("all PV done -> bar.sync", t[53] - t[59], " -> O stored", t[54] - t[59], " -> masses+end", t[60] - t[59])
