@@ -797,9 +797,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             const int col = 64 * wg + 32 * c4;
             uint32_t r0[32], r1[32];
             tmem_ld32(tl + col_o(0) + col, r0);
-            tmem_ld32(tl + col_o(1) + col, r1);
+            if (!fast) tmem_ld32(tl + col_o(1) + col, r1);  // fast path: col_o(1) holds P, one shared O
             tmem_wait_ld_r(r0);
-            tmem_wait_ld_r(r1);
+            if (!fast) tmem_wait_ld_r(r1);
             if (row_ok) {
                 uint32_t wv[16];
 #pragma unroll
