@@ -93,10 +93,16 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment to start: only rows taken after this point
+            # (inside the timed region) are summarised
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.first = len(self.rows)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -116,6 +122,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        self.rows = self.rows[getattr(self, "first", 0):]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         def num(x):
@@ -276,6 +283,7 @@ def run_b200(args, rank, world, local_rank):
             traffic = None
     lk_bytes = lookup_bytes(steps, CFG, Hkv, d, H)
     lk_ms = prof["lookup_ms"] / max(1, args.steps)
+    iso = isolated_kernels(eng, steps, H, Hkv, d, dev) if rank == 0 else {}
 
     if rank == 0:
         cpu = None
@@ -303,15 +311,58 @@ def run_b200(args, rank, world, local_rank):
                                    "of the same K streams (event nodes perturb the pipeline, so the headline "
                                    "region has none); achieved = algorithmic QK^T+PV flops / event time",
                          "peak_src": peaks["src"] + " burst bf16 (sustained %.1f)" % peaks["bf16_sust"],
-                         "lookup": {"achieved_gbs": lk_bytes / (lk_ms / 1000.0) / 1e9 if lk_ms > 0 else None,
+                         "lookup": {"in_stream_gbs": lk_bytes / (lk_ms / 1000.0) / 1e9 if lk_ms > 0 else None,
                                     "peak_gbs": peaks["hbm"], "bytes_per_stream": lk_bytes,
-                                    "ms_per_stream": lk_ms}},
+                                    "in_stream_ms_per_stream": lk_ms,
+                                    "note": "in-stream: the lookup shares the GPU with the attention of the previous "
+                                            "step (20 free SMs); isolated: same launch alone, steady state"} | iso},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+
+
+def isolated_kernels(eng, steps, H, Hkv, d, dev):
+    """Steady-state per-launch times of the lookup (relevance scan + exact top-k)
+    and of the attention re-launched alone with the last chunk step's
+    parameters (infllm_debug_kernel_bench; run after the timed work, it
+    disturbs the engine state), plus the standalone lookup at the C3 index
+    size (U = 8159 units, 1M-token stream) where the scan is HBM-sized."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2402_04617_b200 import _lib, lookup
+
+    out = {}
+    try:
+        last = steps[-1]
+        us = C.c_double()
+        _lib.check(_lib.lib().infllm_debug_kernel_bench(eng.h, 1, 50, C.byref(us)))
+        b = last["units"] * CFG["n_repr"] * Hkv * d * 2 + last["lx"] * H * d * 2
+        out["isolated_us"] = us.value
+        out["isolated_gbs"] = b / (us.value * 1e-6) / 1e9
+        out["isolated_units"] = last["units"]
+        U = 8159
+        reprk = torch.randn(U, Hkv, CFG["n_repr"], d, device=dev).bfloat16()
+        qsum = torch.randn(Hkv, d, device=dev, dtype=torch.float64)
+        for _ in range(3):
+            lookup(qsum, reprk, CFG["n_lookup"])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(20):
+            lookup(qsum, reprk, CFG["n_lookup"])
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / 20
+        out["c3_units"] = U
+        out["c3_us"] = ms * 1000.0
+        out["c3_gbs"] = U * CFG["n_repr"] * Hkv * d * 2 / (ms * 1e-3) / 1e9
+    except Exception as ex:  # diagnostic only
+        out["isolated_error"] = str(ex)
+    return out
 
 
 def run_e2e(eng, Q, K, V, n, C, dev, args, world):
@@ -352,7 +403,7 @@ def run_e2e(eng, Q, K, V, n, C, dev, args, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--tokens", type=int, default=N_TOKENS)
