@@ -334,7 +334,7 @@ def isolated_kernels(eng, steps, H, Hkv, d, dev):
 
     import torch
 
-    from paper_2402_04617_b200 import _lib, lookup
+    from paper_2402_04617_b200 import _lib
 
     out = {}
     try:
@@ -345,21 +345,38 @@ def isolated_kernels(eng, steps, H, Hkv, d, dev):
         out["isolated_us"] = us.value
         out["isolated_gbs"] = b / (us.value * 1e-6) / 1e9
         out["isolated_units"] = last["units"]
-        U = 8159
-        reprk = torch.randn(U, Hkv, CFG["n_repr"], d, device=dev).bfloat16()
-        qsum = torch.randn(Hkv, d, device=dev, dtype=torch.float64)
-        for _ in range(3):
-            lookup(qsum, reprk, CFG["n_lookup"])
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(20):
-            lookup(qsum, reprk, CFG["n_lookup"])
-        e1.record()
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / 20
-        out["c3_units"] = U
-        out["c3_us"] = ms * 1000.0
-        out["c3_gbs"] = U * CFG["n_repr"] * Hkv * d * 2 / (ms * 1e-3) / 1e9
+        # standalone lookups on random bf16 indices, timed as CUDA-graph replays
+        # (device time, no host gaps): the C3 index (8159 units, 1M-token stream)
+        # and a 131072-unit index where the relevance scan is HBM-sized
+        for tag, U, km in (("c3", 8159, CFG["n_lookup"]), ("scan131k", 131072, 0)):
+            reprk = torch.randn(U, Hkv, CFG["n_repr"], d, device=dev).bfloat16()
+            qsum = torch.randn(Hkv, d, device=dev, dtype=torch.float64)
+            rel = torch.empty(U, device=dev, dtype=torch.float64)
+            ids = torch.empty(max(1, km), device=dev, dtype=torch.int64)
+            s_ = torch.cuda.Stream(dev)
+
+            def call():
+                _lib.check(_lib.lib().infllm_lookup(qsum.data_ptr(), reprk.data_ptr(), _lib.DTYPE_BF16, U,
+                                                    CFG["n_repr"], Hkv, d, km, rel.data_ptr(), ids.data_ptr(),
+                                                    s_.cuda_stream))
+            with torch.cuda.stream(s_):
+                call()
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s_):
+                    for _ in range(10):
+                        call()
+                g.replay()
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s_)
+                g.replay()
+                e1.record(s_)
+                torch.cuda.synchronize(dev)
+            ms = e0.elapsed_time(e1) / 10
+            out[f"{tag}_units"] = U
+            out[f"{tag}_us"] = ms * 1000.0
+            out[f"{tag}_gbs"] = U * CFG["n_repr"] * Hkv * d * 2 / (ms * 1e-3) / 1e9
     except Exception as ex:  # diagnostic only
         out["isolated_error"] = str(ex)
     return out

@@ -710,8 +710,73 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
     if (threadIdx.x == 0) *p.done = 0;
 }
 
+// bf16, head_dim 128, r_k 4, <= 8 KV groups (the C1-C3 shapes): lane l owns
+// dims [4l, 4l+4) of every representative row, so its slice of the chunk query
+// sums stays in registers (no shared-memory traffic per unit); warps stride
+// over units and keep all 32 row loads of a unit in flight before the math.
+// Single shard: per lane the groups are summed in order 0..G-1, then one warp
+// tree; sharded: one warp tree per group (partials exchanged by the caller).
+__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
+    const int lane = threadIdx.x % 32;
+    const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+    double q[8][4];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+    for (int64_t u = warp0; u < p.U; u += nwarps) {
+        const bf16* base = static_cast<const bf16*>(p.repr) + u * p.G * 512 + 4 * lane;
+        uint2 x[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r)
+            if (r < 4 * p.G) x[r] = __ldcs(reinterpret_cast<const uint2*>(base + r * 128));
+        double rel = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= p.G) break;
+            double a = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint2 v = x[4 * g + r];
+                a = fma(q[g][0], static_cast<double>(__uint_as_float(v.x << 16)), a);
+                a = fma(q[g][1], static_cast<double>(__uint_as_float(v.x & 0xffff0000u)), a);
+                a = fma(q[g][2], static_cast<double>(__uint_as_float(v.y << 16)), a);
+                a = fma(q[g][3], static_cast<double>(__uint_as_float(v.y & 0xffff0000u)), a);
+            }
+            if (p.fused) {
+                rel += a;
+            } else {
+                a = warp_sum_d(a);
+                if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+            }
+        }
+        if (p.fused) {
+            rel = warp_sum_d(rel);
+            if (lane == 0) p.rel[u] = rel;
+        }
+    }
+    if (p.fused != 1) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+    if (threadIdx.x == 0) *p.done = 0;
+}
+
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
     const int warps = 8;
+    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8) {
+        // one unit per warp up to two waves of resident blocks, then warps stride
+        const int64_t want = (p.U + warps - 1) / warps;
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(want, 148 * 4));
+        k_lookup_reg<<<blocks, warps * 32, 0, st>>>(p);
+        return;
+    }
     const unsigned blocks = static_cast<unsigned>((p.U + warps - 1) / warps);
     const size_t smem = sizeof(double) * p.G * (p.d + 2 * ((p.d + 15) / 16));
     if (dtype_bf16)

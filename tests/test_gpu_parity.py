@@ -205,3 +205,21 @@ def test_topk_ties_and_sizes(U, k):
     want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
     assert np.array_equal(rel.cpu().numpy(), want)
     assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))
+
+
+@pytest.mark.parametrize("U,k", [(991, 16), (8159, 16), (20000, 32)])
+def test_lookup_bf16_c2_shape(U, k):
+    """The register-resident relevance scan (bf16, d 128, r_k 4, 8 KV groups) and
+    the multi-block top-k at C2/C3 index sizes: small-integer data makes every
+    fp64 sum exact, so rel must equal the oracle's bit for bit."""
+    from paper_2402_04617_b200 import lookup
+
+    rng = np.random.default_rng(U + k)
+    G, rk, d, H = 8, 4, 128, 32
+    reprk = rng.integers(-3, 4, size=(U, G, rk, d)).astype(np.float32)
+    qb = rng.integers(-2, 3, size=(4, H, d)).astype(np.float32)
+    qsum = qb.astype(np.float64).reshape(4, G, H // G, d).sum(axis=(0, 2))
+    rel, ids = lookup(torch.from_numpy(qsum).cuda(), torch.from_numpy(reprk).cuda().bfloat16(), k)
+    want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
+    assert np.array_equal(rel.cpu().numpy(), want)
+    assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))

@@ -3,7 +3,8 @@ import sys
 sys.path.insert(0, '.')
 import torch
 from paper_2402_04617_b200 import lookup
-G, rk, d, km = 8, 4, 128, 16
+G, rk, d = 8, 4, 128
+km = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 for U in [991, 8159, 32768, 131072]:
     repr_keys = torch.randn(U, G, rk, d, device="cuda").bfloat16()
     qsum = torch.randn(G, d, device="cuda", dtype=torch.float64)
