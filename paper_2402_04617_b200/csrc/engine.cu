@@ -328,6 +328,8 @@ struct infllm_engine {
         L.rel.grow(cap * sizeof(double), st);
         L.relw.grow(cap * sizeof(double), st);
         L.lookup_part.grow(cap * Gt * sizeof(double), st);
+        // multi-block top-k candidates (sized here: no allocation may happen inside a captured step)
+        L.cand.grow(static_cast<size_t>(topk_multi_scratch(cap, std::max<int64_t>(cfg.n_lookup, 1))) * 16, st);
         L.unit_cap = cap;
     }
 
@@ -617,8 +619,7 @@ struct infllm_engine {
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
             if (lp.fused == 2) {
-                const int64_t nc = topk_multi_scratch(n_units0, n_sel);
-                L.cand.grow(static_cast<size_t>(nc) * 16, st);
+                const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
                     launch_topk_multi(L.rel.as<double>(), n_units0, n_sel, cv, reinterpret_cast<int64_t*>(cv + nc),

@@ -223,3 +223,30 @@ def test_lookup_bf16_c2_shape(U, k):
     want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
     assert np.array_equal(rel.cpu().numpy(), want)
     assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))
+
+
+def test_encode_stream_replay_beyond_2048_units():
+    """Graph replay of a stream whose lookups run the multi-block top-k
+    (> 2048 units): scratch is sized before capture, so the captured graph
+    replays (a graph holding an allocation cannot be relaunched) and repeats
+    the first run exactly."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=512, init_size=128, n_lookup=8, hot_capacity=16)
+    n = 2300 * 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    q = (torch.randn((n, 8, 128), generator=g, device="cuda") * 0.3).bfloat16()
+    k = (torch.randn((n, 2, 128), generator=g, device="cuda") * 0.3).bfloat16()
+    v = torch.randn((n, 2, 128), generator=g, device="cuda").bfloat16()
+    eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=8, n_kv_heads=2, head_dim=128),
+                       dtype=torch.bfloat16)
+    eng.reserve(n)
+    first = eng.encode_stream(q, k, v).clone()
+    m1, t1 = eng.metrics(), eng.trace()
+    assert m1["units"] > 2048
+    eng.reset()
+    again = eng.encode_stream(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.equal(first, again)
+    assert eng.metrics() == m1 and eng.trace() == t1
