@@ -768,8 +768,86 @@ __global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
     if (threadIdx.x == 0) *p.done = 0;
 }
 
+// Large indices: the same math fed by cp.async (16-byte LDGSTS) into a
+// 3-deep per-warp shared-memory ring, so each warp keeps the next two units
+// (16 KB) in flight while it computes one; 8 warps x 3 x 8 KB per SM.
+constexpr int kScanStages = 3;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
+    extern __shared__ __align__(16) uint8_t scan_smem[];
+    const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
+    uint8_t* ring = scan_smem + static_cast<size_t>(wib) * kScanStages * 8192;
+    const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + wib;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+    const int64_t bytes_u = static_cast<int64_t>(p.G) * 512 * 2;  // one unit's repr rows
+    double q[8][4];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+    auto issue = [&](int64_t u, int stage) {
+        if (u < p.U) {
+            const uint8_t* src = static_cast<const uint8_t*>(p.repr) + u * bytes_u;
+            uint8_t* dst = ring + stage * 8192;
+            for (int64_t off = 16 * lane; off < bytes_u; off += 512) cp_async16(dst + off, src + off);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int st = 0; st < kScanStages - 1; ++st) issue(warp0 + st * nwarps, st);
+    int stage = 0;
+    for (int64_t u = warp0; u < p.U; u += nwarps) {
+        issue(u + (kScanStages - 1) * nwarps, (stage + kScanStages - 1) % kScanStages);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
+        __syncwarp();
+        const uint8_t* buf = ring + stage * 8192 + 8 * lane;
+        double rel = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= p.G) break;
+            double a = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint2 v = *reinterpret_cast<const uint2*>(buf + (4 * g + r) * 256);
+                a = fma(q[g][0], static_cast<double>(__uint_as_float(v.x << 16)), a);
+                a = fma(q[g][1], static_cast<double>(__uint_as_float(v.x & 0xffff0000u)), a);
+                a = fma(q[g][2], static_cast<double>(__uint_as_float(v.y << 16)), a);
+                a = fma(q[g][3], static_cast<double>(__uint_as_float(v.y & 0xffff0000u)), a);
+            }
+            if (p.fused) {
+                rel += a;
+            } else {
+                a = warp_sum_d(a);
+                if (lane == 0) p.part[u * p.Gtot + p.g0 + g] = a;
+            }
+        }
+        if (p.fused) {
+            rel = warp_sum_d(rel);
+            if (lane == 0) p.rel[u] = rel;
+        }
+        __syncwarp();  // the stage is refilled next iteration
+        stage = (stage + 1) % kScanStages;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
     const int warps = 8;
+    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.fused != 1 && p.U >= 148 * 8 * 4) {
+        // large index (multi-block top-k follows): streaming scan, one block per SM
+        const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_lookup_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr = true;
+        }
+        k_lookup_stream<<<148, 256, smem, st>>>(p);
+        return;
+    }
     if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8) {
         // one unit per warp up to two waves of resident blocks, then warps stride
         const int64_t want = (p.U + warps - 1) / warps;
