@@ -608,7 +608,7 @@ struct infllm_engine {
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
             last_lkp = lp;
-            if (!(debug_skip & 2)) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
@@ -622,8 +622,7 @@ struct infllm_engine {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
-                    launch_topk_multi(L.rel.as<double>(), n_units0, n_sel, cv, reinterpret_cast<int64_t*>(cv + nc),
-                                      sel_b, st);
+                    launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
             launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
             if (prof) {
@@ -1469,11 +1468,10 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         lp.g0 = 0;
         lp.r_k = static_cast<int>(r_k);
         lp.d = head_dim;
-        lp.fused = 2;  // relevance scan, then the multi-block exact top-k
-        launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
-        if (k > 0)
-            launch_topk_multi(rel, n_units, k, cand.as<double>(), reinterpret_cast<int64_t*>(cand.as<double>() + nc),
-                              ids, st);
+        lp.n_sel = k;
+        lp.sel = ids;
+        launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
+                           reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
         ck(cudaGetLastError(), "lookup");
     });
 }

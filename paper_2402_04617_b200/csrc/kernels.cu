@@ -781,8 +781,11 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
     extern __shared__ __align__(16) uint8_t scan_smem[];
     const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
     uint8_t* ring = scan_smem + static_cast<size_t>(wib) * kScanStages * 8192;
-    const int64_t warp0 = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + wib;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+    // contiguous slice per block (its candidates then come out in unit order)
+    const int64_t S = (p.U + gridDim.x - 1) / gridDim.x;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * S, s1 = s0 + S < p.U ? s0 + S : p.U;
+    const int64_t warp0 = s0 + wib;
+    const int64_t nwarps = blockDim.x / 32;
     const int64_t bytes_u = static_cast<int64_t>(p.G) * 512 * 2;  // one unit's repr rows
     double q[8][4];
 #pragma unroll
@@ -790,7 +793,7 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
     auto issue = [&](int64_t u, int stage) {
-        if (u < p.U) {
+        if (u < s1) {
             const uint8_t* src = static_cast<const uint8_t*>(p.repr) + u * bytes_u;
             uint8_t* dst = ring + stage * 8192;
             for (int64_t off = 16 * lane; off < bytes_u; off += 512) cp_async16(dst + off, src + off);
@@ -800,7 +803,7 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
 #pragma unroll
     for (int st = 0; st < kScanStages - 1; ++st) issue(warp0 + st * nwarps, st);
     int stage = 0;
-    for (int64_t u = warp0; u < p.U; u += nwarps) {
+    for (int64_t u = warp0; u < s1; u += nwarps) {
         issue(u + (kScanStages - 1) * nwarps, (stage + kScanStages - 1) % kScanStages);
         asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
         __syncwarp();
@@ -833,21 +836,24 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
         stage = (stage + 1) % kScanStages;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (!p.cand_v) return;
+    // this block's slice: top n_sel candidates for the final merge (k_topk_final)
+    __shared__ int64_t loc[128];
+    __threadfence_block();
+    __syncthreads();
+    const int64_t len = s1 > s0 ? s1 - s0 : 0;
+    const int64_t kk = p.n_sel < len ? p.n_sel : len;
+    if (kk > 0) block_topk_radix(p.rel + s0, len, kk, loc);
+    __syncthreads();
+    for (int r = threadIdx.x; r < p.n_sel; r += blockDim.x) {
+        const bool ok = r < kk;
+        p.cand_v[blockIdx.x * p.n_sel + r] = ok ? p.rel[s0 + loc[r]] : -INFINITY;
+        p.cand_i[blockIdx.x * p.n_sel + r] = ok ? s0 + loc[r] : -1;
+    }
 }
 
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st) {
     const int warps = 8;
-    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.fused != 1 && p.U >= 148 * 8 * 4) {
-        // large index (multi-block top-k follows): streaming scan, one block per SM
-        const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_lookup_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            attr = true;
-        }
-        k_lookup_stream<<<148, 256, smem, st>>>(p);
-        return;
-    }
     if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8) {
         // one unit per warp up to two waves of resident blocks, then warps stride
         const int64_t want = (p.U + warps - 1) / warps;
@@ -1121,7 +1127,36 @@ __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const
     __syncthreads();
     for (int r = threadIdx.x; r < k; r += blockDim.x) sel[r] = cand_i[loc[r]];
 }
-int64_t topk_multi_scratch(int64_t U, int64_t k) { return ((U + kSliceU - 1) / kSliceU) * k; }
+constexpr int kScanBlocks = 148;  // streaming scan: one block per SM, one slice each
+int64_t topk_multi_scratch(int64_t U, int64_t k) {
+    const int64_t nb = (U + kSliceU - 1) / kSliceU;
+    return (nb > kScanBlocks ? nb : kScanBlocks) * k;
+}
+void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
+    p.fused = 2;
+    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.U >= kScanBlocks * 8 * 4 &&
+        p.U <= static_cast<int64_t>(kScanBlocks) * kSliceU && p.n_sel >= 0 &&
+        kScanBlocks * p.n_sel <= 1024 * kRadixE) {
+        // large index: streaming scan with the per-slice top-k fused, then one merge block
+        const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_lookup_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            attr = true;
+        }
+        p.cand_v = p.n_sel > 0 ? cand_v : nullptr;
+        p.cand_i = p.n_sel > 0 ? cand_i : nullptr;
+        k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p);
+        if (p.n_sel > 0)
+            k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, static_cast<int64_t>(kScanBlocks) * p.n_sel, p.n_sel,
+                                             p.sel);
+        return;
+    }
+    p.cand_v = nullptr;
+    p.cand_i = nullptr;
+    launch_lookup(p, dtype_bf16, st);
+    if (p.n_sel > 0) launch_topk_multi(p.rel, p.U, p.n_sel, cand_v, cand_i, p.sel, st);
+}
 void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                        cudaStream_t st) {
     if (U <= 0 || k <= 0) return;

@@ -73,6 +73,8 @@ struct LookupParams {
     int64_t U, n_sel;
     int G, Gtot, g0, r_k, d;
     int fused;           // 1: single shard: rel + top-k in this launch; 2: rel only (multi-block top-k follows)
+    double* cand_v;      // fused 2, streaming scan: per-block top-k candidates [gridDim][n_sel]
+    int64_t* cand_i;
 };
 
 struct TopkParams {
@@ -201,6 +203,8 @@ template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
 // exact top-k (rel desc, id asc) over rel[U] for large U; scratch of topk_multi_scratch(U, k) entries each
+// lookup (fused == 2) + exact top-k for a single shard; cand_v / cand_i scratch as above
+void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st);
 int64_t topk_multi_scratch(int64_t U, int64_t k);
 void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                        cudaStream_t st);
