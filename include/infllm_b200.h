@@ -144,7 +144,12 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * allows, 0 = CUDA-core attention), "cuda_graphs" (1 = graph-replayed
  * encode_stream, default), "attn_score_bound" (1 = the tcgen05 attention may
  * use the per-row score bound |q| |k|_max as a fixed softmax offset, default;
- * 0 = always the online-max path). */
+ * 0 = always the online-max path), "host_tier_slots" (S > 0: unit pages live
+ * in a pinned-host tier and the attention reads them from an S-slot GPU unit
+ * cache filled on demand over PCIe on a side stream -- the north star's
+ * host-offloaded store; TieredStore's hot/cold tiers (memory.hpp:165-168) are
+ * bookkeeping only in the reference, outputs are identical either way;
+ * 2*n_lookup <= S <= 16384; set before reserve() and the first step). */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if
@@ -205,6 +210,10 @@ int infllm_unit_freq(infllm_engine_t eng, int32_t layer, double* host_freq, int3
  * records (step, unit_id, hit). */
 int infllm_trace(infllm_engine_t eng, int32_t layer, int64_t* host_step, int64_t* host_unit,
                  int32_t* host_hit, int64_t cap, int64_t* n_out);
+/* Host tier counters of `layer` since the last reset: out[0] unit pages
+ * copied host -> GPU cache, out[1] retrieved units already resident in the
+ * cache, out[2] H2D bytes, out[3] slot count (0: host tier off). */
+int infllm_tier_stats(infllm_engine_t eng, int32_t layer, int64_t* out4);
 /* Number of kernels this engine launched so far (all layers). */
 int infllm_kernel_launches(infllm_engine_t eng, int64_t* n_out);
 /* Fill host_out with the dominant attention kernel's average device time of

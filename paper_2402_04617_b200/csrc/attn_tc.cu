@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     ts.len = sLen;
     if (threadIdx.x < a.n_sel) {
         const int64_t id = a.sel[threadIdx.x];
-        sSel[threadIdx.x] = static_cast<int32_t>(id);
+        sSel[threadIdx.x] = a.sel_slot ? a.sel_slot[threadIdx.x] : static_cast<int32_t>(id);  // page index
         sLen[threadIdx.x] = a.unit_len[id];
     }
 

@@ -123,6 +123,32 @@ struct DBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// mapped pinned host allocation (host tier unit pages); device-addressable via UVA
+struct HBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void grow(size_t b) {  // keep contents; the caller has drained every stream touching it
+        if (b <= bytes) return;
+        void* n = nullptr;
+        ck(cudaHostAlloc(&n, b, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc (host tier)");
+        if (p) std::memcpy(n, p, bytes);
+        std::memset(static_cast<uint8_t*>(n) + bytes, 0, b - bytes);
+        if (p) cudaFreeHost(p);
+        p = n;
+        bytes = b;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void* dev() const {
+        void* d = nullptr;
+        if (p) ck(cudaHostGetDevicePointer(&d, p, 0), "cudaHostGetDevicePointer");
+        return d;
+    }
+};
+
 __global__ void k_empty() {}
 // throughput probes: 8 independent FMA chains x n iterations per thread
 __global__ void k_probe_f64(double* out, int n) {
@@ -219,6 +245,11 @@ struct infllm_engine {
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
         DBuf kmax2;  // [kPB step buffers][G] running max |k|^2 (attention score bound)
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
+        // host tier (tier_slots > 0): unit pages in mapped pinned host memory,
+        // the attention reads them from tier_slots device cache slots
+        HBuf host_k, host_krot, host_v;
+        void *dhost_k = nullptr, *dhost_krot = nullptr, *dhost_v = nullptr;
+        DBuf slot_k, slot_krot, slot_v, slot_unit, slot_used, unit_slot, sel_slot, tier_miss, tier_stats;
     };
     std::vector<Layer> layers;
 
@@ -274,6 +305,7 @@ struct infllm_engine {
     std::vector<GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
     bool use_graphs = true;
+    int64_t tier_slots = 0;  // host tier: GPU unit-cache slots (0: unit pages resident in HBM)
     bool capturing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_attn_ev = nullptr;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_lookup_ev = nullptr;
@@ -312,9 +344,37 @@ struct infllm_engine {
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
         const int64_t cap = std::max<int64_t>({need, 2 * L.unit_cap, 16});
-        L.unit_k.grow(cap * unit_elems_k() * esz, st);
-        if (cfg.position_mode == INFLLM_POSITION_ABSOLUTE) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
-        L.unit_v.grow(cap * unit_elems_v() * esz, st);
+        const bool absolute = cfg.position_mode == INFLLM_POSITION_ABSOLUTE;
+        if (tier_slots > 0) {
+            ck(cudaStreamSynchronize(st), "sync before host-tier growth");
+            L.host_k.grow(cap * unit_elems_k() * esz);
+            if (absolute) L.host_krot.grow(cap * unit_elems_k() * esz);
+            L.host_v.grow(cap * unit_elems_v() * esz);
+            L.dhost_k = L.host_k.dev();
+            L.dhost_krot = L.host_krot.dev();
+            L.dhost_v = L.host_v.dev();
+            if (!L.slot_k.p) {
+                const int64_t S = tier_slots;
+                L.slot_k.alloc(S * unit_elems_k() * esz, st);
+                if (absolute) L.slot_krot.alloc(S * unit_elems_k() * esz, st);
+                L.slot_v.alloc(S * unit_elems_v() * esz, st);
+                L.slot_unit.alloc(S * sizeof(int64_t), st, false);
+                ck(cudaMemsetAsync(L.slot_unit.p, 0xff, L.slot_unit.bytes, st), "memset");
+                L.slot_used.alloc(S * sizeof(int64_t), st);
+                const size_t km = static_cast<size_t>(std::max<int64_t>(cfg.n_lookup, 1));
+                L.sel_slot.alloc(2 * km * sizeof(int32_t), st);
+                L.tier_miss.alloc((2 * km + 1) * sizeof(int32_t), st);
+                L.tier_stats.alloc(4 * sizeof(int64_t), st);
+            }
+            L.unit_slot.grow(cap * sizeof(int32_t), st);
+            k_fill_i32<<<static_cast<unsigned>((cap - L.unit_cap + 255) / 256), 256, 0, st>>>(
+                L.unit_slot.as<int32_t>() + L.unit_cap, cap - L.unit_cap, -1);
+            ++launches;
+        } else {
+            L.unit_k.grow(cap * unit_elems_k() * esz, st);
+            if (absolute) L.unit_krot.grow(cap * unit_elems_k() * esz, st);
+            L.unit_v.grow(cap * unit_elems_v() * esz, st);
+        }
         L.unit_scores.grow(cap * cfg.unit_size * sizeof(float), st);
         L.repr.grow(cap * static_cast<size_t>(Gs) * cfg.n_repr * d * esz, st);
         L.repr_idx.grow(cap * cfg.n_repr * sizeof(int32_t), st);
@@ -342,6 +402,11 @@ struct infllm_engine {
         L.trace.grow(cap * 3 * sizeof(int64_t), st);
         L.trace_cap = cap;
     }
+
+    // where unit pages are written (HBM pool, or the host tier)
+    void* upage_k(const Layer& L) const { return tier_slots > 0 ? L.dhost_k : L.unit_k.p; }
+    void* upage_krot(const Layer& L) const { return tier_slots > 0 ? L.dhost_krot : L.unit_krot.p; }
+    void* upage_v(const Layer& L) const { return tier_slots > 0 ? L.dhost_v : L.unit_v.p; }
 
     // make `st` wait for everything queued on the side stream
     void join_side(cudaStream_t st) {
@@ -381,8 +446,8 @@ struct infllm_engine {
         sp.ring_k = L.ring_k.p;
         sp.ring_krot = L.ring_krot.p;
         sp.ring_v = L.ring_v.p;
-        sp.unit_krot = L.unit_krot.p;
-        sp.unit_v = L.unit_v.p;
+        sp.unit_krot = upage_krot(L);
+        sp.unit_v = upage_v(L);
         sp.vl = vl;
     }
 
@@ -502,9 +567,9 @@ struct infllm_engine {
             ep.init_k = L.init_k.p;
             ep.init_krot = L.init_krot.p;
             ep.init_v = L.init_v.p;
-            ep.unit_k = L.unit_k.p;
-            ep.unit_krot = L.unit_krot.p;
-            ep.unit_v = L.unit_v.p;
+            ep.unit_k = upage_k(L);
+            ep.unit_krot = upage_krot(L);
+            ep.unit_v = upage_v(L);
             ep.ev_part = L.ev_part.as<double>();
             ep.pop0 = L.local_start;
             ep.n_init = to_init;
@@ -555,7 +620,7 @@ struct infllm_engine {
                 SelectParams sp{};
                 sp.unit_scores = L.unit_scores.as<float>();
                 sp.unit_len = L.ulen.as<int32_t>();
-                sp.unit_k = L.unit_k.p;
+                sp.unit_k = upage_k(L);
                 sp.repr = L.repr.p;
                 sp.repr_idx = L.repr_idx.as<int32_t>();
                 sp.u0 = L.n_units;
@@ -625,6 +690,31 @@ struct infllm_engine {
                     launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
             launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
+            if (tier_slots > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
+                TierParams tp2{};
+                tp2.sel = sel_b;
+                tp2.sel_slot = L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
+                tp2.unit_slot = L.unit_slot.as<int32_t>();
+                tp2.slot_unit = L.slot_unit.as<int64_t>();
+                tp2.slot_used = L.slot_used.as<int64_t>();
+                tp2.miss = L.tier_miss.as<int32_t>() + 1;
+                tp2.miss_n = L.tier_miss.as<int32_t>();
+                tp2.stats = L.tier_stats.as<int64_t>();
+                tp2.host_k = L.dhost_k;
+                tp2.host_krot = L.dhost_krot;
+                tp2.host_v = L.dhost_v;
+                tp2.slot_k = L.slot_k.p;
+                tp2.slot_krot = L.slot_krot.p;
+                tp2.slot_v = L.slot_v.p;
+                tp2.n_sel = n_sel;
+                tp2.S = tier_slots;
+                tp2.step = L.step;
+                tp2.page_k = static_cast<int64_t>(unit_elems_k() * esz);
+                tp2.page_v = static_cast<int64_t>(unit_elems_v() * esz);
+                tp2.kmax = static_cast<int>(n_sel);
+                launch_tier(tp2, st);
+                launches += 2;
+            }
             if (prof) {
                 record(evp.second, st);
                 (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
@@ -651,11 +741,13 @@ struct infllm_engine {
         ap.init_k = L.init_k.p;
         ap.init_krot = L.init_krot.p;
         ap.init_v = L.init_v.p;
-        ap.unit_k = L.unit_k.p;
-        ap.unit_krot = L.unit_krot.p;
-        ap.unit_v = L.unit_v.p;
+        const bool tier = tier_slots > 0;
+        ap.unit_k = tier ? L.slot_k.p : L.unit_k.p;
+        ap.unit_krot = tier ? L.slot_krot.p : L.unit_krot.p;
+        ap.unit_v = tier ? L.slot_v.p : L.unit_v.p;
         ap.unit_len = L.ulen.as<int32_t>();
         ap.sel = sel_b;
+        ap.sel_slot = tier ? L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1) : nullptr;
         ap.ring_k = L.ring_k.p;
         ap.ring_krot = L.ring_krot.p;
         ap.ring_v = L.ring_v.p;
@@ -684,7 +776,7 @@ struct infllm_engine {
         ap.want_mass = want_mass;
         ap.scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.hpp:140
         ap.vl = vl;
-        ap.unit_cap = L.unit_cap;
+        ap.unit_cap = tier ? tier_slots : L.unit_cap;
         last_ap = ap;
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
@@ -967,7 +1059,7 @@ struct infllm_engine {
             SelectParams sp{};
             sp.unit_scores = L.unit_scores.as<float>();
             sp.unit_len = L.ulen.as<int32_t>();
-            sp.unit_k = L.unit_k.p;
+            sp.unit_k = upage_k(L);
             sp.repr = L.repr.p;
             sp.repr_idx = L.repr_idx.as<int32_t>();
             sp.u0 = L.n_units;
@@ -1131,8 +1223,11 @@ int infllm_engine_destroy(infllm_engine_t e) {
             for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
                             &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
-                            &L.ev_part})
+                            &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
+                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats})
                 b->release(st);
+        for (auto& L : e->layers)
+            for (auto* h : {&L.host_k, &L.host_krot, &L.host_v}) h->release();
         for (auto& p : e->ev_attn) {
             cudaEventDestroy(p.first);
             cudaEventDestroy(p.second);
@@ -1202,6 +1297,12 @@ int infllm_engine_reset(infllm_engine_t e, void* stream) {
             ck(cudaMemsetAsync(L.lru.p, 0, L.lru.bytes, st), "memset");
             if (L.hot.p) ck(cudaMemsetAsync(L.hot.p, 0, L.hot.bytes, st), "memset");
             if (L.freq.p) ck(cudaMemsetAsync(L.freq.p, 0, L.freq.bytes, st), "memset");
+            if (L.slot_unit.p) {  // host tier: empty GPU unit cache
+                ck(cudaMemsetAsync(L.slot_unit.p, 0xff, L.slot_unit.bytes, st), "memset");
+                ck(cudaMemsetAsync(L.slot_used.p, 0, L.slot_used.bytes, st), "memset");
+                ck(cudaMemsetAsync(L.unit_slot.p, 0xff, L.unit_slot.bytes, st), "memset");
+                ck(cudaMemsetAsync(L.tier_stats.p, 0, L.tier_stats.bytes, st), "memset");
+            }
             if (L.ulen.p) {
                 k_fill_i32<<<static_cast<unsigned>((L.unit_cap + 255) / 256), 256, 0, st>>>(
                     L.ulen.as<int32_t>(), L.unit_cap, static_cast<int32_t>(e->cfg.unit_size));
@@ -1223,6 +1324,17 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->debug_skip = value;
         else if (k == "attn_score_bound")
             e->score_bound = value != 0;
+        else if (k == "host_tier_slots") {
+            for (auto& L : e->layers)
+                if (L.unit_cap > 0 && value != e->tier_slots)
+                    throw ConfigError("host_tier_slots must be set before reserve() and the first step");
+            const int64_t km = std::max<int64_t>(e->cfg.n_lookup, 1);
+            if (value != 0 && (value < 2 * km || value > 16384))
+                throw ConfigError("host_tier_slots must be 0 or in [2*n_lookup, 16384]");
+            if (value != 0 && ((e->unit_elems_k() * e->esz) % 16 != 0 || (e->unit_elems_v() * e->esz) % 16 != 0))
+                throw ConfigError("host_tier_slots: unit pages must be multiples of 16 bytes");
+            e->tier_slots = value;
+        }
         else
             throw ConfigError("unknown option '" + k + "'");
     });
@@ -1374,6 +1486,22 @@ int infllm_trace(infllm_engine_t e, int32_t layer, int64_t* host_step, int64_t* 
             host_unit[i] = t[static_cast<size_t>(3 * i + 1)];
             host_hit[i] = static_cast<int32_t>(t[static_cast<size_t>(3 * i + 2)]);
         }
+    });
+}
+
+int infllm_tier_stats(infllm_engine_t e, int32_t layer, int64_t* out4) {
+    return guard([&] {
+        if (!e || !out4) throw ConfigError("null argument");
+        if (layer < 0 || layer >= e->n_layers) throw StreamError("layer out of range");
+        const auto& L = e->layers[static_cast<size_t>(layer)];
+        out4[0] = out4[1] = out4[2] = 0;
+        out4[3] = e->tier_slots;
+        if (!L.tier_stats.p) return;
+        ck(cudaDeviceSynchronize(), "sync");
+        int64_t st[4];
+        ck(cudaMemcpy(st, L.tier_stats.p, sizeof(st), cudaMemcpyDeviceToHost), "D2H");
+        for (int i = 0; i < 3; ++i) out4[i] = st[i];
+        if (st[3] != 0) throw StreamError("host tier: slot assignment failed");
     });
 }
 

@@ -1286,6 +1286,7 @@ __global__ void __launch_bounds__(kThreads) k_attn_simt(AttnParams p) {
             kind = 1;
             id = p.sel[seg - 1];
             seg_len = p.unit_len[id];
+            if (p.sel_slot) id = p.sel_slot[seg - 1];  // host tier: the unit's GPU cache slot page
             seg_start = 0;
         } else {
             kind = 2;
@@ -1596,6 +1597,139 @@ __global__ void __launch_bounds__(256) k_lru(LruParams p) {
 }
 
 void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 256, 0, st>>>(p); }
+
+// ---- host tier: GPU unit-cache slot assignment + PCIe page pull ----
+// One warp. Slot stamps (layer step + 2) live in shared memory for the whole
+// assignment; hits are stamped first so no miss can take them, then each miss
+// takes the least-recently-stamped slot (tie: lower slot) whose last use is
+// older than the previous step of this layer (that attention may still be
+// reading it: the lookup of step t overlaps the attention of step t-1).
+__global__ void __launch_bounds__(32) k_tier_assign(TierParams p) {
+    extern __shared__ int64_t s_used[];  // [S]
+    __shared__ int32_t s_slot[kTopkMax];
+    const int lane = threadIdx.x;
+    const int64_t stamp = p.step + 2;
+    for (int64_t s = lane; s < p.S; s += 32) s_used[s] = p.slot_used[s];
+    for (int64_t j = lane; j < p.n_sel; j += 32) s_slot[j] = p.unit_slot[p.sel[j]];
+    __syncwarp();
+    int64_t hits = 0;
+    for (int64_t j = lane; j < p.n_sel; j += 32)
+        if (s_slot[j] >= 0) {
+            s_used[s_slot[j]] = stamp;
+            ++hits;
+        }
+    __syncwarp();
+    int nm = 0, fail = 0;
+    for (int64_t j = 0; j < p.n_sel; ++j) {
+        if (s_slot[j] >= 0) continue;
+        int64_t bv = INT64_MAX;
+        int bs = -1;
+        for (int s = lane; s < p.S; s += 32)
+            if (s_used[s] <= p.step && s_used[s] < bv) {
+                bv = s_used[s];
+                bs = s;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+            if (os >= 0 && (bs < 0 || ov < bv || (ov == bv && os < bs))) {
+                bv = ov;
+                bs = os;
+            }
+        }
+        if (bs < 0) {  // cannot happen with S >= 2 k_m (checked on the host)
+            ++fail;
+            continue;
+        }
+        if (lane == 0) {
+            const int64_t id = p.sel[j];
+            const int64_t old = p.slot_unit[bs];
+            if (old >= 0) p.unit_slot[old] = -1;
+            p.unit_slot[id] = bs;
+            p.slot_unit[bs] = id;
+            s_used[bs] = stamp;
+            s_slot[j] = bs;
+            p.miss[nm] = bs;
+            p.miss[p.n_sel + nm] = static_cast<int32_t>(j);
+        }
+        ++nm;
+        __syncwarp();
+    }
+    __syncwarp();
+    for (int64_t s = lane; s < p.S; s += 32) p.slot_used[s] = s_used[s];
+    for (int64_t j = lane; j < p.n_sel; j += 32) p.sel_slot[j] = s_slot[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+    if (lane == 0) {
+        *p.miss_n = nm;
+        p.stats[0] += nm;
+        p.stats[1] += hits;
+        p.stats[2] += static_cast<int64_t>(nm) * (p.page_k * (p.host_krot ? 2 : 1) + p.page_v);
+        p.stats[3] += fail;
+    }
+}
+
+// grid (max misses, chunks of 32 KB over the unit's K | K_rot | V pages):
+// 8 independent 16-byte loads in flight per thread from mapped host memory.
+constexpr int kTierChunk = 256 * 8 * 16;
+__global__ void __launch_bounds__(256) k_tier_copy(TierParams p) {
+    const int j = blockIdx.x;
+    if (j >= *p.miss_n) return;
+    const int64_t slot = p.miss[j];
+    const int64_t id = p.sel[p.miss[p.n_sel + j]];
+    // chunk c of the K page, then of the V page, then of the K_rot page
+    const int64_t ck = (p.page_k + kTierChunk - 1) / kTierChunk, cv = (p.page_v + kTierChunk - 1) / kTierChunk;
+    int64_t c = blockIdx.y;
+    const uint8_t* src;
+    uint8_t* dst;
+    int64_t page;
+    if (c < ck) {
+        src = static_cast<const uint8_t*>(p.host_k);
+        dst = static_cast<uint8_t*>(p.slot_k);
+        page = p.page_k;
+    } else if ((c -= ck) < cv) {
+        src = static_cast<const uint8_t*>(p.host_v);
+        dst = static_cast<uint8_t*>(p.slot_v);
+        page = p.page_v;
+    } else {
+        c -= cv;
+        if (!p.host_krot || c >= ck) return;
+        src = static_cast<const uint8_t*>(p.host_krot);
+        dst = static_cast<uint8_t*>(p.slot_krot);
+        page = p.page_k;
+    }
+    const int64_t off = c * kTierChunk, len = page - off;
+    src += id * page + off;
+    dst += slot * page + off;
+    const int64_t n16 = (len < kTierChunk ? len : kTierChunk) / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    uint4 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int64_t i = threadIdx.x + 256 * u;
+        if (i < n16) r[u] = __ldg(s4 + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int64_t i = threadIdx.x + 256 * u;
+        if (i < n16) d4[i] = r[u];
+    }
+}
+
+void launch_tier(const TierParams& p, cudaStream_t st) {
+    const size_t smem = static_cast<size_t>(p.S) * sizeof(int64_t);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaFuncSetAttribute(k_tier_assign, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        attr = smem;
+    }
+    k_tier_assign<<<1, 32, smem, st>>>(p);
+    const int64_t ck = (p.page_k + kTierChunk - 1) / kTierChunk, cv = (p.page_v + kTierChunk - 1) / kTierChunk;
+    dim3 grid(static_cast<unsigned>(p.kmax), static_cast<unsigned>(ck * (p.host_krot ? 2 : 1) + cv));
+    k_tier_copy<<<grid, 256, 0, st>>>(p);
+}
 
 __device__ void warp_select(const float* sc, int len, int r_k, int* out);
 

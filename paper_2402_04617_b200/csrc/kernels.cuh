@@ -97,6 +97,7 @@ struct AttnParams {
     const void* unit_v;
     const int32_t* unit_len;
     const int64_t* sel;
+    const int32_t* sel_slot;  // host tier: GPU cache slot of each retrieved unit (unit_k/v are slot pages), or null
     const void* ring_k;
     const void* ring_krot;
     const void* ring_v;
@@ -140,6 +141,34 @@ struct LruParams {
     int Gtot, G, rep, n_mt, H_total, mass_src;
     double decay;
     int64_t bytes_per_token;
+};
+
+// Host tier (north star: pinned-host unit store + GPU-resident LRU unit
+// cache). Unit pages live in mapped pinned host memory ([U][G][l_bs][d] K,
+// V^T pages as in HBM mode); the attention reads them from S device slots.
+// k_tier_assign maps this step's retrieved ids to slots (hits keep theirs;
+// misses take the least-recently-used slot not read by this layer's previous
+// or current step) and k_tier_copy pulls the missing pages over PCIe with
+// device-initiated loads, so the lookup -> copy -> attention chain needs no
+// host synchronisation and stays graph-capturable.
+struct TierParams {
+    const int64_t* sel;   // [n_sel] retrieved ids (ascending)
+    int32_t* sel_slot;    // [n_sel] out: slot of each
+    int32_t* unit_slot;   // [Ucap] slot holding the unit, -1 if not resident
+    int64_t* slot_unit;   // [S] unit in the slot, -1 if empty
+    int64_t* slot_used;   // [S] (layer step of the last use) + 2, 0 = never used
+    int32_t* miss;        // [2][n_sel]: slot and selection index of each unit to copy
+    int32_t* miss_n;      // [1]
+    int64_t* stats;       // [4] page loads, slot hits, H2D bytes, assignment failures
+    const void* host_k;
+    const void* host_krot;  // absolute position mode only
+    const void* host_v;
+    void* slot_k;
+    void* slot_krot;
+    void* slot_v;
+    int64_t n_sel, S, step;
+    int64_t page_k, page_v;  // bytes of one unit's K (and K_rot) / V page, all groups
+    int kmax;                // grid.x of the copy (max misses)
 };
 
 struct EvictParams {
@@ -213,6 +242,7 @@ void launch_mass(const MassParams& p, cudaStream_t st);
 void launch_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep, int n_mt,
                             cudaStream_t st);
 void launch_lru(const LruParams& p, cudaStream_t st);
+void launch_tier(const TierParams& p, cudaStream_t st);  // k_tier_assign + k_tier_copy
 template <typename T> void launch_evict(const EvictParams& p, cudaStream_t st);
 void launch_finalize(const FinalizeParams& p, cudaStream_t st);
 template <typename T> void launch_select(const SelectParams& p, cudaStream_t st);

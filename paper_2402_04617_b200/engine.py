@@ -183,6 +183,12 @@ class StreamEngine:
         k = min(cap, n.value)
         return list(zip(st[:k].tolist(), un[:k].tolist(), hit[:k].tolist()))
 
+    def tier_stats(self, layer=0):
+        """Host tier counters: page loads, cache hits, H2D bytes, slots (infllm_tier_stats)."""
+        out = (C.c_int64 * 4)()
+        check(lib().infllm_tier_stats(self.h, int(layer), out))
+        return dict(loads=out[0], cache_hits=out[1], h2d_bytes=out[2], slots=out[3])
+
     def kernel_launches(self):
         n = C.c_int64()
         check(lib().infllm_kernel_launches(self.h, C.byref(n)))

@@ -3,7 +3,10 @@
 # (per KV head) repeated over a 64-token span at a random offset in the evicted
 # region, and the last 4 tokens (decode steps) querying with that key. Reports
 # prefill throughput and whether every probe lookup retrieved the span's units.
-#   python tools/c3_planted.py [n_tokens=1048576]
+# slots > 0: host-offloaded unit store (pinned host pages) + an S-slot GPU unit
+# cache (engine option host_tier_slots); reports page loads, cache hit rate
+# and the achieved H2D GB/s of the page pulls.
+#   python tools/c3_planted.py [n_tokens=1048576] [slots=0]
 import sys
 import time
 
@@ -14,7 +17,7 @@ from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine  # noqa
 import bench  # noqa: E402
 
 
-def run(n, seed=0, verbose=True):
+def run(n, seed=0, verbose=True, slots=0):
     cfg, shape = bench.CFG, bench.SHAPE
     H, Hkv, d = shape["n_heads"], shape["n_kv_heads"], shape["head_dim"]
     L, I, bs, C = cfg["local_size"], cfg["init_size"], cfg["unit_size"], cfg["chunk_size"]
@@ -36,6 +39,8 @@ def run(n, seed=0, verbose=True):
     Q[npre:] = (key.repeat_interleave(H // Hkv, 0) * 3.0).bfloat16()
     expected = sorted({(t - I) // bs for t in (a, a + 63)})
     eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(**shape), dtype=torch.bfloat16)
+    if slots:
+        eng.set_option("host_tier_slots", slots)
     eng.reserve(n)
     out = torch.empty((npre, H, d), device="cuda", dtype=torch.bfloat16)
     eng.encode_stream(Q[:npre], K[:npre], V[:npre], out=out)  # graph capture + first replay
@@ -45,6 +50,7 @@ def run(n, seed=0, verbose=True):
     eng.encode_stream(Q[:npre], K[:npre], V[:npre], out=out)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
+    ts = eng.tier_stats() if slots else None
     hits = []
     for i in range(npre, n):
         r = eng.step(Q[i:i + 1], K[i:i + 1], V[i:i + 1], decode=True)
@@ -54,8 +60,14 @@ def run(n, seed=0, verbose=True):
         print(f"n={n}: prefill {npre} tokens in {dt * 1e3:.1f} ms = {npre / dt / 1e6:.2f} Mtok/s "
               f"(units {m['units']}, plant at {a}, expected units {expected}), probe recall "
               f"{sum(hits)}/{len(hits)}", flush=True)
-    return all(hits), npre / dt
+        if ts:
+            req = ts["loads"] + ts["cache_hits"]
+            print(f"  host tier: {slots} GPU slots, {ts['loads']} page loads / {req} retrieved units "
+                  f"(cache hit rate {ts['cache_hits'] / max(req, 1):.3f}; reference LRU misses {m['misses']}), "
+                  f"{ts['h2d_bytes'] / 1e9:.2f} GB H2D = {ts['h2d_bytes'] / dt / 1e9:.1f} GB/s over the prefill",
+                  flush=True)
+    return all(hits), npre / dt, ts
 
 
 if __name__ == "__main__":
-    run(int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20)
+    run(int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20, slots=int(sys.argv[2]) if len(sys.argv) > 2 else 0)
