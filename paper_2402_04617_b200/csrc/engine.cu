@@ -211,6 +211,11 @@ struct infllm_engine {
     static constexpr int kPrepAhead = 2;  // chunks the prep stream may run ahead of the attention
     static constexpr int kPB = kPrepAhead + 1;  // prep-output buffers (qa, qc, chunk sums, key-norm bound)
     cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[kPB] = {nullptr, nullptr, nullptr};
+    // host tier: slot assignment + PCIe page pulls of step t on their own stream
+    // (after lookup t, before attention t), so lookup t+1 does not queue behind them
+    cudaStream_t tier_stream = nullptr;
+    cudaEvent_t e_tier = nullptr, e_tierdone = nullptr;
+    int64_t tier_seq = -1;  // step that last queued work on the tier stream
     int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
@@ -418,6 +423,11 @@ struct infllm_engine {
         ck(cudaStreamWaitEvent(st, e_prepdone, 0), "wait");
         ck(cudaEventRecord(e_evdone, evict_stream), "record");
         ck(cudaStreamWaitEvent(st, e_evdone, 0), "wait");
+        if (tier_seq >= 0 && (capture_seq0 < 0 || tier_seq >= capture_seq0)) {  // only a stream that joined
+            ck(cudaEventRecord(e_tierdone, tier_stream), "record");
+            ck(cudaStreamWaitEvent(st, e_tierdone, 0), "wait");
+        }
+        tier_seq = -1;
         lru_seq[0] = lru_seq[1] = -1;
         for (auto& a : attn_seq) a = -1;
         lookup_seq = -1;
@@ -690,31 +700,6 @@ struct infllm_engine {
                     launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
             launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
-            if (tier_slots > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
-                TierParams tp2{};
-                tp2.sel = sel_b;
-                tp2.sel_slot = L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
-                tp2.unit_slot = L.unit_slot.as<int32_t>();
-                tp2.slot_unit = L.slot_unit.as<int64_t>();
-                tp2.slot_used = L.slot_used.as<int64_t>();
-                tp2.miss = L.tier_miss.as<int32_t>() + 1;
-                tp2.miss_n = L.tier_miss.as<int32_t>();
-                tp2.stats = L.tier_stats.as<int64_t>();
-                tp2.host_k = L.dhost_k;
-                tp2.host_krot = L.dhost_krot;
-                tp2.host_v = L.dhost_v;
-                tp2.slot_k = L.slot_k.p;
-                tp2.slot_krot = L.slot_krot.p;
-                tp2.slot_v = L.slot_v.p;
-                tp2.n_sel = n_sel;
-                tp2.S = tier_slots;
-                tp2.step = L.step;
-                tp2.page_k = static_cast<int64_t>(unit_elems_k() * esz);
-                tp2.page_v = static_cast<int64_t>(unit_elems_v() * esz);
-                tp2.kmax = static_cast<int>(n_sel);
-                launch_tier(tp2, st);
-                launches += 2;
-            }
             if (prof) {
                 record(evp.second, st);
                 (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
@@ -723,6 +708,35 @@ struct infllm_engine {
 
         ck(cudaEventRecord(e_topk, side), "record");
         if (!(debug_skip & 32)) ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");  // 32: timing experiment only
+        if (tier_slots > 0 && n_sel > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
+            ck(cudaStreamWaitEvent(tier_stream, e_topk, 0), "wait");
+            TierParams tp2{};
+            tp2.sel = sel_b;
+            tp2.sel_slot = L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
+            tp2.unit_slot = L.unit_slot.as<int32_t>();
+            tp2.slot_unit = L.slot_unit.as<int64_t>();
+            tp2.slot_used = L.slot_used.as<int64_t>();
+            tp2.miss = L.tier_miss.as<int32_t>() + 1;
+            tp2.miss_n = L.tier_miss.as<int32_t>();
+            tp2.stats = L.tier_stats.as<int64_t>();
+            tp2.host_k = L.dhost_k;
+            tp2.host_krot = L.dhost_krot;
+            tp2.host_v = L.dhost_v;
+            tp2.slot_k = L.slot_k.p;
+            tp2.slot_krot = L.slot_krot.p;
+            tp2.slot_v = L.slot_v.p;
+            tp2.n_sel = n_sel;
+            tp2.S = tier_slots;
+            tp2.step = L.step;
+            tp2.page_k = static_cast<int64_t>(unit_elems_k() * esz);
+            tp2.page_v = static_cast<int64_t>(unit_elems_v() * esz);
+            tp2.kmax = static_cast<int>(n_sel);
+            launch_tier(tp2, tier_stream);
+            tier_seq = kseq;
+            launches += 2;
+            ck(cudaEventRecord(e_tier, tier_stream), "record");
+            ck(cudaStreamWaitEvent(main, e_tier, 0), "wait");
+        }
         ck(cudaEventRecord(e_lookup, side), "record");
         lookup_seq = kseq;
         // this parity's mass buffers were last read by LRU(k-2)
@@ -1173,9 +1187,10 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         ck(cudaStreamCreateWithFlags(&e->lru_stream, cudaStreamNonBlocking), "lru stream");
         ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
         ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
+        ck(cudaStreamCreateWithFlags(&e->tier_stream, cudaStreamNonBlocking), "tier stream");
         for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone,
                          &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone, &e->e_attnp[0],
-                         &e->e_attnp[1], &e->e_attnp[2]})
+                         &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
         e->chunk_qsum.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
@@ -1251,11 +1266,11 @@ int infllm_engine_destroy(infllm_engine_t e) {
         for (int b = 0; b < infllm_engine::kNB; ++b)
             for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
-                        e->evict_stream})
+                        e->evict_stream, e->tier_stream})
             if (s2) cudaStreamDestroy(s2);
         for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone, e->e_prep,
                         e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone, e->e_attnp[0], e->e_attnp[1],
-                        e->e_attnp[2]})
+                        e->e_attnp[2], e->e_tier, e->e_tierdone})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         delete e;
