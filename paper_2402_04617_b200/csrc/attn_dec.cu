@@ -1,0 +1,422 @@
+// attn_dec.cu — K4: decode attention (l_x = 1) for one or a batch of
+// sequences, bf16, d = d_v = 128, 128-token units (V^T pages).
+//
+// Reference: attend (attention.hpp:116-230) with a single query row, as
+// StreamEngine::decode_step runs it (engine.hpp:100-103): window = [initial |
+// retrieved units | local window | the token itself], clamped positions
+// (far keys: rope(q, l_L) . k_raw, near keys: rope(q, pos) . rope(k, pos),
+// attention.hpp:165-201), scale 1/sqrt(d), max-subtracted softmax, plus the
+// per-unit attention masses for the LRU (engine.hpp:271-283).
+//
+// One query row reads every key once: the step is HBM-bound (K + V^T of the
+// ~6.3K-key window = 25.7 MB per C2 sequence), so it is split-KV
+// ("flash-decoding") on CUDA cores: grid (splits, KV groups, sequences); a
+// CTA streams a contiguous run of 128-key tiles of its (sequence, group) and
+// keeps an online softmax for the group's query heads; the last CTA of a
+// (sequence, group) merges the splits (log-sum-exp) and finishes the masses.
+#include "attn_dec.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace infllm {
+
+namespace {
+
+constexpr int kW = 8;           // warps: 16 keys each for S = QK^T and for P V
+constexpr int kThr = 32 * kW;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2f(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+struct DecTile {
+    int src;  // 0 init, 1 unit, 2 ring
+    int lo, hi;
+    int64_t key0, page;
+};
+
+// window tile t (window order, engine.hpp:187-221)
+__device__ __forceinline__ DecTile dec_tile(const AttnParams& a, int t, int n_init, int64_t near0) {
+    DecTile r;
+    if (t < n_init) {
+        r.src = 0;
+        r.key0 = 128 * static_cast<int64_t>(t);
+        r.page = t;
+        r.lo = 0;
+        r.hi = static_cast<int>(min(static_cast<int64_t>(128), a.init_len - r.key0));
+    } else if (t < n_init + a.n_sel) {
+        const int u = t - n_init;
+        const int64_t id = a.sel[u];
+        r.src = 1;
+        r.key0 = 0;
+        r.page = a.sel_slot ? a.sel_slot[u] : id;
+        r.lo = 0;
+        r.hi = a.unit_len[id];
+    } else {
+        const int64_t P = near0 + 128 * static_cast<int64_t>(t - n_init - a.n_sel);
+        r.src = 2;
+        r.key0 = P;
+        r.page = 0;
+        r.lo = static_cast<int>(max(static_cast<int64_t>(0), a.local_start - P));
+        r.hi = static_cast<int>(min(static_cast<int64_t>(128), a.s + 1 - P));
+    }
+    return r;
+}
+
+__device__ __forceinline__ int dec_tiles(const AttnParams& a, int& n_init, int64_t& near0) {
+    n_init = static_cast<int>((a.init_len + 127) / 128);
+    near0 = (a.local_start / 128) * 128;
+    return n_init + a.n_sel + static_cast<int>((a.s + 1 - near0 + 127) / 128);
+}
+
+// shared-memory stage of one 128-key tile: K rows and V^T rows with 272-byte
+// rows (256 + 16 pad: ldmatrix conflict-free). Decode keys of the ring are
+// always within l_L of the query (the local window holds l_L tokens), so a
+// ring page is attended with rotated keys only; init / unit pages are far
+// (clamped: rope(q, l_L) . k_raw, attention.hpp:165-173).
+constexpr int kRowB = 272;
+constexpr int kMatB = 128 * kRowB;  // 34816
+constexpr int kStageB = 2 * kMatB;
+constexpr int kStages = 2;
+constexpr int kDecSmem = kStages * kStageB;
+
+__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+// D += A(16x16 bf16; rows >= 8 are zero: the <= 8 query heads of a group) * B(16x8)
+__device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// cp.async of tile `tl` (K page then V^T page, 2 x 32 KB contiguous) into stage `sb`
+__device__ __forceinline__ void dec_load(const AttnParams& a, const DecTile& tl, int g, uint32_t sb) {
+    const bf16 *k, *v;
+    int rows = 128;
+    if (tl.src == 0) {
+        k = static_cast<const bf16*>(a.init_k) + (static_cast<int64_t>(g) * a.l_I + tl.key0) * 128;
+        v = static_cast<const bf16*>(a.init_v) + (static_cast<int64_t>(g) * a.vl.nI + tl.page) * 128 * 128;
+        rows = static_cast<int>(min(static_cast<int64_t>(128), a.l_I - tl.key0));  // stay inside the init rows
+    } else if (tl.src == 1) {
+        k = static_cast<const bf16*>(a.unit_k) + (tl.page * a.G + g) * 128 * 128;
+        v = static_cast<const bf16*>(a.unit_v) + (tl.page * a.G + g) * 128 * 128;
+    } else {
+        const int64_t sl = tl.key0 % a.R;
+        k = static_cast<const bf16*>(a.ring_krot) + (static_cast<int64_t>(g) * a.R + sl) * 128;
+        v = static_cast<const bf16*>(a.ring_v) + (static_cast<int64_t>(g) * (a.R / 128) + sl / 128) * 128 * 128;
+    }
+    const int c = threadIdx.x & 15, r0 = threadIdx.x >> 4;  // 16 threads per 256-byte row
+    const uint32_t so = r0 * kRowB + c * 16;
+    const bf16* kp = k + r0 * 128 + c * 8;
+    const bf16* vp = v + r0 * 128 + c * 8;
+#pragma unroll
+    for (int i = 0; i < 128 / (kThr / 16); ++i) {
+        const int r = r0 + i * (kThr / 16);
+        if (r < rows) cpa16(sb + so + i * (kThr / 16) * kRowB, kp + i * (kThr / 16) * 128);
+        cpa16(sb + kMatB + so + i * (kThr / 16) * kRowB, vp + i * (kThr / 16) * 128);
+    }
+}
+
+__device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& sc, int b, int x, int nsplit) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    __shared__ float sred[kW][kDecMaxRep], sl_red[kW][kDecMaxRep];
+    __shared__ float s_m[kDecMaxRep], s_alpha[kDecMaxRep], s_M[kDecMaxRep], s_L[kDecMaxRep];
+    __shared__ bool s_last;
+
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (query head) / column pair
+    const int g = blockIdx.y, rep = a.rep;
+    const float sl2 = a.scale * kLog2e;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
+
+    int n_init;
+    int64_t near0;
+    const int T = dec_tiles(a, n_init, near0);
+    const int tps = (T + nsplit - 1) / nsplit;
+    const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
+
+    for (int st = 0; st < kStages; ++st) {  // prefetch the first tiles
+        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0), g, sbase + st * kStageB);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    // query fragments (A operand, row = query head of the group, zero beyond rep):
+    // rope(q, pos) for ring pages, rope(q, l_L) for init / unit pages; 8 k-steps of 16 dims
+    uint32_t qa[8][2], qc[8][2];
+    {
+        const bool hv = gq < rep;
+        const int64_t qrow = static_cast<int64_t>(g * rep + (hv ? gq : 0)) * a.lxp * 128;
+        const bf16* pa = static_cast<const bf16*>(a.qa) + qrow;
+        const bf16* pc = static_cast<const bf16*>(a.qc) + qrow;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            qa[kk][0] = hv ? *reinterpret_cast<const uint32_t*>(pa + 16 * kk + 2 * tq) : 0u;
+            qa[kk][1] = hv ? *reinterpret_cast<const uint32_t*>(pa + 16 * kk + 8 + 2 * tq) : 0u;
+            qc[kk][0] = hv ? *reinterpret_cast<const uint32_t*>(pc + 16 * kk + 2 * tq) : 0u;
+            qc[kk][1] = hv ? *reinterpret_cast<const uint32_t*>(pc + 16 * kk + 8 + 2 * tq) : 0u;
+        }
+    }
+    if (tid < kDecMaxRep) s_m[tid] = -INFINITY;
+    float o[16][4];  // O fragments of this warp's keys: 16 n-tiles of 8 dims (rows gq)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    float lsum = 0.f;  // this thread's share of the softmax denominator of row gq
+    const int k0 = 16 * warp;  // this warp's keys of every tile
+
+    for (int t = t0; t < t1; ++t) {
+        const int st = (t - t0) % kStages;
+        const DecTile tl = dec_tile(a, t, n_init, near0);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
+        __syncthreads();
+        const uint32_t sk = sbase + st * kStageB, sv = sk + kMatB;
+        // ---- S = Q K^T for keys k0..k0+15 (2 n-tiles) ----
+        float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        const bool far = tl.src != 2;
+        const uint32_t kaddr = sk + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * kRowB + ((lane >> 3) & 1) * 16;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kaddr + kk * 32, b0, b1, b2, b3);
+            const uint32_t A0 = far ? qc[kk][0] : qa[kk][0], A2 = far ? qc[kk][1] : qa[kk][1];
+            mma16816(s2[0], A0, A2, b0, b1);
+            mma16816(s2[1], A0, A2, b2, b3);
+        }
+        // mask + scale (log2 domain): row gq, key k0 + 8 j + 2 tq + e
+        float sv2[2][2];
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = k0 + 8 * j + 2 * tq + e;
+                const float v = (col >= tl.lo && col < tl.hi) ? s2[j][e] * sl2 : -INFINITY;
+                sv2[j][e] = v;
+                tmax = fmaxf(tmax, v);
+            }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+        if (tq == 0 && gq < kDecMaxRep) sred[warp][gq] = tmax;
+        __syncthreads();
+        if (tid < rep) {
+            float tm = sred[0][tid];
+#pragma unroll
+            for (int w = 1; w < kW; ++w) tm = fmaxf(tm, sred[w][tid]);
+            const float mo = s_m[tid];
+            const float mn = fmaxf(mo, tm);
+            s_m[tid] = mn;
+            s_alpha[tid] = mo == -INFINITY ? 0.f : ex2f(mo - mn);
+        }
+        __syncthreads();
+        const int hr = gq < kDecMaxRep ? gq : 0;
+        const float mrow = s_m[hr], al = s_alpha[hr];
+        float p[2][2], psum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                p[j][e] = sv2[j][e] == -INFINITY ? 0.f : ex2f(sv2[j][e] - mrow);
+                psum += p[j][e];
+            }
+        lsum = lsum * al + psum;
+        if (tl.src == 1 && a.want_mass) {  // the unit's mass relative to this tile's running max
+            float e2 = psum;
+            e2 += __shfl_xor_sync(0xffffffffu, e2, 1);
+            e2 += __shfl_xor_sync(0xffffffffu, e2, 2);
+            if (tq == 0 && gq < kDecMaxRep) sl_red[warp][gq] = e2;
+        }
+        // ---- O = O alpha + P V over this warp's 16 keys (one k-step; P from the S fragments) ----
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            o[j][0] *= al;
+            o[j][1] *= al;
+        }
+        const uint32_t A0 = pack_bf16(p[0][0], p[0][1]), A2 = pack_bf16(p[1][0], p[1][1]);
+        const uint32_t vaddr = sv + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowB + (k0 + ((lane >> 3) & 1) * 8) * 2;
+#pragma unroll
+        for (int jp = 0; jp < 8; ++jp) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(vaddr + 16 * jp * kRowB, b0, b1, b2, b3);
+            mma16816(o[2 * jp], A0, A2, b0, b1);
+            mma16816(o[2 * jp + 1], A0, A2, b2, b3);
+        }
+        __syncthreads();  // every warp is done with this stage
+        if (tl.src == 1 && a.want_mass && tid < rep) {
+            float e = 0.f;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) e += sl_red[w][tid];
+            const int u = t - n_init;
+            float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + tid) * sc.max_sel + u) * 2;
+            mr[0] = e;
+            mr[1] = s_m[tid];
+        }
+        if (t + kStages < t1) dec_load(a, dec_tile(a, t + kStages, n_init, near0), g, sbase + st * kStageB);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // ---- this split's partial (m, l, O) per head; the warps' O summed in smem ----
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    if (tq == 0 && gq < kDecMaxRep) sred[warp][gq] = lsum;
+    float* so = reinterpret_cast<float*>(dsm);  // [kW][rep][128] (the stages are free now)
+    __syncthreads();
+    if (gq < rep) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            *reinterpret_cast<float2*>(&so[(warp * rep + gq) * 128 + 8 * j + 2 * tq]) = make_float2(o[j][0], o[j][1]);
+    }
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(rep) * 130;
+    float* part = sc.part + ((static_cast<int64_t>(b) * a.G + g) * nsplit + x) * stride;
+    if (tid < rep) {
+        float l = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) l += sred[w][tid];
+        part[tid * 130 + 0] = s_m[tid];
+        part[tid * 130 + 1] = l;
+    }
+    for (int i = tid; i < rep * 128; i += kThr) {
+        const int h = i / 128, c = i % 128;
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) v += so[(w * rep + h) * 128 + c];
+        part[h * 130 + 2 + c] = v;
+    }
+    // ---- the last split of (sequence, group) merges ----
+    __threadfence();
+    __syncthreads();
+    unsigned* cnt = sc.cnt + static_cast<int64_t>(b) * a.G + g;
+    if (tid == 0) s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(nsplit - 1);
+    __syncthreads();
+    if (!s_last || (sc.dbg & 2)) {
+        if (s_last && tid == 0) *cnt = 0;
+        return;
+    }
+    __threadfence();
+    const float* p0 = sc.part + (static_cast<int64_t>(b) * a.G + g) * nsplit * stride;
+    __shared__ float s_w[kDecMaxSplits][kDecMaxRep], s_ls[kDecMaxSplits][kDecMaxRep];
+    // mass records of the retrieved units, loaded up front (one round trip)
+    float mrec[2 * kDecMaxRep];
+    const bool mass_thread = a.want_mass && a.mass_part && tid < a.n_sel;
+    if (mass_thread) {
+#pragma unroll
+        for (int h = 0; h < kDecMaxRep; ++h) {
+            if (h >= rep) break;
+            const float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + h) * sc.max_sel + tid) * 2;
+            mrec[2 * h] = __ldcg(mr);
+            mrec[2 * h + 1] = __ldcg(mr + 1);
+        }
+    }
+    for (int i = tid; i < nsplit * rep; i += kThr) {
+        const int xs = i / rep, h = i % rep;
+        s_w[xs][h] = __ldcg(p0 + xs * stride + h * 130);
+        s_ls[xs][h] = __ldcg(p0 + xs * stride + h * 130 + 1);
+    }
+    // this thread's O values: (split, head, dim) with dim = tid % 128, heads split over the two halves
+    const int c = tid & 127, hh = tid >> 7;
+    __syncthreads();
+    if (tid < rep) {
+        float M = -INFINITY;
+        for (int xs = 0; xs < nsplit; ++xs) M = fmaxf(M, s_w[xs][tid]);
+        float L = 0.f;
+        for (int xs = 0; xs < nsplit; ++xs) {
+            const float mx = s_w[xs][tid];
+            if (mx != -INFINITY) L += s_ls[xs][tid] * ex2f(mx - M);
+        }
+        s_M[tid] = M;
+        s_L[tid] = L;
+    }
+    __syncthreads();
+    for (int i = tid; i < nsplit * rep; i += kThr) {
+        const int xs = i / rep, h = i % rep;
+        const float mx = s_w[xs][h];
+        s_w[xs][h] = mx == -INFINITY ? 0.f : ex2f(mx - s_M[h]) / s_L[h];
+    }
+    __syncthreads();
+    for (int h = hh; h < rep; h += 2) {
+        float acc = 0.f;
+        for (int x0 = 0; x0 < nsplit; x0 += 32) {
+            float ov[32];
+#pragma unroll
+            for (int u = 0; u < 32; ++u) ov[u] = x0 + u < nsplit ? __ldcg(p0 + (x0 + u) * stride + h * 130 + 2 + c) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+                if (x0 + u < nsplit) acc = fmaf(ov[u], s_w[x0 + u][h], acc);
+        }
+        static_cast<bf16*>(a.out)[static_cast<int64_t>(g * rep + h) * a.dv + c] = __float2bfloat16_rn(acc);
+    }
+    // masses of the retrieved units: this group's heads' normalised weights of
+    // the unit's keys, summed (engine.hpp:271-283; the LRU divides by H)
+    if (mass_thread) {
+        double msum = 0.0;
+#pragma unroll
+        for (int h = 0; h < kDecMaxRep; ++h) {
+            if (h >= rep) break;
+            msum += static_cast<double>(mrec[2 * h] * ex2f(mrec[2 * h + 1] - s_M[h]) / s_L[h]);
+        }
+        a.mass_part[static_cast<int64_t>(tid) * a.Gtot + a.g0 + g] = msum;
+    }
+    if (tid == 0) *cnt = 0;
+}
+
+__global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch sc) {
+    dec_body(a, sc, 0, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restrict__ ps, DecScratch sc) {
+    dec_body(ps[blockIdx.z], sc, blockIdx.z, blockIdx.x, gridDim.x);
+}
+
+int pick_splits(int64_t max_tiles, int G, int B) {
+    const int64_t want = (148 + static_cast<int64_t>(G) * B - 1) / (static_cast<int64_t>(G) * B);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, max_tiles, kDecMaxSplits})));
+}
+
+}  // namespace
+
+bool attn_dec_supported(int d, int dv, int unit_size, int rep, bool absolute, int dtype_bf16) {
+    return dtype_bf16 && d == 128 && dv == 128 && unit_size == 128 && rep <= kDecMaxRep && !absolute;
+}
+
+int64_t dec_max_tiles(const AttnParams& a) {
+    const int64_t n_init = (a.init_len + 127) / 128, near0 = (a.local_start / 128) * 128;
+    return n_init + a.n_sel + (a.s + 1 - near0 + 127) / 128;
+}
+
+void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st) {
+    DecScratch sc = sc0;
+    static const int dbg = getenv("INFLLM_DEC_DBG") ? atoi(getenv("INFLLM_DEC_DBG")) : 0;
+    static const int nsf = getenv("INFLLM_DEC_SPLITS") ? atoi(getenv("INFLLM_DEC_SPLITS")) : 0;
+    sc.dbg = dbg;
+    const int ns = nsf > 0 ? std::min<int>(nsf, static_cast<int>(dec_max_tiles(a))) : pick_splits(dec_max_tiles(a), a.G, 1);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attn_dec1, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+        cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+        attr = true;
+    }
+    k_attn_dec1<<<dim3(ns, a.G, 1), kThr, kDecSmem, st>>>(a, sc);
+}
+
+void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,
+                           cudaStream_t st) {
+    const int ns = pick_splits(max_tiles, G, B);
+    cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
+    k_attn_decb<<<dim3(ns, G, B), kThr, kDecSmem, st>>>(dev_params, sc);
+}
+
+}  // namespace infllm

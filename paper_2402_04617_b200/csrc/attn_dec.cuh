@@ -1,0 +1,32 @@
+// attn_dec.cuh — K4 decode attention (l_x = 1), single sequence or batched.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace infllm {
+
+constexpr int kDecMaxRep = 8;      // query heads per KV group
+constexpr int kDecMaxSplits = 64;  // KV splits per (sequence, group)
+
+// scratch of one launch: split partials (m, l, O[128]) per head, per-unit
+// (mass, running max) records, and per-(sequence, group) arrival counters
+// (zero-initialised once; the merging CTA resets its counter)
+struct DecScratch {
+    float* part;    // [B][G][splits][rep][130]
+    float* mass;    // [B][H][max_sel][2]
+    unsigned* cnt;  // [B][G]
+    int max_sel;
+    int dbg;  // timing experiments only: bit0 skip tiles, bit1 skip merge
+};
+inline size_t dec_part_floats(int B, int G, int rep) {
+    return static_cast<size_t>(B) * G * kDecMaxSplits * rep * 130;
+}
+
+bool attn_dec_supported(int d, int dv, int unit_size, int rep, bool absolute, int dtype_bf16);
+int64_t dec_max_tiles(const AttnParams& a);
+void launch_attn_dec(const AttnParams& a, const DecScratch& sc, cudaStream_t st);
+// dev_params: B AttnParams in device memory; G KV groups per sequence (all equal)
+void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,
+                           cudaStream_t st);
+
+}  // namespace infllm

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/infllm_b200.h"
+#include "attn_dec.cuh"
 #include "attn_tc.cuh"
 #include "kernels.cuh"
 
@@ -197,6 +198,8 @@ struct infllm_engine {
     bool use_tc = false;
     bool tc_disabled = false;
     bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
+    bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
+    bool dec_disabled = false;
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -236,6 +239,7 @@ struct infllm_engine {
 
     // scratch shared by layers (layers run sequentially on one stream)
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, tsum, topk_done, evict_done;
+    DBuf dec_part, dec_mass, dec_cnt;  // K4 decode scratch (one sequence)
 
     struct Layer {
         int64_t n_fed = 0, step = 0, local_start = 0, init_len = 0;
@@ -408,10 +412,25 @@ struct infllm_engine {
         L.trace_cap = cap;
     }
 
+    DecScratch dec_scratch() const {
+        return DecScratch{dec_part.as<float>(), dec_mass.as<float>(), dec_cnt.as<unsigned>(),
+                          static_cast<int>(std::max<int64_t>(cfg.n_lookup, 1)), 0};
+    }
+
     // where unit pages are written (HBM pool, or the host tier)
     void* upage_k(const Layer& L) const { return tier_slots > 0 ? L.dhost_k : L.unit_k.p; }
     void* upage_krot(const Layer& L) const { return tier_slots > 0 ? L.dhost_krot : L.unit_krot.p; }
     void* upage_v(const Layer& L) const { return tier_slots > 0 ? L.dhost_v : L.unit_v.p; }
+
+    bool one_stream = false;           // current step runs on the caller's stream only
+    bool pipe_dirty = false;           // pipeline streams may hold work the caller's stream does not wait for
+    bool multi_stream_decode = false;  // option: keep the five-stream pipeline for decode steps
+    void rec(cudaEvent_t e, cudaStream_t s2) {
+        if (!one_stream) ck(cudaEventRecord(e, s2), "record");
+    }
+    void wt(cudaStream_t s2, cudaEvent_t e) {
+        if (!one_stream) ck(cudaStreamWaitEvent(s2, e, 0), "wait");
+    }
 
     // make `st` wait for everything queued on the side stream
     void join_side(cudaStream_t st) {
@@ -432,6 +451,7 @@ struct infllm_engine {
         for (auto& a : attn_seq) a = -1;
         lookup_seq = -1;
         evict_seq = -1;
+        pipe_dirty = false;
     }
 
     void gather(double* buf, int64_t rows, cudaStream_t st) {
@@ -495,18 +515,26 @@ struct infllm_engine {
         const int64_t kseq = seq++;
         const int b = static_cast<int>(kseq & 1);
         const int pb = static_cast<int>(kseq % kPB);  // prep-output buffer (the prep runs up to 2 steps ahead)
-        cudaStream_t main = st, side = side_stream, pst = prep_stream, est = evict_stream;
+        // decode steps (one token) run on the caller's stream alone: the
+        // multi-stream pipeline only pays for chunk-sized steps, and skipping
+        // its ~25 event calls halves the host cost of a decode step
+        one_stream = lx == 1 && !capturing && !multi_stream_decode;
+        cudaStream_t main = st, side = one_stream ? st : side_stream, pst = one_stream ? st : prep_stream,
+                     est = one_stream ? st : evict_stream;
+        cudaStream_t lru_st = one_stream ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
+        if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
+        pipe_dirty = !one_stream;
         if (fork) {
-            ck(cudaEventRecord(e_call, main), "record");
-            ck(cudaStreamWaitEvent(side, e_call, 0), "wait");
-            ck(cudaStreamWaitEvent(pst, e_call, 0), "wait");
+            rec(e_call, main);
+            wt(side, e_call);
+            wt(pst, e_call);
         }
-        if (inputs_ready) ck(cudaStreamWaitEvent(pst, inputs_ready, 0), "wait");
+        if (inputs_ready) wt(pst, inputs_ready);
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
-            ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // sel of this parity: attention + LRU k-2
+            wt(side, e_lru[b]);  // sel of this parity: attention + LRU k-2
         // qa/qc/chunk sums of this buffer were last read by attention k-3 (and its lookup)
         if (attn_seq[pb] >= 0 && (capture_seq0 < 0 || attn_seq[pb] >= capture_seq0))
-            ck(cudaStreamWaitEvent(pst, e_attnp[pb], 0), "wait");
+            wt(pst, e_attnp[pb]);
         // chunk query sums are double-buffered by step parity: the lookup of step
         // k-2 (which read this parity) ran before attention k-2, covered by e_lru[b]
         void* qa_b = static_cast<uint8_t*>(qa.p) + pb * qa_half;
@@ -550,8 +578,8 @@ struct infllm_engine {
         last_bf16 = std::is_same_v<T, bf16>;
         if (!(debug_skip & 8)) launch_prep<T>(pp, st);
         launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
-        ck(cudaEventRecord(e_prep, pst), "record");
-        ck(cudaStreamWaitEvent(side, e_prep, 0), "wait");
+        rec(e_prep, pst);
+        wt(side, e_prep);
         st = side;
 
         // window roll: init pinning, eviction, representative scoring, packing.
@@ -562,9 +590,9 @@ struct infllm_engine {
         const int64_t n_units0 = L.n_units, init_len0 = L.init_len, local_start0 = L.local_start;
         // this step's lookup (side stream) sees the units completed by the previous step
         if (evict_seq >= 0 && (capture_seq0 < 0 || evict_seq >= capture_seq0))
-            ck(cudaStreamWaitEvent(side, e_evict, 0), "wait");
+            wt(side, e_evict);
         st = est;
-        ck(cudaStreamWaitEvent(est, e_prep, 0), "wait");
+        wt(est, e_prep);
         if (overflow > 0) {
             // UnitPacker::add: an empty packer starts its pending run at the
             // first evicted token (memory.hpp:65-66)
@@ -653,7 +681,7 @@ struct infllm_engine {
             L.local_start += overflow;
             L.init_len += to_init;
         }
-        ck(cudaEventRecord(e_evict, est), "record");
+        rec(e_evict, est);
         evict_seq = kseq;
         st = side;
 
@@ -706,10 +734,10 @@ struct infllm_engine {
             }
         }
 
-        ck(cudaEventRecord(e_topk, side), "record");
-        if (!(debug_skip & 32)) ck(cudaStreamWaitEvent(main, e_topk, 0), "wait");  // 32: timing experiment only
+        rec(e_topk, side);
+        if (!(debug_skip & 32)) wt(main, e_topk);  // 32: timing experiment only
         if (tier_slots > 0 && n_sel > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
-            ck(cudaStreamWaitEvent(tier_stream, e_topk, 0), "wait");
+            wt(tier_st, e_topk);
             TierParams tp2{};
             tp2.sel = sel_b;
             tp2.sel_slot = L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
@@ -731,17 +759,17 @@ struct infllm_engine {
             tp2.page_k = static_cast<int64_t>(unit_elems_k() * esz);
             tp2.page_v = static_cast<int64_t>(unit_elems_v() * esz);
             tp2.kmax = static_cast<int>(n_sel);
-            launch_tier(tp2, tier_stream);
+            launch_tier(tp2, tier_st);
             tier_seq = kseq;
             launches += 2;
-            ck(cudaEventRecord(e_tier, tier_stream), "record");
-            ck(cudaStreamWaitEvent(main, e_tier, 0), "wait");
+            rec(e_tier, tier_st);
+            wt(main, e_tier);
         }
-        ck(cudaEventRecord(e_lookup, side), "record");
+        rec(e_lookup, side);
         lookup_seq = kseq;
         // this parity's mass buffers were last read by LRU(k-2)
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
-            ck(cudaStreamWaitEvent(main, e_lru[b], 0), "wait");
+            wt(main, e_lru[b]);
         st = main;
         double* mass_cta_b = mass_cta.as<double>() + b * mass_cta_half;
         double* mass_part_b = L.mass_part.as<double>() + b * std::max<int64_t>(cfg.n_lookup, 1) * Gt;
@@ -791,6 +819,10 @@ struct infllm_engine {
         ap.scale = 1.0f / std::sqrt(static_cast<float>(d));  // attention.hpp:140
         ap.vl = vl;
         ap.unit_cap = tier ? tier_slots : L.unit_cap;
+        ap.mass_part = mass_part_b;
+        ap.Gtot = Gt;
+        ap.g0 = g0;
+        const bool dec_ran = lx == 1 && use_dec && !dec_disabled;
         last_ap = ap;
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
@@ -799,6 +831,9 @@ struct infllm_engine {
         }
         if constexpr (std::is_same_v<T, bf16>) {
             if (debug_skip & 1) {
+            } else if (dec_ran) {
+                launch_attn_dec(ap, dec_scratch(), st);
+                ++launches;
             } else if (tc_eligible(lx)) {
                 launches += launch_attn_tc(ap, st);
             } else {
@@ -816,10 +851,12 @@ struct infllm_engine {
 
         // attention masses -> lookup bookkeeping, frequency update, capacity
         // (engine.hpp:257,271-285; memory.hpp:254-300)
-        const bool tc_ran = std::is_same_v<T, bf16> && tc_eligible(lx);
+        const bool tc_ran = std::is_same_v<T, bf16> && tc_eligible(lx) && !dec_ran;
         int mass_src = 0;
         if (want_mass) {
-            if (tc_ran && attn_tc_masses_in_kernel(static_cast<int>(n_sel))) {
+            if (dec_ran) {
+                gather(mass_part_b, n_sel, st);  // per-group masses written by the decode kernel
+            } else if (tc_ran && attn_tc_masses_in_kernel(static_cast<int>(n_sel))) {
                 if (Gs == Gt) {
                     mass_src = 1;
                 } else {
@@ -870,17 +907,22 @@ struct infllm_engine {
         lp.decay = cfg.decay;
         lp.bytes_per_token = static_cast<int64_t>(Gs) * (d + dv) * static_cast<int64_t>(esz);
         // TieredStore bookkeeping runs on its own stream, off the attention critical path
-        ck(cudaEventRecord(e_attn, main), "record");
-        ck(cudaEventRecord(e_attnp[pb], main), "record");
+        rec(e_attn, main);
+        rec(e_attnp[pb], main);
         attn_seq[pb] = kseq;
-        ck(cudaStreamWaitEvent(lru_stream, e_attn, 0), "wait");
+        wt(lru_st, e_attn);
         last_lp = lp;
-        if (!(debug_skip & 16)) launch_lru(lp, lru_stream);
+        if (!(debug_skip & 16)) launch_lru(lp, lru_st);
         ++launches;
-        ck(cudaEventRecord(e_lru[b], lru_stream), "record");
+        rec(e_lru[b], lru_st);
         lru_seq[b] = kseq;
         st = side;
 
+        if (one_stream) {  // nothing was recorded: no later step may wait on this step's events
+            lru_seq[0] = lru_seq[1] = -1;
+            for (auto& a2 : attn_seq) a2 = -1;
+            lookup_seq = evict_seq = tier_seq = -1;
+        }
         L.trace_count += n_sel;
         L.last_n_sel = n_sel;
         L.last_b = b;
@@ -1171,6 +1213,8 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->use_tc = dtype == INFLLM_DTYPE_BF16 && attn_tc_supported(e->d, e->dv, static_cast<int>(cfg->unit_size),
                                                                      cfg->position_mode == INFLLM_POSITION_ABSOLUTE);
         e->vl.vt = e->use_tc ? 1 : 0;
+        e->use_dec = e->use_tc && attn_dec_supported(e->d, e->dv, static_cast<int>(cfg->unit_size), e->rep,
+                                                     cfg->position_mode == INFLLM_POSITION_ABSOLUTE, 1);
         e->vl.R = e->R;
         e->vl.nI = static_cast<int>((std::max<int64_t>(cfg->init_size, 1) + 127) / 128);
         e->vl.l_I = cfg->init_size;
@@ -1205,6 +1249,11 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
         e->mass_cta_half = static_cast<int64_t>(e->Hs) * (e->lxp / 128) * km;
         e->mass_cta.alloc(2 * e->mass_cta_half * sizeof(double), st);
+        if (e->use_dec) {
+            e->dec_part.alloc(dec_part_floats(1, e->Gs, e->rep) * sizeof(float), st, false);
+            e->dec_mass.alloc(static_cast<size_t>(e->Hs) * km * 2 * sizeof(float), st);
+            e->dec_cnt.alloc(static_cast<size_t>(e->Gs) * sizeof(unsigned), st);
+        }
         e->layers.resize(static_cast<size_t>(e->n_layers));
         for (auto& L : e->layers) {
             L.ring_k.alloc(static_cast<size_t>(e->Gs) * e->R * e->d * es, st);
@@ -1233,7 +1282,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         if (!e) return;
         cudaDeviceSynchronize();
         cudaStream_t st = nullptr;
-        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->tsum, &e->topk_done, &e->evict_done}) b->release(st);
+        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->tsum, &e->topk_done, &e->evict_done, &e->dec_part, &e->dec_mass, &e->dec_cnt}) b->release(st);
         for (auto& L : e->layers)
             for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
@@ -1339,6 +1388,10 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->debug_skip = value;
         else if (k == "attn_score_bound")
             e->score_bound = value != 0;
+        else if (k == "decode_kernel")
+            e->dec_disabled = value == 0;
+        else if (k == "multi_stream_decode")
+            e->multi_stream_decode = value != 0;
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
                 if (L.unit_cap > 0 && value != e->tier_slots)

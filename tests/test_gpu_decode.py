@@ -1,0 +1,78 @@
+"""K4 decode attention (l_x = 1, split-KV on CUDA cores) and batched decode.
+
+decode_step (engine.hpp:100-103) runs the full step with a single query row:
+lookup of that token, attention over [initial | retrieved units | local |
+itself], one evicted token per step once the window is full, a completed unit
+every 128 steps, LRU. Bars: ids, representatives, counters and trace exact vs
+the oracle; outputs within 2e-2 (bf16 inputs, oracle on the rounded values).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests.parity_util import compare_state, gaussian_inputs, rel_err, run_pair
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(chunk_size=256, unit_size=128, n_repr=4, local_size=1024, init_size=128, n_lookup=8, hot_capacity=12)
+
+
+def _check(oeng, geng, recs, tol=2e-2):
+    worst = 0.0
+    for r in recs:
+        assert r["o_ids"] == r["g_ids"], f"step {r['step']}: {r['o_ids']} vs {r['g_ids']}"
+        worst = max(worst, rel_err(r["g_out"], r["o_out"]))
+    assert worst <= tol, worst
+    diffs, repr_bad = compare_state(oeng, geng)
+    assert not diffs, diffs
+    assert not repr_bad
+    assert oeng.trace() == geng.trace()
+    return worst
+
+
+@pytest.mark.parametrize("slots", [0, 16])
+def test_decode_kernel_vs_oracle(slots):
+    """300 decode steps after a 4K prefill: units complete during decode (every
+    128 evictions), retrieved units change every step; optionally through the
+    host tier."""
+    n_pre, n_dec = 4096, 300
+    n = n_pre + n_dec
+    q, k, v = gaussian_inputs(51, n, 8, 2, 128, scale=0.3, bf16=True)
+    sched = O.encode_schedule(n_pre, 256, 0) + [1] * n_dec
+    opts = {"host_tier_slots": slots} if slots else {}
+    oeng, geng, recs = run_pair(CFG, 8, 2, 128, q, k, v, sched, decode_tail=n_dec, dtype=torch.bfloat16,
+                                options=opts)
+    _check(oeng, geng, recs)
+    assert oeng.metrics()["units"] > (n_pre - 128 - 1024) // 128  # units were created during decode
+
+
+def test_decode_kernel_matches_tc_path():
+    """K4 vs the tcgen05 kernel on the same decode steps (C2 head shape)."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=2048, init_size=128, n_lookup=16, hot_capacity=32)
+    n_pre, n_dec = 8192, 64
+    q, k, v = gaussian_inputs(52, n_pre + n_dec, 32, 8, 128, scale=0.3, bf16=True)
+    qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+    outs = []
+    for dec in (1, 0):
+        eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128),
+                           dtype=torch.bfloat16)
+        eng.set_option("decode_kernel", dec)
+        eng.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
+        o = [eng.decode_step(qt[i:i + 1], kt[i:i + 1], vt[i:i + 1]).float().cpu() for i in range(n_pre, n_pre + n_dec)]
+        outs.append((torch.cat(o).numpy(), eng.metrics(), eng.trace()))
+    assert rel_err(outs[0][0], outs[1][0]) < 2e-2
+    assert outs[0][1] == outs[1][1]
+    assert outs[0][2] == outs[1][2]
+
+
+def test_decode_from_empty_stream():
+    """Decode-only stream from token 0 (no units for the first steps, init
+    pinning while decoding): the window grows from one key."""
+    cfg = dict(chunk_size=64, unit_size=128, n_repr=4, local_size=256, init_size=128, n_lookup=4, hot_capacity=8)
+    n = 700
+    q, k, v = gaussian_inputs(53, n, 8, 2, 128, scale=0.3, bf16=True)
+    oeng, geng, recs = run_pair(cfg, 8, 2, 128, q, k, v, [1] * n, decode_tail=n, dtype=torch.bfloat16)
+    _check(oeng, geng, recs)
