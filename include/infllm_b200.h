@@ -149,7 +149,10 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * cache filled on demand over PCIe on a side stream -- the north star's
  * host-offloaded store; TieredStore's hot/cold tiers (memory.hpp:165-168) are
  * bookkeeping only in the reference, outputs are identical either way;
- * 2*n_lookup <= S <= 16384; set before reserve() and the first step). */
+ * 2*n_lookup <= S <= 16384; set before reserve() and the first step),
+ * "decode_kernel" (1 = split-KV decode attention for one-token steps,
+ * default; 0 = the prefill attention kernel), "multi_stream_decode" (1 = run
+ * decode steps through the five-stream pipeline; default 0 = caller's stream). */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if
@@ -179,6 +182,17 @@ int infllm_encode_stream_host(infllm_engine_t eng, int32_t layer, const void* ho
  * lookup_mode == none. */
 int infllm_decode_step(infllm_engine_t eng, int32_t layer, const void* q, const void* k,
                        const void* v, void* out, void* stream);
+
+/* Batched decode (BASELINE configs[4]): one
+ * StreamEngine::decode_step (engine.hpp:100-103) for each of n independent
+ * sequences, engine i owning sequence i. q [n][H][d], k/v [n][H_kv][d], out
+ * [n][H][d_v], device memory. Every stage (prep, eviction, unit selection,
+ * lookup + top-k, attention, LRU) is one launch for all n sequences when the
+ * engines share config and shape (bf16, d = 128, unit 128, single shard, no
+ * host tier); otherwise the engines step one after another. Results equal n
+ * decode_step calls. */
+int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const void* q,
+                        const void* k, const void* v, void* out, void* stream);
 
 /* StreamEngine::finish (engine.hpp:115-119): flushes each layer's held-back
  * partial unit. Synchronous. */

@@ -182,8 +182,32 @@ __global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
 
 }  // namespace
 
+// parameters of one batched decode step, gathered from each engine's step()
+struct DecodeCollector {
+    std::vector<PrepParams> prep;
+    std::vector<EvictParams> evict;
+    std::vector<SelectParams> select;
+    std::vector<LookupParams> lookup;
+    std::vector<AttnParams> attn;
+    std::vector<LruParams> lru;
+};
+
+// device/host resources of batched decode calls (owned by the batch's first engine)
+struct BatchCtx {
+    static constexpr int kSlots = 2;
+    void* host[kSlots] = {nullptr, nullptr};  // pinned parameter staging
+    void* dev[kSlots] = {nullptr, nullptr};   // device parameter tables
+    size_t cap = 0;
+    cudaEvent_t done[kSlots] = {nullptr, nullptr};
+    int slot = 0;
+    DBuf part, mass, cnt;  // K4 batch scratch
+    int part_B = 0, mass_B = 0;
+};
+
 struct infllm_engine {
     infllm_engine_config cfg{};
+    DecodeCollector* coll = nullptr;  // decode_batch: record kernel parameters instead of launching
+    std::unique_ptr<BatchCtx> bctx;
     int H = 1, Gt = 1, rep = 1, d = 0, dv = 0, n_layers = 1;
     int g0 = 0, Gs = 1, Hs = 1;  // shard
     int dtype = INFLLM_DTYPE_F32;
@@ -576,7 +600,10 @@ struct infllm_engine {
         pp.kmax2_prev = kbound ? L.kmax2.as<float>() + ((lb + kPB - 1) % kPB) * Gs : nullptr;
         last_pp = pp;
         last_bf16 = std::is_same_v<T, bf16>;
-        if (!(debug_skip & 8)) launch_prep<T>(pp, st);
+        if (coll)
+            coll->prep.push_back(pp);
+        else if (!(debug_skip & 8))
+            launch_prep<T>(pp, st);
         launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
         rec(e_prep, pst);
         wt(side, e_prep);
@@ -637,7 +664,12 @@ struct infllm_engine {
             ep.done = evict_done.as<unsigned int>();
             ep.page_mode = page_mode() ? 1 : 0;
             last_ep = ep;
-            if (!(debug_skip & 4)) launch_evict<T>(ep, st);
+            if (coll) {
+                if (!ep.fused) throw StreamError("decode_batch: sharded eviction is not batched");
+                if (ep.n_init + ep.n_evict > 0) coll->evict.push_back(ep);
+            } else if (!(debug_skip & 4)) {
+                launch_evict<T>(ep, st);
+            }
             ++launches;
             if (!ep.fused && to_evict > 0) {
                 gather(L.ev_part.as<double>(), to_evict, st);
@@ -668,7 +700,10 @@ struct infllm_engine {
                 sp.d = d;
                 sp.l_bs = static_cast<int>(cfg.unit_size);
                 set_page(sp, L, L.pend_start);
-                if (!(debug_skip & 4)) launch_select<T>(sp, st);
+                if (coll)
+                    coll->select.push_back(sp);
+                else if (!(debug_skip & 4))
+                    launch_select<T>(sp, st);
                 ++launches;
                 for (int64_t c = 0; c < completed; ++c) {
                     L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
@@ -711,7 +746,12 @@ struct infllm_engine {
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
             last_lkp = lp;
-            if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            if (coll) {  // batched: relevance scan (rel only) + one top-k block per sequence
+                lp.fused = 2;
+                coll->lookup.push_back(lp);
+            }
+            if (coll) {
+            } else if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
@@ -721,7 +761,7 @@ struct infllm_engine {
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
-            if (lp.fused == 2) {
+            if (lp.fused == 2 && !coll) {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
@@ -832,7 +872,10 @@ struct infllm_engine {
         if constexpr (std::is_same_v<T, bf16>) {
             if (debug_skip & 1) {
             } else if (dec_ran) {
-                launch_attn_dec(ap, dec_scratch(), st);
+                if (coll)
+                    coll->attn.push_back(ap);
+                else
+                    launch_attn_dec(ap, dec_scratch(), st);
                 ++launches;
             } else if (tc_eligible(lx)) {
                 launches += launch_attn_tc(ap, st);
@@ -912,7 +955,10 @@ struct infllm_engine {
         attn_seq[pb] = kseq;
         wt(lru_st, e_attn);
         last_lp = lp;
-        if (!(debug_skip & 16)) launch_lru(lp, lru_st);
+        if (coll)
+            coll->lru.push_back(lp);
+        else if (!(debug_skip & 16))
+            launch_lru(lp, lru_st);
         ++launches;
         rec(e_lru[b], lru_st);
         lru_seq[b] = kseq;
@@ -1137,6 +1183,22 @@ struct infllm_engine {
     }
 };
 
+namespace {
+bool batchable(const infllm_engine* e, const infllm_engine* e0, int32_t layer) {
+    return e && e->dtype == INFLLM_DTYPE_BF16 && e->use_dec && !e->dec_disabled && e->Gs == e->Gt &&
+           e->tier_slots == 0 && e->page_mode() && e->H == e0->H && e->Gt == e0->Gt && e->d == e0->d &&
+           e->dv == e0->dv && e->device == e0->device && std::memcmp(&e->cfg, &e0->cfg, sizeof(e->cfg)) == 0 &&
+           layer >= 0 && layer < e->n_layers && e->layers[static_cast<size_t>(layer)].n_units <= 8192;
+}
+template <typename P>
+size_t put(std::vector<uint8_t>& buf, const std::vector<P>& v) {
+    const size_t off = (buf.size() + 255) / 256 * 256;
+    buf.resize(off + v.size() * sizeof(P));
+    if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(P));
+    return off;
+}
+}  // namespace
+
 extern "C" {
 
 const char* infllm_last_error(void) { return g_err.c_str(); }
@@ -1322,6 +1384,14 @@ int infllm_engine_destroy(infllm_engine_t e) {
                         e->e_attnp[2], e->e_tier, e->e_tierdone})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
+        if (e->bctx) {
+            for (int t = 0; t < BatchCtx::kSlots; ++t) {
+                if (e->bctx->host[t]) cudaFreeHost(e->bctx->host[t]);
+                if (e->bctx->dev[t]) cudaFree(e->bctx->dev[t]);
+                if (e->bctx->done[t]) cudaEventDestroy(e->bctx->done[t]);
+            }
+            for (auto* b : {&e->bctx->part, &e->bctx->mass, &e->bctx->cnt}) b->release(nullptr);
+        }
         delete e;
     });
 }
@@ -1429,6 +1499,108 @@ int infllm_decode_step(infllm_engine_t e, int32_t layer, const void* q, const vo
             e->step<bf16>(layer, q, k, v, 1, true, out, st);
         else
             e->step<float>(layer, q, k, v, 1, true, out, st);
+    });
+}
+
+// Batched decode: one decode step of `n` independent
+// sequences (one engine each), every stage one launch for all of them. Each
+// engine's step() runs in collect mode (host stream arithmetic, pool growth,
+// parameter structs, no launches); the parameter tables go to the device in
+// one copy; then prep, eviction, unit selection, lookup + top-k, K4 attention
+// and LRU each launch once with grid.z (or grid.x) = sequence.
+int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const void* q, const void* k,
+                        const void* v, void* out, void* stream) {
+    return guard([&] {
+        if (!engs || n < 1) throw ConfigError("decode_batch: no engines");
+        auto st = static_cast<cudaStream_t>(stream);
+        infllm_engine* e0 = engs[0];
+        if (!e0) throw ConfigError("null engine");
+        const size_t qrow = static_cast<size_t>(e0->Hs) * e0->d * e0->esz, krow = static_cast<size_t>(e0->Gs) * e0->d * e0->esz;
+        const size_t vrow = static_cast<size_t>(e0->Gs) * e0->dv * e0->esz, orow = static_cast<size_t>(e0->Hs) * e0->dv * e0->esz;
+        bool all = true;
+        for (int32_t i = 0; i < n; ++i) all = all && batchable(engs[i], e0, layer);
+        for (int32_t i = 0; i < n && all; ++i)
+            for (int32_t j = 0; j < i; ++j)
+                if (engs[i] == engs[j]) all = false;
+        auto at = [](const void* p, size_t off) { return static_cast<const uint8_t*>(p) + off; };
+        if (!all) {  // other shapes / modes: the per-engine decode step, sequence by sequence
+            for (int32_t i = 0; i < n; ++i) {
+                if (!engs[i]) throw ConfigError("null engine");
+                if (engs[i]->dtype == INFLLM_DTYPE_BF16)
+                    engs[i]->step<bf16>(layer, at(q, i * qrow), at(k, i * krow), at(v, i * vrow),
+                                        1, true, const_cast<uint8_t*>(at(out, i * orow)), st);
+                else
+                    engs[i]->step<float>(layer, at(q, i * qrow), at(k, i * krow), at(v, i * vrow),
+                                         1, true, const_cast<uint8_t*>(at(out, i * orow)), st);
+            }
+            return;
+        }
+        DecodeCollector c;
+        for (int32_t i = 0; i < n; ++i) {
+            engs[i]->coll = &c;
+            try {
+                engs[i]->step<bf16>(layer, at(q, i * qrow), at(k, i * krow), at(v, i * vrow), 1, true,
+                                    const_cast<uint8_t*>(at(out, i * orow)), st);
+            } catch (...) {
+                engs[i]->coll = nullptr;
+                throw;
+            }
+            engs[i]->coll = nullptr;
+        }
+        if (static_cast<int32_t>(c.prep.size()) != n || static_cast<int32_t>(c.attn.size()) != n ||
+            static_cast<int32_t>(c.lru.size()) != n)
+            throw StreamError("decode_batch: unexpected step shape");
+        if (!e0->bctx) e0->bctx = std::make_unique<BatchCtx>();
+        BatchCtx& bc = *e0->bctx;
+        std::vector<uint8_t> buf;
+        const size_t o_prep = put(buf, c.prep), o_ev = put(buf, c.evict), o_sel = put(buf, c.select);
+        const size_t o_lk = put(buf, c.lookup), o_at = put(buf, c.attn), o_lru = put(buf, c.lru);
+        const int s = bc.slot;
+        bc.slot = (bc.slot + 1) % BatchCtx::kSlots;
+        if (bc.done[s]) ck(cudaEventSynchronize(bc.done[s]), "batch slot");  // the batch two calls back
+        if (buf.size() > bc.cap) {
+            ck(cudaDeviceSynchronize(), "batch table growth");
+            for (int t = 0; t < BatchCtx::kSlots; ++t) {
+                if (bc.host[t]) cudaFreeHost(bc.host[t]);
+                if (bc.dev[t]) cudaFree(bc.dev[t]);
+                bc.host[t] = bc.dev[t] = nullptr;
+            }
+            bc.cap = buf.size() * 2;
+            for (int t = 0; t < BatchCtx::kSlots; ++t) {
+                ck(cudaHostAlloc(&bc.host[t], bc.cap, cudaHostAllocDefault), "cudaHostAlloc");
+                ck(cudaMalloc(&bc.dev[t], bc.cap), "cudaMalloc");
+                if (!bc.done[t]) ck(cudaEventCreateWithFlags(&bc.done[t], cudaEventDisableTiming), "event");
+            }
+        }
+        std::memcpy(bc.host[s], buf.data(), buf.size());
+        ck(cudaMemcpyAsync(bc.dev[s], bc.host[s], buf.size(), cudaMemcpyHostToDevice, st), "batch tables H2D");
+        uint8_t* dt = static_cast<uint8_t*>(bc.dev[s]);
+        // K4 batch scratch
+        const int rep = e0->rep, G = e0->Gs;
+        const int km = static_cast<int>(std::max<int64_t>(e0->cfg.n_lookup, 1));
+        if (bc.part_B < n) {
+            ck(cudaStreamSynchronize(st), "scratch growth");
+            bc.part.alloc(dec_part_floats(n, G, rep) * sizeof(float), st, false);
+            bc.mass.alloc(static_cast<size_t>(n) * e0->Hs * km * 2 * sizeof(float), st);
+            bc.cnt.alloc(static_cast<size_t>(n) * G * sizeof(unsigned), st);
+            bc.part_B = n;
+        }
+        int64_t ev_max = 0, sel_max = 0, lk_max = 0, tiles_max = 0;
+        for (auto& ep : c.evict) ev_max = std::max<int64_t>(ev_max, ep.n_init + ep.n_evict);
+        for (auto& sp : c.select) sel_max = std::max<int64_t>(sel_max, sp.n_units);
+        for (auto& lp : c.lookup) lk_max = std::max<int64_t>(lk_max, decode_batch_lookup_blocks(lp.U));
+        for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
+        launch_decode_batch_stage(0, dt + o_prep, n, G, st);
+        if (!c.evict.empty())
+            launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
+        if (!c.select.empty())
+            launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
+        if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
+        launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
+                              DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0}, st);
+        launch_decode_batch_stage(4, dt + o_lru, n, 0, st);
+        ck(cudaGetLastError(), "decode_batch launch");
+        ck(cudaEventRecord(bc.done[s], st), "record");
     });
 }
 

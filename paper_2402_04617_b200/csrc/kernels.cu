@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(1024) k_prefix(PrepParams p) {
 
 // ---- vectorised prep path (head_dim, value_dim multiples of 8) ----------------
 // (1) per-step rotation-factor table: one fp64 sincos per (token, pair)
-__global__ void k_rope_table(PrepParams p) {
+__device__ __forceinline__ void rope_table_body(const PrepParams& p) {
     const int pairs = p.d / 2;
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p.kmax2 && t < p.G) p.kmax2[t] = p.kmax2_prev[t];  // k_prep_tok raises it with this chunk's keys
@@ -155,6 +155,7 @@ __global__ void k_rope_table(PrepParams p) {
     rope_cs(p.freqs, a, p.s + i, c, s);
     p.rtab[t] = make_float2(c, s);
 }
+__global__ void k_rope_table(PrepParams p) { rope_table_body(p); }
 
 template <typename T>
 struct V8 {
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_fused(PrepParams p) {
 // group query sums go to qs[token][g][:] plus a per-tile column sum.
 constexpr int kTokTile = 16;
 template <typename T>
-__global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
+__device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
     __shared__ double sqs[kTokTile][128 + 2];
     __shared__ T svt[128][kTokTile + 2];
     const int g = blockIdx.y;
@@ -554,9 +555,14 @@ __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
     }
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
+    prep_tok_body<T>(p);
+}
+
 // (6) fp64 prefix into the P ring from the per-token sums and the tile sums:
 // block = (tile, group), thread = dim; rows of P written whole (coalesced).
-__global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
+__device__ __forceinline__ void prefix_tiles_body(const PrepParams& p) {
     const int tile = blockIdx.x, g = blockIdx.y, c = threadIdx.x;
     if (c >= p.d) return;
     const int64_t stride = static_cast<int64_t>(p.G) * p.d;
@@ -579,6 +585,7 @@ __global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
         p.chunk_qsum[g * p.d + c] = all;
     }
 }
+__global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) { prefix_tiles_body(p); }
 
 template <typename T>
 void launch_prep(const PrepParams& p, cudaStream_t st) {
@@ -716,10 +723,10 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
 // over units and keep all 32 row loads of a unit in flight before the math.
 // Single shard: per lane the groups are summed in order 0..G-1, then one warp
 // tree; sharded: one warp tree per group (partials exchanged by the caller).
-__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
+__device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nblocks) {
     const int lane = threadIdx.x % 32;
     const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * blockDim.x / 32;
+    const int64_t nwarps = static_cast<int64_t>(nblocks) * blockDim.x / 32;
     double q[8][4];
 #pragma unroll
     for (int g = 0; g < 8; ++g)
@@ -760,13 +767,14 @@ __global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
     __shared__ bool last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == static_cast<unsigned>(nblocks - 1);
     __syncthreads();
     if (!last) return;
     __threadfence();
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
     if (threadIdx.x == 0) *p.done = 0;
 }
+__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) { lookup_reg_body(p, gridDim.x); }
 
 // Large indices: the same math fed by cp.async (16-byte LDGSTS) into a
 // 3-deep per-warp shared-memory ring, so each warp keeps the next two units
@@ -1476,7 +1484,7 @@ void launch_mass(const MassParams& p, cudaStream_t st) {
 // residency peaks (303-308). All global reads are issued up front by 8
 // warps; the sequential logic then runs in warp 0 over shared memory.
 constexpr int kLruMax = 512;  // hot_capacity + k_m bound
-__global__ void __launch_bounds__(256) k_lru(LruParams p) {
+__device__ __forceinline__ void lru_body(const LruParams& p) {
     __shared__ int64_t ids[kLruMax];
     __shared__ double fr[kLruMax];
     __shared__ int64_t sel[kTopkMax];
@@ -1596,6 +1604,7 @@ __global__ void __launch_bounds__(256) k_lru(LruParams p) {
     }
 }
 
+__global__ void __launch_bounds__(256) k_lru(LruParams p) { lru_body(p); }
 void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 256, 0, st>>>(p); }
 
 // ---- host tier: GPU unit-cache slot assignment + PCIe page pull ----
@@ -1831,7 +1840,7 @@ __global__ void __launch_bounds__(256) k_evict(EvictParams p) {
 // k_finalize) or sums the groups in order 0..G-1 in-block and writes the
 // finalized score (finalize_front, repr_score.hpp:72-82).
 template <typename T>
-__global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
+__device__ __forceinline__ void evict_tok_body(const EvictParams& p) {
     __shared__ double part[32];
     const int g = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t idx = blockIdx.x;
@@ -1900,6 +1909,11 @@ __global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
         for (int gg = 0; gg < p.G; ++gg) tot += part[gg];
         p.unit_scores[u * p.l_bs + off] = static_cast<float>(tot / static_cast<double>(p.L));
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
+    evict_tok_body<T>(p);
 }
 
 template <typename T>
@@ -2009,7 +2023,7 @@ __device__ void select_page(const SelectParams& p, int64_t u, int g, const int* 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_select(SelectParams p) {
+__device__ __forceinline__ void select_body(const SelectParams& p) {
     __shared__ int idx[32];
     const int64_t u = p.u0 + blockIdx.x;
     const int len = p.unit_len[u];
@@ -2051,6 +2065,11 @@ __global__ void __launch_bounds__(256) k_select(SelectParams p) {
 }
 
 template <typename T>
+__global__ void __launch_bounds__(256) k_select(SelectParams p) {
+    select_body<T>(p);
+}
+
+template <typename T>
 void launch_select(const SelectParams& p, cudaStream_t st) {
     if (p.n_units <= 0) return;
     k_select<T><<<dim3(static_cast<unsigned>(p.n_units), p.page_mode ? p.G : 1), p.page_mode ? 256 : 128, 0, st>>>(p);
@@ -2077,4 +2096,77 @@ void launch_select_standalone(const float* scores, const int64_t* lens, int64_t 
                                                                                   r_k, idx);
 }
 
+}  // namespace infllm
+
+namespace infllm {
+// ---- batched decode: one launch per stage for B sequences (grid.z = sequence;
+// per-sequence parameter tables in device memory) -------------------------------
+__global__ void k_rope_table_b(const PrepParams* __restrict__ ps) { rope_table_body(ps[blockIdx.z]); }
+__global__ void __launch_bounds__(256) k_prep_tok_b(const PrepParams* __restrict__ ps) {
+    prep_tok_body<bf16>(ps[blockIdx.z]);
+}
+__global__ void __launch_bounds__(128) k_prefix_tiles_b(const PrepParams* __restrict__ ps) {
+    prefix_tiles_body(ps[blockIdx.z]);
+}
+__global__ void __launch_bounds__(256) k_evict_tok_b(const EvictParams* __restrict__ ps) {
+    const EvictParams& p = ps[blockIdx.z];
+    if (blockIdx.x >= p.n_init + p.n_evict) return;
+    evict_tok_body<bf16>(p);
+}
+__global__ void __launch_bounds__(256) k_select_b(const SelectParams* __restrict__ ps) {
+    const SelectParams& p = ps[blockIdx.z];
+    if (blockIdx.x >= p.n_units) return;
+    select_body<bf16>(p);
+}
+// relevance scan only (fused == 2 semantics: rel[u] written, no top-k)
+__device__ __forceinline__ int lookup_blocks(int64_t U) {
+    const int64_t want = (U + 7) / 8;
+    return static_cast<int>(want < 148 * 4 ? want : 148 * 4);
+}
+__global__ void __launch_bounds__(256, 2) k_lookup_reg_b(const LookupParams* __restrict__ ps) {
+    const LookupParams& p = ps[blockIdx.z];
+    const int nb = lookup_blocks(p.U);
+    if (static_cast<int>(blockIdx.x) >= nb) return;
+    lookup_reg_body(p, nb);
+}
+__global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
+    const LookupParams& p = ps[blockIdx.x];
+    block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+}
+__global__ void __launch_bounds__(256) k_lru_b(const LruParams* __restrict__ ps) { lru_body(ps[blockIdx.x]); }
+
+void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st) {
+    switch (stage) {
+        case 0: {  // K7 prep of one token per sequence (the chunk-path kernels, l_x = 1)
+            const PrepParams* ps = static_cast<const PrepParams*>(tab);
+            k_rope_table_b<<<dim3(1, 1, B), 256, 0, st>>>(ps);
+            k_prep_tok_b<<<dim3(1, static_cast<unsigned>(gx), B), 256, 0, st>>>(ps);
+            k_prefix_tiles_b<<<dim3(1, static_cast<unsigned>(gx), B), 128, 0, st>>>(ps);
+            break;
+        }
+        case 1:  // eviction of the token(s) leaving the local window (gx = max tokens; block = 32 x G)
+            k_evict_tok_b<<<dim3(static_cast<unsigned>(gx & 0xffffffff), 1, B), static_cast<unsigned>(32 * (gx >> 32)), 0, st>>>(
+                static_cast<const EvictParams*>(tab));
+            break;
+        case 2:  // completed units: representative selection + page copy (gx = max units; grid.y = G)
+            k_select_b<<<dim3(static_cast<unsigned>(gx & 0xffffffff), static_cast<unsigned>(gx >> 32), B), 256, 0, st>>>(
+                static_cast<const SelectParams*>(tab));
+            break;
+        case 3: {  // relevance scan + exact top-k (rel desc, id asc)
+            const LookupParams* ps = static_cast<const LookupParams*>(tab);
+            k_lookup_reg_b<<<dim3(static_cast<unsigned>(gx), 1, B), 256, 0, st>>>(ps);
+            k_topk_b<<<B, 1024, 0, st>>>(ps);
+            break;
+        }
+        case 4:  // LRU / tier bookkeeping
+            k_lru_b<<<B, 256, 0, st>>>(static_cast<const LruParams*>(tab));
+            break;
+        default:
+            break;
+    }
+}
+int64_t decode_batch_lookup_blocks(int64_t U) {
+    const int64_t want = (U + 7) / 8;
+    return want < 148 * 4 ? want : 148 * 4;
+}
 }  // namespace infllm

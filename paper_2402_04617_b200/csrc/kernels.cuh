@@ -249,6 +249,13 @@ template <typename T> void launch_evict(const EvictParams& p, cudaStream_t st);
 void launch_finalize(const FinalizeParams& p, cudaStream_t st);
 template <typename T> void launch_select(const SelectParams& p, cudaStream_t st);
 
+// batched decode stages (grid.z / grid.x = sequence; tab = device array of B params):
+// 0 prep (PrepParams), 1 evict (EvictParams, gx = max tokens | G << 32), 2 select
+// (SelectParams, gx = max units | G << 32), 3 lookup + top-k (LookupParams,
+// gx = max scan blocks), 4 LRU (LruParams)
+void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st);
+int64_t decode_batch_lookup_blocks(int64_t U);
+
 // standalone select (C ABI infllm_select_representatives)
 void launch_select_standalone(const float* scores, const int64_t* lens, int64_t n_units, int64_t unit_len,
                               int64_t r_k, int64_t* idx, cudaStream_t st);

@@ -204,6 +204,22 @@ class StreamEngine:
         return dict(attn_ms=a.value, attn_launches=na.value, lookup_ms=b.value, lookup_launches=nb.value)
 
 
+def decode_batch(engines, q, k, v, out=None, layer=0, stream=None):
+    """One decode step of len(engines) independent sequences (infllm_decode_batch):
+    q [B][H][d], k/v [B][H_kv][d] device tensors; returns out [B][H][d_v]."""
+    e0 = engines[0]
+    for t in (q, k, v):
+        if t.device != e0.device or t.dtype != e0.dtype or not t.is_contiguous() or t.shape[0] != len(engines):
+            raise ValueError("q/k/v must be contiguous [B][heads][dim] tensors of the engines' dtype/device")
+    if out is None:
+        out = torch.empty((len(engines), e0.n_heads_local, e0.shape.value_dim), dtype=e0.dtype, device=e0.device)
+    hs = (C.c_void_p * len(engines))(*[e.h.value for e in engines])
+    st = (stream or torch.cuda.current_stream(e0.device)).cuda_stream
+    check(lib().infllm_decode_batch(hs, len(engines), layer, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                    st))
+    return out
+
+
 def select_representatives(scores: torch.Tensor, r_k: int, lens: torch.Tensor | None = None) -> torch.Tensor:
     """select_representatives (repr_score.hpp:94-112), batched over units on the GPU.
     scores [n_units][unit_len] fp32 CUDA -> idx [n_units][r_k] int64 (-1 = unused)."""

@@ -76,3 +76,80 @@ def test_decode_from_empty_stream():
     q, k, v = gaussian_inputs(53, n, 8, 2, 128, scale=0.3, bf16=True)
     oeng, geng, recs = run_pair(cfg, 8, 2, 128, q, k, v, [1] * n, decode_tail=n, dtype=torch.bfloat16)
     _check(oeng, geng, recs)
+
+
+def _prefilled(cfg, n_pre, seeds, H=8, Hkv=2):
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    engs, data = [], []
+    for sd in seeds:
+        q, k, v = gaussian_inputs(sd, n_pre + 400, H, Hkv, 128, scale=0.3, bf16=True)
+        e = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=H, n_kv_heads=Hkv, head_dim=128),
+                         dtype=torch.bfloat16)
+        qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+        if n_pre:
+            e.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
+        engs.append(e)
+        data.append((qt, kt, vt))
+    return engs, data
+
+
+@pytest.mark.parametrize("n_pre", [0, 3000])
+def test_decode_batch_matches_per_sequence(n_pre):
+    """decode_batch over 5 sequences (different contents, so different retrieved
+    units; n_pre = 0: sequences start empty and pass through init pinning and
+    their first units while batched) == decode_step per sequence: ids, counters,
+    trace exact, outputs within bf16 rounding of the split-KV merge order."""
+    from paper_2402_04617_b200 import decode_batch
+
+    seeds = [61, 62, 63, 64, 65]
+    steps = 300 if n_pre else 400
+    a, da = _prefilled(CFG, n_pre, seeds)
+    b, db = _prefilled(CFG, n_pre, seeds)
+    worst = 0.0
+    for t in range(n_pre, n_pre + steps):
+        q = torch.stack([d[0][t] for d in db])
+        k = torch.stack([d[1][t] for d in db])
+        v = torch.stack([d[2][t] for d in db])
+        got = decode_batch(b, q, k, v)
+        for i, e in enumerate(a):
+            ref = e.decode_step(da[i][0][t:t + 1], da[i][1][t:t + 1], da[i][2][t:t + 1])
+            assert e.retrieved_ids() == b[i].retrieved_ids(), (t, i)
+            worst = max(worst, rel_err(got[i].float().cpu().numpy(), ref[0].float().cpu().numpy()))
+    assert worst < 2e-2, worst
+    for ea, eb in zip(a, b):
+        assert ea.metrics() == eb.metrics()
+        assert ea.trace() == eb.trace()
+        m = ea.metrics()
+        for u in range(m["units"]):
+            assert ea.unit_info(u) == eb.unit_info(u)
+
+
+def test_decode_batch_vs_oracle():
+    """One batched sequence set against the CPU oracle directly."""
+    from paper_2402_04617_b200 import decode_batch
+
+    n_pre, steps, seeds = 2048, 160, [71, 72]
+    engs, data = _prefilled(CFG, n_pre, seeds)
+    oengs = []
+    for sd in seeds:
+        q, k, v = gaussian_inputs(sd, n_pre + 400, 8, 2, 128, scale=0.3, bf16=True)
+        oe = O.OracleEngine(O.EngineConfig.make(**CFG), O.ModelShape.make(n_heads=8, n_kv_heads=2, head_dim=128),
+                            n_threads=8)
+        for off in range(0, n_pre, 256):
+            oe.step(q[off:off + 256], k[off:off + 256], v[off:off + 256])
+        oengs.append((oe, q, k, v))
+    worst = 0.0
+    for t in range(n_pre, n_pre + steps):
+        q = torch.stack([d[0][t] for d in data])
+        k = torch.stack([d[1][t] for d in data])
+        v = torch.stack([d[2][t] for d in data])
+        got = decode_batch(engs, q, k, v).float().cpu().numpy()
+        for i, (oe, oq, ok, ov) in enumerate(oengs):
+            r = oe.step(oq[t:t + 1], ok[t:t + 1], ov[t:t + 1], decode=True)
+            assert r.retrieved_ids == engs[i].retrieved_ids()
+            worst = max(worst, rel_err(got[i:i + 1], r.out))
+    assert worst < 2e-2, worst
+    for i, (oe, *_) in enumerate(oengs):
+        diffs, repr_bad = compare_state(oe, engs[i])
+        assert not diffs and not repr_bad
