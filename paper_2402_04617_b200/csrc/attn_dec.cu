@@ -40,7 +40,8 @@ struct DecTile {
 };
 
 // window tile t (window order, engine.hpp:187-221)
-__device__ __forceinline__ DecTile dec_tile(const AttnParams& a, int t, int n_init, int64_t near0) {
+__device__ __forceinline__ DecTile dec_tile(const AttnParams& a, int t, int n_init, int64_t near0,
+                                            const int32_t* s_page, const int32_t* s_len) {
     DecTile r;
     if (t < n_init) {
         r.src = 0;
@@ -50,12 +51,11 @@ __device__ __forceinline__ DecTile dec_tile(const AttnParams& a, int t, int n_in
         r.hi = static_cast<int>(min(static_cast<int64_t>(128), a.init_len - r.key0));
     } else if (t < n_init + a.n_sel) {
         const int u = t - n_init;
-        const int64_t id = a.sel[u];
         r.src = 1;
         r.key0 = 0;
-        r.page = a.sel_slot ? a.sel_slot[u] : id;
+        r.page = s_page[u];  // unit page (or host-tier cache slot), staged in shared memory
         r.lo = 0;
-        r.hi = a.unit_len[id];
+        r.hi = s_len[u];
     } else {
         const int64_t P = near0 + 128 * static_cast<int64_t>(t - n_init - a.n_sel);
         r.src = 2;
@@ -81,7 +81,7 @@ __device__ __forceinline__ int dec_tiles(const AttnParams& a, int& n_init, int64
 constexpr int kRowB = 272;
 constexpr int kMatB = 128 * kRowB;  // 34816
 constexpr int kStageB = 2 * kMatB;
-constexpr int kStages = 2;
+constexpr int kStages = 3;
 constexpr int kDecSmem = kStages * kStageB;
 
 __device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
@@ -138,9 +138,16 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     __shared__ float sred[kW][kDecMaxRep], sl_red[kW][kDecMaxRep];
     __shared__ float s_m[kDecMaxRep], s_alpha[kDecMaxRep], s_M[kDecMaxRep], s_L[kDecMaxRep];
     __shared__ bool s_last;
+    __shared__ int32_t s_page[kDecMaxSel], s_len[kDecMaxSel];
 
     const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
     const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (query head) / column pair
+    for (int u = tid; u < a.n_sel; u += kThr) {  // the retrieved units' pages and lengths
+        const int64_t id = a.sel[u];
+        s_page[u] = a.sel_slot ? a.sel_slot[u] : static_cast<int32_t>(id);
+        s_len[u] = a.unit_len[id];
+    }
+    __syncthreads();
     const int g = blockIdx.y, rep = a.rep;
     const float sl2 = a.scale * kLog2e;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
@@ -152,7 +159,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
 
     for (int st = 0; st < kStages; ++st) {  // prefetch the first tiles
-        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0), g, sbase + st * kStageB);
+        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, sbase + st * kStageB);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // query fragments (A operand, row = query head of the group, zero beyond rep):
@@ -180,7 +187,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
 
     for (int t = t0; t < t1; ++t) {
         const int st = (t - t0) % kStages;
-        const DecTile tl = dec_tile(a, t, n_init, near0);
+        const DecTile tl = dec_tile(a, t, n_init, near0, s_page, s_len);
         asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
         __syncthreads();
         const uint32_t sk = sbase + st * kStageB, sv = sk + kMatB;
@@ -264,7 +271,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             mr[0] = e;
             mr[1] = s_m[tid];
         }
-        if (t + kStages < t1) dec_load(a, dec_tile(a, t + kStages, n_init, near0), g, sbase + st * kStageB);
+        if (t + kStages < t1) dec_load(a, dec_tile(a, t + kStages, n_init, near0, s_page, s_len), g, sbase + st * kStageB);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -378,11 +385,20 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch 
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restrict__ ps, DecScratch sc) {
-    dec_body(ps[blockIdx.z], sc, blockIdx.z, blockIdx.x, gridDim.x);
+    // this sequence's parameters in shared memory (read all through the tile loop)
+    __shared__ __align__(16) AttnParams sa;
+    static_assert(sizeof(AttnParams) % 4 == 0, "word copy");
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(AttnParams) / 4); i += kThr)
+        reinterpret_cast<uint32_t*>(&sa)[i] = reinterpret_cast<const uint32_t*>(ps + blockIdx.z)[i];
+    __syncthreads();
+    dec_body(sa, sc, blockIdx.z, blockIdx.x, gridDim.x);
 }
 
 int pick_splits(int64_t max_tiles, int G, int B) {
-    const int64_t want = (148 + static_cast<int64_t>(G) * B - 1) / (static_cast<int64_t>(G) * B);
+    // one sequence: ~one CTA per SM (short splits keep the latency down); a batch:
+    // ~3 CTAs per SM over the whole launch (load balance across waves)
+    const int64_t target = B == 1 ? 148 : 148 * 3;
+    const int64_t want = (target + static_cast<int64_t>(G) * B - 1) / (static_cast<int64_t>(G) * B);
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, max_tiles, kDecMaxSplits})));
 }
 

@@ -7,6 +7,7 @@ namespace infllm {
 
 constexpr int kDecMaxRep = 8;      // query heads per KV group
 constexpr int kDecMaxSplits = 64;  // KV splits per (sequence, group)
+constexpr int kDecMaxSel = 128;    // retrieved units (n_lookup)
 
 // scratch of one launch: split partials (m, l, O[128]) per head, per-unit
 // (mass, running max) records, and per-(sequence, group) arrival counters

@@ -1588,7 +1588,13 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         int64_t ev_max = 0, sel_max = 0, lk_max = 0, tiles_max = 0;
         for (auto& ep : c.evict) ev_max = std::max<int64_t>(ev_max, ep.n_init + ep.n_evict);
         for (auto& sp : c.select) sel_max = std::max<int64_t>(sel_max, sp.n_units);
-        for (auto& lp : c.lookup) lk_max = std::max<int64_t>(lk_max, decode_batch_lookup_blocks(lp.U));
+        int64_t lk_reg = 0, lk_str = 0;
+        for (auto& lp : c.lookup) {
+            const int64_t bl = decode_batch_lookup_blocks(lp.U);
+            lk_reg = std::max<int64_t>(lk_reg, bl & 0xffffffff);
+            lk_str = std::max<int64_t>(lk_str, bl >> 32);
+        }
+        lk_max = lk_reg | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
         launch_decode_batch_stage(0, dt + o_prep, n, G, st);
         if (!c.evict.empty())

@@ -785,12 +785,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                  "l"(gmem)
                  : "memory");
 }
-__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
+__device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nblocks) {
     extern __shared__ __align__(16) uint8_t scan_smem[];
     const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
     uint8_t* ring = scan_smem + static_cast<size_t>(wib) * kScanStages * 8192;
     // contiguous slice per block (its candidates then come out in unit order)
-    const int64_t S = (p.U + gridDim.x - 1) / gridDim.x;
+    const int64_t S = (p.U + nblocks - 1) / nblocks;
     const int64_t s0 = static_cast<int64_t>(blockIdx.x) * S, s1 = s0 + S < p.U ? s0 + S : p.U;
     const int64_t warp0 = s0 + wib;
     const int64_t nwarps = blockDim.x / 32;
@@ -1128,6 +1128,7 @@ __global__ void __launch_bounds__(256) k_topk_local(const double* rel, int64_t U
         cand_i[blockIdx.x * k + r] = ok ? s0 + loc[r] : -1;
     }
 }
+__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) { lookup_stream_body(p, gridDim.x); }
 __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const int64_t* cand_i, int64_t n, int64_t k,
                                                      int64_t* sel) {
     __shared__ int64_t loc[kTopkMaxSel];
@@ -2129,6 +2130,14 @@ __global__ void __launch_bounds__(256, 2) k_lookup_reg_b(const LookupParams* __r
     if (static_cast<int>(blockIdx.x) >= nb) return;
     lookup_reg_body(p, nb);
 }
+// streaming variant: 8 warps x 8 units per block, cp.async ring per warp
+__device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 63) / 64); }
+__global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* __restrict__ ps) {
+    const LookupParams& p = ps[blockIdx.z];
+    const int nb = stream_blocks(p.U);
+    if (static_cast<int>(blockIdx.x) >= nb) return;
+    lookup_stream_body(p, nb);
+}
 __global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
     const LookupParams& p = ps[blockIdx.x];
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
@@ -2154,7 +2163,18 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             break;
         case 3: {  // relevance scan + exact top-k (rel desc, id asc)
             const LookupParams* ps = static_cast<const LookupParams*>(tab);
-            k_lookup_reg_b<<<dim3(static_cast<unsigned>(gx), 1, B), 256, 0, st>>>(ps);
+            static const bool use_reg = getenv("INFLLM_BATCH_LOOKUP_REG") != nullptr;  // A/B experiments only
+            if (use_reg) {
+                k_lookup_reg_b<<<dim3(static_cast<unsigned>(gx & 0xffffffff), 1, B), 256, 0, st>>>(ps);
+            } else {
+                const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
+                static bool attr = false;
+                if (!attr) {
+                    cudaFuncSetAttribute(k_lookup_stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                    attr = true;
+                }
+                k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
+            }
             k_topk_b<<<B, 1024, 0, st>>>(ps);
             break;
         }
@@ -2165,8 +2185,8 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             break;
     }
 }
-int64_t decode_batch_lookup_blocks(int64_t U) {
+int64_t decode_batch_lookup_blocks(int64_t U) {  // reg-scan blocks | stream-scan blocks << 32
     const int64_t want = (U + 7) / 8;
-    return want < 148 * 4 ? want : 148 * 4;
+    return (want < 148 * 4 ? want : 148 * 4) | (((U + 63) / 64) << 32);
 }
 }  // namespace infllm
