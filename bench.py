@@ -284,6 +284,7 @@ def run_b200(args, rank, world, local_rank):
     lk_bytes = lookup_bytes(steps, CFG, Hkv, d, H)
     lk_ms = prof["lookup_ms"] / max(1, args.steps)
     iso = isolated_kernels(eng, steps, H, Hkv, d, dev) if rank == 0 else {}
+    extra = other_configs(Q, K, V, dev) if (rank == 0 and not args.no_extra) else {}
 
     if rank == 0:
         cpu = None
@@ -320,6 +321,7 @@ def run_b200(args, rank, world, local_rank):
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "other_configs": extra,
         }
         print(json.dumps(line), flush=True)
 
@@ -382,6 +384,96 @@ def isolated_kernels(eng, steps, H, Hkv, d, dev):
     return out
 
 
+def other_configs(Q, K, V, dev, batch=32, dec_steps=24):
+    """The other BASELINE.json configs, measured on the same box after the
+    headline (not part of `value`):
+    C4 decode: `batch` independent sequences prefilled to 128K tokens, then one
+    infllm_decode_batch call per step (every stage one launch for the batch),
+    device time per step over `dec_steps` steps (CUDA events); also the
+    single-sequence decode_step latency.
+    C3: the 1M-token planted stream with the host-offloaded unit store
+    (pinned-host pages + 48-slot GPU unit cache): prefill tokens/s, probe
+    recall, page loads / cache hit rate, H2D GB/s (tools/c3_planted.py)."""
+    import torch
+
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, decode_batch
+
+    out = {}
+    H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
+    n = Q.shape[0]
+    try:
+        g = torch.Generator(device=dev)
+        g.manual_seed(77)
+        tot = dec_steps + 4
+        qd = torch.randn((tot, batch, H, d), generator=g, device=dev).bfloat16()
+        kd = torch.randn((tot, batch, Hkv, d), generator=g, device=dev).bfloat16()
+        vd = torch.randn((tot, batch, Hkv, d), generator=g, device=dev).bfloat16()
+        res = torch.empty((batch, H, d), device=dev, dtype=torch.bfloat16)
+        engs = []
+        for _ in range(batch):
+            e = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16)
+            e.reserve(n + tot + 1)
+            e.encode_stream(Q, K, V)
+            engs.append(e)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for t in range(4):
+            decode_batch(engs, qd[t], kd[t], vd[t], out=res)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for t in range(4, tot):
+            decode_batch(engs, qd[t], kd[t], vd[t], out=res)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        step_ms = e0.elapsed_time(e1) / dec_steps
+        units = engs[0].metrics()["units"]
+        kv_b = batch * (CFG["init_size"] + CFG["n_lookup"] * CFG["unit_size"] + CFG["local_size"] + 1) * Hkv * d * 4
+        ix_b = batch * units * CFG["n_repr"] * Hkv * d * 2
+        # one sequence, decode_step (caller's stream, split-KV attention)
+        one = engs[0]
+        q1 = qd[:, 0:1].contiguous()
+        k1 = kd[:, 0:1].contiguous()
+        v1 = vd[:, 0:1].contiguous()
+        one.reset()
+        one.encode_stream(Q, K, V)
+        for t in range(4):
+            one.decode_step(q1[t], k1[t], v1[t])
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for t in range(4, tot):
+            one.decode_step(q1[t], k1[t], v1[t])
+        e1.record()
+        torch.cuda.synchronize(dev)
+        one_ms = e0.elapsed_time(e1) / dec_steps
+        out["c4_decode"] = {
+            "workload": f"C4: {batch} sequences x 128K context, Llama-3-8B heads, one decode token per sequence per "
+                        f"step (infllm_decode_batch)", "batch": batch, "context": n, "steps": dec_steps,
+            "step_ms": step_ms, "tokens_per_s": batch / (step_ms / 1e3),
+            "hbm_bytes_per_step": kv_b + ix_b, "hbm_gbs": (kv_b + ix_b) / (step_ms / 1e3) / 1e9,
+            "single_sequence_step_ms": one_ms,
+            "timing": "CUDA events around dec_steps consecutive batched steps (device time incl. host gaps)"}
+        for e in engs:
+            e.close()
+        del engs
+    except Exception as ex:  # reported, not fatal
+        out["c4_decode"] = {"error": str(ex)}
+    torch.cuda.empty_cache()
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import c3_planted
+
+        ok, tps, ts = c3_planted.run(1 << 20, verbose=False, slots=48)
+        req = ts["loads"] + ts["cache_hits"]
+        out["c3_host_tier"] = {
+            "workload": "C3: 1M-token planted stream, unit pages in pinned host memory, 48-slot GPU unit cache "
+                        "(host_tier_slots)", "tokens_per_s": tps, "probe_recall": 1.0 if ok else 0.0,
+            "page_loads": ts["loads"], "cache_hit_rate": ts["cache_hits"] / max(req, 1),
+            "h2d_gb": ts["h2d_bytes"] / 1e9, "h2d_gbs": ts["h2d_bytes"] / ((1 << 20) / tps) / 1e9}
+    except Exception as ex:
+        out["c3_host_tier"] = {"error": str(ex)}
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_e2e(eng, Q, K, V, n, C, dev, args, world):
     """Same metric through the C-ABI with HOST buffers: infllm_encode_stream_host
     copies each chunk's q/k/v from pinned memory and each output chunk back
@@ -427,6 +519,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tc", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 host-tier and C4 decode figures")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
