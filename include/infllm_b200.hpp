@@ -19,6 +19,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <array>
 #include <vector>
 
 #include "infllm_b200.h"
@@ -171,10 +172,29 @@ public:
         return out;
     }
 
+    /// Engine options (infllm_engine_set_option): "host_tier_slots", "decode_kernel", ...
+    void set_option(const char* key, int64_t value) { check(infllm_engine_set_option(h_, key, value)); }
+    /// Host tier counters: page loads, cache hits, H2D bytes, slots (infllm_tier_stats).
+    std::array<int64_t, 4> tier_stats(int layer = 0) const {
+        std::array<int64_t, 4> s{};
+        check(infllm_tier_stats(h_, layer, s.data()));
+        return s;
+    }
+
 private:
     EngineConfig config_;
     ModelShape shape_;
     infllm_engine_t h_ = nullptr;
 };
+
+/// One decode step of engines.size() independent sequences (infllm_decode_batch):
+/// q [B][H][d], k/v [B][H_kv][d], out [B][H][d_v] device pointers.
+inline void decode_batch(const std::vector<StreamEngine*>& engines, int layer, const void* q, const void* k,
+                         const void* v, void* out, void* stream = nullptr) {
+    std::vector<infllm_engine_t> hs;
+    hs.reserve(engines.size());
+    for (auto* e : engines) hs.push_back(e->handle());
+    check(infllm_decode_batch(hs.data(), static_cast<int32_t>(hs.size()), layer, q, k, v, out, stream));
+}
 
 }  // namespace infllm
