@@ -7,6 +7,7 @@
 // pinning, unit packing boundaries), so a step is a fixed kernel sequence on
 // the caller's stream with no host synchronisation.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -150,6 +151,55 @@ struct HBuf {
     }
 };
 
+// Green context (driver API through cudaGetDriverEntryPoint: no -lcuda) that
+// owns `n_sms` SMs: the engine's side streams are created in it, so the
+// prep / lookup / eviction / LRU kernels of the next steps run on that
+// partition only and never hold SMs the attention CTAs (one per SM, 128 of
+// them at C2) are waiting for; the attention stays on the whole device.
+template <typename F>
+F drv(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+        throw CudaError(std::string("driver entry point ") + name + " unavailable");
+    return reinterpret_cast<F>(p);
+}
+struct SidePartition {
+    CUgreenCtx ctx = nullptr;
+    int sms = 0;
+};
+SidePartition make_side_partition(int device, int n_sms) {
+    using GetDev = CUresult (*)(CUdevice*, int);
+    using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+    using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+    using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+    using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+    CUdevice dev;
+    if (drv<GetDev>("cuDeviceGet")(&dev, device) != CUDA_SUCCESS) throw CudaError("cuDeviceGet");
+    CUdevResource all, part, rem;
+    if (drv<GetRes>("cuDeviceGetDevResource")(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+        throw CudaError("cuDeviceGetDevResource");
+    unsigned n = 1;
+    if (drv<Split>("cuDevSmResourceSplitByCount")(&part, &n, &all, &rem, 0, static_cast<unsigned>(n_sms)) !=
+            CUDA_SUCCESS || n != 1)
+        throw CudaError("cuDevSmResourceSplitByCount");
+    CUdevResourceDesc desc;
+    if (drv<GenDesc>("cuDevResourceGenerateDesc")(&desc, &part, 1) != CUDA_SUCCESS)
+        throw CudaError("cuDevResourceGenerateDesc");
+    SidePartition sp;
+    if (drv<Create>("cuGreenCtxCreate")(&sp.ctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+        throw CudaError("cuGreenCtxCreate");
+    sp.sms = static_cast<int>(part.sm.smCount);
+    return sp;
+}
+cudaStream_t side_partition_stream(const SidePartition& sp) {
+    using SCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+    CUstream st;
+    if (drv<SCreate>("cuGreenCtxStreamCreate")(&st, sp.ctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+        throw CudaError("cuGreenCtxStreamCreate");
+    return reinterpret_cast<cudaStream_t>(st);
+}
+
 __global__ void k_empty() {}
 // throughput probes: 8 independent FMA chains x n iterations per thread
 __global__ void k_probe_f64(double* out, int n) {
@@ -243,6 +293,7 @@ struct infllm_engine {
     cudaStream_t tier_stream = nullptr;
     cudaEvent_t e_tier = nullptr, e_tierdone = nullptr;
     int64_t tier_seq = -1;  // step that last queued work on the tier stream
+    SidePartition side_part{};  // option side_sms: side streams confined to a green context
     int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
@@ -1335,6 +1386,13 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
         ck(cudaStreamSynchronize(st), "engine_create");
+        if (const char* ss = std::getenv("INFLLM_SIDE_SMS")) {  // default for the side-stream partition
+            const int64_t v = std::atoll(ss);
+            if (v > 0) {
+                infllm_engine* raw = e.get();
+                if (infllm_engine_set_option(raw, "side_sms", v) != INFLLM_OK) throw CudaError(g_err);
+            }
+        }
         *out = e.release();
     });
 }
@@ -1462,6 +1520,27 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->dec_disabled = value == 0;
         else if (k == "multi_stream_decode")
             e->multi_stream_decode = value != 0;
+        else if (k == "side_sms") {  // 0: side streams on the whole device; n: on an n-SM partition
+            ck(cudaDeviceSynchronize(), "side_sms");
+            for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream}) {
+                if (*s2) cudaStreamDestroy(*s2);
+                *s2 = nullptr;
+            }
+            if (value > 0) {
+                if (!e->side_part.ctx) e->side_part = make_side_partition(e->device, static_cast<int>(value));
+                for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream})
+                    *s2 = side_partition_stream(e->side_part);
+            } else {
+                for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream})
+                    ck(cudaStreamCreateWithFlags(s2, cudaStreamNonBlocking), "stream");
+            }
+            for (auto& g : e->graphs)  // captured graphs name the old streams' work: recapture
+                if (g.exec) cudaGraphExecDestroy(g.exec);
+            e->graphs.clear();
+            e->lru_seq[0] = e->lru_seq[1] = -1;
+            for (auto& a2 : e->attn_seq) a2 = -1;
+            e->lookup_seq = e->evict_seq = e->tier_seq = -1;
+        }
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
                 if (L.unit_cap > 0 && value != e->tier_slots)

@@ -29,6 +29,18 @@ __global__ void k(int iters, float* out, unsigned long long* cyc) {
                     asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(v[i]), "f"(v[i - 1]));
                     v[i - 1] = __uint_as_float(pk << 16) - 1.0f;
                 }
+            } else if (KIND == 4) {  // ex2.approx.f16x2: two exponentials per instruction (elements counted)
+                if (i & 1) {
+                    uint32_t x = __float_as_uint(v[i]), y;
+                    asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+                    v[i] = __uint_as_float(y);
+                }
+            } else if (KIND == 5) {  // ex2.approx.ftz.bf16x2
+                if (i & 1) {
+                    uint32_t x = __float_as_uint(v[i]), y;
+                    asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+                    v[i] = __uint_as_float(y);
+                }
             } else {  // bf16x2 pack (cvt.rn.bf16x2.f32) feeding back into the chain
                 uint32_t pk;
                 asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(v[i]), "f"(v[(i + 1) & 7]));
@@ -50,7 +62,7 @@ int main() {
     cudaMalloc(&o, 1 << 24);
     cudaMalloc(&c, 8);
     for (int threads : {128, 256, 512, 1024}) {
-        for (int kind : {0, 3}) {
+        for (int kind : {0, 3, 4, 5}) {
             const int iters = 4096;
             if (kind == 0)
                 k<0><<<148, threads>>>(iters, o, c);
@@ -58,12 +70,16 @@ int main() {
                 k<1><<<148, threads>>>(iters, o, c);
             else if (kind == 2)
                 k<2><<<148, threads>>>(iters, o, c);
-            else
+            else if (kind == 3)
                 k<3><<<148, threads>>>(iters, o, c);
+            else if (kind == 4)
+                k<4><<<148, threads>>>(iters, o, c);
+            else
+                k<5><<<148, threads>>>(iters, o, c);
             cudaDeviceSynchronize();
             unsigned long long cy;
             cudaMemcpy(&cy, c, 8, cudaMemcpyDeviceToHost);
-            printf("%s threads=%d: %.2f ops/clk/SM\n", kind == 0 ? "ex2" : kind == 1 ? "ffma" : kind == 2 ? "cvt.bf16x2(+fadd,and)" : "ex2 + pack per pair (elements)", threads,
+            printf("%s threads=%d: %.2f ops/clk/SM\n", kind == 0 ? "ex2" : kind == 1 ? "ffma" : kind == 2 ? "cvt.bf16x2(+fadd,and)" : kind == 3 ? "ex2 + pack per pair (elements)" : kind == 4 ? "ex2.f16x2 (elements)" : "ex2.bf16x2 (elements)", threads,
                    (double)threads * iters * 8 / cy);
         }
     }
