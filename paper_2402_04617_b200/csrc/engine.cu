@@ -596,7 +596,10 @@ struct infllm_engine {
         one_stream = lx == 1 && !capturing && !multi_stream_decode;
         cudaStream_t main = st, side = one_stream ? st : side_stream, pst = one_stream ? st : prep_stream,
                      est = one_stream ? st : evict_stream;
-        cudaStream_t lru_st = one_stream ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
+        // decode steps keep the LRU bookkeeping on its own stream (off the critical
+        // path: no later prep / lookup / attention reads it), with real events
+        const bool lru_side = one_stream && !coll && !(debug_skip & 64);
+        cudaStream_t lru_st = (one_stream && !lru_side) ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
         if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
         pipe_dirty = !one_stream;
         if (fork) {
@@ -605,8 +608,12 @@ struct infllm_engine {
             wt(pst, e_call);
         }
         if (inputs_ready) wt(pst, inputs_ready);
-        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
-            wt(side, e_lru[b]);  // sel of this parity: attention + LRU k-2
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0)) {
+            if (lru_side)
+                ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // side == caller's stream
+            else
+                wt(side, e_lru[b]);  // sel of this parity: attention + LRU k-2
+        }
         // qa/qc/chunk sums of this buffer were last read by attention k-3 (and its lookup)
         if (attn_seq[pb] >= 0 && (capture_seq0 < 0 || attn_seq[pb] >= capture_seq0))
             wt(pst, e_attnp[pb]);
@@ -1005,6 +1012,10 @@ struct infllm_engine {
         rec(e_attnp[pb], main);
         attn_seq[pb] = kseq;
         wt(lru_st, e_attn);
+        if (lru_side) {
+            ck(cudaEventRecord(e_attn, main), "record");
+            ck(cudaStreamWaitEvent(lru_st, e_attn, 0), "wait");
+        }
         last_lp = lp;
         if (coll)
             coll->lru.push_back(lp);
@@ -1012,11 +1023,12 @@ struct infllm_engine {
             launch_lru(lp, lru_st);
         ++launches;
         rec(e_lru[b], lru_st);
+        if (lru_side) ck(cudaEventRecord(e_lru[b], lru_st), "record");
         lru_seq[b] = kseq;
         st = side;
 
-        if (one_stream) {  // nothing was recorded: no later step may wait on this step's events
-            lru_seq[0] = lru_seq[1] = -1;
+        if (one_stream) {  // nothing else was recorded: no later step may wait on those events
+            if (!lru_side) lru_seq[0] = lru_seq[1] = -1;
             for (auto& a2 : attn_seq) a2 = -1;
             lookup_seq = evict_seq = tier_seq = -1;
         }
