@@ -17,6 +17,7 @@
 #include "attn_dec.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 namespace infllm {
@@ -395,11 +396,24 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restr
 }
 
 int pick_splits(int64_t max_tiles, int G, int B) {
-    // one sequence: ~one CTA per SM (short splits keep the latency down); a batch:
-    // ~3 CTAs per SM over the whole launch (load balance across waves)
-    const int64_t target = B == 1 ? 148 : 148 * 3;
-    const int64_t want = (target + static_cast<int64_t>(G) * B - 1) / (static_cast<int64_t>(G) * B);
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, max_tiles, kDecMaxSplits})));
+    const int64_t items = static_cast<int64_t>(G) * B;
+    if (items < 148) {  // few sequences: ~one CTA per SM, short splits keep the latency down
+        const int64_t want = (148 + items - 1) / items;
+        return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, max_tiles, kDecMaxSplits})));
+    }
+    // a batch (1 CTA per SM): the split count whose CTA total fills its last wave
+    // best (the per-CTA prologue and the merge favour fewer splits on ties)
+    int best = 1;
+    double best_eff = 0.0;
+    for (int sp = 1; sp <= 8 && sp * 4 <= max_tiles; ++sp) {
+        const double waves = static_cast<double>(items * sp) / 148.0;
+        const double eff = waves / std::ceil(waves);
+        if (eff > best_eff + 1e-3) {
+            best_eff = eff;
+            best = sp;
+        }
+    }
+    return best;
 }
 
 }  // namespace

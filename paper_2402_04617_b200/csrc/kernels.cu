@@ -2131,7 +2131,7 @@ __global__ void __launch_bounds__(256, 2) k_lookup_reg_b(const LookupParams* __r
     lookup_reg_body(p, nb);
 }
 // streaming variant: 8 warps x 8 units per block, cp.async ring per warp
-__device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 63) / 64); }
+__device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 255) / 256); }
 __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* __restrict__ ps) {
     const LookupParams& p = ps[blockIdx.z];
     const int nb = stream_blocks(p.U);
@@ -2187,6 +2187,6 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
 }
 int64_t decode_batch_lookup_blocks(int64_t U) {  // reg-scan blocks | stream-scan blocks << 32
     const int64_t want = (U + 7) / 8;
-    return (want < 148 * 4 ? want : 148 * 4) | (((U + 63) / 64) << 32);
+    return (want < 148 * 4 ? want : 148 * 4) | (((U + 255) / 256) << 32);
 }
 }  // namespace infllm
