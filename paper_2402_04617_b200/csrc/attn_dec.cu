@@ -24,7 +24,7 @@ namespace infllm {
 
 namespace {
 
-constexpr int kW = 8;           // warps: 16 keys each for S = QK^T and for P V
+constexpr int kW = kDecWarps;  // warps: 16 keys each for S = QK^T and for P V
 constexpr int kThr = 32 * kW;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -137,7 +137,7 @@ __device__ __forceinline__ void dec_load(const AttnParams& a, const DecTile& tl,
 __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& sc, int b, int x, int nsplit) {
     extern __shared__ __align__(128) uint8_t dsm[];
     __shared__ float sred[kW][kDecMaxRep], sl_red[kW][kDecMaxRep];
-    __shared__ float s_m[kDecMaxRep], s_alpha[kDecMaxRep], s_M[kDecMaxRep], s_L[kDecMaxRep];
+    __shared__ float s_m[kDecMaxRep], s_M[kDecMaxRep], s_L[kDecMaxRep];
     __shared__ bool s_last;
     __shared__ int32_t s_page[kDecMaxSel], s_len[kDecMaxSel];
 
@@ -159,7 +159,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int tps = (T + nsplit - 1) / nsplit;
     const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
 
-    for (int st = 0; st < kStages; ++st) {  // prefetch the first tiles
+    for (int st = 0; st < kStages - 1; ++st) {  // prefetch the first tiles
         if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, sbase + st * kStageB);
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -179,7 +179,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             qc[kk][1] = hv ? *reinterpret_cast<const uint32_t*>(pc + 16 * kk + 8 + 2 * tq) : 0u;
         }
     }
-    if (tid < kDecMaxRep) s_m[tid] = -INFINITY;
+    float mw = -INFINITY;  // this warp's running max of row gq (log2 domain): online softmax per warp
     float o[16][4];  // O fragments of this warp's keys: 16 n-tiles of 8 dims (rows gq)
 #pragma unroll
     for (int j = 0; j < 16; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
@@ -189,8 +189,13 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     for (int t = t0; t < t1; ++t) {
         const int st = (t - t0) % kStages;
         const DecTile tl = dec_tile(a, t, n_init, near0, s_page, s_len);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 1) : "memory");
-        __syncthreads();
+        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
+        __syncthreads();  // tile t visible to every warp; every warp is done with tile t-1
+        // refill the stage of tile t-1 with tile t+kStages-1 (one barrier per tile)
+        if (t + kStages - 1 < t1)
+            dec_load(a, dec_tile(a, t + kStages - 1, n_init, near0, s_page, s_len), g,
+                     sbase + ((t - t0 + kStages - 1) % kStages) * kStageB);
+        asm volatile("cp.async.commit_group;" ::: "memory");
         const uint32_t sk = sbase + st * kStageB, sv = sk + kMatB;
         // ---- S = Q K^T for keys k0..k0+15 (2 n-tiles) ----
         float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -218,40 +223,35 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             }
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
         tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-        if (tq == 0 && gq < kDecMaxRep) sred[warp][gq] = tmax;
-        __syncthreads();
-        if (tid < rep) {
-            float tm = sred[0][tid];
-#pragma unroll
-            for (int w = 1; w < kW; ++w) tm = fmaxf(tm, sred[w][tid]);
-            const float mo = s_m[tid];
-            const float mn = fmaxf(mo, tm);
-            s_m[tid] = mn;
-            s_alpha[tid] = mo == -INFINITY ? 0.f : ex2f(mo - mn);
-        }
-        __syncthreads();
-        const int hr = gq < kDecMaxRep ? gq : 0;
-        const float mrow = s_m[hr], al = s_alpha[hr];
+        const float mn = fmaxf(mw, tmax);
+        const float al = mn == -INFINITY ? 1.f : (mw == -INFINITY ? 0.f : ex2f(mw - mn));
+        mw = mn;
         float p[2][2], psum = 0.f;
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                p[j][e] = sv2[j][e] == -INFINITY ? 0.f : ex2f(sv2[j][e] - mrow);
+                p[j][e] = sv2[j][e] == -INFINITY ? 0.f : ex2f(sv2[j][e] - mn);
                 psum += p[j][e];
             }
         lsum = lsum * al + psum;
-        if (tl.src == 1 && a.want_mass) {  // the unit's mass relative to this tile's running max
+        if (tl.src == 1 && a.want_mass) {  // this warp's share of the unit's mass, relative to its running max
             float e2 = psum;
             e2 += __shfl_xor_sync(0xffffffffu, e2, 1);
             e2 += __shfl_xor_sync(0xffffffffu, e2, 2);
-            if (tq == 0 && gq < kDecMaxRep) sl_red[warp][gq] = e2;
+            if (tq == 0 && gq < rep) {
+                float* mr = sc.mass + (((static_cast<int64_t>(b) * a.H + g * rep + gq) * sc.max_sel + (t - n_init)) * kW + warp) * 2;
+                mr[0] = e2;
+                mr[1] = mn;
+            }
         }
         // ---- O = O alpha + P V over this warp's 16 keys (one k-step; P from the S fragments) ----
+        if (__any_sync(0xffffffffu, al != 1.f)) {  // the max moved for some row of this warp
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            o[j][0] *= al;
-            o[j][1] *= al;
+            for (int j = 0; j < 16; ++j) {
+                o[j][0] *= al;
+                o[j][1] *= al;
+            }
         }
         const uint32_t A0 = pack_bf16(p[0][0], p[0][1]), A2 = pack_bf16(p[1][0], p[1][1]);
         const uint32_t vaddr = sv + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowB + (k0 + ((lane >> 3) & 1) * 8) * 2;
@@ -262,26 +262,32 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             mma16816(o[2 * jp], A0, A2, b0, b1);
             mma16816(o[2 * jp + 1], A0, A2, b2, b3);
         }
-        __syncthreads();  // every warp is done with this stage
-        if (tl.src == 1 && a.want_mass && tid < rep) {
-            float e = 0.f;
-#pragma unroll
-            for (int w = 0; w < kW; ++w) e += sl_red[w][tid];
-            const int u = t - n_init;
-            float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + tid) * sc.max_sel + u) * 2;
-            mr[0] = e;
-            mr[1] = s_m[tid];
-        }
-        if (t + kStages < t1) dec_load(a, dec_tile(a, t + kStages, n_init, near0, s_page, s_len), g, sbase + st * kStageB);
-        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // ---- this split's partial (m, l, O) per head; the warps' O summed in smem ----
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // ---- this split's partial (m, l, O) per head: the warps' online softmaxes merged ----
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-    if (tq == 0 && gq < kDecMaxRep) sred[warp][gq] = lsum;
+    if (tq == 0 && gq < kDecMaxRep) {
+        sred[warp][gq] = mw;
+        sl_red[warp][gq] = lsum;
+    }
     float* so = reinterpret_cast<float*>(dsm);  // [kW][rep][128] (the stages are free now)
     __syncthreads();
+    if (tid < rep) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) M = fmaxf(M, sred[w][tid]);
+        float l = 0.f;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+            const float f = sred[w][tid] == -INFINITY ? 0.f : ex2f(sred[w][tid] - M);
+            sred[w][tid] = f;  // the warp's scale factor
+            l += sl_red[w][tid] * f;
+        }
+        s_m[tid] = M;
+        s_L[tid] = l;
+    }
     if (gq < rep) {
 #pragma unroll
         for (int j = 0; j < 16; ++j)
@@ -291,17 +297,14 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int64_t stride = static_cast<int64_t>(rep) * 130;
     float* part = sc.part + ((static_cast<int64_t>(b) * a.G + g) * nsplit + x) * stride;
     if (tid < rep) {
-        float l = 0.f;
-#pragma unroll
-        for (int w = 0; w < kW; ++w) l += sred[w][tid];
         part[tid * 130 + 0] = s_m[tid];
-        part[tid * 130 + 1] = l;
+        part[tid * 130 + 1] = s_L[tid];
     }
     for (int i = tid; i < rep * 128; i += kThr) {
         const int h = i / 128, c = i % 128;
         float v = 0.f;
 #pragma unroll
-        for (int w = 0; w < kW; ++w) v += so[(w * rep + h) * 128 + c];
+        for (int w = 0; w < kW; ++w) v = fmaf(so[(w * rep + h) * 128 + c], sred[w][h], v);
         part[h * 130 + 2 + c] = v;
     }
     // ---- the last split of (sequence, group) merges ----
@@ -318,17 +321,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const float* p0 = sc.part + (static_cast<int64_t>(b) * a.G + g) * nsplit * stride;
     __shared__ float s_w[kDecMaxSplits][kDecMaxRep], s_ls[kDecMaxSplits][kDecMaxRep];
     // mass records of the retrieved units, loaded up front (one round trip)
-    float mrec[2 * kDecMaxRep];
     const bool mass_thread = a.want_mass && a.mass_part && tid < a.n_sel;
-    if (mass_thread) {
-#pragma unroll
-        for (int h = 0; h < kDecMaxRep; ++h) {
-            if (h >= rep) break;
-            const float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + h) * sc.max_sel + tid) * 2;
-            mrec[2 * h] = __ldcg(mr);
-            mrec[2 * h + 1] = __ldcg(mr + 1);
-        }
-    }
     for (int i = tid; i < nsplit * rep; i += kThr) {
         const int xs = i / rep, h = i % rep;
         s_w[xs][h] = __ldcg(p0 + xs * stride + h * 130);
@@ -371,10 +364,15 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     // the unit's keys, summed (engine.hpp:271-283; the LRU divides by H)
     if (mass_thread) {
         double msum = 0.0;
+        for (int h = 0; h < rep; ++h) {
+            const float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + h) * sc.max_sel + tid) * kW * 2;
+            float rec[2 * kW];
 #pragma unroll
-        for (int h = 0; h < kDecMaxRep; ++h) {
-            if (h >= rep) break;
-            msum += static_cast<double>(mrec[2 * h] * ex2f(mrec[2 * h + 1] - s_M[h]) / s_L[h]);
+            for (int i = 0; i < 2 * kW; ++i) rec[i] = __ldcg(mr + i);
+            float e = 0.f;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) e += rec[2 * w + 1] == -INFINITY ? 0.f : rec[2 * w] * ex2f(rec[2 * w + 1] - s_M[h]);
+            msum += static_cast<double>(e / s_L[h]);
         }
         a.mass_part[static_cast<int64_t>(tid) * a.Gtot + a.g0 + g] = msum;
     }

@@ -8,13 +8,14 @@ namespace infllm {
 constexpr int kDecMaxRep = 8;      // query heads per KV group
 constexpr int kDecMaxSplits = 64;  // KV splits per (sequence, group)
 constexpr int kDecMaxSel = 128;    // retrieved units (n_lookup)
+constexpr int kDecWarps = 8;       // warps per CTA (per-warp unit mass records)
 
 // scratch of one launch: split partials (m, l, O[128]) per head, per-unit
 // (mass, running max) records, and per-(sequence, group) arrival counters
 // (zero-initialised once; the merging CTA resets its counter)
 struct DecScratch {
     float* part;    // [B][G][splits][rep][130]
-    float* mass;    // [B][H][max_sel][2]
+    float* mass;    // [B][H][max_sel][kDecWarps][2] per-warp (mass, running max)
     unsigned* cnt;  // [B][G]
     int max_sel;
     int dbg;  // timing experiments only: bit0 skip tiles, bit1 skip merge

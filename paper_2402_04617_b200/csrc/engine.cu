@@ -1376,7 +1376,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->mass_cta.alloc(2 * e->mass_cta_half * sizeof(double), st);
         if (e->use_dec) {
             e->dec_part.alloc(dec_part_floats(1, e->Gs, e->rep) * sizeof(float), st, false);
-            e->dec_mass.alloc(static_cast<size_t>(e->Hs) * km * 2 * sizeof(float), st);
+            e->dec_mass.alloc(static_cast<size_t>(e->Hs) * km * kDecWarps * 2 * sizeof(float), st);
             e->dec_cnt.alloc(static_cast<size_t>(e->Gs) * sizeof(unsigned), st);
         }
         e->layers.resize(static_cast<size_t>(e->n_layers));
@@ -1672,7 +1672,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         if (bc.part_B < n) {
             ck(cudaStreamSynchronize(st), "scratch growth");
             bc.part.alloc(dec_part_floats(n, G, rep) * sizeof(float), st, false);
-            bc.mass.alloc(static_cast<size_t>(n) * e0->Hs * km * 2 * sizeof(float), st);
+            bc.mass.alloc(static_cast<size_t>(n) * e0->Hs * km * kDecWarps * 2 * sizeof(float), st);
             bc.cnt.alloc(static_cast<size_t>(n) * G * sizeof(unsigned), st);
             bc.part_B = n;
         }
