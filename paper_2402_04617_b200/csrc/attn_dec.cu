@@ -15,6 +15,8 @@
 // keeps an online softmax for the group's query heads; the last CTA of a
 // (sequence, group) merges the splits (log-sum-exp) and finishes the masses.
 #include "attn_dec.cuh"
+#include "tc_prims.cuh"
+#include "tmap.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -79,15 +81,14 @@ __device__ __forceinline__ int dec_tiles(const AttnParams& a, int& n_init, int64
 // always within l_L of the query (the local window holds l_L tokens), so a
 // ring page is attended with rotated keys only; init / unit pages are far
 // (clamped: rope(q, l_L) . k_raw, attention.hpp:165-173).
-constexpr int kRowB = 272;
-constexpr int kMatB = 128 * kRowB;  // 34816
+// stage = K tile then V^T tile, each two TMA boxes of [128 rows][64 cols] bf16
+// with the 128-byte swizzle (16-byte chunk c of row r at chunk c ^ (r & 7))
+constexpr int kBoxB = 128 * 128;    // 16 KB
+constexpr int kMatB = 2 * kBoxB;    // 32 KB
 constexpr int kStageB = 2 * kMatB;
 constexpr int kStages = 3;
-constexpr int kDecSmem = kStages * kStageB;
+constexpr int kDecSmem = kStages * kStageB + 1024;  // + alignment slack (SW128 boxes: 1024 B)
 
-__device__ __forceinline__ void cpa16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -101,45 +102,45 @@ __device__ __forceinline__ void mma16816(float* d, uint32_t a0, uint32_t a2, uin
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&v);
-}
+using tc::pack_bf16;
 
-// cp.async of tile `tl` (K page then V^T page, 2 x 32 KB contiguous) into stage `sb`
-__device__ __forceinline__ void dec_load(const AttnParams& a, const DecTile& tl, int g, uint32_t sb) {
-    const bf16 *k, *v;
-    int rows = 128;
+// tile `tl` into stage `sb`: four TMA boxes (K cols 0-63 / 64-127, V^T keys
+// 0-63 / 64-127) issued by one thread, completion counted in bytes on `bar`.
+// Tensor maps (device memory, one set per engine): 0 init K, 1 init V^T,
+// 2 unit K, 3 unit V^T, 4 ring K_rot, 5 ring V^T.
+__device__ __forceinline__ void dec_load(const AttnParams& a, const DecTile& tl, int g, uint8_t* sb, uint64_t* bar) {
+    if (threadIdx.x != 0) return;
+    const CUtensorMap* tm = static_cast<const CUtensorMap*>(a.dec_maps);
+    int mk, mv, rk, rv;
     if (tl.src == 0) {
-        k = static_cast<const bf16*>(a.init_k) + (static_cast<int64_t>(g) * a.l_I + tl.key0) * 128;
-        v = static_cast<const bf16*>(a.init_v) + (static_cast<int64_t>(g) * a.vl.nI + tl.page) * 128 * 128;
-        rows = static_cast<int>(min(static_cast<int64_t>(128), a.l_I - tl.key0));  // stay inside the init rows
+        mk = 0, mv = 1;
+        rk = static_cast<int>(g * a.l_I + tl.key0);
+        rv = static_cast<int>((g * a.vl.nI + tl.page) * 128);
     } else if (tl.src == 1) {
-        k = static_cast<const bf16*>(a.unit_k) + (tl.page * a.G + g) * 128 * 128;
-        v = static_cast<const bf16*>(a.unit_v) + (tl.page * a.G + g) * 128 * 128;
+        mk = 2, mv = 3;
+        rk = rv = static_cast<int>((tl.page * a.G + g) * 128);
     } else {
         const int64_t sl = tl.key0 % a.R;
-        k = static_cast<const bf16*>(a.ring_krot) + (static_cast<int64_t>(g) * a.R + sl) * 128;
-        v = static_cast<const bf16*>(a.ring_v) + (static_cast<int64_t>(g) * (a.R / 128) + sl / 128) * 128 * 128;
+        mk = 4, mv = 5;
+        rk = static_cast<int>(g * a.R + sl);
+        rv = static_cast<int>((g * (a.R / 128) + sl / 128) * 128);
     }
-    const int c = threadIdx.x & 15, r0 = threadIdx.x >> 4;  // 16 threads per 256-byte row
-    const uint32_t so = r0 * kRowB + c * 16;
-    const bf16* kp = k + r0 * 128 + c * 8;
-    const bf16* vp = v + r0 * 128 + c * 8;
-#pragma unroll
-    for (int i = 0; i < 128 / (kThr / 16); ++i) {
-        const int r = r0 + i * (kThr / 16);
-        if (r < rows) cpa16(sb + so + i * (kThr / 16) * kRowB, kp + i * (kThr / 16) * 128);
-        cpa16(sb + kMatB + so + i * (kThr / 16) * kRowB, vp + i * (kThr / 16) * 128);
-    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage was last read by ldmatrix
+    tc::mbar_expect_tx(bar, kStageB);
+    tc::tma_load_2d(tm + mk, bar, sb, 0, rk);
+    tc::tma_load_2d(tm + mk, bar, sb + kBoxB, 64, rk);
+    tc::tma_load_2d(tm + mv, bar, sb + kMatB, 0, rv);
+    tc::tma_load_2d(tm + mv, bar, sb + kMatB + kBoxB, 64, rv);
 }
 
 __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& sc, int b, int x, int nsplit) {
-    extern __shared__ __align__(128) uint8_t dsm[];
+    extern __shared__ __align__(1024) uint8_t dsm_raw[];
+    uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     __shared__ float sred[kW][kDecMaxRep], sl_red[kW][kDecMaxRep];
     __shared__ float s_m[kDecMaxRep], s_M[kDecMaxRep], s_L[kDecMaxRep];
     __shared__ bool s_last;
     __shared__ int32_t s_page[kDecMaxSel], s_len[kDecMaxSel];
+    __shared__ __align__(8) uint64_t s_bar[kStages];
 
     const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
     const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (query head) / column pair
@@ -148,10 +149,14 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
         s_page[u] = a.sel_slot ? a.sel_slot[u] : static_cast<int32_t>(id);
         s_len[u] = a.unit_len[id];
     }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) tc::mbar_init(&s_bar[i], 1);
+        tc::fence_barrier_init();
+    }
     __syncthreads();
     const int g = blockIdx.y, rep = a.rep;
     const float sl2 = a.scale * kLog2e;
-    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));  // 1024-aligned
 
     int n_init;
     int64_t near0;
@@ -159,10 +164,8 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int tps = (T + nsplit - 1) / nsplit;
     const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
 
-    for (int st = 0; st < kStages - 1; ++st) {  // prefetch the first tiles
-        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, sbase + st * kStageB);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    }
+    for (int st = 0; st < kStages - 1; ++st)  // prefetch the first tiles
+        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, dsm + st * kStageB, &s_bar[st]);
     // query fragments (A operand, row = query head of the group, zero beyond rep):
     // rope(q, pos) for ring pages, rope(q, l_L) for init / unit pages; 8 k-steps of 16 dims
     uint32_t qa[8][2], qc[8][2];
@@ -189,22 +192,24 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     for (int t = t0; t < t1; ++t) {
         const int st = (t - t0) % kStages;
         const DecTile tl = dec_tile(a, t, n_init, near0, s_page, s_len);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kStages - 2) : "memory");
-        __syncthreads();  // tile t visible to every warp; every warp is done with tile t-1
+        __syncthreads();  // every warp is done with tile t-1
         // refill the stage of tile t-1 with tile t+kStages-1 (one barrier per tile)
-        if (t + kStages - 1 < t1)
-            dec_load(a, dec_tile(a, t + kStages - 1, n_init, near0, s_page, s_len), g,
-                     sbase + ((t - t0 + kStages - 1) % kStages) * kStageB);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (t + kStages - 1 < t1) {
+            const int sn = (t - t0 + kStages - 1) % kStages;
+            dec_load(a, dec_tile(a, t + kStages - 1, n_init, near0, s_page, s_len), g, dsm + sn * kStageB, &s_bar[sn]);
+        }
+        tc::mbar_wait(&s_bar[st], static_cast<uint32_t>(((t - t0) / kStages) & 1));
         const uint32_t sk = sbase + st * kStageB, sv = sk + kMatB;
         // ---- S = Q K^T for keys k0..k0+15 (2 n-tiles) ----
         float s2[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
         const bool far = tl.src != 2;
-        const uint32_t kaddr = sk + (k0 + (lane & 7) + ((lane >> 4) & 1) * 8) * kRowB + ((lane >> 3) & 1) * 16;
+        const int krow = k0 + (lane & 7) + ((lane >> 4) & 1) * 8, khalf = (lane >> 3) & 1;
+        const uint32_t kbase = sk + krow * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
             uint32_t b0, b1, b2, b3;
-            ldsm_x4(kaddr + kk * 32, b0, b1, b2, b3);
+            const int chunk = 2 * (kk & 3) + khalf;  // 16-byte chunk within the 128-byte swizzled row
+            ldsm_x4(kbase + (kk >> 2) * kBoxB + ((chunk ^ (krow & 7)) << 4), b0, b1, b2, b3);
             const uint32_t A0 = far ? qc[kk][0] : qa[kk][0], A2 = far ? qc[kk][1] : qa[kk][1];
             mma16816(s2[0], A0, A2, b0, b1);
             mma16816(s2[1], A0, A2, b2, b3);
@@ -254,16 +259,18 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             }
         }
         const uint32_t A0 = pack_bf16(p[0][0], p[0][1]), A2 = pack_bf16(p[1][0], p[1][1]);
-        const uint32_t vaddr = sv + ((lane & 7) + ((lane >> 4) & 1) * 8) * kRowB + (k0 + ((lane >> 3) & 1) * 8) * 2;
+        const int vkey = k0 + ((lane >> 3) & 1) * 8;  // first key of this lane's 8-key chunk
+        const int vchunk = (vkey & 63) >> 3;
+        const uint32_t vbase = sv + (vkey >> 6) * kBoxB;
 #pragma unroll
         for (int jp = 0; jp < 8; ++jp) {
             uint32_t b0, b1, b2, b3;
-            ldsm_x4(vaddr + 16 * jp * kRowB, b0, b1, b2, b3);
+            const int vrow = 16 * jp + (lane & 7) + ((lane >> 4) & 1) * 8;  // value dim
+            ldsm_x4(vbase + vrow * 128 + ((vchunk ^ (vrow & 7)) << 4), b0, b1, b2, b3);
             mma16816(o[2 * jp], A0, A2, b0, b1);
             mma16816(o[2 * jp + 1], A0, A2, b2, b3);
         }
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     // ---- this split's partial (m, l, O) per head: the warps' online softmaxes merged ----
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
@@ -418,6 +425,17 @@ int pick_splits(int64_t max_tiles, int G, int B) {
 
 bool attn_dec_supported(int d, int dv, int unit_size, int rep, bool absolute, int dtype_bf16) {
     return dtype_bf16 && d == 128 && dv == 128 && unit_size == 128 && rep <= kDecMaxRep && !absolute;
+}
+
+void dec_encode_maps(const AttnParams& a, int64_t unit_rows, void* host6) {
+    CUtensorMap* m = static_cast<CUtensorMap*>(host6);
+    const uint64_t G = static_cast<uint64_t>(a.G);
+    m[0] = make_tmap_bf16_sw128(a.init_k, G * static_cast<uint64_t>(a.l_I), 128, 128);
+    m[1] = make_tmap_bf16_sw128(a.init_v, G * a.vl.nI * 128, 128, 128);
+    m[2] = make_tmap_bf16_sw128(a.unit_k ? a.unit_k : a.ring_k, a.unit_k ? static_cast<uint64_t>(unit_rows) : 128, 128, 128);
+    m[3] = make_tmap_bf16_sw128(a.unit_v ? a.unit_v : a.ring_v, a.unit_v ? static_cast<uint64_t>(unit_rows) : 128, 128, 128);
+    m[4] = make_tmap_bf16_sw128(a.ring_krot, G * static_cast<uint64_t>(a.R), 128, 128);
+    m[5] = make_tmap_bf16_sw128(a.ring_v, G * static_cast<uint64_t>(a.R), 128, 128);
 }
 
 int64_t dec_max_tiles(const AttnParams& a) {

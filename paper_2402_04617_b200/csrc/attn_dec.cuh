@@ -24,6 +24,9 @@ inline size_t dec_part_floats(int B, int G, int rep) {
     return static_cast<size_t>(B) * G * kDecMaxSplits * rep * 130;
 }
 
+// host: the K4 tensor maps of one layer (6 x CUtensorMap, 64-byte aligned
+// host buffer) for its current buffers; unit_rows = unit (or slot) pages x G x 128
+void dec_encode_maps(const AttnParams& a, int64_t unit_rows, void* host6);
 bool attn_dec_supported(int d, int dv, int unit_size, int rep, bool absolute, int dtype_bf16);
 int64_t dec_max_tiles(const AttnParams& a);
 void launch_attn_dec(const AttnParams& a, const DecScratch& sc, cudaStream_t st);

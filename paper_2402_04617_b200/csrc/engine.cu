@@ -329,6 +329,8 @@ struct infllm_engine {
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
         DBuf kmax2;  // [kPB step buffers][G] running max |k|^2 (attention score bound)
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
+        DBuf dec_maps;  // K4 TMA tensor maps (6), re-encoded when a buffer moves
+        std::vector<const void*> dec_maps_key;
         // host tier (tier_slots > 0): unit pages in mapped pinned host memory,
         // the attention reads them from tier_slots device cache slots
         HBuf host_k, host_krot, host_v;
@@ -921,6 +923,20 @@ struct infllm_engine {
         ap.Gtot = Gt;
         ap.g0 = g0;
         const bool dec_ran = lx == 1 && use_dec && !dec_disabled;
+        if (dec_ran) {  // K4 tensor maps of this layer's buffers (rebuilt only when one moved or grew)
+            const int64_t urows = (tier ? tier_slots : L.unit_cap) * static_cast<int64_t>(Gs) * 128;
+            std::vector<const void*> key{ap.init_k, ap.init_v, ap.unit_k, ap.unit_v, ap.ring_krot, ap.ring_v,
+                                         reinterpret_cast<const void*>(urows)};
+            if (key != L.dec_maps_key || !L.dec_maps.p) {
+                alignas(64) CUtensorMap hm[6];
+                dec_encode_maps(ap, urows, hm);
+                if (!L.dec_maps.p) L.dec_maps.alloc(sizeof(hm), st, false);
+                ck(cudaMemcpyAsync(L.dec_maps.p, hm, sizeof(hm), cudaMemcpyHostToDevice, st), "tensor maps H2D");
+                ck(cudaStreamSynchronize(st), "tensor maps");  // hm is a stack buffer
+                L.dec_maps_key = key;
+            }
+            ap.dec_maps = L.dec_maps.p;
+        }
         last_ap = ap;
         std::pair<cudaEvent_t, cudaEvent_t> eva{};
         if (prof) {
@@ -1420,7 +1436,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
                             &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
                             &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
-                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats})
+                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps})
                 b->release(st);
         for (auto& L : e->layers)
             for (auto* h : {&L.host_k, &L.host_krot, &L.host_v}) h->release();

@@ -108,6 +108,7 @@ struct AttnParams {
     double* mass_cta;  // [H][n_mt][n_sel] (tcgen05 path)
     const float* kmax2;  // [G] max |k|^2 over all keys (score bound), or null
     double* mass_part;   // decode kernel (K4): per-group unit masses [n_sel][Gtot], or null
+    const void* dec_maps;  // decode kernel (K4): 6 TMA tensor maps in device memory (see attn_dec.cu)
     int Gtot, g0;
     int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
