@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "tc_prims.cuh"
 
 namespace infllm {
 
@@ -800,21 +801,30 @@ __device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nb
     for (int g = 0; g < 8; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+    // one bulk copy (TMA engine) per unit row block, completion on a per-(warp, stage) mbarrier
+    __shared__ __align__(8) uint64_t sbar[8][kScanStages];
+    if (lane == 0)
+        for (int st = 0; st < kScanStages; ++st) tc::mbar_init(&sbar[wib][st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
     auto issue = [&](int64_t u, int stage) {
-        if (u < s1) {
-            const uint8_t* src = static_cast<const uint8_t*>(p.repr) + u * bytes_u;
-            uint8_t* dst = ring + stage * 8192;
-            for (int64_t off = 16 * lane; off < bytes_u; off += 512) cp_async16(dst + off, src + off);
+        if (u < s1 && lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage was read by this warp
+            tc::mbar_expect_tx(&sbar[wib][stage], static_cast<uint32_t>(bytes_u));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             tc::smem_u32(ring + stage * 8192)),
+                         "l"(static_cast<const uint8_t*>(p.repr) + u * bytes_u), "r"(static_cast<uint32_t>(bytes_u)),
+                         "r"(tc::smem_u32(&sbar[wib][stage]))
+                         : "memory");
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
     for (int st = 0; st < kScanStages - 1; ++st) issue(warp0 + st * nwarps, st);
     int stage = 0;
-    for (int64_t u = warp0; u < s1; u += nwarps) {
+    int64_t it = 0;
+    for (int64_t u = warp0; u < s1; u += nwarps, ++it) {
         issue(u + (kScanStages - 1) * nwarps, (stage + kScanStages - 1) % kScanStages);
-        asm volatile("cp.async.wait_group %0;" ::"n"(kScanStages - 1) : "memory");
-        __syncwarp();
+        tc::mbar_wait(&sbar[wib][stage], static_cast<uint32_t>((it / kScanStages) & 1));
         const uint8_t* buf = ring + stage * 8192 + 8 * lane;
         double rel = 0.0;
 #pragma unroll
@@ -843,7 +853,6 @@ __device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nb
         __syncwarp();  // the stage is refilled next iteration
         stage = (stage + 1) % kScanStages;
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (!p.cand_v) return;
     // this block's slice: top n_sel candidates for the final merge (k_topk_final)
     __shared__ int64_t loc[128];
