@@ -233,7 +233,12 @@ __global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
 }  // namespace
 
 // parameters of one batched decode step, gathered from each engine's step()
+struct DecFrontRec {  // layout of the batched decode-front table (kernels.cu DecFront)
+    PrepParams p;
+    EvictParams ep;
+};
 struct DecodeCollector {
+    std::vector<DecFrontRec> front;
     std::vector<PrepParams> prep;
     std::vector<EvictParams> evict;
     std::vector<SelectParams> select;
@@ -660,11 +665,25 @@ struct infllm_engine {
         pp.kmax2_prev = kbound ? L.kmax2.as<float>() + ((lb + kPB - 1) % kPB) * Gs : nullptr;
         last_pp = pp;
         last_bf16 = std::is_same_v<T, bf16>;
-        if (coll)
+        // one-token steps on one stream: prep and eviction fused into one launch
+        // (issued at the eviction site below)
+        bool fused_front = false;
+        if constexpr (std::is_same_v<T, bf16>)
+            fused_front = lx == 1 && (one_stream || coll) && dec_front_supported(pp) && page_mode() && Gs == Gt &&
+                          !(debug_skip & (8 | 4 | 128));
+        auto issue_front = [&](const EvictParams& ep2, cudaStream_t s2) {
+            if (coll)
+                coll->front.push_back(DecFrontRec{pp, ep2});
+            else
+                launch_dec_front(pp, ep2, s2);
+        };
+        if (fused_front) {
+        } else if (coll)
             coll->prep.push_back(pp);
         else if (!(debug_skip & 8))
             launch_prep<T>(pp, st);
-        launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
+        if (!fused_front)
+            launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
         rec(e_prep, pst);
         wt(side, e_prep);
         st = side;
@@ -724,7 +743,9 @@ struct infllm_engine {
             ep.done = evict_done.as<unsigned int>();
             ep.page_mode = page_mode() ? 1 : 0;
             last_ep = ep;
-            if (coll) {
+            if (fused_front) {
+                issue_front(ep, st);
+            } else if (coll) {
                 if (!ep.fused) throw StreamError("decode_batch: sharded eviction is not batched");
                 if (ep.n_init + ep.n_evict > 0) coll->evict.push_back(ep);
             } else if (!(debug_skip & 4)) {
@@ -775,6 +796,9 @@ struct infllm_engine {
             L.pend_count = new_pending - completed * cfg.unit_size;
             L.local_start += overflow;
             L.init_len += to_init;
+        } else if (fused_front) {
+            issue_front(EvictParams{}, st);  // nothing leaves the window: prep only
+            ++launches;
         }
         rec(e_evict, est);
         evict_seq = kseq;
@@ -1654,12 +1678,16 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             }
             engs[i]->coll = nullptr;
         }
-        if (static_cast<int32_t>(c.prep.size()) != n || static_cast<int32_t>(c.attn.size()) != n ||
+        if (static_cast<int32_t>(c.prep.size() + c.front.size()) != n || static_cast<int32_t>(c.attn.size()) != n ||
             static_cast<int32_t>(c.lru.size()) != n)
             throw StreamError("decode_batch: unexpected step shape");
         if (!e0->bctx) e0->bctx = std::make_unique<BatchCtx>();
         BatchCtx& bc = *e0->bctx;
         std::vector<uint8_t> buf;
+        if (!c.front.empty() && static_cast<int32_t>(c.front.size()) != n)
+            throw StreamError("decode_batch: mixed decode-front shapes");
+        if (dec_front_size() != sizeof(DecFrontRec)) throw StreamError("decode_batch: front record layout");
+        const size_t o_front = put(buf, c.front);
         const size_t o_prep = put(buf, c.prep), o_ev = put(buf, c.evict), o_sel = put(buf, c.select);
         const size_t o_lk = put(buf, c.lookup), o_at = put(buf, c.attn), o_lru = put(buf, c.lru);
         const int s = bc.slot;
@@ -1703,7 +1731,10 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         lk_max = lk_reg | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
-        launch_decode_batch_stage(0, dt + o_prep, n, G, st);
+        if (!c.front.empty())
+            launch_dec_front_batch(dt + o_front, n, G, st);
+        else
+            launch_decode_batch_stage(0, dt + o_prep, n, G, st);
         if (!c.evict.empty())
             launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
         if (!c.select.empty())

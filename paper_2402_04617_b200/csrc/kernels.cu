@@ -2109,6 +2109,105 @@ void launch_select_standalone(const float* scores, const int64_t* lens, int64_t 
 }  // namespace infllm
 
 namespace infllm {
+
+// ---- decode front: K7 prep of one token + eviction of the token leaving the
+// local window, one block of 32 x G threads per sequence (warp = KV group).
+// Same arithmetic as k_rope_table + k_prep_tok + k_prefix_tiles +
+// k_evict_tok at l_x = 1 (rope factors from fp64 angles, query sums in head
+// order, P[s+1] = P[s] + qs, r_m from the prefix difference), in one launch.
+__device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictParams& ep) {
+    const int g = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t pos = p.s;
+    if (lane < 16) {
+        const int c8 = lane;
+        const bf16* qg = static_cast<const bf16*>(p.q);
+        constexpr int kMaxRep = 8;
+        V8<bf16> qv[kMaxRep];
+#pragma unroll
+        for (int hh = 0; hh < kMaxRep; ++hh)
+            if (hh < p.rep) qv[hh] = ld8(qg + (g * p.rep + hh) * p.d + 8 * c8);
+        const V8<bf16> kv = ld8(static_cast<const bf16*>(p.k) + g * p.d + 8 * c8);
+        const V8<bf16> vv = ld8(static_cast<const bf16*>(p.v) + g * p.dv + 8 * c8);
+        float2 f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rope_cs(p.freqs, 4 * c8 + j, pos, f[j].x, f[j].y);
+        V8<bf16> kr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float y0, y1;
+            rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
+            kr.v[2 * j] = from_f<bf16>(y0);
+            kr.v[2 * j + 1] = from_f<bf16>(y1);
+        }
+        float kn2 = 0.f;  // as k_prep_tok (the bound is |k|^2 accumulated twice)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
+        const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
+        st8(static_cast<bf16*>(p.ring_k) + ro, kv);
+        st8(static_cast<bf16*>(p.ring_krot) + ro, kr);
+        double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int hh = 0; hh < kMaxRep; ++hh) {
+            if (hh >= p.rep) break;
+            V8<bf16> qa, qc;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float x0 = to_f(qv[hh].v[2 * j]), x1 = to_f(qv[hh].v[2 * j + 1]);
+                float y0, y1;
+                rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
+                qa.v[2 * j] = from_f<bf16>(y0);
+                qa.v[2 * j + 1] = from_f<bf16>(y1);
+                const int a = 4 * c8 + j;
+                rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
+                qc.v[2 * j] = from_f<bf16>(y0);
+                qc.v[2 * j + 1] = from_f<bf16>(y1);
+                qs[2 * j] += static_cast<double>(x0);
+                qs[2 * j + 1] += static_cast<double>(x1);
+            }
+            const int64_t qo = (static_cast<int64_t>(g * p.rep + hh) * p.lxp) * p.d + 8 * c8;
+            st8(static_cast<bf16*>(p.qa) + qo, qa);
+            st8(static_cast<bf16*>(p.qc) + qo, qc);
+        }
+        bf16* rv = static_cast<bf16*>(p.ring_v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) rv[p.vl.ring(g, pos, 8 * c8 + e)] = vv.v[e];
+        // prefix ring and chunk query sum (k_prefix_tiles at l_x = 1)
+        const double* Pin = p.P + ((pos % p.R) * p.G + g) * p.d + 8 * c8;
+        double* Pout = p.P + (((pos + 1) % p.R) * p.G + g) * p.d + 8 * c8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            Pout[e] = Pin[e] + qs[e];
+            p.chunk_qsum[g * p.d + 8 * c8 + e] = 0.0 + (qs[e] + 0.0);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) kn2 += __shfl_xor_sync(0x0000ffffu, kn2, o);
+        if (lane == 0 && p.kmax2) p.kmax2[g] = fmaxf(p.kmax2_prev[g], kn2);
+    }
+    if (ep.n_init + ep.n_evict == 0) return;  // uniform: nothing leaves the window this step
+    __syncthreads();  // this step's P row is read by the eviction score
+    evict_tok_body<bf16>(ep);
+}
+__global__ void __launch_bounds__(1024) k_dec_front(PrepParams p, EvictParams ep) { dec_front_body(p, ep); }
+struct DecFront {
+    PrepParams p;
+    EvictParams ep;
+};
+__global__ void __launch_bounds__(1024) k_dec_front_b(const DecFront* __restrict__ fs) {
+    dec_front_body(fs[blockIdx.z].p, fs[blockIdx.z].ep);
+}
+bool dec_front_supported(const PrepParams& p) {
+    return p.d == 128 && p.dv == 128 && p.rep <= 8 && p.G <= 32 && p.lx == 1 && p.vl.vt;
+}
+void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t st) {
+    k_dec_front<<<1, 32 * p.G, 0, st>>>(p, ep);
+}
+void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st) {
+    k_dec_front_b<<<dim3(1, 1, B), 32 * G, 0, st>>>(static_cast<const DecFront*>(tab));
+}
+size_t dec_front_size() { return sizeof(DecFront); }
+
 // ---- batched decode: one launch per stage for B sequences (grid.z = sequence;
 // per-sequence parameter tables in device memory) -------------------------------
 __global__ void k_rope_table_b(const PrepParams* __restrict__ ps) { rope_table_body(ps[blockIdx.z]); }

@@ -256,6 +256,11 @@ template <typename T> void launch_select(const SelectParams& p, cudaStream_t st)
 // gx = max scan blocks), 4 LRU (LruParams)
 void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st);
 int64_t decode_batch_lookup_blocks(int64_t U);
+// decode front (one token): prep + eviction in one launch; batched: tab = B x {PrepParams, EvictParams}
+bool dec_front_supported(const PrepParams& p);
+void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t st);
+void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st);
+size_t dec_front_size();
 
 // standalone select (C ABI infllm_select_representatives)
 void launch_select_standalone(const float* scores, const int64_t* lens, int64_t n_units, int64_t unit_len,
