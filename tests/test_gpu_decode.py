@@ -153,3 +153,48 @@ def test_decode_batch_vs_oracle():
     for i, (oe, *_) in enumerate(oengs):
         diffs, repr_bad = compare_state(oe, engs[i])
         assert not diffs and not repr_bad
+
+
+@pytest.mark.parametrize("H,Hkv", [(8, 8), (4, 1), (16, 2), (24, 8)])
+def test_decode_head_layouts(H, Hkv):
+    """K4 + decode front over GQA ratios 1, 3, 4, 8 (MHA-like to 8 query heads
+    per KV group): prefill, then decode steps that cross a unit boundary."""
+    cfg = dict(chunk_size=256, unit_size=128, n_repr=4, local_size=512, init_size=128, n_lookup=4, hot_capacity=6)
+    n_pre, n_dec = 1536, 140
+    q, k, v = gaussian_inputs(80 + H, n_pre + n_dec, H, Hkv, 128, scale=0.3, bf16=True)
+    sched = O.encode_schedule(n_pre, 256, 0) + [1] * n_dec
+    oeng, geng, recs = run_pair(cfg, H, Hkv, 128, q, k, v, sched, decode_tail=n_dec, dtype=torch.bfloat16)
+    _check(oeng, geng, recs)
+
+
+def test_decode_batch_mixed_lengths():
+    """decode_batch over sequences at different stream positions (empty, inside
+    the first window, past several units) in the same batch."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, decode_batch
+
+    seeds, pres = [91, 92, 93], [0, 700, 3000]
+    a, b, data = [], [], []
+    for sd, n_pre in zip(seeds, pres):
+        q, k, v = gaussian_inputs(sd, n_pre + 200, 8, 2, 128, scale=0.3, bf16=True)
+        qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+        for lst in (a, b):
+            e = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(n_heads=8, n_kv_heads=2, head_dim=128),
+                             dtype=torch.bfloat16)
+            if n_pre:
+                e.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
+            lst.append(e)
+        data.append((qt, kt, vt, n_pre))
+    worst = 0.0
+    for t in range(200):
+        q = torch.stack([d[0][d[3] + t] for d in data])
+        k = torch.stack([d[1][d[3] + t] for d in data])
+        v = torch.stack([d[2][d[3] + t] for d in data])
+        got = decode_batch(b, q, k, v)
+        for i, (qt, kt, vt, n_pre) in enumerate(data):
+            s = n_pre + t
+            ref = a[i].decode_step(qt[s:s + 1], kt[s:s + 1], vt[s:s + 1])
+            assert a[i].retrieved_ids() == b[i].retrieved_ids(), (t, i)
+            worst = max(worst, rel_err(got[i].float().cpu().numpy(), ref[0].float().cpu().numpy()))
+    assert worst < 2e-2
+    for ea, eb in zip(a, b):
+        assert ea.metrics() == eb.metrics() and ea.trace() == eb.trace()
