@@ -490,8 +490,6 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
         const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
         st8(static_cast<T*>(p.ring_k) + ro, kv);
         st8(static_cast<T*>(p.ring_krot) + ro, kr);
@@ -2139,9 +2137,7 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
             kr.v[2 * j] = from_f<bf16>(y0);
             kr.v[2 * j + 1] = from_f<bf16>(y1);
         }
-        float kn2 = 0.f;  // as k_prep_tok (the bound is |k|^2 accumulated twice)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
+        float kn2 = 0.f;  // |k|^2, as k_prep_tok
 #pragma unroll
         for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
         const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
