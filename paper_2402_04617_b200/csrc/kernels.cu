@@ -988,6 +988,7 @@ __device__ void block_topk(const double* rel, double* work, int64_t U, int64_t n
 // (multiple of 32) with U <= blockDim * kRadixE.
 constexpr int kRadixE = 8;
 __device__ __forceinline__ uint64_t order_key(double v) {
+    if (v == 0.0) v = 0.0;  // -0.0 == +0.0 for the reference's comparator (memory.hpp:245-252): one key
     const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
