@@ -566,7 +566,15 @@ __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p) {
     if (c >= p.d) return;
     const int64_t stride = static_cast<int64_t>(p.G) * p.d;
     double run = p.P[((p.s % p.R) * p.G + g) * p.d + c];
-    for (int t = 0; t < tile; ++t) run += p.tsum[t * stride + g * p.d + c];
+    // earlier tiles' sums: loads issued together, added in tile order (same rounding)
+    for (int t0 = 0; t0 < tile; t0 += 16) {
+        double ts[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) ts[k] = t0 + k < tile ? p.tsum[(t0 + k) * stride + g * p.d + c] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (t0 + k < tile) run += ts[k];
+    }
     const int64_t i0 = static_cast<int64_t>(tile) * kTokTile;
     const int nt = static_cast<int>(min(static_cast<int64_t>(kTokTile), p.lx - i0));
     double v[kTokTile];
@@ -2006,19 +2014,33 @@ __device__ void select_page(const SelectParams& p, int64_t u, int g, const int* 
     const int64_t rowb = static_cast<int64_t>(128) * p.d * static_cast<int64_t>(sizeof(T)) / 16;  // uint4 per K page
     const uint4* sk = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d);
     uint4* dk = reinterpret_cast<uint4*>(static_cast<T*>(const_cast<void*>(p.unit_k)) + ((u * p.G + g) * 128) * p.d);
-    for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dk[t] = sk[t];
-    if (p.absolute) {
-        const uint4* skr = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_krot) + (g * p.R + slot) * p.d);
-        uint4* dkr = reinterpret_cast<uint4*>(static_cast<T*>(p.unit_krot) + ((u * p.G + g) * 128) * p.d);
-        for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dkr[t] = skr[t];
-    }
     const int64_t vb = static_cast<int64_t>(128) * p.dv * static_cast<int64_t>(sizeof(T)) / 16;
     const T* rv = static_cast<const T*>(p.ring_v);
     T* uv = static_cast<T*>(p.unit_v);
     // both layouts keep a unit's values contiguous: V^T page [dv][128] or rows [128][dv]
     const uint4* sv = reinterpret_cast<const uint4*>(rv + (p.vl.vt ? p.vl.ring(g, slot, 0) : (g * p.R + slot) * p.dv));
     uint4* dv = reinterpret_cast<uint4*>(uv + p.vl.unit(u, g, 0, 0));
-    for (int64_t t = threadIdx.x; t < vb; t += blockDim.x) dv[t] = sv[t];
+    // K and V pages: 8 + 8 independent 16-byte loads in flight per thread, then the stores
+    for (int64_t t0 = 0; t0 < rowb || t0 < vb; t0 += 8 * static_cast<int64_t>(blockDim.x)) {
+        uint4 rk4[8], rv4[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t t = t0 + threadIdx.x + i * static_cast<int64_t>(blockDim.x);
+            if (t < rowb) rk4[i] = sk[t];
+            if (t < vb) rv4[i] = sv[t];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int64_t t = t0 + threadIdx.x + i * static_cast<int64_t>(blockDim.x);
+            if (t < rowb) dk[t] = rk4[i];
+            if (t < vb) dv[t] = rv4[i];
+        }
+    }
+    if (p.absolute) {
+        const uint4* skr = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_krot) + (g * p.R + slot) * p.d);
+        uint4* dkr = reinterpret_cast<uint4*>(static_cast<T*>(p.unit_krot) + ((u * p.G + g) * 128) * p.d);
+        for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dkr[t] = skr[t];
+    }
     // representative rows of this group straight from the ring (memory.hpp:111-123)
     const T* rk = static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d;
     T* rp = static_cast<T*>(p.repr) + ((u * p.G + g) * p.r_k) * p.d;
@@ -2224,18 +2246,7 @@ __global__ void __launch_bounds__(256) k_select_b(const SelectParams* __restrict
     if (blockIdx.x >= p.n_units) return;
     select_body<bf16>(p);
 }
-// relevance scan only (fused == 2 semantics: rel[u] written, no top-k)
-__device__ __forceinline__ int lookup_blocks(int64_t U) {
-    const int64_t want = (U + 7) / 8;
-    return static_cast<int>(want < 148 * 4 ? want : 148 * 4);
-}
-__global__ void __launch_bounds__(256, 2) k_lookup_reg_b(const LookupParams* __restrict__ ps) {
-    const LookupParams& p = ps[blockIdx.z];
-    const int nb = lookup_blocks(p.U);
-    if (static_cast<int>(blockIdx.x) >= nb) return;
-    lookup_reg_body(p, nb);
-}
-// streaming variant: 8 warps x 8 units per block, cp.async ring per warp
+// streaming relevance scan per sequence slice (8 warps, bulk-copy ring per warp); rel[u] only
 __device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 255) / 256); }
 __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* __restrict__ ps) {
     const LookupParams& p = ps[blockIdx.z];
@@ -2268,18 +2279,13 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             break;
         case 3: {  // relevance scan + exact top-k (rel desc, id asc)
             const LookupParams* ps = static_cast<const LookupParams*>(tab);
-            static const bool use_reg = getenv("INFLLM_BATCH_LOOKUP_REG") != nullptr;  // A/B experiments only
-            if (use_reg) {
-                k_lookup_reg_b<<<dim3(static_cast<unsigned>(gx & 0xffffffff), 1, B), 256, 0, st>>>(ps);
-            } else {
-                const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
-                static bool attr = false;
-                if (!attr) {
-                    cudaFuncSetAttribute(k_lookup_stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-                    attr = true;
-                }
-                k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
+            const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_lookup_stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                attr = true;
             }
+            k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
             k_topk_b<<<B, 1024, 0, st>>>(ps);
             break;
         }
