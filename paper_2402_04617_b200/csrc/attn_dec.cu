@@ -152,6 +152,8 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) tc::mbar_init(&s_bar[i], 1);
         tc::fence_barrier_init();
+        // the maps are rewritten in place when a buffer of the layer moves
+        for (int i = 0; i < 6; ++i) tc::acquire_tmap(static_cast<const CUtensorMap*>(a.dec_maps) + i);
     }
     __syncthreads();
     const int g = blockIdx.y, rep = a.rep;
@@ -460,9 +462,12 @@ void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st
 
 void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,
                            cudaStream_t st) {
+    static const int dbg = getenv("INFLLM_DEC_DBG") ? atoi(getenv("INFLLM_DEC_DBG")) : 0;
+    DecScratch s2 = sc;
+    s2.dbg = dbg;
     const int ns = pick_splits(max_tiles, G, B);
     cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
-    k_attn_decb<<<dim3(ns, G, B), kThr, kDecSmem, st>>>(dev_params, sc);
+    k_attn_decb<<<dim3(ns, G, B), kThr, kDecSmem, st>>>(dev_params, s2);
 }
 
 }  // namespace infllm

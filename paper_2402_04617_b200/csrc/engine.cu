@@ -336,6 +336,7 @@ struct infllm_engine {
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
         DBuf dec_maps;  // K4 TMA tensor maps (6), re-encoded when a buffer moves
         std::vector<const void*> dec_maps_key;
+        std::vector<uint8_t> dec_maps_host;  // what was written (INFLLM_BATCH_SYNC checks)
         // host tier (tier_slots > 0): unit pages in mapped pinned host memory,
         // the attention reads them from tier_slots device cache slots
         HBuf host_k, host_krot, host_v;
@@ -392,8 +393,20 @@ struct infllm_engine {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, lookup_ev;
         int64_t replays_in_window = 0;
         int64_t steps = 0;
+        std::vector<const void*> bufs;  // device addresses baked into the graph (buf_snapshot)
     };
     std::vector<GraphEntry> graphs;
+    static void drop_graph(GraphEntry& g) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        for (auto* evs : {&g.attn_ev, &g.lookup_ev})
+            for (auto& p : *evs) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
+        g.attn_ev.clear();
+        g.lookup_ev.clear();
+    }
     cudaStream_t cap_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
     bool use_graphs = true;
     int64_t tier_slots = 0;  // host tier: GPU unit-cache slots (0: unit pages resident in HBM)
@@ -429,6 +442,45 @@ struct infllm_engine {
     size_t unit_elems_k() const { return static_cast<size_t>(Gs) * cfg.unit_size * d; }
     size_t unit_elems_v() const { return static_cast<size_t>(Gs) * cfg.unit_size * dv; }
 
+    // every device buffer the engine owns (a captured step graph holds their addresses)
+    std::vector<DBuf*> dev_buffers() {
+        std::vector<DBuf*> v{&qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
+                             &tsum, &topk_done, &evict_done, &dec_part, &dec_mass, &dec_cnt};
+        for (int b = 0; b < kNB; ++b)
+            for (auto* x : {&stage_q[b], &stage_k[b], &stage_v[b], &stage_o[b]}) v.push_back(x);
+        for (auto& L : layers)
+            for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
+                            &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
+                            &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
+                            &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
+                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps})
+                v.push_back(b);
+        return v;
+    }
+    std::vector<const void*> buf_snapshot() {
+        std::vector<const void*> r;
+        for (auto* b : dev_buffers()) r.push_back(b->p);
+        for (auto& L : layers)
+            for (const void* h : {L.dhost_k, L.dhost_krot, L.dhost_v}) r.push_back(h);
+        return r;
+    }
+    // INFLLM_BATCH_SYNC: the K4 tensor maps in device memory still hold what was written
+    void dbg_maps(const char* where) {
+        static const bool on = std::getenv("INFLLM_BATCH_SYNC") != nullptr;
+        if (!on) return;
+        ck(cudaDeviceSynchronize(), where);
+        for (auto& L : layers) {
+            if (!L.dec_maps.p || L.dec_maps_host.empty()) continue;
+            std::vector<uint8_t> d(L.dec_maps_host.size());
+            ck(cudaMemcpy(d.data(), L.dec_maps.p, d.size(), cudaMemcpyDeviceToHost), "dbg maps");
+            for (size_t i = 0; i < d.size(); ++i)
+                if (d[i] != L.dec_maps_host[i]) {
+                    std::fprintf(stderr, "dbg maps of engine %p changed at %s: byte %zu (map %zu) %02x -> %02x, maps at %p\n",
+                                 static_cast<void*>(this), where, i, i / 128, L.dec_maps_host[i], d[i], L.dec_maps.p);
+                    break;
+                }
+        }
+    }
     void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.unit_cap) return;
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
@@ -955,9 +1007,12 @@ struct infllm_engine {
                 alignas(64) CUtensorMap hm[6];
                 dec_encode_maps(ap, urows, hm);
                 if (!L.dec_maps.p) L.dec_maps.alloc(sizeof(hm), st, false);
+                if (reinterpret_cast<uintptr_t>(L.dec_maps.p) % 128)
+                    throw StreamError("K4 tensor maps: device buffer not 128-byte aligned");
                 ck(cudaMemcpyAsync(L.dec_maps.p, hm, sizeof(hm), cudaMemcpyHostToDevice, st), "tensor maps H2D");
                 ck(cudaStreamSynchronize(st), "tensor maps");  // hm is a stack buffer
                 L.dec_maps_key = key;
+                L.dec_maps_host.assign(reinterpret_cast<const uint8_t*>(hm), reinterpret_cast<const uint8_t*>(hm) + sizeof(hm));
             }
             ap.dec_maps = L.dec_maps.p;
         }
@@ -1164,6 +1219,7 @@ struct infllm_engine {
         if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
         if (n < 1) throw StreamError("encode_stream: empty stream");
         Layer& L = layers[static_cast<size_t>(li)];
+        dbg_maps("encode_stream begin");
         if (!cap_stream) {
             ck(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking), "stream");
@@ -1190,6 +1246,15 @@ struct infllm_engine {
             return;
         }
         const HostState cur = save(L);
+        // a graph whose buffers have moved since its capture (pool growth, decode
+        // scratch, ...) would replay into freed memory: drop it
+        const std::vector<const void*> bufs = buf_snapshot();
+        for (size_t i = graphs.size(); i-- > 0;)
+            if (graphs[i].bufs != bufs) {
+                ck(cudaStreamSynchronize(st), "graph drop");
+                drop_graph(graphs[i]);
+                graphs.erase(graphs.begin() + static_cast<std::ptrdiff_t>(i));
+            }
         GraphEntry* ge = nullptr;
         for (auto& g : graphs)
             if (g.layer == li && g.q == q && g.k == k && g.v == v && g.out == out && g.n == n && g.host == host &&
@@ -1207,6 +1272,7 @@ struct infllm_engine {
             g.host = host;
             g.prof = prof;
             g.before = cur;
+            g.bufs = bufs;
             const int64_t l0 = launches;
             cudaGraph_t graph = nullptr;
             capturing = true;
@@ -1454,14 +1520,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         if (!e) return;
         cudaDeviceSynchronize();
         cudaStream_t st = nullptr;
-        for (auto* b : {&e->qa, &e->qc, &e->chunk_qsum, &e->mass_e, &e->mass_m, &e->row_m, &e->row_l, &e->mass_cta, &e->rtab, &e->qsb, &e->tsum, &e->topk_done, &e->evict_done, &e->dec_part, &e->dec_mass, &e->dec_cnt}) b->release(st);
-        for (auto& L : e->layers)
-            for (auto* b : {&L.ring_k, &L.ring_krot, &L.ring_v, &L.P, &L.init_k, &L.init_krot, &L.init_v, &L.unit_k,
-                            &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
-                            &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
-                            &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
-                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps})
-                b->release(st);
+        for (auto* b : e->dev_buffers()) b->release(st);
         for (auto& L : e->layers)
             for (auto* h : {&L.host_k, &L.host_krot, &L.host_v}) h->release();
         for (auto& p : e->ev_attn) {
@@ -1473,19 +1532,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
             cudaEventDestroy(p.second);
         }
         for (auto ev : e->ev_pool) cudaEventDestroy(ev);
-        for (auto& g : e->graphs) {
-            if (g.exec) cudaGraphExecDestroy(g.exec);
-            for (auto& p : g.attn_ev) {
-                cudaEventDestroy(p.first);
-                cudaEventDestroy(p.second);
-            }
-            for (auto& p : g.lookup_ev) {
-                cudaEventDestroy(p.first);
-                cudaEventDestroy(p.second);
-            }
-        }
-        for (int b = 0; b < infllm_engine::kNB; ++b)
-            for (auto* x : {&e->stage_q[b], &e->stage_k[b], &e->stage_v[b], &e->stage_o[b]}) x->release(nullptr);
+        for (auto& g : e->graphs) infllm_engine::drop_graph(g);
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
                         e->evict_stream, e->tier_stream})
             if (s2) cudaStreamDestroy(s2);
@@ -1529,6 +1576,7 @@ int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
 int infllm_engine_reset(infllm_engine_t e, void* stream) {
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
+        e->dbg_maps("reset begin");
         e->join_side(st);
         for (auto& L : e->layers) {
             L.n_fed = L.step = L.local_start = L.init_len = 0;
@@ -1554,6 +1602,7 @@ int infllm_engine_reset(infllm_engine_t e, void* stream) {
             }
         }
         ck(cudaGetLastError(), "reset");
+        e->dbg_maps("reset end");
     });
 }
 
@@ -1586,8 +1635,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
                 for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream})
                     ck(cudaStreamCreateWithFlags(s2, cudaStreamNonBlocking), "stream");
             }
-            for (auto& g : e->graphs)  // captured graphs name the old streams' work: recapture
-                if (g.exec) cudaGraphExecDestroy(g.exec);
+            for (auto& g : e->graphs) infllm_engine::drop_graph(g);  // they name the old streams' work: recapture
             e->graphs.clear();
             e->lru_seq[0] = e->lru_seq[1] = -1;
             for (auto& a2 : e->attn_seq) a2 = -1;
@@ -1731,6 +1779,13 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         lk_max = lk_reg | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
+        // INFLLM_BATCH_SYNC: synchronise after every stage (fault isolation only)
+        static const bool dsync = std::getenv("INFLLM_BATCH_SYNC") != nullptr;
+        auto chk = [&](const char* what) {
+            if (dsync) ck(cudaStreamSynchronize(st), what);
+        };
+        chk("decode_batch tables");
+        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("decode_batch begin");
         if (!c.front.empty())
             launch_dec_front_batch(dt + o_front, n, G, st);
         else
@@ -1739,10 +1794,34 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
         if (!c.select.empty())
             launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
+        chk("decode_batch front/evict/select");
+        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after front/evict/select");
         if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
+        chk("decode_batch lookup");
+        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lookup");
+        if (dsync) {  // fault isolation: the attention's inputs, checked on the host
+            for (size_t i = 0; i < c.attn.size(); ++i) {
+                const AttnParams& ap = c.attn[i];
+                std::vector<int64_t> sel(ap.n_sel);
+                if (ap.n_sel) ck(cudaMemcpy(sel.data(), ap.sel, ap.n_sel * sizeof(int64_t), cudaMemcpyDeviceToHost), "dbg sel");
+                alignas(64) CUtensorMap dm[6], hm[6];
+                ck(cudaMemcpy(dm, ap.dec_maps, sizeof(dm), cudaMemcpyDeviceToHost), "dbg maps");
+                dec_encode_maps(ap, ap.unit_cap * static_cast<int64_t>(ap.G) * 128, hm);
+                int64_t lo = INT64_MAX, hi = INT64_MIN;
+                for (auto x : sel) lo = std::min(lo, x), hi = std::max(hi, x);
+                std::fprintf(stderr, "dbg seq %zu: n_sel %d sel [%lld, %lld] unit_cap %lld s %lld init %lld local %lld tiles %lld maps %p same %d\n",
+                             i, ap.n_sel, (long long)lo, (long long)hi, (long long)ap.unit_cap, (long long)ap.s,
+                             (long long)ap.init_len, (long long)ap.local_start, (long long)dec_max_tiles(ap), ap.dec_maps,
+                             std::memcmp(dm, hm, sizeof(dm)) == 0);
+            }
+        }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0}, st);
+        chk("decode_batch attention");
+        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after attention");
         launch_decode_batch_stage(4, dt + o_lru, n, 0, st);
+        chk("decode_batch lru");
+        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lru");
         ck(cudaGetLastError(), "decode_batch launch");
         ck(cudaEventRecord(bc.done[s], st), "record");
     });
@@ -1757,6 +1836,7 @@ int infllm_encode_stream(infllm_engine_t e, int32_t layer, const void* q, const 
             e->encode_stream<bf16>(layer, q, k, v, n_tokens, out, st, false);
         else
             e->encode_stream<float>(layer, q, k, v, n_tokens, out, st, false);
+        e->dbg_maps("encode_stream end");
     });
 }
 

@@ -198,3 +198,45 @@ def test_decode_batch_mixed_lengths():
     assert worst < 2e-2
     for ea, eb in zip(a, b):
         assert ea.metrics() == eb.metrics() and ea.trace() == eb.trace()
+
+
+def test_graph_recaptured_after_buffers_move():
+    """encode_stream replays a captured graph when the stream state repeats
+    (after reset). Decode steps past the reserved trace grow (move) buffers the
+    graph baked in; the replay must not write into the freed memory: the
+    second prefill matches the first bit for bit (outputs, trace), and a
+    batched decode over engines that went through this runs clean."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, decode_batch
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=2048, init_size=128, n_lookup=16, hot_capacity=32)
+    n_pre, n_dec = 8192, 200
+    q, k, v = gaussian_inputs(53, n_pre + n_dec, 32, 8, 128, scale=0.3, bf16=True)
+    qt, kt, vt = [torch.from_numpy(x).cuda().bfloat16() for x in (q, k, v)]
+    engs = [StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128),
+                         dtype=torch.bfloat16) for _ in range(3)]
+    try:
+        for e in engs:
+            e.reserve(n_pre + 1)  # the decode tail grows the trace / unit pool past this
+        e0 = engs[0]
+        ob0 = torch.empty((n_pre, 32, 128), device="cuda", dtype=torch.bfloat16)  # same pointers: graph cache hit
+        out1 = e0.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre], out=ob0).clone()
+        tr1 = e0.trace()
+        for t in range(n_pre, n_pre + n_dec):
+            e0.decode_step(qt[t:t + 1], kt[t:t + 1], vt[t:t + 1])
+        torch.cuda.synchronize()
+        e0.reset()
+        out2 = e0.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre], out=ob0).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(out1, out2)
+        assert e0.trace() == tr1
+        for e in engs[1:]:
+            e.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
+        ob = torch.empty((3, 32, 128), device="cuda", dtype=torch.bfloat16)
+        for t in range(n_pre, n_pre + 16):
+            decode_batch(engs, qt[t].expand(3, 32, 128).contiguous(), kt[t].expand(3, 8, 128).contiguous(),
+                         vt[t].expand(3, 8, 128).contiguous(), out=ob)
+        torch.cuda.synchronize()
+        assert torch.equal(ob[0], ob[1]) and torch.equal(ob[1], ob[2])
+    finally:
+        for e in engs:
+            e.close()
