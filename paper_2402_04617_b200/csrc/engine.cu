@@ -396,6 +396,7 @@ struct infllm_engine {
         std::vector<const void*> bufs;  // device addresses baked into the graph (buf_snapshot)
     };
     std::vector<GraphEntry> graphs;
+    static constexpr size_t kMaxGraphs = 8;
     static void drop_graph(GraphEntry& g) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g.exec = nullptr;
@@ -1307,6 +1308,11 @@ struct infllm_engine {
             g.launches = launches - l0;
             launches = l0;
             restore(L, cur);
+            if (graphs.size() >= kMaxGraphs) {  // bounded cache: the oldest capture goes
+                ck(cudaStreamSynchronize(st), "graph drop");
+                drop_graph(graphs.front());
+                graphs.erase(graphs.begin());
+            }
             graphs.push_back(std::move(g));
             ge = &graphs.back();
         }
