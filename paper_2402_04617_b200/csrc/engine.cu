@@ -1777,13 +1777,12 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         int64_t ev_max = 0, sel_max = 0, lk_max = 0, tiles_max = 0;
         for (auto& ep : c.evict) ev_max = std::max<int64_t>(ev_max, ep.n_init + ep.n_evict);
         for (auto& sp : c.select) sel_max = std::max<int64_t>(sel_max, sp.n_units);
-        int64_t lk_reg = 0, lk_str = 0;
+        int64_t lk_units = 0, lk_str = 0;  // all sequences' units | per-sequence scan blocks << 32
         for (auto& lp : c.lookup) {
-            const int64_t bl = decode_batch_lookup_blocks(lp.U);
-            lk_reg = std::max<int64_t>(lk_reg, bl & 0xffffffff);
-            lk_str = std::max<int64_t>(lk_str, bl >> 32);
+            lk_units += lp.U;
+            lk_str = std::max<int64_t>(lk_str, decode_batch_lookup_blocks(lp.U) >> 32);
         }
-        lk_max = lk_reg | (lk_str << 32);
+        lk_max = std::min<int64_t>(lk_units, 0xffffffff) | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
         // INFLLM_BATCH_SYNC: synchronise after every stage (fault isolation only)
         static const bool dsync = std::getenv("INFLLM_BATCH_SYNC") != nullptr;

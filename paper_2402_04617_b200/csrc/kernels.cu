@@ -2254,6 +2254,100 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* 
     if (static_cast<int>(blockIdx.x) >= nb) return;
     lookup_stream_body(p, nb);
 }
+// balanced variant: one block per SM over the concatenated unit ranges of all
+// sequences (contiguous share per block, warps strided inside it), so a batch
+// of long indices has no partial last wave; same per-unit arithmetic and order
+// as lookup_stream_body (bit-identical rel[u]).
+constexpr int kScanMaxB = 256;
+__global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams* __restrict__ ps, int B) {
+    extern __shared__ __align__(16) uint8_t scan_smem[];
+    __shared__ int64_t s_off[kScanMaxB + 1];
+    __shared__ const uint8_t* s_repr[kScanMaxB];
+    __shared__ const double* s_q[kScanMaxB];
+    __shared__ double* s_rel[kScanMaxB];
+    __shared__ __align__(8) uint64_t sbar[8][kScanStages];
+    const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        s_repr[b] = static_cast<const uint8_t*>(ps[b].repr);
+        s_q[b] = ps[b].qsum;
+        s_rel[b] = ps[b].rel;
+    }
+    if (threadIdx.x == 0) {
+        int64_t o = 0;
+        for (int b = 0; b < B; ++b) {
+            s_off[b] = o;
+            o += ps[b].U;
+        }
+        s_off[B] = o;
+    }
+    const int G = ps[0].G;
+    if (lane == 0)
+        for (int st = 0; st < kScanStages; ++st) tc::mbar_init(&sbar[wib][st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const int64_t total = s_off[B];
+    const int64_t S = (total + gridDim.x - 1) / gridDim.x;
+    const int64_t s0 = static_cast<int64_t>(blockIdx.x) * S, s1 = s0 + S < total ? s0 + S : total;
+    const int64_t nwarps = blockDim.x / 32;
+    const int64_t bytes_u = static_cast<int64_t>(G) * 512 * 2;
+    uint8_t* ring = scan_smem + static_cast<size_t>(wib) * kScanStages * 8192;
+    int ib = 0, cb = -1;  // sequence cursors of the issue side and the compute side (t only grows)
+    auto seq_of = [&](int64_t t, int& c) {
+        while (c + 1 < B && t >= s_off[c + 1]) ++c;
+        return c;
+    };
+    auto issue = [&](int64_t t, int stage) {
+        if (t < s1 && lane == 0) {
+            const int b = seq_of(t, ib);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc::mbar_expect_tx(&sbar[wib][stage], static_cast<uint32_t>(bytes_u));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             tc::smem_u32(ring + stage * 8192)),
+                         "l"(s_repr[b] + (t - s_off[b]) * bytes_u), "r"(static_cast<uint32_t>(bytes_u)),
+                         "r"(tc::smem_u32(&sbar[wib][stage]))
+                         : "memory");
+        }
+    };
+    const int64_t warp0 = s0 + wib;
+#pragma unroll
+    for (int st = 0; st < kScanStages - 1; ++st) issue(warp0 + st * nwarps, st);
+    double q[8][4];
+    int stage = 0;
+    int64_t it = 0;
+    for (int64_t t = warp0; t < s1; t += nwarps, ++it) {
+        issue(t + (kScanStages - 1) * nwarps, (stage + kScanStages - 1) % kScanStages);
+        int b = cb;
+        if (b < 0 || t >= s_off[b + 1]) {  // first unit of a sequence for this warp: its query sums
+            if (cb < 0) cb = 0;
+            b = seq_of(t, cb);
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) q[g][j] = g < G ? s_q[b][g * 128 + 4 * lane + j] : 0.0;
+        }
+        tc::mbar_wait(&sbar[wib][stage], static_cast<uint32_t>((it / kScanStages) & 1));
+        const uint8_t* buf = ring + stage * 8192 + 8 * lane;
+        double rel = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= G) break;
+            double a = 0.0;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const uint2 v = *reinterpret_cast<const uint2*>(buf + (4 * g + r) * 256);
+                a = fma(q[g][0], static_cast<double>(__uint_as_float(v.x << 16)), a);
+                a = fma(q[g][1], static_cast<double>(__uint_as_float(v.x & 0xffff0000u)), a);
+                a = fma(q[g][2], static_cast<double>(__uint_as_float(v.y << 16)), a);
+                a = fma(q[g][3], static_cast<double>(__uint_as_float(v.y & 0xffff0000u)), a);
+            }
+            rel += a;
+        }
+        rel = warp_sum_d(rel);
+        if (lane == 0) s_rel[b][t - s_off[b]] = rel;
+        __syncwarp();  // the stage is refilled next iteration
+        stage = (stage + 1) % kScanStages;
+    }
+}
 __global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
     const LookupParams& p = ps[blockIdx.x];
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
@@ -2285,7 +2379,21 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
                 cudaFuncSetAttribute(k_lookup_stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
                 attr = true;
             }
-            k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
+            static const bool per_seq = getenv("INFLLM_BATCH_SCAN_PERSEQ") != nullptr;  // A/B experiments
+            if (!per_seq && B <= kScanMaxB) {
+                static bool attr2 = false;
+                if (!attr2) {
+                    cudaFuncSetAttribute(k_lookup_stream_bal, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+                    attr2 = true;
+                }
+                // one block per SM (fewer when the batch's units are few: >= 64 units per block)
+                const int64_t units = (gx & 0xffffffff);
+                const unsigned nb = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(148, units / 64)));
+                k_lookup_stream_bal<<<nb, 256, smem, st>>>(ps, B);
+            } else {
+                k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
+            }
             k_topk_b<<<B, 1024, 0, st>>>(ps);
             break;
         }
@@ -2296,8 +2404,7 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             break;
     }
 }
-int64_t decode_batch_lookup_blocks(int64_t U) {  // reg-scan blocks | stream-scan blocks << 32
-    const int64_t want = (U + 7) / 8;
-    return (want < 148 * 4 ? want : 148 * 4) | (((U + 255) / 256) << 32);
+int64_t decode_batch_lookup_blocks(int64_t U) {  // per-sequence stream-scan blocks << 32
+    return ((U + 255) / 256) << 32;
 }
 }  // namespace infllm
