@@ -144,10 +144,20 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
 
     const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
     const int gq = lane >> 2, tq = lane & 3;  // mma fragment row (query head) / column pair
-    for (int u = tid; u < a.n_sel; u += kThr) {  // the retrieved units' pages and lengths
-        const int64_t id = a.sel[u];
-        s_page[u] = a.sel_slot ? a.sel_slot[u] : static_cast<int32_t>(id);
-        s_len[u] = a.unit_len[id];
+    int n_init;
+    int64_t near0;
+    const int T = dec_tiles(a, n_init, near0);
+    const int tps = (T + nsplit - 1) / nsplit;
+    const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
+    if (t0 < n_init + a.n_sel && t1 > n_init) {
+        // this split attends retrieved units: wait for the lookup grid when launched
+        // as its programmatic dependent (no-op otherwise)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int u = tid; u < a.n_sel; u += kThr) {  // the retrieved units' pages and lengths
+            const int64_t id = a.sel[u];
+            s_page[u] = a.sel_slot ? a.sel_slot[u] : static_cast<int32_t>(id);
+            s_len[u] = a.unit_len[id];
+        }
     }
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) tc::mbar_init(&s_bar[i], 1);
@@ -159,12 +169,6 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int g = blockIdx.y, rep = a.rep;
     const float sl2 = a.scale * kLog2e;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));  // 1024-aligned
-
-    int n_init;
-    int64_t near0;
-    const int T = dec_tiles(a, n_init, near0);
-    const int tps = (T + nsplit - 1) / nsplit;
-    const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
 
     for (int st = 0; st < kStages - 1; ++st)  // prefetch the first tiles
         if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, dsm + st * kStageB, &s_bar[st]);
@@ -457,7 +461,19 @@ void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st
         cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
         attr = true;
     }
-    k_attn_dec1<<<dim3(ns, a.G, 1), kThr, kDecSmem, st>>>(a, sc);
+    // programmatic dependent launch after the lookup (INFLLM_DEC_PDL=0: plain launch)
+    static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ns, a.G, 1);
+    cfg.blockDim = dim3(kThr);
+    cfg.dynamicSmemBytes = kDecSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_attn_dec1, a, sc);
 }
 
 void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,

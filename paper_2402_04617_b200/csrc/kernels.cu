@@ -781,7 +781,12 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
     if (threadIdx.x == 0) *p.done = 0;
 }
-__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) { lookup_reg_body(p, gridDim.x); }
+__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
+    // a decode step's K4 may start its CTAs that do not read the selection now
+    // (programmatic dependent launch; those that do wait for this grid)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    lookup_reg_body(p, gridDim.x);
+}
 
 // Large indices: the same math fed by cp.async (16-byte LDGSTS) into a
 // 3-deep per-warp shared-memory ring, so each warp keeps the next two units
