@@ -1149,9 +1149,16 @@ __global__ void __launch_bounds__(256) k_topk_local(const double* rel, int64_t U
         cand_i[blockIdx.x * k + r] = ok ? s0 + loc[r] : -1;
     }
 }
-__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) { lookup_stream_body(p, gridDim.x); }
+__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge block may launch (PDL)
+    lookup_stream_body(p, gridDim.x);
+}
 __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const int64_t* cand_i, int64_t n, int64_t k,
                                                      int64_t* sel) {
+    // as a programmatic dependent of the scan: let a decode step's K4 launch,
+    // then wait for the scan's candidates (both no-ops on a plain launch)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ int64_t loc[kTopkMaxSel];
     block_topk_radix(cand_v, n, k, loc);
     __syncthreads();
@@ -1177,9 +1184,20 @@ void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t*
         p.cand_v = p.n_sel > 0 ? cand_v : nullptr;
         p.cand_i = p.n_sel > 0 ? cand_i : nullptr;
         k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p);
-        if (p.n_sel > 0)
-            k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, static_cast<int64_t>(kScanBlocks) * p.n_sel, p.n_sel,
-                                             p.sel);
+        if (p.n_sel > 0) {
+            static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(1);
+            cfg.blockDim = dim3(1024);
+            cfg.stream = st;
+            cudaLaunchAttribute la[1];
+            la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            la[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = la;
+            cfg.numAttrs = pdl ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, k_topk_final, static_cast<const double*>(cand_v), static_cast<const int64_t*>(cand_i),
+                               static_cast<int64_t>(kScanBlocks) * p.n_sel, p.n_sel, p.sel);
+        }
         return;
     }
     p.cand_v = nullptr;
