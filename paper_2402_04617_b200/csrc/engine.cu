@@ -247,6 +247,13 @@ struct DecodeCollector {
     std::vector<LruParams> lru;
 };
 
+// an event shared by the engines of a batch (the last batched LRU they joined)
+struct SharedEvent {
+    cudaEvent_t ev = nullptr;
+    ~SharedEvent() {
+        if (ev) cudaEventDestroy(ev);
+    }
+};
 // device/host resources of batched decode calls (owned by the batch's first engine)
 struct BatchCtx {
     static constexpr int kSlots = 2;
@@ -257,12 +264,28 @@ struct BatchCtx {
     int slot = 0;
     DBuf part, mass, cnt;  // K4 batch scratch
     int part_B = 0, mass_B = 0;
+    // the LRU stage runs on its own stream, overlapping the next call's front,
+    // eviction and selection; the next call's lookup waits for it (it rewrites
+    // the selection buffers the LRU reads)
+    cudaStream_t lru_st = nullptr;
+    cudaEvent_t ev_k4 = nullptr;
+    std::shared_ptr<SharedEvent> lru_ev;
+    bool lru_pending = false;
 };
 
 struct infllm_engine {
     infllm_engine_config cfg{};
     DecodeCollector* coll = nullptr;  // decode_batch: record kernel parameters instead of launching
     std::unique_ptr<BatchCtx> bctx;
+    std::shared_ptr<SharedEvent> ext_dep;  // a batched LRU on another stream that touched this engine
+    void join_ext(cudaStream_t st) {       // order `st` after it (engine calls outside a batch)
+        if (!ext_dep) return;
+        ck(cudaStreamWaitEvent(st, ext_dep->ev, 0), "wait");
+        ext_dep.reset();
+    }
+    void sync_ext() {  // before pool growth (buffers the LRU may still read or write)
+        if (ext_dep) ck(cudaEventSynchronize(ext_dep->ev), "sync");
+    }
     int H = 1, Gt = 1, rep = 1, d = 0, dv = 0, n_layers = 1;
     int g0 = 0, Gs = 1, Hs = 1;  // shard
     int dtype = INFLLM_DTYPE_F32;
@@ -484,6 +507,7 @@ struct infllm_engine {
     }
     void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.unit_cap) return;
+        sync_ext();
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
@@ -539,6 +563,7 @@ struct infllm_engine {
 
     void ensure_trace(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.trace_cap) return;
+        sync_ext();
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
@@ -630,6 +655,7 @@ struct infllm_engine {
         if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
         if (lx < 1) throw StreamError("step: empty batch");
         if (!decode && lx > cfg.chunk_size) throw StreamError("encode_chunk: batch exceeds chunk_size");
+        if (!coll) join_ext(st);
         Layer& L = layers[static_cast<size_t>(li)];
         const bool lookup_enabled = decode ? cfg.lookup_mode != INFLLM_LOOKUP_NONE
                                            : cfg.lookup_mode == INFLLM_LOOKUP_ENCODE_AND_DECODE;
@@ -1221,6 +1247,7 @@ struct infllm_engine {
         if (n < 1) throw StreamError("encode_stream: empty stream");
         Layer& L = layers[static_cast<size_t>(li)];
         dbg_maps("encode_stream begin");
+        join_ext(st);
         if (!cap_stream) {
             ck(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "stream");
             ck(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking), "stream");
@@ -1554,6 +1581,8 @@ int infllm_engine_destroy(infllm_engine_t e) {
                 if (e->bctx->done[t]) cudaEventDestroy(e->bctx->done[t]);
             }
             for (auto* b : {&e->bctx->part, &e->bctx->mass, &e->bctx->cnt}) b->release(nullptr);
+            if (e->bctx->lru_st) cudaStreamDestroy(e->bctx->lru_st);
+            if (e->bctx->ev_k4) cudaEventDestroy(e->bctx->ev_k4);
         }
         delete e;
     });
@@ -1569,6 +1598,7 @@ int infllm_engine_set_allgather(infllm_engine_t e, infllm_allgather_fn fn, void*
 int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
     return guard([&] {
         cudaStream_t st = nullptr;
+        e->sync_ext();
         const int64_t units = std::max<int64_t>(0, max_tokens - e->cfg.init_size) / e->cfg.unit_size + 2;
         for (auto& L : e->layers) {
             e->ensure_units(L, units, st);
@@ -1583,6 +1613,7 @@ int infllm_engine_reset(infllm_engine_t e, void* stream) {
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
         e->dbg_maps("reset begin");
+        e->join_ext(st);
         e->join_side(st);
         for (auto& L : e->layers) {
             L.n_fed = L.step = L.local_start = L.init_len = 0;
@@ -1720,6 +1751,8 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             }
             return;
         }
+        for (int32_t i = 0; i < n; ++i)  // an LRU of another batch context still touching this engine
+            if (engs[i]->ext_dep && (!e0->bctx || engs[i]->ext_dep != e0->bctx->lru_ev)) engs[i]->join_ext(st);
         DecodeCollector c;
         for (int32_t i = 0; i < n; ++i) {
             engs[i]->coll = &c;
@@ -1801,6 +1834,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
         chk("decode_batch front/evict/select");
         for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after front/evict/select");
+        if (bc.lru_pending) ck(cudaStreamWaitEvent(st, bc.lru_ev->ev, 0), "wait");  // the previous call's LRU
         if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
         chk("decode_batch lookup");
         for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lookup");
@@ -1824,11 +1858,29 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0}, st);
         chk("decode_batch attention");
         for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after attention");
-        launch_decode_batch_stage(4, dt + o_lru, n, 0, st);
-        chk("decode_batch lru");
+        static const bool lru_inline = std::getenv("INFLLM_BATCH_LRU_INLINE") != nullptr;  // A/B experiments
+        cudaStream_t lst = st;
+        if (!lru_inline) {
+            if (!bc.lru_st) {
+                ck(cudaStreamCreateWithFlags(&bc.lru_st, cudaStreamNonBlocking), "stream");
+                ck(cudaEventCreateWithFlags(&bc.ev_k4, cudaEventDisableTiming), "event");
+                bc.lru_ev = std::make_shared<SharedEvent>();
+                ck(cudaEventCreateWithFlags(&bc.lru_ev->ev, cudaEventDisableTiming), "event");
+            }
+            ck(cudaEventRecord(bc.ev_k4, st), "record");
+            ck(cudaStreamWaitEvent(bc.lru_st, bc.ev_k4, 0), "wait");
+            lst = bc.lru_st;
+        }
+        launch_decode_batch_stage(4, dt + o_lru, n, 0, lst);
+        if (dsync) ck(cudaStreamSynchronize(lst), "decode_batch lru");
         for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lru");
         ck(cudaGetLastError(), "decode_batch launch");
-        ck(cudaEventRecord(bc.done[s], st), "record");
+        if (lst != st) {
+            ck(cudaEventRecord(bc.lru_ev->ev, lst), "record");
+            bc.lru_pending = true;
+            for (int32_t i = 0; i < n; ++i) engs[i]->ext_dep = bc.lru_ev;
+        }
+        ck(cudaEventRecord(bc.done[s], lst), "record");  // lst follows everything of this call
     });
 }
 
@@ -1860,6 +1912,7 @@ int infllm_encode_stream_host(infllm_engine_t e, int32_t layer, const void* host
 int infllm_finish(infllm_engine_t e, void* stream) {
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
+        e->join_ext(st);
         if (e->dtype == INFLLM_DTYPE_BF16)
             e->finish<bf16>(st);
         else
