@@ -472,7 +472,7 @@ void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = pdl && sc.pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_attn_dec1, a, sc);
 }
 
@@ -483,7 +483,19 @@ void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t m
     s2.dbg = dbg;
     const int ns = pick_splits(max_tiles, G, B);
     cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
-    k_attn_decb<<<dim3(ns, G, B), kThr, kDecSmem, st>>>(dev_params, s2);
+    // programmatic dependent of the top-k: splits without retrieved units start early
+    static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ns, G, B);
+    cfg.blockDim = dim3(kThr);
+    cfg.dynamicSmemBytes = kDecSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = pdl && sc.pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k_attn_decb, dev_params, s2);
 }
 
 }  // namespace infllm

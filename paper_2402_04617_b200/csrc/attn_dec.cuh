@@ -19,6 +19,8 @@ struct DecScratch {
     unsigned* cnt;  // [B][G]
     int max_sel;
     int dbg;  // timing experiments only: bit0 skip tiles, bit1 skip merge
+    int pdl;  // 1: the kernel right before K4 on its stream is the lookup (or its top-k), whose
+              // inputs were complete before it started: K4 may launch as its programmatic dependent
 };
 inline size_t dec_part_floats(int B, int G, int rep) {
     return static_cast<size_t>(B) * G * kDecMaxSplits * rep * 130;

@@ -574,7 +574,7 @@ struct infllm_engine {
 
     DecScratch dec_scratch() const {
         return DecScratch{dec_part.as<float>(), dec_mass.as<float>(), dec_cnt.as<unsigned>(),
-                          static_cast<int>(std::max<int64_t>(cfg.n_lookup, 1)), 0};
+                          static_cast<int>(std::max<int64_t>(cfg.n_lookup, 1)), 0, 0};
     }
 
     // where unit pages are written (HBM pool, or the host tier)
@@ -885,6 +885,7 @@ struct infllm_engine {
 
 
         // K1 + K2: lookup (memory.hpp:239-269)
+        bool k4_pdl = false;  // the lookup is the last kernel before K4 on the caller's stream
         if (do_lookup) {
             std::pair<cudaEvent_t, cudaEvent_t> evp{};
             if (prof) {
@@ -931,6 +932,7 @@ struct infllm_engine {
                     launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
             launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
+            k4_pdl = one_stream && !coll && !prof && !(debug_skip & 2) && n_sel > 0 && lp.fused != 0;
             if (prof) {
                 record(evp.second, st);
                 (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
@@ -1054,8 +1056,11 @@ struct infllm_engine {
             } else if (dec_ran) {
                 if (coll)
                     coll->attn.push_back(ap);
-                else
-                    launch_attn_dec(ap, dec_scratch(), st);
+                else {
+                    DecScratch sc = dec_scratch();
+                    sc.pdl = k4_pdl ? 1 : 0;
+                    launch_attn_dec(ap, sc, st);
+                }
                 ++launches;
             } else if (tc_eligible(lx)) {
                 launches += launch_attn_tc(ap, st);
@@ -1855,7 +1860,9 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             }
         }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
-                              DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0}, st);
+                              DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0,
+                                         0},  // programmatic launch measured no better for the batch
+                              st);
         chk("decode_batch attention");
         for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after attention");
         static const bool lru_inline = std::getenv("INFLLM_BATCH_LRU_INLINE") != nullptr;  // A/B experiments

@@ -2283,6 +2283,7 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* 
 // as lookup_stream_body (bit-identical rel[u]).
 constexpr int kScanMaxB = 256;
 __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams* __restrict__ ps, int B) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the top-k blocks may launch (PDL)
     extern __shared__ __align__(16) uint8_t scan_smem[];
     __shared__ int64_t s_off[kScanMaxB + 1];
     __shared__ const uint8_t* s_repr[kScanMaxB];
@@ -2372,6 +2373,9 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
     }
 }
 __global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
+    // programmatic dependent of the scan: K4 may launch now; the relevance must be complete
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const LookupParams& p = ps[blockIdx.x];
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
 }
@@ -2417,7 +2421,17 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             } else {
                 k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
             }
-            k_topk_b<<<B, 1024, 0, st>>>(ps);
+            static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(static_cast<unsigned>(B));
+            cfg.blockDim = dim3(1024);
+            cfg.stream = st;
+            cudaLaunchAttribute la[1];
+            la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            la[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = la;
+            cfg.numAttrs = pdl ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, k_topk_b, ps);
             break;
         }
         case 4:  // LRU / tier bookkeeping
