@@ -1744,7 +1744,12 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             for (int32_t j = 0; j < i; ++j)
                 if (engs[i] == engs[j]) all = false;
         auto at = [](const void* p, size_t off) { return static_cast<const uint8_t*>(p) + off; };
-        if (!all) {  // other shapes / modes: the per-engine decode step, sequence by sequence
+        // one sequence: the single-sequence chain (programmatic K4, fused lookup)
+        // is shorter than the batched stages (46 vs 73 us @128K); same ids, counters
+        // and trace (tests/test_gpu_decode.py::test_decode_batch_of_one)
+        static const bool one_batched = getenv("INFLLM_BATCH1") && atoi(getenv("INFLLM_BATCH1")) == 1;
+        if (n == 1 && !one_batched) all = false;
+        if (!all) {  // other shapes / modes / one sequence: the per-engine decode step, sequence by sequence
             for (int32_t i = 0; i < n; ++i) {
                 if (!engs[i]) throw ConfigError("null engine");
                 if (engs[i]->dtype == INFLLM_DTYPE_BF16)

@@ -125,6 +125,33 @@ def test_decode_batch_matches_per_sequence(n_pre):
             assert ea.unit_info(u) == eb.unit_info(u)
 
 
+def test_decode_batch_of_one():
+    """decode_batch over one sequence takes the single-sequence chain; calls of
+    one and of two sequences alternate over the same engines (the LRU stream
+    of a batched call carried into the next single call and back) and match
+    decode_step per sequence: ids, counters, trace exact."""
+    from paper_2402_04617_b200 import decode_batch
+
+    seeds = [71, 72]
+    a, da = _prefilled(CFG, 2500, seeds)
+    b, db = _prefilled(CFG, 2500, seeds)
+    worst = 0.0
+    for t in range(2500, 2700):
+        sub = [0] if t % 3 == 0 else [1] if t % 3 == 1 else [0, 1]
+        q = torch.stack([db[i][0][t] for i in sub])
+        k = torch.stack([db[i][1][t] for i in sub])
+        v = torch.stack([db[i][2][t] for i in sub])
+        got = decode_batch([b[i] for i in sub], q, k, v)
+        for j, i in enumerate(sub):
+            ref = a[i].decode_step(da[i][0][t:t + 1], da[i][1][t:t + 1], da[i][2][t:t + 1])
+            assert a[i].retrieved_ids() == b[i].retrieved_ids(), (t, i)
+            worst = max(worst, rel_err(got[j].float().cpu().numpy(), ref[0].float().cpu().numpy()))
+    assert worst < 2e-2, worst
+    for ea, eb in zip(a, b):
+        assert ea.metrics() == eb.metrics()
+        assert ea.trace() == eb.trace()
+
+
 def test_decode_batch_vs_oracle():
     """One batched sequence set against the CPU oracle directly."""
     from paper_2402_04617_b200 import decode_batch
