@@ -1205,9 +1205,20 @@ void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t*
     launch_lookup(p, dtype_bf16, st);
     if (p.n_sel > 0) launch_topk_multi(p.rel, p.U, p.n_sel, cand_v, cand_i, p.sel, st);
 }
+// up to 1024 * kRadixE units one block selects directly (ids are the indices)
+__global__ void __launch_bounds__(1024) k_topk_one(const double* rel, int64_t U, int64_t k, int64_t* sel) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    block_topk_radix(rel, U, k, sel);
+}
 void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                        cudaStream_t st) {
     if (U <= 0 || k <= 0) return;
+    static const bool one = !(getenv("INFLLM_TOPK_ONE") && atoi(getenv("INFLLM_TOPK_ONE")) == 0);
+    if (one && U <= 1024 * kRadixE) {
+        k_topk_one<<<1, 1024, 0, st>>>(rel, U, std::min<int64_t>(k, U), sel);
+        return;
+    }
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
     k_topk_local<<<static_cast<unsigned>(nb), 256, 0, st>>>(rel, U, k, cand_v, cand_i);
     k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, nb * k, std::min<int64_t>(k, U), sel);

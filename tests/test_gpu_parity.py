@@ -207,7 +207,7 @@ def test_topk_ties_and_sizes(U, k):
     assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))
 
 
-@pytest.mark.parametrize("U,k", [(991, 16), (8159, 16), (20000, 32)])
+@pytest.mark.parametrize("U,k", [(991, 16), (2049, 16), (4063, 16), (3000, 128), (8159, 16), (20000, 32)])
 def test_lookup_bf16_c2_shape(U, k):
     """The register-resident relevance scan (bf16, d 128, r_k 4, 8 KV groups) and
     the multi-block top-k at C2/C3 index sizes: small-integer data makes every
