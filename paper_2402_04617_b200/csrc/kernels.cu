@@ -1171,7 +1171,9 @@ int64_t topk_multi_scratch(int64_t U, int64_t k) {
 }
 void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
     p.fused = 2;
-    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.U >= kScanBlocks * 8 * 4 &&
+    static const int64_t stream_min = getenv("INFLLM_STREAM_MIN_U") ? atoll(getenv("INFLLM_STREAM_MIN_U"))
+                                                                     : 2049;  // past the fused last-block top-k
+    if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.U >= stream_min &&
         p.U <= static_cast<int64_t>(kScanBlocks) * kSliceU && p.n_sel >= 0 &&
         kScanBlocks * p.n_sel <= 1024 * kRadixE) {
         // large index: streaming scan with the per-slice top-k fused, then one merge block
