@@ -189,7 +189,8 @@ int infllm_decode_step(infllm_engine_t eng, int32_t layer, const void* q, const 
  * [n][H][d_v], device memory. Every stage (prep, eviction, unit selection,
  * lookup + top-k, attention, LRU) is one launch for all n sequences when the
  * engines share config and shape (bf16, d = 128, unit 128, single shard, no
- * host tier); otherwise the engines step one after another. Results equal n
+ * host tier) and n > 1; otherwise (and for one sequence, whose single-sequence
+ * chain is shorter) the engines step one after another. Results equal n
  * decode_step calls. */
 int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const void* q,
                         const void* k, const void* v, void* out, void* stream);
