@@ -925,13 +925,14 @@ struct infllm_engine {
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
+            int n_lk = lp.fused == 1 ? 1 : 2;
             if (lp.fused == 2 && !coll) {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
-                    launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
+                    n_lk = launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
-            launches += lp.fused == 1 ? 1 : (lp.fused == 2 ? 3 : 2);
+            launches += n_lk;
             k4_pdl = one_stream && !coll && !prof && !(debug_skip & 2) && n_sel > 0 && lp.fused != 0;
             if (prof) {
                 record(evp.second, st);
@@ -2132,6 +2133,9 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         lp.d = head_dim;
         lp.n_sel = k;
         lp.sel = ids;
+        static thread_local DBuf cnt;  // block counter of the folded merge (zeroed once, re-zeroed by the kernel)
+        cnt.grow(64, st);
+        lp.done = cnt.as<unsigned int>();
         launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
                            reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
         ck(cudaGetLastError(), "lookup");

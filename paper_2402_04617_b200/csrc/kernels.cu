@@ -1149,9 +1149,62 @@ __global__ void __launch_bounds__(256) k_topk_local(const double* rel, int64_t U
         cand_i[blockIdx.x * k + r] = ok ? s0 + loc[r] : -1;
     }
 }
-__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge block may launch (PDL)
+// Final top-k of the slice candidates in one block of T threads, T * kRadixE
+// at a time: the kept k (ascending index = ascending id, candidates being in
+// id order) are prepended to the next window, so (rel desc, id asc) carries.
+__device__ void merge_candidates(const double* cv, const int64_t* ci, int64_t n, int64_t k, int64_t* sel, double* tv,
+                                 int64_t* ti) {
+    __shared__ int64_t loc[kTopkMaxSel];
+    const int64_t C = static_cast<int64_t>(blockDim.x) * kRadixE;
+    int64_t m = 0, next = 0;
+    for (;;) {
+        const int64_t take = C - m < n - next ? C - m : n - next;
+        for (int64_t i = threadIdx.x; i < take; i += blockDim.x) {
+            tv[m + i] = cv[next + i];
+            ti[m + i] = ci[next + i];
+        }
+        __syncthreads();
+        m += take;
+        next += take;
+        const int64_t kk = k < m ? k : m;
+        block_topk_radix(tv, m, kk, loc);
+        __syncthreads();
+        if (next == n) {
+            for (int r = threadIdx.x; r < kk; r += blockDim.x) sel[r] = ti[loc[r]];
+            return;
+        }
+        double v = 0.0;
+        int64_t id = -1;
+        if (threadIdx.x < kk) {
+            v = tv[loc[threadIdx.x]];
+            id = ti[loc[threadIdx.x]];
+        }
+        __syncthreads();
+        if (threadIdx.x < kk) {
+            tv[threadIdx.x] = v;
+            ti[threadIdx.x] = id;
+        }
+        __syncthreads();
+        m = kk;
+    }
+}
+// fold != 0: the last block to finish merges the candidates (no merge launch)
+__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p, int fold) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge block / K4 may launch (PDL)
     lookup_stream_body(p, gridDim.x);
+    if (!fold) return;
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    extern __shared__ __align__(16) uint8_t scan_smem[];  // the scan's stage ring is free now
+    double* tv = reinterpret_cast<double*>(scan_smem);
+    int64_t* ti = reinterpret_cast<int64_t*>(scan_smem + sizeof(double) * blockDim.x * kRadixE);
+    merge_candidates(p.cand_v, p.cand_i, static_cast<int64_t>(gridDim.x) * p.n_sel, p.n_sel, p.sel, tv, ti);
+    if (threadIdx.x == 0) *p.done = 0;
 }
 __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const int64_t* cand_i, int64_t n, int64_t k,
                                                      int64_t* sel) {
@@ -1169,7 +1222,7 @@ int64_t topk_multi_scratch(int64_t U, int64_t k) {
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
     return (nb > kScanBlocks ? nb : kScanBlocks) * k;
 }
-void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
+int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
     p.fused = 2;
     static const int64_t stream_min = getenv("INFLLM_STREAM_MIN_U") ? atoll(getenv("INFLLM_STREAM_MIN_U"))
                                                                      : 2049;  // past the fused last-block top-k
@@ -1185,7 +1238,13 @@ void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t*
         }
         p.cand_v = p.n_sel > 0 ? cand_v : nullptr;
         p.cand_i = p.n_sel > 0 ? cand_i : nullptr;
-        k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p);
+        // folded merge (last scan block, 256 threads, windows of 2048): off by default, measured
+        // slower than the 1024-thread merge block launched as a programmatic dependent
+        // (512K decode 62 vs 57 us/step); INFLLM_SCAN_FOLD=1 enables it
+        static const bool fold_ok = getenv("INFLLM_SCAN_FOLD") && atoi(getenv("INFLLM_SCAN_FOLD")) == 1;
+        const int fold = fold_ok && p.done && p.n_sel > 0 ? 1 : 0;
+        k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p, fold);
+        if (fold) return 1;
         if (p.n_sel > 0) {
             static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
             cudaLaunchConfig_t cfg{};
@@ -1199,13 +1258,15 @@ void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t*
             cfg.numAttrs = pdl ? 1 : 0;
             cudaLaunchKernelEx(&cfg, k_topk_final, static_cast<const double*>(cand_v), static_cast<const int64_t*>(cand_i),
                                static_cast<int64_t>(kScanBlocks) * p.n_sel, p.n_sel, p.sel);
+            return 2;
         }
-        return;
+        return 1;
     }
     p.cand_v = nullptr;
     p.cand_i = nullptr;
     launch_lookup(p, dtype_bf16, st);
-    if (p.n_sel > 0) launch_topk_multi(p.rel, p.U, p.n_sel, cand_v, cand_i, p.sel, st);
+    if (p.n_sel > 0 && p.U > 0) return 1 + launch_topk_multi(p.rel, p.U, p.n_sel, cand_v, cand_i, p.sel, st);
+    return 1;
 }
 // up to 1024 * kRadixE units one block selects directly (ids are the indices)
 __global__ void __launch_bounds__(1024) k_topk_one(const double* rel, int64_t U, int64_t k, int64_t* sel) {
@@ -1213,17 +1274,18 @@ __global__ void __launch_bounds__(1024) k_topk_one(const double* rel, int64_t U,
     asm volatile("griddepcontrol.wait;" ::: "memory");
     block_topk_radix(rel, U, k, sel);
 }
-void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
-                       cudaStream_t st) {
-    if (U <= 0 || k <= 0) return;
+int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
+                      cudaStream_t st) {
+    if (U <= 0 || k <= 0) return 0;
     static const bool one = !(getenv("INFLLM_TOPK_ONE") && atoi(getenv("INFLLM_TOPK_ONE")) == 0);
     if (one && U <= 1024 * kRadixE) {
         k_topk_one<<<1, 1024, 0, st>>>(rel, U, std::min<int64_t>(k, U), sel);
-        return;
+        return 1;
     }
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
     k_topk_local<<<static_cast<unsigned>(nb), 256, 0, st>>>(rel, U, k, cand_v, cand_i);
     k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, nb * k, std::min<int64_t>(k, U), sel);
+    return 2;
 }
 
 __global__ void __launch_bounds__(1024) k_topk(TopkParams p) {

@@ -236,9 +236,10 @@ void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
 // exact top-k (rel desc, id asc) over rel[U] for large U; scratch of topk_multi_scratch(U, k) entries each
 // lookup (fused == 2) + exact top-k for a single shard; cand_v / cand_i scratch as above
-void launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st);
+// returns the number of kernels launched
+int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st);
 int64_t topk_multi_scratch(int64_t U, int64_t k);
-void launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
+int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                        cudaStream_t st);
 template <typename T> void launch_attn_simt(const AttnParams& p, cudaStream_t st);
 void launch_mass(const MassParams& p, cudaStream_t st);
