@@ -250,7 +250,7 @@ int infllm_select_representatives(const float* scores, const int64_t* lens, int6
 /* TieredStore::relevance_all + lookup's top-k (memory.hpp:217-253) over an
  * explicit representative index: qsum [n_kv_heads][head_dim] fp64 (sum of
  * the chunk's queries over the heads of each KV group), repr
- * [n_units][r_k][n_kv_heads][head_dim] (dtype), -> rel [n_units] fp64 and
+ * [n_units][n_kv_heads][r_k][head_dim] (dtype), -> rel [n_units] fp64 and
  * ids [min(k_m, n_units)] ascending. */
 int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n_units,
                   int64_t r_k, int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel,

@@ -148,7 +148,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     int64_t near0;
     const int T = dec_tiles(a, n_init, near0);
     const int tps = (T + nsplit - 1) / nsplit;
-    const int t0 = x * tps, t1 = (sc.dbg & 1) ? t0 : min(T, t0 + tps);
+    const int t0 = x * tps, t1 = min(T, t0 + tps);
     if (t0 < n_init + a.n_sel && t1 > n_init) {
         // this split attends retrieved units: wait for the lookup grid when launched
         // as its programmatic dependent (no-op otherwise)
@@ -326,7 +326,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     unsigned* cnt = sc.cnt + static_cast<int64_t>(b) * a.G + g;
     if (tid == 0) s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(nsplit - 1);
     __syncthreads();
-    if (!s_last || (sc.dbg & 2)) {
+    if (!s_last) {
         if (s_last && tid == 0) *cnt = 0;
         return;
     }
@@ -450,19 +450,15 @@ int64_t dec_max_tiles(const AttnParams& a) {
 }
 
 void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st) {
-    DecScratch sc = sc0;
-    static const int dbg = getenv("INFLLM_DEC_DBG") ? atoi(getenv("INFLLM_DEC_DBG")) : 0;
-    static const int nsf = getenv("INFLLM_DEC_SPLITS") ? atoi(getenv("INFLLM_DEC_SPLITS")) : 0;
-    sc.dbg = dbg;
-    const int ns = nsf > 0 ? std::min<int>(nsf, static_cast<int>(dec_max_tiles(a))) : pick_splits(dec_max_tiles(a), a.G, 1);
+    const DecScratch& sc = sc0;
+    const int ns = pick_splits(dec_max_tiles(a), a.G, 1);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_attn_dec1, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
         cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
         attr = true;
     }
-    // programmatic dependent launch after the lookup (INFLLM_DEC_PDL=0: plain launch)
-    static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
+    // programmatic dependent launch after the lookup (sc.pdl)
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ns, a.G, 1);
     cfg.blockDim = dim3(kThr);
@@ -472,19 +468,16 @@ void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = pdl && sc.pdl ? 1 : 0;
+    cfg.numAttrs = sc.pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_attn_dec1, a, sc);
 }
 
 void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,
                            cudaStream_t st) {
-    static const int dbg = getenv("INFLLM_DEC_DBG") ? atoi(getenv("INFLLM_DEC_DBG")) : 0;
-    DecScratch s2 = sc;
-    s2.dbg = dbg;
+    const DecScratch& s2 = sc;
     const int ns = pick_splits(max_tiles, G, B);
     cudaFuncSetAttribute(k_attn_decb, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem);
     // programmatic dependent of the top-k: splits without retrieved units start early
-    static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ns, G, B);
     cfg.blockDim = dim3(kThr);
@@ -494,7 +487,7 @@ void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t m
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = pdl && sc.pdl ? 1 : 0;
+    cfg.numAttrs = sc.pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_attn_decb, dev_params, s2);
 }
 

@@ -18,7 +18,6 @@ struct DecScratch {
     float* mass;    // [B][H][max_sel][kDecWarps][2] per-warp (mass, running max)
     unsigned* cnt;  // [B][G]
     int max_sel;
-    int dbg;  // timing experiments only: bit0 skip tiles, bit1 skip merge
     int pdl;  // 1: the kernel right before K4 on its stream is the lookup (or its top-k), whose
               // inputs were complete before it started: K4 may launch as its programmatic dependent
 };

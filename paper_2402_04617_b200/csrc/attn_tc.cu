@@ -910,10 +910,8 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     P.a = a;
     const uint64_t R = static_cast<uint64_t>(a.R);
     const uint64_t ucap = static_cast<uint64_t>(a.unit_cap > 0 ? a.unit_cap : 1);
-    // INFLLM_ATTN_CLUSTER caps the cluster (placement experiments only)
-    static const int cmax = getenv("INFLLM_ATTN_CLUSTER") ? atoi(getenv("INFLLM_ATTN_CLUSTER")) : ATTN_MAX_CLUSTER;
     int csize = 1;
-    while (csize * 2 <= cmax && a.rep % (csize * 2) == 0) csize *= 2;
+    while (csize * 2 <= ATTN_MAX_CLUSTER && a.rep % (csize * 2) == 0) csize *= 2;
     const int box = 128 / csize;
     TmapKey key{{a.qa, a.qc, a.ring_k, a.ring_krot, a.ring_v, a.init_k, a.init_v, a.unit_k, a.unit_v},
                 {static_cast<uint64_t>(a.H) * a.lxp, a.G * R, ucap,
@@ -978,15 +976,6 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     la[1].val.clusterDim.z = 1;
     cfg.attrs = la;
     cfg.numAttrs = 2;
-    if (getenv("INFLLM_ATTN_OCC")) {
-        static bool once = false;
-        if (!once) {
-            once = true;
-            int nc = 0;
-            cudaOccupancyMaxActiveClusters(&nc, k_attn_tc, &cfg);
-            fprintf(stderr, "k_attn_tc: grid %u x %u, cluster %d, max active clusters %d\n", grid.x, grid.y, csize, nc);
-        }
-    }
     cudaLaunchKernelEx(&cfg, k_attn_tc, P);
     return 1;
 }

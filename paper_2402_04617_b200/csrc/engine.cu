@@ -151,55 +151,6 @@ struct HBuf {
     }
 };
 
-// Green context (driver API through cudaGetDriverEntryPoint: no -lcuda) that
-// owns `n_sms` SMs: the engine's side streams are created in it, so the
-// prep / lookup / eviction / LRU kernels of the next steps run on that
-// partition only and never hold SMs the attention CTAs (one per SM, 128 of
-// them at C2) are waiting for; the attention stays on the whole device.
-template <typename F>
-F drv(const char* name) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p)
-        throw CudaError(std::string("driver entry point ") + name + " unavailable");
-    return reinterpret_cast<F>(p);
-}
-struct SidePartition {
-    CUgreenCtx ctx = nullptr;
-    int sms = 0;
-};
-SidePartition make_side_partition(int device, int n_sms) {
-    using GetDev = CUresult (*)(CUdevice*, int);
-    using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
-    using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
-    using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
-    using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
-    CUdevice dev;
-    if (drv<GetDev>("cuDeviceGet")(&dev, device) != CUDA_SUCCESS) throw CudaError("cuDeviceGet");
-    CUdevResource all, part, rem;
-    if (drv<GetRes>("cuDeviceGetDevResource")(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
-        throw CudaError("cuDeviceGetDevResource");
-    unsigned n = 1;
-    if (drv<Split>("cuDevSmResourceSplitByCount")(&part, &n, &all, &rem, 0, static_cast<unsigned>(n_sms)) !=
-            CUDA_SUCCESS || n != 1)
-        throw CudaError("cuDevSmResourceSplitByCount");
-    CUdevResourceDesc desc;
-    if (drv<GenDesc>("cuDevResourceGenerateDesc")(&desc, &part, 1) != CUDA_SUCCESS)
-        throw CudaError("cuDevResourceGenerateDesc");
-    SidePartition sp;
-    if (drv<Create>("cuGreenCtxCreate")(&sp.ctx, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
-        throw CudaError("cuGreenCtxCreate");
-    sp.sms = static_cast<int>(part.sm.smCount);
-    return sp;
-}
-cudaStream_t side_partition_stream(const SidePartition& sp) {
-    using SCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
-    CUstream st;
-    if (drv<SCreate>("cuGreenCtxStreamCreate")(&st, sp.ctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
-        throw CudaError("cuGreenCtxStreamCreate");
-    return reinterpret_cast<cudaStream_t>(st);
-}
-
 __global__ void k_empty() {}
 // throughput probes: 8 independent FMA chains x n iterations per thread
 __global__ void k_probe_f64(double* out, int n) {
@@ -321,7 +272,6 @@ struct infllm_engine {
     cudaStream_t tier_stream = nullptr;
     cudaEvent_t e_tier = nullptr, e_tierdone = nullptr;
     int64_t tier_seq = -1;  // step that last queued work on the tier stream
-    SidePartition side_part{};  // option side_sms: side streams confined to a green context
     int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
@@ -359,7 +309,6 @@ struct infllm_engine {
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
         DBuf dec_maps;  // K4 TMA tensor maps (6), re-encoded when a buffer moves
         std::vector<const void*> dec_maps_key;
-        std::vector<uint8_t> dec_maps_host;  // what was written (INFLLM_BATCH_SYNC checks)
         // host tier (tier_slots > 0): unit pages in mapped pinned host memory,
         // the attention reads them from tier_slots device cache slots
         HBuf host_k, host_krot, host_v;
@@ -488,23 +437,6 @@ struct infllm_engine {
             for (const void* h : {L.dhost_k, L.dhost_krot, L.dhost_v}) r.push_back(h);
         return r;
     }
-    // INFLLM_BATCH_SYNC: the K4 tensor maps in device memory still hold what was written
-    void dbg_maps(const char* where) {
-        static const bool on = std::getenv("INFLLM_BATCH_SYNC") != nullptr;
-        if (!on) return;
-        ck(cudaDeviceSynchronize(), where);
-        for (auto& L : layers) {
-            if (!L.dec_maps.p || L.dec_maps_host.empty()) continue;
-            std::vector<uint8_t> d(L.dec_maps_host.size());
-            ck(cudaMemcpy(d.data(), L.dec_maps.p, d.size(), cudaMemcpyDeviceToHost), "dbg maps");
-            for (size_t i = 0; i < d.size(); ++i)
-                if (d[i] != L.dec_maps_host[i]) {
-                    std::fprintf(stderr, "dbg maps of engine %p changed at %s: byte %zu (map %zu) %02x -> %02x, maps at %p\n",
-                                 static_cast<void*>(this), where, i, i / 128, L.dec_maps_host[i], d[i], L.dec_maps.p);
-                    break;
-                }
-        }
-    }
     void ensure_units(Layer& L, int64_t need, cudaStream_t st) {
         if (need <= L.unit_cap) return;
         sync_ext();
@@ -574,7 +506,7 @@ struct infllm_engine {
 
     DecScratch dec_scratch() const {
         return DecScratch{dec_part.as<float>(), dec_mass.as<float>(), dec_cnt.as<unsigned>(),
-                          static_cast<int>(std::max<int64_t>(cfg.n_lookup, 1)), 0, 0};
+                          static_cast<int>(std::max<int64_t>(cfg.n_lookup, 1)), 0};
     }
 
     // where unit pages are written (HBM pool, or the host tier)
@@ -1042,7 +974,6 @@ struct infllm_engine {
                 ck(cudaMemcpyAsync(L.dec_maps.p, hm, sizeof(hm), cudaMemcpyHostToDevice, st), "tensor maps H2D");
                 ck(cudaStreamSynchronize(st), "tensor maps");  // hm is a stack buffer
                 L.dec_maps_key = key;
-                L.dec_maps_host.assign(reinterpret_cast<const uint8_t*>(hm), reinterpret_cast<const uint8_t*>(hm) + sizeof(hm));
             }
             ap.dec_maps = L.dec_maps.p;
         }
@@ -1252,7 +1183,6 @@ struct infllm_engine {
         if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
         if (n < 1) throw StreamError("encode_stream: empty stream");
         Layer& L = layers[static_cast<size_t>(li)];
-        dbg_maps("encode_stream begin");
         join_ext(st);
         if (!cap_stream) {
             ck(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "stream");
@@ -1543,13 +1473,6 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
         ck(cudaStreamSynchronize(st), "engine_create");
-        if (const char* ss = std::getenv("INFLLM_SIDE_SMS")) {  // default for the side-stream partition
-            const int64_t v = std::atoll(ss);
-            if (v > 0) {
-                infllm_engine* raw = e.get();
-                if (infllm_engine_set_option(raw, "side_sms", v) != INFLLM_OK) throw CudaError(g_err);
-            }
-        }
         *out = e.release();
     });
 }
@@ -1618,7 +1541,6 @@ int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
 int infllm_engine_reset(infllm_engine_t e, void* stream) {
     return guard([&] {
         auto st = static_cast<cudaStream_t>(stream);
-        e->dbg_maps("reset begin");
         e->join_ext(st);
         e->join_side(st);
         for (auto& L : e->layers) {
@@ -1645,13 +1567,21 @@ int infllm_engine_reset(infllm_engine_t e, void* stream) {
             }
         }
         ck(cudaGetLastError(), "reset");
-        e->dbg_maps("reset end");
     });
 }
 
 int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) {
     return guard([&] {
+        if (!e) throw ConfigError("null engine");
         const std::string k = key ? key : "";
+        // captured stream graphs bake in the launch choices these options make:
+        // drop them so the next encode_stream recaptures with the new setting
+        if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
+            k == "debug_skip") {
+            ck(cudaDeviceSynchronize(), "set_option");
+            for (auto& g : e->graphs) infllm_engine::drop_graph(g);
+            e->graphs.clear();
+        }
         if (k == "tc_attention")
             e->tc_disabled = value == 0;
         else if (k == "cuda_graphs")
@@ -1664,26 +1594,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->dec_disabled = value == 0;
         else if (k == "multi_stream_decode")
             e->multi_stream_decode = value != 0;
-        else if (k == "side_sms") {  // 0: side streams on the whole device; n: on an n-SM partition
-            ck(cudaDeviceSynchronize(), "side_sms");
-            for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream}) {
-                if (*s2) cudaStreamDestroy(*s2);
-                *s2 = nullptr;
-            }
-            if (value > 0) {
-                if (!e->side_part.ctx) e->side_part = make_side_partition(e->device, static_cast<int>(value));
-                for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream})
-                    *s2 = side_partition_stream(e->side_part);
-            } else {
-                for (auto* s2 : {&e->side_stream, &e->lru_stream, &e->prep_stream, &e->evict_stream, &e->tier_stream})
-                    ck(cudaStreamCreateWithFlags(s2, cudaStreamNonBlocking), "stream");
-            }
-            for (auto& g : e->graphs) infllm_engine::drop_graph(g);  // they name the old streams' work: recapture
-            e->graphs.clear();
-            e->lru_seq[0] = e->lru_seq[1] = -1;
-            for (auto& a2 : e->attn_seq) a2 = -1;
-            e->lookup_seq = e->evict_seq = e->tier_seq = -1;
-        }
+
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
                 if (L.unit_cap > 0 && value != e->tier_slots)
@@ -1748,8 +1659,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         // one sequence: the single-sequence chain (programmatic K4, fused lookup)
         // is shorter than the batched stages (46 vs 73 us @128K); same ids, counters
         // and trace (tests/test_gpu_decode.py::test_decode_batch_of_one)
-        static const bool one_batched = getenv("INFLLM_BATCH1") && atoi(getenv("INFLLM_BATCH1")) == 1;
-        if (n == 1 && !one_batched) all = false;
+        if (n == 1) all = false;
         if (!all) {  // other shapes / modes / one sequence: the per-engine decode step, sequence by sequence
             for (int32_t i = 0; i < n; ++i) {
                 if (!engs[i]) throw ConfigError("null engine");
@@ -1828,13 +1738,6 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         lk_max = std::min<int64_t>(lk_units, 0xffffffff) | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
-        // INFLLM_BATCH_SYNC: synchronise after every stage (fault isolation only)
-        static const bool dsync = std::getenv("INFLLM_BATCH_SYNC") != nullptr;
-        auto chk = [&](const char* what) {
-            if (dsync) ck(cudaStreamSynchronize(st), what);
-        };
-        chk("decode_batch tables");
-        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("decode_batch begin");
         if (!c.front.empty())
             launch_dec_front_batch(dt + o_front, n, G, st);
         else
@@ -1843,37 +1746,14 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
         if (!c.select.empty())
             launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
-        chk("decode_batch front/evict/select");
-        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after front/evict/select");
         if (bc.lru_pending) ck(cudaStreamWaitEvent(st, bc.lru_ev->ev, 0), "wait");  // the previous call's LRU
         if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
-        chk("decode_batch lookup");
-        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lookup");
-        if (dsync) {  // fault isolation: the attention's inputs, checked on the host
-            for (size_t i = 0; i < c.attn.size(); ++i) {
-                const AttnParams& ap = c.attn[i];
-                std::vector<int64_t> sel(ap.n_sel);
-                if (ap.n_sel) ck(cudaMemcpy(sel.data(), ap.sel, ap.n_sel * sizeof(int64_t), cudaMemcpyDeviceToHost), "dbg sel");
-                alignas(64) CUtensorMap dm[6], hm[6];
-                ck(cudaMemcpy(dm, ap.dec_maps, sizeof(dm), cudaMemcpyDeviceToHost), "dbg maps");
-                dec_encode_maps(ap, ap.unit_cap * static_cast<int64_t>(ap.G) * 128, hm);
-                int64_t lo = INT64_MAX, hi = INT64_MIN;
-                for (auto x : sel) lo = std::min(lo, x), hi = std::max(hi, x);
-                std::fprintf(stderr, "dbg seq %zu: n_sel %d sel [%lld, %lld] unit_cap %lld s %lld init %lld local %lld tiles %lld maps %p same %d\n",
-                             i, ap.n_sel, (long long)lo, (long long)hi, (long long)ap.unit_cap, (long long)ap.s,
-                             (long long)ap.init_len, (long long)ap.local_start, (long long)dec_max_tiles(ap), ap.dec_maps,
-                             std::memcmp(dm, hm, sizeof(dm)) == 0);
-            }
-        }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
-                              DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km, 0,
+                              DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
                                          0},  // programmatic launch measured no better for the batch
                               st);
-        chk("decode_batch attention");
-        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after attention");
-        static const bool lru_inline = std::getenv("INFLLM_BATCH_LRU_INLINE") != nullptr;  // A/B experiments
         cudaStream_t lst = st;
-        if (!lru_inline) {
+        {
             if (!bc.lru_st) {
                 ck(cudaStreamCreateWithFlags(&bc.lru_st, cudaStreamNonBlocking), "stream");
                 ck(cudaEventCreateWithFlags(&bc.ev_k4, cudaEventDisableTiming), "event");
@@ -1885,8 +1765,6 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             lst = bc.lru_st;
         }
         launch_decode_batch_stage(4, dt + o_lru, n, 0, lst);
-        if (dsync) ck(cudaStreamSynchronize(lst), "decode_batch lru");
-        for (int32_t i = 0; i < n; ++i) engs[i]->dbg_maps("after lru");
         ck(cudaGetLastError(), "decode_batch launch");
         if (lst != st) {
             ck(cudaEventRecord(bc.lru_ev->ev, lst), "record");
@@ -1906,7 +1784,6 @@ int infllm_encode_stream(infllm_engine_t e, int32_t layer, const void* q, const 
             e->encode_stream<bf16>(layer, q, k, v, n_tokens, out, st, false);
         else
             e->encode_stream<float>(layer, q, k, v, n_tokens, out, st, false);
-        e->dbg_maps("encode_stream end");
     });
 }
 
@@ -2119,7 +1996,15 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         if (n_units <= 0) return;
         const int64_t k = std::min(k_m, n_units);
         const int64_t nc = topk_multi_scratch(n_units, std::max<int64_t>(k, 1));
-        static thread_local DBuf cand;  // grow-only scratch (a per-call allocation would dominate small lookups)
+        // grow-only scratch shared by this thread's calls (a per-call allocation would
+        // dominate small lookups); a call on any stream first waits for the previous
+        // call's kernels, so neither the reuse nor a growth free can race with them
+        static thread_local DBuf cand, cnt;
+        static thread_local cudaEvent_t last = nullptr;
+        if (!last)
+            ck(cudaEventCreateWithFlags(&last, cudaEventDisableTiming), "event");
+        else
+            ck(cudaStreamWaitEvent(st, last, 0), "wait");
         cand.grow(static_cast<size_t>(nc) * 16, st);
         LookupParams lp{};
         lp.qsum = qsum;
@@ -2133,12 +2018,12 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         lp.d = head_dim;
         lp.n_sel = k;
         lp.sel = ids;
-        static thread_local DBuf cnt;  // block counter of the folded merge (zeroed once, re-zeroed by the kernel)
-        cnt.grow(64, st);
+        cnt.grow(64, st);  // block counter of the folded merge (zeroed once, re-zeroed by the kernel)
         lp.done = cnt.as<unsigned int>();
         launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
                            reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
         ck(cudaGetLastError(), "lookup");
+        ck(cudaEventRecord(last, st), "record");
     });
 }
 
@@ -2222,10 +2107,7 @@ int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, d
 int infllm_debug_timestamps(unsigned long long* out64) {
     return guard([&] {
         ck(cudaDeviceSynchronize(), "sync");
-        if (getenv("INFLLM_TS_ATTN"))
-            debug_read_attn_timestamps(out64);
-        else
-            debug_read_timestamps(out64);
+        debug_read_timestamps(out64);
     });
 }
 

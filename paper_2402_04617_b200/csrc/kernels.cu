@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <stdexcept>
+#include <string>
 
 #include "kernels.cuh"
 #include "tc_prims.cuh"
@@ -1283,6 +1285,10 @@ int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, i
         return 1;
     }
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
+    // the final block holds at most 1024 * kRadixE candidates (block_topk_radix)
+    if (nb * k > 1024 * kRadixE)
+        throw std::invalid_argument("lookup: n_units * n_lookup beyond the top-k capacity (U <= " +
+                                    std::to_string(1024 * kRadixE / k * kSliceU) + " units at this n_lookup)");
     k_topk_local<<<static_cast<unsigned>(nb), 256, 0, st>>>(rel, U, k, cand_v, cand_i);
     k_topk_final<<<1, 1024, 0, st>>>(cand_v, cand_i, nb * k, std::min<int64_t>(k, U), sel);
     return 2;
