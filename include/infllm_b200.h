@@ -238,6 +238,21 @@ int infllm_profile_begin(infllm_engine_t eng, int32_t enable);
 int infllm_profile_read(infllm_engine_t eng, double* attn_ms_total, int64_t* attn_launches,
                         double* lookup_ms_total, int64_t* lookup_launches);
 
+/* Device timeline (tracing; the reference's PhaseTimings, engine.hpp:43-49,
+ * at kernel granularity): while enabled, thread 0 of every block of the step
+ * kernels appends (kernel kind, SM id, globaltimer start / end in ns) to a
+ * device ring of `capacity` records. Kernel kinds: 0 attention (K3), 1 RoPE
+ * table, 2 prep, 3 prefix, 4 lookup scan, 5 top-k, 6 eviction + scoring,
+ * 7 representative selection, 8 LRU, 9 host-tier copy, 10 decode attention
+ * (K4), 11 decode front, 12 mass reduction. capacity 0 disables (the
+ * default). Process-wide; synchronous. */
+int infllm_timeline_enable(int64_t capacity);
+/* Copy up to cap records out; *n_out = records written since the last reset
+ * (may exceed the capacity: the ring keeps the first `capacity`). reset != 0
+ * clears the ring. Synchronous. */
+int infllm_timeline_read(uint32_t* kernel, uint32_t* sm, uint64_t* t0, uint64_t* t1, int64_t cap,
+                         int64_t* n_out, int32_t reset);
+
 /* ---- standalone operators (device pointers, async on stream) ---- */
 
 /* select_representatives (repr_score.hpp:94-112) for `n_units` units at

@@ -124,6 +124,8 @@ SIGNATURES = {
     "infllm_debug_tc_selftest": (C.c_int, [P, P, P, P, P, P]),
     "infllm_debug_kernel_bench": (C.c_int, [P, i32, i32, f64p]),
     "infllm_debug_timestamps": (C.c_int, [P]),
+    "infllm_timeline_enable": (C.c_int, [i64]),
+    "infllm_timeline_read": (C.c_int, [P, P, P, P, i64, i64p, i32]),
 }
 
 

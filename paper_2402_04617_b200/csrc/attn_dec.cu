@@ -393,7 +393,9 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch sc) {
+    TL_BEGIN();
     dec_body(a, sc, 0, blockIdx.x, gridDim.x);
+    TL_END(TL_DEC);
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restrict__ ps, DecScratch sc) {
@@ -443,6 +445,8 @@ void dec_encode_maps(const AttnParams& a, int64_t unit_rows, void* host6) {
     m[4] = make_tmap_bf16_sw128(a.ring_krot, G * static_cast<uint64_t>(a.R), 128, 128);
     m[5] = make_tmap_bf16_sw128(a.ring_v, G * static_cast<uint64_t>(a.R), 128, 128);
 }
+
+cudaError_t tl_bind_attn_dec(const TlBuf& b) { return tl_bind_tu(b); }
 
 int64_t dec_max_tiles(const AttnParams& a) {
     const int64_t n_init = (a.init_len + 127) / 128, near0 = (a.local_start / 128) * 128;

@@ -10,6 +10,7 @@
 
 __device__ unsigned long long g_attn_ts[64];
 namespace infllm {
+cudaError_t tl_bind_attn_tc(const TlBuf& b) { return tl_bind_tu(b); }
 void debug_read_attn_timestamps(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, g_attn_ts, sizeof(unsigned long long) * 64);
 }
@@ -396,6 +397,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     int32_t* sSel = reinterpret_cast<int32_t*>(sML + 4 * 128);                         // [k_m] unit ids
     int32_t* sLen = sSel + kMaxSel;                                                    // [k_m] unit lengths
 
+    // launched as a programmatic dependent of the previous step's attention
+    // (AttnParams::pdl): this CTA takes its SM as soon as one frees, then waits
+    // here for every upstream grid; the next step's attention may do the same
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    TL_BEGIN();
     if (threadIdx.x == 0) ATS1(56);
     uint64_t cta_t0 = 0;
     if (ATTN_CTA_TS && threadIdx.x == 0) {
@@ -879,6 +886,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         }
     }
     if (warp == 1) tmem_dealloc(tbase, 512);
+    TL_END(TL_ATTN);
 }
 
 bool attn_tc_masses_in_kernel(int n_sel) { return n_sel <= kMassSlots; }
@@ -967,15 +975,17 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute la[2];
+    cudaLaunchAttribute la[3];
     la[0].id = cudaLaunchAttributePriority;
     la[0].val.priority = prio_hi;
     la[1].id = cudaLaunchAttributeClusterDimension;  // the csize query heads of one KV group
     la[1].val.clusterDim.x = 1;
     la[1].val.clusterDim.y = static_cast<unsigned>(csize);
     la[1].val.clusterDim.z = 1;
+    la[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[2].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = a.pdl ? 3 : 2;
     cudaLaunchKernelEx(&cfg, k_attn_tc, P);
     return 1;
 }

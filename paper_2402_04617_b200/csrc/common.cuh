@@ -59,6 +59,44 @@ __device__ __forceinline__ float warp_max_f(float v) {
     return v;
 }
 
+// Device timeline (infllm_timeline_*): thread 0 of every block of the step
+// kernels appends (kernel, SM, globaltimer start, end) to a device ring when a
+// buffer is bound, so the overlap of the five step streams can be read back
+// without a profiler. Unbound (the default) it costs one timer read and one
+// predicated branch per block.
+enum TlKernel : unsigned {
+    TL_ATTN = 0, TL_ROPE, TL_PREP, TL_PREFIX, TL_LOOKUP, TL_TOPK, TL_EVICT, TL_SELECT, TL_LRU, TL_TIER,
+    TL_DEC, TL_DEC_FRONT, TL_MASS, TL_KINDS
+};
+struct TlRec {
+    unsigned long long t0, t1;
+    unsigned kid, sm;
+};
+struct TlBuf {
+    TlRec* rec;
+    unsigned long long* cnt;
+    unsigned long long cap;
+};
+static __device__ TlBuf g_tl;  // one per translation unit, bound by tl_bind_tu
+static inline cudaError_t tl_bind_tu(const TlBuf& b) { return cudaMemcpyToSymbol(g_tl, &b, sizeof(b)); }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_put(unsigned kid, unsigned long long t0) {
+    const unsigned long long i = atomicAdd(g_tl.cnt, 1ull);
+    if (i >= g_tl.cap) return;
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_tl.rec[i] = TlRec{t0, gtimer(), kid, sm};
+}
+#define TL_BEGIN() const unsigned long long tl_t0_ = threadIdx.x == 0 ? ::infllm::gtimer() : 0ull
+#define TL_END(kid)                                                              \
+    do {                                                                         \
+        if (threadIdx.x == 0 && ::infllm::g_tl.rec) ::infllm::tl_put((kid), tl_t0_); \
+    } while (0)
+
 // Device LRU/bookkeeping state of one layer's TieredStore (memory.hpp:170-323).
 struct LruState {
     int64_t hot_count;

@@ -253,6 +253,7 @@ struct infllm_engine {
     bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
     bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
     bool dec_disabled = false;
+    bool attn_pdl = false;  // option attn_pdl: K3 as a programmatic dependent of the kernel before it
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -995,6 +996,7 @@ struct infllm_engine {
                 }
                 ++launches;
             } else if (tc_eligible(lx)) {
+                ap.pdl = attn_pdl && !fork && !one_stream ? 1 : 0;
                 launches += launch_attn_tc(ap, st);
             } else {
                 launch_attn_simt<T>(ap, st);
@@ -1577,7 +1579,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // captured stream graphs bake in the launch choices these options make:
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
-            k == "debug_skip") {
+            k == "attn_pdl" || k == "debug_skip") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1594,6 +1596,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->dec_disabled = value == 0;
         else if (k == "multi_stream_decode")
             e->multi_stream_decode = value != 0;
+        else if (k == "attn_pdl")
+            e->attn_pdl = value != 0;
 
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
@@ -2108,6 +2112,59 @@ int infllm_debug_timestamps(unsigned long long* out64) {
     return guard([&] {
         ck(cudaDeviceSynchronize(), "sync");
         debug_read_timestamps(out64);
+    });
+}
+
+// Device timeline (common.cuh TlRec): every block of the step kernels appends
+// (kernel, SM, start, end) while a buffer is bound.
+namespace {
+struct Timeline {
+    TlRec* rec = nullptr;
+    unsigned long long* cnt = nullptr;
+    int64_t cap = 0;
+} g_timeline;
+void timeline_bind(const TlBuf& b) {
+    ck(tl_bind_kernels(b), "timeline bind");
+    ck(tl_bind_attn_tc(b), "timeline bind");
+    ck(tl_bind_attn_dec(b), "timeline bind");
+}
+}  // namespace
+
+int infllm_timeline_enable(int64_t capacity) {
+    return guard([&] {
+        ck(cudaDeviceSynchronize(), "timeline");
+        timeline_bind(TlBuf{nullptr, nullptr, 0});
+        if (g_timeline.rec) cudaFree(g_timeline.rec);
+        if (g_timeline.cnt) cudaFree(g_timeline.cnt);
+        g_timeline = Timeline{};
+        if (capacity <= 0) return;
+        ck(cudaMalloc(&g_timeline.rec, static_cast<size_t>(capacity) * sizeof(TlRec)), "timeline alloc");
+        ck(cudaMalloc(&g_timeline.cnt, sizeof(unsigned long long)), "timeline alloc");
+        ck(cudaMemset(g_timeline.cnt, 0, sizeof(unsigned long long)), "timeline");
+        g_timeline.cap = capacity;
+        timeline_bind(TlBuf{g_timeline.rec, g_timeline.cnt, static_cast<unsigned long long>(capacity)});
+    });
+}
+
+int infllm_timeline_read(uint32_t* kernel, uint32_t* sm, uint64_t* t0, uint64_t* t1, int64_t cap, int64_t* n_out,
+                         int32_t reset) {
+    return guard([&] {
+        *n_out = 0;
+        if (!g_timeline.rec) return;
+        ck(cudaDeviceSynchronize(), "timeline");
+        unsigned long long n = 0;
+        ck(cudaMemcpy(&n, g_timeline.cnt, sizeof(n), cudaMemcpyDeviceToHost), "timeline");
+        const int64_t m = std::min<int64_t>({static_cast<int64_t>(n), g_timeline.cap, cap});
+        std::vector<TlRec> r(static_cast<size_t>(std::max<int64_t>(m, 0)));
+        if (m > 0) ck(cudaMemcpy(r.data(), g_timeline.rec, m * sizeof(TlRec), cudaMemcpyDeviceToHost), "timeline");
+        for (int64_t i = 0; i < m; ++i) {
+            kernel[i] = r[i].kid;
+            sm[i] = r[i].sm;
+            t0[i] = r[i].t0;
+            t1[i] = r[i].t1;
+        }
+        *n_out = static_cast<int64_t>(n);
+        if (reset) ck(cudaMemset(g_timeline.cnt, 0, sizeof(unsigned long long)), "timeline");
     });
 }
 

@@ -24,6 +24,8 @@ __device__ unsigned long long g_dbg_ts[64];
         if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_dbg_ts[(i)] = clock64(); \
     } while (0)
 
+cudaError_t tl_bind_kernels(const TlBuf& b) { return tl_bind_tu(b); }
+
 void debug_read_timestamps(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, g_dbg_ts, sizeof(unsigned long long) * 64);
 }
@@ -158,7 +160,11 @@ __device__ __forceinline__ void rope_table_body(const PrepParams& p) {
     rope_cs(p.freqs, a, p.s + i, c, s);
     p.rtab[t] = make_float2(c, s);
 }
-__global__ void k_rope_table(PrepParams p) { rope_table_body(p); }
+__global__ void k_rope_table(PrepParams p) {
+    TL_BEGIN();
+    rope_table_body(p);
+    TL_END(TL_ROPE);
+}
 
 template <typename T>
 struct V8 {
@@ -558,7 +564,9 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
+    TL_BEGIN();
     prep_tok_body<T>(p);
+    TL_END(TL_PREP);
 }
 
 // (6) fp64 prefix into the P ring from the per-token sums and the tile sums:
@@ -594,7 +602,11 @@ __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p) {
         p.chunk_qsum[g * p.d + c] = all;
     }
 }
-__global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) { prefix_tiles_body(p); }
+__global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
+    TL_BEGIN();
+    prefix_tiles_body(p);
+    TL_END(TL_PREFIX);
+}
 
 template <typename T>
 void launch_prep(const PrepParams& p, cudaStream_t st) {
@@ -787,7 +799,9 @@ __global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
     // a decode step's K4 may start its CTAs that do not read the selection now
     // (programmatic dependent launch; those that do wait for this grid)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    TL_BEGIN();
     lookup_reg_body(p, gridDim.x);
+    TL_END(TL_LOOKUP);
 }
 
 // Large indices: the same math fed by cp.async (16-byte LDGSTS) into a
@@ -1193,7 +1207,9 @@ __device__ void merge_candidates(const double* cv, const int64_t* ci, int64_t n,
 // fold != 0: the last block to finish merges the candidates (no merge launch)
 __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p, int fold) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge block / K4 may launch (PDL)
+    TL_BEGIN();
     lookup_stream_body(p, gridDim.x);
+    TL_END(TL_LOOKUP);
     if (!fold) return;
     __shared__ bool last;
     __threadfence();
@@ -1214,10 +1230,12 @@ __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const
     // then wait for the scan's candidates (both no-ops on a plain launch)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    TL_BEGIN();
     __shared__ int64_t loc[kTopkMaxSel];
     block_topk_radix(cand_v, n, k, loc);
     __syncthreads();
     for (int r = threadIdx.x; r < k; r += blockDim.x) sel[r] = cand_i[loc[r]];
+    TL_END(TL_TOPK);
 }
 constexpr int kScanBlocks = 148;  // streaming scan: one block per SM, one slice each
 int64_t topk_multi_scratch(int64_t U, int64_t k) {
@@ -1274,7 +1292,9 @@ int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* 
 __global__ void __launch_bounds__(1024) k_topk_one(const double* rel, int64_t U, int64_t k, int64_t* sel) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    TL_BEGIN();
     block_topk_radix(rel, U, k, sel);
+    TL_END(TL_TOPK);
 }
 int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                       cudaStream_t st) {
@@ -1725,7 +1745,11 @@ __device__ __forceinline__ void lru_body(const LruParams& p) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_lru(LruParams p) { lru_body(p); }
+__global__ void __launch_bounds__(256) k_lru(LruParams p) {
+    TL_BEGIN();
+    lru_body(p);
+    TL_END(TL_LRU);
+}
 void launch_lru(const LruParams& p, cudaStream_t st) { k_lru<<<1, 256, 0, st>>>(p); }
 
 // ---- host tier: GPU unit-cache slot assignment + PCIe page pull ----
@@ -2034,7 +2058,9 @@ __device__ __forceinline__ void evict_tok_body(const EvictParams& p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
+    TL_BEGIN();
     evict_tok_body<T>(p);
+    TL_END(TL_EVICT);
 }
 
 template <typename T>
@@ -2201,7 +2227,9 @@ __device__ __forceinline__ void select_body(const SelectParams& p) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_select(SelectParams p) {
+    TL_BEGIN();
     select_body<T>(p);
+    TL_END(TL_SELECT);
 }
 
 template <typename T>
@@ -2312,7 +2340,11 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
     __syncthreads();  // this step's P row is read by the eviction score
     evict_tok_body<bf16>(ep);
 }
-__global__ void __launch_bounds__(1024) k_dec_front(PrepParams p, EvictParams ep) { dec_front_body(p, ep); }
+__global__ void __launch_bounds__(1024) k_dec_front(PrepParams p, EvictParams ep) {
+    TL_BEGIN();
+    dec_front_body(p, ep);
+    TL_END(TL_DEC_FRONT);
+}
 struct DecFront {
     PrepParams p;
     EvictParams ep;

@@ -113,6 +113,7 @@ struct AttnParams {
     int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;
+    int pdl;  // K3: programmatic dependent launch after the previous kernel on its stream
     float scale;
     VLayout vl;
 };
@@ -231,6 +232,10 @@ struct SelectParams {
 };
 
 void debug_read_timestamps(unsigned long long* out);
+// bind the device timeline buffer in each translation unit (kernels.cu, attn_tc.cu, attn_dec.cu)
+cudaError_t tl_bind_kernels(const TlBuf& b);
+cudaError_t tl_bind_attn_tc(const TlBuf& b);
+cudaError_t tl_bind_attn_dec(const TlBuf& b);
 template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
