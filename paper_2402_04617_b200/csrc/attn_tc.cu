@@ -398,10 +398,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     int32_t* sLen = sSel + kMaxSel;                                                    // [k_m] unit lengths
 
     // launched as a programmatic dependent of the previous step's attention
-    // (AttnParams::pdl): this CTA takes its SM as soon as one frees, then waits
-    // here for every upstream grid; the next step's attention may do the same
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (AttnParams::pdl > 0): this CTA may take an SM as soon as one frees (before
+    // pending side-stream blocks do) and waits here for every upstream grid.
+    // It lets the next step's attention launch when a.pdl tiles remain (below).
+    if (P.a.pdl > 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     TL_BEGIN();
     if (threadIdx.x == 0) ATS1(56);
     uint64_t cta_t0 = 0;
@@ -422,6 +422,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     ts.init(a, m);
     ts.sel = sSel;
     ts.len = sLen;
+    if (a.ready_flag) {  // prefill pipeline: this step's lookup (after its prep / eviction) is done
+        if (threadIdx.x == 0) flag_wait(a.ready_flag, a.ready_val);
+        __syncthreads();
+    }
     if (threadIdx.x < a.n_sel) {
         const int64_t id = a.sel[threadIdx.x];
         sSel[threadIdx.x] = a.sel_slot ? a.sel_slot[threadIdx.x] : static_cast<int32_t>(id);  // page index
@@ -490,7 +494,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 tma_load_2d(&P.tm_qc, q_full, sQc, 0, qrow);
                 tma_load_2d(&P.tm_qc, q_full, sQc + 16384, 64, qrow);
             }
+            const int trig = a.pdl ? max(0, ts.T - abs(a.pdl)) : 0;
             for (int j = 0; j < ts.T; ++j) {
+                if (is_k && j == trig) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
                 const Tile t = ts.get(a, j);
                 const CUtensorMap* map;
                 int row;

@@ -253,7 +253,11 @@ struct infllm_engine {
     bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
     bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
     bool dec_disabled = false;
-    bool attn_pdl = false;  // option attn_pdl: K3 as a programmatic dependent of the kernel before it
+    int lookup_upb = 48;
+    bool attn_flag = false;
+    int prep_blocks = 0;  // option prep_blocks: grid cap of the chunk prep kernels (0: none)
+    bool prep_fused = true;  // option prep_fused: one-kernel chunk prep (side.cu) where the shape allows  // option attn_flag: K3 waits on the step-ready flag instead of graph edges  // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
+    int attn_pdl = 0;  // option attn_pdl = n > 0: K3 t+1 launches programmatically when K3 t has n tiles left
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -263,21 +267,28 @@ struct infllm_engine {
     // eviction/selection on the side stream (it only waits for step k-1's lookup,
     // the last reader of the chunk query sums it rewrites).
     cudaStream_t side_stream = nullptr, lru_stream = nullptr, prep_stream = nullptr, evict_stream = nullptr;
-    cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[2] = {nullptr, nullptr};
+    // selection / mass buffers rotate over kSB steps: the lookup of step k reuses
+    // the buffers of step k - kSB, read by its attention and LRU
+    static constexpr int kSB = 3;
+    cudaEvent_t e_call = nullptr, e_topk = nullptr, e_side = nullptr, e_lru[kSB] = {nullptr, nullptr, nullptr};
     cudaEvent_t e_attn = nullptr, e_lrudone = nullptr, e_prep = nullptr, e_lookup = nullptr, e_prepdone = nullptr;
-    static constexpr int kPrepAhead = 2;  // chunks the prep stream may run ahead of the attention
-    static constexpr int kPB = kPrepAhead + 1;  // prep-output buffers (qa, qc, chunk sums, key-norm bound)
+    // The prep runs up to kPB - 1 chunks ahead of the attention: prep outputs
+    // (qa, qc, chunk sums, key-norm bound) rotate over kPB buffers, the prep of
+    // step k waits for the attention of step k - kPB, and the ring holds
+    // l_L + kPB chunks + 1 slots, so the chunk being prepared never overwrites
+    // a key an attention that may still run reads.
+    static constexpr int kPB = 3;
     cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[kPB] = {nullptr, nullptr, nullptr};
+    int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     // host tier: slot assignment + PCIe page pulls of step t on their own stream
     // (after lookup t, before attention t), so lookup t+1 does not queue behind them
     cudaStream_t tier_stream = nullptr;
     cudaEvent_t e_tier = nullptr, e_tierdone = nullptr;
     int64_t tier_seq = -1;  // step that last queued work on the tier stream
-    int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
     int64_t lookup_seq = -1;         // step that last recorded e_lookup
     int64_t evict_seq = -1;          // step that last recorded e_evict
     int64_t seq = 0;                 // engine-wide step counter
-    int64_t lru_seq[2] = {-1, -1};   // step that last recorded e_lru[b]
+    int64_t lru_seq[kSB] = {-1, -1, -1};  // step that last recorded e_lru[b]
     int64_t capture_seq0 = -1;       // first step of the graph being captured (-1: not capturing)
     size_t qa_half = 0;              // bytes of one qa/qc buffer
     int64_t mass_cta_half = 0;       // doubles in one mass_cta buffer
@@ -292,6 +303,7 @@ struct infllm_engine {
                                      // bit2 evict/finalize/select, bit3 prep, bit4 LRU (results invalid)
 
     // scratch shared by layers (layers run sequentially on one stream)
+    DBuf prep_sync;  // k_prep_chunk look-back state
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, tsum, topk_done, evict_done;
     DBuf dec_part, dec_mass, dec_cnt;  // K4 decode scratch (one sequence)
 
@@ -307,6 +319,7 @@ struct infllm_engine {
         DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
         DBuf kmax2;  // [kPB step buffers][G] running max |k|^2 (attention score bound)
+        DBuf ready;  // int64 step-ready flag: the lookup of step s publishes s, K3 of step s waits for it
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
         DBuf dec_maps;  // K4 TMA tensor maps (6), re-encoded when a buffer moves
         std::vector<const void*> dec_maps_key;
@@ -418,7 +431,7 @@ struct infllm_engine {
 
     // every device buffer the engine owns (a captured step graph holds their addresses)
     std::vector<DBuf*> dev_buffers() {
-        std::vector<DBuf*> v{&qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
+        std::vector<DBuf*> v{&prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
                              &tsum, &topk_done, &evict_done, &dec_part, &dec_mass, &dec_cnt};
         for (int b = 0; b < kNB; ++b)
             for (auto* x : {&stage_q[b], &stage_k[b], &stage_v[b], &stage_o[b]}) v.push_back(x);
@@ -427,7 +440,7 @@ struct infllm_engine {
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
                             &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
                             &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
-                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps})
+                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps, &L.ready})
                 v.push_back(b);
         return v;
     }
@@ -463,7 +476,7 @@ struct infllm_engine {
                 ck(cudaMemsetAsync(L.slot_unit.p, 0xff, L.slot_unit.bytes, st), "memset");
                 L.slot_used.alloc(S * sizeof(int64_t), st);
                 const size_t km = static_cast<size_t>(std::max<int64_t>(cfg.n_lookup, 1));
-                L.sel_slot.alloc(2 * km * sizeof(int32_t), st);
+                L.sel_slot.alloc(kSB * km * sizeof(int32_t), st);
                 L.tier_miss.alloc((2 * km + 1) * sizeof(int32_t), st);
                 L.tier_stats.alloc(4 * sizeof(int64_t), st);
             }
@@ -540,7 +553,7 @@ struct infllm_engine {
             ck(cudaStreamWaitEvent(st, e_tierdone, 0), "wait");
         }
         tier_seq = -1;
-        lru_seq[0] = lru_seq[1] = -1;
+        for (auto& x : lru_seq) x = -1;
         for (auto& a : attn_seq) a = -1;
         lookup_seq = -1;
         evict_seq = -1;
@@ -607,8 +620,8 @@ struct infllm_engine {
         // stream fork: side waits for the caller's point (inputs) and for the
         // main-stream step k-2 that last read this parity's buffers
         const int64_t kseq = seq++;
-        const int b = static_cast<int>(kseq & 1);
-        const int pb = static_cast<int>(kseq % kPB);  // prep-output buffer (the prep runs up to 2 steps ahead)
+        const int b = static_cast<int>(kseq % kSB);   // selection / mass buffers
+        const int pb = static_cast<int>(kseq % kPB);  // prep-output buffers
         // decode steps (one token) run on the caller's stream alone: the
         // multi-stream pipeline only pays for chunk-sized steps, and skipping
         // its ~25 event calls halves the host cost of a decode step
@@ -621,7 +634,14 @@ struct infllm_engine {
         cudaStream_t lru_st = (one_stream && !lru_side) ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
         if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
         pipe_dirty = !one_stream;
+        // K3 of the prefill pipeline depends on its lookup (and through it on the
+        // prep, eviction and LRU) via a device flag instead of cross-stream graph
+        // edges: its only stream predecessor is the previous step's K3, so it can
+        // launch as that one's programmatic dependent and take SMs as they free
+        const bool flag_mode = std::is_same_v<T, bf16> && attn_flag && !one_stream && !coll && tier_slots == 0 &&
+                               tc_eligible(lx) && !(lx == 1 && use_dec && !dec_disabled) && !(debug_skip & 32);
         if (fork) {
+            if (flag_mode) ck(cudaMemsetAsync(L.ready.p, 0xff, sizeof(int64_t), main), "flag reset");
             rec(e_call, main);
             wt(side, e_call);
             wt(pst, e_call);
@@ -631,13 +651,11 @@ struct infllm_engine {
             if (lru_side)
                 ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // side == caller's stream
             else
-                wt(side, e_lru[b]);  // sel of this parity: attention + LRU k-2
+                wt(side, e_lru[b]);  // selection buffer b: attention + LRU k-kSB
         }
-        // qa/qc/chunk sums of this buffer were last read by attention k-3 (and its lookup)
+        // prep-output buffer pb (and the ring slots of this chunk) were last read by attention k-kPB
         if (attn_seq[pb] >= 0 && (capture_seq0 < 0 || attn_seq[pb] >= capture_seq0))
             wt(pst, e_attnp[pb]);
-        // chunk query sums are double-buffered by step parity: the lookup of step
-        // k-2 (which read this parity) ran before attention k-2, covered by e_lru[b]
         void* qa_b = static_cast<uint8_t*>(qa.p) + pb * qa_half;
         void* qc_b = static_cast<uint8_t*>(qc.p) + pb * qa_half;
         int64_t* sel_b = L.sel.as<int64_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
@@ -666,6 +684,8 @@ struct infllm_engine {
         pp.d = d;
         pp.dv = dv;
         pp.freqs = freqs;
+        pp.max_blocks = prep_blocks;
+        pp.sync = prep_fused ? prep_sync.p : nullptr;
         pp.vl = vl;
         pp.rtab = rtab.as<float2>();
         pp.qs = qsb.as<double>();
@@ -689,12 +709,17 @@ struct infllm_engine {
             else
                 launch_dec_front(pp, ep2, s2);
         };
+        const bool prep_one = std::is_same_v<T, bf16> && !fused_front && !coll && prep_chunk_supported(pp);
         if (fused_front) {
-        } else if (coll)
+        } else if (coll) {
             coll->prep.push_back(pp);
-        else if (!(debug_skip & 8))
-            launch_prep<T>(pp, st);
-        if (!fused_front)
+        } else if (prep_one) {
+            if (!(debug_skip & 8)) launch_prep_chunk(pp, st);
+            launches += 1;
+        } else {
+            if (!(debug_skip & 8)) launch_prep<T>(pp, st);
+        }
+        if (!fused_front && !prep_one)
             launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
         rec(e_prep, pst);
         wt(side, e_prep);
@@ -819,6 +844,7 @@ struct infllm_engine {
 
         // K1 + K2: lookup (memory.hpp:239-269)
         bool k4_pdl = false;  // the lookup is the last kernel before K4 on the caller's stream
+        bool last_lkp_fast = false;  // this step's lookup publishes the ready flag itself
         if (do_lookup) {
             std::pair<cudaEvent_t, cudaEvent_t> evp{};
             if (prof) {
@@ -842,12 +868,27 @@ struct infllm_engine {
             lp.sel = sel_b;
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
+            lp.early_dependents = one_stream ? 1 : 0;  // decode: K4 follows as a programmatic dependent
+            lp.ready_flag = nullptr;
+            lp.ready_val = L.step;
             last_lkp = lp;
             if (coll) {  // batched: relevance scan (rel only) + one top-k block per sequence
                 lp.fused = 2;
                 coll->lookup.push_back(lp);
             }
-            if (coll) {
+            const bool fast = !coll && Gs == Gt && lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
+            last_lkp_fast = fast && !(debug_skip & 2);
+            if (fast) {
+                // one launch: scan + exact top-k; few fat blocks inside the prefill
+                // pipeline (the attention holds most SMs), one unit per warp in decode
+                const int64_t nc = topk_multi_scratch(n_units0, n_sel);
+                lp.cand_v = L.cand.as<double>();
+                lp.cand_i = reinterpret_cast<int64_t*>(L.cand.as<double>() + nc);
+                lp.fused = 1;
+                lp.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
+                if (!(debug_skip & 2))
+                    launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units0, one_stream ? 8 : lookup_upb), st);
+            } else if (coll) {
             } else if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
             TopkParams tp{};
@@ -859,7 +900,7 @@ struct infllm_engine {
             tp.Gtot = Gt;
             if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
             int n_lk = lp.fused == 1 ? 1 : 2;
-            if (lp.fused == 2 && !coll) {
+            if (lp.fused == 2 && !coll && !fast) {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
                 if (!(debug_skip & 2))
@@ -873,10 +914,17 @@ struct infllm_engine {
             }
         }
 
+        if (flag_mode && !(do_lookup && last_lkp_fast)) {
+            launch_flag_set(L.ready.as<int64_t>(), L.step, side);
+            ++launches;
+        }
         rec(e_topk, side);
-        if (!(debug_skip & 32)) wt(main, e_topk);  // 32: timing experiment only
+        if (!flag_mode && !(debug_skip & 32)) wt(main, e_topk);  // 32: timing experiment only
         if (tier_slots > 0 && n_sel > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
             wt(tier_st, e_topk);
+            // k_tier_assign keeps the slots of steps k-1 and k: the attention of k-2 must be done
+            const int b2 = static_cast<int>((kseq + kSB - 2) % kSB);
+            if (lru_seq[b2] == kseq - 2 && (capture_seq0 < 0 || lru_seq[b2] >= capture_seq0)) wt(tier_st, e_lru[b2]);
             TierParams tp2{};
             tp2.sel = sel_b;
             tp2.sel_slot = L.sel_slot.as<int32_t>() + b * std::max<int64_t>(cfg.n_lookup, 1);
@@ -907,8 +955,8 @@ struct infllm_engine {
         rec(e_lookup, side);
         lookup_seq = kseq;
         // this parity's mass buffers were last read by LRU(k-2)
-        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
-            wt(main, e_lru[b]);
+        if (!flag_mode && lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+            wt(main, e_lru[b]);  // flag mode: the lookup waited for it
         st = main;
         double* mass_cta_b = mass_cta.as<double>() + b * mass_cta_half;
         double* mass_part_b = L.mass_part.as<double>() + b * std::max<int64_t>(cfg.n_lookup, 1) * Gt;
@@ -996,7 +1044,9 @@ struct infllm_engine {
                 }
                 ++launches;
             } else if (tc_eligible(lx)) {
-                ap.pdl = attn_pdl && !fork && !one_stream ? 1 : 0;
+                ap.pdl = !fork && !one_stream ? attn_pdl : 0;
+                ap.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
+                ap.ready_val = L.step;
                 launches += launch_attn_tc(ap, st);
             } else {
                 launch_attn_simt<T>(ap, st);
@@ -1089,7 +1139,8 @@ struct infllm_engine {
         st = side;
 
         if (one_stream) {  // nothing else was recorded: no later step may wait on those events
-            if (!lru_side) lru_seq[0] = lru_seq[1] = -1;
+            if (!lru_side)
+                for (auto& x : lru_seq) x = -1;
             for (auto& a2 : attn_seq) a2 = -1;
             lookup_seq = evict_seq = tier_seq = -1;
         }
@@ -1403,7 +1454,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
         // ring: the local window, the chunk being attended and the two chunks the
         // prep stream may run ahead by never share a slot
-        const int64_t need = cfg->local_size + (1 + infllm_engine::kPrepAhead) * cfg->chunk_size + 1;
+        const int64_t need = cfg->local_size + infllm_engine::kPB * cfg->chunk_size + 1;
         e->R = (need + 127) / 128 * 128;
         e->lxp = (cfg->chunk_size + 127) / 128 * 128;
         for (int a = 0; a < e->d / 2; ++a) {  // rotary.hpp:25-30 (RotaryTable::make)
@@ -1434,10 +1485,11 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
         ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
         ck(cudaStreamCreateWithFlags(&e->tier_stream, cudaStreamNonBlocking), "tier stream");
-        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_attn, &e->e_lrudone,
-                         &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone, &e->e_attnp[0],
-                         &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
+        for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_lru[2], &e->e_attn,
+                         &e->e_lrudone, &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone,
+                         &e->e_attnp[0], &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
+        e->prep_sync.alloc(prep_chunk_sync_bytes(), st);
         e->chunk_qsum.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
         e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
@@ -1450,7 +1502,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->tsum.alloc(static_cast<size_t>((cfg->chunk_size + 15) / 16) * e->Gs * e->d * sizeof(double), st);
         e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
         e->mass_cta_half = static_cast<int64_t>(e->Hs) * (e->lxp / 128) * km;
-        e->mass_cta.alloc(2 * e->mass_cta_half * sizeof(double), st);
+        e->mass_cta.alloc(infllm_engine::kSB * e->mass_cta_half * sizeof(double), st);
         if (e->use_dec) {
             e->dec_part.alloc(dec_part_floats(1, e->Gs, e->rep) * sizeof(float), st, false);
             e->dec_mass.alloc(static_cast<size_t>(e->Hs) * km * kDecWarps * 2 * sizeof(float), st);
@@ -1463,6 +1515,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ring_v.alloc(static_cast<size_t>(e->Gs) * e->R * e->dv * es, st);
             L.P.alloc(static_cast<size_t>(e->R) * e->Gs * e->d * sizeof(double), st);
             L.kmax2.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * sizeof(float), st);
+            L.ready.alloc(sizeof(int64_t), st);
             const size_t ni = static_cast<size_t>(std::max<int64_t>(cfg->init_size, 1));
             L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
             if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
@@ -1470,8 +1523,8 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.init_v.alloc(static_cast<size_t>(e->Gs) * (e->vl.vt ? e->vl.nI * 128 : ni) * e->dv * es, st);
             L.hot_list.alloc(static_cast<size_t>(cfg->hot_capacity + km + 1) * sizeof(int64_t), st);
             L.lru.alloc(sizeof(LruState), st);
-            L.sel.alloc(2 * km * sizeof(int64_t), st);
-            L.mass_part.alloc(2 * km * e->Gt * sizeof(double), st);
+            L.sel.alloc(infllm_engine::kSB * km * sizeof(int64_t), st);
+            L.mass_part.alloc(infllm_engine::kSB * km * e->Gt * sizeof(double), st);
             L.ev_part.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gt * sizeof(double), st);
         }
         ck(cudaStreamSynchronize(st), "engine_create");
@@ -1500,9 +1553,9 @@ int infllm_engine_destroy(infllm_engine_t e) {
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
                         e->evict_stream, e->tier_stream})
             if (s2) cudaStreamDestroy(s2);
-        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_attn, e->e_lrudone, e->e_prep,
-                        e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone, e->e_attnp[0], e->e_attnp[1],
-                        e->e_attnp[2], e->e_tier, e->e_tierdone})
+        for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_lru[2], e->e_attn,
+                        e->e_lrudone, e->e_prep, e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone,
+                        e->e_attnp[0], e->e_attnp[1], e->e_attnp[2], e->e_tier, e->e_tierdone})
             if (ev) cudaEventDestroy(ev);
         cudaDeviceSynchronize();
         if (e->bctx) {
@@ -1579,7 +1632,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // captured stream graphs bake in the launch choices these options make:
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
-            k == "attn_pdl" || k == "debug_skip") {
+            k == "attn_pdl" || k == "lookup_units_per_block" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1596,8 +1649,16 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->dec_disabled = value == 0;
         else if (k == "multi_stream_decode")
             e->multi_stream_decode = value != 0;
+        else if (k == "prep_fused")
+            e->prep_fused = value != 0;
+        else if (k == "prep_blocks")
+            e->prep_blocks = static_cast<int>(std::clamp<int64_t>(value, 0, 1 << 20));
+        else if (k == "attn_flag")
+            e->attn_flag = value != 0;
+        else if (k == "lookup_units_per_block")
+            e->lookup_upb = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
         else if (k == "attn_pdl")
-            e->attn_pdl = value != 0;
+            e->attn_pdl = static_cast<int>(std::clamp<int64_t>(value, -(1 << 20), 1 << 20));
 
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
@@ -2024,8 +2085,14 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         lp.sel = ids;
         cnt.grow(64, st);  // block counter of the folded merge (zeroed once, re-zeroed by the kernel)
         lp.done = cnt.as<unsigned int>();
-        launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
-                           reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
+        lp.fused = 1;
+        lp.cand_v = cand.as<double>();
+        lp.cand_i = reinterpret_cast<int64_t*>(cand.as<double>() + nc);
+        if (lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16))
+            launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units, 8), st);
+        else
+            launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
+                               reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
         ck(cudaGetLastError(), "lookup");
         ck(cudaEventRecord(last, st), "record");
     });
@@ -2127,6 +2194,8 @@ void timeline_bind(const TlBuf& b) {
     ck(tl_bind_kernels(b), "timeline bind");
     ck(tl_bind_attn_tc(b), "timeline bind");
     ck(tl_bind_attn_dec(b), "timeline bind");
+    ck(tl_bind_lookup(b), "timeline bind");
+    ck(tl_bind_side(b), "timeline bind");
 }
 }  // namespace
 

@@ -26,6 +26,9 @@ __device__ unsigned long long g_dbg_ts[64];
 
 cudaError_t tl_bind_kernels(const TlBuf& b) { return tl_bind_tu(b); }
 
+__global__ void k_flag_set(int64_t* f, int64_t v) { flag_release(f, v); }
+void launch_flag_set(int64_t* flag, int64_t val, cudaStream_t st) { k_flag_set<<<1, 1, 0, st>>>(flag, val); }
+
 void debug_read_timestamps(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, g_dbg_ts, sizeof(unsigned long long) * 64);
 }
@@ -149,9 +152,8 @@ __global__ void __launch_bounds__(1024) k_prefix(PrepParams p) {
 
 // ---- vectorised prep path (head_dim, value_dim multiples of 8) ----------------
 // (1) per-step rotation-factor table: one fp64 sincos per (token, pair)
-__device__ __forceinline__ void rope_table_body(const PrepParams& p) {
+__device__ __forceinline__ void rope_table_body(const PrepParams& p, int64_t t) {
     const int pairs = p.d / 2;
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p.kmax2 && t < p.G) p.kmax2[t] = p.kmax2_prev[t];  // k_prep_tok raises it with this chunk's keys
     if (t >= p.lx * pairs) return;
     const int64_t i = t / pairs;
@@ -162,7 +164,9 @@ __device__ __forceinline__ void rope_table_body(const PrepParams& p) {
 }
 __global__ void k_rope_table(PrepParams p) {
     TL_BEGIN();
-    rope_table_body(p);
+    const int64_t n = p.lx * (p.d / 2), stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < (n > p.G ? n : p.G); t += stride)
+        rope_table_body(p, t);
     TL_END(TL_ROPE);
 }
 
@@ -460,12 +464,11 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep_fused(PrepParams p) {
 // group query sums go to qs[token][g][:] plus a per-tile column sum.
 constexpr int kTokTile = 16;
 template <typename T>
-__device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
+__device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g) {
     __shared__ double sqs[kTokTile][128 + 2];
     __shared__ T svt[128][kTokTile + 2];
-    const int g = blockIdx.y;
     const int tt = threadIdx.x / 16, c8 = threadIdx.x % 16;  // token in tile, dim chunk
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * kTokTile + tt;
+    const int64_t i = static_cast<int64_t>(bx) * kTokTile + tt;
     const bool live = i < p.lx;
     const int64_t pos = p.s + i;
     const T* qg = static_cast<const T*>(p.q);
@@ -548,11 +551,11 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
         const int c = threadIdx.x;
         double a = 0.0;
         for (int t = 0; t < kTokTile; ++t) a += sqs[t][c];
-        p.tsum[(static_cast<int64_t>(blockIdx.x) * p.G + g) * p.d + c] = a;
+        p.tsum[(static_cast<int64_t>(bx) * p.G + g) * p.d + c] = a;
     }
     if (p.vl.vt) {
         // transposed value page rows: 16 consecutive positions of one dim
-        const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTokTile;
+        const int64_t i0 = static_cast<int64_t>(bx) * kTokTile;
         const int nt = static_cast<int>(min(static_cast<int64_t>(kTokTile), p.lx - i0));
         T* rv = static_cast<T*>(p.ring_v);
         for (int t = threadIdx.x; t < 128 * kTokTile; t += blockDim.x) {
@@ -565,14 +568,18 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
     TL_BEGIN();
-    prep_tok_body<T>(p);
+    const int tiles = static_cast<int>((p.lx + kTokTile - 1) / kTokTile);
+    for (int item = blockIdx.x; item < tiles * p.G; item += gridDim.x) {
+        prep_tok_body<T>(p, item % tiles, item / tiles);
+        __syncthreads();  // shared tiles are reused by the next item
+    }
     TL_END(TL_PREP);
 }
 
 // (6) fp64 prefix into the P ring from the per-token sums and the tile sums:
 // block = (tile, group), thread = dim; rows of P written whole (coalesced).
-__device__ __forceinline__ void prefix_tiles_body(const PrepParams& p) {
-    const int tile = blockIdx.x, g = blockIdx.y, c = threadIdx.x;
+__device__ __forceinline__ void prefix_tiles_body(const PrepParams& p, int tile, int g, int ntiles) {
+    const int c = threadIdx.x;
     if (c >= p.d) return;
     const int64_t stride = static_cast<int64_t>(p.G) * p.d;
     double run = p.P[((p.s % p.R) * p.G + g) * p.d + c];
@@ -596,15 +603,17 @@ __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p) {
         run += v[j];
         p.P[(((p.s + i0 + j + 1) % p.R) * p.G + g) * p.d + c] = run;
     }
-    if (tile == gridDim.x - 1) {  // chunk total = sum of the tile sums, in order
+    if (tile == ntiles - 1) {  // chunk total = sum of the tile sums, in order
         double all = 0.0;
-        for (int t = 0; t < static_cast<int>(gridDim.x); ++t) all += p.tsum[t * stride + g * p.d + c];
+        for (int t = 0; t < ntiles; ++t) all += p.tsum[t * stride + g * p.d + c];
         p.chunk_qsum[g * p.d + c] = all;
     }
 }
 __global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
     TL_BEGIN();
-    prefix_tiles_body(p);
+    const int tiles = static_cast<int>((p.lx + kTokTile - 1) / kTokTile);
+    for (int item = blockIdx.x; item < tiles * p.G; item += gridDim.x)
+        prefix_tiles_body(p, item % tiles, item / tiles, tiles);
     TL_END(TL_PREFIX);
 }
 
@@ -613,9 +622,11 @@ void launch_prep(const PrepParams& p, cudaStream_t st) {
     if (p.d == 128 && p.dv == 128 && p.rep <= 8 && p.rtab && p.tsum) {
         const int64_t nt = p.lx * (p.d / 2);
         const unsigned tiles = static_cast<unsigned>((p.lx + kTokTile - 1) / kTokTile);
-        k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
-        k_prep_tok<T><<<dim3(tiles, p.G), 256, 0, st>>>(p);
-        k_prefix_tiles<<<dim3(tiles, p.G), 128, 0, st>>>(p);
+        const unsigned items = tiles * static_cast<unsigned>(p.G);
+        const unsigned cap = p.max_blocks > 0 ? static_cast<unsigned>(p.max_blocks) : items;
+        k_rope_table<<<std::min(static_cast<unsigned>((nt + 255) / 256), cap), 256, 0, st>>>(p);
+        k_prep_tok<T><<<std::min(items, cap), 256, 0, st>>>(p);
+        k_prefix_tiles<<<std::min(items, cap), 128, 0, st>>>(p);
         return;
     }
     if (p.d % 8 == 0 && p.dv == p.d && p.rep <= 8 && p.rtab) {
@@ -798,7 +809,7 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
 __global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
     // a decode step's K4 may start its CTAs that do not read the selection now
     // (programmatic dependent launch; those that do wait for this grid)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (p.early_dependents) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     TL_BEGIN();
     lookup_reg_body(p, gridDim.x);
     TL_END(TL_LOOKUP);
@@ -1206,7 +1217,7 @@ __device__ void merge_candidates(const double* cv, const int64_t* ci, int64_t n,
 }
 // fold != 0: the last block to finish merges the candidates (no merge launch)
 __global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p, int fold) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the merge block / K4 may launch (PDL)
+    if (p.early_dependents) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // merge block / K4 (PDL)
     TL_BEGIN();
     lookup_stream_body(p, gridDim.x);
     TL_END(TL_LOOKUP);
@@ -1240,7 +1251,8 @@ __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const
 constexpr int kScanBlocks = 148;  // streaming scan: one block per SM, one slice each
 int64_t topk_multi_scratch(int64_t U, int64_t k) {
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
-    return (nb > kScanBlocks ? nb : kScanBlocks) * k;
+    const int64_t n = (nb > kScanBlocks ? nb : kScanBlocks) * k;
+    return n > 148 * 32 ? n : 148 * 32;  // also the block lists of k_lookup_topk (lookup.cu)
 }
 int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
     p.fused = 2;
@@ -2365,12 +2377,14 @@ size_t dec_front_size() { return sizeof(DecFront); }
 
 // ---- batched decode: one launch per stage for B sequences (grid.z = sequence;
 // per-sequence parameter tables in device memory) -------------------------------
-__global__ void k_rope_table_b(const PrepParams* __restrict__ ps) { rope_table_body(ps[blockIdx.z]); }
+__global__ void k_rope_table_b(const PrepParams* __restrict__ ps) {
+    rope_table_body(ps[blockIdx.z], static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
+}
 __global__ void __launch_bounds__(256) k_prep_tok_b(const PrepParams* __restrict__ ps) {
-    prep_tok_body<bf16>(ps[blockIdx.z]);
+    prep_tok_body<bf16>(ps[blockIdx.z], blockIdx.x, blockIdx.y);
 }
 __global__ void __launch_bounds__(128) k_prefix_tiles_b(const PrepParams* __restrict__ ps) {
-    prefix_tiles_body(ps[blockIdx.z]);
+    prefix_tiles_body(ps[blockIdx.z], blockIdx.x, blockIdx.y, gridDim.x);
 }
 __global__ void __launch_bounds__(256) k_evict_tok_b(const EvictParams* __restrict__ ps) {
     const EvictParams& p = ps[blockIdx.z];

@@ -59,6 +59,8 @@ struct PrepParams {
     const float* kmax2_prev;  // [G] the previous step's copy
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
+    int max_blocks;  // grid cap of the chunk prep kernels (0: one block per work item)
+    void* sync;      // k_prep_chunk look-back state (prep_chunk_sync_bytes, zeroed once), or null
     VLayout vl;
     RopeFreqs freqs;
 };
@@ -75,6 +77,9 @@ struct LookupParams {
     int fused;           // 1: single shard: rel + top-k in this launch; 2: rel only (multi-block top-k follows)
     double* cand_v;      // fused 2, streaming scan: per-block top-k candidates [gridDim][n_sel]
     int64_t* cand_i;
+    int early_dependents;  // 1: let a programmatic dependent (decode K4) launch at kernel entry
+    int64_t* ready_flag;   // non-null: the last block publishes ready_val here once sel is written
+    int64_t ready_val;
 };
 
 struct TopkParams {
@@ -114,6 +119,10 @@ struct AttnParams {
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;
     int pdl;  // K3: programmatic dependent launch after the previous kernel on its stream
+    // K3 in the prefill pipeline: wait until *ready_flag >= ready_val (published by the
+    // lookup of this step, which itself followed the prep, eviction and LRU it needs)
+    const int64_t* ready_flag;
+    int64_t ready_val;
     float scale;
     VLayout vl;
 };
@@ -232,10 +241,20 @@ struct SelectParams {
 };
 
 void debug_read_timestamps(unsigned long long* out);
+// publish a step-ready flag (release) from a stream: steps whose lookup does not set it
+void launch_flag_set(int64_t* flag, int64_t val, cudaStream_t st);
+// side.cu: one-kernel chunk prep (bf16, d = dv = 128, transposed values), bitwise
+// equal to rope table + k_prep_tok + k_prefix_tiles; 32-token tiles, lx <= 32 * kPrepChunkMaxTiles
+constexpr int kPrepChunkMaxTiles = 64;
+size_t prep_chunk_sync_bytes();
+bool prep_chunk_supported(const PrepParams& p);
+void launch_prep_chunk(const PrepParams& p, cudaStream_t st);
+cudaError_t tl_bind_side(const TlBuf& b);
 // bind the device timeline buffer in each translation unit (kernels.cu, attn_tc.cu, attn_dec.cu)
 cudaError_t tl_bind_kernels(const TlBuf& b);
 cudaError_t tl_bind_attn_tc(const TlBuf& b);
 cudaError_t tl_bind_attn_dec(const TlBuf& b);
+cudaError_t tl_bind_lookup(const TlBuf& b);
 template <typename T> void launch_prep(const PrepParams& p, cudaStream_t st);
 void launch_lookup(const LookupParams& p, int dtype_bf16, cudaStream_t st);
 void launch_topk(const TopkParams& p, cudaStream_t st);
@@ -244,6 +263,11 @@ void launch_topk(const TopkParams& p, cudaStream_t st);
 // returns the number of kernels launched
 int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st);
 int64_t topk_multi_scratch(int64_t U, int64_t k);
+// lookup.cu: relevance scan + exact top-k (k_m <= 32) in one launch; candidates
+// p.cand_v / p.cand_i hold blocks x 32 entries (within topk_multi_scratch)
+bool lookup_topk_supported(const LookupParams& p, int dtype_bf16);
+int lookup_topk_blocks(int64_t U, int units_per_block);
+void launch_lookup_topk_fast(const LookupParams& p, int blocks, cudaStream_t st);
 int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                        cudaStream_t st);
 template <typename T> void launch_attn_simt(const AttnParams& p, cudaStream_t st);

@@ -54,6 +54,11 @@ base = t0.min()
 t0 -= base
 t1 -= base
 print(f"stream {ev0.elapsed_time(ev1):.3f} ms (timeline on), {m} block records")
+for k in range(100, 120):  # kernel phase marks (kid >= 100)
+    sel = kid == k
+    if sel.any():
+        d = (t1[sel] - t0[sel]) / 1e3
+        print(f"  phase {k - 100:3d}: n {sel.sum():6d} us mean {d.mean():7.2f} median {np.median(d):7.2f} max {d.max():7.2f}")
 for k in range(len(KINDS)):
     sel = kid == k
     if sel.any():
@@ -101,3 +106,38 @@ if nl > 101:
                   f"end max {(t1[s2].max() - a) / 1e3:8.2f} SMs {len(np.unique(sm[s2]))}")
     print(f"  attn 100: start [0, {(rows[100, 1] - a) / 1e3:.2f}] end [{(rows[100, 2] - a) / 1e3:.2f}, "
           f"{(rows[100, 3] - a) / 1e3:.2f}]; attn 101 start [{(rows[101, 0] - a) / 1e3:.2f}, {(rows[101, 1] - a) / 1e3:.2f}]")
+
+
+def launches(k, thr_ns=10000):
+    """Segments the blocks of kernel kind k into launches by start-time gaps."""
+    idx = np.where(kid == k)[0]
+    idx = idx[np.argsort(t0[idx])]
+    if len(idx) == 0:
+        return np.zeros((0, 4))
+    cut = np.where(np.diff(t0[idx]) > thr_ns)[0] + 1
+    segs = np.split(idx, cut)
+    return np.array([(t0[s].min(), t0[s].max(), t1[s].max(), len(s)) for s in segs], np.float64)
+
+
+LK = {KINDS[k]: launches(k) for k in range(1, len(KINDS)) if (kid == k).any()}
+print("launch counts:", {k: len(v) for k, v in LK.items()})
+# for each attention launch i >= 20: the latest-ending launch of each kind that ended before A_i's first CTA start
+slack = {k: [] for k in LK}
+for i in range(20, nl):
+    s0 = rows[i, 0]
+    for k, v in LK.items():
+        before = v[v[:, 2] <= s0]
+        if len(before):
+            slack[k].append((s0 - before[:, 2].max()) / 1e3)
+prev_end = (rows[20:, 0] - rows[19:-1, 3]) / 1e3
+print(f"A_i first start - A_(i-1) last end: median {np.median(prev_end):.2f} p90 {np.percentile(prev_end, 90):.2f}")
+for k, v in slack.items():
+    if v:
+        v = np.array(v)
+        print(f"A_i first start - last {k:9s} end: median {np.median(v):7.2f} p10 {np.percentile(v, 10):7.2f} "
+              f"min {v.min():7.2f}")
+for k, v in LK.items():
+    d = (v[:, 2] - v[:, 0]) / 1e3
+    sp = (v[:, 1] - v[:, 0]) / 1e3
+    print(f"{k:9s} launch span us median {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f}; block start spread "
+          f"median {np.median(sp):6.2f}; blocks/launch {np.median(v[:, 3]):.0f}")
