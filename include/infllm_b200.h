@@ -271,6 +271,89 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
                   int64_t r_k, int32_t n_kv_heads, int32_t head_dim, int64_t k_m, double* rel,
                   int64_t* ids, void* stream);
 
+/* ---- stand-alone reference operators (the pieces StreamEngine::step composes) ---- */
+
+/* blockmem::Segment kinds (attention.hpp:14-26) */
+#define INFLLM_SEG_INITIAL 0
+#define INFLLM_SEG_RETRIEVED 1
+#define INFLLM_SEG_LOCAL 2
+
+/* blockmem::SegmentView (attention.hpp:28-51): one window segment; keys are
+ * raw (un-rotated, rotary.hpp is applied at attention time). Device pointers,
+ * token-major, element type = dtype. */
+typedef struct infllm_segment {
+    int32_t kind;        /* INFLLM_SEG_* */
+    int64_t start_abs;   /* absolute position of the first token */
+    int64_t n_tokens;
+    const void* keys;    /* [n_tokens][n_kv_heads][head_dim] */
+    const void* values;  /* [n_tokens][n_kv_heads][value_dim] */
+} infllm_segment;
+
+/* blockmem::attend (attention.hpp:116-230): the batch q/k/v [l_x][heads][dim]
+ * (device) at absolute positions start_abs.. attends over the window
+ * segments in order, then causally over itself; clamped or absolute
+ * positions per position_mode with l_L = local_size. out [l_x][n_heads][dv].
+ * seg_mass (device, may be NULL): per segment sum over heads, rows and its
+ * columns of the softmax weights / n_heads (the unit mass of
+ * engine.hpp:271-283, for retrieved segments). weights (device, may be NULL):
+ * the full weights [n_heads][l_x][n_ctx + l_x] (emit_weights,
+ * attention.hpp:227). Asynchronous on stream except for a small parameter
+ * upload. */
+int infllm_attend(const infllm_model_shape* shape, int32_t dtype, int32_t position_mode, int64_t local_size,
+                  const infllm_segment* window, int32_t n_segments, const void* q, const void* k,
+                  const void* v, int64_t l_x, int64_t start_abs, void* out, double* seg_mass, float* weights,
+                  void* stream);
+
+/* blockmem::TieredStore (memory.hpp:170-323) on the device: the
+ * representative index ([units][n_kv_heads][r_k][head_dim], dtype), decayed
+ * frequency scores, hot tier, counters and trace. Store calls are
+ * synchronous (they return the reference's StreamError conditions). */
+typedef struct infllm_store* infllm_store_t;
+/* TieredStore(hot_capacity, decay, n_heads) (memory.hpp:172-175) + the
+ * index shape; bytes_per_token feeds hot_bytes (MemoryUnit::bytes). */
+int infllm_store_create(int64_t hot_capacity, double decay, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                        int64_t n_repr, int32_t dtype, int64_t bytes_per_token, infllm_store_t* out);
+int infllm_store_destroy(infllm_store_t s);
+/* add_unit (memory.hpp:196-212): the next unit id; repr_keys [n][n_kv][d]
+ * (device, n <= n_repr representative keys); the unit holds unit_tokens
+ * tokens; it starts cold. */
+int infllm_store_add_unit(infllm_store_t s, const void* repr_keys, int64_t n, int64_t unit_tokens,
+                          int64_t* unit_id);
+/* begin_step (memory.hpp:214): the step id the next lookup records. */
+int infllm_store_begin_step(infllm_store_t s, int64_t step);
+/* relevance_all + lookup (memory.hpp:217-269): batch queries q
+ * [l_x][n_heads][d] (device) -> ids (host, ascending, min(k_m, units)),
+ * hit/miss bookkeeping and trace; rel (device, may be NULL) [units] fp64. */
+int infllm_store_lookup(infllm_store_t s, const void* q, int64_t l_x, int64_t k_m, int64_t* host_ids, int64_t* n_ids,
+                        double* rel);
+/* update_frequency (memory.hpp:273-281): host (id, mass) pairs. */
+int infllm_store_update_frequency(infllm_store_t s, const int64_t* host_ids, const double* host_mass, int64_t n);
+/* enforce_capacity (memory.hpp:285-300) and note_step_boundary (303-308). */
+int infllm_store_enforce_capacity(infllm_store_t s);
+int infllm_store_note_step_boundary(infllm_store_t s);
+/* counters (memory.hpp:151-157,181): units, hot_units, peaks, hits, misses,
+ * loads, evictions, requested. */
+int infllm_store_counters(infllm_store_t s, infllm_layer_metrics* m);
+/* trace (memory.hpp:159-163,182) and per-unit s_b / tier (memory.hpp:27). */
+int infllm_store_trace(infllm_store_t s, int64_t* host_step, int64_t* host_unit, int32_t* host_hit, int64_t cap,
+                       int64_t* n_out);
+int infllm_store_unit_freq(infllm_store_t s, double* host_freq, int32_t* host_hot, int64_t n);
+
+/* blockmem::ScoreAccumulator (repr_score.hpp:21-89): fp64 band sums of the
+ * queries each pending key will see before it leaves the local window. */
+typedef struct infllm_score_acc* infllm_score_acc_t;
+int infllm_score_acc_create(int64_t local_size, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                            int32_t dtype, infllm_score_acc_t* out);
+int infllm_score_acc_destroy(infllm_score_acc_t a);
+/* accumulate (repr_score.hpp:39-69): batch q [l_x][n_heads][d] (device) at
+ * absolute position s; pending_keys [n_pending][n_kv][d] (device) covering
+ * every pending token [lo, s + l_x). Errors as the reference's StreamError. */
+int infllm_score_acc_accumulate(infllm_score_acc_t a, const void* q, int64_t l_x, int64_t s,
+                                const void* pending_keys, int64_t n_pending, void* stream);
+/* finalize_front (repr_score.hpp:72-82): the first n scores (sum / l_L as
+ * float) into host_out, and drops them. Synchronous. */
+int infllm_score_acc_finalize_front(infllm_score_acc_t a, int64_t n, float* host_out);
+
 /* Diagnostic: steady-state per-launch time (us) of one kernel family
  * (0 prep, 1 lookup + fused top-k, 2 attention, 3 evict + fused select,
  * 4 LRU) re-launched with the parameters of the engine's last step.

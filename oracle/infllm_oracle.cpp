@@ -1405,4 +1405,212 @@ int32_t oracle_gen_planted(uint64_t seed, int64_t length, int64_t plant_len, con
     });
 }
 
+
+// ---- stand-alone operators (the C-ABI's infllm_attend / infllm_store_* / infllm_score_acc_*) ----
+
+struct oracle_store {
+    TieredStore s;
+    int Hkv = 1, d = 0;
+};
+
+oracle_store* oracle_store_create(int64_t hot_capacity, double decay, int32_t H, int32_t Hkv, int32_t d,
+                                  int64_t bytes_per_token) {
+    auto* x = new oracle_store();
+    x->s.hot_capacity = hot_capacity;  // TieredStore(hot_capacity, decay, n_heads) (memory.hpp:172-175)
+    x->s.decay = decay;
+    x->s.H = H;
+    x->s.rep = H / Hkv;
+    x->s.repr_index.resize(static_cast<size_t>(Hkv));
+    x->s.unit_bytes_per_token = static_cast<std::size_t>(bytes_per_token);
+    x->Hkv = Hkv;
+    x->d = d;
+    return x;
+}
+void oracle_store_destroy(oracle_store* x) { delete x; }
+
+// add_unit (memory.hpp:196-212); repr_keys [n][Hkv][d]
+int32_t oracle_store_add_unit(oracle_store* x, const float* repr_keys, int64_t n, int64_t unit_tokens, int64_t* id) {
+    return guard([&] {
+        MemoryUnit u;
+        u.unit_id = x->s.total_units();
+        for (int g = 0; g < x->Hkv; ++g) {
+            u.keys.emplace_back(unit_tokens, 0);  // only the size matters here (hot_bytes)
+            Mat<Scalar> rk(n, x->d);
+            for (Index r = 0; r < n; ++r)
+                std::memcpy(rk.row(r), repr_keys + (r * x->Hkv + g) * x->d, sizeof(Scalar) * static_cast<size_t>(x->d));
+            u.repr_keys.push_back(std::move(rk));
+        }
+        if (id) *id = u.unit_id;
+        x->s.add_unit(std::move(u));
+    });
+}
+int32_t oracle_store_begin_step(oracle_store* x, int64_t step) {
+    x->s.step = step;
+    return 0;
+}
+// lookup (memory.hpp:239-269); q [l_x][H][d]
+int32_t oracle_store_lookup(oracle_store* x, const float* q, int64_t l_x, int64_t k_m, int64_t* ids, int64_t* n) {
+    return guard([&] {
+        std::vector<Mat<Scalar>> qh;
+        for (int h = 0; h < x->s.H; ++h) {
+            Mat<Scalar> m(l_x, x->d);
+            for (Index i = 0; i < l_x; ++i)
+                std::memcpy(m.row(i), q + (i * x->s.H + h) * x->d, sizeof(Scalar) * static_cast<size_t>(x->d));
+            qh.push_back(std::move(m));
+        }
+        const auto r = x->s.lookup(qh, k_m);
+        for (size_t i = 0; i < r.size(); ++i) ids[i] = r[i];
+        *n = static_cast<int64_t>(r.size());
+    });
+}
+int32_t oracle_store_update_frequency(oracle_store* x, const int64_t* ids, const double* mass, int64_t n) {
+    return guard([&] {
+        std::vector<std::pair<std::int64_t, double>> m;
+        for (int64_t i = 0; i < n; ++i) m.emplace_back(ids[i], mass[i]);
+        x->s.update_frequency(m);
+    });
+}
+int32_t oracle_store_enforce_capacity(oracle_store* x) {
+    return guard([&] { x->s.enforce_capacity(); });
+}
+int32_t oracle_store_note_step_boundary(oracle_store* x) {
+    return guard([&] { x->s.note_step_boundary(); });
+}
+int32_t oracle_store_counters(oracle_store* x, infllm_layer_metrics* m) {
+    *m = x->s.counters;
+    m->units = x->s.total_units();
+    m->hot_units = static_cast<int64_t>(x->s.hot.size());
+    m->peak_hot_units = x->s.peak_hot_units;
+    m->peak_hot_bytes = static_cast<int64_t>(x->s.peak_hot_bytes);
+    return 0;
+}
+int32_t oracle_store_trace(oracle_store* x, int64_t* step, int64_t* unit, int32_t* hit, int64_t cap, int64_t* n_out) {
+    const auto& t = x->s.trace;
+    *n_out = static_cast<int64_t>(t.size());
+    for (int64_t i = 0; i < std::min<int64_t>(cap, static_cast<int64_t>(t.size())); ++i) {
+        step[i] = t[static_cast<size_t>(i)].step;
+        unit[i] = t[static_cast<size_t>(i)].unit_id;
+        hit[i] = t[static_cast<size_t>(i)].hit ? 1 : 0;
+    }
+    return 0;
+}
+int32_t oracle_store_unit_freq(oracle_store* x, double* freq, int32_t* hot, int64_t n) {
+    for (int64_t i = 0; i < std::min<int64_t>(n, x->s.total_units()); ++i) {
+        freq[i] = x->s.units[static_cast<size_t>(i)].freq_score;
+        hot[i] = x->s.units[static_cast<size_t>(i)].hot ? 1 : 0;
+    }
+    return 0;
+}
+
+struct oracle_score_acc {
+    ScoreAccumulator a;
+    int H = 1, Hkv = 1, d = 0;
+};
+oracle_score_acc* oracle_score_acc_create(int64_t local_size, int32_t H, int32_t Hkv, int32_t d) {
+    auto* x = new oracle_score_acc{ScoreAccumulator{local_size, 0, 0, 0, {}, 1}, H, Hkv, d};
+    return x;
+}
+void oracle_score_acc_destroy(oracle_score_acc* x) { delete x; }
+// accumulate (repr_score.hpp:39-69): q [l_x][H][d], keys [n_pending][Hkv][d]
+int32_t oracle_score_acc_accumulate(oracle_score_acc* x, const float* q, int64_t l_x, int64_t s, const float* keys,
+                                    int64_t n_pending) {
+    return guard([&] {
+        std::vector<Mat<Scalar>> qh, kh;
+        for (int h = 0; h < x->H; ++h) {
+            Mat<Scalar> m(l_x, x->d);
+            for (Index i = 0; i < l_x; ++i)
+                std::memcpy(m.row(i), q + (i * x->H + h) * x->d, sizeof(Scalar) * static_cast<size_t>(x->d));
+            qh.push_back(std::move(m));
+        }
+        for (int g = 0; g < x->Hkv; ++g) {
+            Mat<Scalar> m(n_pending, x->d);
+            for (Index i = 0; i < n_pending; ++i)
+                std::memcpy(m.row(i), keys + (i * x->Hkv + g) * x->d, sizeof(Scalar) * static_cast<size_t>(x->d));
+            kh.push_back(std::move(m));
+        }
+        x->a.accumulate(s, qh, kh, x->H / x->Hkv);
+    });
+}
+int32_t oracle_score_acc_finalize_front(oracle_score_acc* x, int64_t n, float* out) {
+    return guard([&] {
+        const auto r = x->a.finalize_front(n);
+        for (size_t i = 0; i < r.size(); ++i) out[i] = r[i];
+    });
+}
+
+// attend (attention.hpp:116-230) over explicit segments; token-major host tensors
+int32_t oracle_attend(int32_t H, int32_t Hkv, int32_t d, int32_t dv, int32_t position_mode, int64_t local_size,
+                      const int32_t* seg_kind, const int64_t* seg_start, const int64_t* seg_n,
+                      const float* const* seg_keys, const float* const* seg_values, int32_t n_seg, const float* q,
+                      const float* k, const float* v, int64_t l_x, int64_t start_abs, float* out, double* seg_mass,
+                      float* weights) {
+    return guard([&] {
+        oracle_engine e;
+        e.cfg.local_size = local_size;
+        e.cfg.position_mode = position_mode;
+        e.H = H;
+        e.Hkv = Hkv;
+        e.rep = H / Hkv;
+        e.d = d;
+        e.dv = dv;
+        auto per_group = [&](const float* src, Index n, int cols) {
+            std::vector<Mat<Scalar>> m;
+            for (int g = 0; g < Hkv; ++g) {
+                Mat<Scalar> x(n, cols);
+                for (Index i = 0; i < n; ++i)
+                    std::memcpy(x.row(i), src + (i * Hkv + g) * cols, sizeof(Scalar) * static_cast<size_t>(cols));
+                m.push_back(std::move(x));
+            }
+            return m;
+        };
+        std::vector<std::vector<Mat<Scalar>>> sk, sv;
+        for (int s2 = 0; s2 < n_seg; ++s2) {
+            sk.push_back(per_group(seg_keys[s2], seg_n[s2], d));
+            sv.push_back(per_group(seg_values[s2], seg_n[s2], dv));
+        }
+        std::vector<SegmentView> segs;
+        Index n_ctx = 0;
+        for (int s2 = 0; s2 < n_seg; ++s2) {
+            SegmentView sg;
+            sg.kind = seg_kind[s2] == INFLLM_SEG_INITIAL ? Seg::initial
+                      : seg_kind[s2] == INFLLM_SEG_RETRIEVED ? Seg::retrieved
+                                                              : Seg::local;
+            sg.start_abs = seg_start[s2];
+            sg.unit_id = -1;
+            for (int g = 0; g < Hkv; ++g) {
+                sg.keys.push_back(&sk[static_cast<size_t>(s2)][static_cast<size_t>(g)]);
+                sg.values.push_back(&sv[static_cast<size_t>(s2)][static_cast<size_t>(g)]);
+            }
+            n_ctx += seg_n[s2];
+            segs.push_back(std::move(sg));
+        }
+        const auto bk = per_group(k, l_x, d), bv = per_group(v, l_x, dv);
+        const Index n_all = n_ctx + l_x;
+        std::vector<double> mass(static_cast<size_t>(n_seg), 0.0);
+        for (int h = 0; h < H; ++h) {
+            Mat<Scalar> qh(l_x, d), oh, wh;
+            for (Index i = 0; i < l_x; ++i)
+                std::memcpy(qh.row(i), q + (i * H + h) * d, sizeof(Scalar) * static_cast<size_t>(d));
+            e.attend_head(h, qh, start_abs, segs, bk[static_cast<size_t>(h / e.rep)], bv[static_cast<size_t>(h / e.rep)],
+                          oh, &wh);
+            for (Index i = 0; i < l_x; ++i)
+                for (int c = 0; c < dv; ++c) out[(i * H + h) * dv + c] = oh(i, c);
+            if (weights)
+                for (Index i = 0; i < l_x; ++i)
+                    std::memcpy(weights + (static_cast<int64_t>(h) * l_x + i) * n_all, wh.row(i),
+                                sizeof(Scalar) * static_cast<size_t>(n_all));
+            Index col = 0;  // engine.hpp:271-283
+            for (int s2 = 0; s2 < n_seg; ++s2) {
+                double m = 0.0;
+                for (Index i = 0; i < l_x; ++i)
+                    for (Index j = 0; j < seg_n[s2]; ++j) m += static_cast<double>(wh(i, col + j));
+                mass[static_cast<size_t>(s2)] += m;
+                col += seg_n[s2];
+            }
+        }
+        if (seg_mass)
+            for (int s2 = 0; s2 < n_seg; ++s2) seg_mass[s2] = mass[static_cast<size_t>(s2)] / H;
+    });
+}
+
 }  // extern "C"

@@ -92,6 +92,33 @@ double oracle_relevance_unit(const float* q, int64_t l_x, int32_t H, int32_t Hkv
 double oracle_mean_repr_relevance(const double* unit_keys, int64_t n, const double* q,
                                   int64_t l_x, int32_t H, int32_t Hkv, int32_t d);
 
+/* ---- stand-alone operators, mirroring the C-ABI's infllm_attend /
+ * infllm_store_* / infllm_score_acc_* ---- */
+typedef struct oracle_store oracle_store;
+oracle_store* oracle_store_create(int64_t hot_capacity, double decay, int32_t H, int32_t Hkv, int32_t d,
+                                  int64_t bytes_per_token);
+void oracle_store_destroy(oracle_store* x);
+int32_t oracle_store_add_unit(oracle_store* x, const float* repr_keys, int64_t n, int64_t unit_tokens, int64_t* id);
+int32_t oracle_store_begin_step(oracle_store* x, int64_t step);
+int32_t oracle_store_lookup(oracle_store* x, const float* q, int64_t l_x, int64_t k_m, int64_t* ids, int64_t* n);
+int32_t oracle_store_update_frequency(oracle_store* x, const int64_t* ids, const double* mass, int64_t n);
+int32_t oracle_store_enforce_capacity(oracle_store* x);
+int32_t oracle_store_note_step_boundary(oracle_store* x);
+int32_t oracle_store_counters(oracle_store* x, infllm_layer_metrics* m);
+int32_t oracle_store_trace(oracle_store* x, int64_t* step, int64_t* unit, int32_t* hit, int64_t cap, int64_t* n_out);
+int32_t oracle_store_unit_freq(oracle_store* x, double* freq, int32_t* hot, int64_t n);
+typedef struct oracle_score_acc oracle_score_acc;
+oracle_score_acc* oracle_score_acc_create(int64_t local_size, int32_t H, int32_t Hkv, int32_t d);
+void oracle_score_acc_destroy(oracle_score_acc* x);
+int32_t oracle_score_acc_accumulate(oracle_score_acc* x, const float* q, int64_t l_x, int64_t s, const float* keys,
+                                    int64_t n_pending);
+int32_t oracle_score_acc_finalize_front(oracle_score_acc* x, int64_t n, float* out);
+int32_t oracle_attend(int32_t H, int32_t Hkv, int32_t d, int32_t dv, int32_t position_mode, int64_t local_size,
+                      const int32_t* seg_kind, const int64_t* seg_start, const int64_t* seg_n,
+                      const float* const* seg_keys, const float* const* seg_values, int32_t n_seg, const float* q,
+                      const float* k, const float* v, int64_t l_x, int64_t start_abs, float* out, double* seg_mass,
+                      float* weights);
+
 /* ---- double-precision brute-force oracles (oracle.hpp) ---- */
 /* dense_attention (oracle.hpp:64-97); token-major double tensors */
 int32_t oracle_dense_attention(const double* q, const double* k, const double* v, int64_t n,

@@ -151,6 +151,26 @@ def lib():
                                            C.c_int32, f32p]
         L.oracle_gen_planted.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.POINTER(EngineConfig),
                                          C.c_int64, C.c_int32, i64p, i64p, i64p, i64p, i64p]
+        L.oracle_store_create.restype = P
+        L.oracle_store_create.argtypes = [C.c_int64, C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int64]
+        L.oracle_store_destroy.argtypes = [P]
+        L.oracle_store_add_unit.argtypes = [P, f32p, C.c_int64, C.c_int64, i64p]
+        L.oracle_store_begin_step.argtypes = [P, C.c_int64]
+        L.oracle_store_lookup.argtypes = [P, f32p, C.c_int64, C.c_int64, i64p, i64p]
+        L.oracle_store_update_frequency.argtypes = [P, i64p, f64p, C.c_int64]
+        L.oracle_store_enforce_capacity.argtypes = [P]
+        L.oracle_store_note_step_boundary.argtypes = [P]
+        L.oracle_store_counters.argtypes = [P, C.POINTER(LayerMetrics)]
+        L.oracle_store_trace.argtypes = [P, i64p, i64p, C.POINTER(C.c_int32), C.c_int64, i64p]
+        L.oracle_store_unit_freq.argtypes = [P, f64p, C.POINTER(C.c_int32), C.c_int64]
+        L.oracle_score_acc_create.restype = P
+        L.oracle_score_acc_create.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32]
+        L.oracle_score_acc_destroy.argtypes = [P]
+        L.oracle_score_acc_accumulate.argtypes = [P, f32p, C.c_int64, C.c_int64, f32p, C.c_int64]
+        L.oracle_score_acc_finalize_front.argtypes = [P, C.c_int64, f32p]
+        L.oracle_attend.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                    C.POINTER(C.c_int32), i64p, i64p, C.POINTER(f32p), C.POINTER(f32p), C.c_int32,
+                                    f32p, f32p, f32p, C.c_int64, C.c_int64, f32p, f64p, f32p]
         _lib = L
     return _lib
 
@@ -295,6 +315,116 @@ class OracleEngine:
 
 
 # ---------------------------------------------------------------- standalone
+class OracleStore:
+    """TieredStore (memory.hpp:170-323) on an explicit representative index."""
+
+    def __init__(self, hot_capacity, decay, H, Hkv, d, bytes_per_token):
+        self.Hkv, self.d = Hkv, d
+        self.h = lib().oracle_store_create(hot_capacity, decay, H, Hkv, d, bytes_per_token)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_store_destroy(self.h)
+            self.h = None
+
+    def add_unit(self, repr_keys, unit_tokens):
+        rk = f32(repr_keys)
+        uid = C.c_int64()
+        _check(lib().oracle_store_add_unit(self.h, _p(rk, C.c_float), rk.shape[0], unit_tokens, C.byref(uid)))
+        return uid.value
+
+    def begin_step(self, step):
+        lib().oracle_store_begin_step(self.h, step)
+
+    def lookup(self, q, k_m):
+        q = f32(q)
+        ids = np.zeros(max(1, k_m), np.int64)
+        n = C.c_int64()
+        _check(lib().oracle_store_lookup(self.h, _p(q, C.c_float), q.shape[0], k_m, _p(ids, C.c_int64), C.byref(n)))
+        return ids[: n.value].tolist()
+
+    def update_frequency(self, pairs):
+        ids = np.array([p[0] for p in pairs] or [0], np.int64)
+        ms = np.array([p[1] for p in pairs] or [0.0], np.float64)
+        _check(lib().oracle_store_update_frequency(self.h, _p(ids, C.c_int64), _p(ms, C.c_double), len(pairs)))
+
+    def enforce_capacity(self):
+        _check(lib().oracle_store_enforce_capacity(self.h))
+
+    def note_step_boundary(self):
+        _check(lib().oracle_store_note_step_boundary(self.h))
+
+    def counters(self):
+        m = LayerMetrics()
+        lib().oracle_store_counters(self.h, C.byref(m))
+        return m.as_dict()
+
+    def trace(self, cap=1 << 16):
+        st, un = np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+        hit = np.zeros(cap, np.int32)
+        n = C.c_int64()
+        lib().oracle_store_trace(self.h, _p(st, C.c_int64), _p(un, C.c_int64), _p(hit, C.c_int32), cap, C.byref(n))
+        k = min(n.value, cap)
+        return list(zip(st[:k].tolist(), un[:k].tolist(), hit[:k].tolist()))
+
+    def unit_freq(self, n):
+        f = np.zeros(max(1, n), np.float64)
+        hot = np.zeros(max(1, n), np.int32)
+        lib().oracle_store_unit_freq(self.h, _p(f, C.c_double), _p(hot, C.c_int32), n)
+        return f[:n], hot[:n]
+
+
+class OracleScoreAccumulator:
+    """ScoreAccumulator (repr_score.hpp:21-89)."""
+
+    def __init__(self, local_size, H, Hkv, d):
+        self.h = lib().oracle_score_acc_create(local_size, H, Hkv, d)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oracle_score_acc_destroy(self.h)
+            self.h = None
+
+    def accumulate(self, q, s, pending_keys):
+        q, k = f32(q), f32(pending_keys)
+        _check(lib().oracle_score_acc_accumulate(self.h, _p(q, C.c_float), q.shape[0], s, _p(k, C.c_float),
+                                                 k.shape[0]))
+
+    def finalize_front(self, n):
+        out = np.zeros(max(1, n), np.float32)
+        _check(lib().oracle_score_acc_finalize_front(self.h, n, _p(out, C.c_float)))
+        return out[:n]
+
+
+SEG_KINDS = {"initial": 0, "retrieved": 1, "local": 2}
+
+
+def attend(segments, q, k, v, start_abs, local_size, position_mode="clamped", emit_weights=False):
+    """attend (attention.hpp:116-230) over segments [(kind, start_abs, keys [n][Hkv][d], values [n][Hkv][dv])]
+    plus the causal batch q [l_x][H][d], k/v [l_x][Hkv][*]; returns (out, seg_mass, weights|None)."""
+    q, k, v = f32(q), f32(k), f32(v)
+    l_x, H, d = q.shape
+    Hkv, dv = v.shape[1], v.shape[2]
+    ns = len(segments)
+    kinds = (C.c_int32 * max(1, ns))(*[SEG_KINDS[s[0]] if isinstance(s[0], str) else s[0] for s in segments])
+    starts = np.array([s[1] for s in segments] or [0], np.int64)
+    keys = [f32(s[2]) for s in segments]
+    vals = [f32(s[3]) for s in segments]
+    ns_arr = np.array([x.shape[0] for x in keys] or [0], np.int64)
+    f32p = C.POINTER(C.c_float)
+    kp = (f32p * max(1, ns))(*[_p(x, C.c_float) for x in keys])
+    vp = (f32p * max(1, ns))(*[_p(x, C.c_float) for x in vals])
+    n_ctx = int(sum(x.shape[0] for x in keys))
+    out = np.zeros((l_x, H, dv), np.float32)
+    mass = np.zeros(max(1, ns), np.float64)
+    w = np.zeros((H, l_x, n_ctx + l_x), np.float32) if emit_weights else None
+    pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else position_mode
+    _check(lib().oracle_attend(H, Hkv, d, dv, pm, local_size, kinds, _p(starts, C.c_int64), _p(ns_arr, C.c_int64), kp,
+                               vp, ns, _p(q, C.c_float), _p(k, C.c_float), _p(v, C.c_float), l_x, start_abs,
+                               _p(out, C.c_float), _p(mass, C.c_double), _p(w, C.c_float) if w is not None else None))
+    return out, mass[:ns], w
+
+
 def select_representatives(scores, r_k):
     s = f32(scores)
     idx = np.zeros(max(1, min(r_k, len(s))), np.int64)

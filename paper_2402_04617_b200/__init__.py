@@ -6,7 +6,9 @@ see DESIGN.md.
 """
 from ._lib import (ConfigError, CudaError, EngineConfig, InfLLMError, LayerMetrics, ModelShape, StreamError, build,
                    lib)
-from .engine import LayerStepOutput, StreamEngine, decode_batch, lookup, select_representatives
+from .engine import (LayerStepOutput, ScoreAccumulator, StreamEngine, TieredStore, attend, decode_batch, lookup,
+                     select_representatives)
 
 __all__ = ["ConfigError", "CudaError", "EngineConfig", "InfLLMError", "LayerMetrics", "ModelShape", "StreamError",
-           "StreamEngine", "LayerStepOutput", "decode_batch", "build", "lib", "lookup", "select_representatives"]
+           "StreamEngine", "LayerStepOutput", "decode_batch", "build", "lib", "lookup", "select_representatives", "attend",
+           "TieredStore", "ScoreAccumulator"]

@@ -85,6 +85,15 @@ class LayerMetrics(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class Segment(C.Structure):
+    """infllm_segment: blockmem::SegmentView (attention.hpp:28-51)."""
+
+    _fields_ = [("kind", C.c_int32), ("start_abs", C.c_int64), ("n_tokens", C.c_int64), ("keys", C.c_void_p),
+                ("values", C.c_void_p)]
+
+
+SEG_KINDS = {"initial": 0, "retrieved": 1, "local": 2}
+
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                            C.c_void_p)
 
@@ -125,6 +134,23 @@ SIGNATURES = {
     "infllm_debug_kernel_bench": (C.c_int, [P, i32, i32, f64p]),
     "infllm_debug_timestamps": (C.c_int, [P]),
     "infllm_timeline_enable": (C.c_int, [i64]),
+    "infllm_attend": (C.c_int, [C.POINTER(ModelShape), i32, i32, i64, C.POINTER(Segment), i32, P, P, P, i64, i64, P,
+                                P, P, P]),
+    "infllm_store_create": (C.c_int, [i64, f64, i32, i32, i32, i64, i32, i64, C.POINTER(P)]),
+    "infllm_store_destroy": (C.c_int, [P]),
+    "infllm_store_add_unit": (C.c_int, [P, P, i64, i64, i64p]),
+    "infllm_store_begin_step": (C.c_int, [P, i64]),
+    "infllm_store_lookup": (C.c_int, [P, P, i64, i64, i64p, i64p, P]),
+    "infllm_store_update_frequency": (C.c_int, [P, i64p, f64p, i64]),
+    "infllm_store_enforce_capacity": (C.c_int, [P]),
+    "infllm_store_note_step_boundary": (C.c_int, [P]),
+    "infllm_store_counters": (C.c_int, [P, C.POINTER(LayerMetrics)]),
+    "infllm_store_trace": (C.c_int, [P, i64p, i64p, i32p, i64, i64p]),
+    "infllm_store_unit_freq": (C.c_int, [P, f64p, i32p, i64]),
+    "infllm_score_acc_create": (C.c_int, [i64, i32, i32, i32, i32, C.POINTER(P)]),
+    "infllm_score_acc_destroy": (C.c_int, [P]),
+    "infllm_score_acc_accumulate": (C.c_int, [P, P, i64, i64, P, i64, P]),
+    "infllm_score_acc_finalize_front": (C.c_int, [P, i64, C.POINTER(C.c_float)]),
     "infllm_timeline_read": (C.c_int, [P, P, P, P, i64, i64p, i32]),
 }
 

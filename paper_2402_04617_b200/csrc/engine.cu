@@ -253,11 +253,12 @@ struct infllm_engine {
     bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
     bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
     bool dec_disabled = false;
-    int lookup_upb = 48;
-    bool attn_flag = false;
-    int prep_blocks = 0;  // option prep_blocks: grid cap of the chunk prep kernels (0: none)
-    bool prep_fused = true;  // option prep_fused: one-kernel chunk prep (side.cu) where the shape allows  // option attn_flag: K3 waits on the step-ready flag instead of graph edges  // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
-    int attn_pdl = 0;  // option attn_pdl = n > 0: K3 t+1 launches programmatically when K3 t has n tiles left
+    int lookup_upb = 48;      // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
+    bool attn_flag = false;   // option attn_flag: K3 waits on a step-ready flag instead of graph edges
+    int prep_blocks = 0;      // option prep_blocks: grid cap of the chunk prep kernels (0: none)
+    bool prep_fused = false;  // option prep_fused: one-kernel chunk prep (side.cu) where the shape allows
+    int attn_pdl = 0;  // option attn_pdl = n != 0: K3 t+1 launches programmatically when K3 t has |n| tiles
+                       // left (n > 0: it then waits for its upstream grids; n < 0: it does not)
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -2181,6 +2182,411 @@ int infllm_debug_timestamps(unsigned long long* out64) {
         debug_read_timestamps(out64);
     });
 }
+
+// ---- stand-alone reference operators (standalone.cu) ----
+namespace {
+RopeFreqs make_freqs(int d, int64_t local_size) {  // rotary.hpp:25-30 (RotaryTable::make)
+    RopeFreqs f{};
+    for (int a = 0; a < d / 2; ++a) {
+        f.f[a] = std::pow(10000.0, -2.0 * a / d);
+        const double ang = static_cast<double>(local_size) * f.f[a];
+        f.cL[a] = static_cast<float>(std::cos(ang));
+        f.sL[a] = static_cast<float>(std::sin(ang));
+    }
+    return f;
+}
+}  // namespace
+
+struct infllm_store {
+    int64_t cap = 0;
+    double decay = 0.0;
+    int H = 1, G = 1, d = 0, r_k = 1, dtype = INFLLM_DTYPE_F32;
+    size_t esz = 4;
+    int64_t bpt = 0;
+    int64_t n_units = 0, unit_cap = 0, trace_cap = 0, trace_count = 0, step = 0;
+    DBuf repr, freq, hot, hot_list, unit_tokens, lru, trace, err, qsum, rel, ids, cand, done, up_ids, up_mass;
+    cudaStream_t st = nullptr;
+    StoreDev dev() {
+        return StoreDev{lru.as<LruState>(), trace.as<int64_t>(), freq.as<double>(), hot.as<int8_t>(),
+                        hot_list.as<int64_t>(), unit_tokens.as<int32_t>(), err.as<int>(), n_units, cap, bpt, decay};
+    }
+    void ensure_units(int64_t n) {
+        if (n <= unit_cap) return;
+        const int64_t c = std::max<int64_t>({n, 2 * unit_cap, 64});
+        repr.grow(static_cast<size_t>(c) * G * r_k * d * esz, st);
+        freq.grow(c * sizeof(double), st);
+        hot.grow(c * sizeof(int8_t), st);
+        hot_list.grow(c * sizeof(int64_t), st);
+        unit_tokens.grow(c * sizeof(int32_t), st);
+        rel.grow(c * sizeof(double), st);
+        cand.grow(static_cast<size_t>(topk_multi_scratch(c, 128)) * 16, st);
+        unit_cap = c;
+    }
+    void check_err() {
+        int e = 0;
+        ck(cudaMemcpyAsync(&e, err.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "store");
+        if (!e) return;
+        ck(cudaMemsetAsync(err.p, 0, sizeof(int), st), "memset");
+        if (e == 1) throw StreamError("update_frequency: mass for a unit that is not hot");
+        throw StreamError("TieredStore: hot tier over capacity at step end");
+    }
+};
+
+struct infllm_score_acc {
+    int64_t L = 0, lo = 0, hi = 0, next_q = 0, ring0 = 0, cap = 0;
+    int H = 1, G = 1, d = 0, dtype = INFLLM_DTYPE_F32;
+    DBuf sums, out;
+};
+
+extern "C" {
+
+int infllm_attend(const infllm_model_shape* shape, int32_t dtype, int32_t position_mode, int64_t local_size,
+                  const infllm_segment* window, int32_t n_segments, const void* q, const void* k, const void* v,
+                  int64_t l_x, int64_t start_abs, void* out, double* seg_mass, float* weights, void* stream) {
+    return guard([&] {
+        if (!shape) throw ConfigError("null shape");
+        validate_shape(*shape);
+        if (dtype != INFLLM_DTYPE_F32 && dtype != INFLLM_DTYPE_BF16) throw ConfigError("dtype must be f32 or bf16");
+        if (position_mode != INFLLM_POSITION_CLAMPED && position_mode != INFLLM_POSITION_ABSOLUTE)
+            throw ConfigError("position_mode: unknown value");
+        if (l_x < 1) throw StreamError("attend: empty batch");  // attention.hpp:123
+        if (n_segments < 0 || (n_segments > 0 && !window)) throw ConfigError("attend: bad window");
+        const int H = shape->n_heads, G = shape->n_kv_heads > 0 ? shape->n_kv_heads : H, d = shape->head_dim;
+        const int dv = shape->value_dim > 0 ? shape->value_dim : d;
+        if (d > 256) throw ConfigError("head_dim <= 256 supported");
+        auto st = static_cast<cudaStream_t>(stream);
+        const size_t esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
+        std::vector<uint8_t> segs(std::max<size_t>(1, static_cast<size_t>(n_segments)) * attend_seg_bytes());
+        int64_t n_ctx = 0;
+        for (int32_t i = 0; i < n_segments; ++i) {
+            const infllm_segment& sg = window[i];
+            if (sg.kind < INFLLM_SEG_INITIAL || sg.kind > INFLLM_SEG_LOCAL) throw ConfigError("attend: segment kind");
+            if (sg.n_tokens < 0 || (sg.n_tokens > 0 && (!sg.keys || !sg.values)))
+                throw StreamError("attend: segment without keys / values");
+            attend_pack_seg(segs.data(), i, sg.keys, sg.values, sg.start_abs, sg.n_tokens, n_ctx, sg.kind);
+            n_ctx += sg.n_tokens;
+        }
+        const int64_t n_all = n_ctx + l_x;
+        void *d_segs = nullptr, *scratch = nullptr;
+        const size_t b_scores = weights ? 0 : static_cast<size_t>(H) * l_x * n_all * sizeof(float);
+        const size_t b_part = static_cast<size_t>(H) * l_x * std::max(1, n_segments) * sizeof(double);
+        const size_t b_qrot = 2 * static_cast<size_t>(H) * l_x * d * sizeof(float);
+        const size_t b_krot = static_cast<size_t>(n_all) * G * d * sizeof(float);
+        auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+        ck(cudaMallocAsync(&d_segs, segs.size(), st), "cudaMallocAsync");
+        ck(cudaMallocAsync(&scratch, al(b_scores) + al(b_part) + al(b_qrot) + al(b_krot), st), "cudaMallocAsync");
+        ck(cudaMemcpyAsync(d_segs, segs.data(), segs.size(), cudaMemcpyHostToDevice, st), "H2D");
+        uint8_t* p8 = static_cast<uint8_t*>(scratch);
+        AttendLaunch L{};
+        L.dev_segs = d_segs;
+        L.n_seg = n_segments;
+        L.q = q;
+        L.k = k;
+        L.v = v;
+        L.out = out;
+        L.scores = weights ? weights : reinterpret_cast<float*>(p8);
+        L.mass_part = reinterpret_cast<double*>(p8 + al(b_scores));
+        L.mass = seg_mass;
+        L.qrot = reinterpret_cast<float*>(p8 + al(b_scores) + al(b_part));
+        L.krot = reinterpret_cast<float*>(p8 + al(b_scores) + al(b_part) + al(b_qrot));
+        L.lx = l_x;
+        L.n_ctx = n_ctx;
+        L.start_abs = start_abs;
+        L.local_size = local_size;
+        L.H = H;
+        L.G = G;
+        L.d = d;
+        L.dv = dv;
+        L.absolute = position_mode == INFLLM_POSITION_ABSOLUTE;
+        L.bf16 = dtype == INFLLM_DTYPE_BF16;
+        L.freqs = make_freqs(d, local_size);
+        (void)esz;
+        attend_run(L, st);
+        ck(cudaGetLastError(), "attend");
+        ck(cudaFreeAsync(scratch, st), "cudaFreeAsync");
+        ck(cudaFreeAsync(d_segs, st), "cudaFreeAsync");
+        ck(cudaStreamSynchronize(st), "attend");  // the host segment table is freed on return
+    });
+}
+
+int infllm_store_create(int64_t hot_capacity, double decay, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim,
+                        int64_t n_repr, int32_t dtype, int64_t bytes_per_token, infllm_store_t* out) {
+    return guard([&] {
+        if (!out) throw ConfigError("null argument");
+        if (hot_capacity < 0) throw ConfigError("hot_capacity must be >= 0");
+        if (decay < 0.0 || decay > 1.0) throw ConfigError("decay must lie in [0, 1]");
+        if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || head_dim < 1 || n_repr < 1 || n_repr > 32)
+            throw ConfigError("TieredStore: bad shape");
+        if (dtype != INFLLM_DTYPE_F32 && dtype != INFLLM_DTYPE_BF16) throw ConfigError("dtype must be f32 or bf16");
+        auto s = std::make_unique<infllm_store>();
+        s->cap = hot_capacity;
+        s->decay = decay;
+        s->H = n_heads;
+        s->G = n_kv_heads;
+        s->d = head_dim;
+        s->r_k = static_cast<int>(n_repr);
+        s->dtype = dtype;
+        s->esz = dtype == INFLLM_DTYPE_BF16 ? 2 : 4;
+        s->bpt = bytes_per_token;
+        ck(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking), "stream");
+        s->lru.alloc(sizeof(LruState), s->st);
+        s->err.alloc(sizeof(int), s->st);
+        s->qsum.alloc(static_cast<size_t>(n_kv_heads) * head_dim * sizeof(double), s->st);
+        s->ids.alloc(128 * sizeof(int64_t), s->st);
+        s->done.alloc(64, s->st);
+        s->up_ids.alloc(1024 * sizeof(int64_t), s->st);
+        s->up_mass.alloc(1024 * sizeof(double), s->st);
+        s->ensure_units(64);
+        ck(cudaStreamSynchronize(s->st), "store create");
+        *out = s.release();
+    });
+}
+
+int infllm_store_destroy(infllm_store_t s) {
+    return guard([&] {
+        if (!s) return;
+        cudaStreamSynchronize(s->st);
+        for (auto* b : {&s->repr, &s->freq, &s->hot, &s->hot_list, &s->unit_tokens, &s->lru, &s->trace, &s->err, &s->qsum,
+                        &s->rel, &s->ids, &s->cand, &s->done, &s->up_ids, &s->up_mass})
+            b->release(s->st);
+        cudaStreamSynchronize(s->st);
+        cudaStreamDestroy(s->st);
+        delete s;
+    });
+}
+
+int infllm_store_add_unit(infllm_store_t s, const void* repr_keys, int64_t n, int64_t unit_tokens, int64_t* unit_id) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        if (n < 1 || n > s->r_k || !repr_keys) throw StreamError("add_unit: 1..n_repr representative keys required");
+        s->ensure_units(s->n_units + 1);
+        const int64_t u = s->n_units;
+        store_put_repr(repr_keys, s->repr.p, u, static_cast<int>(n), s->r_k, s->G, s->d, static_cast<int>(s->esz), s->st);
+        const int32_t tok = static_cast<int32_t>(unit_tokens);
+        ck(cudaMemcpyAsync(s->unit_tokens.as<int32_t>() + u, &tok, sizeof(tok), cudaMemcpyHostToDevice, s->st), "H2D");
+        ck(cudaStreamSynchronize(s->st), "add_unit");
+        s->n_units = u + 1;  // new units start cold (memory.hpp:199)
+        if (unit_id) *unit_id = u;
+    });
+}
+
+int infllm_store_begin_step(infllm_store_t s, int64_t step) {
+    if (!s) return INFLLM_ERR_ARG;
+    s->step = step;
+    return INFLLM_OK;
+}
+
+int infllm_store_lookup(infllm_store_t s, const void* q, int64_t l_x, int64_t k_m, int64_t* host_ids, int64_t* n_ids,
+                        double* rel) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        if (k_m > 128) throw ConfigError("k_m <= 128 supported");
+        const int64_t take = std::min<int64_t>(k_m, s->n_units);  // memory.hpp:240
+        if (n_ids) *n_ids = std::max<int64_t>(take, 0);
+        if (take <= 0) return;
+        if (s->trace_count + take > s->trace_cap) {
+            const int64_t c = std::max<int64_t>({s->trace_count + take, 2 * s->trace_cap, 1024});
+            s->trace.grow(static_cast<size_t>(c) * 3 * sizeof(int64_t), s->st);
+            s->trace_cap = c;
+        }
+        store_qsum(q, l_x, s->H, s->G, s->d, s->dtype == INFLLM_DTYPE_BF16, s->qsum.as<double>(), s->st);
+        LookupParams lp{};
+        lp.qsum = s->qsum.as<double>();
+        lp.repr = s->repr.p;
+        lp.rel = rel ? rel : s->rel.as<double>();
+        lp.U = s->n_units;
+        lp.G = s->G;
+        lp.Gtot = s->G;
+        lp.r_k = s->r_k;
+        lp.d = s->d;
+        lp.n_sel = take;
+        lp.sel = s->ids.as<int64_t>();
+        lp.done = s->done.as<unsigned int>();
+        const int64_t nc = topk_multi_scratch(s->unit_cap, 128);
+        lp.fused = 1;
+        lp.cand_v = s->cand.as<double>();
+        lp.cand_i = reinterpret_cast<int64_t*>(s->cand.as<double>() + nc);
+        const bool bf = s->dtype == INFLLM_DTYPE_BF16;
+        if (lookup_topk_supported(lp, bf))
+            launch_lookup_topk_fast(lp, lookup_topk_blocks(s->n_units, 8), s->st);
+        else
+            launch_lookup_topk(lp, bf, lp.cand_v, lp.cand_i, s->st);
+        store_book(s->dev(), s->ids.as<int64_t>(), take, s->step, s->st);
+        s->trace_count += take;
+        ck(cudaGetLastError(), "store lookup");
+        if (host_ids)
+            ck(cudaMemcpyAsync(host_ids, s->ids.p, take * sizeof(int64_t), cudaMemcpyDeviceToHost, s->st), "D2H");
+        ck(cudaStreamSynchronize(s->st), "store lookup");
+    });
+}
+
+int infllm_store_update_frequency(infllm_store_t s, const int64_t* host_ids, const double* host_mass, int64_t n) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        if (n < 0 || (n > 0 && (!host_ids || !host_mass))) throw ConfigError("update_frequency: bad arguments");
+        if (static_cast<size_t>(n) * sizeof(int64_t) > s->up_ids.bytes) {
+            s->up_ids.grow(n * sizeof(int64_t), s->st);
+            s->up_mass.grow(n * sizeof(double), s->st);
+        }
+        if (n > 0) {
+            ck(cudaMemcpyAsync(s->up_ids.p, host_ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, s->st), "H2D");
+            ck(cudaMemcpyAsync(s->up_mass.p, host_mass, n * sizeof(double), cudaMemcpyHostToDevice, s->st), "H2D");
+        }
+        store_update(s->dev(), s->up_ids.as<int64_t>(), s->up_mass.as<double>(), n, s->st);
+        ck(cudaGetLastError(), "update_frequency");
+        s->check_err();
+    });
+}
+
+int infllm_store_enforce_capacity(infllm_store_t s) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        store_enforce(s->dev(), s->st);
+        ck(cudaGetLastError(), "enforce_capacity");
+        s->check_err();
+    });
+}
+
+int infllm_store_note_step_boundary(infllm_store_t s) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        store_boundary(s->dev(), s->st);
+        ck(cudaGetLastError(), "note_step_boundary");
+        s->check_err();
+    });
+}
+
+int infllm_store_counters(infllm_store_t s, infllm_layer_metrics* m) {
+    return guard([&] {
+        if (!s || !m) throw ConfigError("null argument");
+        LruState x{};
+        ck(cudaMemcpyAsync(&x, s->lru.p, sizeof(x), cudaMemcpyDeviceToHost, s->st), "D2H");
+        ck(cudaStreamSynchronize(s->st), "counters");
+        m->units = s->n_units;
+        m->hot_units = x.hot_count;
+        m->peak_hot_units = x.peak_hot_units;
+        m->peak_hot_bytes = x.peak_hot_bytes;
+        m->hits = x.hits;
+        m->misses = x.misses;
+        m->loads = x.loads;
+        m->evictions = x.evictions;
+        m->requested = x.requested;
+    });
+}
+
+int infllm_store_trace(infllm_store_t s, int64_t* host_step, int64_t* host_unit, int32_t* host_hit, int64_t cap,
+                       int64_t* n_out) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        *n_out = s->trace_count;
+        const int64_t n = std::min(cap, s->trace_count);
+        if (n <= 0) return;
+        std::vector<int64_t> t(static_cast<size_t>(3 * n));
+        ck(cudaMemcpyAsync(t.data(), s->trace.p, t.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s->st), "D2H");
+        ck(cudaStreamSynchronize(s->st), "trace");
+        for (int64_t i = 0; i < n; ++i) {
+            host_step[i] = t[static_cast<size_t>(3 * i)];
+            host_unit[i] = t[static_cast<size_t>(3 * i + 1)];
+            host_hit[i] = static_cast<int32_t>(t[static_cast<size_t>(3 * i + 2)]);
+        }
+    });
+}
+
+int infllm_store_unit_freq(infllm_store_t s, double* host_freq, int32_t* host_hot, int64_t n) {
+    return guard([&] {
+        if (!s) throw ConfigError("null store");
+        n = std::min(n, s->n_units);
+        if (n <= 0) return;
+        std::vector<int8_t> h(static_cast<size_t>(n));
+        ck(cudaMemcpyAsync(host_freq, s->freq.p, n * sizeof(double), cudaMemcpyDeviceToHost, s->st), "D2H");
+        ck(cudaMemcpyAsync(h.data(), s->hot.p, n, cudaMemcpyDeviceToHost, s->st), "D2H");
+        ck(cudaStreamSynchronize(s->st), "unit_freq");
+        for (int64_t i = 0; i < n; ++i) host_hot[i] = h[static_cast<size_t>(i)];
+    });
+}
+
+int infllm_score_acc_create(int64_t local_size, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t dtype,
+                            infllm_score_acc_t* out) {
+    return guard([&] {
+        if (!out) throw ConfigError("null argument");
+        if (local_size < 1) throw ConfigError("local_size must be >= 1");
+        if (n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || head_dim < 1)
+            throw ConfigError("ScoreAccumulator: bad shape");
+        if (dtype != INFLLM_DTYPE_F32 && dtype != INFLLM_DTYPE_BF16) throw ConfigError("dtype must be f32 or bf16");
+        auto a = std::make_unique<infllm_score_acc>();
+        a->L = local_size;
+        a->H = n_heads;
+        a->G = n_kv_heads;
+        a->d = head_dim;
+        a->dtype = dtype;
+        *out = a.release();
+    });
+}
+
+int infllm_score_acc_destroy(infllm_score_acc_t a) {
+    return guard([&] {
+        if (!a) return;
+        cudaDeviceSynchronize();
+        a->sums.release(nullptr);
+        a->out.release(nullptr);
+        cudaDeviceSynchronize();
+        delete a;
+    });
+}
+
+int infllm_score_acc_accumulate(infllm_score_acc_t a, const void* q, int64_t l_x, int64_t s, const void* pending_keys,
+                                int64_t n_pending, void* stream) {
+    return guard([&] {
+        if (!a) throw ConfigError("null accumulator");
+        auto st = static_cast<cudaStream_t>(stream);
+        // repr_score.hpp:42-49
+        if (s != a->next_q) throw StreamError("ScoreAccumulator: out-of-order query batch");
+        if (a->hi != s) throw StreamError("ScoreAccumulator: pending range out of sync");
+        const int64_t hi = s + l_x;
+        if (n_pending != hi - a->lo) throw StreamError("ScoreAccumulator: pending keys do not cover range");
+        if (hi - a->lo > a->cap) {  // grow the ring, live range re-based at 0
+            const int64_t c = std::max<int64_t>({hi - a->lo, 2 * a->cap, 1024});
+            DBuf nb;
+            nb.alloc(c * sizeof(double), st);
+            const int64_t live = a->hi - a->lo;
+            for (int64_t j = 0; j < live;) {  // at most two contiguous pieces
+                const int64_t src = (a->ring0 + j) % std::max<int64_t>(a->cap, 1);
+                const int64_t len = std::min(live - j, a->cap - src);
+                ck(cudaMemcpyAsync(nb.as<double>() + j, a->sums.as<double>() + src, len * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, st),
+                   "D2D");
+                j += len;
+            }
+            a->sums.release(st);
+            a->sums = nb;
+            nb.p = nullptr;
+            a->cap = c;
+            a->ring0 = 0;
+        }
+        score_acc_zero(a->sums.as<double>(), a->ring0 + (a->hi - a->lo), l_x, a->cap, st);  // new pending sums
+        score_acc_run(q, l_x, s, pending_keys, n_pending, a->lo, a->L, a->H, a->G, a->d,
+                      a->dtype == INFLLM_DTYPE_BF16, a->sums.as<double>(), a->ring0, a->cap, st);
+        ck(cudaGetLastError(), "accumulate");
+        a->hi = hi;
+        a->next_q = hi;
+    });
+}
+
+int infllm_score_acc_finalize_front(infllm_score_acc_t a, int64_t n, float* host_out) {
+    return guard([&] {
+        if (!a) throw ConfigError("null accumulator");
+        if (n > a->hi - a->lo) throw StreamError("ScoreAccumulator: finalize beyond range");  // repr_score.hpp:73
+        if (n <= 0) return;
+        if (static_cast<size_t>(n) * sizeof(float) > a->out.bytes) a->out.alloc(n * sizeof(float), nullptr, false);
+        score_acc_final(a->sums.as<double>(), a->ring0, a->cap, n, a->L, a->out.as<float>(), nullptr);
+        ck(cudaMemcpy(host_out, a->out.p, n * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+        a->ring0 = (a->ring0 + n) % a->cap;
+        a->lo += n;
+    });
+}
+
+}  // extern "C"
 
 // Device timeline (common.cuh TlRec): every block of the step kernels appends
 // (kernel, SM, start, end) while a buffer is bound.

@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "../../include/infllm_b200.h"
 
 namespace infllm {
 
@@ -243,6 +244,47 @@ struct SelectParams {
 void debug_read_timestamps(unsigned long long* out);
 // publish a step-ready flag (release) from a stream: steps whose lookup does not set it
 void launch_flag_set(int64_t* flag, int64_t val, cudaStream_t st);
+// standalone.cu: the reference's stand-alone operators (attend, TieredStore, ScoreAccumulator)
+struct AttendLaunch {
+    const void* dev_segs;  // AttendSeg[n_seg] in device memory (attend_pack_seg)
+    int n_seg;
+    const void *q, *k, *v;
+    void* out;
+    float* scores;       // [H][lx][n_ctx + lx] (the weights)
+    double* mass_part;   // [H][lx][n_seg] scratch
+    double* mass;        // [n_seg] or null
+    float* qrot;         // [2][H][lx][d] scratch
+    float* krot;         // [n_ctx + lx][G][d] scratch
+    int64_t lx, n_ctx, start_abs, local_size;
+    int H, G, d, dv, absolute, bf16;
+    RopeFreqs freqs;
+};
+size_t attend_seg_bytes();
+void attend_pack_seg(void* dst, int idx, const void* keys, const void* values, int64_t start_abs, int64_t n,
+                     int64_t col0, int kind);
+void attend_run(const AttendLaunch& L, cudaStream_t st);
+struct StoreDev {
+    LruState* lru;
+    int64_t* trace;
+    double* freq;
+    int8_t* hot;
+    int64_t* hot_list;
+    int32_t* unit_tokens;
+    int* err;
+    int64_t n_units, cap, bytes_per_token;
+    double decay;
+};
+void store_qsum(const void* q, int64_t lx, int H, int G, int d, bool bf16, double* qsum, cudaStream_t st);
+void store_put_repr(const void* src, void* repr, int64_t u, int n_repr, int r_k, int G, int d, int esz, cudaStream_t st);
+void store_book(const StoreDev& s, const int64_t* ids, int64_t n, int64_t step, cudaStream_t st);
+void store_update(const StoreDev& s, const int64_t* ids, const double* mass, int64_t n, cudaStream_t st);
+void store_enforce(const StoreDev& s, cudaStream_t st);
+void store_boundary(const StoreDev& s, cudaStream_t st);
+void score_acc_run(const void* q, int64_t lx, int64_t s, const void* keys, int64_t n_pending, int64_t lo, int64_t L,
+                   int H, int G, int d, bool bf16, double* sums, int64_t ring0, int64_t cap, cudaStream_t st);
+void score_acc_final(const double* sums, int64_t ring0, int64_t cap, int64_t n, int64_t L, float* out, cudaStream_t st);
+void score_acc_zero(double* sums, int64_t from, int64_t n, int64_t cap, cudaStream_t st);
+
 // side.cu: one-kernel chunk prep (bf16, d = dv = 128, transposed values), bitwise
 // equal to rope table + k_prep_tok + k_prefix_tiles; 32-token tiles, lx <= 32 * kPrepChunkMaxTiles
 constexpr int kPrepChunkMaxTiles = 64;

@@ -245,3 +245,136 @@ def lookup(qsum: torch.Tensor, repr_keys: torch.Tensor, k_m: int):
                               U, rk, G, d, k_m, rel.data_ptr(), ids.data_ptr(),
                               torch.cuda.current_stream(repr_keys.device).cuda_stream))
     return rel, ids[: min(k_m, U)]
+
+
+def attend(segments, q, k, v, start_abs, local_size, position_mode="clamped", emit_weights=False, stream=None):
+    """blockmem::attend (attention.hpp:116-230) on the GPU (infllm_attend).
+
+    segments: [(kind, start_abs, keys [n][H_kv][d], values [n][H_kv][d_v])] device tensors, kind in
+    "initial" / "retrieved" / "local" (attention.hpp:14-26), keys raw; q [l_x][H][d], k/v [l_x][H_kv][*]
+    the causal batch at absolute positions start_abs... Returns (out [l_x][H][d_v], per-segment mass
+    (engine.hpp:271-283), weights [H][l_x][n_ctx + l_x] fp32 or None)."""
+    l_x, H, d = q.shape
+    Hkv, dv = v.shape[1], v.shape[2]
+    dt = _DT[q.dtype]
+    for t in [q, k, v] + [x for s in segments for x in (s[2], s[3])]:
+        if t.dtype != q.dtype or not t.is_contiguous() or t.device != q.device:
+            raise ValueError("attend: contiguous tensors of one dtype on one device")
+    ns = len(segments)
+    segs = (_lib.Segment * max(1, ns))()
+    for i, (kind, start, keys, vals) in enumerate(segments):
+        segs[i] = _lib.Segment(_lib.SEG_KINDS[kind] if isinstance(kind, str) else kind, start, keys.shape[0],
+                               keys.data_ptr(), vals.data_ptr())
+    n_ctx = sum(s[2].shape[0] for s in segments)
+    out = torch.empty((l_x, H, dv), dtype=q.dtype, device=q.device)
+    mass = torch.zeros(max(1, ns), dtype=torch.float64, device=q.device)
+    w = torch.empty((H, l_x, n_ctx + l_x), dtype=torch.float32, device=q.device) if emit_weights else None
+    shape = ModelShape.make(n_heads=H, n_kv_heads=Hkv, head_dim=d, value_dim=dv)
+    pm = _lib.POSITION_MODES[position_mode] if isinstance(position_mode, str) else position_mode
+    st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+    check(lib().infllm_attend(C.byref(shape), dt, pm, local_size, segs, ns, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                              l_x, start_abs, out.data_ptr(), mass.data_ptr(), w.data_ptr() if w is not None else None,
+                              st))
+    return out, mass[:ns], w
+
+
+class TieredStore:
+    """blockmem::TieredStore (memory.hpp:170-323) on the GPU (infllm_store_*)."""
+
+    def __init__(self, hot_capacity, decay, n_heads, n_kv_heads, head_dim, n_repr=4, dtype=torch.bfloat16,
+                 bytes_per_token=0):
+        h = C.c_void_p()
+        check(lib().infllm_store_create(hot_capacity, decay, n_heads, n_kv_heads, head_dim, n_repr, _DT[dtype],
+                                        bytes_per_token, C.byref(h)))
+        self.h, self.dtype, self.k_cap = h, dtype, 128
+
+    def close(self):
+        if getattr(self, "h", None):
+            try:
+                lib().infllm_store_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    __del__ = close
+
+    def add_unit(self, repr_keys, unit_tokens):
+        """add_unit (memory.hpp:196-212): repr_keys [n][H_kv][d] device -> unit id."""
+        uid = C.c_int64()
+        check(lib().infllm_store_add_unit(self.h, repr_keys.contiguous().data_ptr(), repr_keys.shape[0], unit_tokens,
+                                          C.byref(uid)))
+        return uid.value
+
+    def begin_step(self, step):
+        check(lib().infllm_store_begin_step(self.h, step))
+
+    def lookup(self, q, k_m, rel=None):
+        """lookup (memory.hpp:239-269): batch queries q [l_x][H][d] (device) -> ascending ids."""
+        ids = np.zeros(max(1, k_m), np.int64)
+        n = C.c_int64()
+        check(lib().infllm_store_lookup(self.h, q.contiguous().data_ptr(), q.shape[0], k_m,
+                                        ids.ctypes.data_as(_lib.i64p), C.byref(n),
+                                        rel.data_ptr() if rel is not None else None))
+        return ids[: n.value].tolist()
+
+    def update_frequency(self, pairs):
+        ids = np.array([p[0] for p in pairs] or [0], np.int64)
+        ms = np.array([p[1] for p in pairs] or [0.0], np.float64)
+        check(lib().infllm_store_update_frequency(self.h, ids.ctypes.data_as(_lib.i64p), ms.ctypes.data_as(_lib.f64p),
+                                                  len(pairs)))
+
+    def enforce_capacity(self):
+        check(lib().infllm_store_enforce_capacity(self.h))
+
+    def note_step_boundary(self):
+        check(lib().infllm_store_note_step_boundary(self.h))
+
+    def counters(self):
+        m = LayerMetrics()
+        check(lib().infllm_store_counters(self.h, C.byref(m)))
+        return m.as_dict()
+
+    def trace(self, cap=1 << 16):
+        st, un = np.zeros(cap, np.int64), np.zeros(cap, np.int64)
+        hit = np.zeros(cap, np.int32)
+        n = C.c_int64()
+        check(lib().infllm_store_trace(self.h, st.ctypes.data_as(_lib.i64p), un.ctypes.data_as(_lib.i64p),
+                                       hit.ctypes.data_as(_lib.i32p), cap, C.byref(n)))
+        k = min(cap, n.value)
+        return list(zip(st[:k].tolist(), un[:k].tolist(), hit[:k].tolist()))
+
+    def unit_freq(self, n):
+        f = np.zeros(max(1, n), np.float64)
+        hot = np.zeros(max(1, n), np.int32)
+        check(lib().infllm_store_unit_freq(self.h, f.ctypes.data_as(_lib.f64p), hot.ctypes.data_as(_lib.i32p), n))
+        return f[:n], hot[:n]
+
+
+class ScoreAccumulator:
+    """blockmem::ScoreAccumulator (repr_score.hpp:21-89) on the GPU (infllm_score_acc_*)."""
+
+    def __init__(self, local_size, n_heads, n_kv_heads, head_dim, dtype=torch.float32):
+        h = C.c_void_p()
+        check(lib().infllm_score_acc_create(local_size, n_heads, n_kv_heads, head_dim, _DT[dtype], C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            try:
+                lib().infllm_score_acc_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    __del__ = close
+
+    def accumulate(self, q, s, pending_keys, stream=None):
+        st = (stream or torch.cuda.current_stream(q.device)).cuda_stream
+        check(lib().infllm_score_acc_accumulate(self.h, q.contiguous().data_ptr(), q.shape[0], s,
+                                                pending_keys.contiguous().data_ptr(), pending_keys.shape[0], st))
+
+    def finalize_front(self, n):
+        torch.cuda.synchronize()
+        out = np.zeros(max(1, n), np.float32)
+        check(lib().infllm_score_acc_finalize_front(self.h, n, out.ctypes.data_as(C.POINTER(C.c_float))))
+        return out[:n]
