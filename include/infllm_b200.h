@@ -253,6 +253,22 @@ int infllm_timeline_enable(int64_t capacity);
 int infllm_timeline_read(uint32_t* kernel, uint32_t* sm, uint64_t* t0, uint64_t* t1, int64_t cap,
                          int64_t* n_out, int32_t reset);
 
+/* StreamEngine::metrics().timings (PhaseTimings, engine.hpp:43-49; cli.cpp
+ * timings_ms) measured on the device: summed event time of each phase's
+ * launches over the profile window (infllm_profile_begin), in ms, in the
+ * order lookup, attend, score (query sums / prefix for the representative
+ * scores, ring append, RoPE), evict (eviction scoring, unit packing,
+ * representative selection, frequency update and capacity); launches4 (may
+ * be NULL) gets the number of timed launch groups per phase. Phases overlap
+ * on the engine's streams, so the sum exceeds the wall time. */
+int infllm_phase_timings(infllm_engine_t eng, double* ms4, int64_t* launches4);
+/* StreamEngine::invariant_checks / invariant_violations (engine.hpp:88-89):
+ * check_softmax (361-371) counts one check per head and row of every step
+ * that attended retrieved units (a violation: a row whose softmax
+ * denominator is not a positive finite number, checked on the device) and
+ * check_conservation (373-383) one per layer step. Synchronous. */
+int infllm_invariants(infllm_engine_t eng, uint64_t* checks, uint64_t* violations);
+
 /* ---- standalone operators (device pointers, async on stream) ---- */
 
 /* select_representatives (repr_score.hpp:94-112) for `n_units` units at

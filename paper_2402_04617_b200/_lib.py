@@ -128,6 +128,8 @@ SIGNATURES = {
     "infllm_decode_batch": (C.c_int, [C.POINTER(C.c_void_p), i32, i32, P, P, P, P, P]),
     "infllm_profile_begin": (C.c_int, [P, i32]),
     "infllm_profile_read": (C.c_int, [P, f64p, i64p, f64p, i64p]),
+    "infllm_phase_timings": (C.c_int, [P, f64p, i64p]),
+    "infllm_invariants": (C.c_int, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "infllm_select_representatives": (C.c_int, [P, P, i64, i64, i64, P, P]),
     "infllm_lookup": (C.c_int, [P, P, i32, i64, i64, i32, i32, i64, P, P, P]),
     "infllm_debug_tc_selftest": (C.c_int, [P, P, P, P, P, P]),

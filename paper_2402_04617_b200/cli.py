@@ -8,6 +8,13 @@ CLI (src/cli.cpp:396-540) for the subcommands on the hot path:
   run    -- one stream with a decode tail (cmd_run, cli.cpp:169-199), optional
             engine trace export in the reference's text format
             (`step unit hit|miss`, cache_sim.hpp:181-184) and JSON report
+  oracle-check -- the three self-checks of cmd_oracle_check (cli.cpp:239-351):
+            the engine (on the GPU) against brute-force references restated
+            from the reference's oracle.hpp (dense causal attention, windowed
+            full-retrieval attention, batch representative scores), computed
+            in float64 with torch on the same device; same JSON report
+            (checks[{check, max_abs_err, mean_abs_err, compared, mismatches,
+            tolerance, pass}], ok) and exit code (0 iff every check passes)
 
 Engine flags mirror the EngineConfig field names; `--config file.json`
 provides the base values (unknown keys rejected, config_io.hpp:16-40) and
@@ -58,10 +65,12 @@ def config_to_json(cfg) -> dict:
 
 
 def metrics_to_json(eng, n_layers: int, tokens: int, steps: int, wall_ms: float) -> dict:
-    """metrics_to_json (cli.cpp:38-69). The engine runs whole steps on the
-    device without per-phase host timers, so timings_ms reports the stream's
-    wall time; invariant counters are the reference's CPU self-checks and
-    have no device counterpart (null)."""
+    """metrics_to_json (cli.cpp:38-69). timings_ms: PhaseTimings
+    (engine.hpp:43-49) as device time per phase (infllm_phase_timings; the
+    phases overlap on the engine's streams) plus the stream's wall time; the
+    adapter phase does not exist (q/k/v are inputs). invariant_checks /
+    _violations: check_softmax on the device + check_conservation
+    (engine.hpp:361-383)."""
     layers = []
     for li in range(n_layers):
         m = eng.metrics(li)
@@ -72,8 +81,11 @@ def metrics_to_json(eng, n_layers: int, tokens: int, steps: int, wall_ms: float)
             "evictions": m["evictions"], "requested": req, "hit_rate": m["hits"] / req if req else 0.0,
             "miss_rate": m["misses"] / req if req else 0.0,
         })
-    return {"tokens": tokens, "steps": steps, "invariant_checks": None, "invariant_violations": None,
-            "timings_ms": {"stream": wall_ms}, "layers": layers}
+    ph = eng.phase_timings()
+    checks, violations = eng.invariants()
+    return {"tokens": tokens, "steps": steps, "invariant_checks": checks, "invariant_violations": violations,
+            "timings_ms": {"adapter": 0.0, "lookup": ph["lookup"], "attend": ph["attend"], "score": ph["score"],
+                           "evict": ph["evict"], "wall": wall_ms}, "layers": layers}
 
 
 def _engine(args):
@@ -119,6 +131,7 @@ def _stream(eng, args, q, k, v, decode_tail=0):
 
     n = q.shape[0]
     n_pre = n - decode_tail
+    eng.profile_begin(True)  # per-phase device timings (timings_ms)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for li in range(args.n_layers):
@@ -177,6 +190,171 @@ def cmd_run(args) -> dict:
     return report
 
 
+# ---------------------------------------------------------------- oracle-check
+def _schedule(length, chunk, tail):
+    """encode_schedule (cli.cpp:133-142)."""
+    sched, left = [], length - tail
+    while left > 0:
+        sched.append(min(chunk, left))
+        left -= sched[-1]
+    return sched + [1] * tail
+
+
+def _rope(x, pos):
+    """detail::rotate (oracle.hpp:30-45 / rotary.hpp:15-51) in float64: pairs (2a, 2a+1),
+    angle pos * 10000^(-2a/d); x [..., n, d], pos [n] (or a scalar)."""
+    import torch
+
+    d = x.shape[-1]
+    a = torch.arange(d // 2, device=x.device, dtype=torch.float64)
+    theta = torch.pow(torch.tensor(10000.0, dtype=torch.float64, device=x.device), -2.0 * a / d)
+    pos = torch.as_tensor(pos, dtype=torch.float64, device=x.device)
+    ang = pos.reshape(-1, 1) * theta if pos.dim() else pos * theta
+    c, s = torch.cos(ang), torch.sin(ang)
+    y = x.clone()
+    x0, x1 = x[..., 0:2 * (d // 2):2], x[..., 1:2 * (d // 2):2]
+    y[..., 0:2 * (d // 2):2] = x0 * c - x1 * s
+    y[..., 1:2 * (d // 2):2] = x0 * s + x1 * c
+    return y
+
+
+def _report(name, got, want, tol):
+    import torch
+
+    err = (got.double() - want).abs()
+    return {"check": name, "max_abs_err": float(err.max()), "mean_abs_err": float(err.mean()),
+            "compared": int(err.numel()), "mismatches": int((err > tol).sum()), "tolerance": tol,
+            "pass": bool((err > tol).sum() == 0)}
+
+
+def _run_collect(eng, q, k, v, sched, tail):
+    """run_engine_collect (cli.cpp:89-119) with explicit q/k/v: stacked outputs."""
+    import torch
+
+    outs, fed = [], 0
+    first_decode = len(sched) - tail
+    for i, b in enumerate(sched):
+        sl = slice(fed, fed + b)
+        if i >= first_decode:
+            outs.append(eng.decode_step(q[sl].contiguous(), k[sl].contiguous(), v[sl].contiguous()))
+        else:
+            outs.append(eng.encode_chunk(q[sl].contiguous(), k[sl].contiguous(), v[sl].contiguous()))
+        fed += b
+    torch.cuda.synchronize()
+    return torch.cat(outs, 0)
+
+
+def cmd_oracle_check(args) -> dict:
+    import torch
+
+    from . import EngineConfig, ModelShape, ScoreAccumulator, StreamEngine
+
+    base = {}
+    if args.config:
+        with open(args.config) as f:
+            base = config_from_json(json.load(f))
+    for kname in CONFIG_KEYS:
+        val = getattr(args, kname, None)
+        if val is not None:
+            base[kname] = LOOKUP_MODES.get(val, val) if kname == "lookup_mode" else POSITION_MODES.get(val, val) \
+                if kname == "position_mode" else val
+    cfg0 = EngineConfig.make(**base)
+    dtype = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+    n, H, d = args.length, args.n_heads, args.head_dim
+    Hkv = args.n_kv_heads or H
+    rep_h = H // Hkv
+    shape = ModelShape.make(n_heads=H, n_kv_heads=Hkv, head_dim=d)
+    dev = torch.device("cuda", args.device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(args.seed)
+    q = torch.randn((n, H, d), generator=g, device=dev).to(dtype)
+    k = torch.randn((n, Hkv, d), generator=g, device=dev).to(dtype)
+    v = torch.randn((n, Hkv, d), generator=g, device=dev).to(dtype)
+    q64, k64, v64 = q.double(), k.double(), v.double()
+    tail = min(32, n // 8)
+    tol_attn = 1e-5 if dtype == torch.float32 else 2e-2
+    scale = 1.0 / d ** 0.5
+    kh = k64.repeat_interleave(rep_h, dim=1)  # key / value of each query head's group
+    vh = v64.repeat_interleave(rep_h, dim=1)
+    pos = torch.arange(n, device=dev)
+    checks = []
+
+    def softmax_pv(logits, vals):  # detail::softmax_inplace (oracle.hpp:47-57), float64
+        w = torch.softmax(logits, dim=-1)
+        return torch.einsum("hij,hjd->hid", w, vals)
+
+    # 1. degenerate configuration vs the dense causal oracle (cli.cpp:248-271, oracle.hpp:64-97)
+    c = dict(cfg0.as_dict())
+    c["local_size"] = max(c["local_size"], n)
+    c["position_mode"] = POSITION_MODES["absolute"]
+    sched = _schedule(n, c["chunk_size"], tail)
+    eng = StreamEngine(EngineConfig.make(**c), shape, dtype=dtype, device=args.device)
+    got = _run_collect(eng, q, k, v, sched, tail)
+    eng.close()
+    qa = _rope(q64.transpose(0, 1), pos)  # [H][n][d]
+    ka = _rope(kh.transpose(0, 1), pos)
+    logits = torch.einsum("hid,hjd->hij", qa, ka) * scale
+    logits.masked_fill_(torch.triu(torch.ones(n, n, dtype=torch.bool, device=dev), 1), float("-inf"))
+    want = softmax_pv(logits, vh.transpose(0, 1)).transpose(0, 1)
+    checks.append(_report("degenerate_vs_dense", got, want, tol_attn))
+    del logits, qa, ka
+
+    # 2. full-retrieval configuration vs the windowed clamped oracle (cli.cpp:274-299, oracle.hpp:103-168)
+    c = dict(cfg0.as_dict())
+    c["position_mode"] = POSITION_MODES["clamped"]
+    c["lookup_mode"] = LOOKUP_MODES["encode_and_decode"]
+    c["n_lookup"] = n // c["unit_size"] + 2
+    c["hot_capacity"] = max(c["hot_capacity"], c["n_lookup"])
+    sched = _schedule(n, c["chunk_size"], tail)
+    eng = StreamEngine(EngineConfig.make(**c), shape, dtype=dtype, device=args.device)
+    got = _run_collect(eng, q, k, v, sched, tail)
+    eng.close()
+    L, I, U = c["local_size"], c["init_size"], c["unit_size"]
+    q_abs = _rope(q64.transpose(0, 1), pos)
+    q_cap = _rope(q64.transpose(0, 1), torch.tensor(float(L), device=dev))
+    k_rot = _rope(kh.transpose(0, 1), pos)
+    k_raw = kh.transpose(0, 1)
+    want = torch.zeros((H, n, d), dtype=torch.float64, device=dev)
+    fed = 0
+    for b in sched:
+        local_begin = max(0, fed - L)
+        init_len = min(I, local_begin)
+        evicted = max(0, local_begin - I)
+        packed = evicted - evicted % U
+        vis = torch.cat([torch.arange(0, init_len), torch.arange(I, I + packed), torch.arange(local_begin, fed + b)]).to(dev)
+        rows = torch.arange(fed, fed + b, device=dev)
+        dist = rows.view(-1, 1) - vis.view(1, -1)
+        cap = (vis.view(1, -1) < local_begin) | (dist > L)
+        s_cap = torch.einsum("hid,hjd->hij", q_cap[:, rows], k_raw[:, vis])
+        s_abs = torch.einsum("hid,hjd->hij", q_abs[:, rows], k_rot[:, vis])
+        logits = torch.where(cap, s_cap, s_abs) * scale
+        logits.masked_fill_(dist < 0, float("-inf"))  # causal batch prefix
+        want[:, fed:fed + b] = softmax_pv(logits, vh.transpose(0, 1)[:, vis])
+        fed += b
+    checks.append(_report("full_retrieval_vs_windowed", got, want.transpose(0, 1), tol_attn))
+
+    # 3. incremental representative scores vs the batch definition (cli.cpp:301-342, oracle.hpp:173-184)
+    L = int(cfg0.local_size)
+    acc = ScoreAccumulator(L, H, Hkv, d, dtype)
+    fed = 0
+    while fed < n:
+        b = min(int(cfg0.chunk_size), n - fed)
+        acc.accumulate(q[fed:fed + b].contiguous(), fed, k[:fed + b].contiguous())
+        fed += b
+    got_r = torch.from_numpy(acc.finalize_front(n)).to(dev)
+    acc.close()
+    dots = torch.einsum("ihd,mhd->im", q64, kh)  # [query i][key m] summed over heads
+    band = (pos.view(-1, 1) > pos.view(1, -1)) & (pos.view(-1, 1) <= pos.view(1, -1) + L)
+    want_r = (dots * band).sum(0) / L
+    checks.append(_report("repr_scores_incremental_vs_batch", got_r, want_r, 1e-6))
+
+    report = {"seed": args.seed, "length": n, "config": config_to_json(cfg0), "dtype": args.dtype,
+              "inputs": "seeded N(0,1) q/k/v on the device (the engine takes explicit q/k/v; SURVEY M7)",
+              "checks": checks, "ok": all(ch["pass"] for ch in checks)}
+    _write(args.out, report)
+    return report
+
+
 def _write(path, obj):
     if path:
         with open(path, "w") as f:
@@ -213,12 +391,21 @@ def build_parser() -> argparse.ArgumentParser:
     r.add_argument("--length", type=int, default=8192)
     r.add_argument("--decode_tail", type=int, default=32)
     r.add_argument("--trace-out", dest="trace_out", default="")
+    oc = sub.add_parser("oracle-check", help="compare the engine to brute-force references (cmd_oracle_check)")
+    common(oc)
+    oc.set_defaults(n_heads=4, n_kv_heads=2, head_dim=64, dtype="f32")
+    oc.add_argument("--length", type=int, default=1024)
     return ap
 
 
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
+        if args.cmd == "oracle-check":
+            rep = cmd_oracle_check(args)
+            for ch in rep["checks"]:  # cli.cpp:511-516
+                print(f"{ch['check']}: max_abs_err={ch['max_abs_err']:.3g} {'ok' if ch['pass'] else 'FAIL'}")
+            return 0 if rep["ok"] else 1
         rep = cmd_bench(args) if args.cmd == "bench" else cmd_run(args)
     except Exception as ex:  # cli.cpp:533-538: one-line message, exit code 1
         print(f"error: {ex}", file=sys.stderr)

@@ -353,6 +353,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
         }
         s_M[tid] = M;
         s_L[tid] = L;
+        if (a.inv_violations && !(L > 0.f && isfinite(L))) atomicAdd(a.inv_violations, 1ull);  // check_softmax
     }
     __syncthreads();
     for (int i = tid; i < nsplit * rep; i += kThr) {

@@ -801,6 +801,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         const float a1 = l1 > 0.f ? ex2(m1 - mf) : 0.f;
         const float lf = fast ? l0 + l1 : l0 * a0 + l1 * a1;
         const float inv = 1.f / lf;
+        if (a.inv_violations && row_ok && wg == 0 && !(lf > 0.f && isfinite(lf) && isfinite(inv)))
+            atomicAdd(a.inv_violations, 1ull);  // check_softmax (engine.hpp:361-371)
         // fast path: one O holding both warpgroups' sums, both at the same fixed offset
         const float w0 = fast ? inv : a0 * inv, w1 = fast ? 0.f : a1 * inv;
         // warpgroup wg writes value dims [64 wg, 64 wg + 64)

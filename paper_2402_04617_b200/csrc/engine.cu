@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/infllm_b200.h"
 #include "attn_dec.cuh"
 #include "attn_tc.cuh"
@@ -31,6 +33,17 @@ using namespace infllm;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX ranges named after the reference's PhaseTimings (engine.hpp:43-49):
+// host-side brackets of each phase's launches (nsys / Nsight show them)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+// device-time phases (PhaseTimings order minus the adapter)
+constexpr int kPhLookup = 0, kPhAttend = 1, kPhScore = 2, kPhEvict = 3, kPhases = 4;
 
 struct ConfigError : std::invalid_argument {
     using std::invalid_argument::invalid_argument;
@@ -377,7 +390,8 @@ struct infllm_engine {
         HostState before, after;
         cudaGraphExec_t exec = nullptr;
         int64_t launches = 0;
-        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> attn_ev, lookup_ev;
+        uint64_t inv_checks = 0, inv_bad = 0;  // invariant checks the captured steps make per replay
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];  // profile events per phase
         int64_t replays_in_window = 0;
         int64_t steps = 0;
         std::vector<const void*> bufs;  // device addresses baked into the graph (buf_snapshot)
@@ -387,20 +401,19 @@ struct infllm_engine {
     static void drop_graph(GraphEntry& g) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
         g.exec = nullptr;
-        for (auto* evs : {&g.attn_ev, &g.lookup_ev})
-            for (auto& p : *evs) {
+        for (auto& evs : g.ev) {
+            for (auto& p : evs) {
                 cudaEventDestroy(p.first);
                 cudaEventDestroy(p.second);
             }
-        g.attn_ev.clear();
-        g.lookup_ev.clear();
+            evs.clear();
+        }
     }
     cudaStream_t cap_stream = nullptr, h2d_stream = nullptr, d2h_stream = nullptr;
     bool use_graphs = true;
     int64_t tier_slots = 0;  // host tier: GPU unit-cache slots (0: unit pages resident in HBM)
     bool capturing = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_attn_ev = nullptr;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_lookup_ev = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* cap_ev = nullptr;  // [kPhases] of the graph being captured
     static constexpr int kNB = 3;  // host-pointer staging buffers (groups of kGroup chunks)
     DBuf stage_q[kNB], stage_k[kNB], stage_v[kNB], stage_o[kNB];
 
@@ -413,7 +426,26 @@ struct infllm_engine {
 
     // profiling (dominant kernel + lookup timing with events on the caller stream)
     bool prof = false;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_attn, ev_lookup;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[kPhases];
+    // brackets one phase's launches on `st` with timing events (profile mode)
+    // NVTX range named after the reference's phase (host side, for nsys) and,
+    // in profile mode, device timing events on the phase's stream
+    std::pair<cudaEvent_t, cudaEvent_t> phase_begin(const char* name, cudaStream_t st) {
+        nvtxRangePushA(name);
+        if (!prof) return {};
+        std::pair<cudaEvent_t, cudaEvent_t> p{take_event(), take_event()};
+        record(p.first, st);
+        return p;
+    }
+    void phase_end(int ph, std::pair<cudaEvent_t, cudaEvent_t> p, cudaStream_t st) {
+        nvtxRangePop();
+        if (!prof) return;
+        record(p.second, st);
+        (capturing ? cap_ev : ev)[ph].push_back(p);
+    }
+    // invariant counters (engine.hpp:88-89, 361-383)
+    uint64_t inv_checks = 0, inv_conservation_bad = 0;
+    DBuf inv_dev;  // device count of check_softmax violations
     std::vector<cudaEvent_t> ev_pool;
 
     cudaEvent_t take_event() {
@@ -432,7 +464,7 @@ struct infllm_engine {
 
     // every device buffer the engine owns (a captured step graph holds their addresses)
     std::vector<DBuf*> dev_buffers() {
-        std::vector<DBuf*> v{&prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
+        std::vector<DBuf*> v{&inv_dev, &prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
                              &tsum, &topk_done, &evict_done, &dec_part, &dec_mass, &dec_cnt};
         for (int b = 0; b < kNB; ++b)
             for (auto* x : {&stage_q[b], &stage_k[b], &stage_v[b], &stage_o[b]}) v.push_back(x);
@@ -711,6 +743,7 @@ struct infllm_engine {
                 launch_dec_front(pp, ep2, s2);
         };
         const bool prep_one = std::is_same_v<T, bf16> && !fused_front && !coll && prep_chunk_supported(pp);
+        const auto evs = fused_front ? std::pair<cudaEvent_t, cudaEvent_t>{} : phase_begin("score", st);
         if (fused_front) {
         } else if (coll) {
             coll->prep.push_back(pp);
@@ -722,6 +755,7 @@ struct infllm_engine {
         }
         if (!fused_front && !prep_one)
             launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
+        if (!fused_front) phase_end(kPhScore, evs, st);
         rec(e_prep, pst);
         wt(side, e_prep);
         st = side;
@@ -737,6 +771,7 @@ struct infllm_engine {
             wt(side, e_evict);
         st = est;
         wt(est, e_prep);
+        const auto eve = (overflow > 0 || fused_front) ? phase_begin("evict", st) : std::pair<cudaEvent_t, cudaEvent_t>{};
         if (overflow > 0) {
             // UnitPacker::add: an empty packer starts its pending run at the
             // first evicted token (memory.hpp:65-66)
@@ -838,6 +873,7 @@ struct infllm_engine {
             issue_front(EvictParams{}, st);  // nothing leaves the window: prep only
             ++launches;
         }
+        if (overflow > 0 || fused_front) phase_end(kPhEvict, eve, est);
         rec(e_evict, est);
         evict_seq = kseq;
         st = side;
@@ -847,11 +883,7 @@ struct infllm_engine {
         bool k4_pdl = false;  // the lookup is the last kernel before K4 on the caller's stream
         bool last_lkp_fast = false;  // this step's lookup publishes the ready flag itself
         if (do_lookup) {
-            std::pair<cudaEvent_t, cudaEvent_t> evp{};
-            if (prof) {
-                evp = {take_event(), take_event()};
-                record(evp.first, st);
-            }
+            const auto evp = phase_begin("lookup", st);
             LookupParams lp{};
             lp.qsum = chunk_qsum.as<double>() + pb * Gs * d;
             lp.repr = L.repr.p;
@@ -909,10 +941,7 @@ struct infllm_engine {
             }
             launches += n_lk;
             k4_pdl = one_stream && !coll && !prof && !(debug_skip & 2) && n_sel > 0 && lp.fused != 0;
-            if (prof) {
-                record(evp.second, st);
-                (capturing ? *cap_lookup_ev : ev_lookup).push_back(evp);
-            }
+            phase_end(kPhLookup, evp, st);
         }
 
         if (flag_mode && !(do_lookup && last_lkp_fast)) {
@@ -1028,11 +1057,8 @@ struct infllm_engine {
             ap.dec_maps = L.dec_maps.p;
         }
         last_ap = ap;
-        std::pair<cudaEvent_t, cudaEvent_t> eva{};
-        if (prof) {
-            eva = {take_event(), take_event()};
-            record(eva.first, st);
-        }
+        ap.inv_violations = inv_dev.as<unsigned long long>();
+        const auto eva = phase_begin("attend", st);
         if constexpr (std::is_same_v<T, bf16>) {
             if (debug_skip & 1) {
             } else if (dec_ran) {
@@ -1057,10 +1083,8 @@ struct infllm_engine {
             launch_attn_simt<T>(ap, st);
             ++launches;
         }
-        if (prof) {
-            record(eva.second, st);
-            (capturing ? *cap_attn_ev : ev_attn).push_back(eva);
-        }
+        phase_end(kPhAttend, eva, st);
+        if (want_mass) inv_checks += static_cast<uint64_t>(Hs) * lx;  // check_softmax rows (engine.hpp:266)
 
         // attention masses -> lookup bookkeeping, frequency update, capacity
         // (engine.hpp:257,271-285; memory.hpp:254-300)
@@ -1129,10 +1153,12 @@ struct infllm_engine {
             ck(cudaStreamWaitEvent(lru_st, e_attn, 0), "wait");
         }
         last_lp = lp;
+        const auto evl = coll ? std::pair<cudaEvent_t, cudaEvent_t>{} : phase_begin("evict", lru_st);
         if (coll)
             coll->lru.push_back(lp);
         else if (!(debug_skip & 16))
             launch_lru(lp, lru_st);
+        if (!coll) phase_end(kPhEvict, evl, lru_st);
         ++launches;
         rec(e_lru[b], lru_st);
         if (lru_side) ck(cudaEventRecord(e_lru[b], lru_st), "record");
@@ -1150,6 +1176,11 @@ struct infllm_engine {
         L.last_b = b;
         L.n_fed += lx;
         L.step += 1;
+        {  // check_conservation (engine.hpp:373-383): every fed token is initial, local, pending or in a unit
+            ++inv_checks;
+            const int64_t in_units = L.n_units ? L.unit_start.back() + L.unit_len.back() - cfg.init_size : 0;
+            if (L.init_len + (L.n_fed - L.local_start) + L.pend_count + in_units != L.n_fed) ++inv_conservation_bad;
+        }
         ck(cudaGetLastError(), "kernel launch");
     }
 
@@ -1234,6 +1265,7 @@ struct infllm_engine {
     template <typename T>
     void encode_stream(int li, const void* q, const void* k, const void* v, int64_t n, void* out, cudaStream_t st,
                        bool host) {
+        NvtxRange nv("encode_stream");
         if (li < 0 || li >= n_layers) throw StreamError("layer out of range");
         if (n < 1) throw StreamError("encode_stream: empty stream");
         Layer& L = layers[static_cast<size_t>(li)];
@@ -1292,10 +1324,10 @@ struct infllm_engine {
             g.before = cur;
             g.bufs = bufs;
             const int64_t l0 = launches;
+            const uint64_t c0 = inv_checks, b0 = inv_conservation_bad;
             cudaGraph_t graph = nullptr;
             capturing = true;
-            cap_attn_ev = &g.attn_ev;
-            cap_lookup_ev = &g.lookup_ev;
+            cap_ev = g.ev;
             const int64_t seq0 = seq;
             ck(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal), "begin capture");
             capture_seq0 = seq;
@@ -1324,6 +1356,10 @@ struct infllm_engine {
             g.after = save(L);
             g.launches = launches - l0;
             launches = l0;
+            g.inv_checks = inv_checks - c0;
+            g.inv_bad = inv_conservation_bad - b0;
+            inv_checks = c0;
+            inv_conservation_bad = b0;
             restore(L, cur);
             if (graphs.size() >= kMaxGraphs) {  // bounded cache: the oldest capture goes
                 ck(cudaStreamSynchronize(st), "graph drop");
@@ -1338,6 +1374,8 @@ struct infllm_engine {
         seq += ge->steps;
         restore(L, ge->after);
         launches += ge->launches;
+        inv_checks += ge->inv_checks;
+        inv_conservation_bad += ge->inv_bad;
         if (prof) ge->replays_in_window++;
     }
 
@@ -1491,6 +1529,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
                          &e->e_attnp[0], &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
         e->prep_sync.alloc(prep_chunk_sync_bytes(), st);
+        e->inv_dev.alloc(sizeof(unsigned long long), st);
         e->chunk_qsum.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
         e->mass_e.alloc(static_cast<size_t>(e->Hs) * cfg->chunk_size * km * sizeof(float), st);
@@ -1541,14 +1580,11 @@ int infllm_engine_destroy(infllm_engine_t e) {
         for (auto* b : e->dev_buffers()) b->release(st);
         for (auto& L : e->layers)
             for (auto* h : {&L.host_k, &L.host_krot, &L.host_v}) h->release();
-        for (auto& p : e->ev_attn) {
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
-        }
-        for (auto& p : e->ev_lookup) {
-            cudaEventDestroy(p.first);
-            cudaEventDestroy(p.second);
-        }
+        for (auto& evs : e->ev)
+            for (auto& p : evs) {
+                cudaEventDestroy(p.first);
+                cudaEventDestroy(p.second);
+            }
         for (auto ev : e->ev_pool) cudaEventDestroy(ev);
         for (auto& g : e->graphs) infllm_engine::drop_graph(g);
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
@@ -1990,59 +2026,76 @@ int infllm_kernel_launches(infllm_engine_t e, int64_t* n_out) {
 
 int infllm_profile_begin(infllm_engine_t e, int32_t enable) {
     return guard([&] {
-        for (auto& p : e->ev_attn) {
-            e->ev_pool.push_back(p.first);
-            e->ev_pool.push_back(p.second);
+        for (auto& evs : e->ev) {
+            for (auto& p : evs) {
+                e->ev_pool.push_back(p.first);
+                e->ev_pool.push_back(p.second);
+            }
+            evs.clear();
         }
-        for (auto& p : e->ev_lookup) {
-            e->ev_pool.push_back(p.first);
-            e->ev_pool.push_back(p.second);
-        }
-        e->ev_attn.clear();
-        e->ev_lookup.clear();
         for (auto& g : e->graphs) g.replays_in_window = 0;
         e->prof = enable != 0;
     });
 }
 
-int infllm_profile_read(infllm_engine_t e, double* attn_ms, int64_t* attn_n, double* lookup_ms, int64_t* lookup_n) {
-    return guard([&] {
-        ck(cudaDeviceSynchronize(), "sync");
-        double a = 0, b = 0;
-        for (auto& p : e->ev_attn) {
-            float ms = 0;
-            ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
-            a += ms;
+namespace {
+// device time of each phase's launches in the profile window (ms) and launch counts
+void phase_sums(infllm_engine* e, double* ms, int64_t* n) {
+    ck(cudaDeviceSynchronize(), "sync");
+    for (int ph = 0; ph < kPhases; ++ph) {
+        ms[ph] = 0;
+        n[ph] = static_cast<int64_t>(e->ev[ph].size());
+        for (auto& p : e->ev[ph]) {
+            float t = 0;
+            ck(cudaEventElapsedTime(&t, p.first, p.second), "elapsed");
+            ms[ph] += t;
         }
-        for (auto& p : e->ev_lookup) {
-            float ms = 0;
-            ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
-            b += ms;
-        }
-        int64_t na = static_cast<int64_t>(e->ev_attn.size()), nb = static_cast<int64_t>(e->ev_lookup.size());
         // graph replays: event nodes hold the timings of the latest replay
         for (auto& g : e->graphs) {
             if (g.replays_in_window == 0) continue;
-            double ga = 0, gb = 0;
-            for (auto& p : g.attn_ev) {
-                float ms = 0;
-                ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
-                ga += ms;
+            double gt = 0;
+            for (auto& p : g.ev[ph]) {
+                float t = 0;
+                ck(cudaEventElapsedTime(&t, p.first, p.second), "elapsed");
+                gt += t;
             }
-            for (auto& p : g.lookup_ev) {
-                float ms = 0;
-                ck(cudaEventElapsedTime(&ms, p.first, p.second), "elapsed");
-                gb += ms;
-            }
-            a += ga * g.replays_in_window;
-            b += gb * g.replays_in_window;
-            na += static_cast<int64_t>(g.attn_ev.size()) * g.replays_in_window;
-            nb += static_cast<int64_t>(g.lookup_ev.size()) * g.replays_in_window;
+            ms[ph] += gt * g.replays_in_window;
+            n[ph] += static_cast<int64_t>(g.ev[ph].size()) * g.replays_in_window;
         }
-        *attn_ms = a;
-        *attn_n = na;
-        *lookup_ms = b;
-        *lookup_n = nb;
+    }
+}
+}  // namespace
+
+int infllm_profile_read(infllm_engine_t e, double* attn_ms, int64_t* attn_n, double* lookup_ms, int64_t* lookup_n) {
+    return guard([&] {
+        double ms[kPhases];
+        int64_t n[kPhases];
+        phase_sums(e, ms, n);
+        *attn_ms = ms[kPhAttend];
+        *attn_n = n[kPhAttend];
+        *lookup_ms = ms[kPhLookup];
+        *lookup_n = n[kPhLookup];
+    });
+}
+
+int infllm_phase_timings(infllm_engine_t e, double* ms4, int64_t* launches4) {
+    return guard([&] {
+        if (!e || !ms4) throw ConfigError("null argument");
+        int64_t n[kPhases];
+        phase_sums(e, ms4, n);
+        if (launches4)
+            for (int ph = 0; ph < kPhases; ++ph) launches4[ph] = n[ph];
+    });
+}
+
+int infllm_invariants(infllm_engine_t e, uint64_t* checks, uint64_t* violations) {
+    return guard([&] {
+        if (!e || !checks || !violations) throw ConfigError("null argument");
+        unsigned long long dev = 0;
+        ck(cudaDeviceSynchronize(), "sync");
+        ck(cudaMemcpy(&dev, e->inv_dev.p, sizeof(dev), cudaMemcpyDeviceToHost), "D2H");
+        *checks = e->inv_checks;
+        *violations = e->inv_conservation_bad + dev;
     });
 }
 

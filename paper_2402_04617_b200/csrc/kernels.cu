@@ -1552,6 +1552,8 @@ __global__ void __launch_bounds__(kThreads) k_attn_simt(AttnParams p) {
     if (qvalid) {
         T* out = static_cast<T*>(p.out) + (qi * p.H + h) * dv;
         const float inv = 1.f / l;
+        if (p.inv_violations && sub == 0 && !(l > 0.f && isfinite(l) && isfinite(inv)))
+            atomicAdd(p.inv_violations, 1ull);  // check_softmax (engine.hpp:361-371)
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             const int c = sub + 8 * t;

@@ -124,6 +124,9 @@ struct AttnParams {
     // lookup of this step, which itself followed the prep, eviction and LRU it needs)
     const int64_t* ready_flag;
     int64_t ready_val;
+    // check_softmax (engine.hpp:361-371) on the device: rows whose softmax
+    // denominator is not a positive finite number add one here (or null)
+    unsigned long long* inv_violations;
     float scale;
     VLayout vl;
 };

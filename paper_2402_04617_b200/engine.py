@@ -197,6 +197,19 @@ class StreamEngine:
     def profile_begin(self, enable=True):
         check(lib().infllm_profile_begin(self.h, int(enable)))
 
+    def phase_timings(self):
+        """PhaseTimings (engine.hpp:43-49) of the profile window: device ms per phase."""
+        ms = (C.c_double * 4)()
+        n = (C.c_int64 * 4)()
+        check(lib().infllm_phase_timings(self.h, ms, n))
+        return {"lookup": ms[0], "attend": ms[1], "score": ms[2], "evict": ms[3]}
+
+    def invariants(self):
+        """(invariant_checks, invariant_violations) (engine.hpp:88-89)."""
+        c, v = C.c_uint64(), C.c_uint64()
+        check(lib().infllm_invariants(self.h, C.byref(c), C.byref(v)))
+        return c.value, v.value
+
     def profile_read(self):
         a, b = C.c_double(), C.c_double()
         na, nb = C.c_int64(), C.c_int64()

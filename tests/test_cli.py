@@ -57,3 +57,31 @@ def test_cli_bench_and_run(tmp_path):
     assert sum(ln.endswith(" hit") for ln in lines) == m["hits"]
     step, unit, flag = lines[0].split()
     assert int(step) >= 0 and int(unit) >= 0 and flag in ("hit", "miss")
+
+
+@pytest.mark.gpu
+def test_cli_oracle_check(tmp_path):
+    """cmd_oracle_check (cli.cpp:239-351): the three self-checks pass, report schema and exit code."""
+    out = tmp_path / "oc.json"
+    rc = cli.main(["oracle-check", "--length", "768", "--chunk_size", "128", "--local_size", "256", "--init_size", "64",
+                   "--n_lookup", "4", "--out", str(out)])
+    rep = json.loads(out.read_text())
+    assert [c["check"] for c in rep["checks"]] == ["degenerate_vs_dense", "full_retrieval_vs_windowed",
+                                                   "repr_scores_incremental_vs_batch"]
+    for c in rep["checks"]:
+        assert set(c) == {"check", "max_abs_err", "mean_abs_err", "compared", "mismatches", "tolerance", "pass"}
+        assert c["pass"], c
+    assert rep["ok"] and rc == 0
+
+
+@pytest.mark.gpu
+def test_cli_metrics_timings_and_invariants(tmp_path):
+    out = tmp_path / "run.json"
+    rc = cli.main(["run", "--length", "4096", "--decode_tail", "8", "--n_heads", "8", "--n_kv_heads", "2",
+                   "--chunk_size", "256", "--local_size", "1024", "--n_lookup", "4", "--out", str(out)])
+    assert rc == 0
+    m = json.loads(out.read_text())["metrics"]
+    assert set(m["timings_ms"]) >= {"adapter", "lookup", "attend", "score", "evict"}
+    assert m["timings_ms"]["attend"] > 0 and m["timings_ms"]["lookup"] > 0
+    # check_conservation once per step, check_softmax per head and row of the steps that retrieved units
+    assert m["invariant_checks"] > m["steps"] and m["invariant_violations"] == 0
