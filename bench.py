@@ -174,6 +174,45 @@ def cpu_sample(threads, steps=2, warm=8192, seed=0):
                 seconds=dt)
 
 
+C0_CFG = dict(chunk_size=128, unit_size=128, n_repr=4, local_size=512, init_size=64, n_lookup=4, hot_capacity=32,
+              decay=0.1)
+
+
+def cpu_reference_c0(n=8192, seed=0):
+    """The reference itself (oracle/_ref: StreamEngine<float> compiled here from
+    /root/reference's headers, prebuilt by build() and shipped with the repo)
+    beside the oracle port on BASELINE configs[0] (C0: 1 head, d 64, 8K tokens,
+    the reference's own synthetic adapter), both single-threaded: tokens/s of
+    each and whether their outputs are bitwise equal. This calibrates the port
+    that stands in for the reference at C2, where the reference has no
+    warm-start path and a steady-state step would need minutes of ramp-up."""
+    from oracle import oracle as O
+    from oracle import ref as R
+
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libblockmem_ref.so")):
+        return {"available": False, "why": "oracle/_ref not built (needs /root/reference at build time)"}
+    shape = O.ModelShape.make(n_heads=1, head_dim=64)
+    ids = O.noise_ids(seed, n)
+    q, k, v = O.adapter_batch(seed, shape, ids)
+    sched = O.encode_schedule(n, C0_CFG["chunk_size"], 32)
+    t0 = time.perf_counter()
+    re = R.RefEngine(O.EngineConfig.make(**C0_CFG), 1, 64)
+    re.set_inputs(q, k, v)
+    ro = [re.step(b, decode=i >= len(sched) - 32)[0][0] for i, b in enumerate(sched)]
+    t_ref = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oe = O.OracleEngine(O.EngineConfig.make(**C0_CFG), shape, n_threads=1)
+    po, fed = [], 0
+    for i, b in enumerate(sched):
+        po.append(oe.step(q[fed:fed + b], k[fed:fed + b], v[fed:fed + b], decode=i >= len(sched) - 32).out)
+        fed += b
+    t_port = time.perf_counter() - t0
+    return {"available": True, "workload": "C0 (configs[0]): 1 head, d 64, 8192-token adapter stream, chunk 128, "
+                                           "window 512, k_m 4, 32 decode steps",
+            "reference_tokens_per_s": n / t_ref, "port_tokens_per_s": n / t_port, "cores": 1,
+            "outputs_bitwise_equal": bool(np.array_equal(np.concatenate(ro), np.concatenate(po)))}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -192,6 +231,10 @@ def run_reference(args, rank, world):
                                    "l_L 4096, l_I 128, chunk 512; CPU sample of steady-state chunk steps"},
             "cpu_baseline": {k: vals[-1][k] for k in ("unit", "cores", "kind", "sample")} | {"value": v},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        line["reference_c0"] = cpu_reference_c0()
+    except Exception as ex:  # reported, not fatal
+        line["reference_c0"] = {"available": False, "why": str(ex)}
     print(json.dumps(line), flush=True)
 
 
@@ -287,13 +330,24 @@ def run_b200(args, rank, world, local_rank):
     extra = other_configs(Q, K, V, dev) if (rank == 0 and not args.no_extra) else {}
 
     if rank == 0:
-        cpu = None
+        cpu = cpu_all = cpu_c0 = None
         if world == 1 and not args.no_cpu:
+            # the reference runs one stream per core (no intra-stream threads, proj/CMakeLists.txt;
+            # parallel.hpp only spreads trials): the primary baseline is one core per stream
             try:
-                cpu = cpu_sample(os.cpu_count() or 1, steps=10)
+                cpu = cpu_sample(1, steps=1)
                 cpu.pop("seconds", None)
             except Exception as ex:  # reported, not fatal
                 cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+            try:
+                cpu_all = cpu_sample(os.cpu_count() or 1, steps=2)
+                cpu_all.pop("seconds", None)
+            except Exception as ex:
+                cpu_all = {"value": None, "sample": f"failed: {ex}"}
+            try:
+                cpu_c0 = cpu_reference_c0()
+            except Exception as ex:
+                cpu_c0 = {"available": False, "why": str(ex)}
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -318,6 +372,8 @@ def run_b200(args, rank, world, local_rank):
                                     "note": "in-stream: the lookup shares the GPU with the attention of the previous "
                                             "step (20 free SMs); isolated: same launch alone, steady state"} | iso},
             "cpu_baseline": cpu,
+            "cpu_baseline_all_cores": cpu_all,
+            "cpu_reference_c0": cpu_c0,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
@@ -384,89 +440,143 @@ def isolated_kernels(eng, steps, H, Hkv, d, dev):
     return out
 
 
-def other_configs(Q, K, V, dev, batch=32, dec_steps=24):
-    """The other BASELINE.json configs, measured on the same box after the
-    headline (not part of `value`):
-    C4 decode: `batch` independent sequences prefilled to 128K tokens, then one
-    infllm_decode_batch call per step (every stage one launch for the batch),
-    device time per step over `dec_steps` steps (CUDA events); also the
-    single-sequence decode_step latency.
-    C3: the 1M-token planted stream with the host-offloaded unit store
-    (pinned-host pages + 48-slot GPU unit cache): prefill tokens/s, probe
-    recall, page loads / cache hit rate, H2D GB/s (tools/c3_planted.py)."""
+def c1_stream(dev, steps=5):
+    """BASELINE configs[1] (C1): Mistral-7B heads (32q/8kv, d 128), one 32K-token
+    stream, same InfLLM settings; device-resident tokens/s (graph-replayed
+    encode_stream, CUDA events) and the attention's roofline over its steps."""
+    import torch
+
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    n = 32768
+    g = torch.Generator(device=dev)
+    g.manual_seed(4321)
+    H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
+    q = torch.randn((n, H, d), generator=g, device=dev).bfloat16()
+    k = torch.randn((n, Hkv, d), generator=g, device=dev).bfloat16()
+    v = torch.randn((n, Hkv, d), generator=g, device=dev).bfloat16()
+    eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16)
+    eng.reserve(n)
+    out = torch.empty_like(q)
+    for _ in range(3):
+        eng.reset()
+        eng.encode_stream(q, k, v, out=out)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        eng.reset()
+        eng.encode_stream(q, k, v, out=out)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / steps
+    eng.profile_begin(True)
+    eng.reset()
+    eng.encode_stream(q, k, v, out=out)
+    prof = eng.profile_read()
+    eng.close()
+    sch = stream_schedule(n, CFG)
+    flops = attention_flops(sch, H, d)
+    peak = load_peaks()["bf16"]
+    return {"workload": "C1 (configs[1]): Mistral-7B-inst-v0.2 heads (32q/8kv, d128), one 32K-token stream, "
+                        "unit 128, r_k 4, k_m 16, init 128, window 4K, chunk 512, bf16",
+            "tokens_per_s": n / (ms / 1e3), "ms_per_stream": ms,
+            "attention_tflops": flops / (prof["attn_ms"] / 1e3) / 1e12,
+            "attention_frac_of_peak": flops / (prof["attn_ms"] / 1e3) / 1e12 / peak}
+
+
+def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), dec_steps=16):
+    """BASELINE configs[4] (C4): decode-step latency at 128K / 512K context for
+    B = 1..32 independent sequences (infllm_decode_batch: every stage one
+    launch for the batch; B = 1 is the single-sequence decode_step chain).
+    The sequences are prefilled once per context through encode_stream; each
+    B reuses the first B of them. Device time per step over dec_steps steps."""
     import torch
 
     from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, decode_batch
 
-    out = {}
     H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
-    n = Q.shape[0]
-    try:
+    bmax = max(batches)
+    rows = []
+    for ctx in contexts:
         g = torch.Generator(device=dev)
-        g.manual_seed(77)
-        tot = dec_steps + 4
-        qd = torch.randn((tot, batch, H, d), generator=g, device=dev).bfloat16()
-        kd = torch.randn((tot, batch, Hkv, d), generator=g, device=dev).bfloat16()
-        vd = torch.randn((tot, batch, Hkv, d), generator=g, device=dev).bfloat16()
-        res = torch.empty((batch, H, d), device=dev, dtype=torch.bfloat16)
+        g.manual_seed(ctx)
+        Q = torch.randn((ctx, H, d), generator=g, device=dev).bfloat16()
+        K = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
+        V = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
+        tot = (dec_steps + 2) * len(batches) + 4
         engs = []
-        for _ in range(batch):
+        for _ in range(bmax):
             e = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16)
-            e.reserve(n + tot + 1)
+            e.reserve(ctx + tot + 1)
             e.encode_stream(Q, K, V)
             engs.append(e)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        for t in range(4):
-            decode_batch(engs, qd[t], kd[t], vd[t], out=res)
-        torch.cuda.synchronize(dev)
-        e0.record()
-        for t in range(4, tot):
-            decode_batch(engs, qd[t], kd[t], vd[t], out=res)
-        e1.record()
-        torch.cuda.synchronize(dev)
-        step_ms = e0.elapsed_time(e1) / dec_steps
-        units = engs[0].metrics()["units"]
-        kv_b = batch * (CFG["init_size"] + CFG["n_lookup"] * CFG["unit_size"] + CFG["local_size"] + 1) * Hkv * d * 4
-        ix_b = batch * units * CFG["n_repr"] * Hkv * d * 2
-        # one sequence, decode_step (caller's stream, split-KV attention)
-        one = engs[0]
-        q1 = qd[:, 0:1].contiguous()
-        k1 = kd[:, 0:1].contiguous()
-        v1 = vd[:, 0:1].contiguous()
-        one.reset()
-        one.encode_stream(Q, K, V)
-        for t in range(4):
-            one.decode_step(q1[t], k1[t], v1[t])
-        torch.cuda.synchronize(dev)
-        e0.record()
-        for t in range(4, tot):
-            one.decode_step(q1[t], k1[t], v1[t])
-        e1.record()
-        torch.cuda.synchronize(dev)
-        one_ms = e0.elapsed_time(e1) / dec_steps
-        out["c4_decode"] = {
-            "workload": f"C4: {batch} sequences x 128K context, Llama-3-8B heads, one decode token per sequence per "
-                        f"step (infllm_decode_batch)", "batch": batch, "context": n, "steps": dec_steps,
-            "step_ms": step_ms, "tokens_per_s": batch / (step_ms / 1e3),
-            "hbm_bytes_per_step": kv_b + ix_b, "hbm_gbs": (kv_b + ix_b) / (step_ms / 1e3) / 1e9,
-            "single_sequence_step_ms": one_ms,
-            "timing": "CUDA events around dec_steps consecutive batched steps (device time incl. host gaps)"}
+        del Q, K, V
+        qd = torch.randn((tot, bmax, H, d), generator=g, device=dev).bfloat16()
+        kd = torch.randn((tot, bmax, Hkv, d), generator=g, device=dev).bfloat16()
+        vd = torch.randn((tot, bmax, Hkv, d), generator=g, device=dev).bfloat16()
+        t = 0
+        for B in batches:
+            sub = engs[:B]
+            res = torch.empty((B, H, d), device=dev, dtype=torch.bfloat16)
+            for _ in range(2):
+                decode_batch(sub, qd[t, :B].contiguous(), kd[t, :B].contiguous(), vd[t, :B].contiguous(), out=res)
+                t += 1
+            qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
+            ks = [kd[t + i, :B].contiguous() for i in range(dec_steps)]
+            vs = [vd[t + i, :B].contiguous() for i in range(dec_steps)]
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(dec_steps):
+                decode_batch(sub, qs[i], ks[i], vs[i], out=res)
+            e1.record()
+            torch.cuda.synchronize(dev)
+            t += dec_steps
+            ms = e0.elapsed_time(e1) / dec_steps
+            units = sub[0].metrics()["units"]
+            kv_b = B * (CFG["init_size"] + CFG["n_lookup"] * CFG["unit_size"] + CFG["local_size"] + 1) * Hkv * d * 4
+            ix_b = B * units * CFG["n_repr"] * Hkv * d * 2
+            rows.append({"context": ctx, "batch": B, "step_us": ms * 1e3, "tokens_per_s": B / (ms / 1e3),
+                         "hbm_bytes_per_step": kv_b + ix_b, "hbm_gbs": (kv_b + ix_b) / (ms / 1e3) / 1e9})
         for e in engs:
             e.close()
-        del engs
-    except Exception as ex:  # reported, not fatal
-        out["c4_decode"] = {"error": str(ex)}
-    torch.cuda.empty_cache()
+        del engs, qd, kd, vd
+        torch.cuda.empty_cache()
+    return {"workload": "C4 (configs[4]): decode step latency, Llama-3-8B heads, 128K / 512K context, B "
+                        "independent sequences per step (infllm_decode_batch; B = 1: decode_step chain)",
+            "timing": f"CUDA events around {dec_steps} consecutive steps (device time incl. host launch gaps)",
+            "hbm_bytes": "K/V^T of init + k_m units + local window + the new token, plus the repr index scan",
+            "peak_gbs": load_peaks()["hbm"], "grid": rows}
+
+
+def other_configs(Q, K, V, dev):
+    """The other BASELINE.json configs, measured on the same box after the
+    headline (not part of `value`): C1 (32K stream), C4 (decode grid) and C3
+    (1M-token planted stream with the host-offloaded unit store and the
+    32-slot GPU unit cache of SURVEY §8d: prefill tokens/s, probe recall,
+    page loads / cache hit rate, H2D GB/s; tools/c3_planted.py)."""
+    import torch
+
+    out = {}
+    for name, fn in (("c1_stream", lambda: c1_stream(dev)), ("c4_decode", lambda: decode_grid(dev))):
+        try:
+            out[name] = fn()
+        except Exception as ex:  # reported, not fatal
+            out[name] = {"error": str(ex)}
+        torch.cuda.empty_cache()
     try:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import c3_planted
 
-        ok, tps, ts = c3_planted.run(1 << 20, verbose=False, slots=48)
+        slots = 32
+        ok, tps, ts = c3_planted.run(1 << 20, verbose=False, slots=slots)
         req = ts["loads"] + ts["cache_hits"]
         out["c3_host_tier"] = {
-            "workload": "C3: 1M-token planted stream, unit pages in pinned host memory, 48-slot GPU unit cache "
-                        "(host_tier_slots)", "tokens_per_s": tps, "probe_recall": 1.0 if ok else 0.0,
+            "workload": f"C3 (configs[3]): 1M-token planted stream, unit pages in pinned host memory, {slots}-slot "
+                        "GPU unit cache (host_tier_slots)", "tokens_per_s": tps, "probe_recall": 1.0 if ok else 0.0,
             "page_loads": ts["loads"], "cache_hit_rate": ts["cache_hits"] / max(req, 1),
+            "miss_rate": ts["loads"] / max(req, 1),
             "h2d_gb": ts["h2d_bytes"] / 1e9, "h2d_gbs": ts["h2d_bytes"] / ((1 << 20) / tps) / 1e9}
     except Exception as ex:
         out["c3_host_tier"] = {"error": str(ex)}

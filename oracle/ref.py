@@ -1,9 +1,11 @@
 """TEST INFRASTRUCTURE ONLY — ctypes binding of oracle/_ref, the reference
 engine compiled from /root/reference/proj/include where it lies (against the
 Eigen-subset shim, see oracle/Makefile). Used to pin the oracle restatement
-(tests/test_oracle_pin.py) and to generate tests/golden fixtures
-(tests/golden/make_golden.py). /root/reference is absent on the GPU box, so
-nothing that runs there imports this module.
+(tests/test_oracle_pin.py), to generate tests/golden fixtures
+(tests/golden/make_golden.py) and, in bench.py's CPU legs only, to time the
+reference beside the port on C0. /root/reference is absent on the GPU box:
+there only the prebuilt oracle/_ref/*.so (shipped with the repo snapshot)
+are loaded, never rebuilt.
 """
 from __future__ import annotations
 

@@ -97,6 +97,16 @@ __device__ __forceinline__ void tl_put(unsigned kid, unsigned long long t0) {
         if (threadIdx.x == 0 && ::infllm::g_tl.rec) ::infllm::tl_put((kid), tl_t0_); \
     } while (0)
 
+// phase marks inside a kernel (timeline kinds 100 + k): thread 0 of each block
+// records [mark, now] and restarts `mark` (a variable holding the last mark)
+#define TL_MARK(k, mark)                                    \
+    do {                                                    \
+        if (threadIdx.x == 0 && ::infllm::g_tl.rec) {       \
+            ::infllm::tl_put(100 + (k), (mark));            \
+            (mark) = ::infllm::gtimer();                    \
+        }                                                   \
+    } while (0)
+
 // step-ready flags between the side streams and the attention (engine.cu)
 __device__ __forceinline__ void flag_release(int64_t* f, int64_t v) {
     asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(f), "l"(v) : "memory");

@@ -267,6 +267,7 @@ struct infllm_engine {
     bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
     bool dec_disabled = false;
     int lookup_upb = 48;      // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
+    int lookup_upb_decode = 8;  // option lookup_units_per_block_decode: the same for one-token steps (whole GPU)
     bool attn_flag = false;   // option attn_flag: K3 waits on a step-ready flag instead of graph edges
     int prep_blocks = 0;      // option prep_blocks: grid cap of the chunk prep kernels (0: none)
     bool prep_fused = false;  // option prep_fused: one-kernel chunk prep (side.cu) where the shape allows
@@ -909,7 +910,10 @@ struct infllm_engine {
                 lp.fused = 2;
                 coll->lookup.push_back(lp);
             }
-            const bool fast = !coll && Gs == Gt && lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
+            // one-token steps keep the latency-tuned two-kernel path (fused radix tail, K4
+            // as its programmatic dependent); chunk steps take the one-launch kernel sized
+            // for the ~20 SMs the attention leaves free
+            const bool fast = !coll && !one_stream && Gs == Gt && lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
             last_lkp_fast = fast && !(debug_skip & 2);
             if (fast) {
                 // one launch: scan + exact top-k; few fat blocks inside the prefill
@@ -919,8 +923,9 @@ struct infllm_engine {
                 lp.cand_i = reinterpret_cast<int64_t*>(L.cand.as<double>() + nc);
                 lp.fused = 1;
                 lp.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
+                last_lkp = lp;
                 if (!(debug_skip & 2))
-                    launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units0, one_stream ? 8 : lookup_upb), st);
+                    launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units0, one_stream ? lookup_upb_decode : lookup_upb), st);
             } else if (coll) {
             } else if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
             if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
@@ -1669,7 +1674,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // captured stream graphs bake in the launch choices these options make:
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
-            k == "attn_pdl" || k == "lookup_units_per_block" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
+            k == "attn_pdl" || k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1692,6 +1697,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->prep_blocks = static_cast<int>(std::clamp<int64_t>(value, 0, 1 << 20));
         else if (k == "attn_flag")
             e->attn_flag = value != 0;
+        else if (k == "lookup_units_per_block_decode")
+            e->lookup_upb_decode = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
         else if (k == "lookup_units_per_block")
             e->lookup_upb = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
         else if (k == "attn_pdl")
@@ -2120,9 +2127,12 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
         // call's kernels, so neither the reuse nor a growth free can race with them
         static thread_local DBuf cand, cnt;
         static thread_local cudaEvent_t last = nullptr;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        ck(cudaStreamIsCapturing(st, &cs), "capture status");
+        const bool capturing_now = cs != cudaStreamCaptureStatusNone;  // a graph orders its own nodes
         if (!last)
             ck(cudaEventCreateWithFlags(&last, cudaEventDisableTiming), "event");
-        else
+        else if (!capturing_now)
             ck(cudaStreamWaitEvent(st, last, 0), "wait");
         cand.grow(static_cast<size_t>(nc) * 16, st);
         LookupParams lp{};
@@ -2148,7 +2158,7 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
             launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cand.as<double>(),
                                reinterpret_cast<int64_t*>(cand.as<double>() + nc), st);
         ck(cudaGetLastError(), "lookup");
-        ck(cudaEventRecord(last, st), "record");
+        if (!capturing_now) ck(cudaEventRecord(last, st), "record");
     });
 }
 
@@ -2166,7 +2176,12 @@ int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, d
                 case 0:
                     if (e->last_bf16) launch_prep<bf16>(e->last_pp, st); else launch_prep<float>(e->last_pp, st);
                     break;
-                case 1: launch_lookup(e->last_lkp, e->last_bf16, st); break;
+                case 1:  // the engine's lookup of the last step, sized as in a decode step (whole GPU)
+                    if (e->last_lkp.cand_v && lookup_topk_supported(e->last_lkp, e->last_bf16))
+                        launch_lookup_topk_fast(e->last_lkp, lookup_topk_blocks(e->last_lkp.U, e->lookup_upb_decode), st);
+                    else
+                        launch_lookup(e->last_lkp, e->last_bf16, st);
+                    break;
                 case 2:
                     if (e->last_bf16 && e->tc_eligible(e->last_ap.lx)) launch_attn_tc(e->last_ap, st);
                     else if (e->last_bf16) launch_attn_simt<bf16>(e->last_ap, st);

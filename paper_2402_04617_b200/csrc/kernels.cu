@@ -1252,7 +1252,8 @@ constexpr int kScanBlocks = 148;  // streaming scan: one block per SM, one slice
 int64_t topk_multi_scratch(int64_t U, int64_t k) {
     const int64_t nb = (U + kSliceU - 1) / kSliceU;
     const int64_t n = (nb > kScanBlocks ? nb : kScanBlocks) * k;
-    return n > 148 * 32 ? n : 148 * 32;  // also the block lists of k_lookup_topk (lookup.cu)
+    const int64_t m = n > 148 * 32 ? n : 148 * 32;  // also the block lists of k_lookup_topk (lookup.cu)
+    return (m + 1) / 2 * 2;  // the id half starts 16-byte aligned (bulk copies)
 }
 int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
     p.fused = 2;

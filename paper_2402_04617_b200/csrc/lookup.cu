@@ -72,32 +72,48 @@ __device__ __forceinline__ void warp_merge(uint64_t& k, int& i, uint64_t bk, int
 }
 }  // namespace
 
+constexpr int kLkMaxSlice = 1024;  // units per block (keys staged in shared memory)
+constexpr int kLkSurv = 1024;      // survivors of the threshold filter kept for the final sort
+
+// the best 32 of n (key, id) pairs in shared memory, sorted desc, in warp `lane`s registers
+__device__ __forceinline__ void warp_top32(const uint64_t* key, const int* id, int n, uint64_t& bk, int& bi,
+                                           int lane) {
+    bk = 0;
+    bi = -1;
+    for (int c = 0; c < n; c += 32) {
+        uint64_t k = c + lane < n ? key[c + lane] : 0ull;
+        int i = c + lane < n ? id[c + lane] : -1;
+        warp_sort_desc(k, i, lane);
+        if (c == 0) {
+            bk = k;
+            bi = i;
+        } else {
+            warp_merge(bk, bi, k, i, lane);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p) {
     if (p.early_dependents) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // decode K4 (PDL)
     TL_BEGIN();
     extern __shared__ __align__(128) uint8_t lk_smem[];
     __shared__ __align__(8) uint64_t sbar[kLkWarps][kLkStages];
+    __shared__ __align__(8) uint64_t cbar;
     __shared__ double sq[8 * 128];
+    __shared__ uint64_t skey[kLkMaxSlice];
+    __shared__ int sid[kLkMaxSlice];
     __shared__ uint64_t slk[kLkWarps][32];
     __shared__ int sli[kLkWarps][32];
+    __shared__ uint64_t s_tau;
+    __shared__ int s_cnt;
     __shared__ bool last;
     const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
     const int nb = static_cast<int>(gridDim.x);
     const int64_t S = (p.U + nb - 1) / nb;
     const int64_t s0 = min(static_cast<int64_t>(blockIdx.x) * S, p.U), s1 = min(s0 + S, p.U);
+    const int ns = static_cast<int>(s1 - s0);
     const int64_t bytes_u = static_cast<int64_t>(p.G) * 512 * 2;
     uint8_t* ring = lk_smem + static_cast<size_t>(wib) * kLkStages * kLkStageBytes;
-    for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) sq[t] = p.qsum[t];
-    if (lane == 0)
-        for (int st = 0; st < kLkStages; ++st) tc::mbar_init(&sbar[wib][st], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    double q[8][4];
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? sq[g * 128 + 4 * lane + j] : 0.0;
-
     auto issue = [&](int64_t u, int stage) {
         if (u < s1 && lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage was read by this warp
@@ -110,99 +126,158 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
                 : "memory");
         }
     };
+    // each warp's first units are in flight before anything else happens
+    if (lane == 0) {
+        for (int st = 0; st < kLkStages; ++st) tc::mbar_init(&sbar[wib][st], 1);
+        if (wib == 0) tc::mbar_init(&cbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
     const int64_t u0 = s0 + wib;
 #pragma unroll
     for (int st = 0; st < kLkStages - 1; ++st) issue(u0 + st * kLkWarps, st);
+    for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) sq[t] = p.qsum[t];
+    __syncthreads();
+    unsigned long long mark = tl_t0_;
+    double q[8][4];
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? sq[g * 128 + 4 * lane + j] : 0.0;
+
     int stage = 0;
     int64_t it = 0;
-    // running top-32 of this warp's units
+    for (int64_t u = u0; u < s1; u += kLkWarps, ++it) {
+        issue(u + (kLkStages - 1) * kLkWarps, (stage + kLkStages - 1) % kLkStages);
+        tc::mbar_wait(&sbar[wib][stage], static_cast<uint32_t>((it / kLkStages) & 1));
+        const uint8_t* buf = ring + stage * kLkStageBytes + 8 * lane;
+        double rel = 0.0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+            if (g >= p.G) break;
+            double a = 0.0;
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const uint2 v = *reinterpret_cast<const uint2*>(buf + (4 * g + rr) * 256);
+                a = fma(q[g][0], static_cast<double>(__uint_as_float(v.x << 16)), a);
+                a = fma(q[g][1], static_cast<double>(__uint_as_float(v.x & 0xffff0000u)), a);
+                a = fma(q[g][2], static_cast<double>(__uint_as_float(v.y << 16)), a);
+                a = fma(q[g][3], static_cast<double>(__uint_as_float(v.y & 0xffff0000u)), a);
+            }
+            rel += a;
+        }
+        rel = warp_sum_d(rel);
+        if (lane == 0) {
+            if (p.rel) p.rel[u] = rel;
+            skey[u - s0] = lk_key(rel);
+            sid[u - s0] = static_cast<int>(u);
+        }
+        __syncwarp();  // the stage is refilled next iteration
+        stage = (stage + 1) % kLkStages;
+    }
+    __syncthreads();
+    TL_MARK(0, mark);  // scan
+    if (p.n_sel <= 0) return;
+    // this block's best 32 (rel desc, id asc), published for the last block
+    if (wib == 0) {
+        uint64_t bk;
+        int bi;
+        warp_top32(skey, sid, ns, bk, bi, lane);
+        p.cand_v[blockIdx.x * 32 + lane] = __longlong_as_double(static_cast<long long>(bk));
+        reinterpret_cast<int64_t*>(p.cand_i)[blockIdx.x * 32 + lane] = bi;
+        __syncwarp();
+        if (lane == 0) {
+            unsigned prev = 0;
+            if (nb > 1) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                prev = atomicAdd(p.done, 1u);
+            }
+            last = prev == static_cast<unsigned>(nb - 1);
+        }
+    }
+    __syncthreads();
+    TL_MARK(1, mark);  // block list published
+    TL_END(TL_LOOKUP);
+    if (!last) return;
+    if (nb > 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // last block: every block list into shared memory with two bulk copies
+    uint64_t* ck_all = reinterpret_cast<uint64_t*>(lk_smem);
+    int64_t* ci_all = reinterpret_cast<int64_t*>(lk_smem + static_cast<size_t>(nb) * 32 * sizeof(uint64_t));
+    uint64_t* sv = reinterpret_cast<uint64_t*>(lk_smem + static_cast<size_t>(nb) * 32 * 16);  // survivors
+    int* si = reinterpret_cast<int*>(sv + kLkSurv);
+    if (threadIdx.x == 0) {
+        const uint32_t nbytes = static_cast<uint32_t>(nb) * 32 * 8;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc::mbar_expect_tx(&cbar, 2 * nbytes);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         tc::smem_u32(ck_all)),
+                     "l"(p.cand_v), "r"(nbytes), "r"(tc::smem_u32(&cbar))
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         tc::smem_u32(ci_all)),
+                     "l"(p.cand_i), "r"(nbytes), "r"(tc::smem_u32(&cbar))
+                     : "memory");
+        s_cnt = 0;
+        s_tau = 0;
+    }
+    tc::mbar_wait(&cbar, 0);
+    __syncthreads();
+    TL_MARK(2, mark);  // candidates staged
+    // threshold: the k-th best of any block list is a lower bound of the global k-th best
+    const int k = static_cast<int>(p.n_sel < 32 ? p.n_sel : 32);
+    {
+        uint64_t t = 0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) t = max(t, ck_all[b * 32 + k - 1]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_xor_sync(kFull, t, o));
+        if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_tau), static_cast<unsigned long long>(t));
+    }
+    __syncthreads();
+    const uint64_t tau = s_tau;
+    for (int t = threadIdx.x; t < nb * 32; t += blockDim.x) {
+        const int id = static_cast<int>(ci_all[t]);
+        if (id >= 0 && ck_all[t] >= tau) {
+            const int slot = atomicAdd(&s_cnt, 1);
+            if (slot < kLkSurv) {
+                sv[slot] = ck_all[t];
+                si[slot] = id;
+            }
+        }
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
     uint64_t bk = 0;
     int bi = -1;
-    for (int64_t base = s0; base < s1; base += 32 * kLkWarps) {
-        // up to 32 units of this warp per batch: unit u = base + wib + 8 * r, r < 32
-        uint64_t ck = 0;
-        int ci = -1;
-#pragma unroll 1
-        for (int r = 0; r < 32; ++r) {
-            const int64_t u = base + wib + static_cast<int64_t>(kLkWarps) * r;
-            if (u >= s1) break;
-            issue(u + (kLkStages - 1) * kLkWarps, (stage + kLkStages - 1) % kLkStages);
-            tc::mbar_wait(&sbar[wib][stage], static_cast<uint32_t>((it / kLkStages) & 1));
-            const uint8_t* buf = ring + stage * kLkStageBytes + 8 * lane;
-            double rel = 0.0;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-                if (g >= p.G) break;
-                double a = 0.0;
-#pragma unroll
-                for (int rr = 0; rr < 4; ++rr) {
-                    const uint2 v = *reinterpret_cast<const uint2*>(buf + (4 * g + rr) * 256);
-                    a = fma(q[g][0], static_cast<double>(__uint_as_float(v.x << 16)), a);
-                    a = fma(q[g][1], static_cast<double>(__uint_as_float(v.x & 0xffff0000u)), a);
-                    a = fma(q[g][2], static_cast<double>(__uint_as_float(v.y << 16)), a);
-                    a = fma(q[g][3], static_cast<double>(__uint_as_float(v.y & 0xffff0000u)), a);
-                }
-                rel += a;
-            }
-            rel = warp_sum_d(rel);
-            if (lane == 0 && p.rel) p.rel[u] = rel;
-            if (lane == r) {
-                ck = lk_key(rel);
-                ci = static_cast<int>(u);
-            }
-            __syncwarp();  // the stage is refilled next iteration
-            stage = (stage + 1) % kLkStages;
-            ++it;
+    if (cnt <= kLkSurv) {
+        const int per = (cnt + kLkWarps - 1) / kLkWarps;  // each warp the best 32 of its share, then warp 0
+        const int a0 = min(cnt, wib * per), a1 = min(cnt, a0 + per);
+        if (cnt <= 32) {
+            if (wib == 0) warp_top32(sv, si, cnt, bk, bi, lane);
+        } else {
+            warp_top32(sv + a0, si + a0, a1 - a0, bk, bi, lane);
+            slk[wib][lane] = bk;
+            sli[wib][lane] = bi;
+            __syncthreads();
+            if (wib == 0)
+                for (int w = 1; w < kLkWarps; ++w) warp_merge(bk, bi, slk[w][lane], sli[w][lane], lane);
         }
-        warp_sort_desc(ck, ci, lane);
-        warp_merge(bk, bi, ck, ci, lane);
-    }
-    // block list: warp 0 merges the 8 warp lists
-    slk[wib][lane] = bk;
-    sli[wib][lane] = bi;
-    __syncthreads();
-    if (wib == 0) {
-        for (int w = 1; w < kLkWarps; ++w) warp_merge(bk, bi, slk[w][lane], sli[w][lane], lane);
-        p.cand_v[blockIdx.x * 32 + lane] = __longlong_as_double(static_cast<long long>(bk));
-        p.cand_i[blockIdx.x * 32 + lane] = bi;
-    }
-    TL_END(TL_LOOKUP);
-    if (nb == 1) {
-        last = true;
-    } else {
-        __threadfence();
+    } else {  // more than kLkSurv keys tie at the threshold: merge every block list
+        for (int b = wib; b < nb; b += kLkWarps)
+            warp_merge(bk, bi, ck_all[b * 32 + lane], static_cast<int>(ci_all[b * 32 + lane]), lane);
+        slk[wib][lane] = bk;
+        sli[wib][lane] = bi;
         __syncthreads();
-        if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == static_cast<unsigned>(nb - 1);
-        __syncthreads();
-        if (!last) return;
-        __threadfence();
+        if (wib == 0)
+            for (int w = 1; w < kLkWarps; ++w) warp_merge(bk, bi, slk[w][lane], sli[w][lane], lane);
     }
-    // last block: merge the nb block lists (staged in the now idle stage ring)
-    uint64_t* ck_all = reinterpret_cast<uint64_t*>(lk_smem);
-    int* ci_all = reinterpret_cast<int*>(lk_smem + static_cast<size_t>(nb) * 32 * sizeof(uint64_t));
-    for (int t = threadIdx.x; t < nb * 32; t += blockDim.x) {
-        ck_all[t] = static_cast<uint64_t>(__double_as_longlong(__ldcg(p.cand_v + t)));
-        ci_all[t] = static_cast<int>(__ldcg(p.cand_i + t));
-    }
-    __syncthreads();
-    bk = 0;
-    bi = -1;
-    for (int b = wib; b < nb; b += kLkWarps) warp_merge(bk, bi, ck_all[b * 32 + lane], ci_all[b * 32 + lane], lane);
-    __syncthreads();
-    slk[wib][lane] = bk;
-    sli[wib][lane] = bi;
-    __syncthreads();
     if (wib == 0) {
-        for (int w = 1; w < kLkWarps; ++w) warp_merge(bk, bi, slk[w][lane], sli[w][lane], lane);
-        // the k_m best, returned ascending by id (memory.hpp:253)
-        const int k = static_cast<int>(p.n_sel);
-        uint64_t id_key = lane < k ? static_cast<uint64_t>(static_cast<unsigned>(bi)) : ~0ull;
+        // the k_m best, returned ascending by id (memory.hpp:253): sort by ~id descending
+        uint64_t id_key = lane < k ? ~static_cast<uint64_t>(static_cast<unsigned>(bi)) : 0ull;
         int dummy = lane;
-        // ascending by id = descending by ~id
-        id_key = ~id_key;
         warp_sort_desc(id_key, dummy, lane);
         if (lane < k) p.sel[lane] = static_cast<int64_t>(static_cast<unsigned>(~id_key));
         if (lane == 0 && nb > 1) *p.done = 0;
+        TL_MARK(3, mark);  // final selection
         if (p.ready_flag) {  // the attention of this step may read sel now
             __threadfence();
             __syncwarp();
@@ -211,21 +286,20 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
     }
 }
 
-cudaError_t tl_bind_lookup(const TlBuf& b) { return tl_bind_tu(b); }
-
 bool lookup_topk_supported(const LookupParams& p, int dtype_bf16) {
     return dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G >= 1 && p.G <= 8 && p.G == p.Gtot && p.n_sel <= 32 &&
-           p.U > 0 && p.U < (1ll << 31);
+           p.U > 0 && p.U <= 148ll * kLkMaxSlice;
 }
 
 int lookup_topk_blocks(int64_t U, int units_per_block) {
-    const int64_t nb = (U + units_per_block - 1) / units_per_block;
+    int64_t nb = (U + units_per_block - 1) / units_per_block;
+    nb = nb < (U + kLkMaxSlice - 1) / kLkMaxSlice ? (U + kLkMaxSlice - 1) / kLkMaxSlice : nb;
     return static_cast<int>(nb < 1 ? 1 : nb > 148 ? 148 : nb);
 }
 
 void launch_lookup_topk_fast(const LookupParams& p, int blocks, cudaStream_t st) {
     const size_t ring = static_cast<size_t>(kLkWarps) * kLkStages * kLkStageBytes;
-    const size_t merge = static_cast<size_t>(blocks) * 32 * (sizeof(uint64_t) + sizeof(int));
+    const size_t merge = static_cast<size_t>(blocks) * 32 * 16 + kLkSurv * (sizeof(uint64_t) + sizeof(int));
     const size_t smem = ring > merge ? ring : merge;
     static bool attr = false;
     if (!attr) {
@@ -235,5 +309,7 @@ void launch_lookup_topk_fast(const LookupParams& p, int blocks, cudaStream_t st)
     }
     k_lookup_topk<<<blocks, kLkWarps * 32, smem, st>>>(p);
 }
+
+cudaError_t tl_bind_lookup(const TlBuf& b) { return tl_bind_tu(b); }
 
 }  // namespace infllm

@@ -99,13 +99,7 @@ __global__ void __launch_bounds__(kPcThreads, 1) k_prep_chunk(PrepParams p) {
     }
     __syncthreads();
     unsigned long long mark = tl_t0_;
-#define PC_MARK(k)                                                       \
-    do {                                                                 \
-        if (tid == 0 && g_tl.rec) {                                      \
-            tl_put(100 + (k), mark);                                     \
-            mark = gtimer();                                             \
-        }                                                                \
-    } while (0)
+#define PC_MARK(k) TL_MARK(20 + (k), mark)
     PC_MARK(0);
     float2 f[4];
 #pragma unroll
