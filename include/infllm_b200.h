@@ -133,6 +133,26 @@ typedef int (*infllm_allgather_fn)(void* user, double* buf, int64_t rows, int32_
                                    int32_t g_count, int32_t g_total, void* stream);
 int infllm_engine_set_allgather(infllm_engine_t eng, infllm_allgather_fn fn, void* user);
 
+/* KV-group sharding over NCCL: the same exchange as the hook
+ * above, done by the library itself with ncclAllGather on the engine's streams
+ * (graph-capturable, so sharded streams stay CUDA-graph replayed). Rank 0
+ * makes an id with infllm_nccl_unique_id and the host broadcasts its 128
+ * bytes; every rank then calls infllm_engine_set_comm with its engine, which
+ * must own KV groups [rank G/n, (rank + 1) G/n). NCCL is loaded at run time
+ * (libnccl.so.2); INFLLM_ERR_NCCL when it is missing. Option "gather_output"
+ * = 1 makes the step's `out` the full [l_x][n_heads][value_dim] tensor,
+ * all-gathered over the shards after the attention (C-2). */
+int infllm_nccl_unique_id(uint8_t* id128);
+int infllm_engine_set_comm(infllm_engine_t eng, const uint8_t* id128, int32_t rank, int32_t nranks);
+
+/* The exchange arithmetic on the host (no GPU): gathered [nranks][rows]
+ * [g_count] fp64 per-group partials as an all-gather delivers them -> out
+ * [rows], each row summed over all groups in group order (exactly the
+ * association the device uses after the exchange); and the lookup's top-k
+ * (memory.hpp:240-253: rel desc, id asc, returned ascending). */
+int infllm_exchange_fold_host(const double* gathered, int64_t rows, int32_t nranks, int32_t g_count, double* out);
+int infllm_topk_host(const double* rel, int64_t n, int64_t k, int64_t* ids, int64_t* n_out);
+
 /* Pre-size the unit pool and trace for a stream of max_tokens tokens (the
  * reference grows its std::vectors on demand; the engine grows its device
  * pools too, this only moves the growth out of the timed region). */

@@ -110,6 +110,10 @@ SIGNATURES = {
     "infllm_engine_destroy": (C.c_int, [P]),
     "infllm_engine_set_allgather": (C.c_int, [P, ALLGATHER_FN, P]),
     "infllm_engine_reserve": (C.c_int, [P, i64]),
+    "infllm_nccl_unique_id": (C.c_int, [P]),
+    "infllm_engine_set_comm": (C.c_int, [P, P, i32, i32]),
+    "infllm_exchange_fold_host": (C.c_int, [f64p, i64, i32, i32, f64p]),
+    "infllm_topk_host": (C.c_int, [f64p, i64, i64, i64p, i64p]),
     "infllm_engine_reset": (C.c_int, [P, P]),
     "infllm_engine_set_option": (C.c_int, [P, C.c_char_p, i64]),
     "infllm_encode_chunk": (C.c_int, [P, i32, P, P, P, i64, P, P]),

@@ -210,6 +210,7 @@ struct Tile {
 // straddle the l_L distance threshold for this CTA's 128 rows appear twice.
 struct TileSched {
     int n_init, n_units, n_near, n_mixed, r_mixed, T;
+    int j0;  // split-KV: this CTA's tiles are [j0, j0 + T) of the window's T_all
     int64_t near0, near_end, qp_lo, qp_hi;
     const int32_t* sel;  // retrieved unit ids and lengths, staged in shared memory
     const int32_t* len;
@@ -243,9 +244,14 @@ struct TileSched {
                 ++n_mixed;
             }
         }
-        T = n_init + n_units + n_near + n_mixed;
+        const int T_all = n_init + n_units + n_near + n_mixed;
+        // split-KV (AttnParams::n_split > 1): a contiguous share of the tile list
+        const int ns = a.n_split > 1 ? a.n_split : 1, sp = a.n_split > 1 ? static_cast<int>(blockIdx.z) : 0;
+        j0 = static_cast<int>(static_cast<int64_t>(T_all) * sp / ns);
+        T = static_cast<int>(static_cast<int64_t>(T_all) * (sp + 1) / ns) - j0;
     }
-    __device__ Tile get(const AttnParams& a, int j) const {
+    __device__ Tile get(const AttnParams& a, int jl) const {
+        const int j = jl + j0;
         Tile t;
         t.slot = -1;
         if (j < n_init) {
@@ -415,7 +421,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         atomicMax(reinterpret_cast<unsigned long long*>(g_attn_ts) + 1, cta_t0);
     }
     const AttnParams& a = P.a;
-    const bool mass_in_kernel = a.want_mass && a.n_sel <= kMassSlots;
+    const bool split = a.n_split > 1;
+    const bool mass_in_kernel = a.want_mass && a.n_sel <= kMassSlots && !split;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int m = blockIdx.x, h = blockIdx.y, g = h / a.rep;
     TileSched ts;
@@ -800,13 +807,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
         const float a0 = l0 > 0.f ? ex2(m0 - mf) : 0.f;
         const float a1 = l1 > 0.f ? ex2(m1 - mf) : 0.f;
         const float lf = fast ? l0 + l1 : l0 * a0 + l1 * a1;
-        const float inv = 1.f / lf;
-        if (a.inv_violations && row_ok && wg == 0 && !(lf > 0.f && isfinite(lf) && isfinite(inv)))
+        const float inv = split ? 1.f : 1.f / lf;  // split-KV: unnormalised partials, merged by k_attn_merge
+        if (a.inv_violations && row_ok && wg == 0 && !split && !(lf > 0.f && isfinite(lf) && isfinite(inv)))
             atomicAdd(a.inv_violations, 1ull);  // check_softmax (engine.hpp:361-371)
+        if (split && row_ok && wg == 0) {
+            float* ml = a.split_ml + ((static_cast<int64_t>(blockIdx.z) * a.H + h) * a.lxp + i) * 2;
+            ml[0] = mf;
+            ml[1] = lf;
+        }
         // fast path: one O holding both warpgroups' sums, both at the same fixed offset
         const float w0 = fast ? inv : a0 * inv, w1 = fast ? 0.f : a1 * inv;
         // warpgroup wg writes value dims [64 wg, 64 wg + 64)
         bf16* out = static_cast<bf16*>(a.out) + (i * a.H + h) * a.dv + 64 * wg;
+        float* pout = split ? a.split_o + ((static_cast<int64_t>(blockIdx.z) * a.H + h) * a.lxp + i) * 128 + 64 * wg
+                            : nullptr;
 #pragma unroll
         for (int c4 = 0; c4 < 2; ++c4) {
             const int col = 64 * wg + 32 * c4;
@@ -815,7 +829,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
             if (!fast) tmem_ld32(tl + col_o(1) + col, r1);  // fast path: col_o(1) holds P, one shared O
             tmem_wait_ld_r(r0);
             if (!fast) tmem_wait_ld_r(r1);
-            if (row_ok) {
+            if (row_ok && split) {
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 4) {
+                    float4 o4;
+                    o4.x = w0 != 0.f ? __uint_as_float(r0[jj]) * w0 : 0.f;
+                    o4.y = w0 != 0.f ? __uint_as_float(r0[jj + 1]) * w0 : 0.f;
+                    o4.z = w0 != 0.f ? __uint_as_float(r0[jj + 2]) * w0 : 0.f;
+                    o4.w = w0 != 0.f ? __uint_as_float(r0[jj + 3]) * w0 : 0.f;
+                    if (w1 != 0.f) {
+                        o4.x += __uint_as_float(r1[jj]) * w1;
+                        o4.y += __uint_as_float(r1[jj + 1]) * w1;
+                        o4.z += __uint_as_float(r1[jj + 2]) * w1;
+                        o4.w += __uint_as_float(r1[jj + 3]) * w1;
+                    }
+                    *reinterpret_cast<float4*>(pout + 32 * c4 + jj) = o4;
+                }
+            } else if (row_ok) {
                 uint32_t wv[16];
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
@@ -868,7 +898,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 const double* r4 = sRed + tid * 4;
                 a.mass_cta[(static_cast<int64_t>(h) * gridDim.x + m) * a.n_sel + tid] = ((r4[0] + r4[1]) + r4[2]) + r4[3];
             }
-        } else if (row_ok && a.want_mass && wg == 0) {
+        } else if (row_ok && a.want_mass && wg == 0 && !split) {
             a.row_m[static_cast<int64_t>(h) * a.lx + i] = mf * 0.6931471805599453f;
             a.row_l[static_cast<int64_t>(h) * a.lx + i] = lf;
         }
@@ -898,6 +928,39 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
 }
 
 bool attn_tc_masses_in_kernel(int n_sel) { return n_sel <= kMassSlots; }
+
+// split-KV merge: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M), splits in
+// order (deterministic); the row's (M ln 2, L) feed the unit-mass reduction
+// (k_mass). Fast-path splits share the fixed offset, so the weights are 1.
+__global__ void __launch_bounds__(128) k_attn_merge(AttnParams a) {
+    const int64_t i = blockIdx.x;
+    const int h = blockIdx.y, c = threadIdx.x;
+    const int S = a.n_split;
+    const float* ml = a.split_ml + (static_cast<int64_t>(h) * a.lxp + i) * 2;
+    const int64_t sstride = static_cast<int64_t>(a.H) * a.lxp;
+    float M = -INFINITY;
+    for (int sp = 0; sp < S; ++sp) {
+        const float l = ml[sp * sstride * 2 + 1];
+        if (l > 0.f) M = fmaxf(M, ml[sp * sstride * 2]);
+    }
+    float L = 0.f, o = 0.f;
+    for (int sp = 0; sp < S; ++sp) {
+        const float l = ml[sp * sstride * 2 + 1];
+        if (!(l > 0.f)) continue;
+        const float w = ex2(ml[sp * sstride * 2] - M);
+        L = fmaf(l, w, L);
+        o = fmaf(a.split_o[((sp * sstride) + static_cast<int64_t>(h) * a.lxp + i) * 128 + c], w, o);
+    }
+    const float inv = 1.f / L;
+    static_cast<bf16*>(a.out)[(i * a.H + h) * a.dv + c] = __float2bfloat16_rn(o * inv);
+    if (c == 0) {
+        if (a.inv_violations && !(L > 0.f && isfinite(L) && isfinite(inv))) atomicAdd(a.inv_violations, 1ull);
+        if (a.want_mass) {
+            a.row_m[static_cast<int64_t>(h) * a.lx + i] = M * 0.6931471805599453f;
+            a.row_l[static_cast<int64_t>(h) * a.lx + i] = L;
+        }
+    }
+}
 
 bool attn_tc_supported(int d, int dv, int unit_size, bool absolute) {
     return d == 128 && dv == 128 && unit_size == 128 && !absolute;
@@ -969,7 +1032,7 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
         cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    dim3 grid(static_cast<unsigned>((a.lx + 127) / 128), a.H);
+    dim3 grid(static_cast<unsigned>((a.lx + 127) / 128), a.H, a.n_split > 1 ? a.n_split : 1);
     // highest launch priority: the side-stream kernels of the next step must
     // not hold SMs the attention CTAs (one per SM) are waiting for
     static int prio_hi = 1;
@@ -995,6 +1058,10 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     cfg.attrs = la;
     cfg.numAttrs = a.pdl ? 3 : 2;
     cudaLaunchKernelEx(&cfg, k_attn_tc, P);
+    if (a.n_split > 1) {
+        k_attn_merge<<<dim3(static_cast<unsigned>(a.lx), a.H), 128, 0, st>>>(a);
+        return 2;
+    }
     return 1;
 }
 

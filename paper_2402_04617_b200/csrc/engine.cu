@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only: the library is resolved at run time (dlopen)
 #include <nvtx3/nvToolsExt.h>
 
 #include "../../include/infllm_b200.h"
@@ -189,6 +191,59 @@ __global__ void k_probe_f32(float* out, int n) {
     if (s == 12345.0f) out[0] = s;
 }
 
+// NCCL, resolved at run time: the library loads (and runs single-GPU) without it;
+// a process that already loaded one (torch) shares that copy (RTLD_NOLOAD first)
+struct Nccl {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const Nccl& nccl() {
+    static Nccl n = [] {
+        Nccl x;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return x;
+        x.get_unique_id = reinterpret_cast<decltype(x.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        x.comm_init_rank = reinterpret_cast<decltype(x.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        x.all_gather = reinterpret_cast<decltype(x.all_gather)>(dlsym(h, "ncclAllGather"));
+        x.comm_destroy = reinterpret_cast<decltype(x.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        x.error_string = reinterpret_cast<decltype(x.error_string)>(dlsym(h, "ncclGetErrorString"));
+        return x;
+    }();
+    if (!n.get_unique_id || !n.comm_init_rank || !n.all_gather) throw ExchangeError("NCCL (libnccl.so.2) not available");
+    return n;
+}
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw ExchangeError(std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "NCCL error"));
+}
+
+// exchange layout: the fp64 partials of the engine are [rows][g_total] with this
+// shard's columns [g0, g0 + G); NCCL all-gathers contiguous [rows][G] blocks per
+// rank, rank r owning groups [r G, (r + 1) G)
+__global__ void k_pack_cols(const double* buf, int64_t rows, int gt, int g0, int g, double* send) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < rows * g) send[t] = buf[(t / g) * gt + g0 + t % g];
+}
+__global__ void k_unpack_cols(const double* recv, int64_t rows, int gt, int g, double* buf) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // over [rank][row][col]
+    if (t >= rows * gt) return;
+    const int64_t r = t / (rows * g), rem = t % (rows * g);
+    buf[(rem / g) * gt + r * g + rem % g] = recv[t];
+}
+// output all-gather: [rank][lx][Hs][dv] -> [lx][H][dv]
+__global__ void k_interleave_heads(const uint8_t* recv, int64_t lx, int hs, int nr, int64_t row_bytes, uint8_t* out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // 16-byte pieces
+    const int64_t per = row_bytes / 16, n = static_cast<int64_t>(nr) * lx * hs * per;
+    if (t >= n) return;
+    const int64_t piece = t % per, hh = (t / per) % hs, i = (t / (per * hs)) % lx, r = t / (per * hs * lx);
+    reinterpret_cast<uint4*>(out)[((i * nr + r) * hs + hh) * per + piece] = reinterpret_cast<const uint4*>(recv)[t];
+}
+
 __global__ void k_fill_i32(int32_t* x, int64_t n, int32_t v) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) x[i] = v;
@@ -266,6 +321,7 @@ struct infllm_engine {
     bool score_bound = true;  // tcgen05 attention: fixed-offset softmax when the bound allows
     bool use_dec = false;     // K4 split-KV decode attention for l_x = 1 steps
     bool dec_disabled = false;
+    int attn_splits = 0;      // option attn_splits: split-KV K3 (0: auto, when the grid leaves SMs idle)
     int lookup_upb = 48;      // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
     int lookup_upb_decode = 8;  // option lookup_units_per_block_decode: the same for one-token steps (whole GPU)
     bool attn_flag = false;   // option attn_flag: K3 waits on a step-ready flag instead of graph edges
@@ -319,6 +375,7 @@ struct infllm_engine {
 
     // scratch shared by layers (layers run sequentially on one stream)
     DBuf prep_sync;  // k_prep_chunk look-back state
+    DBuf split_o, split_ml;  // split-KV K3 partials
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, tsum, topk_done, evict_done;
     DBuf dec_part, dec_mass, dec_cnt;  // K4 decode scratch (one sequence)
 
@@ -465,7 +522,7 @@ struct infllm_engine {
 
     // every device buffer the engine owns (a captured step graph holds their addresses)
     std::vector<DBuf*> dev_buffers() {
-        std::vector<DBuf*> v{&inv_dev, &prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
+        std::vector<DBuf*> v{&ex_send, &ex_recv, &out_stage, &out_recv, &split_o, &split_ml, &inv_dev, &prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
                              &tsum, &topk_done, &evict_done, &dec_part, &dec_mass, &dec_cnt};
         for (int b = 0; b < kNB; ++b)
             for (auto* x : {&stage_q[b], &stage_k[b], &stage_v[b], &stage_o[b]}) v.push_back(x);
@@ -539,6 +596,7 @@ struct infllm_engine {
         // multi-block top-k candidates (sized here: no allocation may happen inside a captured step)
         L.cand.grow(static_cast<size_t>(topk_multi_scratch(cap, std::max<int64_t>(cfg.n_lookup, 1))) * 16, st);
         L.unit_cap = cap;
+        ensure_exchange(std::max<int64_t>({cap, cfg.chunk_size, cfg.n_lookup}));
     }
 
     void ensure_trace(Layer& L, int64_t need, cudaStream_t st) {
@@ -594,10 +652,37 @@ struct infllm_engine {
         pipe_dirty = false;
     }
 
+    // cross-shard exchange C-1: the other shards' columns of a
+    // [rows][Gt] fp64 partial buffer, in stream order on `st`
     void gather(double* buf, int64_t rows, cudaStream_t st) {
-        if (!allgather || Gs == Gt) return;
+        if (Gs == Gt || rows <= 0) return;
+        if (comm) {
+            if (coll) throw StreamError("decode_batch: sharded engines are not batched");
+            const unsigned nb = static_cast<unsigned>((rows * Gs + 255) / 256);
+            k_pack_cols<<<nb, 256, 0, st>>>(buf, rows, Gt, g0, Gs, ex_send.as<double>());
+            nck(nccl().all_gather(ex_send.p, ex_recv.p, static_cast<size_t>(rows) * Gs, ncclDouble,
+                                  static_cast<ncclComm_t>(comm), st),
+                "ncclAllGather (partials)");
+            k_unpack_cols<<<static_cast<unsigned>((rows * Gt + 255) / 256), 256, 0, st>>>(ex_recv.as<double>(), rows,
+                                                                                         Gt, Gs, buf);
+            launches += 2;
+            return;
+        }
+        if (!allgather) return;
         if (allgather(allgather_user, buf, rows, g0, Gs, Gt, st) != 0)
             throw ExchangeError("allgather hook failed");
+    }
+    // NCCL communicator over the KV-group shards (infllm_engine_set_comm)
+    void* comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
+    bool gather_output = false;  // option gather_output: C-2 all-gather of the outputs to all heads
+    DBuf ex_send, ex_recv, out_stage, out_recv;
+    void ensure_exchange(int64_t rows) {
+        if (!comm) return;
+        const size_t need = static_cast<size_t>(std::max<int64_t>(rows, 1)) * Gt * sizeof(double);
+        if (ex_recv.bytes >= need) return;
+        ex_send.alloc(need / comm_size + 256, nullptr, false);
+        ex_recv.alloc(need, nullptr, false);
     }
 
     // Units are whole 128-token ring pages (they start at l_I + 128 u and every
@@ -620,6 +705,33 @@ struct infllm_engine {
         sp.unit_v = upage_v(L);
         sp.vl = vl;
     }
+
+    // split-KV for the tcgen05 attention: a KV-group shard (or a short chunk)
+    // leaves most SMs idle with one CTA per (128 rows, head); splitting each
+    // CTA's tile list over grid.z fills them (>= 4 tiles per split)
+    int pick_splits_tc(int64_t lx, const AttnParams& ap) {
+        const int64_t ctas = ((lx + 127) / 128) * static_cast<int64_t>(Hs);
+        const int64_t tiles = (ap.init_len + 127) / 128 + ap.n_sel + (ap.s + lx - ap.local_start + 127) / 128 + 2;
+        int64_t S = attn_splits > 0 ? attn_splits : 148 / std::max<int64_t>(ctas, 1);
+        S = std::clamp<int64_t>(std::min<int64_t>(S, tiles / 4), 1, kMaxSplitsTc);
+        if (S > 1) ensure_split_scratch(S);
+        return static_cast<int>(S);
+    }
+    void ensure_split_scratch(int64_t S) {
+        const size_t need_o = static_cast<size_t>(S) * Hs * lxp * 128 * sizeof(float);
+        const size_t need_ml = static_cast<size_t>(S) * Hs * lxp * 2 * sizeof(float);
+        if (split_o.bytes >= need_o && split_ml.bytes >= need_ml) return;
+        if (capturing) throw StreamError("split-KV scratch must be sized before capture");
+        ck(cudaDeviceSynchronize(), "split scratch");
+        split_o.alloc(need_o, nullptr, false);
+        split_ml.alloc(need_ml, nullptr, false);
+    }
+    // the most splits any step of this engine can take (a 1-tile-row chunk)
+    int64_t max_splits_tc() const {
+        const int64_t s = attn_splits > 0 ? attn_splits : 148 / std::max(Hs, 1);
+        return std::clamp<int64_t>(s, 1, kMaxSplitsTc);
+    }
+    static constexpr int kMaxSplitsTc = 16;
 
     bool tc_eligible(int64_t lx) const {
         (void)lx;
@@ -1001,7 +1113,10 @@ struct infllm_engine {
         AttnParams ap{};
         ap.qa = qa_b;
         ap.qc = qc_b;
-        ap.out = out;
+        // C-2: with gather_output the caller's `out` holds all heads; this shard's
+        // heads go to a staging buffer and are all-gathered after the attention
+        const bool gout = comm && gather_output && Gs != Gt && !coll;
+        ap.out = gout ? out_stage.p : out;
         ap.init_k = L.init_k.p;
         ap.init_krot = L.init_krot.p;
         ap.init_v = L.init_v.p;
@@ -1077,6 +1192,11 @@ struct infllm_engine {
                 ++launches;
             } else if (tc_eligible(lx)) {
                 ap.pdl = !fork && !one_stream ? attn_pdl : 0;
+                ap.n_split = pick_splits_tc(lx, ap);
+                if (ap.n_split > 1) {
+                    ap.split_o = split_o.as<float>();
+                    ap.split_ml = split_ml.as<float>();
+                }
                 ap.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
                 ap.ready_val = L.step;
                 launches += launch_attn_tc(ap, st);
@@ -1089,6 +1209,16 @@ struct infllm_engine {
             ++launches;
         }
         phase_end(kPhAttend, eva, st);
+        if (gout) {
+            const int64_t row = static_cast<int64_t>(dv) * static_cast<int64_t>(esz);
+            nck(nccl().all_gather(out_stage.p, out_recv.p, static_cast<size_t>(lx * Hs * row), ncclUint8,
+                                  static_cast<ncclComm_t>(comm), st),
+                "ncclAllGather (outputs)");
+            const int64_t pieces = comm_size * lx * Hs * (row / 16);
+            k_interleave_heads<<<static_cast<unsigned>((pieces + 255) / 256), 256, 0, st>>>(
+                out_recv.as<uint8_t>(), lx, Hs, comm_size, row, static_cast<uint8_t*>(out));
+            ++launches;
+        }
         if (want_mass) inv_checks += static_cast<uint64_t>(Hs) * lx;  // check_softmax rows (engine.hpp:266)
 
         // attention masses -> lookup bookkeeping, frequency update, capacity
@@ -1098,7 +1228,7 @@ struct infllm_engine {
         if (want_mass) {
             if (dec_ran) {
                 gather(mass_part_b, n_sel, st);  // per-group masses written by the decode kernel
-            } else if (tc_ran && attn_tc_masses_in_kernel(static_cast<int>(n_sel))) {
+            } else if (tc_ran && attn_tc_masses_in_kernel(static_cast<int>(n_sel)) && ap.n_split <= 1) {
                 if (Gs == Gt) {
                     mass_src = 1;
                 } else {
@@ -1282,6 +1412,7 @@ struct infllm_engine {
         }
         // capacity for the whole stream up front (no pool growth inside a graph)
         const int64_t steps = (n + cfg.chunk_size - 1) / cfg.chunk_size;
+        if (use_tc && max_splits_tc() > 1) ensure_split_scratch(max_splits_tc());
         ensure_units(L, L.n_units + (L.pend_count + n) / cfg.unit_size + 2, st);
         ensure_trace(L, L.trace_count + steps * std::max<int64_t>(cfg.n_lookup, 1), st);
         if (host && !stage_q[0].p) {
@@ -1592,6 +1723,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
             }
         for (auto ev : e->ev_pool) cudaEventDestroy(ev);
         for (auto& g : e->graphs) infllm_engine::drop_graph(g);
+        if (e->comm) nccl().comm_destroy(static_cast<ncclComm_t>(e->comm));
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
                         e->evict_stream, e->tier_stream})
             if (s2) cudaStreamDestroy(s2);
@@ -1619,6 +1751,70 @@ int infllm_engine_set_allgather(infllm_engine_t e, infllm_allgather_fn fn, void*
     e->allgather = fn;
     e->allgather_user = user;
     return INFLLM_OK;
+}
+
+int infllm_nccl_unique_id(uint8_t* id128) {
+    return guard([&] {
+        if (!id128) throw ConfigError("null argument");
+        ncclUniqueId id;
+        nck(nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(id128, id.internal, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+int infllm_engine_set_comm(infllm_engine_t e, const uint8_t* id128, int32_t rank, int32_t nranks) {
+    return guard([&] {
+        if (!e || !id128) throw ConfigError("null argument");
+        if (e->comm) throw ConfigError("set_comm: the engine already has a communicator");
+        if (nranks < 1 || rank < 0 || rank >= nranks) throw ConfigError("set_comm: bad rank / nranks");
+        if (e->Gt % nranks || e->Gs * nranks != e->Gt || e->g0 != rank * e->Gs)
+            throw ConfigError("set_comm: rank r must own KV groups [r G/n, (r + 1) G/n)");
+        ncclUniqueId id;
+        std::memcpy(id.internal, id128, NCCL_UNIQUE_ID_BYTES);
+        ck(cudaSetDevice(e->device), "cudaSetDevice");
+        ncclComm_t c = nullptr;
+        nck(nccl().comm_init_rank(&c, nranks, id, rank), "ncclCommInitRank");
+        e->comm = c;
+        e->comm_rank = rank;
+        e->comm_size = nranks;
+        int64_t cap = 0;
+        for (auto& L : e->layers) cap = std::max(cap, L.unit_cap);
+        e->ensure_exchange(std::max<int64_t>({cap, e->cfg.chunk_size, e->cfg.n_lookup}));
+        const size_t ob = static_cast<size_t>(e->cfg.chunk_size) * e->Hs * e->dv * e->esz;
+        e->out_stage.alloc(ob, nullptr, false);
+        e->out_recv.alloc(ob * nranks, nullptr, false);
+        ck(cudaDeviceSynchronize(), "set_comm");
+    });
+}
+
+int infllm_exchange_fold_host(const double* gathered, int64_t rows, int32_t nranks, int32_t g_count, double* out) {
+    return guard([&] {
+        if (rows < 0 || nranks < 1 || g_count < 1 || (rows > 0 && (!gathered || !out)))
+            throw ConfigError("exchange_fold: bad arguments");
+        for (int64_t u = 0; u < rows; ++u) {  // group order 0..g_total-1, as k_topk / k_finalize sum them
+            double a = 0.0;
+            for (int32_t r = 0; r < nranks; ++r)
+                for (int32_t g = 0; g < g_count; ++g) a += gathered[(static_cast<int64_t>(r) * rows + u) * g_count + g];
+            out[u] = a;
+        }
+    });
+}
+
+int infllm_topk_host(const double* rel, int64_t n, int64_t k, int64_t* ids, int64_t* n_out) {
+    return guard([&] {
+        if (n < 0 || k < 0 || (n > 0 && (!rel || !ids)) || !n_out) throw ConfigError("topk: bad arguments");
+        const int64_t take = std::min(k, n);  // memory.hpp:240-253
+        std::vector<int64_t> idx(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) idx[static_cast<size_t>(i)] = i;
+        auto better = [&](int64_t a, int64_t b) {
+            const double ra = rel[a] == 0.0 ? 0.0 : rel[a], rb = rel[b] == 0.0 ? 0.0 : rel[b];
+            return ra != rb ? ra > rb : a < b;
+        };
+        std::partial_sort(idx.begin(), idx.begin() + take, idx.end(), better);
+        std::sort(idx.begin(), idx.begin() + take);
+        for (int64_t i = 0; i < take; ++i) ids[i] = idx[static_cast<size_t>(i)];
+        *n_out = take;
+    });
 }
 
 int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
@@ -1674,7 +1870,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // captured stream graphs bake in the launch choices these options make:
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
-            k == "attn_pdl" || k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
+            k == "attn_pdl" || k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
+            k == "gather_output" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1697,6 +1894,10 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->prep_blocks = static_cast<int>(std::clamp<int64_t>(value, 0, 1 << 20));
         else if (k == "attn_flag")
             e->attn_flag = value != 0;
+        else if (k == "gather_output")
+            e->gather_output = value != 0;
+        else if (k == "attn_splits")
+            e->attn_splits = static_cast<int>(std::clamp<int64_t>(value, 0, infllm_engine::kMaxSplitsTc));
         else if (k == "lookup_units_per_block_decode")
             e->lookup_upb_decode = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
         else if (k == "lookup_units_per_block")

@@ -127,6 +127,12 @@ struct AttnParams {
     // check_softmax (engine.hpp:361-371) on the device: rows whose softmax
     // denominator is not a positive finite number add one here (or null)
     unsigned long long* inv_violations;
+    // split-KV K3 (n_split > 1): grid.z = split, each CTA a contiguous share of the
+    // window's tiles; partials O [split][H][lxp][128] and (m, l) [split][H][lxp][2]
+    // (fp32, exp2 domain), merged by k_attn_merge; masses then go through k_mass
+    int n_split;
+    float* split_o;
+    float* split_ml;
     float scale;
     VLayout vl;
 };

@@ -69,6 +69,12 @@ class StreamEngine:
     def set_option(self, key: str, value: int):
         check(lib().infllm_engine_set_option(self.h, key.encode(), int(value)))
 
+    def set_comm(self, rank: int, world: int, group=None):
+        """KV-group sharding over the library's NCCL communicator (see shard.attach_nccl)."""
+        from .shard import attach_nccl
+
+        attach_nccl(self, rank, world, group)
+
     def set_allgather(self, fn):
         """fn(buf_ptr, rows, g0, g_count, g_total, stream_ptr) -> 0; see infllm_allgather_fn."""
         if fn is None:

@@ -10,13 +10,16 @@ buffer (its own columns) and calls the exchange hook; after the hook every
 shard holds every column and sums groups 0..g_total-1 in fixed order, so the
 selected ids are bit-identical for any shard count (C-1 in SURVEY §8e).
 
-Two hooks:
-  * ``DistExchange`` — one process per GPU, ``torch.distributed`` all-gather
-    (NCCL on GPUs; gloo works for the host-side logic tests);
+Two transports:
+  * ``attach_nccl`` — one process per GPU: the library's own NCCL
+    communicator (ncclAllGather on the engine's streams, graph-capturable);
   * ``ThreadExchange`` — several shards driven by host threads in ONE process
-    (a host-synchronised exchange: each shard syncs its stream, publishes its
-    columns, waits for the others). Used to test sharding on a single GPU
-    without kernels that wait on each other.
+    through the infllm_allgather_fn hook (a host-synchronised exchange: each
+    shard syncs its stream, publishes its columns, waits for the others).
+    Used to test sharding on a single GPU without kernels that wait on each
+    other.
+``fold_host`` / ``topk_host`` run the library's exchange arithmetic on the
+host (the multi-process CPU tests drive it over gloo).
 """
 from __future__ import annotations
 
@@ -34,24 +37,58 @@ def shard_range(n_kv_heads: int, rank: int, world: int):
     return rank * gc, gc
 
 
-def merge_columns(buf: torch.Tensor, gathered: torch.Tensor, g_count: int) -> None:
-    """gathered [world][rows][g_count] (rank order == group order) -> buf [rows][g_total]."""
-    world, rows, _ = gathered.shape
-    buf.copy_(gathered.permute(1, 0, 2).reshape(rows, world * g_count))
+def attach_nccl(engine, rank: int, world: int, group=None) -> None:
+    """Give `engine` (this rank's KV-group shard) the library's own NCCL
+    communicator (infllm_engine_set_comm): rank 0 makes the 128-byte NCCL id,
+    torch.distributed (any backend) broadcasts it, every rank joins. The
+    engine then all-gathers its fp64 partials with ncclAllGather on its own
+    streams, inside captured stream graphs (C-1), and with option
+    gather_output the outputs of every head (C-2)."""
+    import ctypes as C
 
-
-def exchange(buf: torch.Tensor, g0: int, g_count: int, group=None) -> None:
-    """All-gather the per-group partial columns of buf [rows][g_total] in place."""
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
-    rows, g_total = buf.shape
-    if world * g_count != g_total:
-        raise ValueError("shards must own equal KV-group blocks")
-    local = buf[:, g0:g0 + g_count].contiguous()
-    gathered = torch.empty((world * rows, g_count), dtype=buf.dtype, device=buf.device)
-    dist.all_gather_into_tensor(gathered, local, group=group)
-    merge_columns(buf, gathered.view(world, rows, g_count), g_count)
+    from ._lib import check, lib
+
+    buf = (C.c_uint8 * 128)()
+    if rank == 0:
+        check(lib().infllm_nccl_unique_id(buf))
+    box = [bytes(buf)]
+    dist.broadcast_object_list(box, src=0, group=group)
+    idb = (C.c_uint8 * 128).from_buffer_copy(box[0])
+    check(lib().infllm_engine_set_comm(engine.h, idb, rank, world))
+
+
+def fold_host(gathered: np.ndarray) -> np.ndarray:
+    """The library's exchange arithmetic on the host (infllm_exchange_fold_host):
+    gathered [world][rows][g_count] fp64 partial blocks, as an all-gather
+    delivers them, -> per-row sums over all groups in group order 0..g_total-1
+    (the order k_topk / k_finalize / the LRU use on the device)."""
+    import ctypes as C
+
+    from ._lib import check, lib
+
+    g = np.ascontiguousarray(gathered, np.float64)
+    world, rows, gc = g.shape
+    out = np.zeros(max(rows, 1), np.float64)
+    check(lib().infllm_exchange_fold_host(g.ctypes.data_as(C.POINTER(C.c_double)), rows, world, gc,
+                                          out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out[:rows]
+
+
+def topk_host(rel: np.ndarray, k: int) -> list:
+    """TieredStore::lookup's selection (memory.hpp:240-253) on the host
+    (infllm_topk_host): top k by (rel desc, id asc), returned ascending."""
+    import ctypes as C
+
+    from ._lib import check, lib
+
+    r = np.ascontiguousarray(rel, np.float64)
+    ids = np.zeros(max(1, k), np.int64)
+    n = C.c_int64()
+    check(lib().infllm_topk_host(r.ctypes.data_as(C.POINTER(C.c_double)), len(r), k,
+                                 ids.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(n)))
+    return ids[:n.value].tolist()
 
 
 class _DevArray:
@@ -66,26 +103,6 @@ def device_buffer(ptr: int, rows: int, cols: int, device) -> torch.Tensor:
     return torch.as_tensor(_DevArray(ptr, rows, cols), device=device)
 
 
-class DistExchange:
-    """infllm_allgather_fn backed by torch.distributed (NCCL), issued on the
-    engine's stream so it orders with the producing and consuming kernels."""
-
-    def __init__(self, device, group=None):
-        self.device = torch.device(device)
-        self.group = group
-
-    def __call__(self, buf_ptr, rows, g0, g_count, g_total, stream_ptr) -> int:
-        try:
-            if rows == 0:
-                return 0
-            buf = device_buffer(buf_ptr, rows, g_total, self.device)
-            with torch.cuda.stream(torch.cuda.ExternalStream(stream_ptr, device=self.device)):
-                exchange(buf, g0, g_count, self.group)
-            return 0
-        except Exception:  # the C side turns a non-zero return into INFLLM_ERR_NCCL
-            return 1
-
-
 class ThreadExchange:
     """Host-synchronised exchange among `n_shards` engines in one process,
     each driven by its own host thread."""
@@ -96,6 +113,7 @@ class ThreadExchange:
         self.barrier = threading.Barrier(n_shards)
         self.host = None
         self.calls = 0
+        self.errors = []
 
     def hook(self):
         def fn(buf_ptr, rows, g0, g_count, g_total, stream_ptr):
@@ -112,7 +130,8 @@ class ThreadExchange:
                 torch.cuda.synchronize(self.device)
                 self.barrier.wait()
                 return 0
-            except Exception:
+            except Exception as exc:  # kept for the caller; the C side reports INFLLM_ERR_NCCL
+                self.errors.append(repr(exc))
                 self.barrier.abort()
                 return 1
 

@@ -1,8 +1,10 @@
 """Host-side logic of KV-group sharding on CPU: world_size-2
-torch.distributed (gloo) processes run the same partial exchange the engine's
-allgather hook performs on GPUs (paper_2402_04617_b200/shard.py), then the
-fixed group-order sums and the (rel desc, id asc) top-k are checked against
-the unsharded computation and the oracle.
+torch.distributed (gloo) processes stand in for the NCCL ranks. Each rank
+computes its KV groups' fp64 relevance partials, the all-gather delivers the
+contiguous [rank][rows][groups] blocks NCCL would, and the library's own
+exchange arithmetic (infllm_exchange_fold_host: the column fold in group
+order the device runs after ncclAllGather) and its top-k (infllm_topk_host)
+produce the ids, checked against the unsharded fold and the oracle.
 """
 import os
 import socket
@@ -13,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2402_04617_b200.shard import merge_columns, shard_range
+from paper_2402_04617_b200.shard import fold_host, shard_range, topk_host
 
 
 def _free_port():
@@ -46,21 +48,16 @@ def _worker(rank, world, port, result_q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2402_04617_b200.shard import exchange
-
         G, U, k = 8, 500, 16
         rng = np.random.default_rng(0)  # same inputs on every rank
         q = rng.standard_normal((64, 32, 32)).astype(np.float32)
         reprk = rng.standard_normal((U, G, 4, 32)).astype(np.float32)
         g0, gc = shard_range(G, rank, world)
-        buf = torch.from_numpy(group_partials(q, reprk, range(g0, g0 + gc)))
-        # the engine leaves the other shards' columns uninitialised: poison them
-        mask = torch.ones(G, dtype=torch.bool)
-        mask[g0:g0 + gc] = False
-        buf[:, mask] = float("nan")
-        exchange(buf, g0, gc)
-        rel = buf.numpy().sum(axis=1)  # fixed group order 0..G-1, like k_topk
-        result_q.put((rank, rel.tobytes(), topk_ids(rel, k)))
+        mine = torch.from_numpy(np.ascontiguousarray(group_partials(q, reprk, range(g0, g0 + gc))[:, g0:g0 + gc]))
+        gathered = torch.empty((world * U, gc), dtype=torch.float64)
+        dist.all_gather_into_tensor(gathered, mine)  # [rank][rows][groups], as ncclAllGather delivers it
+        rel = fold_host(gathered.numpy().reshape(world, U, gc))
+        result_q.put((rank, rel.tobytes(), topk_host(rel, k)))
     finally:
         dist.destroy_process_group()
 
@@ -72,11 +69,15 @@ def test_shard_range():
         shard_range(8, 0, 3)
 
 
-def test_merge_columns_order():
-    g = torch.arange(2 * 3 * 4, dtype=torch.float64).reshape(2, 3, 4)  # [world][rows][gc]
-    buf = torch.zeros(3, 8, dtype=torch.float64)
-    merge_columns(buf, g, 4)
-    assert torch.equal(buf[:, :4], g[0]) and torch.equal(buf[:, 4:], g[1])
+def test_fold_host_group_order():
+    """[rank][rows][groups] blocks fold as rank 0's groups, then rank 1's: group order 0..g_total-1."""
+    g = np.arange(2 * 3 * 4, dtype=np.float64).reshape(2, 3, 4) + 0.25
+    want = np.concatenate([g[0], g[1]], axis=1)
+    ref = np.zeros(3)
+    for c in range(8):  # sequential fold in group order, like k_topk
+        ref = ref + want[:, c]
+    assert fold_host(g).tobytes() == ref.tobytes()
+    assert topk_host(np.array([1.0, 3.0, 3.0, -0.0, 0.0, 2.0]), 3) == [1, 2, 5]  # ties -> lower id
 
 
 @pytest.mark.parametrize("world", [2])
@@ -100,9 +101,9 @@ def test_gloo_exchange_matches_unsharded(world):
     rng = np.random.default_rng(0)
     q = rng.standard_normal((64, 32, 32)).astype(np.float32)
     reprk = rng.standard_normal((U, G, 4, 32)).astype(np.float32)
-    full = group_partials(q, reprk, range(G)).sum(axis=1)
+    full = fold_host(group_partials(q, reprk, range(G))[None])  # one shard owning every group
     assert np.frombuffer(res[0][1], np.float64).tobytes() == full.tobytes()
-    assert res[0][2] == topk_ids(full, k)
+    assert res[0][2] == topk_ids(full, k) == topk_host(full, k)
     # and the oracle's head-by-head relevance (memory.hpp:217-234) picks the same units
     from oracle import oracle as O
 
