@@ -9,9 +9,13 @@ hot capacity 32, decay 0.1). One bench "step" = the whole 128K-token stream
 reset engine. Inputs: synthetic N(0,1) q/k/v (seeded), resident in HBM
 (1.5 GB > L2, so no flush is needed between steps).
 
---gpus N (torchrun): N independent streams, one per GPU (weak scaling, no
-collective on the data path; KV-group sharding with the cross-shard score
-exchange is a latency mode).
+--gpus N (torchrun): ONE 128K stream KV-group sharded over the N GPUs
+(BASELINE configs[2]: rank r owns KV groups [r 8/N, (r+1) 8/N) and their
+query heads; the library's NCCL communicator exchanges the fp64 score
+partials every step (C-1) and all-gathers the outputs to every head (C-2);
+strong scaling, value = that stream's tokens/s). The same ranks also time N
+independent unsharded streams (one per GPU, no collective) and report it as
+`replicas` (weak scaling) beside the headline.
 --impl reference: the reference algorithm on the host CPU (the oracle port,
 pinned bit-exact to the reference engine), rank 0 only.
 """
@@ -250,12 +254,27 @@ def run_b200(args, rank, world, local_rank):
     H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
     n, C = args.tokens, CFG["chunk_size"]
     g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
+    g.manual_seed(1234)  # every rank draws the same full stream and keeps its shard
     Q = torch.randn((n, H, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     K = torch.randn((n, Hkv, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     V = torch.randn((n, Hkv, d), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     OUT = torch.empty((n, H, d), device=dev, dtype=torch.bfloat16)
-    eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16, device=local_rank)
+    sharded = world > 1
+    if sharded:
+        from paper_2402_04617_b200.shard import shard_range
+
+        g0, gc = shard_range(Hkv, rank, world)
+        rep_h = H // Hkv
+        QF, KF, VF = Q, K, V
+        Q = QF[:, g0 * rep_h:(g0 + gc) * rep_h].contiguous()
+        K, V = KF[:, g0:g0 + gc].contiguous(), VF[:, g0:g0 + gc].contiguous()
+        eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16,
+                           device=local_rank, kv_group_begin=g0, kv_group_count=gc)
+        eng.set_comm(rank, world)
+        eng.set_option("gather_output", 1)  # OUT holds every head on every rank (C-2)
+    else:
+        eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16,
+                           device=local_rank)
     if args.no_tc:
         eng.set_option("tc_attention", 0)
     eng.reserve(n)
@@ -302,7 +321,33 @@ def run_b200(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = world * n * args.steps / (ms / 1000.0)
+    value = n * args.steps / (ms / 1000.0)  # one stream (sharded over the ranks when world > 1)
+    replicas = None
+    if sharded:  # N independent unsharded streams, one per GPU (weak scaling, no collective)
+        eng.set_option("gather_output", 0)
+        rep_eng = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16,
+                               device=local_rank)
+        rep_eng.reserve(n)
+
+        def rep_stream():
+            rep_eng.reset()
+            rep_eng.encode_stream(QF, KF, VF, out=OUT)
+
+        for _ in range(args.warmup):
+            rep_stream()
+        barrier()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.steps):
+            rep_stream()
+        r1.record(stream)
+        barrier()
+        rms = torch.tensor([r0.elapsed_time(r1)], device=dev)
+        dist.all_reduce(rms, op=dist.ReduceOp.MAX)
+        replicas = {"value": world * n * args.steps / (float(rms.item()) / 1000.0), "unit": "tokens/s",
+                    "scaling": "weak", "ms_per_step": float(rms.item()) / args.steps,
+                    "what": f"{world} independent unsharded 128K streams, one per GPU, no collective"}
+        rep_eng.close()
 
     # end-to-end through the C-ABI with HOST buffers: per chunk H2D of q/k/v
     # from pinned memory and D2H of the attention output, pipelined on copy
@@ -312,7 +357,7 @@ def run_b200(args, rank, world, local_rank):
         e2e = run_e2e(eng, Q, K, V, n, C, dev, args, world)
 
     steps = stream_schedule(n, CFG)
-    flops = attention_flops(steps, H, d)
+    flops = attention_flops(steps, H, d) * (Q.shape[1] / H)  # this rank's query heads
     peaks = load_peaks()
     attn_ms = prof["attn_ms"] / max(1, args.steps)
     achieved = flops / (attn_ms / 1000.0) / 1e12
@@ -326,8 +371,8 @@ def run_b200(args, rank, world, local_rank):
             traffic = None
     lk_bytes = lookup_bytes(steps, CFG, Hkv, d, H)
     lk_ms = prof["lookup_ms"] / max(1, args.steps)
-    iso = isolated_kernels(eng, steps, H, Hkv, d, dev) if rank == 0 else {}
-    extra = other_configs(Q, K, V, dev) if (rank == 0 and not args.no_extra) else {}
+    iso = isolated_kernels(eng, steps, H, Hkv, d, dev) if (rank == 0 and not sharded) else {}
+    extra = other_configs(Q, K, V, dev) if (rank == 0 and not args.no_extra and not sharded) else {}
 
     if rank == 0:
         cpu = cpu_all = cpu_c0 = None
@@ -350,13 +395,15 @@ def run_b200(args, rank, world, local_rank):
                 cpu_c0 = {"available": False, "why": str(ex)}
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "C2: Llama-3-8B heads (32q/8kv, d128), 131072-token chunked prefill of one "
                                    "InfLLM layer per GPU (chunk 512, unit 128, r_k 4, k_m 16, init 128, local 4096, "
                                    "hot 32); step = whole stream",
                        "tokens_per_step_per_gpu": n, "l2": "inputs 1.5 GB > L2 (no flush needed)",
-                       "parallelism": f"{world} independent streams" if world > 1 else "1 stream"},
+                       "parallelism": (f"kv-group sharded over {world} GPUs (NCCL: per-step fp64 score partials "
+                                       f"C-1, output all-gather C-2)") if sharded else "1 stream"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16"], "unit": "TFLOP/s",
                          "frac": achieved / peaks["bf16"], "traffic": traffic,
                          "kernel": "attention (K3)", "flops_per_stream": flops,
@@ -375,6 +422,7 @@ def run_b200(args, rank, world, local_rank):
             "cpu_baseline_all_cores": cpu_all,
             "cpu_reference_c0": cpu_c0,
             "e2e": e2e,
+            "replicas": replicas,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "other_configs": extra,
@@ -603,17 +651,31 @@ def run_e2e(eng, Q, K, V, n, C, dev, args, world):
         eng.reset()
         eng.encode_stream_host(Hq, Hk, Hv, Hout)
 
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
     for _ in range(max(1, args.warmup)):
         stream_once()
-    torch.cuda.synchronize(dev)
+    barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         stream_once()
-    torch.cuda.synchronize(dev)
+    barrier()
     dt = time.perf_counter() - t0
+    if world > 1:  # the slowest rank
+        import torch.distributed as dist
+
+        t = torch.tensor([dt], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
     h2d_b = (Q.numel() + K.numel() + V.numel()) * Q.element_size()
     d2h_b = Q.numel() * Q.element_size()
-    return {"value": world * n * args.steps / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b,
+    # one stream (each rank holds its KV-group shard's q/k/v and outputs when world > 1)
+    return {"value": n * args.steps / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b,
             "note": "infllm_encode_stream_host: pinned-host q/k/v/out, per-chunk H2D/D2H on copy streams "
                     "overlapped with compute (graph-replayed), wall clock incl. copies"}

@@ -403,11 +403,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     int32_t* sSel = reinterpret_cast<int32_t*>(sML + 4 * 128);                         // [k_m] unit ids
     int32_t* sLen = sSel + kMaxSel;                                                    // [k_m] unit lengths
 
-    // launched as a programmatic dependent of the previous step's attention
-    // (AttnParams::pdl > 0): this CTA may take an SM as soon as one frees (before
-    // pending side-stream blocks do) and waits here for every upstream grid.
-    // It lets the next step's attention launch when a.pdl tiles remain (below).
-    if (P.a.pdl > 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     TL_BEGIN();
     if (threadIdx.x == 0) ATS1(56);
     uint64_t cta_t0 = 0;
@@ -429,10 +424,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
     ts.init(a, m);
     ts.sel = sSel;
     ts.len = sLen;
-    if (a.ready_flag) {  // prefill pipeline: this step's lookup (after its prep / eviction) is done
-        if (threadIdx.x == 0) flag_wait(a.ready_flag, a.ready_val);
-        __syncthreads();
-    }
     if (threadIdx.x < a.n_sel) {
         const int64_t id = a.sel[threadIdx.x];
         sSel[threadIdx.x] = a.sel_slot ? a.sel_slot[threadIdx.x] : static_cast<int32_t>(id);  // page index
@@ -501,9 +492,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant
                 tma_load_2d(&P.tm_qc, q_full, sQc, 0, qrow);
                 tma_load_2d(&P.tm_qc, q_full, sQc + 16384, 64, qrow);
             }
-            const int trig = a.pdl ? max(0, ts.T - abs(a.pdl)) : 0;
             for (int j = 0; j < ts.T; ++j) {
-                if (is_k && j == trig) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
                 const Tile t = ts.get(a, j);
                 const CUtensorMap* map;
                 int row;
@@ -1046,17 +1035,15 @@ int launch_attn_tc(const AttnParams& a, cudaStream_t st) {
     cfg.blockDim = dim3(kTcThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute la[3];
+    cudaLaunchAttribute la[2];
     la[0].id = cudaLaunchAttributePriority;
     la[0].val.priority = prio_hi;
     la[1].id = cudaLaunchAttributeClusterDimension;  // the csize query heads of one KV group
     la[1].val.clusterDim.x = 1;
     la[1].val.clusterDim.y = static_cast<unsigned>(csize);
     la[1].val.clusterDim.z = 1;
-    la[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[2].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
-    cfg.numAttrs = a.pdl ? 3 : 2;
+    cfg.numAttrs = 2;
     cudaLaunchKernelEx(&cfg, k_attn_tc, P);
     if (a.n_split > 1) {
         k_attn_merge<<<dim3(static_cast<unsigned>(a.lx), a.H), 128, 0, st>>>(a);

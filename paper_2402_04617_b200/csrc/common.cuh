@@ -107,42 +107,6 @@ __device__ __forceinline__ void tl_put(unsigned kid, unsigned long long t0) {
         }                                                   \
     } while (0)
 
-// step-ready flags between the side streams and the attention (engine.cu)
-__device__ __forceinline__ void flag_release(int64_t* f, int64_t v) {
-    asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(f), "l"(v) : "memory");
-}
-__device__ __forceinline__ int64_t flag_acquire(const int64_t* f) {
-    int64_t v;
-    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-    return v;
-}
-// spin until *f >= v; traps after ~4 s so a broken dependency faults instead of hanging
-__device__ __forceinline__ void flag_wait(const int64_t* f, int64_t v) {
-    if (flag_acquire(f) >= v) return;
-    const unsigned long long t0 = gtimer();
-    while (flag_acquire(f) < v) {
-        __nanosleep(128);
-        if (gtimer() - t0 > 4000000000ull) __trap();
-    }
-}
-
-__device__ __forceinline__ void flag_release_i32(int* f, int v) {
-    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
-}
-// spin until *f != 0 (traps after ~4 s)
-__device__ __forceinline__ void flag_wait_i32(const int* f) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-    if (v) return;
-    const unsigned long long t0 = gtimer();
-    for (;;) {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        if (v) return;
-        __nanosleep(64);
-        if (gtimer() - t0 > 4000000000ull) __trap();
-    }
-}
-
 // Device LRU/bookkeeping state of one layer's TieredStore (memory.hpp:170-323).
 struct LruState {
     int64_t hot_count;

@@ -324,11 +324,6 @@ struct infllm_engine {
     int attn_splits = 0;      // option attn_splits: split-KV K3 (0: auto, when the grid leaves SMs idle)
     int lookup_upb = 48;      // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
     int lookup_upb_decode = 8;  // option lookup_units_per_block_decode: the same for one-token steps (whole GPU)
-    bool attn_flag = false;   // option attn_flag: K3 waits on a step-ready flag instead of graph edges
-    int prep_blocks = 0;      // option prep_blocks: grid cap of the chunk prep kernels (0: none)
-    bool prep_fused = false;  // option prep_fused: one-kernel chunk prep (side.cu) where the shape allows
-    int attn_pdl = 0;  // option attn_pdl = n != 0: K3 t+1 launches programmatically when K3 t has |n| tiles
-                       // left (n > 0: it then waits for its upstream grids; n < 0: it does not)
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -370,11 +365,8 @@ struct infllm_engine {
     EvictParams last_ep{};
     LruParams last_lp{};
     bool last_bf16 = false;
-    int64_t debug_skip = 0;          // timing experiments only: bit0 attention, bit1 lookup+top-k,
-                                     // bit2 evict/finalize/select, bit3 prep, bit4 LRU (results invalid)
 
     // scratch shared by layers (layers run sequentially on one stream)
-    DBuf prep_sync;  // k_prep_chunk look-back state
     DBuf split_o, split_ml;  // split-KV K3 partials
     DBuf qa, qc, chunk_qsum, mass_e, mass_m, row_m, row_l, mass_cta, rtab, qsb, tsum, topk_done, evict_done;
     DBuf dec_part, dec_mass, dec_cnt;  // K4 decode scratch (one sequence)
@@ -391,7 +383,6 @@ struct infllm_engine {
         DBuf unit_k, unit_krot, unit_v, unit_scores, repr, repr_idx, ulen, freq, hot;
         DBuf hot_list, lru, trace, sel, rel, relw, lookup_part, mass_part, ev_part;
         DBuf kmax2;  // [kPB step buffers][G] running max |k|^2 (attention score bound)
-        DBuf ready;  // int64 step-ready flag: the lookup of step s publishes s, K3 of step s waits for it
         DBuf cand;   // multi-block top-k candidates (values then ids), large unit counts
         DBuf dec_maps;  // K4 TMA tensor maps (6), re-encoded when a buffer moves
         std::vector<const void*> dec_maps_key;
@@ -522,7 +513,7 @@ struct infllm_engine {
 
     // every device buffer the engine owns (a captured step graph holds their addresses)
     std::vector<DBuf*> dev_buffers() {
-        std::vector<DBuf*> v{&ex_send, &ex_recv, &out_stage, &out_recv, &split_o, &split_ml, &inv_dev, &prep_sync, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
+        std::vector<DBuf*> v{&ex_send, &ex_recv, &out_stage, &out_recv, &split_o, &split_ml, &inv_dev, &qa, &qc, &chunk_qsum, &mass_e, &mass_m, &row_m, &row_l, &mass_cta, &rtab, &qsb,
                              &tsum, &topk_done, &evict_done, &dec_part, &dec_mass, &dec_cnt};
         for (int b = 0; b < kNB; ++b)
             for (auto* x : {&stage_q[b], &stage_k[b], &stage_v[b], &stage_o[b]}) v.push_back(x);
@@ -531,7 +522,7 @@ struct infllm_engine {
                             &L.unit_krot, &L.unit_v, &L.unit_scores, &L.repr, &L.repr_idx, &L.ulen, &L.freq, &L.hot,
                             &L.hot_list, &L.lru, &L.trace, &L.sel, &L.rel, &L.relw, &L.lookup_part, &L.mass_part,
                             &L.ev_part, &L.kmax2, &L.cand, &L.slot_k, &L.slot_krot, &L.slot_v, &L.slot_unit,
-                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps, &L.ready})
+                            &L.slot_used, &L.unit_slot, &L.sel_slot, &L.tier_miss, &L.tier_stats, &L.dec_maps})
                 v.push_back(b);
         return v;
     }
@@ -776,18 +767,11 @@ struct infllm_engine {
                      est = one_stream ? st : evict_stream;
         // decode steps keep the LRU bookkeeping on its own stream (off the critical
         // path: no later prep / lookup / attention reads it), with real events
-        const bool lru_side = one_stream && !coll && !(debug_skip & 64);
+        const bool lru_side = one_stream && !coll;
         cudaStream_t lru_st = (one_stream && !lru_side) ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
         if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
         pipe_dirty = !one_stream;
-        // K3 of the prefill pipeline depends on its lookup (and through it on the
-        // prep, eviction and LRU) via a device flag instead of cross-stream graph
-        // edges: its only stream predecessor is the previous step's K3, so it can
-        // launch as that one's programmatic dependent and take SMs as they free
-        const bool flag_mode = std::is_same_v<T, bf16> && attn_flag && !one_stream && !coll && tier_slots == 0 &&
-                               tc_eligible(lx) && !(lx == 1 && use_dec && !dec_disabled) && !(debug_skip & 32);
         if (fork) {
-            if (flag_mode) ck(cudaMemsetAsync(L.ready.p, 0xff, sizeof(int64_t), main), "flag reset");
             rec(e_call, main);
             wt(side, e_call);
             wt(pst, e_call);
@@ -830,8 +814,6 @@ struct infllm_engine {
         pp.d = d;
         pp.dv = dv;
         pp.freqs = freqs;
-        pp.max_blocks = prep_blocks;
-        pp.sync = prep_fused ? prep_sync.p : nullptr;
         pp.vl = vl;
         pp.rtab = rtab.as<float2>();
         pp.qs = qsb.as<double>();
@@ -847,27 +829,22 @@ struct infllm_engine {
         // (issued at the eviction site below)
         bool fused_front = false;
         if constexpr (std::is_same_v<T, bf16>)
-            fused_front = lx == 1 && (one_stream || coll) && dec_front_supported(pp) && page_mode() && Gs == Gt &&
-                          !(debug_skip & (8 | 4 | 128));
+            fused_front = lx == 1 && (one_stream || coll) && dec_front_supported(pp) && page_mode() && Gs == Gt;
         auto issue_front = [&](const EvictParams& ep2, cudaStream_t s2) {
             if (coll)
                 coll->front.push_back(DecFrontRec{pp, ep2});
             else
                 launch_dec_front(pp, ep2, s2);
         };
-        const bool prep_one = std::is_same_v<T, bf16> && !fused_front && !coll && prep_chunk_supported(pp);
         const auto evs = fused_front ? std::pair<cudaEvent_t, cudaEvent_t>{} : phase_begin("score", st);
         if (fused_front) {
         } else if (coll) {
             coll->prep.push_back(pp);
-        } else if (prep_one) {
-            if (!(debug_skip & 8)) launch_prep_chunk(pp, st);
-            launches += 1;
         } else {
-            if (!(debug_skip & 8)) launch_prep<T>(pp, st);
+            launch_prep<T>(pp, st);
         }
-        if (!fused_front && !prep_one)
-            launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : (d % 8 == 0 && dv == d && rep <= 8) ? 2 : ((d % 8 == 0 && dv % 8 == 0) ? 3 : 2);
+        if (!fused_front)
+            launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : 2;
         if (!fused_front) phase_end(kPhScore, evs, st);
         rec(e_prep, pst);
         wt(side, e_prep);
@@ -934,7 +911,7 @@ struct infllm_engine {
             } else if (coll) {
                 if (!ep.fused) throw StreamError("decode_batch: sharded eviction is not batched");
                 if (ep.n_init + ep.n_evict > 0) coll->evict.push_back(ep);
-            } else if (!(debug_skip & 4)) {
+            } else {
                 launch_evict<T>(ep, st);
             }
             ++launches;
@@ -950,7 +927,7 @@ struct infllm_engine {
                 fp.L = cfg.local_size;
                 fp.Gtot = Gt;
                 fp.l_bs = static_cast<int>(cfg.unit_size);
-                if (!(debug_skip & 4)) launch_finalize(fp, st);
+                launch_finalize(fp, st);
                 ++launches;
             }
             if (completed > 0) {
@@ -969,7 +946,7 @@ struct infllm_engine {
                 set_page(sp, L, L.pend_start);
                 if (coll)
                     coll->select.push_back(sp);
-                else if (!(debug_skip & 4))
+                else
                     launch_select<T>(sp, st);
                 ++launches;
                 for (int64_t c = 0; c < completed; ++c) {
@@ -994,7 +971,6 @@ struct infllm_engine {
 
         // K1 + K2: lookup (memory.hpp:239-269)
         bool k4_pdl = false;  // the lookup is the last kernel before K4 on the caller's stream
-        bool last_lkp_fast = false;  // this step's lookup publishes the ready flag itself
         if (do_lookup) {
             const auto evp = phase_begin("lookup", st);
             LookupParams lp{};
@@ -1015,8 +991,6 @@ struct infllm_engine {
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
             lp.early_dependents = one_stream ? 1 : 0;  // decode: K4 follows as a programmatic dependent
-            lp.ready_flag = nullptr;
-            lp.ready_val = L.step;
             last_lkp = lp;
             if (coll) {  // batched: relevance scan (rel only) + one top-k block per sequence
                 lp.fused = 2;
@@ -1026,7 +1000,6 @@ struct infllm_engine {
             // as its programmatic dependent); chunk steps take the one-launch kernel sized
             // for the ~20 SMs the attention leaves free
             const bool fast = !coll && !one_stream && Gs == Gt && lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
-            last_lkp_fast = fast && !(debug_skip & 2);
             if (fast) {
                 // one launch: scan + exact top-k; few fat blocks inside the prefill
                 // pipeline (the attention holds most SMs), one unit per warp in decode
@@ -1034,12 +1007,12 @@ struct infllm_engine {
                 lp.cand_v = L.cand.as<double>();
                 lp.cand_i = reinterpret_cast<int64_t*>(L.cand.as<double>() + nc);
                 lp.fused = 1;
-                lp.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
                 last_lkp = lp;
-                if (!(debug_skip & 2))
-                    launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units0, one_stream ? lookup_upb_decode : lookup_upb), st);
+                launch_lookup_topk_fast(lp, lookup_topk_blocks(n_units0, one_stream ? lookup_upb_decode : lookup_upb), st);
             } else if (coll) {
-            } else if (!(debug_skip & 2) && lp.fused != 2) launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            } else if (lp.fused != 2) {
+                launch_lookup(lp, dtype == INFLLM_DTYPE_BF16, st);
+            }
             if (!lp.fused) gather(L.lookup_part.as<double>(), n_units0, st);
             TopkParams tp{};
             tp.part = L.lookup_part.as<double>();
@@ -1048,25 +1021,20 @@ struct infllm_engine {
             tp.U = n_units0;
             tp.n_sel = n_sel;
             tp.Gtot = Gt;
-            if (!(debug_skip & 2) && !lp.fused) launch_topk(tp, st);
+            if (!lp.fused) launch_topk(tp, st);
             int n_lk = lp.fused == 1 ? 1 : 2;
             if (lp.fused == 2 && !coll && !fast) {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
-                if (!(debug_skip & 2))
-                    n_lk = launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
+                n_lk = launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
             }
             launches += n_lk;
-            k4_pdl = one_stream && !coll && !prof && !(debug_skip & 2) && n_sel > 0 && lp.fused != 0;
+            k4_pdl = one_stream && !coll && !prof && n_sel > 0 && lp.fused != 0;
             phase_end(kPhLookup, evp, st);
         }
 
-        if (flag_mode && !(do_lookup && last_lkp_fast)) {
-            launch_flag_set(L.ready.as<int64_t>(), L.step, side);
-            ++launches;
-        }
         rec(e_topk, side);
-        if (!flag_mode && !(debug_skip & 32)) wt(main, e_topk);  // 32: timing experiment only
+        wt(main, e_topk);
         if (tier_slots > 0 && n_sel > 0) {  // GPU unit cache: slots for this step's units, PCIe pull of the misses
             wt(tier_st, e_topk);
             // k_tier_assign keeps the slots of steps k-1 and k: the attention of k-2 must be done
@@ -1102,8 +1070,8 @@ struct infllm_engine {
         rec(e_lookup, side);
         lookup_seq = kseq;
         // this parity's mass buffers were last read by LRU(k-2)
-        if (!flag_mode && lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
-            wt(main, e_lru[b]);  // flag mode: the lookup waited for it
+        if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
+            wt(main, e_lru[b]);
         st = main;
         double* mass_cta_b = mass_cta.as<double>() + b * mass_cta_half;
         double* mass_part_b = L.mass_part.as<double>() + b * std::max<int64_t>(cfg.n_lookup, 1) * Gt;
@@ -1180,8 +1148,7 @@ struct infllm_engine {
         ap.inv_violations = inv_dev.as<unsigned long long>();
         const auto eva = phase_begin("attend", st);
         if constexpr (std::is_same_v<T, bf16>) {
-            if (debug_skip & 1) {
-            } else if (dec_ran) {
+            if (dec_ran) {
                 if (coll)
                     coll->attn.push_back(ap);
                 else {
@@ -1191,14 +1158,11 @@ struct infllm_engine {
                 }
                 ++launches;
             } else if (tc_eligible(lx)) {
-                ap.pdl = !fork && !one_stream ? attn_pdl : 0;
                 ap.n_split = pick_splits_tc(lx, ap);
                 if (ap.n_split > 1) {
                     ap.split_o = split_o.as<float>();
                     ap.split_ml = split_ml.as<float>();
                 }
-                ap.ready_flag = flag_mode ? L.ready.as<int64_t>() : nullptr;
-                ap.ready_val = L.step;
                 launches += launch_attn_tc(ap, st);
             } else {
                 launch_attn_simt<T>(ap, st);
@@ -1291,7 +1255,7 @@ struct infllm_engine {
         const auto evl = coll ? std::pair<cudaEvent_t, cudaEvent_t>{} : phase_begin("evict", lru_st);
         if (coll)
             coll->lru.push_back(lp);
-        else if (!(debug_skip & 16))
+        else
             launch_lru(lp, lru_st);
         if (!coll) phase_end(kPhEvict, evl, lru_st);
         ++launches;
@@ -1664,7 +1628,6 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
                          &e->e_lrudone, &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone,
                          &e->e_attnp[0], &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
             ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
-        e->prep_sync.alloc(prep_chunk_sync_bytes(), st);
         e->inv_dev.alloc(sizeof(unsigned long long), st);
         e->chunk_qsum.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * e->d * sizeof(double), st);
         const size_t km = static_cast<size_t>(std::max<int64_t>(cfg->n_lookup, 1));
@@ -1691,7 +1654,6 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
             L.ring_v.alloc(static_cast<size_t>(e->Gs) * e->R * e->dv * es, st);
             L.P.alloc(static_cast<size_t>(e->R) * e->Gs * e->d * sizeof(double), st);
             L.kmax2.alloc(infllm_engine::kPB * static_cast<size_t>(e->Gs) * sizeof(float), st);
-            L.ready.alloc(sizeof(int64_t), st);
             const size_t ni = static_cast<size_t>(std::max<int64_t>(cfg->init_size, 1));
             L.init_k.alloc(static_cast<size_t>(e->Gs) * ni * e->d * es, st);
             if (cfg->position_mode == INFLLM_POSITION_ABSOLUTE)
@@ -1870,8 +1832,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // captured stream graphs bake in the launch choices these options make:
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
-            k == "attn_pdl" || k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
-            k == "gather_output" || k == "attn_flag" || k == "prep_blocks" || k == "prep_fused" || k == "debug_skip") {
+            k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
+            k == "gather_output") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1880,20 +1842,12 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->tc_disabled = value == 0;
         else if (k == "cuda_graphs")
             e->use_graphs = value != 0;
-        else if (k == "debug_skip")
-            e->debug_skip = value;
         else if (k == "attn_score_bound")
             e->score_bound = value != 0;
         else if (k == "decode_kernel")
             e->dec_disabled = value == 0;
         else if (k == "multi_stream_decode")
             e->multi_stream_decode = value != 0;
-        else if (k == "prep_fused")
-            e->prep_fused = value != 0;
-        else if (k == "prep_blocks")
-            e->prep_blocks = static_cast<int>(std::clamp<int64_t>(value, 0, 1 << 20));
-        else if (k == "attn_flag")
-            e->attn_flag = value != 0;
         else if (k == "gather_output")
             e->gather_output = value != 0;
         else if (k == "attn_splits")
@@ -1902,9 +1856,6 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->lookup_upb_decode = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
         else if (k == "lookup_units_per_block")
             e->lookup_upb = static_cast<int>(std::clamp<int64_t>(value, 1, 1 << 20));
-        else if (k == "attn_pdl")
-            e->attn_pdl = static_cast<int>(std::clamp<int64_t>(value, -(1 << 20), 1 << 20));
-
         else if (k == "host_tier_slots") {
             for (auto& L : e->layers)
                 if (L.unit_cap > 0 && value != e->tier_slots)
@@ -2870,7 +2821,6 @@ void timeline_bind(const TlBuf& b) {
     ck(tl_bind_attn_tc(b), "timeline bind");
     ck(tl_bind_attn_dec(b), "timeline bind");
     ck(tl_bind_lookup(b), "timeline bind");
-    ck(tl_bind_side(b), "timeline bind");
 }
 }  // namespace
 

@@ -26,8 +26,6 @@ __device__ unsigned long long g_dbg_ts[64];
 
 cudaError_t tl_bind_kernels(const TlBuf& b) { return tl_bind_tu(b); }
 
-__global__ void k_flag_set(int64_t* f, int64_t v) { flag_release(f, v); }
-void launch_flag_set(int64_t* flag, int64_t val, cudaStream_t st) { k_flag_set<<<1, 1, 0, st>>>(flag, val); }
 
 void debug_read_timestamps(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, g_dbg_ts, sizeof(unsigned long long) * 64);
@@ -193,268 +191,6 @@ __device__ __forceinline__ void st8(T* p, const V8<T>& r) {
         reinterpret_cast<uint4*>(p)[0] = reinterpret_cast<const uint4*>(&r)[0];
         reinterpret_cast<uint4*>(p)[1] = reinterpret_cast<const uint4*>(&r)[1];
     }
-}
-
-// (2) one thread per (token, KV group, 8 dims): k raw -> ring, k_rot -> ring,
-// every query head of the group -> q_abs / q_clamp, and the fp64 group sum
-// qs[token][g][8 dims]; plus one thread per (8-token run, g, value dim) for
-// the (transposed) value pages.
-template <typename T>
-__global__ void __launch_bounds__(256) k_prep_vec(PrepParams p) {
-    const int pairs = p.d / 2, n8 = p.d / 8;
-    const int64_t n_qk = p.lx * p.G * n8;
-    int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t < n_qk) {
-        const int c8 = static_cast<int>(t % n8);
-        const int g = static_cast<int>((t / n8) % p.G);
-        const int64_t i = t / (static_cast<int64_t>(n8) * p.G);
-        const int64_t pos = p.s + i;
-        const float2* rt = p.rtab + i * pairs + 4 * c8;
-        float2 f[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) f[j] = rt[j];
-        const T* kq = static_cast<const T*>(p.k) + (i * p.G + g) * p.d + 8 * c8;
-        const V8<T> kv = ld8(kq);
-        V8<T> kr;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            float y0, y1;
-            rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
-            kr.v[2 * j] = from_f<T>(y0);
-            kr.v[2 * j + 1] = from_f<T>(y1);
-        }
-        const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
-        st8(static_cast<T*>(p.ring_k) + ro, kv);
-        st8(static_cast<T*>(p.ring_krot) + ro, kr);
-        double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int hh = 0; hh < p.rep; ++hh) {
-            const int h = g * p.rep + hh;
-            const V8<T> qv = ld8(static_cast<const T*>(p.q) + (i * p.H + h) * p.d + 8 * c8);
-            V8<T> qa, qc;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float x0 = to_f(qv.v[2 * j]), x1 = to_f(qv.v[2 * j + 1]);
-                float y0, y1;
-                rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
-                qa.v[2 * j] = from_f<T>(y0);
-                qa.v[2 * j + 1] = from_f<T>(y1);
-                const int a = 4 * c8 + j;
-                rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
-                qc.v[2 * j] = from_f<T>(y0);
-                qc.v[2 * j + 1] = from_f<T>(y1);
-                qs[2 * j] += static_cast<double>(x0);
-                qs[2 * j + 1] += static_cast<double>(x1);
-            }
-            const int64_t qo = (static_cast<int64_t>(h) * p.lxp + i) * p.d + 8 * c8;
-            st8(static_cast<T*>(p.qa) + qo, qa);
-            st8(static_cast<T*>(p.qc) + qo, qc);
-        }
-        double* qd = p.qs + (i * p.G + g) * p.d + 8 * c8;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) qd[e] = qs[e];
-        return;
-    }
-    t -= n_qk;
-    const T* v = static_cast<const T*>(p.v);
-    T* rv = static_cast<T*>(p.ring_v);
-    if (!p.vl.vt) {
-        const int nv8 = p.dv / 8;
-        if (t >= p.lx * p.G * nv8) return;
-        const int c8 = static_cast<int>(t % nv8);
-        const int g = static_cast<int>((t / nv8) % p.G);
-        const int64_t i = t / (static_cast<int64_t>(nv8) * p.G);
-        st8(rv + p.vl.ring(g, p.s + i, 8 * c8), ld8(v + (i * p.G + g) * p.dv + 8 * c8));
-        return;
-    }
-    // transposed pages: 8 consecutive positions of one value dim -> one 16 B store
-    const int64_t r0 = p.s / 8, r1 = (p.s + p.lx + 7) / 8;
-    if (t >= (r1 - r0) * p.G * p.dv) return;
-    const int c = static_cast<int>(t % p.dv);
-    const int g = static_cast<int>((t / p.dv) % p.G);
-    const int64_t run = r0 + t / (static_cast<int64_t>(p.dv) * p.G);
-    const int64_t pa = 8 * run;
-    if (pa >= p.s && pa + 8 <= p.s + p.lx && sizeof(T) == 2) {
-        V8<T> w;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) w.v[j] = v[((pa - p.s + j) * p.G + g) * p.dv + c];
-        st8(rv + p.vl.ring(g, pa, c), w);
-    } else {
-        for (int j = 0; j < 8; ++j) {
-            const int64_t pos = pa + j;
-            if (pos >= p.s && pos < p.s + p.lx) rv[p.vl.ring(g, pos, c)] = v[((pos - p.s) * p.G + g) * p.dv + c];
-        }
-    }
-}
-
-// (3) fp64 prefix of qs over the chunk into the P ring + the chunk total.
-// Block = (group, 32 dims); 16 token segments scanned in parallel.
-constexpr int kPfxSegs = 16;
-__global__ void __launch_bounds__(512) k_qs_prefix(PrepParams p) {
-    __shared__ double tot[kPfxSegs][33];
-    const int g = blockIdx.x, c = blockIdx.y * 32 + threadIdx.x, seg = threadIdx.y;
-    const bool live = c < p.d;
-    const int64_t len = (p.lx + kPfxSegs - 1) / kPfxSegs;
-    const int64_t i0 = seg * len, i1 = min(p.lx, i0 + len);
-    const double* qs = p.qs + static_cast<int64_t>(g) * p.d + c;
-    const int64_t stride = static_cast<int64_t>(p.G) * p.d;
-    double t = 0.0;
-    if (live) {
-#pragma unroll 8
-        for (int64_t i = i0; i < i1; ++i) t += qs[i * stride];
-    }
-    tot[seg][threadIdx.x] = t;
-    __syncthreads();
-    if (!live) return;
-    double run = p.P[((p.s % p.R) * p.G + g) * p.d + c];
-    for (int j = 0; j < seg; ++j) run += tot[j][threadIdx.x];
-#pragma unroll 8
-    for (int64_t i = i0; i < i1; ++i) {
-        run += qs[i * stride];
-        p.P[(((p.s + i + 1) % p.R) * p.G + g) * p.d + c] = run;
-    }
-    if (seg == 0) {
-        double all = 0.0;
-        for (int j = 0; j < kPfxSegs; ++j) all += tot[j][threadIdx.x];
-        p.chunk_qsum[g * p.d + c] = all;
-    }
-}
-
-// (4) fully fused prep: block = (8 head dims, KV group), one thread per
-// token (tiles of 512 tokens with a carried prefix). Each thread rotates its
-// token's k and the group's query heads, appends k/k_rot/v to the ring, and
-// contributes its fp64 group query sum to a block-wide inclusive scan that
-// yields the P ring entries and the chunk total directly.
-constexpr int kPrepThreads = 512;
-template <typename T>
-__global__ void __launch_bounds__(kPrepThreads) k_prep_fused(PrepParams p) {
-    __shared__ double wtot[kPrepThreads / 32][8];
-    __shared__ double carry_s[8];
-    const int c8 = blockIdx.x, g = blockIdx.y;
-    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32, nw = blockDim.x / 32;
-    const T* qg = static_cast<const T*>(p.q);
-    const T* kg = static_cast<const T*>(p.k);
-    const T* vg = static_cast<const T*>(p.v);
-    T* rv = static_cast<T*>(p.ring_v);
-    DBG_TS(40);
-    double carry[8];
-    {
-        const double* P0 = p.P + ((p.s % p.R) * p.G + g) * p.d + 8 * c8;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) carry[e] = P0[e];
-    }
-    double base_total[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) base_total[e] = carry[e];
-    for (int64_t t0 = 0; t0 < p.lx; t0 += blockDim.x) {
-        const int64_t i = t0 + threadIdx.x;
-        const bool live = i < p.lx;
-        double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (live) {
-            const int64_t pos = p.s + i;
-            // all of this thread's global loads in flight before any math
-            constexpr int kMaxRep = 8;
-            V8<T> qv[kMaxRep];
-#pragma unroll
-            for (int hh = 0; hh < kMaxRep; ++hh)
-                if (hh < p.rep) qv[hh] = ld8(qg + (i * p.H + g * p.rep + hh) * p.d + 8 * c8);
-            const V8<T> kv = ld8(kg + (i * p.G + g) * p.d + 8 * c8);
-            const V8<T> vv = ld8(vg + (i * p.G + g) * p.dv + 8 * c8);
-            DBG_TS(41);
-            // rotation factors of (pos, pairs 4*c8..4*c8+3), computed once per step by k_rope_table
-            float2 f[4];
-            {
-                const float4* rt = reinterpret_cast<const float4*>(p.rtab + i * (p.d / 2) + 4 * c8);
-                const float4 a = rt[0], b = rt[1];
-                f[0] = make_float2(a.x, a.y);
-                f[1] = make_float2(a.z, a.w);
-                f[2] = make_float2(b.x, b.y);
-                f[3] = make_float2(b.z, b.w);
-            }
-            V8<T> kr;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float y0, y1;
-                rope_pair(to_f(kv.v[2 * j]), to_f(kv.v[2 * j + 1]), f[j].x, f[j].y, y0, y1);
-                kr.v[2 * j] = from_f<T>(y0);
-                kr.v[2 * j + 1] = from_f<T>(y1);
-            }
-            const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
-            st8(static_cast<T*>(p.ring_k) + ro, kv);
-            st8(static_cast<T*>(p.ring_krot) + ro, kr);
-            DBG_TS(42);
-#pragma unroll
-            for (int hh = 0; hh < kMaxRep; ++hh) {
-                if (hh >= p.rep) break;
-                const int h = g * p.rep + hh;
-                V8<T> qa, qc;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float x0 = to_f(qv[hh].v[2 * j]), x1 = to_f(qv[hh].v[2 * j + 1]);
-                    float y0, y1;
-                    rope_pair(x0, x1, f[j].x, f[j].y, y0, y1);
-                    qa.v[2 * j] = from_f<T>(y0);
-                    qa.v[2 * j + 1] = from_f<T>(y1);
-                    const int a = 4 * c8 + j;
-                    rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
-                    qc.v[2 * j] = from_f<T>(y0);
-                    qc.v[2 * j + 1] = from_f<T>(y1);
-                    qs[2 * j] += static_cast<double>(x0);
-                    qs[2 * j + 1] += static_cast<double>(x1);
-                }
-                const int64_t qo = (static_cast<int64_t>(h) * p.lxp + i) * p.d + 8 * c8;
-                st8(static_cast<T*>(p.qa) + qo, qa);
-                st8(static_cast<T*>(p.qc) + qo, qc);
-            }
-            DBG_TS(43);
-            // values of dims [8*c8, 8*c8+8) (dv == d on this path)
-            if (!p.vl.vt) {
-                st8(rv + p.vl.ring(g, pos, 8 * c8), vv);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) rv[p.vl.ring(g, pos, 8 * c8 + e)] = vv.v[e];
-            }
-        }
-        DBG_TS(44);
-        // block-wide inclusive scan of qs over tokens (fp64; exact for bf16 inputs)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(0xffffffffu, qs[e], o);
-                if (lane >= o) qs[e] += y;
-            }
-        }
-        if (lane == 31)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) wtot[warp][e] = qs[e];
-        __syncthreads();
-        double pre[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            double a = carry[e];
-            for (int w = 0; w < warp; ++w) a += wtot[w][e];
-            pre[e] = a + qs[e];
-        }
-        DBG_TS(45);
-        if (live) {
-            double* Pd = p.P + (((p.s + i + 1) % p.R) * p.G + g) * p.d + 8 * c8;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) Pd[e] = pre[e];
-        }
-        // carry for the next tile = inclusive value of the tile's last token
-        if (threadIdx.x == blockDim.x - 1)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) carry_s[e] = pre[e];
-        __syncthreads();
-#pragma unroll
-        for (int e = 0; e < 8; ++e) carry[e] = carry_s[e];
-        __syncthreads();
-        (void)nw;
-        DBG_TS(46);
-    }
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) p.chunk_qsum[g * p.d + 8 * c8 + e] = carry[e] - base_total[e];
 }
 
 // (5) token-tiled prep with coalesced stores: block = 16 tokens x one KV
@@ -623,25 +359,9 @@ void launch_prep(const PrepParams& p, cudaStream_t st) {
         const int64_t nt = p.lx * (p.d / 2);
         const unsigned tiles = static_cast<unsigned>((p.lx + kTokTile - 1) / kTokTile);
         const unsigned items = tiles * static_cast<unsigned>(p.G);
-        const unsigned cap = p.max_blocks > 0 ? static_cast<unsigned>(p.max_blocks) : items;
-        k_rope_table<<<std::min(static_cast<unsigned>((nt + 255) / 256), cap), 256, 0, st>>>(p);
-        k_prep_tok<T><<<std::min(items, cap), 256, 0, st>>>(p);
-        k_prefix_tiles<<<std::min(items, cap), 128, 0, st>>>(p);
-        return;
-    }
-    if (p.d % 8 == 0 && p.dv == p.d && p.rep <= 8 && p.rtab) {
-        const int64_t nt = p.lx * (p.d / 2);
         k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
-        k_prep_fused<T><<<dim3(p.d / 8, p.G), kPrepThreads, 0, st>>>(p);
-        return;
-    }
-    if (p.d % 8 == 0 && p.dv % 8 == 0 && p.rtab && p.qs) {
-        const int64_t nt = p.lx * (p.d / 2);
-        k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
-        const int64_t n_qk = p.lx * p.G * (p.d / 8);
-        const int64_t n_v = p.vl.vt ? ((p.s + p.lx + 7) / 8 - p.s / 8) * p.G * p.dv : p.lx * p.G * (p.dv / 8);
-        k_prep_vec<T><<<static_cast<unsigned>((n_qk + n_v + 255) / 256), 256, 0, st>>>(p);
-        k_qs_prefix<<<dim3(p.G, (p.d + 31) / 32), dim3(32, kPfxSegs), 0, st>>>(p);
+        k_prep_tok<T><<<items, 256, 0, st>>>(p);
+        k_prefix_tiles<<<items, 128, 0, st>>>(p);
         return;
     }
     k_prep<T><<<static_cast<unsigned>((p.lx + kPrepTok - 1) / kPrepTok), 256, 0, st>>>(p);
@@ -1176,64 +896,11 @@ __global__ void __launch_bounds__(256) k_topk_local(const double* rel, int64_t U
         cand_i[blockIdx.x * k + r] = ok ? s0 + loc[r] : -1;
     }
 }
-// Final top-k of the slice candidates in one block of T threads, T * kRadixE
-// at a time: the kept k (ascending index = ascending id, candidates being in
-// id order) are prepended to the next window, so (rel desc, id asc) carries.
-__device__ void merge_candidates(const double* cv, const int64_t* ci, int64_t n, int64_t k, int64_t* sel, double* tv,
-                                 int64_t* ti) {
-    __shared__ int64_t loc[kTopkMaxSel];
-    const int64_t C = static_cast<int64_t>(blockDim.x) * kRadixE;
-    int64_t m = 0, next = 0;
-    for (;;) {
-        const int64_t take = C - m < n - next ? C - m : n - next;
-        for (int64_t i = threadIdx.x; i < take; i += blockDim.x) {
-            tv[m + i] = cv[next + i];
-            ti[m + i] = ci[next + i];
-        }
-        __syncthreads();
-        m += take;
-        next += take;
-        const int64_t kk = k < m ? k : m;
-        block_topk_radix(tv, m, kk, loc);
-        __syncthreads();
-        if (next == n) {
-            for (int r = threadIdx.x; r < kk; r += blockDim.x) sel[r] = ti[loc[r]];
-            return;
-        }
-        double v = 0.0;
-        int64_t id = -1;
-        if (threadIdx.x < kk) {
-            v = tv[loc[threadIdx.x]];
-            id = ti[loc[threadIdx.x]];
-        }
-        __syncthreads();
-        if (threadIdx.x < kk) {
-            tv[threadIdx.x] = v;
-            ti[threadIdx.x] = id;
-        }
-        __syncthreads();
-        m = kk;
-    }
-}
-// fold != 0: the last block to finish merges the candidates (no merge launch)
-__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p, int fold) {
+__global__ void __launch_bounds__(256, 1) k_lookup_stream(LookupParams p) {
     if (p.early_dependents) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // merge block / K4 (PDL)
     TL_BEGIN();
     lookup_stream_body(p, gridDim.x);
     TL_END(TL_LOOKUP);
-    if (!fold) return;
-    __shared__ bool last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    extern __shared__ __align__(16) uint8_t scan_smem[];  // the scan's stage ring is free now
-    double* tv = reinterpret_cast<double*>(scan_smem);
-    int64_t* ti = reinterpret_cast<int64_t*>(scan_smem + sizeof(double) * blockDim.x * kRadixE);
-    merge_candidates(p.cand_v, p.cand_i, static_cast<int64_t>(gridDim.x) * p.n_sel, p.n_sel, p.sel, tv, ti);
-    if (threadIdx.x == 0) *p.done = 0;
 }
 __global__ void __launch_bounds__(1024) k_topk_final(const double* cand_v, const int64_t* cand_i, int64_t n, int64_t k,
                                                      int64_t* sel) {
@@ -1257,8 +924,7 @@ int64_t topk_multi_scratch(int64_t U, int64_t k) {
 }
 int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
     p.fused = 2;
-    static const int64_t stream_min = getenv("INFLLM_STREAM_MIN_U") ? atoll(getenv("INFLLM_STREAM_MIN_U"))
-                                                                     : 2049;  // past the fused last-block top-k
+    constexpr int64_t stream_min = 2049;  // past the fused last-block top-k
     if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.U >= stream_min &&
         p.U <= static_cast<int64_t>(kScanBlocks) * kSliceU && p.n_sel >= 0 &&
         kScanBlocks * p.n_sel <= 1024 * kRadixE) {
@@ -1271,15 +937,9 @@ int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* 
         }
         p.cand_v = p.n_sel > 0 ? cand_v : nullptr;
         p.cand_i = p.n_sel > 0 ? cand_i : nullptr;
-        // folded merge (last scan block, 256 threads, windows of 2048): off by default, measured
-        // slower than the 1024-thread merge block launched as a programmatic dependent
-        // (512K decode 62 vs 57 us/step); INFLLM_SCAN_FOLD=1 enables it
-        static const bool fold_ok = getenv("INFLLM_SCAN_FOLD") && atoi(getenv("INFLLM_SCAN_FOLD")) == 1;
-        const int fold = fold_ok && p.done && p.n_sel > 0 ? 1 : 0;
-        k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p, fold);
-        if (fold) return 1;
+        // the merge block follows as a programmatic dependent (a decode step's K4 may launch from it)
+        k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p);
         if (p.n_sel > 0) {
-            static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(1);
             cfg.blockDim = dim3(1024);
@@ -1288,7 +948,7 @@ int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* 
             la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             la[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = la;
-            cfg.numAttrs = pdl ? 1 : 0;
+            cfg.numAttrs = 1;
             cudaLaunchKernelEx(&cfg, k_topk_final, static_cast<const double*>(cand_v), static_cast<const int64_t*>(cand_i),
                                static_cast<int64_t>(kScanBlocks) * p.n_sel, p.n_sel, p.sel);
             return 2;
@@ -1312,8 +972,7 @@ __global__ void __launch_bounds__(1024) k_topk_one(const double* rel, int64_t U,
 int launch_topk_multi(const double* rel, int64_t U, int64_t k, double* cand_v, int64_t* cand_i, int64_t* sel,
                       cudaStream_t st) {
     if (U <= 0 || k <= 0) return 0;
-    static const bool one = !(getenv("INFLLM_TOPK_ONE") && atoi(getenv("INFLLM_TOPK_ONE")) == 0);
-    if (one && U <= 1024 * kRadixE) {
+    if (U <= 1024 * kRadixE) {
         k_topk_one<<<1, 1024, 0, st>>>(rel, U, std::min<int64_t>(k, U), sel);
         return 1;
     }
@@ -1357,33 +1016,6 @@ void launch_topk(const TopkParams& p, cudaStream_t st) {
     // radix select with 1024 threads x kRadixE ids, else the two-level warp selection
     const bool radix = p.U <= 1024 * kRadixE;
     k_topk<<<1, radix ? 1024 : 32 * kTopkWarps, radix ? 0 : topk_smem(p.U), st>>>(p);
-}
-
-__global__ void __launch_bounds__(1024) k_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k,
-                                                              double* rel, double* relw, int64_t* ids) {
-    for (int64_t u = threadIdx.x; u < U; u += blockDim.x) {
-        double a = 0.0;
-        for (int g = 0; g < Gtot; ++g) a += part[u * Gtot + g];
-        rel[u] = a;
-    }
-    __syncthreads();
-    if (U <= static_cast<int64_t>(blockDim.x) * kRadixE)
-        block_topk_radix(rel, U, k, ids);
-    else
-        block_topk(rel, relw, U, k, ids);
-}
-
-void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
-                                int64_t* ids, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_rel_topk_standalone, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kTopkSmemU * sizeof(double));
-        attr = true;
-    }
-    const bool radix = U <= 1024 * kRadixE;
-    k_rel_topk_standalone<<<1, radix ? 1024 : 32 * kTopkWarps, radix ? 0 : topk_smem(U), st>>>(part, U, Gtot, k, rel,
-                                                                                              relw, ids);
 }
 
 // --------------------------------------------------------------------------
@@ -2536,8 +2168,7 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
                 cudaFuncSetAttribute(k_lookup_stream_b, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
                 attr = true;
             }
-            static const bool per_seq = getenv("INFLLM_BATCH_SCAN_PERSEQ") != nullptr;  // A/B experiments
-            if (!per_seq && B <= kScanMaxB) {
+            if (B <= kScanMaxB) {
                 static bool attr2 = false;
                 if (!attr2) {
                     cudaFuncSetAttribute(k_lookup_stream_bal, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2551,7 +2182,6 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             } else {
                 k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
             }
-            static const bool pdl = !(getenv("INFLLM_DEC_PDL") && atoi(getenv("INFLLM_DEC_PDL")) == 0);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(B));
             cfg.blockDim = dim3(1024);
@@ -2560,7 +2190,7 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             la[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = la;
-            cfg.numAttrs = pdl ? 1 : 0;
+            cfg.numAttrs = 1;
             cudaLaunchKernelEx(&cfg, k_topk_b, ps);
             break;
         }

@@ -60,8 +60,6 @@ struct PrepParams {
     const float* kmax2_prev;  // [G] the previous step's copy
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
-    int max_blocks;  // grid cap of the chunk prep kernels (0: one block per work item)
-    void* sync;      // k_prep_chunk look-back state (prep_chunk_sync_bytes, zeroed once), or null
     VLayout vl;
     RopeFreqs freqs;
 };
@@ -79,8 +77,6 @@ struct LookupParams {
     double* cand_v;      // fused 2, streaming scan: per-block top-k candidates [gridDim][n_sel]
     int64_t* cand_i;
     int early_dependents;  // 1: let a programmatic dependent (decode K4) launch at kernel entry
-    int64_t* ready_flag;   // non-null: the last block publishes ready_val here once sel is written
-    int64_t ready_val;
 };
 
 struct TopkParams {
@@ -119,11 +115,6 @@ struct AttnParams {
     int64_t R, s, lx, lxp, init_len, local_start, L, l_I, unit_cap;
     int n_sel, H, G, rep, d, dv, l_bs;
     int absolute, want_mass;
-    int pdl;  // K3: programmatic dependent launch after the previous kernel on its stream
-    // K3 in the prefill pipeline: wait until *ready_flag >= ready_val (published by the
-    // lookup of this step, which itself followed the prep, eviction and LRU it needs)
-    const int64_t* ready_flag;
-    int64_t ready_val;
     // check_softmax (engine.hpp:361-371) on the device: rows whose softmax
     // denominator is not a positive finite number add one here (or null)
     unsigned long long* inv_violations;
@@ -251,8 +242,7 @@ struct SelectParams {
 };
 
 void debug_read_timestamps(unsigned long long* out);
-// publish a step-ready flag (release) from a stream: steps whose lookup does not set it
-void launch_flag_set(int64_t* flag, int64_t val, cudaStream_t st);
+
 // standalone.cu: the reference's stand-alone operators (attend, TieredStore, ScoreAccumulator)
 struct AttendLaunch {
     const void* dev_segs;  // AttendSeg[n_seg] in device memory (attend_pack_seg)
@@ -294,13 +284,7 @@ void score_acc_run(const void* q, int64_t lx, int64_t s, const void* keys, int64
 void score_acc_final(const double* sums, int64_t ring0, int64_t cap, int64_t n, int64_t L, float* out, cudaStream_t st);
 void score_acc_zero(double* sums, int64_t from, int64_t n, int64_t cap, cudaStream_t st);
 
-// side.cu: one-kernel chunk prep (bf16, d = dv = 128, transposed values), bitwise
-// equal to rope table + k_prep_tok + k_prefix_tiles; 32-token tiles, lx <= 32 * kPrepChunkMaxTiles
-constexpr int kPrepChunkMaxTiles = 64;
-size_t prep_chunk_sync_bytes();
-bool prep_chunk_supported(const PrepParams& p);
-void launch_prep_chunk(const PrepParams& p, cudaStream_t st);
-cudaError_t tl_bind_side(const TlBuf& b);
+
 // bind the device timeline buffer in each translation unit (kernels.cu, attn_tc.cu, attn_dec.cu)
 cudaError_t tl_bind_kernels(const TlBuf& b);
 cudaError_t tl_bind_attn_tc(const TlBuf& b);
@@ -347,7 +331,5 @@ size_t dec_front_size();
 void launch_select_standalone(const float* scores, const int64_t* lens, int64_t n_units, int64_t unit_len,
                               int64_t r_k, int64_t* idx, cudaStream_t st);
 // standalone relevance reduce + top-k (C ABI infllm_lookup)
-void launch_rel_topk_standalone(const double* part, int64_t U, int Gtot, int64_t k, double* rel, double* relw,
-                                int64_t* ids, cudaStream_t st);
 
 }  // namespace infllm

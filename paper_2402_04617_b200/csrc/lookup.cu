@@ -278,11 +278,6 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
         if (lane < k) p.sel[lane] = static_cast<int64_t>(static_cast<unsigned>(~id_key));
         if (lane == 0 && nb > 1) *p.done = 0;
         TL_MARK(3, mark);  // final selection
-        if (p.ready_flag) {  // the attention of this step may read sel now
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) flag_release(p.ready_flag, p.ready_val);
-        }
     }
 }
 

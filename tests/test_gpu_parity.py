@@ -225,37 +225,23 @@ def test_lookup_bf16_c2_shape(U, k):
     assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k))
 
 
-_FOLD_CHILD = """
-import sys, numpy as np, torch
-sys.path.insert(0, '.')
-from oracle import oracle as O
-from paper_2402_04617_b200 import lookup
-for U, k in [(2049, 16), (4063, 16), (9000, 32)]:
+@pytest.mark.parametrize("U,k", [(2049, 16), (4063, 16), (9000, 32), (40000, 16)])
+def test_lookup_heavy_ties_twice(U, k):
+    """The one-launch lookup (block lists + threshold-filtered final selection)
+    on integer-valued representatives, so many units tie on relevance: ids
+    bit-exact against the oracle's (rel desc, id asc) order, two calls in a row
+    (the last-block counter is re-zeroed by the kernel)."""
+    from paper_2402_04617_b200 import lookup
+
     rng = np.random.default_rng(U)
     reprk = rng.integers(-3, 4, size=(U, 8, 4, 128)).astype(np.float32)
     qb = rng.integers(-2, 3, size=(4, 32, 128)).astype(np.float32)
     qsum = qb.astype(np.float64).reshape(4, 8, 4, 128).sum(axis=(0, 2))
-    for _ in range(2):  # the block counter is re-zeroed by the kernel
+    want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
+    for _ in range(2):
         rel, ids = lookup(torch.from_numpy(qsum).cuda(), torch.from_numpy(reprk).cuda().bfloat16(), k)
-        want = O.relevance_all(qb, reprk.transpose(0, 2, 1, 3))
         assert np.array_equal(rel.cpu().numpy(), want)
         assert ids.cpu().tolist() == sorted(O.argsort_topk(want, k)), (U, k)
-print("fold ok")
-"""
-
-
-def test_streaming_scan_folded_merge():
-    """The streaming scan with the merge folded into its last block
-    (INFLLM_SCAN_FOLD=1, off by default; process-wide switch, so a child
-    process): ids bit-exact against the oracle, two calls in a row."""
-    import os
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _FOLD_CHILD], cwd=root, capture_output=True, text=True, timeout=300,
-                       env=dict(os.environ, INFLLM_SCAN_FOLD="1"))
-    assert r.returncode == 0 and "fold ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_encode_stream_replay_beyond_2048_units():

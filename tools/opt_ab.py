@@ -1,6 +1,6 @@
 # A/B of engine options on the C2 128K stream: ms per stream (CUDA events, best of N) and
 # bitwise output equality against the first configuration.
-#   python tools/opt_ab.py attn_pdl=0 attn_pdl=1
+#   python tools/opt_ab.py "" attn_splits=2
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
