@@ -333,11 +333,14 @@ __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p, int tile,
     double v[kTokTile];
 #pragma unroll
     for (int j = 0; j < kTokTile; ++j) v[j] = j < nt ? p.qs[(i0 + j) * stride + g * p.d + c] : 0.0;
+    const int R = static_cast<int>(p.R);
+    int sl = static_cast<int>((p.s + i0 + 1) % p.R);  // one 64-bit division, then wrap by hand
 #pragma unroll
     for (int j = 0; j < kTokTile; ++j) {
         if (j >= nt) break;
         run += v[j];
-        p.P[(((p.s + i0 + j + 1) % p.R) * p.G + g) * p.d + c] = run;
+        p.P[(static_cast<int64_t>(sl) * p.G + g) * p.d + c] = run;
+        if (++sl == R) sl = 0;
     }
     if (tile == ntiles - 1) {  // chunk total = sum of the tile sums, in order
         double all = 0.0;
@@ -526,7 +529,7 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
     if (threadIdx.x == 0) *p.done = 0;
 }
-__global__ void __launch_bounds__(256, 2) k_lookup_reg(LookupParams p) {
+__global__ void __launch_bounds__(256, 1) k_lookup_reg(LookupParams p) {
     // a decode step's K4 may start its CTAs that do not read the selection now
     // (programmatic dependent launch; those that do wait for this grid)
     if (p.early_dependents) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1651,8 +1654,11 @@ __device__ __forceinline__ void evict_tok_body(const EvictParams& p) {
     // issue the score loads first (evictees only)
     double acc = 0.0;
     if (!to_init) {
-        const double* Phi = p.P + (((pos + p.L + 1) % p.R) * p.G + g) * p.d;
-        const double* Plo = p.P + (((pos + 1) % p.R) * p.G + g) * p.d;
+        const int64_t slo = slot + 1 == p.R ? 0 : slot + 1;
+        int64_t shi = slot + 1 + p.L;  // l_L < R: at most one wrap
+        if (shi >= p.R) shi -= p.R;
+        const double* Phi = p.P + (shi * p.G + g) * p.d;
+        const double* Plo = p.P + (slo * p.G + g) * p.d;
         for (int j = 0; j < per; ++j) {
             const int c = c0 + j;
             if (c < p.d) acc += static_cast<double>(to_f(rk[c])) * (Phi[c] - Plo[c]);
@@ -1915,11 +1921,31 @@ namespace infllm {
 // Same arithmetic as k_rope_table + k_prep_tok + k_prefix_tiles +
 // k_evict_tok at l_x = 1 (rope factors from fp64 angles, query sums in head
 // order, P[s+1] = P[s] + qs, r_m from the prefix difference), in one launch.
-__device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictParams& ep) {
+__device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictParams& ep,
+                                               unsigned long long mark = 0) {
     const int g = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t pos = p.s;
+    // the d/2 rotation factors of this position, one fp64 sincos per thread in
+    // parallel (rotary.hpp:25-30; the large-argument reduction is the slow part)
+    __shared__ float2 s_rc[128];
+    for (int a = threadIdx.x; a < p.d / 2; a += blockDim.x) {
+        float c, sn;
+        rope_cs(p.freqs, a, pos, c, sn);
+        s_rc[a] = make_float2(c, sn);
+    }
+    __syncthreads();
+    TL_MARK(40, mark);  // rotation factors
+    // ring slots of this position and the next, computed once (64-bit division
+    // is a subroutine on the GPU)
+    const int R = static_cast<int>(p.R);
+    const int slot = static_cast<int>(pos % p.R), slot1 = slot + 1 == R ? 0 : slot + 1;
     if (lane < 16) {
         const int c8 = lane;
+        // this position's prefix row, loaded with the inputs
+        const double* Pin = p.P + (static_cast<int64_t>(slot) * p.G + g) * p.d + 8 * c8;
+        double pin[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pin[e] = Pin[e];
         const bf16* qg = static_cast<const bf16*>(p.q);
         constexpr int kMaxRep = 8;
         V8<bf16> qv[kMaxRep];
@@ -1930,7 +1956,7 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
         const V8<bf16> vv = ld8(static_cast<const bf16*>(p.v) + g * p.dv + 8 * c8);
         float2 f[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) rope_cs(p.freqs, 4 * c8 + j, pos, f[j].x, f[j].y);
+        for (int j = 0; j < 4; ++j) f[j] = s_rc[4 * c8 + j];
         V8<bf16> kr;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1942,7 +1968,7 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
         float kn2 = 0.f;  // |k|^2, as k_prep_tok
 #pragma unroll
         for (int e = 0; e < 8; ++e) kn2 = fmaf(to_f(kv.v[e]), to_f(kv.v[e]), kn2);
-        const int64_t ro = (static_cast<int64_t>(g) * p.R + pos % p.R) * p.d + 8 * c8;
+        const int64_t ro = (static_cast<int64_t>(g) * R + slot) * p.d + 8 * c8;
         st8(static_cast<bf16*>(p.ring_k) + ro, kv);
         st8(static_cast<bf16*>(p.ring_krot) + ro, kr);
         double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1969,14 +1995,19 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
             st8(static_cast<bf16*>(p.qc) + qo, qc);
         }
         bf16* rv = static_cast<bf16*>(p.ring_v);
+        if (p.vl.vt) {  // transposed value pages [G][R/128][dv][128]
+            const int64_t vb = ((static_cast<int64_t>(g) * (R / 128) + slot / 128) * p.dv + 8 * c8) * 128 + slot % 128;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) rv[p.vl.ring(g, pos, 8 * c8 + e)] = vv.v[e];
+            for (int e = 0; e < 8; ++e) rv[vb + 128 * e] = vv.v[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) rv[p.vl.ring(g, pos, 8 * c8 + e)] = vv.v[e];
+        }
         // prefix ring and chunk query sum (k_prefix_tiles at l_x = 1)
-        const double* Pin = p.P + ((pos % p.R) * p.G + g) * p.d + 8 * c8;
-        double* Pout = p.P + (((pos + 1) % p.R) * p.G + g) * p.d + 8 * c8;
+        double* Pout = p.P + (static_cast<int64_t>(slot1) * p.G + g) * p.d + 8 * c8;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-            Pout[e] = Pin[e] + qs[e];
+            Pout[e] = pin[e] + qs[e];
             p.chunk_qsum[g * p.d + 8 * c8 + e] = 0.0 + (qs[e] + 0.0);
         }
 #pragma unroll
@@ -1985,22 +2016,24 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
     }
     if (ep.n_init + ep.n_evict == 0) return;  // uniform: nothing leaves the window this step
     __syncthreads();  // this step's P row is read by the eviction score
+    TL_MARK(41, mark);  // prep of the token
     evict_tok_body<bf16>(ep);
+    TL_MARK(42, mark);  // eviction of the token leaving the window
 }
-__global__ void __launch_bounds__(1024) k_dec_front(PrepParams p, EvictParams ep) {
+__global__ void __launch_bounds__(256) k_dec_front(PrepParams p, EvictParams ep) {
     TL_BEGIN();
-    dec_front_body(p, ep);
+    dec_front_body(p, ep, tl_t0_);
     TL_END(TL_DEC_FRONT);
 }
 struct DecFront {
     PrepParams p;
     EvictParams ep;
 };
-__global__ void __launch_bounds__(1024) k_dec_front_b(const DecFront* __restrict__ fs) {
+__global__ void __launch_bounds__(256) k_dec_front_b(const DecFront* __restrict__ fs) {
     dec_front_body(fs[blockIdx.z].p, fs[blockIdx.z].ep);
 }
 bool dec_front_supported(const PrepParams& p) {
-    return p.d == 128 && p.dv == 128 && p.rep <= 8 && p.G <= 32 && p.lx == 1 && p.vl.vt;
+    return p.d == 128 && p.dv == 128 && p.rep <= 8 && p.G <= 8 && p.lx == 1 && p.vl.vt;  // one warp per group
 }
 void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t st) {
     k_dec_front<<<1, 32 * p.G, 0, st>>>(p, ep);
