@@ -294,9 +294,13 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
         const int64_t i0 = static_cast<int64_t>(bx) * kTokTile;
         const int nt = static_cast<int>(min(static_cast<int64_t>(kTokTile), p.lx - i0));
         T* rv = static_cast<T*>(p.ring_v);
+        const int R = static_cast<int>(p.R);
+        const int sl0 = static_cast<int>((p.s + i0) % p.R);  // one 64-bit division per block
         for (int t = threadIdx.x; t < 128 * kTokTile; t += blockDim.x) {
             const int c = t / kTokTile, j = t % kTokTile;
-            if (j < nt) rv[p.vl.ring(g, p.s + i0 + j, c)] = svt[c][j];
+            const int sl = sl0 + j >= R ? sl0 + j - R : sl0 + j;
+            // [G][R/128][dv][128] pages (VLayout::ring with vt)
+            if (j < nt) rv[((static_cast<int64_t>(g) * (R / 128) + sl / 128) * p.dv + c) * 128 + sl % 128] = svt[c][j];
         }
     }
 }

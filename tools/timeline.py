@@ -90,6 +90,8 @@ for i in range(20, nl):
         continue
     o = (kid != 0) & (t0 < b) & (t1 > a)
     for k in np.unique(kid[o]):
+        if k >= len(KINDS):
+            continue
         late[KINDS[k]] += int(((kid == k) & o).sum())
         late_sm[KINDS[k]] += len(np.unique(sm[(kid == k) & o]))
 print("side blocks overlapping the attention CTA start window (launches 20+):", dict(late))
