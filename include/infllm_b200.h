@@ -172,7 +172,16 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * 2*n_lookup <= S <= 16384; set before reserve() and the first step),
  * "decode_kernel" (1 = split-KV decode attention for one-token steps,
  * default; 0 = the prefill attention kernel), "multi_stream_decode" (1 = run
- * decode steps through the five-stream pipeline; default 0 = caller's stream). */
+ * decode steps through the five-stream pipeline; default 0 = caller's stream),
+ * "attn_splits" (split-KV tcgen05 attention: 0 = automatic when the grid leaves
+ * SMs idle, else the split count, <= 16), "attn_streams" (2 = chunk-step
+ * attention alternates between two dedicated streams so consecutive launches
+ * overlap at the handoff, default; 1 = the caller's stream),
+ * "graph_node_priority" (1 = instantiate stream graphs honouring the
+ * attention's launch priority; default 0), "lookup_units_per_block" /
+ * "lookup_units_per_block_decode" (K1+K2 grid: units per block in chunk /
+ * one-token steps), "gather_output" (sharded engines: all-gather every head's
+ * output into `out`). Options that change launches drop captured graphs. */
 int infllm_engine_set_option(infllm_engine_t eng, const char* key, int64_t value);
 
 /* StreamEngine::encode_chunk (engine.hpp:92-97) for one layer: lookup (if

@@ -324,6 +324,15 @@ struct infllm_engine {
     int attn_splits = 0;      // option attn_splits: split-KV K3 (0: auto, when the grid leaves SMs idle)
     int lookup_upb = 48;      // option lookup_units_per_block: K1+K2 grid inside the prefill pipeline
     int lookup_upb_decode = 8;  // option lookup_units_per_block_decode: the same for one-token steps (whole GPU)
+    // option attn_streams: chunk-step attention alternates between this many
+    // dedicated high-priority streams (1: the caller's stream). Attention t+1
+    // reads nothing attention t writes (own prep, selection and mass buffers),
+    // so with two streams its CTAs take the SMs attention t frees as they free
+    // up instead of queueing behind t's last CTA while side kernels fill them.
+    int attn_streams = 2;
+    bool graph_prio = false;  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
+    cudaStream_t attn_st[2] = {nullptr, nullptr};
+    cudaEvent_t out_free = nullptr;  // host path: the staging buffer `out` points into is drained
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -346,6 +355,7 @@ struct infllm_engine {
     static constexpr int kPB = 3;
     cudaEvent_t e_evict = nullptr, e_evdone = nullptr, e_attnp[kPB] = {nullptr, nullptr, nullptr};
     int64_t attn_seq[kPB] = {-1, -1, -1};  // step that last recorded e_attnp[pb]
+    int64_t attn_last = -1;                 // step that last recorded e_attn
     // host tier: slot assignment + PCIe page pulls of step t on their own stream
     // (after lookup t, before attention t), so lookup t+1 does not queue behind them
     cudaStream_t tier_stream = nullptr;
@@ -638,6 +648,7 @@ struct infllm_engine {
         tier_seq = -1;
         for (auto& x : lru_seq) x = -1;
         for (auto& a : attn_seq) a = -1;
+        attn_last = -1;
         lookup_seq = -1;
         evict_seq = -1;
         pipe_dirty = false;
@@ -763,7 +774,11 @@ struct infllm_engine {
         // multi-stream pipeline only pays for chunk-sized steps, and skipping
         // its ~25 event calls halves the host cost of a decode step
         one_stream = lx == 1 && !capturing && !multi_stream_decode;
-        cudaStream_t main = st, side = one_stream ? st : side_stream, pst = one_stream ? st : prep_stream,
+        bool dual = false;
+        if constexpr (std::is_same_v<T, bf16>)
+            dual = attn_streams > 1 && !one_stream && !coll && lx > 1 && Gs == Gt && tc_eligible(lx);
+        const cudaStream_t caller = st;
+        cudaStream_t main = dual ? attn_st[kseq & 1] : st, side = one_stream ? st : side_stream, pst = one_stream ? st : prep_stream,
                      est = one_stream ? st : evict_stream;
         // decode steps keep the LRU bookkeeping on its own stream (off the critical
         // path: no later prep / lookup / attention reads it), with real events
@@ -772,7 +787,7 @@ struct infllm_engine {
         if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
         pipe_dirty = !one_stream;
         if (fork) {
-            rec(e_call, main);
+            rec(e_call, caller);
             wt(side, e_call);
             wt(pst, e_call);
         }
@@ -1072,6 +1087,7 @@ struct infllm_engine {
         // this parity's mass buffers were last read by LRU(k-2)
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0))
             wt(main, e_lru[b]);
+        if (dual && out_free) wt(main, out_free);  // host path: stage_o of this group drained
         st = main;
         double* mass_cta_b = mass_cta.as<double>() + b * mass_cta_half;
         double* mass_part_b = L.mass_part.as<double>() + b * std::max<int64_t>(cfg.n_lookup, 1) * Gt;
@@ -1159,6 +1175,9 @@ struct infllm_engine {
                 ++launches;
             } else if (tc_eligible(lx)) {
                 ap.n_split = pick_splits_tc(lx, ap);
+                // one split scratch: after the other stream's attention
+                if (ap.n_split > 1 && dual && attn_last >= 0 && (capture_seq0 < 0 || attn_last >= capture_seq0))
+                    wt(main, e_attn);
                 if (ap.n_split > 1) {
                     ap.split_o = split_o.as<float>();
                     ap.split_ml = split_ml.as<float>();
@@ -1246,6 +1265,7 @@ struct infllm_engine {
         rec(e_attn, main);
         rec(e_attnp[pb], main);
         attn_seq[pb] = kseq;
+        attn_last = kseq;
         wt(lru_st, e_attn);
         if (lru_side) {
             ck(cudaEventRecord(e_attn, main), "record");
@@ -1262,12 +1282,14 @@ struct infllm_engine {
         rec(e_lru[b], lru_st);
         if (lru_side) ck(cudaEventRecord(e_lru[b], lru_st), "record");
         lru_seq[b] = kseq;
+        if (dual) wt(caller, e_attn);  // the caller's stream follows every attention (outputs)
         st = side;
 
         if (one_stream) {  // nothing else was recorded: no later step may wait on those events
             if (!lru_side)
                 for (auto& x : lru_seq) x = -1;
             for (auto& a2 : attn_seq) a2 = -1;
+            attn_last = -1;
             lookup_seq = evict_seq = tier_seq = -1;
         }
         L.trace_count += n_sel;
@@ -1338,12 +1360,14 @@ struct infllm_engine {
             const int64_t goff = gi * GC, glen = std::min<int64_t>(GC, n - goff);
             const int b = static_cast<int>(gi % kNB);
             if (gi >= kNB) ck(cudaStreamWaitEvent(st, ev_out[gi - kNB], 0), "wait");  // stage_o[b] drained
+            out_free = gi >= kNB ? ev_out[gi - kNB] : nullptr;  // the attention streams wait for it too
             for (int64_t off = 0; off < glen; off += C) {
                 const int64_t lx = std::min<int64_t>(C, glen - off);
                 step<T>(li, at(stage_q[b].p, off, Hs * d), at(stage_k[b].p, off, Gs * d),
                         at(stage_v[b].p, off, Gs * dv), lx, false, const_cast<void*>(at(stage_o[b].p, off, Hs * dv)), st,
                         gi == 0 && off == 0, off == 0 ? ev_in[gi] : nullptr);
             }
+            out_free = nullptr;
             ck(cudaEventRecord(ev_comp[gi], st), "record");
             ck(cudaStreamWaitEvent(d2h_stream, ev_comp[gi], 0), "wait");
             ck(cudaMemcpyAsync(const_cast<void*>(at(hout, goff, Hs * dv)), stage_o[b].p, glen * Hs * dv * esz,
@@ -1440,6 +1464,7 @@ struct infllm_engine {
             } catch (...) {
                 capturing = false;
                 capture_seq0 = -1;
+                out_free = nullptr;
                 cudaStreamEndCapture(cap_stream, &graph);
                 if (graph) cudaGraphDestroy(graph);
                 restore(L, cur);
@@ -1451,7 +1476,11 @@ struct infllm_engine {
             g.steps = seq - seq0;
             seq = seq0;
             ck(cudaStreamEndCapture(cap_stream, &graph), "end capture");
-            ck(cudaGraphInstantiate(&g.exec, graph, 0), "graph instantiate");
+            // node priorities (the attention launches carry the highest) are honoured
+            // only with this flag: without it the graph's pending side-kernel blocks and
+            // the next attention's CTAs are dispatched in plain launch order
+            ck(cudaGraphInstantiate(&g.exec, graph, graph_prio ? cudaGraphInstantiateFlagUseNodePriority : 0),
+               "graph instantiate");
             cudaGraphDestroy(graph);
             g.after = save(L);
             g.launches = launches - l0;
@@ -1624,6 +1653,12 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         ck(cudaStreamCreateWithFlags(&e->prep_stream, cudaStreamNonBlocking), "prep stream");
         ck(cudaStreamCreateWithFlags(&e->evict_stream, cudaStreamNonBlocking), "evict stream");
         ck(cudaStreamCreateWithFlags(&e->tier_stream, cudaStreamNonBlocking), "tier stream");
+        {
+            int lo = 0, hi = 0;
+            ck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+            for (auto& s2 : e->attn_st)
+                ck(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi), "attention stream");
+        }
         for (auto* ev : {&e->e_call, &e->e_topk, &e->e_side, &e->e_lru[0], &e->e_lru[1], &e->e_lru[2], &e->e_attn,
                          &e->e_lrudone, &e->e_prep, &e->e_lookup, &e->e_prepdone, &e->e_evict, &e->e_evdone,
                          &e->e_attnp[0], &e->e_attnp[1], &e->e_attnp[2], &e->e_tier, &e->e_tierdone})
@@ -1687,7 +1722,7 @@ int infllm_engine_destroy(infllm_engine_t e) {
         for (auto& g : e->graphs) infllm_engine::drop_graph(g);
         if (e->comm) nccl().comm_destroy(static_cast<ncclComm_t>(e->comm));
         for (auto s2 : {e->cap_stream, e->h2d_stream, e->d2h_stream, e->side_stream, e->lru_stream, e->prep_stream,
-                        e->evict_stream, e->tier_stream})
+                        e->evict_stream, e->tier_stream, e->attn_st[0], e->attn_st[1]})
             if (s2) cudaStreamDestroy(s2);
         for (auto ev : {e->e_call, e->e_topk, e->e_side, e->e_lru[0], e->e_lru[1], e->e_lru[2], e->e_attn,
                         e->e_lrudone, e->e_prep, e->e_lookup, e->e_prepdone, e->e_evict, e->e_evdone,
@@ -1833,7 +1868,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
             k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
-            k == "gather_output") {
+            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1850,6 +1885,10 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->multi_stream_decode = value != 0;
         else if (k == "gather_output")
             e->gather_output = value != 0;
+        else if (k == "graph_node_priority")
+            e->graph_prio = value != 0;
+        else if (k == "attn_streams")
+            e->attn_streams = static_cast<int>(std::clamp<int64_t>(value, 1, 2));
         else if (k == "attn_splits")
             e->attn_splits = static_cast<int>(std::clamp<int64_t>(value, 0, infllm_engine::kMaxSplitsTc));
         else if (k == "lookup_units_per_block_decode")
@@ -2198,27 +2237,44 @@ int infllm_profile_begin(infllm_engine_t e, int32_t enable) {
 }
 
 namespace {
+// device time (ms) during which a phase had launches in flight: the length of
+// the union of its [begin, end] event intervals. Launches of one phase on one
+// stream never overlap (union = sum); chunk-step attention alternates between
+// two streams, and consecutive launches overlap while one's CTAs drain and the
+// next one's start, which a plain sum would count twice.
+double union_ms(const std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    if (v.empty()) return 0;
+    std::vector<std::pair<float, float>> iv;
+    iv.reserve(v.size());
+    for (auto& p : v) {
+        float a = 0, b = 0;
+        ck(cudaEventElapsedTime(&a, v[0].first, p.first), "elapsed");
+        ck(cudaEventElapsedTime(&b, v[0].first, p.second), "elapsed");
+        iv.emplace_back(a, b);
+    }
+    std::sort(iv.begin(), iv.end());
+    double tot = 0, lo = iv[0].first, hi = iv[0].second;
+    for (size_t i = 1; i < iv.size(); ++i) {
+        if (iv[i].first > hi) {
+            tot += hi - lo;
+            lo = iv[i].first;
+            hi = iv[i].second;
+        } else {
+            hi = std::max(hi, static_cast<double>(iv[i].second));
+        }
+    }
+    return tot + (hi - lo);
+}
 // device time of each phase's launches in the profile window (ms) and launch counts
 void phase_sums(infllm_engine* e, double* ms, int64_t* n) {
     ck(cudaDeviceSynchronize(), "sync");
     for (int ph = 0; ph < kPhases; ++ph) {
-        ms[ph] = 0;
         n[ph] = static_cast<int64_t>(e->ev[ph].size());
-        for (auto& p : e->ev[ph]) {
-            float t = 0;
-            ck(cudaEventElapsedTime(&t, p.first, p.second), "elapsed");
-            ms[ph] += t;
-        }
+        ms[ph] = union_ms(e->ev[ph]);
         // graph replays: event nodes hold the timings of the latest replay
         for (auto& g : e->graphs) {
             if (g.replays_in_window == 0) continue;
-            double gt = 0;
-            for (auto& p : g.ev[ph]) {
-                float t = 0;
-                ck(cudaEventElapsedTime(&t, p.first, p.second), "elapsed");
-                gt += t;
-            }
-            ms[ph] += gt * g.replays_in_window;
+            ms[ph] += union_ms(g.ev[ph]) * g.replays_in_window;
             n[ph] += static_cast<int64_t>(g.ev[ph].size()) * g.replays_in_window;
         }
     }
