@@ -376,6 +376,8 @@ __device__ __forceinline__ void tmem_ld32_x(uint32_t taddr, float* x) {
 // Slow path: per-warpgroup online max with lazy rescaling of its own O_w, P
 // over S_w, merged in the epilogue.
 __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant__ TcParams P) {
+    // a programmatic dependent (the engine's prep gate) may launch once every CTA is resident
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQa = smem;

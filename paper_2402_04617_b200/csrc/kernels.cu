@@ -198,9 +198,10 @@ __device__ __forceinline__ void st8(T* p, const V8<T>& r) {
 // q_abs / q_clamp / ring k / k_rot are written by 16 consecutive threads
 // (256 B each); value pages are transposed through shared memory; the fp64
 // group query sums go to qs[token][g][:] plus a per-tile column sum.
+// RP: query heads per KV group when known at compile time (0: p.rep <= 8).
 constexpr int kTokTile = 16;
-template <typename T>
-__device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g) {
+template <typename T, int RP>
+__device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g, unsigned long long& mark) {
     __shared__ double sqs[kTokTile][128 + 2];
     __shared__ T svt[128][kTokTile + 2];
     const int tt = threadIdx.x / 16, c8 = threadIdx.x % 16;  // token in tile, dim chunk
@@ -211,11 +212,12 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
     double qs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     float kn2 = 0.f;  // this thread's part of |k|^2
     if (live) {
-        constexpr int kMaxRep = 8;
+        constexpr int kMaxRep = RP > 0 ? RP : 8;
+        const int nrep = RP > 0 ? RP : p.rep;
         V8<T> qv[kMaxRep];
 #pragma unroll
         for (int hh = 0; hh < kMaxRep; ++hh)
-            if (hh < p.rep) qv[hh] = ld8(qg + (i * p.H + g * p.rep + hh) * p.d + 8 * c8);
+            if (hh < nrep) qv[hh] = ld8(qg + (i * p.H + g * nrep + hh) * p.d + 8 * c8);
         const V8<T> kv = ld8(static_cast<const T*>(p.k) + (i * p.G + g) * p.d + 8 * c8);
         const V8<T> vv = ld8(static_cast<const T*>(p.v) + (i * p.G + g) * p.dv + 8 * c8);
         float2 f[4];
@@ -242,7 +244,7 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
         st8(static_cast<T*>(p.ring_krot) + ro, kr);
 #pragma unroll
         for (int hh = 0; hh < kMaxRep; ++hh) {
-            if (hh >= p.rep) break;
+            if (hh >= nrep) break;
             V8<T> qa, qc;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -258,13 +260,14 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
                 qs[2 * j] += static_cast<double>(x0);
                 qs[2 * j + 1] += static_cast<double>(x1);
             }
-            const int64_t qo = (static_cast<int64_t>(g * p.rep + hh) * p.lxp + i) * p.d + 8 * c8;
+            const int64_t qo = (static_cast<int64_t>(g * nrep + hh) * p.lxp + i) * p.d + 8 * c8;
             st8(static_cast<T*>(p.qa) + qo, qa);
             st8(static_cast<T*>(p.qc) + qo, qc);
         }
         double2* qd = reinterpret_cast<double2*>(p.qs + (i * p.G + g) * p.d + 8 * c8);
 #pragma unroll
         for (int e = 0; e < 4; ++e) qd[e] = make_double2(qs[2 * e], qs[2 * e + 1]);
+        TL_MARK(10, mark);  // rows loaded, rotated, stored
         if (!p.vl.vt) {
             st8(static_cast<T*>(p.ring_v) + p.vl.ring(g, pos, 8 * c8), vv);
         } else {
@@ -282,6 +285,7 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
 #pragma unroll
     for (int e = 0; e < 8; ++e) sqs[tt][8 * c8 + e] = qs[e];
     __syncthreads();
+    TL_MARK(11, mark);  // key-norm bound, tile staged
     // per-tile column sums (token order)
     if (threadIdx.x < 128) {
         const int c = threadIdx.x;
@@ -289,6 +293,7 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
         for (int t = 0; t < kTokTile; ++t) a += sqs[t][c];
         p.tsum[(static_cast<int64_t>(bx) * p.G + g) * p.d + c] = a;
     }
+    TL_MARK(12, mark);  // tile column sums
     if (p.vl.vt) {
         // transposed value page rows: 16 consecutive positions of one dim
         const int64_t i0 = static_cast<int64_t>(bx) * kTokTile;
@@ -302,15 +307,17 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
             // [G][R/128][dv][128] pages (VLayout::ring with vt)
             if (j < nt) rv[((static_cast<int64_t>(g) * (R / 128) + sl / 128) * p.dv + c) * 128 + sl % 128] = svt[c][j];
         }
+        TL_MARK(13, mark);  // value pages
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
+template <typename T, int RP>
+__global__ void __launch_bounds__(256, RP == 4 ? 3 : 1) k_prep_tok(PrepParams p) {
     TL_BEGIN();
+    unsigned long long mark = tl_t0_;
     const int tiles = static_cast<int>((p.lx + kTokTile - 1) / kTokTile);
     for (int item = blockIdx.x; item < tiles * p.G; item += gridDim.x) {
-        prep_tok_body<T>(p, item % tiles, item / tiles);
+        prep_tok_body<T, RP>(p, item % tiles, item / tiles, mark);
         __syncthreads();  // shared tiles are reused by the next item
     }
     TL_END(TL_PREP);
@@ -318,6 +325,7 @@ __global__ void __launch_bounds__(256) k_prep_tok(PrepParams p) {
 
 // (6) fp64 prefix into the P ring from the per-token sums and the tile sums:
 // block = (tile, group), thread = dim; rows of P written whole (coalesced).
+template <typename T>
 __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p, int tile, int g, int ntiles) {
     const int c = threadIdx.x;
     if (c >= p.d) return;
@@ -352,11 +360,12 @@ __device__ __forceinline__ void prefix_tiles_body(const PrepParams& p, int tile,
         p.chunk_qsum[g * p.d + c] = all;
     }
 }
+template <typename T>
 __global__ void __launch_bounds__(128) k_prefix_tiles(PrepParams p) {
     TL_BEGIN();
     const int tiles = static_cast<int>((p.lx + kTokTile - 1) / kTokTile);
     for (int item = blockIdx.x; item < tiles * p.G; item += gridDim.x)
-        prefix_tiles_body(p, item % tiles, item / tiles, tiles);
+        prefix_tiles_body<T>(p, item % tiles, item / tiles, tiles);
     TL_END(TL_PREFIX);
 }
 
@@ -367,8 +376,11 @@ void launch_prep(const PrepParams& p, cudaStream_t st) {
         const unsigned tiles = static_cast<unsigned>((p.lx + kTokTile - 1) / kTokTile);
         const unsigned items = tiles * static_cast<unsigned>(p.G);
         k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
-        k_prep_tok<T><<<items, 256, 0, st>>>(p);
-        k_prefix_tiles<<<items, 128, 0, st>>>(p);
+        if (p.rep == 4)
+            k_prep_tok<T, 4><<<items, 256, 0, st>>>(p);
+        else
+            k_prep_tok<T, 0><<<items, 256, 0, st>>>(p);
+        k_prefix_tiles<T><<<items, 128, 0, st>>>(p);
         return;
     }
     k_prep<T><<<static_cast<unsigned>((p.lx + kPrepTok - 1) / kPrepTok), 256, 0, st>>>(p);
@@ -1547,90 +1559,6 @@ __device__ void warp_select(const float* sc, int len, int r_k, int* out);
 // the rest are evicted into unit pages (engine.hpp:323-340, UnitPacker::add
 // memory.hpp:59-78). r_m partial per group: k_m . (P[m+L+1] - P[m+1]), i.e.
 // sum over the L following queries of the group's q . k_m (repr_score.hpp:53-67).
-// Grid (token groups of 8, KV group); warp w handles one token.
-template <typename T>
-__global__ void __launch_bounds__(256) k_evict(EvictParams p) {
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    const int g = blockIdx.y;
-    // transposed value pages: when this block's 8 tokens are one 8-aligned run
-    // that stays inside one source and one destination page (always the case
-    // for page-aligned units), each value dim moves as one 16 B vector
-    const int64_t idx0 = static_cast<int64_t>(blockIdx.x) * 8;
-    const int64_t pos0 = p.pop0 + idx0;
-    bool fast_v = false;
-    if (p.vl.vt && sizeof(T) == 2 && pos0 % 8 == 0 && idx0 + 8 <= p.n_init + p.n_evict) {
-        const bool all_init = idx0 + 8 <= p.n_init, all_unit = idx0 >= p.n_init;
-        if (all_init) fast_v = true;
-        if (all_unit && (pos0 - p.pend_start) % 8 == 0 && (pos0 - p.pend_start) % p.l_bs <= p.l_bs - 8) fast_v = true;
-    }
-    if (fast_v) {
-        const T* rv = static_cast<const T*>(p.ring_v);
-        for (int c = threadIdx.x; c < p.dv; c += blockDim.x) {
-            const uint4 x = *reinterpret_cast<const uint4*>(rv + p.vl.ring(g, pos0, c));
-            T* dst;
-            if (idx0 < p.n_init) {
-                dst = static_cast<T*>(p.init_v) + p.vl.init(g, pos0, c);
-            } else {
-                const int64_t rel = pos0 - p.pend_start;
-                dst = static_cast<T*>(p.unit_v) + p.vl.unit(p.unit0 + rel / p.l_bs, g, rel % p.l_bs, c);
-            }
-            *reinterpret_cast<uint4*>(dst) = x;
-        }
-    }
-    if (idx >= p.n_init + p.n_evict) return;
-    const int64_t pos = p.pop0 + idx;
-    const int64_t slot = pos % p.R;
-    const T* rk = static_cast<const T*>(p.ring_k) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
-    const T* rkr = static_cast<const T*>(p.ring_krot) + (static_cast<int64_t>(g) * p.R + slot) * p.d;
-    const T* rv = static_cast<const T*>(p.ring_v);
-    T *dk, *dkr;
-    T* dvb;
-    int64_t u = 0, off = 0;
-    const bool to_init = idx < p.n_init;
-    if (to_init) {
-        dk = static_cast<T*>(p.init_k) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d;
-        dkr = p.absolute ? static_cast<T*>(p.init_krot) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d : nullptr;
-        dvb = static_cast<T*>(p.init_v);
-    } else {
-        const int64_t rel = pos - p.pend_start;
-        u = p.unit0 + rel / p.l_bs;
-        off = rel % p.l_bs;
-        dk = static_cast<T*>(p.unit_k) + ((u * p.G + g) * p.l_bs + off) * p.d;
-        dkr = p.absolute ? static_cast<T*>(p.unit_krot) + ((u * p.G + g) * p.l_bs + off) * p.d : nullptr;
-        dvb = static_cast<T*>(p.unit_v);
-    }
-    if ((p.d * sizeof(T)) % 16 == 0) {
-        const int nv = p.d * static_cast<int>(sizeof(T)) / 16;
-        for (int t = lane; t < nv; t += 32) {
-            reinterpret_cast<uint4*>(dk)[t] = reinterpret_cast<const uint4*>(rk)[t];
-            if (dkr) reinterpret_cast<uint4*>(dkr)[t] = reinterpret_cast<const uint4*>(rkr)[t];
-        }
-    } else {
-        for (int c = lane; c < p.d; c += 32) {
-            dk[c] = rk[c];
-            if (dkr) dkr[c] = rkr[c];
-        }
-    }
-    if (!(p.vl.vt && fast_v)) {
-        for (int c = lane; c < p.dv; c += 32) {
-            const T x = rv[p.vl.ring(g, pos, c)];
-            if (to_init)
-                dvb[p.vl.init(g, pos, c)] = x;
-            else
-                dvb[p.vl.unit(u, g, off, c)] = x;
-        }
-    }
-    if (to_init) return;
-    const int64_t e = idx - p.n_init;
-    const double* Phi = p.P + (((pos + p.L + 1) % p.R) * p.G + g) * p.d;
-    const double* Plo = p.P + (((pos + 1) % p.R) * p.G + g) * p.d;
-    double a = 0.0;
-    for (int c = lane; c < p.d; c += 32) a += static_cast<double>(to_f(rk[c])) * (Phi[c] - Plo[c]);
-    a = warp_sum_d(a);
-    if (lane == 0) p.ev_part[e * p.Gtot + p.g0 + g] = a;
-}
-
 // Eviction with all loads in flight at once: block = one popped token, warp
 // = one KV group. Copies k (and k_rot in absolute mode) and v into the
 // initial-token buffer or the token's unit page; for evicted tokens computes
@@ -1720,14 +1648,115 @@ __global__ void __launch_bounds__(256) k_evict_tok(EvictParams p) {
     TL_END(TL_EVICT);
 }
 
+// Chunk steps: one warp per departing token, all of its KV groups (the
+// per-group dots are the same lane slices and xor trees as evict_tok_body,
+// summed in group order, so scores are bitwise identical); eight tokens per
+// block. A chunk's 512 evictions take 64 short blocks instead of 512, so the
+// launch leaves the SMs the attention is about to take after a few
+// microseconds (SM occupancy, not bandwidth, is what it costs the step).
+constexpr int kEvWarps = 8;
+template <typename T>
+__global__ void __launch_bounds__(kEvWarps * 32) k_evict_warp(EvictParams p) {
+    TL_BEGIN();
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kEvWarps;
+    const int64_t idx = i0 + w;
+    const int R = static_cast<int>(p.R);
+    const int sl0 = static_cast<int>((p.pop0 + i0) % p.R);  // one 64-bit division per block
+    if (idx < p.n_init + p.n_evict) {
+        const int64_t pos = p.pop0 + idx;
+        const int slot = sl0 + w >= R ? sl0 + w - R : sl0 + w;
+        const bool to_init = idx < p.n_init;
+        int64_t u = 0;
+        int off = 0;
+        if (!to_init) {
+            const int rel = static_cast<int>(pos - p.pend_start);  // < l_L + l_C: 32-bit division
+            u = p.unit0 + rel / p.l_bs;
+            off = rel % p.l_bs;
+        }
+        const int per = (p.d + 31) / 32;
+        const int c0 = lane * per;
+        int slo = slot + 1 == R ? 0 : slot + 1;
+        int shi = slot + 1 + static_cast<int>(p.L);  // l_L < R: at most one wrap
+        if (shi >= R) shi -= R;
+        double tot = 0.0;
+        for (int g = 0; g < p.G; ++g) {
+            const T* rk = static_cast<const T*>(p.ring_k) + (static_cast<int64_t>(g) * R + slot) * p.d;
+            double acc = 0.0;
+            if (!to_init) {
+                const double* Phi = p.P + (static_cast<int64_t>(shi) * p.G + g) * p.d;
+                const double* Plo = p.P + (static_cast<int64_t>(slo) * p.G + g) * p.d;
+                if (per == 4 && sizeof(T) == 2) {  // d = 128: 8-byte key slice, two 16-byte loads per P row
+                    const uint2 kb = *reinterpret_cast<const uint2*>(rk + c0);
+                    const double2 h0 = *reinterpret_cast<const double2*>(Phi + c0);
+                    const double2 h1 = *reinterpret_cast<const double2*>(Phi + c0 + 2);
+                    const double2 l0 = *reinterpret_cast<const double2*>(Plo + c0);
+                    const double2 l1 = *reinterpret_cast<const double2*>(Plo + c0 + 2);
+                    const T* kk = reinterpret_cast<const T*>(&kb);
+                    acc += static_cast<double>(to_f(kk[0])) * (h0.x - l0.x);
+                    acc += static_cast<double>(to_f(kk[1])) * (h0.y - l0.y);
+                    acc += static_cast<double>(to_f(kk[2])) * (h1.x - l1.x);
+                    acc += static_cast<double>(to_f(kk[3])) * (h1.y - l1.y);
+                } else {
+                    for (int j = 0; j < per; ++j) {
+                        const int c = c0 + j;
+                        if (c < p.d) acc += static_cast<double>(to_f(rk[c])) * (Phi[c] - Plo[c]);
+                    }
+                }
+            }
+            if (!(p.page_mode && !to_init)) {  // page mode: k_select copies whole unit pages
+                T* dk = to_init ? static_cast<T*>(p.init_k) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d
+                                : static_cast<T*>(p.unit_k) + ((u * p.G + g) * p.l_bs + off) * p.d;
+                T* dkr = !p.absolute ? nullptr
+                         : to_init   ? static_cast<T*>(p.init_krot) + (static_cast<int64_t>(g) * p.l_I + pos) * p.d
+                                     : static_cast<T*>(p.unit_krot) + ((u * p.G + g) * p.l_bs + off) * p.d;
+                const T* rkr = static_cast<const T*>(p.ring_krot) + (static_cast<int64_t>(g) * R + slot) * p.d;
+                for (int c = lane; c < p.d; c += 32) {
+                    dk[c] = rk[c];
+                    if (dkr) dkr[c] = rkr[c];
+                }
+                const T* rv = static_cast<const T*>(p.ring_v);
+                T* dvb = static_cast<T*>(to_init ? p.init_v : p.unit_v);
+                for (int c = lane; c < p.dv; c += 32) {
+                    const T x = rv[p.vl.ring(g, pos, c)];
+                    if (to_init)
+                        dvb[p.vl.init(g, pos, c)] = x;
+                    else
+                        dvb[p.vl.unit(u, g, off, c)] = x;
+                }
+            }
+            if (to_init) continue;
+            acc = warp_sum_d(acc);
+            if (!p.fused) {
+                if (lane == 0) p.ev_part[(idx - p.n_init) * p.Gtot + p.g0 + g] = acc;
+            } else {
+                tot += acc;
+            }
+        }
+        if (!to_init && p.fused && lane == 0)
+            p.unit_scores[u * p.l_bs + off] = static_cast<float>(tot / static_cast<double>(p.L));
+    }
+    TL_END(TL_EVICT);
+}
+
 template <typename T>
 void launch_evict(const EvictParams& p, cudaStream_t st) {
     const int64_t n = p.n_init + p.n_evict;
     if (n <= 0) return;
-    if (p.G <= 32)
-        k_evict_tok<T><<<static_cast<unsigned>(n), 32 * p.G, 0, st>>>(p);
-    else
-        k_evict<T><<<dim3(static_cast<unsigned>((n + 7) / 8), p.G), 256, 0, st>>>(p);
+    k_evict_warp<T><<<static_cast<unsigned>((n + kEvWarps - 1) / kEvWarps), kEvWarps * 32, 0, st>>>(p);
+}
+__global__ void k_gate() {}
+void launch_gate(cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_gate);
 }
 template void launch_evict<float>(const EvictParams&, cudaStream_t);
 template void launch_evict<bf16>(const EvictParams&, cudaStream_t);
@@ -1794,10 +1823,15 @@ __device__ void warp_select(const float* sc, int len, int r_k, int* out) {
 
 // page mode: block = (unit, group): the unit's K (and K_rot) rows and its V
 // page are contiguous 32 KB blocks of the ring (slots pos0 + 128 i .. + 127,
-// no wrap since R is a multiple of 128): copied with 16-byte vectors
+// no wrap since R is a multiple of 128): copied with 16-byte vectors by
+// threads [32, blockDim) while warp 0 selects the representatives
 template <typename T>
-__device__ void select_page(const SelectParams& p, int64_t u, int g, const int* idx, int take) {
-    const int64_t slot = (p.pos0 + 128 * (u - p.u0)) % p.R;
+__device__ __forceinline__ int64_t select_page_slot(const SelectParams& p, int64_t u) {
+    return (p.pos0 + 128 * (u - p.u0)) % p.R;
+}
+template <typename T>
+__device__ void select_page_copy(const SelectParams& p, int64_t u, int g, int tid, int nthr) {
+    const int64_t slot = select_page_slot<T>(p, u);
     const int64_t rowb = static_cast<int64_t>(128) * p.d * static_cast<int64_t>(sizeof(T)) / 16;  // uint4 per K page
     const uint4* sk = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d);
     uint4* dk = reinterpret_cast<uint4*>(static_cast<T*>(const_cast<void*>(p.unit_k)) + ((u * p.G + g) * 128) * p.d);
@@ -1808,17 +1842,17 @@ __device__ void select_page(const SelectParams& p, int64_t u, int g, const int* 
     const uint4* sv = reinterpret_cast<const uint4*>(rv + (p.vl.vt ? p.vl.ring(g, slot, 0) : (g * p.R + slot) * p.dv));
     uint4* dv = reinterpret_cast<uint4*>(uv + p.vl.unit(u, g, 0, 0));
     // K and V pages: 8 + 8 independent 16-byte loads in flight per thread, then the stores
-    for (int64_t t0 = 0; t0 < rowb || t0 < vb; t0 += 8 * static_cast<int64_t>(blockDim.x)) {
+    for (int64_t t0 = 0; t0 < rowb || t0 < vb; t0 += 8 * static_cast<int64_t>(nthr)) {
         uint4 rk4[8], rv4[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int64_t t = t0 + threadIdx.x + i * static_cast<int64_t>(blockDim.x);
+            const int64_t t = t0 + tid + i * static_cast<int64_t>(nthr);
             if (t < rowb) rk4[i] = sk[t];
             if (t < vb) rv4[i] = sv[t];
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int64_t t = t0 + threadIdx.x + i * static_cast<int64_t>(blockDim.x);
+            const int64_t t = t0 + tid + i * static_cast<int64_t>(nthr);
             if (t < rowb) dk[t] = rk4[i];
             if (t < vb) dv[t] = rv4[i];
         }
@@ -1826,9 +1860,13 @@ __device__ void select_page(const SelectParams& p, int64_t u, int g, const int* 
     if (p.absolute) {
         const uint4* skr = reinterpret_cast<const uint4*>(static_cast<const T*>(p.ring_krot) + (g * p.R + slot) * p.d);
         uint4* dkr = reinterpret_cast<uint4*>(static_cast<T*>(p.unit_krot) + ((u * p.G + g) * 128) * p.d);
-        for (int64_t t = threadIdx.x; t < rowb; t += blockDim.x) dkr[t] = skr[t];
+        for (int64_t t = tid; t < rowb; t += nthr) dkr[t] = skr[t];
     }
-    // representative rows of this group straight from the ring (memory.hpp:111-123)
+}
+// representative rows of this group straight from the ring (memory.hpp:111-123)
+template <typename T>
+__device__ void select_page_repr(const SelectParams& p, int64_t u, int g, const int* idx, int take) {
+    const int64_t slot = select_page_slot<T>(p, u);
     const T* rk = static_cast<const T*>(p.ring_k) + (g * p.R + slot) * p.d;
     T* rp = static_cast<T*>(p.repr) + ((u * p.G + g) * p.r_k) * p.d;
     const int nv = p.d * static_cast<int>(sizeof(T)) / 16;
@@ -1853,10 +1891,12 @@ __device__ __forceinline__ void select_body(const SelectParams& p) {
             for (int k = 0; k < take; ++k) idx[k] = r[k];
         if (threadIdx.x < p.r_k && blockIdx.y == 0)
             p.repr_idx[u * p.r_k + threadIdx.x] = threadIdx.x < take ? r[threadIdx.x] : -1;
+    } else if (p.page_mode) {
+        select_page_copy<T>(p, u, static_cast<int>(blockIdx.y), threadIdx.x - 32, blockDim.x - 32);
     }
     __syncthreads();
     if (p.page_mode) {
-        select_page<T>(p, u, static_cast<int>(blockIdx.y), idx, take);
+        select_page_repr<T>(p, u, static_cast<int>(blockIdx.y), idx, take);
         return;
     }
     const T* uk = static_cast<const T*>(p.unit_k);
@@ -1883,7 +1923,7 @@ __device__ __forceinline__ void select_body(const SelectParams& p) {
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_select(SelectParams p) {
+__global__ void __launch_bounds__(512) k_select(SelectParams p) {
     TL_BEGIN();
     select_body<T>(p);
     TL_END(TL_SELECT);
@@ -1892,7 +1932,7 @@ __global__ void __launch_bounds__(256) k_select(SelectParams p) {
 template <typename T>
 void launch_select(const SelectParams& p, cudaStream_t st) {
     if (p.n_units <= 0) return;
-    k_select<T><<<dim3(static_cast<unsigned>(p.n_units), p.page_mode ? p.G : 1), p.page_mode ? 256 : 128, 0, st>>>(p);
+    k_select<T><<<dim3(static_cast<unsigned>(p.n_units), p.page_mode ? p.G : 1), p.page_mode ? 512 : 128, 0, st>>>(p);
 }
 template void launch_select<float>(const SelectParams&, cudaStream_t);
 template void launch_select<bf16>(const SelectParams&, cudaStream_t);
@@ -2053,10 +2093,11 @@ __global__ void k_rope_table_b(const PrepParams* __restrict__ ps) {
     rope_table_body(ps[blockIdx.z], static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
 }
 __global__ void __launch_bounds__(256) k_prep_tok_b(const PrepParams* __restrict__ ps) {
-    prep_tok_body<bf16>(ps[blockIdx.z], blockIdx.x, blockIdx.y);
+    unsigned long long mark = 0;
+    prep_tok_body<bf16, 0>(ps[blockIdx.z], blockIdx.x, blockIdx.y, mark);
 }
 __global__ void __launch_bounds__(128) k_prefix_tiles_b(const PrepParams* __restrict__ ps) {
-    prefix_tiles_body(ps[blockIdx.z], blockIdx.x, blockIdx.y, gridDim.x);
+    prefix_tiles_body<bf16>(ps[blockIdx.z], blockIdx.x, blockIdx.y, gridDim.x);
 }
 __global__ void __launch_bounds__(256) k_evict_tok_b(const EvictParams* __restrict__ ps) {
     const EvictParams& p = ps[blockIdx.z];

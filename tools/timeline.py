@@ -143,3 +143,23 @@ for k, v in LK.items():
     sp = (v[:, 1] - v[:, 0]) / 1e3
     print(f"{k:9s} launch span us median {np.median(d):7.2f} p90 {np.percentile(d, 90):7.2f}; block start spread "
           f"median {np.median(sp):6.2f}; blocks/launch {np.median(v[:, 3]):.0f}")
+
+# at each handoff (A_(i-1) last CTA end): side blocks resident then, and side
+# blocks that started between that moment and A_i's last CTA start
+res = Counter()
+res_sm = []
+started = Counter()
+for i in range(20, nl):
+    T = rows[i - 1, 3]
+    o = (kid != 0) & (kid < len(KINDS)) & (t0 <= T) & (t1 > T)
+    for k in np.unique(kid[o]):
+        res[KINDS[k]] += int(((kid == k) & o).sum())
+    res_sm.append(len(np.unique(sm[o])))
+    w = (kid != 0) & (kid < len(KINDS)) & (t0 > T) & (t0 < rows[i, 1])
+    for k in np.unique(kid[w]):
+        started[KINDS[k]] += int(((kid == k) & w).sum())
+n_h = max(1, nl - 20)
+print("side blocks resident at the handoff (per handoff):", {k: round(v / n_h, 1) for k, v in res.items()},
+      f"SMs with a side block: median {np.median(res_sm):.0f}")
+print("side blocks started between the handoff and the last attention CTA start (per handoff):",
+      {k: round(v / n_h, 1) for k, v in started.items()})
