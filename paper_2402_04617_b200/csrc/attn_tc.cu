@@ -23,8 +23,11 @@ void debug_read_attn_timestamps(unsigned long long* out) {
 #ifndef ATTN_CTA_TS
 #define ATTN_CTA_TS 0
 #endif
+// clusters of 2 query heads share each K/V tile by TMA multicast; 4 measured
+// slower in-stream (65.6 vs 66.1 us per C2 step): a 4-CTA cluster needs 4 free
+// SMs of one GPC at once, which the handoff between consecutive attentions rarely has
 #ifndef ATTN_MAX_CLUSTER
-#define ATTN_MAX_CLUSTER 8
+#define ATTN_MAX_CLUSTER 2
 #endif
 #ifndef ATTN_TS_J0
 #define ATTN_TS_J0 20
@@ -376,8 +379,6 @@ __device__ __forceinline__ void tmem_ld32_x(uint32_t taddr, float* x) {
 // Slow path: per-warpgroup online max with lazy rescaling of its own O_w, P
 // over S_w, merged in the epilogue.
 __global__ void __launch_bounds__(kTcThreads, 1) k_attn_tc(const __grid_constant__ TcParams P) {
-    // a programmatic dependent (the engine's prep gate) may launch once every CTA is resident
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQa = smem;

@@ -333,16 +333,6 @@ struct infllm_engine {
     bool graph_prio = false;  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
     cudaStream_t attn_st[2] = {nullptr, nullptr};
     cudaEvent_t out_free = nullptr;  // host path: the staging buffer `out` points into is drained
-    // option prep_gate: with two attention streams, step k's prep kernels follow
-    // attention k-2 on its stream as programmatic dependents of a one-thread gate
-    // kernel, so they are released once every CTA of attention k-2 is resident
-    // (and attention k-3 is done: prep buffers) instead of at the moment an
-    // attention ends, when their blocks would take the SMs the next
-    // attention's CTAs are waiting for
-    bool prep_gate = false;
-    bool prep_used = false;           // prep_stream has work since the last join_side
-    int64_t attn_tail[2] = {-1, -1};  // step whose attention is the last op on attn_st[i]
-    int64_t prep_last = -1;           // step whose prep recorded e_prep last
     VLayout vl{};
     // two-stream step pipeline: the side stream runs prep/lookup/top-k and
     // evict/finalize/select, the caller's (main) stream attention + LRU; step
@@ -647,11 +637,8 @@ struct infllm_engine {
         ck(cudaStreamWaitEvent(st, e_side, 0), "wait");
         ck(cudaEventRecord(e_lrudone, lru_stream), "record");
         ck(cudaStreamWaitEvent(st, e_lrudone, 0), "wait");
-        if (!capturing || prep_used) {  // gated preps run on the attention streams
-            ck(cudaEventRecord(e_prepdone, prep_stream), "record");
-            ck(cudaStreamWaitEvent(st, e_prepdone, 0), "wait");
-        }
-        prep_used = false;
+        ck(cudaEventRecord(e_prepdone, prep_stream), "record");
+        ck(cudaStreamWaitEvent(st, e_prepdone, 0), "wait");
         ck(cudaEventRecord(e_evdone, evict_stream), "record");
         ck(cudaStreamWaitEvent(st, e_evdone, 0), "wait");
         if (tier_seq >= 0 && (capture_seq0 < 0 || tier_seq >= capture_seq0)) {  // only a stream that joined
@@ -662,8 +649,6 @@ struct infllm_engine {
         for (auto& x : lru_seq) x = -1;
         for (auto& a : attn_seq) a = -1;
         attn_last = -1;
-        attn_tail[0] = attn_tail[1] = -1;
-        prep_last = -1;
         lookup_seq = -1;
         evict_seq = -1;
         pipe_dirty = false;
@@ -794,7 +779,7 @@ struct infllm_engine {
             dual = attn_streams > 1 && !one_stream && !coll && lx > 1 && Gs == Gt && tc_eligible(lx);
         const cudaStream_t caller = st;
         cudaStream_t main = dual ? attn_st[kseq & 1] : st, side = one_stream ? st : side_stream,
-                     pst = one_stream ? st : (dual && prep_gate) ? attn_st[kseq & 1] : prep_stream,
+                     pst = one_stream ? st : prep_stream,
                      est = one_stream ? st : evict_stream;
         // decode steps keep the LRU bookkeeping on its own stream (off the critical
         // path: no later prep / lookup / attention reads it), with real events
@@ -802,21 +787,12 @@ struct infllm_engine {
         cudaStream_t lru_st = (one_stream && !lru_side) ? st : lru_stream, tier_st = one_stream ? st : tier_stream;
         if (one_stream && pipe_dirty) join_side(st);  // earlier pipelined steps become upstream of `st`
         pipe_dirty = !one_stream;
-        // prep gate: attention k-2 is the last op on pst (same parity), inside this capture
-        if (dual && prep_gate && attn_tail[kseq & 1] == kseq - 2 && kseq >= 2 &&
-            (capture_seq0 < 0 || kseq - 2 >= capture_seq0)) {
-            launch_gate(pst);
-            ++launches;
-        }
-        if (dual && prep_gate && prep_last >= 0 && (capture_seq0 < 0 || prep_last >= capture_seq0))
-            wt(pst, e_prep);  // the previous step's prep (other stream): prefix rows, key-norm bound
         if (fork) {
             rec(e_call, caller);
             wt(side, e_call);
             wt(pst, e_call);
         }
         if (inputs_ready) wt(pst, inputs_ready);
-        if (pst == prep_stream) prep_used = true;
         if (lru_seq[b] >= 0 && (capture_seq0 < 0 || lru_seq[b] >= capture_seq0)) {
             if (lru_side)
                 ck(cudaStreamWaitEvent(side, e_lru[b], 0), "wait");  // side == caller's stream
@@ -887,7 +863,6 @@ struct infllm_engine {
             launches += (d == 128 && dv == 128 && rep <= 8) ? 3 : 2;
         if (!fused_front) phase_end(kPhScore, evs, st);
         rec(e_prep, pst);
-        prep_last = kseq;
         wt(side, e_prep);
         st = side;
 
@@ -1292,7 +1267,6 @@ struct infllm_engine {
         rec(e_attnp[pb], main);
         attn_seq[pb] = kseq;
         attn_last = kseq;
-        if (dual) attn_tail[kseq & 1] = kseq;
         wt(lru_st, e_attn);
         if (lru_side) {
             ck(cudaEventRecord(e_attn, main), "record");
@@ -1317,8 +1291,6 @@ struct infllm_engine {
                 for (auto& x : lru_seq) x = -1;
             for (auto& a2 : attn_seq) a2 = -1;
             attn_last = -1;
-            attn_tail[0] = attn_tail[1] = -1;
-            prep_last = -1;
             lookup_seq = evict_seq = tier_seq = -1;
         }
         L.trace_count += n_sel;
@@ -1897,7 +1869,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
             k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
-            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority" || k == "prep_gate") {
+            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1914,8 +1886,6 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->multi_stream_decode = value != 0;
         else if (k == "gather_output")
             e->gather_output = value != 0;
-        else if (k == "prep_gate")
-            e->prep_gate = value != 0;
         else if (k == "graph_node_priority")
             e->graph_prio = value != 0;
         else if (k == "attn_streams")

@@ -1745,19 +1745,6 @@ void launch_evict(const EvictParams& p, cudaStream_t st) {
     if (n <= 0) return;
     k_evict_warp<T><<<static_cast<unsigned>((n + kEvWarps - 1) / kEvWarps), kEvWarps * 32, 0, st>>>(p);
 }
-__global__ void k_gate() {}
-void launch_gate(cudaStream_t st) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(32);
-    cfg.stream = st;
-    cudaLaunchAttribute la[1];
-    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = la;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, k_gate);
-}
 template void launch_evict<float>(const EvictParams&, cudaStream_t);
 template void launch_evict<bf16>(const EvictParams&, cudaStream_t);
 

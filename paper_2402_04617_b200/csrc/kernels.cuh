@@ -310,10 +310,6 @@ void launch_mass(const MassParams& p, cudaStream_t st);
 void launch_mass_cta_reduce(const double* mass_cta, double* part, int n_sel, int G, int Gtot, int g0, int rep, int n_mt,
                             cudaStream_t st);
 void launch_lru(const LruParams& p, cudaStream_t st);
-// one-thread kernel launched as a programmatic dependent of the previous
-// kernel on `st` (the engine's prep gate): completes once that kernel's CTAs
-// have all triggered (the tcgen05 attention triggers on entry)
-void launch_gate(cudaStream_t st);
 void launch_tier(const TierParams& p, cudaStream_t st);  // k_tier_assign + k_tier_copy
 template <typename T> void launch_evict(const EvictParams& p, cudaStream_t st);
 void launch_finalize(const FinalizeParams& p, cudaStream_t st);
