@@ -411,13 +411,17 @@ def run_b200(args, rank, world, local_rank):
                          "share_of_step": (attn_ms / (ms / args.steps)) if ms > 0 else None,
                          "timing": "CUDA events around every attention launch on its stream, over a second pass "
                                    "of the same K streams (event nodes perturb the pipeline, so the headline "
-                                   "region has none); achieved = algorithmic QK^T+PV flops / event time",
+                                   "region has none); consecutive launches alternate between two streams and "
+                                   "overlap at the handoff, so the event time is the union of the launches' "
+                                   "[begin, end] intervals; achieved = algorithmic QK^T+PV flops / event time",
                          "peak_src": peaks["src"] + " burst bf16 (sustained %.1f)" % peaks["bf16_sust"],
                          "lookup": {"in_stream_gbs": lk_bytes / (lk_ms / 1000.0) / 1e9 if lk_ms > 0 else None,
                                     "peak_gbs": peaks["hbm"], "bytes_per_stream": lk_bytes,
                                     "in_stream_ms_per_stream": lk_ms,
                                     "note": "in-stream: the lookup shares the GPU with the attention of the previous "
-                                            "step (20 free SMs); isolated: same launch alone, steady state"} | iso},
+                                            "step (20 free SMs); isolated: the last step's lookup launched alone as a "
+                                            "one-token step launches it (whole GPU, graph-replayed); "
+                                            "pipeline_grid_alone: the chunk step's grid launched alone"} | iso},
             "cpu_baseline": cpu,
             "cpu_baseline_all_cores": cpu_all,
             "cpu_reference_c0": cpu_c0,
@@ -448,9 +452,11 @@ def isolated_kernels(eng, steps, H, Hkv, d, dev):
         us = C.c_double()
         _lib.check(_lib.lib().infllm_debug_kernel_bench(eng.h, 1, 50, C.byref(us)))
         b = last["units"] * CFG["n_repr"] * Hkv * d * 2 + last["lx"] * H * d * 2
-        out["isolated_us"] = us.value
+        out["isolated_us"] = us.value  # as a one-token step launches it (whole GPU)
         out["isolated_gbs"] = b / (us.value * 1e-6) / 1e9
         out["isolated_units"] = last["units"]
+        _lib.check(_lib.lib().infllm_debug_kernel_bench(eng.h, 11, 50, C.byref(us)))
+        out["pipeline_grid_alone_us"] = us.value  # the chunk step's few-fat-blocks grid, launched alone
         # standalone lookups on random bf16 indices, timed as CUDA-graph replays
         # (device time, no host gaps): the C3 index (8159 units, 1M-token stream)
         # and a 131072-unit index where the relevance scan is HBM-sized

@@ -400,8 +400,10 @@ int infllm_score_acc_accumulate(infllm_score_acc_t a, const void* q, int64_t l_x
 int infllm_score_acc_finalize_front(infllm_score_acc_t a, int64_t n, float* host_out);
 
 /* Diagnostic: steady-state per-launch time (us) of one kernel family
- * (0 prep, 1 lookup + fused top-k, 2 attention, 3 evict + fused select,
- * 4 LRU) re-launched with the parameters of the engine's last step.
+ * (0 prep, 1 lookup + exact top-k as a one-token step launches it, 2
+ * attention, 3 evict + fused select, 4 LRU, 5 relevance scan only, 6 top-k
+ * only, 11 lookup with the chunk-step in-pipeline grid) re-launched with the
+ * parameters of the engine's last step.
  * Corrupts the engine's stream state: performance investigation only. */
 int infllm_debug_kernel_bench(infllm_engine_t eng, int32_t which, int32_t iters, double* us_per_launch);
 /* Diagnostic: 64 clock64 phase stamps written by instrumented kernels. */

@@ -411,8 +411,8 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restr
 
 int pick_splits(int64_t max_tiles, int G, int B) {
     const int64_t items = static_cast<int64_t>(G) * B;
-    if (items < 148) {  // few sequences: ~one CTA per SM, short splits keep the latency down
-        const int64_t want = (148 + items - 1) / items;
+    if (items < 148) {  // few sequences: one wave of CTAs (<= 148, one per SM), short splits
+        const int64_t want = 148 / items;
         return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, max_tiles, kDecMaxSplits})));
     }
     // a batch (1 CTA per SM): the split count whose CTA total fills its last wave

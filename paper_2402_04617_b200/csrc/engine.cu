@@ -2373,8 +2373,11 @@ int infllm_lookup(const double* qsum, const void* repr, int32_t dtype, int64_t n
 
 // Debug: steady-state duration of one kernel family, re-launched `iters`
 // times (in a CUDA graph) with the parameters of the engine's last step.
-// which: 0 prep, 1 lookup(+fused top-k), 2 attention, 3 evict(+fused select),
-// 4 LRU. Mutates engine state: only for performance investigation.
+// which: 0 prep, 1 lookup (+ exact top-k) as a one-token step launches it,
+// 2 attention, 3 evict (+ fused select), 4 LRU, 5 relevance scan only, 6 top-k
+// only, 7/8 empty kernels, 9/10 fp64/fp32 FMA probes, 11 lookup with the
+// chunk-step (in-pipeline) grid. Mutates engine state: only for performance
+// investigation.
 int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, double* us_per_launch) {
     return guard([&] {
         cudaStream_t st;
@@ -2385,9 +2388,22 @@ int infllm_debug_kernel_bench(infllm_engine_t e, int32_t which, int32_t iters, d
                 case 0:
                     if (e->last_bf16) launch_prep<bf16>(e->last_pp, st); else launch_prep<float>(e->last_pp, st);
                     break;
-                case 1:  // the engine's lookup of the last step, sized as in a decode step (whole GPU)
+                case 1: {  // the last step's lookup as a one-token step runs it (whole GPU):
+                           // k_lookup_reg + fused radix top-k up to 2048 units, else the one-launch scan
+                    LookupParams lp = e->last_lkp;
+                    if (lp.G == lp.Gtot && lp.U <= 256 * 8) {
+                        lp.fused = 1;
+                        launch_lookup(lp, e->last_bf16, st);
+                    } else if (lp.cand_v && lookup_topk_supported(lp, e->last_bf16)) {
+                        launch_lookup_topk_fast(lp, lookup_topk_blocks(lp.U, e->lookup_upb_decode), st);
+                    } else {
+                        launch_lookup(lp, e->last_bf16, st);
+                    }
+                    break;
+                }
+                case 11:  // the chunk-step lookup with its in-pipeline grid (few fat blocks)
                     if (e->last_lkp.cand_v && lookup_topk_supported(e->last_lkp, e->last_bf16))
-                        launch_lookup_topk_fast(e->last_lkp, lookup_topk_blocks(e->last_lkp.U, e->lookup_upb_decode), st);
+                        launch_lookup_topk_fast(e->last_lkp, lookup_topk_blocks(e->last_lkp.U, e->lookup_upb), st);
                     else
                         launch_lookup(e->last_lkp, e->last_bf16, st);
                     break;

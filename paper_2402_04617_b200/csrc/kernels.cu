@@ -1958,11 +1958,12 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
     const int64_t pos = p.s;
     // the d/2 rotation factors of this position, one fp64 sincos per thread in
     // parallel (rotary.hpp:25-30; the large-argument reduction is the slow part)
-    __shared__ float2 s_rc[128];
+    __shared__ float2 s_rc[128], s_cl[128];
     for (int a = threadIdx.x; a < p.d / 2; a += blockDim.x) {
         float c, sn;
         rope_cs(p.freqs, a, pos, c, sn);
         s_rc[a] = make_float2(c, sn);
+        s_cl[a] = make_float2(p.freqs.cL[a], p.freqs.sL[a]);  // lanes index it by dim: no divergent constant loads
     }
     __syncthreads();
     TL_MARK(40, mark);  // rotation factors
@@ -2015,7 +2016,7 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
                 qa.v[2 * j] = from_f<bf16>(y0);
                 qa.v[2 * j + 1] = from_f<bf16>(y1);
                 const int a = 4 * c8 + j;
-                rope_pair(x0, x1, p.freqs.cL[a], p.freqs.sL[a], y0, y1);
+                rope_pair(x0, x1, s_cl[a].x, s_cl[a].y, y0, y1);
                 qc.v[2 * j] = from_f<bf16>(y0);
                 qc.v[2 * j + 1] = from_f<bf16>(y1);
                 qs[2 * j] += static_cast<double>(x0);

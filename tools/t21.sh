@@ -1,0 +1,3 @@
+python tools/decode_timeline.py > gpurun_out/t21_dec.log 2>&1; echo dec_rc=$?
+python tools/decode_timeline.py 524288 > gpurun_out/t21_dec512.log 2>&1; echo dec512_rc=$?
+python -m pytest tests/test_gpu_decode.py tests/test_gpu_parity.py -x -q > gpurun_out/t21_pytest.log 2>&1; echo pytest_rc=$?
