@@ -301,11 +301,25 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
         T* rv = static_cast<T*>(p.ring_v);
         const int R = static_cast<int>(p.R);
         const int sl0 = static_cast<int>((p.s + i0) % p.R);  // one 64-bit division per block
-        for (int t = threadIdx.x; t < 128 * kTokTile; t += blockDim.x) {
-            const int c = t / kTokTile, j = t % kTokTile;
-            const int sl = sl0 + j >= R ? sl0 + j - R : sl0 + j;
-            // [G][R/128][dv][128] pages (VLayout::ring with vt)
-            if (j < nt) rv[((static_cast<int64_t>(g) * (R / 128) + sl / 128) * p.dv + c) * 128 + sl % 128] = svt[c][j];
+        if (sizeof(T) == 2 && nt == kTokTile && sl0 % kTokTile == 0 && p.dv == 128) {
+            // whole 16-aligned tile: the 16 positions of a dim are 32 contiguous bytes
+            // of one page row, written as two 16-byte vectors (thread = dim, half)
+            const int c = threadIdx.x / 2, h = threadIdx.x % 2;
+            if (c < 128) {
+                uint4 w;
+                uint16_t* wv = reinterpret_cast<uint16_t*>(&w);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) wv[e] = reinterpret_cast<const uint16_t*>(&svt[c][8 * h + e])[0];
+                *reinterpret_cast<uint4*>(rv + ((static_cast<int64_t>(g) * (R / 128) + sl0 / 128) * p.dv + c) * 128 +
+                                          sl0 % 128 + 8 * h) = w;
+            }
+        } else {
+            for (int t = threadIdx.x; t < 128 * kTokTile; t += blockDim.x) {
+                const int c = t / kTokTile, j = t % kTokTile;
+                const int sl = sl0 + j >= R ? sl0 + j - R : sl0 + j;
+                // [G][R/128][dv][128] pages (VLayout::ring with vt)
+                if (j < nt) rv[((static_cast<int64_t>(g) * (R / 128) + sl / 128) * p.dv + c) * 128 + sl % 128] = svt[c][j];
+            }
         }
         TL_MARK(13, mark);  // value pages
     }
