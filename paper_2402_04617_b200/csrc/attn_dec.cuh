@@ -19,7 +19,8 @@ struct DecScratch {
     unsigned* cnt;  // [B][G]
     int max_sel;
     int pdl;  // 1: the kernel right before K4 on its stream is the lookup (or its top-k), whose
-              // inputs were complete before it started: K4 may launch as its programmatic dependent
+              // inputs were complete before it started: K4 may launch as its programmatic dependent;
+              // 2: it is the decode front running as the lookup's dependent: every split waits
 };
 inline size_t dec_part_floats(int B, int G, int rep) {
     return static_cast<size_t>(B) * G * kDecMaxSplits * rep * 130;

@@ -330,7 +330,8 @@ struct infllm_engine {
     // so with two streams its CTAs take the SMs attention t frees as they free
     // up instead of queueing behind t's last CTA while side kernels fill them.
     int attn_streams = 2;
-    bool graph_prio = false;  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
+    bool graph_prio = false;
+    bool dec_chain_opt = true;  // option decode_chain  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
     cudaStream_t attn_st[2] = {nullptr, nullptr};
     cudaEvent_t out_free = nullptr;  // host path: the staging buffer `out` points into is drained
     VLayout vl{};
@@ -846,9 +847,20 @@ struct infllm_engine {
         bool fused_front = false;
         if constexpr (std::is_same_v<T, bf16>)
             fused_front = lx == 1 && (one_stream || coll) && dec_front_supported(pp) && page_mode() && Gs == Gt;
+        // decode chain (one-token steps, lookup <= 2048 units): the lookup needs only
+        // this token's q (it forms the group sums itself), so it is launched first and
+        // the fused front follows as its programmatic dependent, overlapping it; the
+        // front and the unit-page copy of a completed unit are issued after the lookup
+        const bool dec_chain = fused_front && one_stream && !coll && !prof && tier_slots == 0 && dec_chain_opt &&
+                               do_lookup && n_sel > 0 && Gs == Gt && L.n_units <= 256 * 8;
+        EvictParams chain_ep{};
+        SelectParams chain_sp{};
+        bool chain_sel = false;
         auto issue_front = [&](const EvictParams& ep2, cudaStream_t s2) {
             if (coll)
                 coll->front.push_back(DecFrontRec{pp, ep2});
+            else if (dec_chain)
+                chain_ep = ep2;
             else
                 launch_dec_front(pp, ep2, s2);
         };
@@ -960,10 +972,14 @@ struct infllm_engine {
                 sp.d = d;
                 sp.l_bs = static_cast<int>(cfg.unit_size);
                 set_page(sp, L, L.pend_start);
-                if (coll)
+                if (coll) {
                     coll->select.push_back(sp);
-                else
+                } else if (dec_chain) {
+                    chain_sp = sp;
+                    chain_sel = true;
+                } else {
                     launch_select<T>(sp, st);
+                }
                 ++launches;
                 for (int64_t c = 0; c < completed; ++c) {
                     L.unit_start.push_back(L.pend_start + c * cfg.unit_size);
@@ -1006,7 +1022,9 @@ struct infllm_engine {
             lp.sel = sel_b;
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
-            lp.early_dependents = one_stream ? 1 : 0;  // decode: K4 follows as a programmatic dependent
+            lp.early_dependents = one_stream ? 1 : 0;  // decode: K4 (or the chained front) follows as a dependent
+            lp.qtok = dec_chain ? q : nullptr;
+            lp.qrep = rep;
             last_lkp = lp;
             if (coll) {  // batched: relevance scan (rel only) + one top-k block per sequence
                 lp.fused = 2;
@@ -1046,6 +1064,13 @@ struct infllm_engine {
             }
             launches += n_lk;
             k4_pdl = one_stream && !coll && !prof && n_sel > 0 && lp.fused != 0;
+            if (dec_chain) {  // the front (and a completed unit's page copy) behind the lookup
+                if (lp.fused != 1) throw StreamError("decode chain: lookup path mismatch");
+                PrepParams pc = pp;
+                pc.dec_chain = 1;
+                launch_dec_front(pc, chain_ep, st);
+                if (chain_sel) launch_select<T>(chain_sp, st);
+            }
             phase_end(kPhLookup, evp, st);
         }
 
@@ -1170,7 +1195,7 @@ struct infllm_engine {
                     coll->attn.push_back(ap);
                 else {
                     DecScratch sc = dec_scratch();
-                    sc.pdl = k4_pdl ? 1 : 0;
+                    sc.pdl = dec_chain ? 2 : k4_pdl ? 1 : 0;
                     launch_attn_dec(ap, sc, st);
                 }
                 ++launches;
@@ -1869,7 +1894,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
             k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
-            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority") {
+            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority" || k == "decode_chain") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1886,6 +1911,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->multi_stream_decode = value != 0;
         else if (k == "gather_output")
             e->gather_output = value != 0;
+        else if (k == "decode_chain")
+            e->dec_chain_opt = value != 0;
         else if (k == "graph_node_priority")
             e->graph_prio = value != 0;
         else if (k == "attn_streams")

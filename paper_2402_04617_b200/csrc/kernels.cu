@@ -437,7 +437,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
     extern __shared__ double sq[];  // [G][qpad(d)]
     const int dp = qpad(p.d);
-    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[(t / p.d) * dp + qpad(t % p.d)] = p.qsum[t];
+    for (int t = threadIdx.x; t < p.G * p.d; t += blockDim.x) sq[(t / p.d) * dp + qpad(t % p.d)] = lk_qsum(p, t);
     __syncthreads();
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t u = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + warp;
@@ -512,17 +512,31 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
     const int lane = threadIdx.x % 32;
     const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int64_t nwarps = static_cast<int64_t>(nblocks) * blockDim.x / 32;
-    double q[8][4];
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
-    for (int64_t u = warp0; u < p.U; u += nwarps) {
+    uint2 x[32];
+    auto load_unit = [&](int64_t u) {
         const bf16* base = static_cast<const bf16*>(p.repr) + u * p.G * 512 + 4 * lane;
-        uint2 x[32];
 #pragma unroll
         for (int r = 0; r < 32; ++r)
             if (r < 4 * p.G) x[r] = __ldcs(reinterpret_cast<const uint2*>(base + r * 128));
+    };
+    if (warp0 < p.U) load_unit(warp0);  // in flight while the query sums are formed
+    double q[8][4];
+    if (p.qtok) {  // decode chain: the token's group query sums, formed once per block
+        __shared__ double s_qs[8 * 128];
+        for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) s_qs[t] = lk_qsum(p, t);
+        __syncthreads();
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? s_qs[g * 128 + 4 * lane + j] : 0.0;
+    } else {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+    }
+    for (int64_t u = warp0; u < p.U; u += nwarps) {
+        if (u != warp0) load_unit(u);
         double rel = 0.0;
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
@@ -591,7 +605,7 @@ __device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nb
 #pragma unroll
     for (int g = 0; g < 8; ++g)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? lk_qsum(p, g * 128 + 4 * lane + j) : 0.0;
     // one bulk copy (TMA engine) per unit row block, completion on a per-(warp, stage) mbarrier
     __shared__ __align__(8) uint64_t sbar[8][kScanStages];
     if (lane == 0)
@@ -2067,8 +2081,12 @@ __device__ __forceinline__ void dec_front_body(const PrepParams& p, const EvictP
     TL_MARK(42, mark);  // eviction of the token leaving the window
 }
 __global__ void __launch_bounds__(256) k_dec_front(PrepParams p, EvictParams ep) {
+    // decode chain: K4 may launch now (it waits for this grid); this grid ends
+    // only after the lookup it overlaps, so K4's wait covers both
+    if (p.dec_chain) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     TL_BEGIN();
     dec_front_body(p, ep, tl_t0_);
+    if (p.dec_chain) asm volatile("griddepcontrol.wait;" ::: "memory");
     TL_END(TL_DEC_FRONT);
 }
 struct DecFront {
@@ -2082,7 +2100,20 @@ bool dec_front_supported(const PrepParams& p) {
     return p.d == 128 && p.dv == 128 && p.rep <= 8 && p.G <= 8 && p.lx == 1 && p.vl.vt;  // one warp per group
 }
 void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t st) {
-    k_dec_front<<<1, 32 * p.G, 0, st>>>(p, ep);
+    if (!p.dec_chain) {
+        k_dec_front<<<1, 32 * p.G, 0, st>>>(p, ep);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the lookup launched just before
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32 * p.G);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_dec_front, p, ep);
 }
 void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st) {
     k_dec_front_b<<<dim3(1, 1, B), 32 * G, 0, st>>>(static_cast<const DecFront*>(tab));

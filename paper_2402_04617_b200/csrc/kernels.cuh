@@ -58,6 +58,8 @@ struct PrepParams {
     double* tsum;        // [lx/16][G][d] per-16-token-tile sums of qs (scratch)
     float* kmax2;             // [G] running max of |k|^2 over every key fed so far (this step's copy)
     const float* kmax2_prev;  // [G] the previous step's copy
+    int dec_chain;  // decode front launched as the lookup's programmatic dependent: lets K4 launch at
+                    // entry, waits for the lookup grid before it exits (K4 waits for the front)
     int64_t s, lx, lxp, R, L;
     int H, G, rep, d, dv;
     VLayout vl;
@@ -77,7 +79,21 @@ struct LookupParams {
     double* cand_v;      // fused 2, streaming scan: per-block top-k candidates [gridDim][n_sel]
     int64_t* cand_i;
     int early_dependents;  // 1: let a programmatic dependent (decode K4) launch at kernel entry
+    // decode: the query sums are formed from the token's q [H][d] (bf16) in the
+    // order the decode front forms them (heads of the group in order from 0.0),
+    // so the lookup does not wait for the front; nullptr: read qsum
+    const void* qtok;
+    int qrep;
 };
+// fp64 query sum of (group, dim) t = g * d + c
+__device__ __forceinline__ double lk_qsum(const LookupParams& p, int t) {
+    if (!p.qtok) return p.qsum[t];
+    const int g = t / p.d, c = t % p.d;
+    const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.qtok) + static_cast<int64_t>(g) * p.qrep * p.d + c;
+    double a = 0.0;
+    for (int hh = 0; hh < p.qrep; ++hh) a += static_cast<double>(__bfloat162float(q[hh * p.d]));
+    return a;
+}
 
 struct TopkParams {
     const double* part;  // [U][Gtot]

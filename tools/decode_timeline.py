@@ -1,6 +1,6 @@
 # Device timeline of single-sequence decode steps at the C2 shape after a prefill
 # of n tokens: per-step kernel spans and idle gaps (is a step GPU- or host-bound?).
-#   python tools/decode_timeline.py [n_tokens] [steps]
+#   python tools/decode_timeline.py [n_tokens] [steps] [opt=val,...]
 import ctypes as C, sys, time, torch, numpy as np
 sys.path.insert(0, '.')
 from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, _lib
@@ -14,6 +14,9 @@ K = torch.randn((n, 8, 128), generator=g, device='cuda').bfloat16()
 V = torch.randn((n, 8, 128), generator=g, device='cuda').bfloat16()
 eng = StreamEngine(EngineConfig.make(**bench.CFG), ModelShape.make(**bench.SHAPE), dtype=torch.bfloat16)
 eng.reserve(n + steps + 64)
+for kv in filter(None, (sys.argv[3] if len(sys.argv) > 3 else "").split(",")):
+    k_, v_ = kv.split("=")
+    eng.set_option(k_, int(v_))
 eng.encode_stream(Q, K, V)
 qd = torch.randn((steps + 16, 1, 32, 128), generator=g, device='cuda').bfloat16()
 kd = torch.randn((steps + 16, 1, 8, 128), generator=g, device='cuda').bfloat16()
