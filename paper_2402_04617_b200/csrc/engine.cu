@@ -852,7 +852,7 @@ struct infllm_engine {
         // the fused front follows as its programmatic dependent, overlapping it; the
         // front and the unit-page copy of a completed unit are issued after the lookup
         const bool dec_chain = fused_front && one_stream && !coll && !prof && tier_slots == 0 && dec_chain_opt &&
-                               do_lookup && n_sel > 0 && Gs == Gt && L.n_units <= 256 * 8;
+                               do_lookup && n_sel > 0 && Gs == Gt;
         EvictParams chain_ep{};
         SelectParams chain_sp{};
         bool chain_sel = false;
@@ -1057,19 +1057,33 @@ struct infllm_engine {
             tp.Gtot = Gt;
             if (!lp.fused) launch_topk(tp, st);
             int n_lk = lp.fused == 1 ? 1 : 2;
+            // decode chain: the front (a programmatic dependent of the scan, waiting for it
+            // before it exits) and a completed unit's page copy go right after the scan
+            struct ChainCtx {
+                PrepParams pp;
+                EvictParams ep;
+                SelectParams sp;
+                bool sel;
+            } cctx{pp, chain_ep, chain_sp, chain_sel};
+            cctx.pp.dec_chain = 1;
+            auto chain_issue = [](void* c, cudaStream_t s2) {
+                auto* x = static_cast<ChainCtx*>(c);
+                launch_dec_front(x->pp, x->ep, s2);
+                if (x->sel) launch_select<T>(x->sp, s2);
+            };
+            bool chain_done = false;
             if (lp.fused == 2 && !coll && !fast) {
                 const int64_t nc = topk_multi_scratch(n_units0, n_sel);  // <= the size ensure_units reserved
                 double* cv = L.cand.as<double>();
-                n_lk = launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st);
+                n_lk = launch_lookup_topk(lp, dtype == INFLLM_DTYPE_BF16, cv, reinterpret_cast<int64_t*>(cv + nc), st,
+                                          dec_chain ? +chain_issue : nullptr, &cctx);
+                chain_done = dec_chain;
             }
             launches += n_lk;
             k4_pdl = one_stream && !coll && !prof && n_sel > 0 && lp.fused != 0;
-            if (dec_chain) {  // the front (and a completed unit's page copy) behind the lookup
+            if (dec_chain && !chain_done) {  // the front (and a completed unit's page copy) behind the lookup
                 if (lp.fused != 1) throw StreamError("decode chain: lookup path mismatch");
-                PrepParams pc = pp;
-                pc.dec_chain = 1;
-                launch_dec_front(pc, chain_ep, st);
-                if (chain_sel) launch_select<T>(chain_sp, st);
+                chain_issue(&cctx, st);
             }
             phase_end(kPhLookup, evp, st);
         }
@@ -1195,7 +1209,7 @@ struct infllm_engine {
                     coll->attn.push_back(ap);
                 else {
                     DecScratch sc = dec_scratch();
-                    sc.pdl = dec_chain ? 2 : k4_pdl ? 1 : 0;
+                    sc.pdl = dec_chain ? 2 : k4_pdl ? 1 : 0;  // behind the chain every split waits
                     launch_attn_dec(ap, sc, st);
                 }
                 ++launches;

@@ -602,10 +602,20 @@ __device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nb
     const int64_t nwarps = blockDim.x / 32;
     const int64_t bytes_u = static_cast<int64_t>(p.G) * 512 * 2;  // one unit's repr rows
     double q[8][4];
+    if (p.qtok) {  // decode chain: the token's group query sums, formed once per block
+        __shared__ double s_qs[8 * 128];
+        for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) s_qs[t] = lk_qsum(p, t);
+        __syncthreads();
 #pragma unroll
-    for (int g = 0; g < 8; ++g)
+        for (int g = 0; g < 8; ++g)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? lk_qsum(p, g * 128 + 4 * lane + j) : 0.0;
+            for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? s_qs[g * 128 + 4 * lane + j] : 0.0;
+    } else {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
+    }
     // one bulk copy (TMA engine) per unit row block, completion on a per-(warp, stage) mbarrier
     __shared__ __align__(8) uint64_t sbar[8][kScanStages];
     if (lane == 0)
@@ -969,7 +979,8 @@ int64_t topk_multi_scratch(int64_t U, int64_t k) {
     const int64_t m = n > 148 * 32 ? n : 148 * 32;  // also the block lists of k_lookup_topk (lookup.cu)
     return (m + 1) / 2 * 2;  // the id half starts 16-byte aligned (bulk copies)
 }
-int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st) {
+int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st,
+                       void (*between)(void*, cudaStream_t), void* ctx) {
     p.fused = 2;
     constexpr int64_t stream_min = 2049;  // past the fused last-block top-k
     if (dtype_bf16 && p.d == 128 && p.r_k == 4 && p.G <= 8 && p.U >= stream_min &&
@@ -986,6 +997,7 @@ int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* 
         p.cand_i = p.n_sel > 0 ? cand_i : nullptr;
         // the merge block follows as a programmatic dependent (a decode step's K4 may launch from it)
         k_lookup_stream<<<kScanBlocks, 256, smem, st>>>(p);
+        if (between) between(ctx, st);
         if (p.n_sel > 0) {
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(1);
@@ -1005,6 +1017,7 @@ int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* 
     p.cand_v = nullptr;
     p.cand_i = nullptr;
     launch_lookup(p, dtype_bf16, st);
+    if (between) between(ctx, st);
     if (p.n_sel > 0 && p.U > 0) return 1 + launch_topk_multi(p.rel, p.U, p.n_sel, cand_v, cand_i, p.sel, st);
     return 1;
 }

@@ -312,7 +312,10 @@ void launch_topk(const TopkParams& p, cudaStream_t st);
 // exact top-k (rel desc, id asc) over rel[U] for large U; scratch of topk_multi_scratch(U, k) entries each
 // lookup (fused == 2) + exact top-k for a single shard; cand_v / cand_i scratch as above
 // returns the number of kernels launched
-int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st);
+// between(ctx, st), when given, is issued right after the relevance scan and
+// before the top-k kernels (the decode chain puts its front there)
+int launch_lookup_topk(LookupParams p, int dtype_bf16, double* cand_v, int64_t* cand_i, cudaStream_t st,
+                       void (*between)(void*, cudaStream_t) = nullptr, void* ctx = nullptr);
 int64_t topk_multi_scratch(int64_t U, int64_t k);
 // lookup.cu: relevance scan + exact top-k (k_m <= 32) in one launch; candidates
 // p.cand_v / p.cand_i hold blocks x 32 entries (within topk_multi_scratch)

@@ -68,6 +68,37 @@ def test_decode_kernel_matches_tc_path():
     assert outs[0][2] == outs[1][2]
 
 
+@pytest.mark.parametrize("n_pre", [8192, 270336])
+def test_decode_chain_matches_sequential_order(n_pre):
+    """The decode chain (lookup first with the query sums formed from q, the
+    front as its programmatic dependent, K4 behind both) against the
+    front -> lookup -> K4 order: the arithmetic is the same, so outputs are
+    bitwise equal; ids, counters and trace identical. C2 head shape, units
+    completing during the decode (every 128 steps). n_pre = 270336: > 2048
+    units, the streaming scan + merge-block lookup with the front between."""
+    from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=2048, init_size=128, n_lookup=16, hot_capacity=32)
+    n_dec = 200
+    g = torch.Generator(device="cuda")
+    g.manual_seed(54)
+    qt = (torch.randn((n_pre + n_dec, 32, 128), generator=g, device="cuda") * 0.5).bfloat16()
+    kt = (torch.randn((n_pre + n_dec, 8, 128), generator=g, device="cuda") * 0.5).bfloat16()
+    vt = torch.randn((n_pre + n_dec, 8, 128), generator=g, device="cuda").bfloat16()
+    runs = []
+    for chain in (1, 0):
+        eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128),
+                           dtype=torch.bfloat16)
+        eng.set_option("decode_chain", chain)
+        eng.reserve(n_pre + n_dec)
+        eng.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
+        o = [eng.decode_step(qt[i:i + 1], kt[i:i + 1], vt[i:i + 1]).clone() for i in range(n_pre, n_pre + n_dec)]
+        runs.append((torch.cat(o), eng.metrics(), eng.trace()))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] == runs[1][2]
+
+
 def test_decode_from_empty_stream():
     """Decode-only stream from token 0 (no units for the first steps, init
     pinning while decoding): the window grows from one key."""
