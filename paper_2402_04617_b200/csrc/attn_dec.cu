@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restr
     for (int i = threadIdx.x; i < static_cast<int>(sizeof(AttnParams) / 4); i += kThr)
         reinterpret_cast<uint32_t*>(&sa)[i] = reinterpret_cast<const uint32_t*>(ps + blockIdx.z)[i];
     __syncthreads();
+    TL_BEGIN();
     dec_body(sa, sc, blockIdx.z, blockIdx.x, gridDim.x);
+    TL_END(TL_DEC);
 }
 
 int pick_splits(int64_t max_tiles, int G, int B) {

@@ -2107,7 +2107,9 @@ struct DecFront {
     EvictParams ep;
 };
 __global__ void __launch_bounds__(256) k_dec_front_b(const DecFront* __restrict__ fs) {
+    TL_BEGIN();
     dec_front_body(fs[blockIdx.z].p, fs[blockIdx.z].ep);
+    TL_END(TL_DEC_FRONT);
 }
 bool dec_front_supported(const PrepParams& p) {
     return p.d == 128 && p.dv == 128 && p.rep <= 8 && p.G <= 8 && p.lx == 1 && p.vl.vt;  // one warp per group
@@ -2153,7 +2155,9 @@ __global__ void __launch_bounds__(256) k_evict_tok_b(const EvictParams* __restri
 __global__ void __launch_bounds__(256) k_select_b(const SelectParams* __restrict__ ps) {
     const SelectParams& p = ps[blockIdx.z];
     if (blockIdx.x >= p.n_units) return;
+    TL_BEGIN();
     select_body<bf16>(p);
+    TL_END(TL_SELECT);
 }
 // streaming relevance scan per sequence slice (8 warps, bulk-copy ring per warp); rel[u] only
 __device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 255) / 256); }
@@ -2170,6 +2174,7 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* 
 constexpr int kScanMaxB = 256;
 __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams* __restrict__ ps, int B) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the top-k blocks may launch (PDL)
+    TL_BEGIN();
     extern __shared__ __align__(16) uint8_t scan_smem[];
     __shared__ int64_t s_off[kScanMaxB + 1];
     __shared__ const uint8_t* s_repr[kScanMaxB];
@@ -2257,15 +2262,22 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
         __syncwarp();  // the stage is refilled next iteration
         stage = (stage + 1) % kScanStages;
     }
+    TL_END(TL_LOOKUP);
 }
 __global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
     // programmatic dependent of the scan: K4 may launch now; the relevance must be complete
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    TL_BEGIN();
     const LookupParams& p = ps[blockIdx.x];
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+    TL_END(TL_TOPK);
 }
-__global__ void __launch_bounds__(256) k_lru_b(const LruParams* __restrict__ ps) { lru_body(ps[blockIdx.x]); }
+__global__ void __launch_bounds__(256) k_lru_b(const LruParams* __restrict__ ps) {
+    TL_BEGIN();
+    lru_body(ps[blockIdx.x]);
+    TL_END(TL_LRU);
+}
 
 void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st) {
     switch (stage) {
