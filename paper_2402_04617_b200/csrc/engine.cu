@@ -716,6 +716,9 @@ struct infllm_engine {
         const int64_t ctas = ((lx + 127) / 128) * static_cast<int64_t>(Hs);
         const int64_t tiles = (ap.init_len + 127) / 128 + ap.n_sel + (ap.s + lx - ap.local_start + 127) / 128 + 2;
         int64_t S = attn_splits > 0 ? attn_splits : 148 / std::max<int64_t>(ctas, 1);
+        // two splits do not pay for the merge and the fp32 partials (G = 2 shards of C2:
+        // 86.0 us per step with, 68.7 without; tools/shard_probe.py)
+        if (attn_splits <= 0 && S < 3) S = 1;
         S = std::clamp<int64_t>(std::min<int64_t>(S, tiles / 4), 1, kMaxSplitsTc);
         if (S > 1) ensure_split_scratch(S);
         return static_cast<int>(S);
