@@ -7,6 +7,7 @@ these sizes would take hours, the oracle (threads over heads) takes minutes.
 
     python tests/golden/make_stream_fixture.py c1   # 64 steps,  ~3 min on 8 cores
     python tests/golden/make_stream_fixture.py c2   # 256 steps, ~12 min on 8 cores
+    python tests/golden/make_stream_fixture.py c4   # the c2 stream + 160 decode steps
 
 BASELINE.json configs[1] (C1, Mistral-7B heads, 32K) and configs[2] (C2,
 Llama-3-8B heads, 128K), exactly as bench.py runs them: 32 q / 8 kv heads,
@@ -105,6 +106,53 @@ def main(name):
 
 COUNTERS = ["units", "hot_units", "peak_hot_units", "hits", "misses", "loads", "evictions", "requested"]
 
+
+C4_DEC = 160  # decode steps after the C2 prefill (a unit completes every 128)
+
+
+def decode_inputs(seed, steps):
+    """One-token q/k/v per decode step, N(0,1) rounded to bf16."""
+    rng = np.random.default_rng(seed)
+    H, Hkv, d = SHAPE["H"], SHAPE["Hkv"], SHAPE["d"]
+    for _ in range(steps):
+        yield (_bf16(rng.standard_normal((1, H, d), dtype=np.float32)),
+               _bf16(rng.standard_normal((1, Hkv, d), dtype=np.float32)),
+               _bf16(rng.standard_normal((1, Hkv, d), dtype=np.float32)))
+
+
+def main_c4():
+    """C4 at 128K: the C2 stream (seed 2) then C4_DEC decode steps (seed 4):
+    per-step ids and output rows of the decode steps, final state."""
+    from oracle import oracle as O
+
+    O.build()
+    n, seed = CASES["c2"]["n"], CASES["c2"]["seed"]
+    eng = O.OracleEngine(O.EngineConfig.make(**CFG),
+                         O.ModelShape.make(n_heads=SHAPE["H"], n_kv_heads=SHAPE["Hkv"], head_dim=SHAPE["d"]),
+                         n_threads=os.cpu_count() or 1)
+    t0 = time.time()
+    for s, (q, k, v) in enumerate(stream_inputs(seed, n)):
+        eng.step(q, k, v)
+        if s % 32 == 0:
+            print(f"c4 prefill step {s} {time.time() - t0:.0f}s", flush=True)
+    ids = np.full((C4_DEC, CFG["n_lookup"]), -1, np.int64)
+    rows = np.zeros((C4_DEC, SHAPE["H"], SHAPE["d"]), np.float32)
+    for s, (q, k, v) in enumerate(decode_inputs(4, C4_DEC)):
+        r = eng.step(q, k, v)
+        ids[s, :len(r.retrieved_ids)] = r.retrieved_ids
+        rows[s] = r.out[0]
+    m = eng.metrics()
+    U = m["units"]
+    infos = [eng.unit_info(u) for u in range(U)]
+    tr = np.array(eng.trace(), np.int64).reshape(-1, 3)
+    np.savez_compressed(
+        os.path.join(HERE, "stream_c4.npz"), n=n, seed=seed, dec_seed=4, ids=ids, rows=rows.astype(np.float16),
+        unit_start=np.array([i["start_abs"] for i in infos], np.int64),
+        unit_size=np.array([i["size"] for i in infos], np.int64),
+        unit_repr=np.array([i["repr_abs"] for i in infos], np.int64).reshape(U, -1),
+        counters=np.array([m[k] for k in COUNTERS], np.int64), trace=tr)
+    print(f"c4: {C4_DEC} decode steps after {n} tokens, {U} units, {len(tr)} trace records, {time.time() - t0:.0f}s; {m}")
+
 if __name__ == "__main__":
-    for nm in sys.argv[1:] or ["c1", "c2"]:
-        main(nm)
+    for nm in sys.argv[1:] or ["c1", "c2", "c4"]:
+        main_c4() if nm == "c4" else main(nm)

@@ -21,6 +21,8 @@ at every step.
   per-step ids come from the trace. Outputs: three oracle rows per step
   (float16 in the fixture: 5e-4 relative rounding against the 2e-2 bar) and
   the per-head mean |out| of every row.
+* test_c4_decode_fixture: configs[4] at 128K for one sequence: the C2 stream
+  then 160 decode steps against tests/golden/stream_c4.npz (oracle).
 """
 import os
 
@@ -28,7 +30,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.golden.make_stream_fixture import CFG, COUNTERS, SHAPE, row_pick, stream_inputs
+from tests.golden.make_stream_fixture import C4_DEC, CFG, COUNTERS, SHAPE, decode_inputs, row_pick, stream_inputs
 from tests.parity_util import compare_state, rel_err
 
 pytestmark = pytest.mark.gpu
@@ -127,3 +129,33 @@ def test_stream_fixture(name):
             worst = max(worst, _check_rows(s, out[s * 512:(s + 1) * 512].float().cpu().numpy(), fx, ridx))
     _check_units_and_counters(geng, fx)
     print(f"{name}: {steps} steps, worst sampled-row rel err {worst:.3e}")
+
+
+def test_c4_decode_fixture():
+    """C4 at 128K (configs[4], one sequence): the C2 stream through
+    encode_stream, then C4_DEC decode_step calls (the decode chain: lookup first,
+    front beside it, K4 behind both) against tests/golden/stream_c4.npz from the
+    oracle: per-step retrieved ids bit-exact, each step's output within 2e-2
+    (||d||_inf / ||ref||_inf over the 32 heads), final unit layout,
+    representatives, counters and trace bit-exact (a unit completes during the
+    decode)."""
+    fx = dict(np.load(os.path.join(GOLD, "stream_c4.npz")))
+    n, seed = int(fx["n"]), int(fx["seed"])
+    geng = _engine()
+    geng.reserve(n + C4_DEC)
+    qs, ks, vs = zip(*stream_inputs(seed, n))
+    q, k, v = (_dev(np.concatenate(x, 0)) for x in (qs, ks, vs))
+    del qs, ks, vs
+    geng.encode_stream(q, k, v)
+    worst = 0.0
+    for s, (dq, dk, dv) in enumerate(decode_inputs(int(fx["dec_seed"]), C4_DEC)):
+        out = geng.decode_step(_dev(dq), _dev(dk), _dev(dv)).float().cpu().numpy()[0]
+        want = [int(x) for x in fx["ids"][s] if x >= 0]
+        got = geng.retrieved_ids()
+        assert got == want, f"decode step {s}: ids {got} vs oracle {want}"
+        e = rel_err(out, fx["rows"][s].astype(np.float32))
+        assert e <= 2e-2, f"decode step {s}: rel err {e:.3e}"
+        worst = max(worst, e)
+    _check_units_and_counters(geng, fx)
+    print(f"c4: {C4_DEC} decode steps after {n} tokens, worst rel err {worst:.3e}")
+
