@@ -126,3 +126,35 @@ def test_tier_option_validation():
     eng.reserve(4096)
     with pytest.raises(InfLLMError):
         eng.set_option("host_tier_slots", 32)  # pools already sized for HBM pages
+
+
+def test_tier_c3_full_size_bitwise():
+    """C3 at its full size (configs[3]: 1M tokens, C2 heads, 32-slot GPU unit
+    cache over the pinned-host store, 8159 units): the graph-replayed stream
+    with the host tier equals the HBM-resident stream bitwise, with identical
+    ids (trace), counters and unit layout. The oracle cannot run 1M tokens in a
+    test; this size-independent property pins the tier at the configuration
+    size (the tier is bookkeeping-only in the reference, memory.hpp:165-168)."""
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=4096, init_size=128, n_lookup=16, hot_capacity=32)
+    n = 1 << 20
+    g = torch.Generator(device="cuda")
+    g.manual_seed(33)
+    q = torch.randn((n, 32, 128), generator=g, device="cuda").bfloat16()
+    k = torch.randn((n, 8, 128), generator=g, device="cuda").bfloat16()
+    v = torch.randn((n, 8, 128), generator=g, device="cuda").bfloat16()
+    outs, metas = [], []
+    for slots in (0, 32):
+        eng = _engine(cfg, 32, 8, 128, torch.bfloat16, slots)
+        eng.reserve(n)
+        out = eng.encode_stream(q, k, v)
+        torch.cuda.synchronize()
+        outs.append(out)
+        metas.append((eng.metrics(), eng.trace(), [eng.unit_info(u)["repr_abs"] for u in range(0, 8159, 97)]))
+        if slots:
+            st = eng.tier_stats()
+            assert st["slots"] == 32 and st["loads"] > 10000  # random queries: the cache mostly misses
+        eng.close()
+    assert torch.equal(outs[0], outs[1])
+    assert metas[0][0] == metas[1][0] and metas[0][0]["units"] == 8159
+    assert metas[0][1] == metas[1][1]
+    assert metas[0][2] == metas[1][2]
