@@ -8,6 +8,7 @@ these sizes would take hours, the oracle (threads over heads) takes minutes.
     python tests/golden/make_stream_fixture.py c1   # 64 steps,  ~3 min on 8 cores
     python tests/golden/make_stream_fixture.py c2   # 256 steps, ~12 min on 8 cores
     python tests/golden/make_stream_fixture.py c4   # the c2 stream + 160 decode steps
+    python tests/golden/make_stream_fixture.py c4_512k   # 512K tokens + 64 decode steps (~1 h)
 
 BASELINE.json configs[1] (C1, Mistral-7B heads, 32K) and configs[2] (C2,
 Llama-3-8B heads, 128K), exactly as bench.py runs them: 32 q / 8 kv heads,
@@ -120,13 +121,16 @@ def decode_inputs(seed, steps):
                _bf16(rng.standard_normal((1, Hkv, d), dtype=np.float32)))
 
 
-def main_c4():
+def main_c4(n=None, seed=None, out="stream_c4.npz", n_dec=None):
     """C4 at 128K: the C2 stream (seed 2) then C4_DEC decode steps (seed 4):
-    per-step ids and output rows of the decode steps, final state."""
+    per-step ids and output rows of the decode steps, final state. With n =
+    524288 (`c4_512k`): the 512K context, whose lookup is the streaming scan."""
     from oracle import oracle as O
 
     O.build()
-    n, seed = CASES["c2"]["n"], CASES["c2"]["seed"]
+    n = n or CASES["c2"]["n"]
+    seed = seed or CASES["c2"]["seed"]
+    C4 = n_dec or C4_DEC
     eng = O.OracleEngine(O.EngineConfig.make(**CFG),
                          O.ModelShape.make(n_heads=SHAPE["H"], n_kv_heads=SHAPE["Hkv"], head_dim=SHAPE["d"]),
                          n_threads=os.cpu_count() or 1)
@@ -135,9 +139,9 @@ def main_c4():
         eng.step(q, k, v)
         if s % 32 == 0:
             print(f"c4 prefill step {s} {time.time() - t0:.0f}s", flush=True)
-    ids = np.full((C4_DEC, CFG["n_lookup"]), -1, np.int64)
-    rows = np.zeros((C4_DEC, SHAPE["H"], SHAPE["d"]), np.float32)
-    for s, (q, k, v) in enumerate(decode_inputs(4, C4_DEC)):
+    ids = np.full((C4, CFG["n_lookup"]), -1, np.int64)
+    rows = np.zeros((C4, SHAPE["H"], SHAPE["d"]), np.float32)
+    for s, (q, k, v) in enumerate(decode_inputs(4, C4)):
         r = eng.step(q, k, v)
         ids[s, :len(r.retrieved_ids)] = r.retrieved_ids
         rows[s] = r.out[0]
@@ -146,13 +150,18 @@ def main_c4():
     infos = [eng.unit_info(u) for u in range(U)]
     tr = np.array(eng.trace(), np.int64).reshape(-1, 3)
     np.savez_compressed(
-        os.path.join(HERE, "stream_c4.npz"), n=n, seed=seed, dec_seed=4, ids=ids, rows=rows.astype(np.float16),
+        os.path.join(HERE, out), n=n, seed=seed, dec_seed=4, n_dec=C4, ids=ids, rows=rows.astype(np.float16),
         unit_start=np.array([i["start_abs"] for i in infos], np.int64),
         unit_size=np.array([i["size"] for i in infos], np.int64),
         unit_repr=np.array([i["repr_abs"] for i in infos], np.int64).reshape(U, -1),
         counters=np.array([m[k] for k in COUNTERS], np.int64), trace=tr)
-    print(f"c4: {C4_DEC} decode steps after {n} tokens, {U} units, {len(tr)} trace records, {time.time() - t0:.0f}s; {m}")
+    print(f"{out}: {C4} decode steps after {n} tokens, {U} units, {len(tr)} trace records, {time.time() - t0:.0f}s; {m}")
 
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["c1", "c2", "c4"]:
-        main_c4() if nm == "c4" else main(nm)
+        if nm == "c4":
+            main_c4()
+        elif nm == "c4_512k":
+            main_c4(n=524288, seed=5, out="stream_c4_512k.npz", n_dec=64)
+        else:
+            main(nm)

@@ -21,8 +21,10 @@ at every step.
   per-step ids come from the trace. Outputs: three oracle rows per step
   (float16 in the fixture: 5e-4 relative rounding against the 2e-2 bar) and
   the per-head mean |out| of every row.
-* test_c4_decode_fixture: configs[4] at 128K for one sequence: the C2 stream
-  then 160 decode steps against tests/golden/stream_c4.npz (oracle).
+* test_c4_decode_fixture: configs[4] for one sequence: at 128K the C2 stream
+  then 160 decode steps (tests/golden/stream_c4.npz), at 512K a 512K-token
+  stream then 64 decode steps (stream_c4_512k.npz: the streaming-scan lookup
+  with the decode front between scan and merge), both from the oracle.
 """
 import os
 
@@ -131,7 +133,8 @@ def test_stream_fixture(name):
     print(f"{name}: {steps} steps, worst sampled-row rel err {worst:.3e}")
 
 
-def test_c4_decode_fixture():
+@pytest.mark.parametrize("fixture", ["stream_c4.npz", "stream_c4_512k.npz"])
+def test_c4_decode_fixture(fixture):
     """C4 at 128K (configs[4], one sequence): the C2 stream through
     encode_stream, then C4_DEC decode_step calls (the decode chain: lookup first,
     front beside it, K4 behind both) against tests/golden/stream_c4.npz from the
@@ -139,16 +142,20 @@ def test_c4_decode_fixture():
     (||d||_inf / ||ref||_inf over the 32 heads), final unit layout,
     representatives, counters and trace bit-exact (a unit completes during the
     decode)."""
-    fx = dict(np.load(os.path.join(GOLD, "stream_c4.npz")))
+    path = os.path.join(GOLD, fixture)
+    if not os.path.exists(path):
+        pytest.skip(f"{fixture} not generated (tests/golden/make_stream_fixture.py)")
+    fx = dict(np.load(path))
     n, seed = int(fx["n"]), int(fx["seed"])
+    n_dec = int(fx["n_dec"]) if "n_dec" in fx else C4_DEC
     geng = _engine()
-    geng.reserve(n + C4_DEC)
+    geng.reserve(n + n_dec)
     qs, ks, vs = zip(*stream_inputs(seed, n))
     q, k, v = (_dev(np.concatenate(x, 0)) for x in (qs, ks, vs))
     del qs, ks, vs
     geng.encode_stream(q, k, v)
     worst = 0.0
-    for s, (dq, dk, dv) in enumerate(decode_inputs(int(fx["dec_seed"]), C4_DEC)):
+    for s, (dq, dk, dv) in enumerate(decode_inputs(int(fx["dec_seed"]), n_dec)):
         out = geng.decode_step(_dev(dq), _dev(dk), _dev(dv)).float().cpu().numpy()[0]
         want = [int(x) for x in fx["ids"][s] if x >= 0]
         got = geng.retrieved_ids()
@@ -157,5 +164,5 @@ def test_c4_decode_fixture():
         assert e <= 2e-2, f"decode step {s}: rel err {e:.3e}"
         worst = max(worst, e)
     _check_units_and_counters(geng, fx)
-    print(f"c4: {C4_DEC} decode steps after {n} tokens, worst rel err {worst:.3e}")
+    print(f"{fixture}: {n_dec} decode steps after {n} tokens, worst rel err {worst:.3e}")
 
