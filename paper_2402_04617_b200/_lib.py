@@ -130,6 +130,7 @@ SIGNATURES = {
     "infllm_kernel_launches": (C.c_int, [P, i64p]),
     "infllm_tier_stats": (C.c_int, [P, i32, i64p]),
     "infllm_decode_batch": (C.c_int, [C.POINTER(C.c_void_p), i32, i32, P, P, P, P, P]),
+    "infllm_debug_host_times": (C.c_int, [P, i32]),
     "infllm_profile_begin": (C.c_int, [P, i32]),
     "infllm_profile_read": (C.c_int, [P, f64p, i64p, f64p, i64p]),
     "infllm_phase_timings": (C.c_int, [P, f64p, i64p]),

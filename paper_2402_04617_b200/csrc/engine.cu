@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -283,13 +284,18 @@ struct BatchCtx {
     int slot = 0;
     DBuf part, mass, cnt;  // K4 batch scratch
     int part_B = 0, mass_B = 0;
-    // the LRU stage runs on its own stream, overlapping the next call's front,
-    // eviction and selection; the next call's lookup waits for it (it rewrites
-    // the selection buffers the LRU reads)
+    // the LRU stage runs on its own stream, overlapping the next calls' work; a
+    // call's lookup rewrites the selection buffer (and its K4 the mass buffer)
+    // the LRU of the call three back read (each engine rotates kSB = 3 buffers,
+    // one step per call), so it waits for that LRU only
     cudaStream_t lru_st = nullptr;
     cudaEvent_t ev_k4 = nullptr;
     std::shared_ptr<SharedEvent> lru_ev;
     bool lru_pending = false;
+    static constexpr int kRing = 3;
+    cudaEvent_t lru_ring[kRing] = {nullptr, nullptr, nullptr};
+    bool ring_set[kRing] = {false, false, false};
+    int64_t calls = 0;
 };
 
 struct infllm_engine {
@@ -1801,6 +1807,8 @@ int infllm_engine_destroy(infllm_engine_t e) {
             for (auto* b : {&e->bctx->part, &e->bctx->mass, &e->bctx->cnt}) b->release(nullptr);
             if (e->bctx->lru_st) cudaStreamDestroy(e->bctx->lru_st);
             if (e->bctx->ev_k4) cudaEventDestroy(e->bctx->ev_k4);
+            for (auto ev : e->bctx->lru_ring)
+                if (ev) cudaEventDestroy(ev);
         }
         delete e;
     });
@@ -2006,9 +2014,27 @@ int infllm_decode_step(infllm_engine_t e, int32_t layer, const void* q, const vo
 // parameter structs, no launches); the parameter tables go to the device in
 // one copy; then prep, eviction, unit selection, lookup + top-k, K4 attention
 // and LRU each launch once with grid.z (or grid.x) = sequence.
+namespace {
+// host time of infllm_decode_batch by section (diagnostic, infllm_debug_host_times)
+double g_dbh[6] = {0, 0, 0, 0, 0, 0};
+inline double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+int infllm_debug_host_times(double* out6, int32_t reset) {
+    return guard([&] {
+        if (out6)
+            for (int i = 0; i < 6; ++i) out6[i] = g_dbh[i];
+        if (reset)
+            for (auto& x : g_dbh) x = 0;
+    });
+}
+
 int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const void* q, const void* k,
                         const void* v, void* out, void* stream) {
     return guard([&] {
+        const double h0 = now_us();
         if (!engs || n < 1) throw ConfigError("decode_batch: no engines");
         auto st = static_cast<cudaStream_t>(stream);
         infllm_engine* e0 = engs[0];
@@ -2040,6 +2066,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         for (int32_t i = 0; i < n; ++i)  // an LRU of another batch context still touching this engine
             if (engs[i]->ext_dep && (!e0->bctx || engs[i]->ext_dep != e0->bctx->lru_ev)) engs[i]->join_ext(st);
         DecodeCollector c;
+        const double h1 = now_us();
         for (int32_t i = 0; i < n; ++i) {
             engs[i]->coll = &c;
             try {
@@ -2051,6 +2078,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             }
             engs[i]->coll = nullptr;
         }
+        const double h2 = now_us();
         if (static_cast<int32_t>(c.prep.size() + c.front.size()) != n || static_cast<int32_t>(c.attn.size()) != n ||
             static_cast<int32_t>(c.lru.size()) != n)
             throw StreamError("decode_batch: unexpected step shape");
@@ -2065,7 +2093,9 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         const size_t o_lk = put(buf, c.lookup), o_at = put(buf, c.attn), o_lru = put(buf, c.lru);
         const int s = bc.slot;
         bc.slot = (bc.slot + 1) % BatchCtx::kSlots;
+        const double h3 = now_us();
         if (bc.done[s]) ck(cudaEventSynchronize(bc.done[s]), "batch slot");  // the batch two calls back
+        const double h4 = now_us();
         if (buf.size() > bc.cap) {
             ck(cudaDeviceSynchronize(), "batch table growth");
             for (int t = 0; t < BatchCtx::kSlots; ++t) {
@@ -2111,7 +2141,8 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
         if (!c.select.empty())
             launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
-        if (bc.lru_pending) ck(cudaStreamWaitEvent(st, bc.lru_ev->ev, 0), "wait");  // the previous call's LRU
+        if (bc.ring_set[bc.calls % BatchCtx::kRing])  // the LRU of the call three back
+            ck(cudaStreamWaitEvent(st, bc.lru_ring[bc.calls % BatchCtx::kRing], 0), "wait");
         if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
@@ -2135,8 +2166,20 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             ck(cudaEventRecord(bc.lru_ev->ev, lst), "record");
             bc.lru_pending = true;
             for (int32_t i = 0; i < n; ++i) engs[i]->ext_dep = bc.lru_ev;
+            const int r = static_cast<int>(bc.calls % BatchCtx::kRing);
+            if (!bc.lru_ring[r]) ck(cudaEventCreateWithFlags(&bc.lru_ring[r], cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(bc.lru_ring[r], lst), "record");
+            bc.ring_set[r] = true;
         }
+        ++bc.calls;
         ck(cudaEventRecord(bc.done[s], lst), "record");  // lst follows everything of this call
+        const double h5 = now_us();
+        g_dbh[0] += h1 - h0;  // argument checks
+        g_dbh[1] += h2 - h1;  // per-sequence step() in collect mode
+        g_dbh[2] += h3 - h2;  // tables
+        g_dbh[3] += h4 - h3;  // wait for the batch two calls back
+        g_dbh[4] += h5 - h4;  // copies and launches
+        g_dbh[5] += 1;
     });
 }
 
