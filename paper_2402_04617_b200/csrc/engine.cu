@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -2015,8 +2016,9 @@ int infllm_decode_step(infllm_engine_t e, int32_t layer, const void* q, const vo
 // one copy; then prep, eviction, unit selection, lookup + top-k, K4 attention
 // and LRU each launch once with grid.z (or grid.x) = sequence.
 namespace {
-// host time of infllm_decode_batch by section (diagnostic, infllm_debug_host_times)
-double g_dbh[6] = {0, 0, 0, 0, 0, 0};
+// host time of infllm_decode_batch by section (diagnostic, infllm_debug_host_times;
+// relaxed atomics: calls from several host threads add up without a data race)
+std::atomic<double> g_dbh[6];
 inline double now_us() {
     return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -2025,9 +2027,9 @@ inline double now_us() {
 int infllm_debug_host_times(double* out6, int32_t reset) {
     return guard([&] {
         if (out6)
-            for (int i = 0; i < 6; ++i) out6[i] = g_dbh[i];
+            for (int i = 0; i < 6; ++i) out6[i] = g_dbh[i].load(std::memory_order_relaxed);
         if (reset)
-            for (auto& x : g_dbh) x = 0;
+            for (auto& x : g_dbh) x.store(0.0, std::memory_order_relaxed);
     });
 }
 
@@ -2174,12 +2176,13 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         ++bc.calls;
         ck(cudaEventRecord(bc.done[s], lst), "record");  // lst follows everything of this call
         const double h5 = now_us();
-        g_dbh[0] += h1 - h0;  // argument checks
-        g_dbh[1] += h2 - h1;  // per-sequence step() in collect mode
-        g_dbh[2] += h3 - h2;  // tables
-        g_dbh[3] += h4 - h3;  // wait for the batch two calls back
-        g_dbh[4] += h5 - h4;  // copies and launches
-        g_dbh[5] += 1;
+        const double parts[6] = {h1 - h0,   // argument checks
+                                 h2 - h1,   // per-sequence step() in collect mode
+                                 h3 - h2,   // tables
+                                 h4 - h3,   // wait for the batch two calls back
+                                 h5 - h4,   // copies and launches
+                                 1.0};
+        for (int i = 0; i < 6; ++i) g_dbh[i].fetch_add(parts[i], std::memory_order_relaxed);
     });
 }
 
