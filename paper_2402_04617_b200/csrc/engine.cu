@@ -1743,7 +1743,7 @@ int infllm_engine_create(const infllm_engine_config* cfg, const infllm_model_sha
         e->topk_done.alloc(sizeof(unsigned int), st);
         e->evict_done.alloc(sizeof(unsigned int), st);
         e->rtab.alloc(static_cast<size_t>(cfg->chunk_size) * std::max(1, e->d / 2) * sizeof(float2), st);
-        e->tsum.alloc(static_cast<size_t>((cfg->chunk_size + 15) / 16) * e->Gs * e->d * sizeof(double), st);
+        e->tsum.alloc(static_cast<size_t>((cfg->chunk_size + kTokTile - 1) / kTokTile) * e->Gs * e->d * sizeof(double), st);
         e->qsb.alloc(static_cast<size_t>(cfg->chunk_size) * e->Gs * e->d * sizeof(double), st);
         e->mass_cta_half = static_cast<int64_t>(e->Hs) * (e->lxp / 128) * km;
         e->mass_cta.alloc(infllm_engine::kSB * e->mass_cta_half * sizeof(double), st);

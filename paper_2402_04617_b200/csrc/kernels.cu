@@ -199,7 +199,6 @@ __device__ __forceinline__ void st8(T* p, const V8<T>& r) {
 // (256 B each); value pages are transposed through shared memory; the fp64
 // group query sums go to qs[token][g][:] plus a per-tile column sum.
 // RP: query heads per KV group when known at compile time (0: p.rep <= 8).
-constexpr int kTokTile = 16;
 template <typename T, int RP>
 __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g, unsigned long long& mark) {
     __shared__ double sqs[kTokTile][128 + 2];
@@ -302,9 +301,10 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
         const int R = static_cast<int>(p.R);
         const int sl0 = static_cast<int>((p.s + i0) % p.R);  // one 64-bit division per block
         if (sizeof(T) == 2 && nt == kTokTile && sl0 % kTokTile == 0 && p.dv == 128) {
-            // whole 16-aligned tile: the 16 positions of a dim are 32 contiguous bytes
-            // of one page row, written as two 16-byte vectors (thread = dim, half)
-            const int c = threadIdx.x / 2, h = threadIdx.x % 2;
+            // whole aligned tile: the kTokTile positions of a dim are contiguous bytes
+            // of one page row, written as 16-byte vectors of 8 (thread = dim, eighth)
+            constexpr int hs = kTokTile / 8;
+            const int c = threadIdx.x / hs, h = threadIdx.x % hs;
             if (c < 128) {
                 uint4 w;
                 uint16_t* wv = reinterpret_cast<uint16_t*>(&w);
@@ -326,7 +326,7 @@ __device__ __forceinline__ void prep_tok_body(const PrepParams& p, int bx, int g
 }
 
 template <typename T, int RP>
-__global__ void __launch_bounds__(256, RP == 4 ? 3 : 1) k_prep_tok(PrepParams p) {
+__global__ void __launch_bounds__(kTokTile * 16, RP == 4 ? 48 / kTokTile : 1) k_prep_tok(PrepParams p) {
     TL_BEGIN();
     unsigned long long mark = tl_t0_;
     const int tiles = static_cast<int>((p.lx + kTokTile - 1) / kTokTile);
@@ -391,9 +391,9 @@ void launch_prep(const PrepParams& p, cudaStream_t st) {
         const unsigned items = tiles * static_cast<unsigned>(p.G);
         k_rope_table<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, st>>>(p);
         if (p.rep == 4)
-            k_prep_tok<T, 4><<<items, 256, 0, st>>>(p);
+            k_prep_tok<T, 4><<<items, kTokTile * 16, 0, st>>>(p);
         else
-            k_prep_tok<T, 0><<<items, 256, 0, st>>>(p);
+            k_prep_tok<T, 0><<<items, kTokTile * 16, 0, st>>>(p);
         k_prefix_tiles<T><<<items, 128, 0, st>>>(p);
         return;
     }
@@ -2140,7 +2140,7 @@ size_t dec_front_size() { return sizeof(DecFront); }
 __global__ void k_rope_table_b(const PrepParams* __restrict__ ps) {
     rope_table_body(ps[blockIdx.z], static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x);
 }
-__global__ void __launch_bounds__(256) k_prep_tok_b(const PrepParams* __restrict__ ps) {
+__global__ void __launch_bounds__(kTokTile * 16) k_prep_tok_b(const PrepParams* __restrict__ ps) {
     unsigned long long mark = 0;
     prep_tok_body<bf16, 0>(ps[blockIdx.z], blockIdx.x, blockIdx.y, mark);
 }
@@ -2284,7 +2284,7 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
         case 0: {  // K7 prep of one token per sequence (the chunk-path kernels, l_x = 1)
             const PrepParams* ps = static_cast<const PrepParams*>(tab);
             k_rope_table_b<<<dim3(1, 1, B), 256, 0, st>>>(ps);
-            k_prep_tok_b<<<dim3(1, static_cast<unsigned>(gx), B), 256, 0, st>>>(ps);
+            k_prep_tok_b<<<dim3(1, static_cast<unsigned>(gx), B), kTokTile * 16, 0, st>>>(ps);
             k_prefix_tiles_b<<<dim3(1, static_cast<unsigned>(gx), B), 128, 0, st>>>(ps);
             break;
         }

@@ -42,6 +42,8 @@ struct VLayout {
     }
 };
 
+// tokens per k_prep_tok block (x 16 threads: one per 8-dim chunk of a token)
+constexpr int kTokTile = 16;
 struct PrepParams {
     const void* q;  // [lx][H][d]
     const void* k;  // [lx][G][d]

@@ -1,0 +1,1 @@
+python tools/lib_ab.py paper_2402_04617_b200/libinfllm_b200.so tmp_libs/libtile32.so > gpurun_out/t60_ab.log 2>&1; echo ab_rc=$?
