@@ -133,7 +133,8 @@ __device__ __forceinline__ void dec_load(const AttnParams& a, const DecTile& tl,
     tc::tma_load_2d(tm + mv, bar, sb + kMatB + kBoxB, 64, rv);
 }
 
-__device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& sc, int b, int x, int nsplit) {
+__device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& sc, int b, int x, int nsplit,
+                                         unsigned long long& mark) {
     extern __shared__ __align__(1024) uint8_t dsm_raw[];
     uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
     __shared__ float sred[kW][kDecMaxRep], sl_red[kW][kDecMaxRep];
@@ -170,6 +171,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     __syncthreads();
     const int g = blockIdx.y, rep = a.rep;
     const float sl2 = a.scale * kLog2e;
+    TL_MARK(50, mark);  // dependencies met, stages initialised
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));  // 1024-aligned
 
     for (int st = 0; st < kStages - 1; ++st)  // prefetch the first tiles
@@ -280,6 +282,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
         }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    TL_MARK(51, mark);  // tiles attended
     // ---- this split's partial (m, l, O) per head: the warps' online softmaxes merged ----
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
     lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
@@ -328,6 +331,7 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     unsigned* cnt = sc.cnt + static_cast<int64_t>(b) * a.G + g;
     if (tid == 0) s_last = atomicAdd(cnt, 1u) == static_cast<unsigned>(nsplit - 1);
     __syncthreads();
+    TL_MARK(52, mark);  // partial published
     if (!s_last) {
         if (s_last && tid == 0) *cnt = 0;
         return;
@@ -393,11 +397,13 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
         a.mass_part[static_cast<int64_t>(tid) * a.Gtot + a.g0 + g] = msum;
     }
     if (tid == 0) *cnt = 0;
+    TL_MARK(53, mark);  // splits merged (the group's last split)
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch sc) {
     TL_BEGIN();
-    dec_body(a, sc, 0, blockIdx.x, gridDim.x);
+    unsigned long long mark = tl_t0_;
+    dec_body(a, sc, 0, blockIdx.x, gridDim.x, mark);
     TL_END(TL_DEC);
 }
 
@@ -409,7 +415,8 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restr
         reinterpret_cast<uint32_t*>(&sa)[i] = reinterpret_cast<const uint32_t*>(ps + blockIdx.z)[i];
     __syncthreads();
     TL_BEGIN();
-    dec_body(sa, sc, blockIdx.z, blockIdx.x, gridDim.x);
+    unsigned long long mark = tl_t0_;
+    dec_body(sa, sc, blockIdx.z, blockIdx.x, gridDim.x, mark);
     TL_END(TL_DEC);
 }
 
