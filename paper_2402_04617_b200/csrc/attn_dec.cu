@@ -325,6 +325,10 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
         for (int w = 0; w < kW; ++w) v = fmaf(so[(w * rep + h) * 128 + c], sred[w][h], v);
         part[h * 130 + 2 + c] = v;
     }
+    if (sc.sep_merge) {  // k_dec_merge combines the splits
+        TL_MARK(52, mark);  // partial published
+        return;
+    }
     // ---- the last split of (sequence, group) merges ----
     __threadfence();
     __syncthreads();
@@ -400,7 +404,116 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     TL_MARK(53, mark);  // splits merged (the group's last split)
 }
 
+// Split merge as its own launch (sep_merge): block (head h < rep, group, sequence)
+// with thread = value dim combines that head's nsplit partials, block h = rep
+// the group's retrieved-unit masses; the arithmetic and its order are the last
+// split's merge below (max and denominator over splits in order, weights, then
+// one fma per split in order), so the outputs are bitwise the same.
+__device__ __forceinline__ void dec_merge_body(const AttnParams& a, const DecScratch& sc, int b, int g, int hsel,
+                                               int nsplit) {
+    const int tid = threadIdx.x, rep = a.rep;
+    const int64_t stride = static_cast<int64_t>(rep) * 130;
+    const float* p0 = sc.part + (static_cast<int64_t>(b) * a.G + g) * nsplit * stride;
+    __shared__ float s_w[kDecMaxSplits][kDecMaxRep], s_ls[kDecMaxSplits][kDecMaxRep];
+    __shared__ float s_M[kDecMaxRep], s_L[kDecMaxRep];
+    const bool masses = hsel == rep;
+    const int h_lo = masses ? 0 : hsel, h_n = masses ? rep : 1;
+    for (int i = tid; i < nsplit * h_n; i += blockDim.x) {
+        const int xs = i / h_n, h = h_lo + i % h_n;
+        s_w[xs][h] = __ldcg(p0 + xs * stride + h * 130);
+        s_ls[xs][h] = __ldcg(p0 + xs * stride + h * 130 + 1);
+    }
+    // this thread's O values (all splits of its dim), issued with the (m, l) loads
+    constexpr int kPre = 32;
+    float ov[kPre];
+    if (!masses) {
+#pragma unroll
+        for (int u = 0; u < kPre; ++u) ov[u] = u < nsplit ? __ldcg(p0 + u * stride + hsel * 130 + 2 + tid) : 0.f;
+    }
+    __syncthreads();
+    if (tid < h_n) {
+        const int h = h_lo + tid;
+        float M = -INFINITY;
+        for (int xs = 0; xs < nsplit; ++xs) M = fmaxf(M, s_w[xs][h]);
+        float L = 0.f;
+        for (int xs = 0; xs < nsplit; ++xs) {
+            const float mx = s_w[xs][h];
+            if (mx != -INFINITY) L += s_ls[xs][h] * ex2f(mx - M);
+        }
+        s_M[h] = M;
+        s_L[h] = L;
+        if (!masses && a.inv_violations && !(L > 0.f && isfinite(L))) atomicAdd(a.inv_violations, 1ull);
+    }
+    __syncthreads();
+    if (masses) {  // the group's heads' normalised weights of each unit's keys, summed (engine.hpp:271-283)
+        if (a.want_mass && a.mass_part)
+            for (int u = tid; u < a.n_sel; u += blockDim.x) {
+                double msum = 0.0;
+                for (int h = 0; h < rep; ++h) {
+                    const float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + h) * sc.max_sel + u) * kW * 2;
+                    float rec[2 * kW];
+#pragma unroll
+                    for (int i = 0; i < 2 * kW; ++i) rec[i] = __ldcg(mr + i);
+                    float e = 0.f;
+#pragma unroll
+                    for (int w = 0; w < kW; ++w)
+                        e += rec[2 * w + 1] == -INFINITY ? 0.f : rec[2 * w] * ex2f(rec[2 * w + 1] - s_M[h]);
+                    msum += static_cast<double>(e / s_L[h]);
+                }
+                a.mass_part[static_cast<int64_t>(u) * a.Gtot + a.g0 + g] = msum;
+            }
+        return;
+    }
+    for (int xs = tid; xs < nsplit; xs += blockDim.x) {
+        const float mx = s_w[xs][hsel];
+        s_w[xs][hsel] = mx == -INFINITY ? 0.f : ex2f(mx - s_M[hsel]) / s_L[hsel];
+    }
+    __syncthreads();
+    float acc = 0.f;
+    for (int x0 = 0; x0 < nsplit; x0 += 32) {
+        float o2[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+            o2[u] = x0 == 0 ? ov[u] : (x0 + u < nsplit ? __ldcg(p0 + (x0 + u) * stride + hsel * 130 + 2 + tid) : 0.f);
+#pragma unroll
+        for (int u = 0; u < 32; ++u)
+            if (x0 + u < nsplit) acc = fmaf(o2[u], s_w[x0 + u][hsel], acc);
+    }
+    static_cast<bf16*>(a.out)[static_cast<int64_t>(g * rep + hsel) * a.dv + tid] = __float2bfloat16_rn(acc);
+}
+__global__ void __launch_bounds__(128) k_dec_merge1(AttnParams a, DecScratch sc, int nsplit) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // K4's partials
+    TL_BEGIN();
+    dec_merge_body(a, sc, 0, blockIdx.y, blockIdx.x, nsplit);
+    TL_END(TL_MASS);
+}
+__global__ void __launch_bounds__(128) k_dec_mergeb(const AttnParams* __restrict__ ps, DecScratch sc, int nsplit) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const AttnParams& a = ps[blockIdx.z];
+    if (static_cast<int>(blockIdx.x) > a.rep) return;
+    TL_BEGIN();
+    dec_merge_body(a, sc, blockIdx.z, blockIdx.y, blockIdx.x, nsplit);
+    TL_END(TL_MASS);
+}
+void launch_dec_merge(const AttnParams* host_a, const AttnParams* dev_params, int B, int G, int rep, int nsplit,
+                      const DecScratch& sc, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of K4 (which lets it launch on entry)
+    cfg.gridDim = dim3(rep + 1, G, B);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    if (host_a)
+        cudaLaunchKernelEx(&cfg, k_dec_merge1, *host_a, sc, nsplit);
+    else
+        cudaLaunchKernelEx(&cfg, k_dec_mergeb, dev_params, sc, nsplit);
+}
+
 __global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch sc) {
+    if (sc.sep_merge) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_dec_merge1
     TL_BEGIN();
     unsigned long long mark = tl_t0_;
     dec_body(a, sc, 0, blockIdx.x, gridDim.x, mark);
@@ -408,6 +521,7 @@ __global__ void __launch_bounds__(kThr, 1) k_attn_dec1(AttnParams a, DecScratch 
 }
 
 __global__ void __launch_bounds__(kThr, 1) k_attn_decb(const AttnParams* __restrict__ ps, DecScratch sc) {
+    if (sc.sep_merge) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // k_dec_mergeb
     // this sequence's parameters in shared memory (read all through the tile loop)
     __shared__ __align__(16) AttnParams sa;
     static_assert(sizeof(AttnParams) % 4 == 0, "word copy");
@@ -486,6 +600,7 @@ void launch_attn_dec(const AttnParams& a, const DecScratch& sc0, cudaStream_t st
     cfg.attrs = la;
     cfg.numAttrs = sc.pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_attn_dec1, a, sc);
+    if (sc.sep_merge) launch_dec_merge(&a, nullptr, 1, a.G, a.rep, ns, sc, st);
 }
 
 void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t max_tiles, const DecScratch& sc,
@@ -505,6 +620,7 @@ void launch_attn_dec_batch(const AttnParams* dev_params, int B, int G, int64_t m
     cfg.attrs = la;
     cfg.numAttrs = sc.pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, k_attn_decb, dev_params, s2);
+    if (sc.sep_merge) launch_dec_merge(nullptr, dev_params, B, G, kDecMaxRep, ns, sc, st);
 }
 
 }  // namespace infllm

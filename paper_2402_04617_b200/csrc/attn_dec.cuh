@@ -21,6 +21,9 @@ struct DecScratch {
     int pdl;  // 1: the kernel right before K4 on its stream is the lookup (or its top-k), whose
               // inputs were complete before it started: K4 may launch as its programmatic dependent;
               // 2: it is the decode front running as the lookup's dependent: every split waits
+    int sep_merge;  // 1: the splits only publish their partials; k_dec_merge (launched right
+                    // after K4, its programmatic dependent) merges every (sequence, group, head)
+                    // in parallel instead of the group's last split alone
 };
 inline size_t dec_part_floats(int B, int G, int rep) {
     return static_cast<size_t>(B) * G * kDecMaxSplits * rep * 130;

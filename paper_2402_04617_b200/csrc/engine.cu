@@ -338,7 +338,8 @@ struct infllm_engine {
     // up instead of queueing behind t's last CTA while side kernels fill them.
     int attn_streams = 2;
     bool graph_prio = false;
-    bool dec_chain_opt = true;  // option decode_chain  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
+    bool dec_chain_opt = true;  // option decode_chain
+    bool dec_merge_opt = true;  // option decode_merge_kernel: K4's split merge as its own parallel launch  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
     cudaStream_t attn_st[2] = {nullptr, nullptr};
     cudaEvent_t out_free = nullptr;  // host path: the staging buffer `out` points into is drained
     VLayout vl{};
@@ -1220,7 +1221,9 @@ struct infllm_engine {
                 else {
                     DecScratch sc = dec_scratch();
                     sc.pdl = dec_chain ? 2 : k4_pdl ? 1 : 0;  // behind the chain every split waits
+                    sc.sep_merge = dec_merge_opt ? 1 : 0;
                     launch_attn_dec(ap, sc, st);
+                    if (sc.sep_merge) ++launches;  // k_dec_merge1
                 }
                 ++launches;
             } else if (tc_eligible(lx)) {
@@ -1940,7 +1943,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         // drop them so the next encode_stream recaptures with the new setting
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
             k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
-            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority" || k == "decode_chain") {
+            k == "gather_output" || k == "attn_streams" || k == "graph_node_priority" || k == "decode_chain" ||
+            k == "decode_merge_kernel") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1959,6 +1963,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->gather_output = value != 0;
         else if (k == "decode_chain")
             e->dec_chain_opt = value != 0;
+        else if (k == "decode_merge_kernel")
+            e->dec_merge_opt = value != 0;
         else if (k == "graph_node_priority")
             e->graph_prio = value != 0;
         else if (k == "attn_streams")
@@ -2148,7 +2154,8 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
-                                         0},  // programmatic launch measured no better for the batch
+                                         0,  // programmatic launch measured no better for the batch
+                                         e0->dec_merge_opt ? 1 : 0},
                               st);
         cudaStream_t lst = st;
         {
