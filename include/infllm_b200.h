@@ -181,7 +181,9 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * attention's launch priority; default 0), "decode_chain" (1 = a one-token
  * step launches the lookup first, forming the query sums from q itself, with
  * the decode front as its programmatic dependent and K4 behind both; default;
- * 0 = front, lookup, K4 in sequence), "lookup_units_per_block" /
+ * 0 = front, lookup, K4 in sequence), "decode_merge_kernel" (1 = the
+ * decode attention's split merge as its own parallel launch, default; 0 = in
+ * each group's last split), "lookup_units_per_block" /
  * "lookup_units_per_block_decode" (K1+K2 grid: units per block in chunk /
  * one-token steps), "gather_output" (sharded engines: all-gather every head's
  * output into `out`). Options that change launches drop captured graphs. */

@@ -99,6 +99,35 @@ def test_decode_chain_matches_sequential_order(n_pre):
     assert runs[0][2] == runs[1][2]
 
 
+@pytest.mark.parametrize("batch", [1, 3])
+def test_decode_merge_kernel_matches_last_split_merge(batch):
+    """K4's split merge as its own launch (decode_merge_kernel = 1) against the
+    merge in each group's last split: same arithmetic in the same order, so
+    outputs are bitwise equal and masses (hence counters and trace) identical."""
+    from paper_2402_04617_b200 import decode_batch
+
+    cfg = dict(chunk_size=512, unit_size=128, n_repr=4, local_size=2048, init_size=128, n_lookup=16, hot_capacity=32)
+    runs = []
+    for mk in (1, 0):
+        engs, data = _prefilled(cfg, 6144, list(range(60, 60 + batch)), H=32, Hkv=8)
+        for e in engs:
+            e.set_option("decode_merge_kernel", mk)
+        outs = []
+        for t in range(150):
+            if batch == 1:
+                qt, kt, vt = data[0]
+                outs.append(engs[0].decode_step(qt[6144 + t:6145 + t], kt[6144 + t:6145 + t], vt[6144 + t:6145 + t]).clone())
+            else:
+                q = torch.stack([d[0][6144 + t] for d in data]).contiguous()
+                k = torch.stack([d[1][6144 + t] for d in data]).contiguous()
+                v = torch.stack([d[2][6144 + t] for d in data]).contiguous()
+                outs.append(decode_batch(engs, q, k, v).clone())
+        runs.append((torch.stack(outs), [e.metrics() for e in engs], [e.trace() for e in engs]))
+    assert torch.equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+    assert runs[0][2] == runs[1][2]
+
+
 def test_decode_from_empty_stream():
     """Decode-only stream from token 0 (no units for the first steps, init
     pinning while decoding): the window grows from one key."""
