@@ -446,10 +446,13 @@ __device__ __forceinline__ void dec_merge_body(const AttnParams& a, const DecScr
     }
     __syncthreads();
     if (masses) {  // the group's heads' normalised weights of each unit's keys, summed (engine.hpp:271-283)
-        if (a.want_mass && a.mass_part)
-            for (int u = tid; u < a.n_sel; u += blockDim.x) {
-                double msum = 0.0;
-                for (int h = 0; h < rep; ++h) {
+        if (a.want_mass && a.mass_part) {
+            // one thread per (unit, head) record, then per unit the heads summed in order
+            __shared__ float s_e[128];
+            for (int u0 = 0; u0 < a.n_sel; u0 += blockDim.x / rep) {
+                const int u = u0 + tid / rep, h = tid % rep;
+                const bool on = tid < (blockDim.x / rep) * rep && u < a.n_sel;
+                if (on) {
                     const float* mr = sc.mass + ((static_cast<int64_t>(b) * a.H + g * rep + h) * sc.max_sel + u) * kW * 2;
                     float rec[2 * kW];
 #pragma unroll
@@ -458,10 +461,17 @@ __device__ __forceinline__ void dec_merge_body(const AttnParams& a, const DecScr
 #pragma unroll
                     for (int w = 0; w < kW; ++w)
                         e += rec[2 * w + 1] == -INFINITY ? 0.f : rec[2 * w] * ex2f(rec[2 * w + 1] - s_M[h]);
-                    msum += static_cast<double>(e / s_L[h]);
+                    s_e[tid] = e / s_L[h];
                 }
-                a.mass_part[static_cast<int64_t>(u) * a.Gtot + a.g0 + g] = msum;
+                __syncthreads();
+                if (on && h == 0) {
+                    double msum = 0.0;
+                    for (int hh = 0; hh < rep; ++hh) msum += static_cast<double>(s_e[tid + hh]);
+                    a.mass_part[static_cast<int64_t>(u) * a.Gtot + a.g0 + g] = msum;
+                }
+                __syncthreads();
             }
+        }
         return;
     }
     for (int xs = tid; xs < nsplit; xs += blockDim.x) {

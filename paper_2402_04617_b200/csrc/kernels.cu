@@ -412,7 +412,7 @@ template void launch_prep<bf16>(const PrepParams&, cudaStream_t);
 // xor-tree: the association does not depend on how groups are sharded. In the
 // single-shard (fused) mode the warp sums the groups in order 0..G-1 into
 // rel[u] and the last block to finish runs the exact top-k (K2) over all units.
-__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out);
+__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out, unsigned long long* mk = nullptr);
 
 __device__ __forceinline__ int qpad(int c);
 template <typename T, int kPer>
@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(256) k_lookup(LookupParams p) {
 // Single shard: per lane the groups are summed in order 0..G-1, then one warp
 // tree; sharded: one warp tree per group (partials exchanged by the caller).
 __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nblocks) {
+    unsigned long long mark = threadIdx.x == 0 ? gtimer() : 0ull;
     const int lane = threadIdx.x % 32;
     const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
     const int64_t nwarps = static_cast<int64_t>(nblocks) * blockDim.x / 32;
@@ -519,11 +520,41 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
         for (int r = 0; r < 32; ++r)
             if (r < 4 * p.G) x[r] = __ldcs(reinterpret_cast<const uint2*>(base + r * 128));
     };
+    // decode chain: this thread's slice of the token's query rows is requested
+    // before the first unit, so it is not queued behind 64 KB of unit loads
+    uint2 qv[8];
+    const bool qpre = p.qtok && p.qrep <= 8 && p.G * 32 <= static_cast<int>(blockDim.x) &&
+                      !(reinterpret_cast<uintptr_t>(p.qtok) & 7);
+    const int qg = threadIdx.x / 32, qc = lane * 4;
+    if (qpre && qg < p.G) {
+        const uint2* qq = reinterpret_cast<const uint2*>(static_cast<const bf16*>(p.qtok) +
+                                                         static_cast<int64_t>(qg) * p.qrep * 128 + qc);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < p.qrep) qv[j] = qq[j * 32];
+    }
     if (warp0 < p.U) load_unit(warp0);  // in flight while the query sums are formed
     double q[8][4];
     if (p.qtok) {  // decode chain: the token's group query sums, formed once per block
         __shared__ double s_qs[8 * 128];
-        for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) s_qs[t] = lk_qsum(p, t);
+        if (!qpre) {
+            lk_stage_qsums(p, s_qs);
+        } else if (qg < p.G) {  // head order, as lk_qsum
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < p.qrep) {
+                    a0 += static_cast<double>(__uint_as_float(qv[j].x << 16));
+                    a1 += static_cast<double>(__uint_as_float(qv[j].x & 0xffff0000u));
+                    a2 += static_cast<double>(__uint_as_float(qv[j].y << 16));
+                    a3 += static_cast<double>(__uint_as_float(qv[j].y & 0xffff0000u));
+                }
+            double* o = s_qs + qg * 128 + qc;
+            o[0] = a0;
+            o[1] = a1;
+            o[2] = a2;
+            o[3] = a3;
+        }
         __syncthreads();
 #pragma unroll
         for (int g = 0; g < 8; ++g)
@@ -535,6 +566,7 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
 #pragma unroll
             for (int j = 0; j < 4; ++j) q[g][j] = g < p.G ? p.qsum[g * 128 + 4 * lane + j] : 0.0;
     }
+    TL_MARK(20, mark);  // query sums in registers
     for (int64_t u = warp0; u < p.U; u += nwarps) {
         if (u != warp0) load_unit(u);
         double rel = 0.0;
@@ -563,14 +595,22 @@ __device__ __forceinline__ void lookup_reg_body(const LookupParams& p, int nbloc
         }
     }
     if (p.fused != 1) return;
+    // arrival: the barrier orders the block's relevance stores before thread 0's
+    // gpu-scope fence + counter update (cumulativity), the last block's thread 0
+    // fences again before the barrier that releases its readers
     __shared__ bool last;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(p.done, 1u) == static_cast<unsigned>(nblocks - 1);
+    TL_MARK(21, mark);  // units scored
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(p.done, 1u) == static_cast<unsigned>(nblocks - 1);
+        if (last) __threadfence();
+    }
     __syncthreads();
     if (!last) return;
-    __threadfence();
-    block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
+    TL_MARK(22, mark);  // last block: arrival counted
+    block_topk_radix(p.rel, p.U, p.n_sel, p.sel, &mark);
+    TL_MARK(23, mark);  // top-k written
     if (threadIdx.x == 0) *p.done = 0;
 }
 __global__ void __launch_bounds__(256, 1) k_lookup_reg(LookupParams p) {
@@ -604,7 +644,7 @@ __device__ __forceinline__ void lookup_stream_body(const LookupParams& p, int nb
     double q[8][4];
     if (p.qtok) {  // decode chain: the token's group query sums, formed once per block
         __shared__ double s_qs[8 * 128];
-        for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) s_qs[t] = lk_qsum(p, t);
+        lk_stage_qsums(p, s_qs);
         __syncthreads();
 #pragma unroll
         for (int g = 0; g < 8; ++g)
@@ -835,40 +875,42 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
     return before;
 }
 
-__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out) {
-    __shared__ int hist[256];
+__device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_t* out, unsigned long long* mk) {
+    __shared__ int hist[2][256];  // pass p counts into hist[p & 1] while hist[(p + 1) & 1] is cleared
     __shared__ int wsum[32];
     __shared__ uint64_t s_prefix, s_mask;
     __shared__ int s_remaining, s_done;
-    const int T = blockDim.x;
+    const int T = blockDim.x, lane = threadIdx.x % 32;
     const int E = static_cast<int>((U + T - 1) / T);
     const int64_t u0 = static_cast<int64_t>(threadIdx.x) * E;
     uint64_t key[kRadixE];
 #pragma unroll
     for (int e = 0; e < kRadixE; ++e) key[e] = (e < E && u0 + e < U) ? order_key(rel[u0 + e]) : 0ull;
+    if (mk) TL_MARK(24, *mk);  // keys loaded (thread 0)
+    for (int i = threadIdx.x; i < 256; i += T) hist[0][i] = 0;
     if (threadIdx.x == 0) {
         s_prefix = 0;
         s_mask = 0;
         s_remaining = static_cast<int>(K);
         s_done = 0;
     }
+    __syncthreads();
     for (int pass = 0; pass < 8; ++pass) {
+        if (s_done) break;  // uniform: written before the last barrier
         const int shift = 56 - 8 * pass;
-        for (int i = threadIdx.x; i < 256; i += T) hist[i] = 0;
-        __syncthreads();
-        if (s_done) break;  // uniform: read after the barrier
+        int* h = hist[pass & 1];
         const uint64_t prefix = s_prefix, mask = s_mask;
 #pragma unroll
         for (int e = 0; e < kRadixE; ++e)
-            if (e < E && u0 + e < U && (key[e] & mask) == prefix) atomicAdd(&hist[(key[e] >> shift) & 255], 1);
+            if (e < E && u0 + e < U && (key[e] & mask) == prefix) atomicAdd(&h[(key[e] >> shift) & 255], 1);
+        for (int i = threadIdx.x; i < 256; i += T) hist[(pass + 1) & 1][i] = 0;
         __syncthreads();
         if (threadIdx.x < 32) {
             // bins high -> low: lane l owns bins 255-8l .. 248-8l
-            const int lane = threadIdx.x;
             int c[8], sum = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                c[j] = hist[255 - 8 * lane - j];
+                c[j] = h[255 - 8 * lane - j];
                 sum += c[j];
             }
             int incl = sum;
@@ -906,22 +948,22 @@ __device__ void block_topk_radix(const double* rel, int64_t U, int64_t K, int64_
         }
         __syncthreads();
     }
+    if (mk) TL_MARK(25, *mk);  // digit passes done
     const uint64_t Tk = s_prefix, Tm = s_mask;
     const int need_eq = s_remaining;  // how many of the (key & Tm) == Tk ids to take, lowest first
-    int n_eq = 0;
-#pragma unroll
-    for (int e = 0; e < kRadixE; ++e) n_eq += (e < E && u0 + e < U && (key[e] & Tm) == Tk) ? 1 : 0;
-    int eq_before = block_excl_scan(n_eq, wsum, nullptr);
-    int n_sel = 0;
-    int eqb = eq_before;
+    // one scan of (above, equal) counts, packed: a thread's first output slot is
+    // the ids above T before it plus the equal ids before it that are taken
+    int n_gt = 0, n_eq = 0;
 #pragma unroll
     for (int e = 0; e < kRadixE; ++e) {
         if (!(e < E && u0 + e < U)) continue;
         const uint64_t km = key[e] & Tm;
-        if (km > Tk) ++n_sel;
-        else if (km == Tk && eqb++ < need_eq) ++n_sel;
+        n_gt += km > Tk ? 1 : 0;
+        n_eq += km == Tk ? 1 : 0;
     }
-    int pos = block_excl_scan(n_sel, wsum, nullptr);
+    const int ex = block_excl_scan(n_gt | (n_eq << 16), wsum, nullptr);
+    int eq_before = ex >> 16;
+    int pos = (ex & 0xffff) + (eq_before < need_eq ? eq_before : need_eq);
 #pragma unroll
     for (int e = 0; e < kRadixE; ++e) {
         if (!(e < E && u0 + e < U)) continue;

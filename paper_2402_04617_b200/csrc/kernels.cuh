@@ -97,6 +97,43 @@ __device__ __forceinline__ double lk_qsum(const LookupParams& p, int t) {
     return a;
 }
 
+// The token's per-group query sums into shared memory s[G * d] (decode chain)
+// or a copy of p.qsum: every head load of a slice is issued before its first
+// add, and the adds run in head order as in lk_qsum (same fp64 sums).
+__device__ __forceinline__ void lk_stage_qsums(const LookupParams& p, double* s) {
+    const int n = p.G * p.d;
+    if (!p.qtok || (p.d & 3) || (reinterpret_cast<uintptr_t>(p.qtok) & 7)) {
+        for (int t = threadIdx.x; t < n; t += blockDim.x) s[t] = lk_qsum(p, t);
+        return;
+    }
+    const int nq = p.d / 4;  // 4-element slices per head row
+    for (int t = threadIdx.x; t < p.G * nq; t += blockDim.x) {
+        const int g = t / nq, c = (t % nq) * 4;
+        const uint2* q = reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(p.qtok) +
+                                                        static_cast<int64_t>(g) * p.qrep * p.d + c);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int h0 = 0; h0 < p.qrep; h0 += 8) {
+            uint2 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (h0 + j < p.qrep) v[j] = q[static_cast<int64_t>(h0 + j) * nq];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (h0 + j < p.qrep) {
+                    a0 += static_cast<double>(__uint_as_float(v[j].x << 16));
+                    a1 += static_cast<double>(__uint_as_float(v[j].x & 0xffff0000u));
+                    a2 += static_cast<double>(__uint_as_float(v[j].y << 16));
+                    a3 += static_cast<double>(__uint_as_float(v[j].y & 0xffff0000u));
+                }
+        }
+        double* o = s + g * p.d + c;
+        o[0] = a0;
+        o[1] = a1;
+        o[2] = a2;
+        o[3] = a3;
+    }
+}
+
 struct TopkParams {
     const double* part;  // [U][Gtot]
     double* rel;         // [U]

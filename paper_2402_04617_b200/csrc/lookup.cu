@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
     const int64_t u0 = s0 + wib;
 #pragma unroll
     for (int st = 0; st < kLkStages - 1; ++st) issue(u0 + st * kLkWarps, st);
-    for (int t = threadIdx.x; t < p.G * 128; t += blockDim.x) sq[t] = lk_qsum(p, t);
+    lk_stage_qsums(p, sq);
     __syncthreads();
     unsigned long long mark = tl_t0_;
     double q[8][4];

@@ -86,10 +86,10 @@ def test_decode_chain_matches_sequential_order(n_pre):
     kt = (torch.randn((n_pre + n_dec, 8, 128), generator=g, device="cuda") * 0.5).bfloat16()
     vt = torch.randn((n_pre + n_dec, 8, 128), generator=g, device="cuda").bfloat16()
     runs = []
-    for chain in (1, 0):
+    for mode in (1, 0):
         eng = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(n_heads=32, n_kv_heads=8, head_dim=128),
                            dtype=torch.bfloat16)
-        eng.set_option("decode_chain", chain)
+        eng.set_option("decode_chain", mode)
         eng.reserve(n_pre + n_dec)
         eng.encode_stream(qt[:n_pre], kt[:n_pre], vt[:n_pre])
         o = [eng.decode_step(qt[i:i + 1], kt[i:i + 1], vt[i:i + 1]).clone() for i in range(n_pre, n_pre + n_dec)]

@@ -70,3 +70,27 @@ for k in range(100, 160):
     if s_.any():
         d_ = (t1a[s_] - t0a[s_]) / 1e3
         print(f"  mark {k - 100:3d}: n {s_.sum():5d} median {np.median(d_):6.2f} us")
+# one step's kernels (launch segments ordered by start), offsets from that step's lookup start
+segs_all = []
+for k in range(len(KINDS)):
+    idx = np.where(kid == k)[0]
+    if not len(idx):
+        continue
+    idx = idx[np.argsort(t0a[idx])]
+    cut = np.where(np.diff(t0a[idx]) > 3000)[0] + 1
+    for x in np.split(idx, cut):
+        segs_all.append((t0a[x].min(), t1a[x].max(), KINDS[k], len(x)))
+segs_all.sort()
+lk = [s_ for s_ in segs_all if s_[2] == "lookup"]
+if len(lk) > 34:
+    for j in (30, 31):
+        a0, b0 = lk[j][0], lk[j + 1][0]
+        print(f"step {j}: lookup-to-lookup {(b0 - a0) / 1e3:.2f} us")
+        for s_ in segs_all:
+            if a0 - 2000 <= s_[0] < b0:
+                print(f"   {s_[2]:9s} {(s_[0] - a0) / 1e3:7.2f} .. {(s_[1] - a0) / 1e3:7.2f} us  ({s_[3]} blocks)")
+        for mk_ in (120, 121, 122, 123, 150, 151, 152, 153):
+            s_ = (kid == mk_) & (t0a >= a0 - 2000) & (t0a < b0)
+            if s_.any():
+                e_ = np.sort((t1a[s_] - a0) / 1e3)
+                print(f"   mark {mk_ - 100}: ends min {e_[0]:6.2f} median {np.median(e_):6.2f} max {e_[-1]:6.2f} us (n {len(e_)})")

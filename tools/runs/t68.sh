@@ -1,0 +1,3 @@
+timeout 300 python tools/decode_timeline.py 131072 64 > gpurun_out/t68_dec.log 2>&1; echo rc=$?
+timeout 300 python tools/decode_timeline.py 524288 64 > gpurun_out/t68_dec512.log 2>&1; echo rc=$?
+timeout 900 python -m pytest tests/test_gpu_decode.py tests/test_gpu_streams.py -x -q > gpurun_out/t68_pytest.log 2>&1; echo pytest_rc=$?
