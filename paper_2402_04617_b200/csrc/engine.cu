@@ -277,11 +277,13 @@ struct SharedEvent {
 };
 // device/host resources of batched decode calls (owned by the batch's first engine)
 struct BatchCtx {
-    static constexpr int kSlots = 2;
-    void* host[kSlots] = {nullptr, nullptr};  // pinned parameter staging
-    void* dev[kSlots] = {nullptr, nullptr};   // device parameter tables
+    // parameter-table slots: a call reuses the slot of the call kSlots back once that
+    // call's LRU (the last reader, on its own stream) is done
+    static constexpr int kSlots = 4;
+    void* host[kSlots] = {};  // pinned parameter staging
+    void* dev[kSlots] = {};   // device parameter tables
     size_t cap = 0;
-    cudaEvent_t done[kSlots] = {nullptr, nullptr};
+    cudaEvent_t done[kSlots] = {};
     int slot = 0;
     DBuf part, mass, cnt;  // K4 batch scratch
     int part_B = 0, mass_B = 0;
@@ -1034,7 +1036,11 @@ struct infllm_engine {
             lp.done = topk_done.as<unsigned int>();
             lp.n_sel = n_sel;
             lp.early_dependents = one_stream ? 1 : 0;  // decode: K4 (or the chained front) follows as a dependent
-            lp.qtok = dec_chain ? q : nullptr;
+            // batched decode with the fused front (one-token steps, bf16 d 128): the scan
+            // forms the query sums from q too, so the batch's fronts run beside it
+            const bool bchain_q = coll && fused_front && dec_chain_opt && Gs == Gt && d == 128 && Gs <= 8 &&
+                                  !(reinterpret_cast<uintptr_t>(q) & 7);
+            lp.qtok = (dec_chain || bchain_q) ? q : nullptr;
             lp.qrep = rep;
             last_lkp = lp;
             if (coll) {  // batched: relevance scan (rel only) + one top-k block per sequence
@@ -2102,7 +2108,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         const int s = bc.slot;
         bc.slot = (bc.slot + 1) % BatchCtx::kSlots;
         const double h3 = now_us();
-        if (bc.done[s]) ck(cudaEventSynchronize(bc.done[s]), "batch slot");  // the batch two calls back
+        if (bc.done[s]) ck(cudaEventSynchronize(bc.done[s]), "batch slot");  // the batch kSlots calls back
         const double h4 = now_us();
         if (buf.size() > bc.cap) {
             ck(cudaDeviceSynchronize(), "batch table growth");
@@ -2141,17 +2147,38 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         lk_max = std::min<int64_t>(lk_units, 0xffffffff) | (lk_str << 32);
         for (auto& ap : c.attn) tiles_max = std::max<int64_t>(tiles_max, dec_max_tiles(ap));
-        if (!c.front.empty())
-            launch_dec_front_batch(dt + o_front, n, G, st);
-        else
-            launch_decode_batch_stage(0, dt + o_prep, n, G, st);
-        if (!c.evict.empty())
-            launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()), ev_max | (static_cast<int64_t>(G) << 32), st);
-        if (!c.select.empty())
-            launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()), sel_max | (static_cast<int64_t>(G) << 32), st);
-        if (bc.ring_set[bc.calls % BatchCtx::kRing])  // the LRU of the call three back
-            ck(cudaStreamWaitEvent(st, bc.lru_ring[bc.calls % BatchCtx::kRing], 0), "wait");
-        if (!c.lookup.empty()) launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
+        // batch chain (every sequence's scan forms its query sums from q): the scan
+        // first, the fronts as its programmatic dependent (they end after it), then
+        // completed units' copies and the top-k; else front, select, scan + top-k
+        // (measured: B = 2 at 128K 63.7 -> 55.9 us per step; from B = 4 on the fronts
+        // compete with the scan for SMs and the order makes no difference)
+        bool bchain = n <= 4 && !c.front.empty() && c.evict.empty() && static_cast<int32_t>(c.lookup.size()) == n;
+        for (auto& lp : c.lookup) bchain = bchain && lp.qtok != nullptr;
+        if (bchain) {
+            if (bc.ring_set[bc.calls % BatchCtx::kRing])  // the LRU of the call three back
+                ck(cudaStreamWaitEvent(st, bc.lru_ring[bc.calls % BatchCtx::kRing], 0), "wait");
+            launch_decode_batch_stage(5, dt + o_lk, n, lk_max, st);
+            launch_dec_front_batch(dt + o_front, n, G, st, 1);
+            if (!c.select.empty())
+                launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()),
+                                          sel_max | (static_cast<int64_t>(G) << 32), st);
+            launch_decode_batch_stage(6, dt + o_lk, n, lk_max, st);
+        } else {
+            if (!c.front.empty())
+                launch_dec_front_batch(dt + o_front, n, G, st);
+            else
+                launch_decode_batch_stage(0, dt + o_prep, n, G, st);
+            if (!c.evict.empty())
+                launch_decode_batch_stage(1, dt + o_ev, static_cast<int>(c.evict.size()),
+                                          ev_max | (static_cast<int64_t>(G) << 32), st);
+            if (!c.select.empty())
+                launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()),
+                                          sel_max | (static_cast<int64_t>(G) << 32), st);
+            if (bc.ring_set[bc.calls % BatchCtx::kRing])  // the LRU of the call three back
+                ck(cudaStreamWaitEvent(st, bc.lru_ring[bc.calls % BatchCtx::kRing], 0), "wait");
+            if (!c.lookup.empty())
+                launch_decode_batch_stage(3, dt + o_lk, static_cast<int>(c.lookup.size()), lk_max, st);
+        }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
                                          0,  // programmatic launch measured no better for the batch

@@ -2148,9 +2148,12 @@ struct DecFront {
     PrepParams p;
     EvictParams ep;
 };
-__global__ void __launch_bounds__(256) k_dec_front_b(const DecFront* __restrict__ fs) {
+__global__ void __launch_bounds__(256) k_dec_front_b(const DecFront* __restrict__ fs, int chain) {
     TL_BEGIN();
     dec_front_body(fs[blockIdx.z].p, fs[blockIdx.z].ep);
+    // batch chain: launched as the relevance scan's programmatic dependent, it ends
+    // after the scan, so the launches that follow see both
+    if (chain) asm volatile("griddepcontrol.wait;" ::: "memory");
     TL_END(TL_DEC_FRONT);
 }
 bool dec_front_supported(const PrepParams& p) {
@@ -2172,8 +2175,21 @@ void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t s
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_dec_front, p, ep);
 }
-void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st) {
-    k_dec_front_b<<<dim3(1, 1, B), 32 * G, 0, st>>>(static_cast<const DecFront*>(tab));
+void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st, int chain) {
+    if (!chain) {
+        k_dec_front_b<<<dim3(1, 1, B), 32 * G, 0, st>>>(static_cast<const DecFront*>(tab), 0);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};  // programmatic dependent of the scan launched just before
+    cfg.gridDim = dim3(1, 1, B);
+    cfg.blockDim = dim3(32 * G);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_dec_front_b, static_cast<const DecFront*>(tab), 1);
 }
 size_t dec_front_size() { return sizeof(DecFront); }
 
@@ -2204,6 +2220,7 @@ __global__ void __launch_bounds__(256) k_select_b(const SelectParams* __restrict
 // streaming relevance scan per sequence slice (8 warps, bulk-copy ring per warp); rel[u] only
 __device__ __forceinline__ int stream_blocks(int64_t U) { return static_cast<int>((U + 255) / 256); }
 __global__ void __launch_bounds__(256, 1) k_lookup_stream_b(const LookupParams* __restrict__ ps) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the top-k (or front) may launch (PDL)
     const LookupParams& p = ps[blockIdx.z];
     const int nb = stream_blocks(p.U);
     if (static_cast<int>(blockIdx.x) >= nb) return;
@@ -2221,12 +2238,14 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
     __shared__ int64_t s_off[kScanMaxB + 1];
     __shared__ const uint8_t* s_repr[kScanMaxB];
     __shared__ const double* s_q[kScanMaxB];
+    __shared__ const uint2* s_qt[kScanMaxB];  // batch chain: the token's q rows (query sums formed here)
     __shared__ double* s_rel[kScanMaxB];
     __shared__ __align__(8) uint64_t sbar[8][kScanStages];
     const int lane = threadIdx.x % 32, wib = threadIdx.x / 32;
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         s_repr[b] = static_cast<const uint8_t*>(ps[b].repr);
         s_q[b] = ps[b].qsum;
+        s_qt[b] = static_cast<const uint2*>(ps[b].qtok);
         s_rel[b] = ps[b].rel;
     }
     if (threadIdx.x == 0) {
@@ -2237,7 +2256,7 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
         }
         s_off[B] = o;
     }
-    const int G = ps[0].G;
+    const int G = ps[0].G, qrep = ps[0].qrep;
     if (lane == 0)
         for (int st = 0; st < kScanStages; ++st) tc::mbar_init(&sbar[wib][st], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2277,10 +2296,36 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
         if (b < 0 || t >= s_off[b + 1]) {  // first unit of a sequence for this warp: its query sums
             if (cb < 0) cb = 0;
             b = seq_of(t, cb);
+            if (s_qt[b]) {  // sums over the group's heads in head order from 0.0 (as lk_qsum)
 #pragma unroll
-            for (int g = 0; g < 8; ++g)
+                for (int g = 0; g < 8; ++g) {
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    if (g < G) {
+                        const uint2* qq = s_qt[b] + static_cast<int64_t>(g) * qrep * 32 + lane;
+                        uint2 v[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) q[g][j] = g < G ? s_q[b][g * 128 + 4 * lane + j] : 0.0;
+                        for (int hh = 0; hh < 8; ++hh)
+                            if (hh < qrep) v[hh] = qq[hh * 32];
+#pragma unroll
+                        for (int hh = 0; hh < 8; ++hh)
+                            if (hh < qrep) {
+                                a0 += static_cast<double>(__uint_as_float(v[hh].x << 16));
+                                a1 += static_cast<double>(__uint_as_float(v[hh].x & 0xffff0000u));
+                                a2 += static_cast<double>(__uint_as_float(v[hh].y << 16));
+                                a3 += static_cast<double>(__uint_as_float(v[hh].y & 0xffff0000u));
+                            }
+                    }
+                    q[g][0] = a0;
+                    q[g][1] = a1;
+                    q[g][2] = a2;
+                    q[g][3] = a3;
+                }
+            } else {
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) q[g][j] = g < G ? s_q[b][g * 128 + 4 * lane + j] : 0.0;
+            }
         }
         tc::mbar_wait(&sbar[wib][stage], static_cast<uint32_t>((it / kScanStages) & 1));
         const uint8_t* buf = ring + stage * 8192 + 8 * lane;
@@ -2338,7 +2383,8 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             k_select_b<<<dim3(static_cast<unsigned>(gx & 0xffffffff), static_cast<unsigned>(gx >> 32), B), 256, 0, st>>>(
                 static_cast<const SelectParams*>(tab));
             break;
-        case 3: {  // relevance scan + exact top-k (rel desc, id asc)
+        case 3:    // relevance scan + exact top-k (rel desc, id asc)
+        case 5: {  // the scan alone (6: the top-k alone)
             const LookupParams* ps = static_cast<const LookupParams*>(tab);
             const size_t smem = static_cast<size_t>(8) * kScanStages * 8192;
             static bool attr = false;
@@ -2362,6 +2408,11 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             } else {
                 k_lookup_stream_b<<<dim3(static_cast<unsigned>(gx >> 32), 1, B), 256, smem, st>>>(ps);
             }
+            if (stage == 5) break;  // batch chain: the front (and a completed unit's copy) come between
+            [[fallthrough]];
+        }
+        case 6: {
+            const LookupParams* ps = static_cast<const LookupParams*>(tab);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(B));
             cfg.blockDim = dim3(1024);

@@ -376,13 +376,14 @@ template <typename T> void launch_select(const SelectParams& p, cudaStream_t st)
 // batched decode stages (grid.z / grid.x = sequence; tab = device array of B params):
 // 0 prep (PrepParams), 1 evict (EvictParams, gx = max tokens | G << 32), 2 select
 // (SelectParams, gx = max units | G << 32), 3 lookup + top-k (LookupParams,
-// gx = max scan blocks), 4 LRU (LruParams)
+// gx = max scan blocks), 4 LRU (LruParams), 5 / 6 the scan / the top-k of stage 3
+// launched apart (batch chain: the front runs beside the scan)
 void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st);
 int64_t decode_batch_lookup_blocks(int64_t U);
 // decode front (one token): prep + eviction in one launch; batched: tab = B x {PrepParams, EvictParams}
 bool dec_front_supported(const PrepParams& p);
 void launch_dec_front(const PrepParams& p, const EvictParams& ep, cudaStream_t st);
-void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st);
+void launch_dec_front_batch(const void* tab, int B, int G, cudaStream_t st, int chain = 0);
 size_t dec_front_size();
 
 // standalone select (C ABI infllm_select_representatives)

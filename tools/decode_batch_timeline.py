@@ -69,3 +69,22 @@ for k in range(len(KINDS)):
         spans = [(t1a[x].max() - t0a[x].min()) / 1e3 for x in segs]
         print(f"  {KINDS[k]:9s} launches {len(segs):4d} span us median {np.median(spans):7.2f} blocks/launch "
               f"{np.median([len(x) for x in segs]):.0f}")
+# one step's launches ordered by start, offsets from that step's lookup-scan start
+segs_all = []
+for k in range(len(KINDS)):
+    idx = np.where(kid == k)[0]
+    if not len(idx):
+        continue
+    idx = idx[np.argsort(t0a[idx])]
+    cut = np.where(np.diff(t0a[idx]) > 3000)[0] + 1
+    for x in np.split(idx, cut):
+        segs_all.append((t0a[x].min(), t1a[x].max(), KINDS[k], len(x)))
+segs_all.sort()
+lk = [s_ for s_ in segs_all if s_[2] == "lookup"]
+if len(lk) > steps // 2 + 2:
+    j = steps // 2
+    a0, b0 = lk[j][0], lk[j + 1][0]
+    print(f"step {j}: lookup-to-lookup {(b0 - a0) / 1e3:.2f} us")
+    for s_ in segs_all:
+        if a0 - 30000 <= s_[0] < b0:
+            print(f"   {s_[2]:9s} {(s_[0] - a0) / 1e3:7.2f} .. {(s_[1] - a0) / 1e3:7.2f} us  ({s_[3]} blocks)")
