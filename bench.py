@@ -543,7 +543,7 @@ def c1_stream(dev, steps=5):
             "attention_frac_of_peak": flops / (prof["attn_ms"] / 1e3) / 1e12 / peak}
 
 
-def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), dec_steps=16):
+def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), dec_steps=48, dec_warm=4):
     """BASELINE configs[4] (C4): decode-step latency at 128K / 512K context for
     B = 1..32 independent sequences (infllm_decode_batch: every stage one
     launch for the batch; B = 1 is the single-sequence decode_step chain).
@@ -564,7 +564,7 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         Q = torch.randn((ctx, H, d), generator=g, device=dev).bfloat16()
         K = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
         V = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
-        tot = (dec_steps + 2) * len(batches) + 4
+        tot = (dec_steps + dec_warm) * len(batches) + 4
         engs = []
         for _ in range(bmax):
             e = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16)
@@ -579,7 +579,7 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         for B in batches:
             sub = engs[:B]
             res = torch.empty((B, H, d), device=dev, dtype=torch.bfloat16)
-            for _ in range(2):
+            for _ in range(dec_warm):
                 decode_batch(sub, qd[t, :B].contiguous(), kd[t, :B].contiguous(), vd[t, :B].contiguous(), out=res)
                 t += 1
             qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
@@ -617,7 +617,8 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         torch.cuda.empty_cache()
     return {"workload": "C4 (configs[4]): decode step latency, Llama-3-8B heads, 128K / 512K context, B "
                         "independent sequences per step (infllm_decode_batch; B = 1: decode_step chain)",
-            "timing": f"CUDA events around {dec_steps} consecutive steps (device time incl. host launch gaps); "
+            "timing": f"CUDA events around {dec_steps} consecutive steps after {dec_warm} untimed ones (device time "
+                      "incl. host launch gaps); "
                       "the loop calls infllm_decode_step (B = 1) / infllm_decode_batch with prepared arguments",
             "hbm_bytes": "K/V^T of init + k_m units + local window + the new token, plus the repr index scan",
             "peak_gbs": load_peaks()["hbm"], "grid": rows}
