@@ -77,7 +77,8 @@ struct TlBuf {
     unsigned long long* cnt;
     unsigned long long cap;
 };
-static __device__ TlBuf g_tl;  // one per translation unit, bound by tl_bind_tu
+static __constant__ TlBuf g_tl;  // one per translation unit, bound by tl_bind_tu (constant bank: the
+                                 // enabled check in every TL_MARK is a broadcast, not a global load)
 static inline cudaError_t tl_bind_tu(const TlBuf& b) { return cudaMemcpyToSymbol(g_tl, &b, sizeof(b)); }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
