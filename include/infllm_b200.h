@@ -180,8 +180,9 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * "graph_node_priority" (1 = instantiate stream graphs honouring the
  * attention's launch priority; default 0), "decode_chain" (1 = a one-token
  * step launches the lookup first, forming the query sums from q itself, with
- * the decode front as its programmatic dependent and K4 behind both; default;
- * 0 = front, lookup, K4 in sequence), "decode_merge_kernel" (1 = the
+ * the decode front as its programmatic dependent and K4 behind both, and a
+ * decode_batch of <= 4 sequences runs its fronts beside its relevance scan;
+ * default; 0 = front, lookup, K4 in sequence), "decode_merge_kernel" (1 = the
  * decode attention's split merge as its own parallel launch, default; 0 = in
  * each group's last split), "lookup_units_per_block" /
  * "lookup_units_per_block_decode" (K1+K2 grid: units per block in chunk /
