@@ -154,7 +154,30 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
     // a split attending retrieved units waits for the lookup grid when launched as its
     // programmatic dependent (no-op otherwise); behind the decode chain's front
     // (pdl 2) every split waits: the front writes this token's rotated query and ring row
-    if (units || sc.pdl == 2) asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int g = blockIdx.y, rep = a.rep;
+    if (threadIdx.x == 0) {  // before any wait: the maps were written before this launch
+        for (int i = 0; i < kStages; ++i) tc::mbar_init(&s_bar[i], 1);
+        tc::fence_barrier_init();
+        // the maps are rewritten in place when a buffer of the layer moves
+        for (int i = 0; i < 6; ++i) tc::acquire_tmap(static_cast<const CUtensorMap*>(a.dec_maps) + i);
+    }
+    unsigned pre = 0;  // stages whose tile was requested before the wait
+    if (units || sc.pdl == 2) {
+        // first tiles that neither the front nor the lookup writes or selects (initial
+        // pages; ring pages wholly before this token, whose page the front writes) are
+        // requested now, so their loads overlap the wait (thread 0 issues: its own
+        // barrier initialisation is ordered before them)
+        for (int st = 0; st < kStages - 1; ++st) {
+            const int t = t0 + st;
+            if (t >= t1 || (t >= n_init && t < n_init + a.n_sel)) continue;
+            const DecTile tl = dec_tile(a, t, n_init, near0, s_page, s_len);
+            if (tl.src == 0 || a.s - tl.key0 >= 128) {
+                dec_load(a, tl, g, dsm + st * kStageB, &s_bar[st]);
+                pre |= 1u << st;
+            }
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     if (units) {
         for (int u = tid; u < a.n_sel; u += kThr) {  // the retrieved units' pages and lengths
             const int64_t id = a.sel[u];
@@ -162,20 +185,14 @@ __device__ __forceinline__ void dec_body(const AttnParams& a, const DecScratch& 
             s_len[u] = a.unit_len[id];
         }
     }
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) tc::mbar_init(&s_bar[i], 1);
-        tc::fence_barrier_init();
-        // the maps are rewritten in place when a buffer of the layer moves
-        for (int i = 0; i < 6; ++i) tc::acquire_tmap(static_cast<const CUtensorMap*>(a.dec_maps) + i);
-    }
     __syncthreads();
-    const int g = blockIdx.y, rep = a.rep;
     const float sl2 = a.scale * kLog2e;
     TL_MARK(50, mark);  // dependencies met, stages initialised
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(dsm));  // 1024-aligned
 
     for (int st = 0; st < kStages - 1; ++st)  // prefetch the first tiles
-        if (t0 + st < t1) dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, dsm + st * kStageB, &s_bar[st]);
+        if (t0 + st < t1 && !((pre >> st) & 1u))
+            dec_load(a, dec_tile(a, t0 + st, n_init, near0, s_page, s_len), g, dsm + st * kStageB, &s_bar[st]);
     // query fragments (A operand, row = query head of the group, zero beyond rep):
     // rope(q, pos) for ring pages, rope(q, l_L) for init / unit pages; 8 k-steps of 16 dims
     uint32_t qa[8][2], qc[8][2];
