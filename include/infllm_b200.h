@@ -182,7 +182,9 @@ int infllm_engine_reset(infllm_engine_t eng, void* stream);
  * step launches the lookup first, forming the query sums from q itself, with
  * the decode front as its programmatic dependent and K4 behind both, and a
  * decode_batch of <= 4 sequences runs its fronts beside its relevance scan;
- * default; 0 = front, lookup, K4 in sequence), "decode_merge_kernel" (1 = the
+ * default; 0 = front, lookup, K4 in sequence), "decode_lookup_fused" (1 =
+ * one-token steps past 2048 units take the one-launch scan + top-k of chunk
+ * steps, default; 0 = the streaming scan + a top-k launch), "decode_merge_kernel" (1 = the
  * decode attention's split merge as its own parallel launch, default; 0 = in
  * each group's last split), "lookup_units_per_block" /
  * "lookup_units_per_block_decode" (K1+K2 grid: units per block in chunk /

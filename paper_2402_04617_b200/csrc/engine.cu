@@ -341,6 +341,8 @@ struct infllm_engine {
     int attn_streams = 2;
     bool graph_prio = false;
     bool dec_chain_opt = true;  // option decode_chain
+    bool dec_lk_fused = true;  // option decode_lookup_fused: one-token steps past 2048 units take k_lookup_topk
+                               // (512K one sequence 40.8 -> 39.7 us per step)
     bool dec_merge_opt = true;  // option decode_merge_kernel: K4's split merge as its own parallel launch  // option graph_node_priority (measured slower: 73.8 vs 70.6 us per C2 step)
     cudaStream_t attn_st[2] = {nullptr, nullptr};
     cudaEvent_t out_free = nullptr;  // host path: the staging buffer `out` points into is drained
@@ -1050,7 +1052,8 @@ struct infllm_engine {
             // one-token steps keep the latency-tuned two-kernel path (fused radix tail, K4
             // as its programmatic dependent); chunk steps take the one-launch kernel sized
             // for the ~20 SMs the attention leaves free
-            const bool fast = !coll && !one_stream && Gs == Gt && lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
+            const bool fast = !coll && (!one_stream || (dec_lk_fused && n_units0 > 256 * 8)) && Gs == Gt &&
+                              lookup_topk_supported(lp, dtype == INFLLM_DTYPE_BF16);
             if (fast) {
                 // one launch: scan + exact top-k; few fat blocks inside the prefill
                 // pipeline (the attention holds most SMs), one unit per warp in decode
@@ -1950,7 +1953,7 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
         if (k == "tc_attention" || k == "attn_score_bound" || k == "decode_kernel" || k == "multi_stream_decode" ||
             k == "lookup_units_per_block" || k == "lookup_units_per_block_decode" || k == "attn_splits" ||
             k == "gather_output" || k == "attn_streams" || k == "graph_node_priority" || k == "decode_chain" ||
-            k == "decode_merge_kernel") {
+            k == "decode_merge_kernel" || k == "decode_lookup_fused") {
             ck(cudaDeviceSynchronize(), "set_option");
             for (auto& g : e->graphs) infllm_engine::drop_graph(g);
             e->graphs.clear();
@@ -1969,6 +1972,8 @@ int infllm_engine_set_option(infllm_engine_t e, const char* key, int64_t value) 
             e->gather_output = value != 0;
         else if (k == "decode_chain")
             e->dec_chain_opt = value != 0;
+        else if (k == "decode_lookup_fused")
+            e->dec_lk_fused = value != 0;
         else if (k == "decode_merge_kernel")
             e->dec_merge_opt = value != 0;
         else if (k == "graph_node_priority")
