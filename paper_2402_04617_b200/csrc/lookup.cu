@@ -231,6 +231,17 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_xor_sync(kFull, t, o));
         if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_tau), static_cast<unsigned long long>(t));
+        // so is the k-th best of the block bests (k distinct units at least that good):
+        // the tighter bound when blocks hold few units (one-token steps, one unit per warp)
+        if (nb >= k)
+            for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+                const uint64_t kb = ck_all[b * 32];
+                const int ib = static_cast<int>(ci_all[b * 32]);
+                int r = 0;
+                for (int j = 0; j < nb; ++j) r += lk_better(ck_all[j * 32], static_cast<int>(ci_all[j * 32]), kb, ib) ? 1 : 0;
+                if (r == k - 1)
+                    atomicMax(reinterpret_cast<unsigned long long*>(&s_tau), static_cast<unsigned long long>(kb));
+            }
     }
     __syncthreads();
     const uint64_t tau = s_tau;
@@ -246,6 +257,32 @@ __global__ void __launch_bounds__(kLkWarps * 32, 1) k_lookup_topk(LookupParams p
     }
     __syncthreads();
     const int cnt = s_cnt;
+    if (cnt >= k && cnt <= static_cast<int>(blockDim.x)) {
+        // few survivors (the usual case): each one's rank among them by direct
+        // comparison, then the selected ids' ascending slots the same way; exact and
+        // order-free, so the same k ids as the merge below, without its ~80
+        // dependent shuffle stages in one warp
+        __shared__ int s_take[kLkWarps * 32];
+        const bool have = static_cast<int>(threadIdx.x) < cnt;
+        const uint64_t mk = have ? sv[threadIdx.x] : 0ull;
+        const int mi = have ? si[threadIdx.x] : -1;
+        int rank = 0;
+        if (have)
+            for (int j = 0; j < cnt; ++j) rank += lk_better(sv[j], si[j], mk, mi) ? 1 : 0;
+        const bool take = have && rank < k;
+        s_take[threadIdx.x] = take ? mi : -1;
+        __syncthreads();
+        if (take) {
+            int pos = 0;
+            for (int j = 0; j < cnt; ++j) pos += (s_take[j] >= 0 && s_take[j] < mi) ? 1 : 0;
+            p.sel[pos] = static_cast<int64_t>(mi);
+        }
+        if (threadIdx.x == 0) {
+            if (nb > 1) *p.done = 0;
+            TL_MARK(3, mark);  // final selection
+        }
+        return;
+    }
     uint64_t bk = 0;
     int bi = -1;
     if (cnt <= kLkSurv) {
