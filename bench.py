@@ -543,7 +543,7 @@ def c1_stream(dev, steps=5):
             "attention_frac_of_peak": flops / (prof["attn_ms"] / 1e3) / 1e12 / peak}
 
 
-def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), dec_steps=48, dec_warm=4):
+def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), dec_steps=48, dec_warm=8, rounds=3):
     """BASELINE configs[4] (C4): decode-step latency at 128K / 512K context for
     B = 1..32 independent sequences (infllm_decode_batch: every stage one
     launch for the batch; B = 1 is the single-sequence decode_step chain).
@@ -564,7 +564,7 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         Q = torch.randn((ctx, H, d), generator=g, device=dev).bfloat16()
         K = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
         V = torch.randn((ctx, Hkv, d), generator=g, device=dev).bfloat16()
-        tot = (dec_steps + dec_warm) * len(batches) + 4
+        tot = (rounds * dec_steps + dec_warm) * len(batches) + 4
         engs = []
         for _ in range(bmax):
             e = StreamEngine(EngineConfig.make(**CFG), ModelShape.make(**SHAPE), dtype=torch.bfloat16)
@@ -582,34 +582,38 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
             for _ in range(dec_warm):
                 decode_batch(sub, qd[t, :B].contiguous(), kd[t, :B].contiguous(), vd[t, :B].contiguous(), out=res)
                 t += 1
-            qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
-            ks = [kd[t + i, :B].contiguous() for i in range(dec_steps)]
-            vs = [vd[t + i, :B].contiguous() for i in range(dec_steps)]
             # the timed loop issues the C-ABI calls with their arguments prepared (what a
             # C++ host issues per step): Python-side argument checks stay outside
             lib_ = _lib.lib()
             st_ = torch.cuda.current_stream(dev).cuda_stream
-            args = [(qs[i].data_ptr(), ks[i].data_ptr(), vs[i].data_ptr()) for i in range(dec_steps)]
             hs = (C.c_void_p * B)(*[e.h.value for e in sub])
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            if B == 1:
-                h0, op = sub[0].h, res.data_ptr()
-                for qp, kp, vp in args:
-                    _lib.check(lib_.infllm_decode_step(h0, 0, qp, kp, vp, op, st_))
-            else:
-                op = res.data_ptr()
-                for qp, kp, vp in args:
-                    _lib.check(lib_.infllm_decode_batch(hs, B, 0, qp, kp, vp, op, st_))
-            e1.record()
-            torch.cuda.synchronize(dev)
-            t += dec_steps
-            ms = e0.elapsed_time(e1) / dec_steps
+            op = res.data_ptr()
+            per_round = []
+            for _ in range(rounds):  # median of rounds: one-time driver / allocator stalls land in one
+                qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
+                ks = [kd[t + i, :B].contiguous() for i in range(dec_steps)]
+                vs = [vd[t + i, :B].contiguous() for i in range(dec_steps)]
+                args = [(qs[i].data_ptr(), ks[i].data_ptr(), vs[i].data_ptr()) for i in range(dec_steps)]
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                if B == 1:
+                    h0 = sub[0].h
+                    for qp, kp, vp in args:
+                        _lib.check(lib_.infllm_decode_step(h0, 0, qp, kp, vp, op, st_))
+                else:
+                    for qp, kp, vp in args:
+                        _lib.check(lib_.infllm_decode_batch(hs, B, 0, qp, kp, vp, op, st_))
+                e1.record()
+                torch.cuda.synchronize(dev)
+                t += dec_steps
+                per_round.append(e0.elapsed_time(e1) / dec_steps)
+            ms = sorted(per_round)[len(per_round) // 2]
             units = sub[0].metrics()["units"]
             kv_b = B * (CFG["init_size"] + CFG["n_lookup"] * CFG["unit_size"] + CFG["local_size"] + 1) * Hkv * d * 4
             ix_b = B * units * CFG["n_repr"] * Hkv * d * 2
-            rows.append({"context": ctx, "batch": B, "step_us": ms * 1e3, "tokens_per_s": B / (ms / 1e3),
+            rows.append({"context": ctx, "batch": B, "step_us": ms * 1e3, "rounds_us": [x * 1e3 for x in per_round],
+                         "tokens_per_s": B / (ms / 1e3),
                          "hbm_bytes_per_step": kv_b + ix_b, "hbm_gbs": (kv_b + ix_b) / (ms / 1e3) / 1e9})
         for e in engs:
             e.close()
@@ -617,8 +621,8 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
         torch.cuda.empty_cache()
     return {"workload": "C4 (configs[4]): decode step latency, Llama-3-8B heads, 128K / 512K context, B "
                         "independent sequences per step (infllm_decode_batch; B = 1: decode_step chain)",
-            "timing": f"CUDA events around {dec_steps} consecutive steps after {dec_warm} untimed ones (device time "
-                      "incl. host launch gaps); "
+            "timing": f"CUDA events around {dec_steps} consecutive steps, median of {rounds} such rounds after "
+                      f"{dec_warm} untimed steps (device time incl. host launch gaps); "
                       "the loop calls infllm_decode_step (B = 1) / infllm_decode_batch with prepared arguments",
             "hbm_bytes": "K/V^T of init + k_m units + local window + the new token, plus the repr index scan",
             "peak_gbs": load_peaks()["hbm"], "grid": rows}
