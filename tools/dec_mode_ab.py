@@ -2,13 +2,20 @@
 # option A/B: host us per call and device us per call (events) through the
 # C-ABI with prepared arguments, rounds interleaved over the option values.
 #   python tools/dec_mode_ab.py [n=131072] [option=decode_chain] [values=1,2] [rounds=3]
+# (DEC_AB_LIB=path.so: time that library build)
 import ctypes as C
 import sys
 import time
 
+import os
+
 import torch
 
 sys.path.insert(0, '.')
+import paper_2402_04617_b200._lib as _L  # noqa: E402
+
+if os.environ.get("DEC_AB_LIB"):  # a library variant (tmp_libs/...) instead of the in-tree build
+    _L.LIB_PATH = os.environ["DEC_AB_LIB"]
 from paper_2402_04617_b200 import EngineConfig, ModelShape, StreamEngine, _lib  # noqa: E402
 import bench  # noqa: E402
 
