@@ -515,11 +515,16 @@ __global__ void __launch_bounds__(128) k_dec_merge1(AttnParams a, DecScratch sc,
     TL_END(TL_MASS);
 }
 __global__ void __launch_bounds__(128) k_dec_mergeb(const AttnParams* __restrict__ ps, DecScratch sc, int nsplit) {
+    // this sequence's parameters into shared memory while K4 drains (the table was
+    // uploaded before K4 launched), then the wait for K4's partials
+    __shared__ __align__(16) AttnParams sa;
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(AttnParams) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&sa)[i] = reinterpret_cast<const uint32_t*>(ps + blockIdx.z)[i];
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const AttnParams& a = ps[blockIdx.z];
-    if (static_cast<int>(blockIdx.x) > a.rep) return;
+    __syncthreads();
+    if (static_cast<int>(blockIdx.x) > sa.rep) return;
     TL_BEGIN();
-    dec_merge_body(a, sc, blockIdx.z, blockIdx.y, blockIdx.x, nsplit);
+    dec_merge_body(sa, sc, blockIdx.z, blockIdx.y, blockIdx.x, nsplit);
     TL_END(TL_MASS);
 }
 void launch_dec_merge(const AttnParams* host_a, const AttnParams* dev_params, int B, int G, int rep, int nsplit,
