@@ -2150,7 +2150,14 @@ struct DecFront {
 };
 __global__ void __launch_bounds__(256) k_dec_front_b(const DecFront* __restrict__ fs, int chain) {
     TL_BEGIN();
-    dec_front_body(fs[blockIdx.z].p, fs[blockIdx.z].ep);
+    // this sequence's parameters (rotation constants included) in shared memory:
+    // the body reads them all through its phases
+    __shared__ __align__(16) DecFront sf;
+    static_assert(sizeof(DecFront) % 4 == 0, "word copy");
+    for (int i = threadIdx.x; i < static_cast<int>(sizeof(DecFront) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(&sf)[i] = reinterpret_cast<const uint32_t*>(fs + blockIdx.z)[i];
+    __syncthreads();
+    dec_front_body(sf.p, sf.ep);
     // batch chain: launched as the relevance scan's programmatic dependent, it ends
     // after the scan, so the launches that follow see both
     if (chain) asm volatile("griddepcontrol.wait;" ::: "memory");
