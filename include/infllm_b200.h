@@ -153,9 +153,10 @@ int infllm_engine_set_comm(infllm_engine_t eng, const uint8_t* id128, int32_t ra
 int infllm_exchange_fold_host(const double* gathered, int64_t rows, int32_t nranks, int32_t g_count, double* out);
 int infllm_topk_host(const double* rel, int64_t n, int64_t k, int64_t* ids, int64_t* n_out);
 
-/* Pre-size the unit pool and trace for a stream of max_tokens tokens (the
- * reference grows its std::vectors on demand; the engine grows its device
- * pools too, this only moves the growth out of the timed region). */
+/* Pre-size the unit pool and trace for a stream of max_tokens tokens plus
+ * 4096 one-token steps of trace (the reference grows its std::vectors on
+ * demand; the engine grows its device pools too, draining its streams, this
+ * only moves the growth out of the timed region). */
 int infllm_engine_reserve(infllm_engine_t eng, int64_t max_tokens);
 /* Return every layer to the empty-stream state (tokens_fed = 0), keeping the
  * device pools; asynchronous on `stream`. */

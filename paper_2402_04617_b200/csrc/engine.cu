@@ -619,7 +619,7 @@ struct infllm_engine {
         if (side_stream) ck(cudaStreamSynchronize(side_stream), "side sync before pool growth");
         if (lru_stream) ck(cudaStreamSynchronize(lru_stream), "lru sync before pool growth");
         if (evict_stream) ck(cudaStreamSynchronize(evict_stream), "evict sync before pool growth");
-        const int64_t cap = std::max<int64_t>({need, 2 * L.trace_cap, 1024});
+        const int64_t cap = std::max<int64_t>({need, 4 * L.trace_cap, 1024});  // rare: each growth drains
         L.trace.grow(cap * 3 * sizeof(int64_t), st);
         L.trace_cap = cap;
     }
@@ -1905,7 +1905,9 @@ int infllm_engine_reserve(infllm_engine_t e, int64_t max_tokens) {
         const int64_t units = std::max<int64_t>(0, max_tokens - e->cfg.init_size) / e->cfg.unit_size + 2;
         for (auto& L : e->layers) {
             e->ensure_units(L, units, st);
-            const int64_t steps = (max_tokens + e->cfg.chunk_size - 1) / e->cfg.chunk_size + 1;
+            // chunk steps of max_tokens plus 4096 one-token steps: a trace growth drains every
+            // stream of the engine (and a batch's LRU), a multi-ms stall inside a decode loop
+            const int64_t steps = (max_tokens + e->cfg.chunk_size - 1) / e->cfg.chunk_size + 1 + 4096;
             e->ensure_trace(L, steps * std::max<int64_t>(e->cfg.n_lookup, 1), st);
         }
         ck(cudaStreamSynchronize(st), "reserve");
