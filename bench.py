@@ -22,6 +22,7 @@ pinned bit-exact to the reference engine), rank 0 only.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -589,6 +590,8 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
             hs = (C.c_void_p * B)(*[e.h.value for e in sub])
             op = res.data_ptr()
             per_round = []
+            gc.collect()
+            gc.disable()  # no collector pause inside a timed round
             for _ in range(rounds):  # median of rounds: one-time driver / allocator stalls land in one
                 qs = [qd[t + i, :B].contiguous() for i in range(dec_steps)]
                 ks = [kd[t + i, :B].contiguous() for i in range(dec_steps)]
@@ -608,6 +611,7 @@ def decode_grid(dev, contexts=(131072, 524288), batches=(1, 2, 4, 8, 16, 32), de
                 torch.cuda.synchronize(dev)
                 t += dec_steps
                 per_round.append(e0.elapsed_time(e1) / dec_steps)
+            gc.enable()
             ms = sorted(per_round)[len(per_round) // 2]
             units = sub[0].metrics()["units"]
             kv_b = B * (CFG["init_size"] + CFG["n_lookup"] * CFG["unit_size"] + CFG["local_size"] + 1) * Hkv * d * 4
