@@ -2117,14 +2117,21 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         const double h3 = now_us();
         if (bc.done[s]) ck(cudaEventSynchronize(bc.done[s]), "batch slot");  // the batch kSlots calls back
         const double h4 = now_us();
-        if (buf.size() > bc.cap) {
+        // capacity for every record a call of n sequences can carry (fronts or preps,
+        // evictions and completed units' copies of all n, ...): a growth drains the
+        // device and re-allocates pinned memory (ms), so it happens once per batch size,
+        // not when a call first carries completed units
+        const size_t worst = static_cast<size_t>(n) * (sizeof(DecFrontRec) + sizeof(PrepParams) + sizeof(EvictParams) +
+                                                       sizeof(SelectParams) + sizeof(LookupParams) + sizeof(AttnParams) +
+                                                       sizeof(LruParams)) + 8 * 256;
+        if (buf.size() > bc.cap || worst > bc.cap) {
             ck(cudaDeviceSynchronize(), "batch table growth");
             for (int t = 0; t < BatchCtx::kSlots; ++t) {
                 if (bc.host[t]) cudaFreeHost(bc.host[t]);
                 if (bc.dev[t]) cudaFree(bc.dev[t]);
                 bc.host[t] = bc.dev[t] = nullptr;
             }
-            bc.cap = buf.size() * 2;
+            bc.cap = std::max(buf.size(), worst);
             for (int t = 0; t < BatchCtx::kSlots; ++t) {
                 ck(cudaHostAlloc(&bc.host[t], bc.cap, cudaHostAllocDefault), "cudaHostAlloc");
                 ck(cudaMalloc(&bc.dev[t], bc.cap), "cudaMalloc");

@@ -1,6 +1,8 @@
 # Long batched decode run: per-round device time and decode_batch host-time
 # breakdown, to locate periodic stalls (which round, host or device side).
-#   python tools/dec_batch_stall.py [n=131072] [B=16] [rounds=20]
+#   python tools/dec_batch_stall.py [n=131072] [B=16] [rounds=20] [B_first=0]
+# (B_first > 0: the first B_first engines step 152 times alone first, as the
+# bench's grid does before a larger batch joins them)
 import ctypes as C
 import sys
 import time
@@ -14,6 +16,7 @@ import bench  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+b_first = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 steps = 48
 cfg, shape = bench.CFG, bench.SHAPE
 H, Hkv, d = shape["n_heads"], shape["n_kv_heads"], shape["head_dim"]
@@ -25,7 +28,7 @@ V = torch.randn((n, Hkv, d), generator=g, device="cuda").bfloat16()
 engs = []
 for _ in range(B):
     e = StreamEngine(EngineConfig.make(**cfg), ModelShape.make(**shape), dtype=torch.bfloat16)
-    e.reserve(n + rounds * steps + 64)
+    e.reserve(n + rounds * steps + 64 + 160)
     e.encode_stream(Q, K, V)
     engs.append(e)
 del Q, K, V
@@ -36,6 +39,11 @@ out = torch.empty((B, H, d), device="cuda", dtype=torch.bfloat16)
 L = _lib.lib()
 st = torch.cuda.current_stream().cuda_stream
 hs = (C.c_void_p * B)(*[e.h.value for e in engs])
+if b_first:
+    for t in range(152):
+        decode_batch(engs[:b_first], qd[t % steps, :b_first].contiguous(), kd[t % steps, :b_first].contiguous(),
+                     vd[t % steps, :b_first].contiguous(), out=out[:b_first])
+    torch.cuda.synchronize()
 for t in range(8):
     decode_batch(engs, qd[t], kd[t], vd[t], out=out)
 torch.cuda.synchronize()
