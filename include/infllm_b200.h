@@ -417,7 +417,8 @@ int infllm_score_acc_finalize_front(infllm_score_acc_t a, int64_t n, float* host
 int infllm_debug_kernel_bench(infllm_engine_t eng, int32_t which, int32_t iters, double* us_per_launch);
 /* Diagnostic: accumulated host time (us) of infllm_decode_batch by section:
  * [0] argument checks, [1] per-sequence step logic, [2] parameter tables,
- * [3] wait for the batch two calls back, [4] copies + launches, [5] calls. */
+ * [3] wait for the parameter-table slot (the batch four calls back),
+ * [4] copies + launches, [5] calls. */
 int infllm_debug_host_times(double* out6, int32_t reset);
 /* Diagnostic: 64 clock64 phase stamps written by instrumented kernels. */
 int infllm_debug_timestamps(unsigned long long* out64);
