@@ -2195,7 +2195,9 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
-                                         0,  // programmatic launch measured no better for the batch
+                                         // past the batch chain the fronts finished before the scan started:
+                                         // K4's splits without retrieved units may start beside the top-k
+                                         bchain ? 0 : 1,
                                          e0->dec_merge_opt ? 1 : 0},
                               st);
         cudaStream_t lst = st;
