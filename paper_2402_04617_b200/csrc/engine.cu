@@ -2176,7 +2176,7 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
             if (!c.select.empty())
                 launch_decode_batch_stage(2, dt + o_sel, static_cast<int>(c.select.size()),
                                           sel_max | (static_cast<int64_t>(G) << 32), st);
-            launch_decode_batch_stage(6, dt + o_lk, n, lk_max, st);
+            launch_decode_batch_stage(7, dt + o_lk, n, lk_max, st);
         } else {
             if (!c.front.empty())
                 launch_dec_front_batch(dt + o_front, n, G, st);
@@ -2195,9 +2195,10 @@ int infllm_decode_batch(infllm_engine_t* engs, int32_t n, int32_t layer, const v
         }
         launch_attn_dec_batch(reinterpret_cast<const AttnParams*>(dt + o_at), n, G, tiles_max,
                               DecScratch{bc.part.as<float>(), bc.mass.as<float>(), bc.cnt.as<unsigned>(), km,
-                                         // past the batch chain the fronts finished before the scan started:
-                                         // K4's splits without retrieved units may start beside the top-k
-                                         bchain ? 0 : 1,
+                                         // K4's splits without retrieved units start beside the top-k: past
+                                         // the batch chain the fronts finished before the scan started, in
+                                         // it the top-k releases K4 only after its wait (fronts complete)
+                                         1,
                                          e0->dec_merge_opt ? 1 : 0},
                               st);
         cudaStream_t lst = st;

@@ -2358,10 +2358,13 @@ __global__ void __launch_bounds__(256, 1) k_lookup_stream_bal(const LookupParams
     }
     TL_END(TL_LOOKUP);
 }
-__global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps) {
-    // programmatic dependent of the scan: K4 may launch now; the relevance must be complete
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+__global__ void __launch_bounds__(1024) k_topk_b(const LookupParams* __restrict__ ps, int late) {
+    // programmatic dependent of the scan: K4 may launch now; the relevance must be complete.
+    // late (batch chain, the fronts between the scan and this launch): K4 launches only
+    // once the fronts (which end after the scan) are complete
+    if (!late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     TL_BEGIN();
     const LookupParams& p = ps[blockIdx.x];
     block_topk_radix(p.rel, p.U, p.n_sel, p.sel);
@@ -2418,7 +2421,8 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             if (stage == 5) break;  // batch chain: the front (and a completed unit's copy) come between
             [[fallthrough]];
         }
-        case 6: {
+        case 6:
+        case 7: {  // 7: the top-k alone, its dependents released after its wait (batch chain)
             const LookupParams* ps = static_cast<const LookupParams*>(tab);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(B));
@@ -2431,7 +2435,7 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             la[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = la;
             cfg.numAttrs = 1;
-            cudaLaunchKernelEx(&cfg, k_topk_b, ps);
+            cudaLaunchKernelEx(&cfg, k_topk_b, ps, stage == 7 ? 1 : 0);
             break;
         }
         case 4:  // LRU / tier bookkeeping

@@ -377,7 +377,8 @@ template <typename T> void launch_select(const SelectParams& p, cudaStream_t st)
 // 0 prep (PrepParams), 1 evict (EvictParams, gx = max tokens | G << 32), 2 select
 // (SelectParams, gx = max units | G << 32), 3 lookup + top-k (LookupParams,
 // gx = max scan blocks), 4 LRU (LruParams), 5 / 6 the scan / the top-k of stage 3
-// launched apart (batch chain: the front runs beside the scan)
+// launched apart (batch chain: the front runs beside the scan), 7 = 6 with the
+// top-k's dependents (K4) released after its wait
 void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cudaStream_t st);
 int64_t decode_batch_lookup_blocks(int64_t U);
 // decode front (one token): prep + eviction in one launch; batched: tab = B x {PrepParams, EvictParams}
