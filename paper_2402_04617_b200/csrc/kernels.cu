@@ -2426,9 +2426,9 @@ void launch_decode_batch_stage(int stage, const void* tab, int B, int64_t gx, cu
             const LookupParams* ps = static_cast<const LookupParams*>(tab);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(static_cast<unsigned>(B));
-            // one block per sequence: 256 threads up to 2048 units (8 keys each: fewer
-            // warps per barrier), else 1024
-            cfg.blockDim = dim3((gx >> 32) <= 8 ? 256 : 1024);
+            // one block per sequence, 8 keys per thread where they fit (fewer warps per
+            // barrier): 256 threads up to 2048 units, 512 up to 4096, else 1024
+            cfg.blockDim = dim3((gx >> 32) <= 8 ? 256 : (gx >> 32) <= 16 ? 512 : 1024);
             cfg.stream = st;
             cudaLaunchAttribute la[1];
             la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
